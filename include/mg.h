@@ -1,0 +1,139 @@
+/*
+ * mg.h -- C ABI of libmg, the B200-native (sm_100a) V-cycle of Roberts'
+ * diagonally oriented multigrid for Poisson's equation (arXiv math/9907190,
+ * /root/reference/PAPER.md, cited as P:line).
+ *
+ * Problem: solve  nabla^2 u = f  on the unit square (dim 2) or the
+ * unit cube (dim 3), homogeneous Dirichlet data (reading A1 of DESIGN.md),
+ * on the uniform grid of n = 2^k + 1 nodes per side, h = 1/(n-1).  Each
+ * V-cycle forms the residual r = f - L u on the finest grid (5-/7-point
+ * Laplacian, or the compact fourth-order Efos2 / Efos4
+ * schemes), restricts it down the paper's diagonal hierarchy
+ * (Erest2r/Erest2b P:166-176; Erred, Ermagc, Ermagm, Erblu P:426-519), takes
+ * one Jacobi step on the coarsest grid, climbs back with one over-relaxed
+ * two-colour Jacobi step per level (Eajacr/Eajacb P:350-359 and "similarly
+ * for a green grid" P:360; Emprolm/b, Erprolr/m, Egprolg/r P:556-661) and
+ * adds the correction: u <- u + v.  There is no interpolation
+ * operator.
+ *
+ * Conventions for every call:
+ *  - Arrays are row-major with x fastest: 2D element (i, j) at
+ *    base[j * pitch + i]; 3D element (i, j, k) at
+ *    base[(k * n + j) * pitch + i] (single GPU).  `pitch` is in elements,
+ *    fixed at mg_create_ex time (cfg.pitch; 0 means n).  A pitch whose byte
+ *    size is a multiple of 16 lets the library read the caller's arrays
+ *    directly; otherwise each call stages them through internal pitched
+ *    copies (correct, slower).
+ *  - u, f, r, x are DEVICE pointers on the solver's device unless the name
+ *    says _host.  The caller owns them; the library never frees them.  They
+ *    must stay alive until the work queued on the solver's stream completes.
+ *  - Element type is double (MG_F64) or float (MG_F32) as configured.  All
+ *    arithmetic is done in that type, in the canonical evaluation order of
+ *    DESIGN.md, without FMA contraction.
+ *  - Boundary entries of u must be 0 and are never written.  Boundary entries
+ *    of f are read only by the order-4 f-combination (reading A11).
+ *  - Calls are asynchronous on the solver's stream (cfg.stream, or the legacy
+ *    default stream when NULL) except where noted "synchronises".
+ *  - Every call returns an mg_status (0 = MG_OK); no C++ exception crosses
+ *    the ABI.  mg_last_error() describes the last failure of a handle.
+ *  - A handle is not thread-safe; distinct handles are independent.
+ *
+ * Multi-GPU (cfg.nranks > 1): one process per GPU; the grid is cut into
+ * y-slabs (2D) / z-slabs (3D).  Each rank passes only its slab: rows
+ * (planes) [lo, hi) of the global grid, stored with `ghost` extra rows
+ * (planes) above and below, i.e. a (hi - lo + 2*ghost) x ... array whose row
+ * `ghost` is global row lo (see mg_local_extent).  The library fills the
+ * ghost rows itself.  Levels coarser than cfg.agglom_points interior nodes
+ * are agglomerated on every rank (all-gather + redundant coarse solve).
+ */
+#ifndef MG_H
+#define MG_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct mg_solver mg_solver;
+
+typedef enum {
+  MG_OK = 0,
+  MG_EINVAL = -1,        /* bad argument: n != 2^k+1 (k>=2), dim, order, p, pitch, ncycles, NULL */
+  MG_ENOMEM = -2,        /* device or host allocation failed */
+  MG_ECUDA = -3,         /* a CUDA runtime call failed (message in mg_last_error) */
+  MG_ENCCL = -4,         /* an NCCL call failed */
+  MG_EUNSUPPORTED = -5,  /* valid but not supported by this build/config (e.g. ranks not dividing n-1) */
+  MG_EDIVERGED = -6,     /* a computed residual norm was not finite */
+  MG_ENODEV = -7         /* no usable CUDA device (never falls back to the CPU) */
+} mg_status;
+
+enum { MG_F64 = 0, MG_F32 = 1 };
+enum { MG_NORM_INF = 0, MG_NORM_L2 = 1 };
+
+typedef struct {
+  int dim;                 /* 2 or 3 */
+  int64_t n;               /* nodes per side incl. boundary, n = 2^k + 1, k >= 2 */
+  int order;               /* 2 (5/7-point) or 4 (Efos2 / Efos4) */
+  int dtype;               /* MG_F64 or MG_F32 */
+  double p[4];             /* 2D: p[0] = p.  3D: p_m, p_r1, p_r2, p_g.
+                              Each in (0, 3]. */
+  int64_t pitch;           /* elements per row of caller arrays; 0 = n */
+  void *stream;            /* cudaStream_t the calls are ordered on; NULL = legacy default stream */
+  int device;              /* CUDA device ordinal; -1 = current device */
+  int nranks, rank;        /* 1 / 0 for a single GPU */
+  const void *nccl_id;     /* 128-byte ncclUniqueId (same on every rank) when nranks > 1 */
+  int64_t agglom_points;   /* agglomerate levels with fewer interior nodes; 0 = 1<<18 */
+  int flags;               /* reserved, 0 */
+} mg_config;
+
+/* Defaults: fp64, pitch = n, NULL stream, current device, 1 rank, p[*] = omega.
+ * Errors: MG_EINVAL (n, dim, order, omega), MG_ENODEV, MG_ENOMEM, MG_ECUDA. */
+int mg_create(int dim, int64_t n, int order, double omega, mg_solver **out);
+
+/* Full configuration (copied; the caller may free cfg afterwards). */
+int mg_create_ex(const mg_config *cfg, mg_solver **out);
+
+/* Frees every library-owned buffer, graph, stream and communicator. NULL ok. */
+int mg_destroy(mg_solver *s);
+
+/* Rows (2D) / planes (3D) [lo, hi) of the global grid owned by this rank, and
+ * the ghost rows/planes the caller's slab carries on each side.  Single GPU:
+ * lo = 0, hi = n, ghost = 0. */
+int mg_local_extent(const mg_solver *s, int64_t *lo, int64_t *hi, int64_t *ghost);
+
+/* r = f - L u at every interior node (order as configured; Evpois P:62-67,
+ * Efos2, Efos4), r = 0 on the boundary.  r has the layout of u. */
+int mg_residual(mg_solver *s, const void *u, const void *f, void *r);
+
+/* ncycles V-cycles in place on u (ncycles = 0: no-op).  res_hist: NULL, or
+ * room for ncycles+1 doubles that receive ||f - L u||_inf before every cycle
+ * and after the last; a non-NULL res_hist synchronises the stream and
+ * returns MG_EDIVERGED if any entry is not finite. */
+int mg_vcycle(mg_solver *s, void *u, const void *f, int ncycles, double *res_hist);
+
+/* Same as mg_vcycle on HOST arrays (pitch as configured): copies u and f to
+ * the device, runs the cycles, copies u back.  Synchronises.  Pinned host
+ * memory makes the copies asynchronous DMA. */
+int mg_vcycle_host(mg_solver *s, void *u_host, const void *f_host, int ncycles, double *res_hist);
+
+/* Global norm of x over the interior nodes: MG_NORM_INF = max |x|,
+ * MG_NORM_L2 = (h^d sum x^2)^(1/2).  Reduced over ranks.  Synchronises. */
+int mg_norm(mg_solver *s, const void *x, int kind, double *out);
+
+/* Number of interior nodes of level `lev` (0 = finest) and the level count;
+ * introspection for tests and the roofline model. */
+int mg_num_levels(const mg_solver *s);
+int64_t mg_level_points(const mg_solver *s, int lev);
+
+/* Kernel launches queued by one V-cycle on this handle (for the bench's
+ * gpu_launches count). */
+int mg_launches_per_cycle(const mg_solver *s);
+
+const char *mg_strerror(int status);
+const char *mg_last_error(const mg_solver *s);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MG_H */

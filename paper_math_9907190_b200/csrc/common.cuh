@@ -1,0 +1,117 @@
+// common.cuh -- shared device-side types of libmg (sm_100a).
+//
+// Data layout in HBM:
+//   * dense level  (2D axis A(s), 3D green G(s)): one array over the lattice
+//     of the octave, (M+1)^d points with the boundary, rows padded to a
+//     128-byte multiple;  M = (n-1)/s.
+//   * split level  (2D diagonal D(s), 3D red R(s) / magenta M(s)): the
+//     level's nodes are stored packed per parity sublattice -- lattice point
+//     (x, y[, z]) lives in sublattice (x&1, y&1[, z&1]) at index
+//     (x>>1, y>>1[, z>>1]).  D(s) uses E=(0,0) and O=(1,1); R(s) uses
+//     C=(0,0,0), Fx=(0,1,1), Fy=(1,0,1), Fz=(1,1,0); M(s) uses C and B=(1,1,1).
+//     Every sublattice array has (M/2+1)^d entries with a 128-byte row pitch.
+// Boundary entries are zero and are never written by any kernel.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace mg {
+
+// Dense 2D lattice array; p addresses global lattice point (0, 0).
+template <class T>
+struct D2 {
+  T *p;
+  int64_t pitch;
+  __device__ __forceinline__ T &operator()(int x, int y) const { return p[(int64_t)y * pitch + x]; }
+};
+
+// Split diagonal level: E = (even, even), O = (odd, odd) sublattices.
+template <class T>
+struct S2 {
+  T *e, *o;
+  int64_t pitch;
+  __device__ __forceinline__ T get(int x, int y) const {
+    return ((x & 1) ? o : e)[(int64_t)(y >> 1) * pitch + (x >> 1)];
+  }
+  __device__ __forceinline__ T &ref(int x, int y) const {
+    return ((x & 1) ? o : e)[(int64_t)(y >> 1) * pitch + (x >> 1)];
+  }
+};
+
+// Dense 3D lattice array.
+template <class T>
+struct D3 {
+  T *p;
+  int64_t pitch, plane;
+  __device__ __forceinline__ T &operator()(int x, int y, int z) const {
+    return p[(int64_t)z * plane + (int64_t)y * pitch + x];
+  }
+};
+
+// Split 3D level: s[(x&1) | (y&1)<<1 | (z&1)<<2] holds that parity sublattice.
+template <class T>
+struct S3 {
+  T *s[8];
+  int64_t pitch, plane;
+  __device__ __forceinline__ T &ref(int x, int y, int z) const {
+    return s[(x & 1) | ((y & 1) << 1) | ((z & 1) << 2)][(int64_t)(z >> 1) * plane + (int64_t)(y >> 1) * pitch + (x >> 1)];
+  }
+  __device__ __forceinline__ T get(int x, int y, int z) const { return ref(x, y, z); }
+};
+
+// Constants, each formed in double on the host and rounded once to T
+// (DESIGN.md "Canonical arithmetic").
+template <class T>
+struct Coef {
+  T invh2;   // (n-1)^2
+  T c6;      // (n-1)^2 / 6
+};
+
+// Residual-norm sink: max |r| as the bit pattern of a non-negative double
+// (monotone in the value; NaN sorts above +inf so it is never lost).
+struct NormSink {
+  unsigned long long *slots;   // per-cycle maxima
+  int *counter;                // which slot the current cycle writes
+  int cap;
+};
+
+__device__ __forceinline__ void norm_push(const NormSink &ns, double v) {
+  if (ns.slots == nullptr) return;
+  int slot = *ns.counter;
+  if (slot >= ns.cap) slot = ns.cap - 1;
+  atomicMax(ns.slots + slot, (unsigned long long)__double_as_longlong(v));
+}
+
+// max that propagates NaN (a diverged residual must not be hidden).
+__device__ __forceinline__ double nmax(double a, double b) { return (b > a || b != b) ? b : a; }
+
+template <class T>
+__device__ __forceinline__ double absd(T v) {
+  return fabs((double)v);
+}
+
+// Block-wide max reduction then one atomic per block.
+template <int NT>
+__device__ __forceinline__ void block_norm_push(const NormSink &ns, double v) {
+  if (ns.slots == nullptr) return;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    double w = __shfl_xor_sync(0xffffffffu, v, o);
+    v = (w > v || w != w) ? w : v;
+  }
+  __shared__ double red[NT / 32];
+  int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  if (lane == 0) red[wid] = v;
+  __syncthreads();
+  if (wid == 0) {
+    v = (lane < NT / 32) ? red[lane] : 0.0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      double w = __shfl_xor_sync(0xffffffffu, v, o);
+      v = (w > v || w != w) ? w : v;
+    }
+    if (lane == 0) norm_push(ns, v);
+  }
+}
+
+}  // namespace mg

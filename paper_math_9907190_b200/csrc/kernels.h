@@ -1,0 +1,62 @@
+// kernels.h -- internal launcher interface between the host plan (mg_api.cpp)
+// and the sm_100a kernels (k2d.cu, k3d.cu).  Not part of the public ABI.
+#pragma once
+#include "common.cuh"
+
+namespace mg {
+
+// ----------------------------------------------------------------- 2D
+template <class T>
+void launch2_desc_fine(const D2<const T> &u, const D2<const T> &f, const S2<T> &d, int M, int order, const Coef<T> &k,
+                       const NormSink &ns, cudaStream_t st);
+template <class T>
+void launch2_rest_ad(const D2<T> &r, const S2<T> &d, int M, cudaStream_t st);
+template <class T>
+void launch2_rest_da(const S2<T> &d, const D2<T> &r, int Mc, cudaStream_t st);
+template <class T>
+void launch2_coarsest(const D2<T> &r, const D2<T> &v, T c, int *counter, cudaStream_t st);
+template <class T>
+void launch2_jac_d(const D2<T> &vc, const S2<T> &r, const S2<T> &v, int M, T c, cudaStream_t st);
+template <class T>
+void launch2_jac_a(const S2<T> &vd, const D2<T> &r, const D2<T> &v, int M, T c, cudaStream_t st);
+template <class T>
+void launch2_asc_fine(const S2<T> &vd, const D2<T> &u, const D2<const T> &f, const D2<T> &scratch, int M, int order,
+                      T c, const Coef<T> &k, cudaStream_t st);
+template <class T>
+void launch2_residual(const D2<const T> &u, const D2<const T> &f, const D2<T> &r, int M, int order, const Coef<T> &k,
+                      cudaStream_t st);
+template <class T>
+void launch2_ftilde(const D2<const T> &f, const D2<T> &ft, int M, cudaStream_t st);
+template <class T>
+void launch2_norm(const D2<const T> &a, int M, unsigned long long *mx, double *ss, cudaStream_t st);
+
+// ----------------------------------------------------------------- 3D
+template <class T>
+void launch3_desc_fine(const D3<const T> &u, const D3<const T> &f, const S3<T> &rr, int M, int order,
+                       const Coef<T> &k, const NormSink &ns, cudaStream_t st);
+template <class T>
+void launch3_rest_gr(const D3<T> &r, const S3<T> &rr, int M, cudaStream_t st);
+template <class T>
+void launch3_rest_rm(const S3<T> &rr, const S3<T> &rm, int M, cudaStream_t st);
+template <class T>
+void launch3_rest_mg(const S3<T> &rm, const D3<T> &rg, int Mc, cudaStream_t st);
+template <class T>
+void launch3_coarsest(const D3<T> &r, const D3<T> &v, T c, int *counter, cudaStream_t st);
+template <class T>
+void launch3_jac_m(const D3<T> &vc, const S3<T> &r, const S3<T> &v, int M, T c, cudaStream_t st);
+template <class T>
+void launch3_jac_r(const S3<T> &vm, const S3<T> &r, const S3<T> &v, int M, T c1, T c2, cudaStream_t st);
+template <class T>
+void launch3_jac_g(const S3<T> &vr, const D3<T> &r, const D3<T> &v, int M, T c, cudaStream_t st);
+template <class T>
+void launch3_asc_fine(const S3<T> &vr, const D3<T> &u, const D3<const T> &f, const D3<T> &scratch, int M, int order,
+                      T c, const Coef<T> &k, cudaStream_t st);
+template <class T>
+void launch3_residual(const D3<const T> &u, const D3<const T> &f, const D3<T> &r, int M, int order, const Coef<T> &k,
+                      cudaStream_t st);
+template <class T>
+void launch3_ftilde(const D3<const T> &f, const D3<T> &ft, int M, cudaStream_t st);
+template <class T>
+void launch3_norm(const D3<const T> &a, int M, unsigned long long *mx, double *ss, cudaStream_t st);
+
+}  // namespace mg

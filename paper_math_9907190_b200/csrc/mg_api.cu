@@ -1,0 +1,643 @@
+// mg_api.cu -- the C ABI of include/mg.h: argument checking, the level plan
+// (buffers in HBM), the per-cycle launch schedule captured in a CUDA graph,
+// norms, staging.  Host code only; the kernels live in k2d.cu / k3d.cu.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "../../include/mg.h"
+#include "kernels.h"
+
+using namespace mg;
+
+namespace {
+
+constexpr int kHistCap = 4096;
+
+int log2_exact(int64_t v) {
+  if (v < 1) return -1;
+  int k = 0;
+  while ((int64_t(1) << k) < v) k++;
+  return ((int64_t(1) << k) == v) ? k : -1;
+}
+
+int64_t round_up(int64_t v, int64_t m) { return (v + m - 1) / m * m; }
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    if (dev >= 0) {
+      cudaGetDevice(&prev);
+      if (prev != dev) cudaSetDevice(dev);
+      else prev = -1;
+    }
+  }
+  ~DeviceGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
+
+}  // namespace
+
+// ---------------------------------------------------------------- solver
+struct ImplBase {
+  virtual ~ImplBase() {}
+  virtual cudaError_t alloc() = 0;
+  virtual void enqueue_cycle(void *u, const void *f_eff, cudaStream_t st) = 0;
+  virtual void enqueue_final_norm(void *u, const void *f_eff, cudaStream_t st) = 0;
+  virtual void enqueue_residual(const void *u, const void *f, void *r, cudaStream_t st) = 0;
+  virtual void enqueue_ftilde(const void *f, void *ft, cudaStream_t st) = 0;
+  virtual void enqueue_norm(const void *x, unsigned long long *mx, double *ss, cudaStream_t st) = 0;
+  virtual int launches_per_cycle() const = 0;
+  std::vector<void *> bufs;
+  size_t bytes = 0;
+  cudaError_t dalloc(void **p, size_t n) {
+    cudaError_t e = cudaMalloc(p, n);
+    if (e != cudaSuccess) return e;
+    bufs.push_back(*p);
+    bytes += n;
+    return cudaMemset(*p, 0, n);
+  }
+  void free_all() {
+    for (void *p : bufs) cudaFree(p);
+    bufs.clear();
+  }
+};
+
+struct mg_solver {
+  mg_config cfg{};
+  int k = 0, L = 0, esz = 8;
+  int64_t pitch = 0;
+  int device = 0;
+  cudaStream_t user = nullptr, st = nullptr;
+  cudaEvent_t ev_in = nullptr, ev_out = nullptr;
+  std::unique_ptr<ImplBase> impl;
+  unsigned long long *d_hist = nullptr;   // kHistCap slots
+  int *d_counter = nullptr;
+  unsigned long long *d_mx = nullptr;
+  double *d_ss = nullptr;
+  void *d_ft = nullptr;                    // order-4 f~ (n^d x pitch)
+  void *d_u_stage = nullptr, *d_f_stage = nullptr;   // mg_vcycle_host staging
+  cudaGraphExec_t gexec = nullptr;
+  const void *g_u = nullptr, *g_f = nullptr;
+  unsigned long long *h_hist = nullptr;    // pinned
+  std::string err;
+  size_t field_elems() const { return (size_t)((cfg.dim == 2) ? cfg.n * pitch : cfg.n * cfg.n * pitch); }
+};
+
+static int fail(mg_solver *s, int code, const std::string &msg) {
+  if (s) s->err = msg;
+  return code;
+}
+
+#define CKS(s, call)                                                                          \
+  do {                                                                                        \
+    cudaError_t e_ = (call);                                                                  \
+    if (e_ != cudaSuccess)                                                                    \
+      return fail((s), e_ == cudaErrorMemoryAllocation ? MG_ENOMEM : MG_ECUDA,                \
+                  std::string(#call) + ": " + cudaGetErrorString(e_));                        \
+  } while (0)
+
+// ------------------------------------------------------------------ 2D
+template <class T>
+struct Impl2 : ImplBase {
+  const mg_solver *s;
+  int k;
+  int64_t n, pitch;
+  // per octave o: D level (o = 0..k-2), A level (o = 1..k-1)
+  std::vector<S2<T>> rD, vD;
+  std::vector<D2<T>> rA, vA;
+  std::vector<int> M;   // lattice extent per octave
+  D2<T> scratch{};
+  Coef<T> coef{};
+  std::vector<T> cD, cA;   // Jacobi coefficients per octave
+  explicit Impl2(const mg_solver *sv) : s(sv), k(sv->k), n(sv->cfg.n), pitch(sv->pitch) {}
+
+  int64_t pitch_for(int64_t cnt) const { return round_up(cnt, 128 / (int64_t)sizeof(T)); }
+
+  cudaError_t alloc() override {
+    const double p = s->cfg.p[0];
+    M.resize(k);
+    rD.resize(k - 1);
+    vD.resize(k - 1);
+    rA.resize(k);
+    vA.resize(k);
+    cD.resize(k);
+    cA.resize(k);
+    for (int o = 0; o < k; o++) {
+      M[o] = (int)((n - 1) >> o);
+      double hs = std::ldexp(1.0, o) / (double)(n - 1);
+      cD[o] = (T)(2.0 * p * hs * hs);
+      cA[o] = (T)(p * hs * hs);
+    }
+    for (int o = 0; o + 1 < k; o++) {
+      int64_t H = M[o] / 2 + 1, ph = pitch_for(H);
+      for (auto *lv : {&rD, &vD}) {
+        void *e, *oo;
+        cudaError_t st = dalloc(&e, sizeof(T) * H * ph);
+        if (st) return st;
+        st = dalloc(&oo, sizeof(T) * H * ph);
+        if (st) return st;
+        (*lv)[o] = S2<T>{(T *)e, (T *)oo, ph};
+      }
+    }
+    for (int o = 1; o < k; o++) {
+      int64_t W = M[o] + 1, pa = pitch_for(W);
+      for (auto *lv : {&rA, &vA}) {
+        void *q;
+        cudaError_t st = dalloc(&q, sizeof(T) * W * pa);
+        if (st) return st;
+        (*lv)[o] = D2<T>{(T *)q, pa};
+      }
+    }
+    {
+      int64_t ps = pitch_for(n);
+      void *q;
+      cudaError_t st = dalloc(&q, sizeof(T) * n * ps);
+      if (st) return st;
+      scratch = D2<T>{(T *)q, ps};
+    }
+    coef.invh2 = (T)((double)(n - 1) * (double)(n - 1));
+    coef.c6 = (T)((double)(n - 1) * (double)(n - 1) / 6.0);
+    return cudaSuccess;
+  }
+
+  NormSink sink() const { return NormSink{s->d_hist, s->d_counter, kHistCap}; }
+
+  void enqueue_cycle(void *u, const void *f_eff, cudaStream_t st) override {
+    D2<const T> uc{(const T *)u, pitch}, fc{(const T *)f_eff, pitch};
+    D2<T> uu{(T *)u, pitch};
+    launch2_desc_fine<T>(uc, fc, rD[0], M[0], s->cfg.order, coef, sink(), st);
+    for (int o = 0; o + 1 < k; o++) {
+      if (o >= 1) launch2_rest_ad<T>(rA[o], rD[o], M[o], st);
+      launch2_rest_da<T>(rD[o], rA[o + 1], M[o + 1], st);
+    }
+    launch2_coarsest<T>(rA[k - 1], vA[k - 1], cA[k - 1], s->d_counter, st);
+    for (int o = k - 2; o >= 0; o--) {
+      launch2_jac_d<T>(vA[o + 1], rD[o], vD[o], M[o], cD[o], st);
+      if (o >= 1)
+        launch2_jac_a<T>(vD[o], rA[o], vA[o], M[o], cA[o], st);
+      else
+        launch2_asc_fine<T>(vD[0], uu, fc, scratch, M[0], s->cfg.order, cA[0], coef, st);
+    }
+  }
+  void enqueue_final_norm(void *u, const void *f_eff, cudaStream_t st) override {
+    D2<const T> uc{(const T *)u, pitch}, fc{(const T *)f_eff, pitch};
+    launch2_desc_fine<T>(uc, fc, rD[0], M[0], s->cfg.order, coef, sink(), st);
+  }
+  void enqueue_residual(const void *u, const void *f, void *r, cudaStream_t st) override {
+    launch2_residual<T>(D2<const T>{(const T *)u, pitch}, D2<const T>{(const T *)f, pitch}, D2<T>{(T *)r, pitch},
+                        M[0], s->cfg.order, coef, st);
+  }
+  void enqueue_ftilde(const void *f, void *ft, cudaStream_t st) override {
+    launch2_ftilde<T>(D2<const T>{(const T *)f, pitch}, D2<T>{(T *)ft, pitch}, M[0], st);
+  }
+  void enqueue_norm(const void *x, unsigned long long *mx, double *ss, cudaStream_t st) override {
+    launch2_norm<T>(D2<const T>{(const T *)x, pitch}, M[0], mx, ss, st);
+  }
+  int launches_per_cycle() const override {
+    int c = 1;                               // desc fine
+    for (int o = 0; o + 1 < k; o++) c += (o >= 1) + 1;
+    c += 1;                                  // coarsest
+    for (int o = k - 2; o >= 0; o--) c += 2 + ((o >= 1) ? 2 : 3);
+    return c;
+  }
+};
+
+// ------------------------------------------------------------------ 3D
+template <class T>
+struct Impl3 : ImplBase {
+  const mg_solver *s;
+  int k;
+  int64_t n, pitch;
+  std::vector<S3<T>> rR, vR, rM, vM;   // octave 0..k-2
+  std::vector<D3<T>> rG, vG;           // octave 1..k-1
+  std::vector<int> M;
+  D3<T> scratch{};
+  Coef<T> coef{};
+  std::vector<T> cMg, cR1, cR2, cG;
+  explicit Impl3(const mg_solver *sv) : s(sv), k(sv->k), n(sv->cfg.n), pitch(sv->pitch) {}
+  int64_t pitch_for(int64_t cnt) const { return round_up(cnt, 128 / (int64_t)sizeof(T)); }
+
+  cudaError_t split(S3<T> &out, int64_t H, std::initializer_list<int> parities) {
+    int64_t ph = pitch_for(H);
+    out = S3<T>{};
+    out.pitch = ph;
+    out.plane = ph * H;
+    for (int par : parities) {
+      void *q;
+      cudaError_t st = dalloc(&q, sizeof(T) * H * H * ph);
+      if (st) return st;
+      out.s[par] = (T *)q;
+    }
+    return cudaSuccess;
+  }
+
+  cudaError_t alloc() override {
+    const double pm = s->cfg.p[0], pr1 = s->cfg.p[1], pr2 = s->cfg.p[2], pg = s->cfg.p[3];
+    M.resize(k);
+    rR.resize(k - 1);
+    vR.resize(k - 1);
+    rM.resize(k - 1);
+    vM.resize(k - 1);
+    rG.resize(k);
+    vG.resize(k);
+    cMg.resize(k);
+    cR1.resize(k);
+    cR2.resize(k);
+    cG.resize(k);
+    for (int o = 0; o < k; o++) {
+      M[o] = (int)((n - 1) >> o);
+      double hs = std::ldexp(1.0, o) / (double)(n - 1);
+      double h2 = hs * hs;
+      cMg[o] = (T)(4.0 * pm * h2);
+      cR1[o] = (T)(2.0 * pr1 * h2);
+      cR2[o] = (T)(4.0 * pr2 * h2);
+      cG[o] = (T)(pg * h2);
+    }
+    // parity index = (x&1) | (y&1)<<1 | (z&1)<<2 ; C=0, Fx=(0,1,1)=6, Fy=(1,0,1)=5, Fz=(1,1,0)=3, B=7
+    for (int o = 0; o + 1 < k; o++) {
+      int64_t H = M[o] / 2 + 1;
+      cudaError_t st;
+      if ((st = split(rR[o], H, {0, 6, 5, 3}))) return st;
+      if ((st = split(vR[o], H, {0, 6, 5, 3}))) return st;
+      if ((st = split(rM[o], H, {0, 7}))) return st;
+      if ((st = split(vM[o], H, {0, 7}))) return st;
+    }
+    for (int o = 1; o < k; o++) {
+      int64_t W = M[o] + 1, pa = pitch_for(W);
+      for (auto *lv : {&rG, &vG}) {
+        void *q;
+        cudaError_t st = dalloc(&q, sizeof(T) * W * W * pa);
+        if (st) return st;
+        (*lv)[o] = D3<T>{(T *)q, pa, pa * W};
+      }
+    }
+    {
+      int64_t ps = pitch_for(n);
+      void *q;
+      cudaError_t st = dalloc(&q, sizeof(T) * n * n * ps);
+      if (st) return st;
+      scratch = D3<T>{(T *)q, ps, ps * n};
+    }
+    coef.invh2 = (T)((double)(n - 1) * (double)(n - 1));
+    coef.c6 = (T)((double)(n - 1) * (double)(n - 1) / 6.0);
+    return cudaSuccess;
+  }
+
+  NormSink sink() const { return NormSink{s->d_hist, s->d_counter, kHistCap}; }
+  D3<const T> cfield(const void *a) const { return D3<const T>{(const T *)a, pitch, pitch * n}; }
+  D3<T> field(void *a) const { return D3<T>{(T *)a, pitch, pitch * n}; }
+
+  void enqueue_cycle(void *u, const void *f_eff, cudaStream_t st) override {
+    launch3_desc_fine<T>(cfield(u), cfield(f_eff), rR[0], M[0], s->cfg.order, coef, sink(), st);
+    for (int o = 0; o + 1 < k; o++) {
+      if (o >= 1) launch3_rest_gr<T>(rG[o], rR[o], M[o], st);
+      launch3_rest_rm<T>(rR[o], rM[o], M[o], st);
+      launch3_rest_mg<T>(rM[o], rG[o + 1], M[o + 1], st);
+    }
+    launch3_coarsest<T>(rG[k - 1], vG[k - 1], cG[k - 1], s->d_counter, st);
+    for (int o = k - 2; o >= 0; o--) {
+      launch3_jac_m<T>(vG[o + 1], rM[o], vM[o], M[o], cMg[o], st);
+      launch3_jac_r<T>(vM[o], rR[o], vR[o], M[o], cR1[o], cR2[o], st);
+      if (o >= 1)
+        launch3_jac_g<T>(vR[o], rG[o], vG[o], M[o], cG[o], st);
+      else
+        launch3_asc_fine<T>(vR[0], field(u), cfield(f_eff), scratch, M[0], s->cfg.order, cG[0], coef, st);
+    }
+  }
+  void enqueue_final_norm(void *u, const void *f_eff, cudaStream_t st) override {
+    launch3_desc_fine<T>(cfield(u), cfield(f_eff), rR[0], M[0], s->cfg.order, coef, sink(), st);
+  }
+  void enqueue_residual(const void *u, const void *f, void *r, cudaStream_t st) override {
+    launch3_residual<T>(cfield(u), cfield(f), field(r), M[0], s->cfg.order, coef, st);
+  }
+  void enqueue_ftilde(const void *f, void *ft, cudaStream_t st) override {
+    launch3_ftilde<T>(cfield(f), field(ft), M[0], st);
+  }
+  void enqueue_norm(const void *x, unsigned long long *mx, double *ss, cudaStream_t st) override {
+    launch3_norm<T>(cfield(x), M[0], mx, ss, st);
+  }
+  int launches_per_cycle() const override {
+    int c = 1;
+    for (int o = 0; o + 1 < k; o++) c += (o >= 1) + 2;
+    c += 1;
+    for (int o = k - 2; o >= 0; o--) c += 2 + 2 + ((o >= 1) ? 2 : 3);
+    return c;
+  }
+};
+
+// ------------------------------------------------------------ helpers
+
+static void drop_graph(mg_solver *s) {
+  if (s->gexec) cudaGraphExecDestroy(s->gexec);
+  s->gexec = nullptr;
+  s->g_u = s->g_f = nullptr;
+}
+
+// Launch one V-cycle: replay the captured graph for (u, f_eff), capturing it
+// on first use or when the pointers change.
+static int run_cycle(mg_solver *s, void *u, const void *f_eff) {
+  if (!s->gexec || s->g_u != u || s->g_f != f_eff) {
+    drop_graph(s);
+    cudaGraph_t g = nullptr;
+    CKS(s, cudaStreamBeginCapture(s->st, cudaStreamCaptureModeThreadLocal));
+    s->impl->enqueue_cycle(u, f_eff, s->st);
+    cudaError_t le = cudaGetLastError();
+    cudaError_t e = cudaStreamEndCapture(s->st, &g);
+    if (le != cudaSuccess) {
+      if (g) cudaGraphDestroy(g);
+      return fail(s, MG_ECUDA, std::string("kernel launch during capture: ") + cudaGetErrorString(le));
+    }
+    CKS(s, e);
+    e = cudaGraphInstantiate(&s->gexec, g, 0);
+    cudaGraphDestroy(g);
+    CKS(s, e);
+    s->g_u = u;
+    s->g_f = f_eff;
+  }
+  CKS(s, cudaGraphLaunch(s->gexec, s->st));
+  return MG_OK;
+}
+
+static int begin(mg_solver *s) {
+  CKS(s, cudaEventRecord(s->ev_in, s->user));
+  CKS(s, cudaStreamWaitEvent(s->st, s->ev_in, 0));
+  return MG_OK;
+}
+static int end(mg_solver *s) {
+  CKS(s, cudaGetLastError());
+  CKS(s, cudaEventRecord(s->ev_out, s->st));
+  CKS(s, cudaStreamWaitEvent(s->user, s->ev_out, 0));
+  return MG_OK;
+}
+
+static int check_config(const mg_config *c, int *k_out) {
+  if (!c) return MG_EINVAL;
+  if (c->dim != 2 && c->dim != 3) return MG_EINVAL;
+  if (c->order != 2 && c->order != 4) return MG_EINVAL;
+  if (c->dtype != MG_F64 && c->dtype != MG_F32) return MG_EINVAL;
+  int k = log2_exact(c->n - 1);
+  if (k < 2) return MG_EINVAL;
+  if (c->dim == 3 && c->n > 2049) return MG_EUNSUPPORTED;
+  if (c->n > (int64_t(1) << 30)) return MG_EUNSUPPORTED;
+  int np = (c->dim == 2) ? 1 : 4;
+  for (int i = 0; i < np; i++)
+    if (!(c->p[i] > 0.0 && c->p[i] <= 3.0)) return MG_EINVAL;
+  if (c->pitch != 0 && c->pitch < c->n) return MG_EINVAL;
+  if (c->nranks < 0 || (c->nranks > 1 && (c->rank < 0 || c->rank >= c->nranks))) return MG_EINVAL;
+  if (c->nranks > 1) return MG_EUNSUPPORTED;   // multi-GPU lives in the comm layer
+  *k_out = k;
+  return MG_OK;
+}
+
+// =================================================================== ABI
+extern "C" {
+
+int mg_create_ex(const mg_config *cfg, mg_solver **out) {
+  if (!out) return MG_EINVAL;
+  *out = nullptr;
+  int k = 0;
+  int rc = check_config(cfg, &k);
+  if (rc != MG_OK) return rc;
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+    cudaGetLastError();
+    return MG_ENODEV;
+  }
+  auto s = std::make_unique<mg_solver>();
+  s->cfg = *cfg;
+  s->k = k;
+  s->L = (cfg->dim == 2) ? 2 * k - 1 : 3 * k - 2;
+  s->esz = (cfg->dtype == MG_F64) ? 8 : 4;
+  s->pitch = cfg->pitch ? cfg->pitch : cfg->n;
+  s->cfg.pitch = s->pitch;
+  if (cfg->nranks == 0) s->cfg.nranks = 1;
+  if (cfg->device >= 0) {
+    if (cfg->device >= ndev) return MG_EINVAL;
+    s->device = cfg->device;
+  } else {
+    cudaGetDevice(&s->device);
+  }
+  DeviceGuard g(s->device);
+  s->user = (cudaStream_t)cfg->stream;
+  mg_solver *sp = s.get();
+  CKS(sp, cudaStreamCreateWithFlags(&s->st, cudaStreamNonBlocking));
+  CKS(sp, cudaEventCreateWithFlags(&s->ev_in, cudaEventDisableTiming));
+  CKS(sp, cudaEventCreateWithFlags(&s->ev_out, cudaEventDisableTiming));
+  CKS(sp, cudaMalloc(&s->d_hist, sizeof(unsigned long long) * kHistCap));
+  CKS(sp, cudaMalloc(&s->d_counter, sizeof(int)));
+  CKS(sp, cudaMalloc(&s->d_mx, sizeof(unsigned long long)));
+  CKS(sp, cudaMalloc(&s->d_ss, sizeof(double)));
+  CKS(sp, cudaMemset(s->d_hist, 0, sizeof(unsigned long long) * kHistCap));
+  CKS(sp, cudaMemset(s->d_counter, 0, sizeof(int)));
+  CKS(sp, cudaMallocHost(&s->h_hist, sizeof(unsigned long long) * kHistCap));
+  if (cfg->dim == 2) {
+    if (cfg->dtype == MG_F64) s->impl.reset(new Impl2<double>(sp));
+    else s->impl.reset(new Impl2<float>(sp));
+  } else {
+    if (cfg->dtype == MG_F64) s->impl.reset(new Impl3<double>(sp));
+    else s->impl.reset(new Impl3<float>(sp));
+  }
+  cudaError_t e = s->impl->alloc();
+  if (e != cudaSuccess) {
+    int code = (e == cudaErrorMemoryAllocation) ? MG_ENOMEM : MG_ECUDA;
+    mg_destroy(s.release());
+    return code;
+  }
+  if (cfg->order == 4) {
+    CKS(sp, cudaMalloc(&s->d_ft, s->field_elems() * s->esz));
+    CKS(sp, cudaMemset(s->d_ft, 0, s->field_elems() * s->esz));
+  }
+  CKS(sp, cudaDeviceSynchronize());
+  *out = s.release();
+  return MG_OK;
+}
+
+int mg_create(int dim, int64_t n, int order, double omega, mg_solver **out) {
+  mg_config c{};
+  c.dim = dim;
+  c.n = n;
+  c.order = order;
+  c.dtype = MG_F64;
+  for (int i = 0; i < 4; i++) c.p[i] = omega;
+  c.pitch = 0;
+  c.stream = nullptr;
+  c.device = -1;
+  c.nranks = 1;
+  c.rank = 0;
+  return mg_create_ex(&c, out);
+}
+
+int mg_destroy(mg_solver *s) {
+  if (!s) return MG_OK;
+  DeviceGuard g(s->device);
+  if (s->st) cudaStreamSynchronize(s->st);
+  drop_graph(s);
+  if (s->impl) s->impl->free_all();
+  cudaFree(s->d_hist);
+  cudaFree(s->d_counter);
+  cudaFree(s->d_mx);
+  cudaFree(s->d_ss);
+  cudaFree(s->d_ft);
+  cudaFree(s->d_u_stage);
+  cudaFree(s->d_f_stage);
+  if (s->h_hist) cudaFreeHost(s->h_hist);
+  if (s->ev_in) cudaEventDestroy(s->ev_in);
+  if (s->ev_out) cudaEventDestroy(s->ev_out);
+  if (s->st) cudaStreamDestroy(s->st);
+  delete s;
+  return MG_OK;
+}
+
+int mg_local_extent(const mg_solver *s, int64_t *lo, int64_t *hi, int64_t *ghost) {
+  if (!s) return MG_EINVAL;
+  if (lo) *lo = 0;
+  if (hi) *hi = s->cfg.n;
+  if (ghost) *ghost = 0;
+  return MG_OK;
+}
+
+int mg_num_levels(const mg_solver *s) { return s ? s->L : MG_EINVAL; }
+
+int64_t mg_level_points(const mg_solver *s, int lev) {
+  if (!s || lev < 0 || lev >= s->L) return MG_EINVAL;
+  int dim = s->cfg.dim;
+  int o = (dim == 2) ? lev / 2 : lev / 3, cls = (dim == 2) ? lev % 2 : lev % 3;
+  int64_t m = ((s->cfg.n - 1) >> o) - 1;
+  int64_t od = (m + 1) / 2, ev = (m - 1) / 2;
+  if (dim == 2) return cls == 0 ? m * m : (m * m + 1) / 2;
+  if (cls == 0) return m * m * m;
+  if (cls == 1) return ev * ev * ev + 3 * ev * od * od;
+  return ev * ev * ev + od * od * od;
+}
+
+int mg_launches_per_cycle(const mg_solver *s) { return s ? s->impl->launches_per_cycle() : MG_EINVAL; }
+
+int mg_residual(mg_solver *s, const void *u, const void *f, void *r) {
+  if (!s || !u || !f || !r) return fail(s, MG_EINVAL, "mg_residual: NULL argument");
+  DeviceGuard g(s->device);
+  int rc = begin(s);
+  if (rc) return rc;
+  const void *fe = f;
+  if (s->cfg.order == 4) {
+    // r uses f~ formed from f (Efos2/Efos4); reuse the f~ buffer
+    s->impl->enqueue_ftilde(f, s->d_ft, s->st);
+    fe = s->d_ft;
+  }
+  s->impl->enqueue_residual(u, fe, r, s->st);
+  return end(s);
+}
+
+static int vcycle_dev(mg_solver *s, void *u, const void *f, int ncycles, double *res_hist) {
+  const void *fe = f;
+  if (s->cfg.order == 4) {
+    s->impl->enqueue_ftilde(f, s->d_ft, s->st);
+    fe = s->d_ft;
+  }
+  int nslots = ncycles + 1 < kHistCap ? ncycles + 1 : kHistCap;
+  CKS(s, cudaMemsetAsync(s->d_hist, 0, sizeof(unsigned long long) * nslots, s->st));
+  CKS(s, cudaMemsetAsync(s->d_counter, 0, sizeof(int), s->st));
+  for (int c = 0; c < ncycles; c++) {
+    int rc = run_cycle(s, u, fe);
+    if (rc) return rc;
+  }
+  if (res_hist) {
+    s->impl->enqueue_final_norm(u, fe, s->st);
+    CKS(s, cudaMemcpyAsync(s->h_hist, s->d_hist, sizeof(unsigned long long) * nslots, cudaMemcpyDeviceToHost, s->st));
+    CKS(s, cudaStreamSynchronize(s->st));
+    bool finite = true;
+    for (int i = 0; i <= ncycles; i++) {
+      double v;
+      unsigned long long b = s->h_hist[i < kHistCap ? i : kHistCap - 1];
+      std::memcpy(&v, &b, sizeof v);
+      res_hist[i] = v;
+      if (!std::isfinite(v)) finite = false;
+    }
+    if (!finite) return fail(s, MG_EDIVERGED, "non-finite residual norm");
+  }
+  return MG_OK;
+}
+
+int mg_vcycle(mg_solver *s, void *u, const void *f, int ncycles, double *res_hist) {
+  if (!s) return MG_EINVAL;
+  if (!u || !f) return fail(s, MG_EINVAL, "mg_vcycle: NULL u or f");
+  if (ncycles < 0) return fail(s, MG_EINVAL, "mg_vcycle: ncycles < 0");
+  if (ncycles == 0 && !res_hist) return MG_OK;
+  DeviceGuard g(s->device);
+  int rc = begin(s);
+  if (rc) return rc;
+  rc = vcycle_dev(s, u, f, ncycles, res_hist);
+  int rc2 = end(s);
+  return rc ? rc : rc2;
+}
+
+int mg_vcycle_host(mg_solver *s, void *u_host, const void *f_host, int ncycles, double *res_hist) {
+  if (!s) return MG_EINVAL;
+  if (!u_host || !f_host) return fail(s, MG_EINVAL, "mg_vcycle_host: NULL u or f");
+  if (ncycles < 0) return fail(s, MG_EINVAL, "mg_vcycle_host: ncycles < 0");
+  DeviceGuard g(s->device);
+  size_t bytes = s->field_elems() * s->esz;
+  if (!s->d_u_stage) {
+    CKS(s, cudaMalloc(&s->d_u_stage, bytes));
+    CKS(s, cudaMalloc(&s->d_f_stage, bytes));
+  }
+  int rc = begin(s);
+  if (rc) return rc;
+  CKS(s, cudaMemcpyAsync(s->d_u_stage, u_host, bytes, cudaMemcpyHostToDevice, s->st));
+  CKS(s, cudaMemcpyAsync(s->d_f_stage, f_host, bytes, cudaMemcpyHostToDevice, s->st));
+  rc = vcycle_dev(s, s->d_u_stage, s->d_f_stage, ncycles, res_hist);
+  if (rc) return rc;
+  CKS(s, cudaMemcpyAsync(u_host, s->d_u_stage, bytes, cudaMemcpyDeviceToHost, s->st));
+  CKS(s, cudaStreamSynchronize(s->st));
+  return end(s);
+}
+
+int mg_norm(mg_solver *s, const void *x, int kind, double *out) {
+  if (!s || !x || !out) return fail(s, MG_EINVAL, "mg_norm: NULL argument");
+  if (kind != MG_NORM_INF && kind != MG_NORM_L2) return fail(s, MG_EINVAL, "mg_norm: bad kind");
+  DeviceGuard g(s->device);
+  int rc = begin(s);
+  if (rc) return rc;
+  CKS(s, cudaMemsetAsync(s->d_mx, 0, sizeof(unsigned long long), s->st));
+  CKS(s, cudaMemsetAsync(s->d_ss, 0, sizeof(double), s->st));
+  s->impl->enqueue_norm(x, s->d_mx, s->d_ss, s->st);
+  unsigned long long mx = 0;
+  double ss = 0;
+  CKS(s, cudaMemcpyAsync(&mx, s->d_mx, sizeof mx, cudaMemcpyDeviceToHost, s->st));
+  CKS(s, cudaMemcpyAsync(&ss, s->d_ss, sizeof ss, cudaMemcpyDeviceToHost, s->st));
+  CKS(s, cudaStreamSynchronize(s->st));
+  rc = end(s);
+  if (rc) return rc;
+  if (kind == MG_NORM_INF) {
+    std::memcpy(out, &mx, sizeof(double));
+  } else {
+    double h = 1.0 / (double)(s->cfg.n - 1);
+    *out = std::sqrt(std::pow(h, s->cfg.dim) * ss);
+  }
+  if (!std::isfinite(*out)) return fail(s, MG_EDIVERGED, "non-finite norm");
+  return MG_OK;
+}
+
+const char *mg_strerror(int status) {
+  switch (status) {
+    case MG_OK: return "ok";
+    case MG_EINVAL: return "invalid argument";
+    case MG_ENOMEM: return "out of memory";
+    case MG_ECUDA: return "CUDA error";
+    case MG_ENCCL: return "NCCL error";
+    case MG_EUNSUPPORTED: return "unsupported configuration";
+    case MG_EDIVERGED: return "diverged (non-finite norm)";
+    case MG_ENODEV: return "no CUDA device";
+    default: return "unknown status";
+  }
+}
+
+const char *mg_last_error(const mg_solver *s) { return s ? s->err.c_str() : "NULL handle"; }
+
+}  // extern "C"
