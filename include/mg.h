@@ -130,6 +130,23 @@ int64_t mg_level_points(const mg_solver *s, int lev);
  * gpu_launches count). */
 int mg_launches_per_cycle(const mg_solver *s);
 
+/* Per-step timing of the V-cycle, for the roofline report.  Runs `ncycles`
+ * cycles on (u, f) exactly like mg_vcycle but launched step by step (no CUDA
+ * graph) with a CUDA event between steps on the solver's stream; fills up to
+ * `cap` entries (one per step of one cycle, finest first) with the step's
+ * name, level, kernel launches, mean duration over the cycles and its
+ * algorithmic bytes (every array the step must read or write,
+ * once, interior nodes only).  Returns the number of steps (> cap: truncated)
+ * or a negative mg_status.  Synchronises. */
+typedef struct {
+  char name[40];
+  int level;          /* finer level the step works on (0 = finest) */
+  int launches;       /* kernel launches in the step */
+  double ms;          /* mean duration per cycle, CUDA events */
+  double alg_bytes;   /* algorithmic bytes moved per launch of the step */
+} mg_step_stat;
+int mg_profile(mg_solver *s, void *u, const void *f, int ncycles, mg_step_stat *out, int cap);
+
 const char *mg_strerror(int status);
 const char *mg_last_error(const mg_solver *s);
 

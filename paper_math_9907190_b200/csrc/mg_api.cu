@@ -44,11 +44,47 @@ struct DeviceGuard {
 
 }  // namespace
 
+// ---------------------------------------------------------------- profiler
+// Step markers: in profile mode every step of the cycle is preceded by a CUDA
+// event on the solver's stream; otherwise the markers cost nothing.
+struct StepInfo {
+  std::string name;
+  int level, launches;
+  double bytes;
+};
+struct Prof {
+  cudaStream_t st = nullptr;
+  bool first = true;
+  std::vector<StepInfo> steps;
+  std::vector<cudaEvent_t> evs;   // (nsteps + 1) per cycle
+  void step(const char *name, int level, int launches, double bytes) {
+    if (first) steps.push_back(StepInfo{name, level, launches, bytes});
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    cudaEventRecord(e, st);
+    evs.push_back(e);
+  }
+  void end_cycle() {
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    cudaEventRecord(e, st);
+    evs.push_back(e);
+    first = false;
+  }
+  ~Prof() {
+    for (auto e : evs) cudaEventDestroy(e);
+  }
+};
+#define STEP(name, lev, nl, bytes) \
+  do {                              \
+    if (prof) prof->step(name, lev, nl, bytes); \
+  } while (0)
+
 // ---------------------------------------------------------------- solver
 struct ImplBase {
   virtual ~ImplBase() {}
   virtual cudaError_t alloc() = 0;
-  virtual void enqueue_cycle(void *u, const void *f_eff, cudaStream_t st) = 0;
+  virtual void enqueue_cycle(void *u, const void *f_eff, cudaStream_t st, Prof *prof = nullptr) = 0;
   virtual void enqueue_final_norm(void *u, const void *f_eff, cudaStream_t st) = 0;
   virtual void enqueue_residual(const void *u, const void *f, void *r, cudaStream_t st) = 0;
   virtual void enqueue_ftilde(const void *f, void *ft, cudaStream_t st) = 0;
@@ -56,6 +92,7 @@ struct ImplBase {
   virtual int launches_per_cycle() const = 0;
   std::vector<void *> bufs;
   size_t bytes = 0;
+  std::vector<double> Nl;   // interior nodes per level
   cudaError_t dalloc(void **p, size_t n) {
     cudaError_t e = cudaMalloc(p, n);
     if (e != cudaSuccess) return e;
@@ -169,21 +206,33 @@ struct Impl2 : ImplBase {
 
   NormSink sink() const { return NormSink{s->d_hist, s->d_counter, kHistCap}; }
 
-  void enqueue_cycle(void *u, const void *f_eff, cudaStream_t st) override {
+  void enqueue_cycle(void *u, const void *f_eff, cudaStream_t st, Prof *prof) override {
     D2<const T> uc{(const T *)u, pitch}, fc{(const T *)f_eff, pitch};
     D2<T> uu{(T *)u, pitch};
+    const double w = sizeof(T);
+    const int L = 2 * k - 1;
+    STEP("desc_fine", 0, 1, w * (2 * Nl[0] + Nl[1]));
     launch2_desc_fine<T>(uc, fc, rD[0], M[0], s->cfg.order, coef, sink(), st);
     for (int o = 0; o + 1 < k; o++) {
-      if (o >= 1) launch2_rest_ad<T>(rA[o], rD[o], M[o], st);
+      if (o >= 1) {
+        STEP("rest_ad", 2 * o, 1, w * (Nl[2 * o] + Nl[2 * o + 1]));
+        launch2_rest_ad<T>(rA[o], rD[o], M[o], st);
+      }
+      STEP("rest_da", 2 * o + 1, 1, w * (Nl[2 * o + 1] + Nl[2 * o + 2]));
       launch2_rest_da<T>(rD[o], rA[o + 1], M[o + 1], st);
     }
+    STEP("coarsest", L - 1, 1, w * 2);
     launch2_coarsest<T>(rA[k - 1], vA[k - 1], cA[k - 1], s->d_counter, st);
     for (int o = k - 2; o >= 0; o--) {
+      STEP("jac_d", 2 * o + 1, 2, w * (Nl[2 * o + 2] + 2 * Nl[2 * o + 1]));
       launch2_jac_d<T>(vA[o + 1], rD[o], vD[o], M[o], cD[o], st);
-      if (o >= 1)
+      if (o >= 1) {
+        STEP("jac_a", 2 * o, 2, w * (Nl[2 * o + 1] + 2 * Nl[2 * o]));
         launch2_jac_a<T>(vD[o], rA[o], vA[o], M[o], cA[o], st);
-      else
+      } else {
+        STEP("asc_fine", 0, 3, w * (Nl[1] + 3 * Nl[0]));
         launch2_asc_fine<T>(vD[0], uu, fc, scratch, M[0], s->cfg.order, cA[0], coef, st);
+      }
     }
   }
   void enqueue_final_norm(void *u, const void *f_eff, cudaStream_t st) override {
@@ -294,21 +343,37 @@ struct Impl3 : ImplBase {
   D3<const T> cfield(const void *a) const { return D3<const T>{(const T *)a, pitch, pitch * n}; }
   D3<T> field(void *a) const { return D3<T>{(T *)a, pitch, pitch * n}; }
 
-  void enqueue_cycle(void *u, const void *f_eff, cudaStream_t st) override {
+  void enqueue_cycle(void *u, const void *f_eff, cudaStream_t st, Prof *prof) override {
+    const double w = sizeof(T);
+    const int L = 3 * k - 2;
+    STEP("desc_fine", 0, 1, w * (2 * Nl[0] + Nl[1]));
     launch3_desc_fine<T>(cfield(u), cfield(f_eff), rR[0], M[0], s->cfg.order, coef, sink(), st);
     for (int o = 0; o + 1 < k; o++) {
-      if (o >= 1) launch3_rest_gr<T>(rG[o], rR[o], M[o], st);
+      int g = 3 * o;
+      if (o >= 1) {
+        STEP("rest_gr", g, 1, w * (Nl[g] + Nl[g + 1]));
+        launch3_rest_gr<T>(rG[o], rR[o], M[o], st);
+      }
+      STEP("rest_rm", g + 1, 1, w * (Nl[g + 1] + Nl[g + 2]));
       launch3_rest_rm<T>(rR[o], rM[o], M[o], st);
+      STEP("rest_mg", g + 2, 1, w * (Nl[g + 2] + Nl[g + 3]));
       launch3_rest_mg<T>(rM[o], rG[o + 1], M[o + 1], st);
     }
+    STEP("coarsest", L - 1, 1, w * 2);
     launch3_coarsest<T>(rG[k - 1], vG[k - 1], cG[k - 1], s->d_counter, st);
     for (int o = k - 2; o >= 0; o--) {
+      int g = 3 * o;
+      STEP("jac_m", g + 2, 2, w * (Nl[g + 3] + 2 * Nl[g + 2]));
       launch3_jac_m<T>(vG[o + 1], rM[o], vM[o], M[o], cMg[o], st);
+      STEP("jac_r", g + 1, 2, w * (Nl[g + 2] + 2 * Nl[g + 1]));
       launch3_jac_r<T>(vM[o], rR[o], vR[o], M[o], cR1[o], cR2[o], st);
-      if (o >= 1)
+      if (o >= 1) {
+        STEP("jac_g", g, 2, w * (Nl[g + 1] + 2 * Nl[g]));
         launch3_jac_g<T>(vR[o], rG[o], vG[o], M[o], cG[o], st);
-      else
+      } else {
+        STEP("asc_fine", 0, 3, w * (Nl[1] + 3 * Nl[0]));
         launch3_asc_fine<T>(vR[0], field(u), cfield(f_eff), scratch, M[0], s->cfg.order, cG[0], coef, st);
+      }
     }
   }
   void enqueue_final_norm(void *u, const void *f_eff, cudaStream_t st) override {
@@ -450,6 +515,7 @@ int mg_create_ex(const mg_config *cfg, mg_solver **out) {
     mg_destroy(s.release());
     return code;
   }
+  for (int l = 0; l < s->L; l++) s->impl->Nl.push_back((double)mg_level_points(sp, l));
   if (cfg->order == 4) {
     CKS(sp, cudaMalloc(&s->d_ft, s->field_elems() * s->esz));
     CKS(sp, cudaMemset(s->d_ft, 0, s->field_elems() * s->esz));
@@ -622,6 +688,46 @@ int mg_norm(mg_solver *s, const void *x, int kind, double *out) {
   }
   if (!std::isfinite(*out)) return fail(s, MG_EDIVERGED, "non-finite norm");
   return MG_OK;
+}
+
+int mg_profile(mg_solver *s, void *u, const void *f, int ncycles, mg_step_stat *out, int cap) {
+  if (!s) return MG_EINVAL;
+  if (!u || !f || ncycles < 1 || cap < 0 || (cap > 0 && !out)) return fail(s, MG_EINVAL, "mg_profile: bad argument");
+  DeviceGuard g(s->device);
+  int rc = begin(s);
+  if (rc) return rc;
+  const void *fe = f;
+  if (s->cfg.order == 4) {
+    s->impl->enqueue_ftilde(f, s->d_ft, s->st);
+    fe = s->d_ft;
+  }
+  CKS(s, cudaMemsetAsync(s->d_counter, 0, sizeof(int), s->st));
+  Prof prof;
+  prof.st = s->st;
+  for (int c = 0; c < ncycles; c++) {
+    s->impl->enqueue_cycle(u, fe, s->st, &prof);
+    prof.end_cycle();
+  }
+  CKS(s, cudaGetLastError());
+  CKS(s, cudaStreamSynchronize(s->st));
+  size_t ns = prof.steps.size();
+  std::vector<double> acc(ns, 0.0);
+  for (int c = 0; c < ncycles; c++)
+    for (size_t i = 0; i < ns; i++) {
+      float ms = 0;
+      CKS(s, cudaEventElapsedTime(&ms, prof.evs[c * (ns + 1) + i], prof.evs[c * (ns + 1) + i + 1]));
+      acc[i] += ms;
+    }
+  for (size_t i = 0; i < ns && (int)i < cap; i++) {
+    std::memset(out[i].name, 0, sizeof out[i].name);
+    std::strncpy(out[i].name, prof.steps[i].name.c_str(), sizeof out[i].name - 1);
+    out[i].level = prof.steps[i].level;
+    out[i].launches = prof.steps[i].launches;
+    out[i].ms = acc[i] / ncycles;
+    out[i].alg_bytes = prof.steps[i].bytes;
+  }
+  rc = end(s);
+  return rc ? rc : (int)ns;
 }
 
 const char *mg_strerror(int status) {

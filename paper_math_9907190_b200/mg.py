@@ -50,6 +50,11 @@ class mg_config(ctypes.Structure):
     ]
 
 
+class mg_step_stat(ctypes.Structure):
+    _fields_ = [("name", ctypes.c_char * 40), ("level", ctypes.c_int), ("launches", ctypes.c_int),
+                ("ms", ctypes.c_double), ("alg_bytes", ctypes.c_double)]
+
+
 EXPORTS = {
     "mg_create": (ctypes.c_int, [ctypes.c_int, ctypes.c_int64, ctypes.c_int, ctypes.c_double, ctypes.c_void_p]),
     "mg_create_ex": (ctypes.c_int, [ctypes.POINTER(mg_config), ctypes.c_void_p]),
@@ -65,6 +70,8 @@ EXPORTS = {
     "mg_num_levels": (ctypes.c_int, [ctypes.c_void_p]),
     "mg_level_points": (ctypes.c_int64, [ctypes.c_void_p, ctypes.c_int]),
     "mg_launches_per_cycle": (ctypes.c_int, [ctypes.c_void_p]),
+    "mg_profile": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int,
+                                  ctypes.POINTER(mg_step_stat), ctypes.c_int]),
     "mg_strerror": (ctypes.c_char_p, [ctypes.c_int]),
     "mg_last_error": (ctypes.c_char_p, [ctypes.c_void_p]),
 }
@@ -158,6 +165,16 @@ def mg_launches_per_cycle(h) -> int:
     return load().mg_launches_per_cycle(h)
 
 
+def mg_profile(h, u_ptr: int, f_ptr: int, ncycles: int, cap: int = 256):
+    """Per-step mean durations (CUDA events) and algorithmic bytes of one cycle."""
+    buf = (mg_step_stat * cap)()
+    rc = load().mg_profile(h, u_ptr, f_ptr, ncycles, buf, cap)
+    if rc < 0:
+        _check(rc, h, "mg_profile")
+    return [dict(name=b.name.decode(), level=b.level, launches=b.launches, ms=b.ms, alg_bytes=b.alg_bytes)
+            for b in buf[: min(rc, cap)]]
+
+
 def mg_last_error(h) -> str:
     return (load().mg_last_error(h) or b"").decode()
 
@@ -248,6 +265,9 @@ class Solver:
         """u_host / f_host: CPU tensors (ideally pinned) of ``self.shape``."""
         assert u_host.shape == self.shape and f_host.shape == self.shape and not u_host.is_cuda
         return mg_vcycle_host(self.h, u_host.data_ptr(), f_host.data_ptr(), ncycles, hist)
+
+    def profile(self, u, f, ncycles: int = 5):
+        return mg_profile(self.h, self._chk(u), self._chk(f), ncycles)
 
     @property
     def levels(self) -> int:
