@@ -38,6 +38,15 @@ struct S2 {
   }
 };
 
+// A shared-memory tile addressed by global lattice coordinates:
+// element (x, y) at p[(y - oy) * ld + (x - ox)].
+template <class T>
+struct Tile2 {
+  const T *p;
+  int ld, ox, oy;
+  __device__ __forceinline__ T operator()(int x, int y) const { return p[(y - oy) * ld + (x - ox)]; }
+};
+
 // Dense 3D lattice array.
 template <class T>
 struct D3 {

@@ -8,85 +8,13 @@
 // Level kernels in this file work on lattice coordinates of one octave
 // s = 2^o (x = i/s, y = j/s), M = (n-1)/s.
 #include "kernels.h"
+#include "ops2.cuh"
 
 namespace mg {
 
 constexpr int NT = 256;
 
 static inline unsigned blocks_for(int64_t n, int nt = NT) { return (unsigned)((n + nt - 1) / nt); }
-
-// ------------------------------------------------------------ residual
-// r = f - L u at an interior node (Evpois).
-//  order 2: 5-point Laplacian, centre first then (i-1,j),(i,j-1),(i+1,j),(i,j+1)
-//           (the neighbour order of Erest2r); 7 flops.
-//  order 4: Efos2 with f~ precomputed: bracket
-//           -20u + 4(u_{i,j-1}+u_{i,j+1}+u_{i-1,j}+u_{i+1,j}) + u_{i+1,j+1}
-//           + u_{i-1,j+1} + u_{i-1,j-1} + u_{i+1,j-1}, times 1/(6h^2).
-template <class T, int ORDER>
-__device__ __forceinline__ T res2(const D2<const T> &u, const D2<const T> &f, int x, int y, const Coef<T> &k) {
-  if (ORDER == 2) {
-    T lap = -((T)4 * u(x, y));
-    lap = lap + u(x - 1, y);
-    lap = lap + u(x, y - 1);
-    lap = lap + u(x + 1, y);
-    lap = lap + u(x, y + 1);
-    lap = lap * k.invh2;
-    return f(x, y) - lap;
-  } else {
-    T ax = u(x, y - 1);
-    ax = ax + u(x, y + 1);
-    ax = ax + u(x - 1, y);
-    ax = ax + u(x + 1, y);
-    T b = -((T)20 * u(x, y));
-    b = b + (T)4 * ax;
-    b = b + u(x + 1, y + 1);
-    b = b + u(x - 1, y + 1);
-    b = b + u(x - 1, y - 1);
-    b = b + u(x + 1, y - 1);
-    return f(x, y) - b * k.c6;
-  }
-}
-
-// r at any lattice node of the finest grid: 0 on the boundary (reading A1).
-template <class T, int ORDER>
-__device__ __forceinline__ T res2z(const D2<const T> &u, const D2<const T> &f, int x, int y, int M, const Coef<T> &k) {
-  if (x <= 0 || y <= 0 || x >= M || y >= M) return (T)0;
-  return res2<T, ORDER>(u, f, x, y, k);
-}
-
-// Erest2r: (1/8)(4r + r_{i-1,j} + r_{i,j-1} + r_{i+1,j} + r_{i,j+1}).
-template <class T>
-__device__ __forceinline__ T erest2r(T c, T w, T s, T e, T n) {
-  T t = (T)4 * c;
-  t = t + w;
-  t = t + s;
-  t = t + e;
-  t = t + n;
-  return t * (T)0.125;
-}
-
-// Erest2b: (1/8)(4r + r_{i-1,j-1} + r_{i+1,j-1} + r_{i+1,j+1} + r_{i-1,j+1}).
-template <class T>
-__device__ __forceinline__ T erest2b(T c, T sw, T se, T ne, T nw) {
-  T t = (T)4 * c;
-  t = t + sw;
-  t = t + se;
-  t = t + ne;
-  t = t + nw;
-  return t * (T)0.125;
-}
-
-// Jacobi (Eajacr/Eajacb P:350-359, green "similarly" P:360):
-// (1/4)(-c r + v1 + v2 + v3 + v4), c = kappa p (sh)^2.
-template <class T>
-__device__ __forceinline__ T jac4(T c, T r, T v1, T v2, T v3, T v4) {
-  T t = -(c * r);
-  t = t + v1;
-  t = t + v2;
-  t = t + v3;
-  t = t + v4;
-  return t * (T)0.25;
-}
 
 // ------------------------------------------------- descent, finest level
 // Fused a1+a2: residual on A(1) recomputed on the fly, Erest2r onto D(1).
@@ -127,92 +55,89 @@ __global__ void __launch_bounds__(NT) k2_desc_fine_ref(D2<const T> u, D2<const T
 }
 
 // ------------------------------------------------- descent, level kernels
-// a2 for s > 1: Erest2r from the dense A(s) residual onto D(s).
 template <class T>
 __global__ void __launch_bounds__(NT) k2_rest_ad_ref(D2<const T> r, S2<T> d, int M) {
-  int H = M / 2 + 1;
   int64_t t = (int64_t)blockIdx.x * NT + threadIdx.x;
-  if (t >= (int64_t)H * H) return;
-  int a = (int)(t % H), b = (int)(t / H);
-  int x = 2 * a, y = 2 * b;
-  if (x >= 2 && y >= 2 && x <= M - 2 && y <= M - 2)
-    d.e[(int64_t)b * d.pitch + a] = erest2r(r(x, y), r(x - 1, y), r(x, y - 1), r(x + 1, y), r(x, y + 1));
-  x += 1;
-  y += 1;
-  if (x <= M - 1 && y <= M - 1)
-    d.o[(int64_t)b * d.pitch + a] = erest2r(r(x, y), r(x - 1, y), r(x, y - 1), r(x + 1, y), r(x, y + 1));
+  if (t < (int64_t)(M / 2 + 1) * (M / 2 + 1)) node_rest_ad(r, d, M, t);
 }
 
-// a3: Erest2b from D(s) onto A(2s); coarse node (X,Y) is lattice node (2X,2Y).
 template <class T>
 __global__ void __launch_bounds__(NT) k2_rest_da_ref(S2<const T> d, D2<T> r, int Mc) {
   int64_t t = (int64_t)blockIdx.x * NT + threadIdx.x;
-  int W = Mc - 1;
-  if (t >= (int64_t)W * W) return;
-  int X = (int)(t % W) + 1, Y = (int)(t / W) + 1;
-  int x = 2 * X, y = 2 * Y;
-  r(X, Y) = erest2b(d.get(x, y), d.get(x - 1, y - 1), d.get(x + 1, y - 1), d.get(x + 1, y + 1), d.get(x - 1, y + 1));
+  if (t < (int64_t)(Mc - 1) * (Mc - 1)) node_rest_da(d, r, Mc, t);
 }
 
-// a4: coarsest level, one interior node (reading A4): v = (1/4)(-p H^2 r).
 template <class T>
 __global__ void k2_coarsest(D2<const T> r, D2<T> v, T c, int *counter) {
-  if (threadIdx.x == 0 && blockIdx.x == 0) {
-    v(1, 1) = (-(c * r(1, 1))) * (T)0.25;
-    if (counter) *counter += 1;   // this cycle's norm slot is complete
-  }
+  if (threadIdx.x == 0 && blockIdx.x == 0) node_coarsest(r, v, c, counter);
 }
 
 // ------------------------------------------------ ascent, diagonal level
-// a5: colour 1 on O (nodes of D(s) not on A(2s)): Eajacr from
-// the coarse A(2s) values at the 4 diagonal neighbours.
 template <class T>
 __global__ void __launch_bounds__(NT) k2_jac_d1_ref(D2<const T> vc, S2<const T> r, S2<T> v, int M, T c) {
-  int W = M / 2;
   int64_t t = (int64_t)blockIdx.x * NT + threadIdx.x;
-  if (t >= (int64_t)W * W) return;
-  int a = (int)(t % W), b = (int)(t / W);
-  int x = 2 * a + 1, y = 2 * b + 1;
-  v.o[(int64_t)b * v.pitch + a] = jac4(c, r.o[(int64_t)b * r.pitch + a], vc((x - 1) / 2, (y - 1) / 2),
-                                       vc((x + 1) / 2, (y - 1) / 2), vc((x + 1) / 2, (y + 1) / 2),
-                                       vc((x - 1) / 2, (y + 1) / 2));
+  if (t < (int64_t)(M / 2) * (M / 2)) node_jac_d1(vc, r, v, M, c, t);
 }
 
-// a6: colour 2 on E (= A(2s) positions): Eajacb from the new O
-// values; uses the D(s) residual at that node (reading A10).
 template <class T>
 __global__ void __launch_bounds__(NT) k2_jac_d2_ref(S2<const T> r, S2<T> v, int M, T c) {
-  int W = M / 2 - 1;
   int64_t t = (int64_t)blockIdx.x * NT + threadIdx.x;
-  if (t >= (int64_t)W * W) return;
-  int a = (int)(t % W) + 1, b = (int)(t / W) + 1;
-  int x = 2 * a, y = 2 * b;
-  v.e[(int64_t)b * v.pitch + a] = jac4(c, r.e[(int64_t)b * r.pitch + a], v.get(x - 1, y - 1), v.get(x + 1, y - 1),
-                                       v.get(x + 1, y + 1), v.get(x - 1, y + 1));
+  if (t < (int64_t)(M / 2 - 1) * (M / 2 - 1)) node_jac_d2(r, v, M, c, t);
 }
 
 // ---------------------------------------------------- ascent, axis level
-// a7 (s > 1): colour 1 on the green-only nodes (x+y odd) from D(s), colour 2
-// on the D(s) nodes from the new green values ("similarly for a green grid",
-// P:228-230; reading A5), c = p (sh)^2.
 template <class T>
 __global__ void __launch_bounds__(NT) k2_jac_a1_ref(S2<const T> vd, D2<const T> r, D2<T> v, int M, T c) {
-  int W = M - 1;
   int64_t t = (int64_t)blockIdx.x * NT + threadIdx.x;
-  if (t >= (int64_t)W * W) return;
-  int x = (int)(t % W) + 1, y = (int)(t / W) + 1;
-  if (((x + y) & 1) == 0) return;
-  v(x, y) = jac4(c, r(x, y), vd.get(x - 1, y), vd.get(x, y - 1), vd.get(x + 1, y), vd.get(x, y + 1));
+  if (t < (int64_t)(M - 1) * (M - 1)) node_jac_a1(vd, r, v, M, c, t);
 }
 
 template <class T>
 __global__ void __launch_bounds__(NT) k2_jac_a2_ref(D2<const T> r, D2<T> v, int M, T c) {
-  int W = M - 1;
   int64_t t = (int64_t)blockIdx.x * NT + threadIdx.x;
-  if (t >= (int64_t)W * W) return;
-  int x = (int)(t % W) + 1, y = (int)(t / W) + 1;
-  if (((x + y) & 1) == 1) return;
-  v(x, y) = jac4(c, r(x, y), v(x - 1, y), v(x, y - 1), v(x + 1, y), v(x, y + 1));
+  if (t < (int64_t)(M - 1) * (M - 1)) node_jac_a2(r, v, M, c, t);
+}
+
+// ------------------------------------------------------ coarse levels
+// One CTA runs every octave o >= oc: the level arrays are tiny (L2/L1
+// resident), so the cost is latency; __syncthreads orders the steps.
+template <class T>
+__global__ void __launch_bounds__(1024) k2_coarse(const Lev2<T> *lv, int oc, int k, int *counter) {
+  const int tid = threadIdx.x, bs = blockDim.x;
+  for (int o = oc; o + 1 < k; o++) {
+    const Lev2<T> L = lv[o];
+    const Lev2<T> Lc = lv[o + 1];
+    int64_t n = (int64_t)(L.M / 2 + 1) * (L.M / 2 + 1);
+    for (int64_t t = tid; t < n; t += bs) node_rest_ad(D2<const T>{L.rA.p, L.rA.pitch}, L.rD, L.M, t);
+    __syncthreads();
+    n = (int64_t)(Lc.M - 1) * (Lc.M - 1);
+    for (int64_t t = tid; t < n; t += bs) node_rest_da(S2<const T>{L.rD.e, L.rD.o, L.rD.pitch}, Lc.rA, Lc.M, t);
+    __syncthreads();
+  }
+  if (tid == 0) {
+    const Lev2<T> L = lv[k - 1];
+    node_coarsest(D2<const T>{L.rA.p, L.rA.pitch}, L.vA, L.cA, counter);
+  }
+  __syncthreads();
+  for (int o = k - 2; o >= oc; o--) {
+    const Lev2<T> L = lv[o];
+    const Lev2<T> Lc = lv[o + 1];
+    const int M = L.M;
+    S2<const T> rD{L.rD.e, L.rD.o, L.rD.pitch};
+    int64_t n = (int64_t)(M / 2) * (M / 2);
+    for (int64_t t = tid; t < n; t += bs) node_jac_d1(D2<const T>{Lc.vA.p, Lc.vA.pitch}, rD, L.vD, M, L.cD, t);
+    __syncthreads();
+    n = (int64_t)(M / 2 - 1) * (M / 2 - 1);
+    for (int64_t t = tid; t < n; t += bs) node_jac_d2(rD, L.vD, M, L.cD, t);
+    __syncthreads();
+    n = (int64_t)(M - 1) * (M - 1);
+    S2<const T> vD{L.vD.e, L.vD.o, L.vD.pitch};
+    D2<const T> rA{L.rA.p, L.rA.pitch};
+    for (int64_t t = tid; t < n; t += bs) node_jac_a1(vD, rA, L.vA, M, L.cA, t);
+    __syncthreads();
+    for (int64_t t = tid; t < n; t += bs) node_jac_a2(rA, L.vA, M, L.cA, t);
+    __syncthreads();
+  }
 }
 
 // ---------------------------------------------------- ascent, finest level
@@ -240,14 +165,14 @@ __global__ void __launch_bounds__(NT) k2_asc_fine2_ref(D2<const T> u, D2<const T
   v(x, y) = jac4(c, r, v(x - 1, y), v(x, y - 1), v(x + 1, y), v(x, y + 1));
 }
 
-// u <- u + v at the interior.
+// u_new <- u_old + v at the interior (u_new may alias u_old).
 template <class T>
-__global__ void __launch_bounds__(NT) k2_update_ref(D2<T> u, D2<const T> v, int M) {
+__global__ void __launch_bounds__(NT) k2_update_ref(D2<const T> uo, D2<const T> v, D2<T> un, int M) {
   int W = M - 1;
   int64_t t = (int64_t)blockIdx.x * NT + threadIdx.x;
   if (t >= (int64_t)W * W) return;
   int x = (int)(t % W) + 1, y = (int)(t / W) + 1;
-  u(x, y) = u(x, y) + v(x, y);
+  un(x, y) = uo(x, y) + v(x, y);
 }
 
 // --------------------------------------------------- standalone residual
@@ -362,8 +287,8 @@ void launch2_jac_a(const S2<T> &vd, const D2<T> &r, const D2<T> &v, int M, T c, 
 }
 
 template <class T>
-void launch2_asc_fine(const S2<T> &vd, const D2<T> &u, const D2<const T> &f, const D2<T> &scratch, int M, int order,
-                      T c, const Coef<T> &k, cudaStream_t st) {
+void launch2_asc_fine(const S2<T> &vd, const D2<T> &u, const D2<const T> &f, const D2<T> &scratch, const D2<T> &un,
+                      int M, int order, T c, const Coef<T> &k, cudaStream_t st) {
   int64_t W = M - 1;
   if (order == 2) {
     k2_asc_fine1_ref<T, 2><<<blocks_for(W * W), NT, 0, st>>>(cs(vd), cd(u), f, scratch, M, c, k);
@@ -372,7 +297,12 @@ void launch2_asc_fine(const S2<T> &vd, const D2<T> &u, const D2<const T> &f, con
     k2_asc_fine1_ref<T, 4><<<blocks_for(W * W), NT, 0, st>>>(cs(vd), cd(u), f, scratch, M, c, k);
     k2_asc_fine2_ref<T, 4><<<blocks_for(W * W), NT, 0, st>>>(cd(u), f, scratch, M, c, k);
   }
-  k2_update_ref<T><<<blocks_for(W * W), NT, 0, st>>>(u, cd(scratch), M);
+  k2_update_ref<T><<<blocks_for(W * W), NT, 0, st>>>(cd(u), cd(scratch), un, M);
+}
+
+template <class T>
+void launch2_coarse(const Lev2<T> *d_lev, int oc, int k, int *counter, cudaStream_t st) {
+  k2_coarse<T><<<1, 1024, 0, st>>>(d_lev, oc, k, counter);
 }
 
 template <class T>
@@ -404,8 +334,10 @@ void launch2_norm(const D2<const T> &a, int M, unsigned long long *mx, double *s
   template void launch2_coarsest<T>(const D2<T> &, const D2<T> &, T, int *, cudaStream_t);                         \
   template void launch2_jac_d<T>(const D2<T> &, const S2<T> &, const S2<T> &, int, T, cudaStream_t);               \
   template void launch2_jac_a<T>(const S2<T> &, const D2<T> &, const D2<T> &, int, T, cudaStream_t);               \
-  template void launch2_asc_fine<T>(const S2<T> &, const D2<T> &, const D2<const T> &, const D2<T> &, int, int, T, \
+  template void launch2_asc_fine<T>(const S2<T> &, const D2<T> &, const D2<const T> &, const D2<T> &, const D2<T> &, \
+                                    int, int, T,                                                                   \
                                     const Coef<T> &, cudaStream_t);                                                \
+  template void launch2_coarse<T>(const Lev2<T> *, int, int, int *, cudaStream_t);                                \
   template void launch2_residual<T>(const D2<const T> &, const D2<const T> &, const D2<T> &, int, int,             \
                                     const Coef<T> &, cudaStream_t);                                                \
   template void launch2_ftilde<T>(const D2<const T> &, const D2<T> &, int, cudaStream_t);                          \

@@ -1,0 +1,734 @@
+// k2f.cu -- 2D TMA tile kernels (sm_100a) for the large levels.
+//
+// Every kernel is a persistent tile pipeline: each CTA walks the tiles
+// blockIdx.x, blockIdx.x + gridDim.x, ...; one elected thread keeps
+// STAGES-1 tiles of TMA loads (cp.async.bulk.tensor, out-of-bounds -> 0) in
+// flight into a ring of shared-memory stages, one mbarrier per stage, while
+// the whole CTA computes the current tile from shared memory.
+//
+// Thread layout inside a tile (TX = 64 fine columns, TY = 32 rows, 8 warps):
+// lane l owns the column pair (x0 + 2l, x0 + 2l + 1), so every shared-memory
+// access of the core is a conflict-free 16-byte (fp64) / 8-byte (fp32) vector
+// access; warps take rows.  The one-node ring around the tile is computed by
+// warps 0-3 in one extra pass.  Node formulas are the shared ones of
+// ops2.cuh, so results are bit-identical to the reference kernels.
+#include "kernels.h"
+#include "ops2.cuh"
+#include "tma.cuh"
+
+namespace mg {
+
+constexpr int al128(int n) { return (n + 127) / 128 * 128; }
+// TMA (measured on B200): the inner box extent AND the box's starting x
+// coordinate must be multiples of 16 bytes (an unaligned start raises
+// "illegal instruction").  w16 rounds an extent up; hx<T>(h) is the x halo
+// actually loaded for a requested halo h (rounded up to 16 bytes).
+template <class T>
+constexpr int w16(int n) {
+  return (n * (int)sizeof(T) + 15) / 16 * 16 / (int)sizeof(T);
+}
+template <class T>
+constexpr int hx(int h) {
+  return (h * (int)sizeof(T) + 15) / 16 * 16 / (int)sizeof(T);
+}
+
+template <class T>
+struct Vec2;
+template <>
+struct Vec2<double> {
+  using t = double2;
+};
+template <>
+struct Vec2<float> {
+  using t = float2;
+};
+template <class T>
+__device__ __forceinline__ void ld2(const T *p, T &a, T &b) {
+  auto v = *reinterpret_cast<const typename Vec2<T>::t *>(p);
+  a = v.x;
+  b = v.y;
+}
+template <class T>
+__device__ __forceinline__ void st2(T *p, T a, T b) {
+  typename Vec2<T>::t v;
+  v.x = a;
+  v.y = b;
+  *reinterpret_cast<typename Vec2<T>::t *>(p) = v;
+}
+
+// A writable shared-memory tile addressed by global lattice coordinates.
+template <class T>
+struct STile {
+  T *p;
+  int ld, ox, oy;
+  __device__ __forceinline__ T *at(int x, int y) const { return p + (y - oy) * ld + (x - ox); }
+  __device__ __forceinline__ T operator()(int x, int y) const { return *at(x, y); }
+};
+template <class T>
+__device__ __forceinline__ STile<T> stile(unsigned char *base, int ld, int ox, int oy) {
+  return STile<T>{(T *)base, ld, ox, oy};
+}
+
+// v(x, y) of a split diagonal level held as two shared-memory tiles (E, O).
+template <class T>
+struct SplitTile2 {
+  STile<T> e, o;
+  __device__ __forceinline__ T operator()(int x, int y) const { return (x & 1) ? o(x >> 1, y >> 1) : e(x >> 1, y >> 1); }
+};
+
+template <class Op>
+__global__ void __launch_bounds__(Op::NT) tile_pipeline(const __grid_constant__ typename Op::Params P) {
+  constexpr int S = Op::STAGES;
+  extern __shared__ __align__(128) unsigned char smem[];
+  __shared__ __align__(8) uint64_t bar[S];
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < S; s++) mbar_init(&bar[s], 1);
+    fence_mbar_init();
+    Op::prefetch(P);
+  }
+  __syncthreads();
+  typename Op::Acc acc;
+  Op::init(acc);
+  const int ntiles = P.ntiles;
+  if (threadIdx.x == 0)
+    for (int j = 0; j + 1 < S; j++) {
+      int tj = blockIdx.x + j * gridDim.x;
+      if (tj < ntiles) Op::issue(P, tj, smem + j * Op::STAGE, &bar[j]);
+    }
+  int i = 0;
+  for (int t = blockIdx.x; t < ntiles; t += gridDim.x, i++) {
+    const int st = i % S;
+    if (threadIdx.x == 0) {
+      int tn = t + (S - 1) * gridDim.x;
+      if (tn < ntiles) {
+        int sn = (i + S - 1) % S;   // consumed at iteration i-1 (synchronised below)
+        fence_proxy_async();
+        Op::issue(P, tn, smem + sn * Op::STAGE, &bar[sn]);
+      }
+    }
+    mbar_wait(&bar[st], (i / S) & 1);
+    Op::compute(P, t, smem + st * Op::STAGE, smem + S * Op::STAGE, acc);
+    __syncthreads();
+  }
+  Op::finish(P, acc);
+}
+
+struct NoAcc {};
+
+constexpr int TX = 64, TY = 32, NT = 256, NW = NT / 32;
+
+__device__ __forceinline__ bool inside(int x, int y, int M) { return x >= 1 && y >= 1 && x <= M - 1 && y <= M - 1; }
+
+// ============================================= finest descent: a1 + a2 fused
+// r = f - L u on the tile and its ring (shared memory), then Erest2r onto
+// E/O of D(1); max|r| over the tile feeds the residual-norm history.
+template <class T, int ORDER, int STG>
+struct OpDesc2Fine {
+  static constexpr int NT = mg::NT, STAGES = STG;
+  static constexpr int HU = hx<T>(2), HF = hx<T>(1), HR = hx<T>(1);
+  static constexpr int UW = w16<T>(TX + HU + 2), UH = TY + 4, FW = w16<T>(TX + HF + 1), FH = TY + 2;
+  static constexpr int RW = w16<T>(TX + HR + 1), RH = TY + 2;
+  static constexpr int U_BYTES = UW * UH * sizeof(T), F_BYTES = FW * FH * sizeof(T);
+  static constexpr int U_OFF = 0, F_OFF = al128(U_BYTES);
+  static constexpr int STAGE = al128(F_OFF + F_BYTES);
+  static constexpr int SMEM = STAGES * STAGE + al128(RW * RH * sizeof(T));
+  struct Params {
+    CUtensorMap tu, tf;
+    S2<T> out;
+    int M, ntx, ntiles;
+    Coef<T> k;
+    NormSink ns;
+  };
+  struct Acc {
+    double mx;
+  };
+  static __device__ void prefetch(const Params &P) {
+    tma_prefetch_desc(&P.tu);
+    tma_prefetch_desc(&P.tf);
+  }
+  static __device__ void init(Acc &a) { a.mx = 0.0; }
+  static __device__ void issue(const Params &P, int t, unsigned char *st, uint64_t *bar) {
+    int x0 = (t % P.ntx) * TX, y0 = (t / P.ntx) * TY;
+    mbar_expect_tx(bar, U_BYTES + F_BYTES);
+    tma_load_2d(st + U_OFF, &P.tu, x0 - HU, y0 - 2, bar);
+    tma_load_2d(st + F_OFF, &P.tf, x0 - HF, y0 - 1, bar);
+  }
+  // residual at (xl, y) and (xl + 1, y), 0 outside the interior
+  static __device__ __forceinline__ void rpair(const STile<T> &U, const STile<T> &F, int xl, int y, int M,
+                                               const Coef<T> &k, T &r0, T &r1) {
+    Nb9<T> q0, q1;
+    ld2(U.at(xl, y), q0.c, q1.c);
+    ld2(U.at(xl, y - 1), q0.s, q1.s);
+    ld2(U.at(xl, y + 1), q0.n, q1.n);
+    q0.w = U(xl - 1, y);
+    q0.e = q1.c;
+    q1.w = q0.c;
+    q1.e = U(xl + 2, y);
+    if (ORDER == 4) {
+      q0.ne = q1.n;
+      q0.nw = U(xl - 1, y + 1);
+      q0.sw = U(xl - 1, y - 1);
+      q0.se = q1.s;
+      q1.ne = U(xl + 2, y + 1);
+      q1.nw = q0.n;
+      q1.sw = q0.s;
+      q1.se = U(xl + 2, y - 1);
+    }
+    T f0, f1;
+    ld2(F.at(xl, y), f0, f1);
+    r0 = inside(xl, y, M) ? res2v<T, ORDER>(q0, f0, k) : (T)0;
+    r1 = inside(xl + 1, y, M) ? res2v<T, ORDER>(q1, f1, k) : (T)0;
+  }
+  static __device__ void compute(const Params &P, int t, unsigned char *st, unsigned char *scr, Acc &acc) {
+    const int x0 = (t % P.ntx) * TX, y0 = (t / P.ntx) * TY, M = P.M;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, xl = x0 + 2 * lane;
+    STile<T> U = stile<T>(st + U_OFF, UW, x0 - HU, y0 - 2);
+    STile<T> F = stile<T>(st + F_OFF, FW, x0 - HF, y0 - 1);
+    STile<T> R = stile<T>(scr, RW, x0 - HR, y0 - 1);
+    T r0, r1;
+#pragma unroll
+    for (int y = y0 + w; y < y0 + TY; y += NW) {
+      rpair(U, F, xl, y, M, P.k, r0, r1);
+      st2(R.at(xl, y), r0, r1);
+      acc.mx = nmax(nmax(acc.mx, absd(r0)), absd(r1));
+    }
+    if (w < 2) {   // ring rows
+      int y = w == 0 ? y0 - 1 : y0 + TY;
+      rpair(U, F, xl, y, M, P.k, r0, r1);
+      st2(R.at(xl, y), r0, r1);
+    } else if (w < 4) {   // ring columns
+      int idx = (w - 2) * 32 + lane;
+      int x = idx < 32 ? x0 - 1 : x0 + TX, y = y0 + (idx & 31);
+      *R.at(x, y) = res2z<T, ORDER>(U, F, x, y, M, P.k);
+    }
+    __syncthreads();
+    const int64_t pitch = P.out.pitch;
+#pragma unroll
+    for (int b = w; b < TY / 2; b += NW) {
+      int y = y0 + 2 * b;
+      T rc, rE, rN, ro;
+      ld2(R.at(xl, y), rc, rE);
+      ld2(R.at(xl, y + 1), rN, ro);
+      int64_t o = (int64_t)(y / 2) * pitch + xl / 2;
+      if (xl >= 2 && xl <= M - 2 && y >= 2 && y <= M - 2)
+        P.out.e[o] = erest2r(rc, R(xl - 1, y), R(xl, y - 1), rE, rN);
+      if (xl + 1 <= M - 1 && y + 1 <= M - 1) P.out.o[o] = erest2r(ro, rN, rE, R(xl + 2, y + 1), R(xl + 1, y + 2));
+    }
+  }
+  static __device__ void finish(const Params &P, Acc &acc) { block_norm_push<NT>(P.ns, acc.mx); }
+};
+
+// ======================================== restriction A(s) -> D(s), s > 1
+template <class T, int STG>
+struct OpRest2AD {
+  static constexpr int NT = mg::NT, STAGES = STG;
+  static constexpr int HR = hx<T>(1);
+  static constexpr int RW = w16<T>(TX + HR + 1), RH = TY + 2;
+  static constexpr int R_BYTES = RW * RH * sizeof(T);
+  static constexpr int STAGE = al128(R_BYTES);
+  static constexpr int SMEM = STAGES * STAGE;
+  struct Params {
+    CUtensorMap tr;
+    S2<T> out;
+    int M, ntx, ntiles;
+  };
+  using Acc = NoAcc;
+  static __device__ void prefetch(const Params &P) { tma_prefetch_desc(&P.tr); }
+  static __device__ void init(Acc &) {}
+  static __device__ void issue(const Params &P, int t, unsigned char *st, uint64_t *bar) {
+    int x0 = (t % P.ntx) * TX, y0 = (t / P.ntx) * TY;
+    mbar_expect_tx(bar, R_BYTES);
+    tma_load_2d(st, &P.tr, x0 - HR, y0 - 1, bar);
+  }
+  static __device__ void compute(const Params &P, int t, unsigned char *st, unsigned char *, Acc &) {
+    const int x0 = (t % P.ntx) * TX, y0 = (t / P.ntx) * TY, M = P.M;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, xl = x0 + 2 * lane;
+    STile<T> R = stile<T>(st, RW, x0 - HR, y0 - 1);
+    const int64_t pitch = P.out.pitch;
+#pragma unroll
+    for (int b = w; b < TY / 2; b += NW) {
+      int y = y0 + 2 * b;
+      T rc, rE, rN, ro;
+      ld2(R.at(xl, y), rc, rE);
+      ld2(R.at(xl, y + 1), rN, ro);
+      int64_t o = (int64_t)(y / 2) * pitch + xl / 2;
+      if (xl >= 2 && xl <= M - 2 && y >= 2 && y <= M - 2)
+        P.out.e[o] = erest2r(rc, R(xl - 1, y), R(xl, y - 1), rE, rN);
+      if (xl + 1 <= M - 1 && y + 1 <= M - 1) P.out.o[o] = erest2r(ro, rN, rE, R(xl + 2, y + 1), R(xl + 1, y + 2));
+    }
+  }
+  static __device__ void finish(const Params &, Acc &) {}
+};
+
+// ===================================== restriction D(s) -> A(2s), Erest2b
+// coarse tile [X0, X0+TX) x [Y0, Y0+TY) of A(2s)
+template <class T, int STG>
+struct OpRest2DA {
+  static constexpr int NT = mg::NT, STAGES = STG;
+  static constexpr int HO = hx<T>(1);
+  static constexpr int EW = w16<T>(TX), EH = TY, OW = w16<T>(TX + HO), OH = TY + 1;
+  static constexpr int E_BYTES = EW * EH * sizeof(T), O_BYTES = OW * OH * sizeof(T);
+  static constexpr int E_OFF = 0, O_OFF = al128(E_BYTES);
+  static constexpr int STAGE = al128(O_OFF + O_BYTES);
+  static constexpr int SMEM = STAGES * STAGE;
+  struct Params {
+    CUtensorMap te, to;
+    D2<T> out;
+    int Mc, ntx, ntiles;
+  };
+  using Acc = NoAcc;
+  static __device__ void prefetch(const Params &P) {
+    tma_prefetch_desc(&P.te);
+    tma_prefetch_desc(&P.to);
+  }
+  static __device__ void init(Acc &) {}
+  static __device__ void issue(const Params &P, int t, unsigned char *st, uint64_t *bar) {
+    int X0 = (t % P.ntx) * TX, Y0 = (t / P.ntx) * TY;
+    mbar_expect_tx(bar, E_BYTES + O_BYTES);
+    tma_load_2d(st + E_OFF, &P.te, X0, Y0, bar);
+    tma_load_2d(st + O_OFF, &P.to, X0 - HO, Y0 - 1, bar);
+  }
+  static __device__ void compute(const Params &P, int t, unsigned char *st, unsigned char *, Acc &) {
+    const int X0 = (t % P.ntx) * TX, Y0 = (t / P.ntx) * TY, Mc = P.Mc;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, X = X0 + 2 * lane;
+    STile<T> E = stile<T>(st + E_OFF, EW, X0, Y0);
+    STile<T> O = stile<T>(st + O_OFF, OW, X0 - HO, Y0 - 1);
+#pragma unroll
+    for (int Y = Y0 + w; Y < Y0 + TY; Y += NW) {
+      if (Y < 1 || Y > Mc - 1) continue;
+      T e0, e1, s0, s1, n0, n1;
+      ld2(E.at(X, Y), e0, e1);
+      ld2(O.at(X, Y - 1), s0, s1);
+      ld2(O.at(X, Y), n0, n1);
+      // Erest2b: 4r + (i-1,j-1) + (i+1,j-1) + (i+1,j+1) + (i-1,j+1); neighbour of
+      // coarse node X at O(X-1, .) and O(X, .)
+      T v0 = erest2b(e0, O(X - 1, Y - 1), s0, n0, O(X - 1, Y));
+      T v1 = erest2b(e1, s0, s1, n1, n0);
+      bool ok0 = X >= 1 && X <= Mc - 1, ok1 = X + 1 <= Mc - 1;
+      if (ok0 && ok1)
+        st2(&P.out(X, Y), v0, v1);
+      else {
+        if (ok0) P.out(X, Y) = v0;
+        if (ok1) P.out(X + 1, Y) = v1;
+      }
+    }
+  }
+  static __device__ void finish(const Params &, Acc &) {}
+};
+
+// ================================ ascent D(s) from A(2s): Eajacr then Eajacb
+// tile in E/O index space [a0, a0+TX) x [b0, b0+TY); the O values are also
+// computed on the one-node ring below/left that the E update needs.
+template <class T, int STG>
+struct OpJac2D {
+  static constexpr int NT = mg::NT, STAGES = STG;
+  static constexpr int HA = hx<T>(1);
+  static constexpr int AW = w16<T>(TX + HA + 1), AH = TY + 2, ROW = w16<T>(TX + HA), ROH = TY + 1,
+                       REW = w16<T>(TX), REH = TY;
+  static constexpr int A_BYTES = AW * AH * sizeof(T), RO_BYTES = ROW * ROH * sizeof(T),
+                       RE_BYTES = REW * REH * sizeof(T);
+  static constexpr int A_OFF = 0, RO_OFF = al128(A_BYTES), RE_OFF = RO_OFF + al128(RO_BYTES);
+  static constexpr int STAGE = al128(RE_OFF + RE_BYTES);
+  static constexpr int VW = w16<T>(TX + HA), VH = TY + 1;
+  static constexpr int SMEM = STAGES * STAGE + al128(VW * VH * sizeof(T));
+  struct Params {
+    CUtensorMap tva, tro, tre;
+    S2<T> v;
+    int M, ntx, ntiles;
+    T c;
+  };
+  using Acc = NoAcc;
+  static __device__ void prefetch(const Params &P) {
+    tma_prefetch_desc(&P.tva);
+    tma_prefetch_desc(&P.tro);
+    tma_prefetch_desc(&P.tre);
+  }
+  static __device__ void init(Acc &) {}
+  static __device__ void issue(const Params &P, int t, unsigned char *st, uint64_t *bar) {
+    int a0 = (t % P.ntx) * TX, b0 = (t / P.ntx) * TY;
+    mbar_expect_tx(bar, A_BYTES + RO_BYTES + RE_BYTES);
+    tma_load_2d(st + A_OFF, &P.tva, a0 - HA, b0 - 1, bar);
+    tma_load_2d(st + RO_OFF, &P.tro, a0 - HA, b0 - 1, bar);
+    tma_load_2d(st + RE_OFF, &P.tre, a0, b0, bar);
+  }
+  static __device__ void compute(const Params &P, int t, unsigned char *st, unsigned char *scr, Acc &) {
+    const int a0 = (t % P.ntx) * TX, b0 = (t / P.ntx) * TY, W = P.M / 2;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, a = a0 + 2 * lane;
+    const T c = P.c;
+    STile<T> VA = stile<T>(st + A_OFF, AW, a0 - HA, b0 - 1);
+    STile<T> RO = stile<T>(st + RO_OFF, ROW, a0 - HA, b0 - 1);
+    STile<T> RE = stile<T>(st + RE_OFF, REW, a0, b0);
+    STile<T> V = stile<T>(scr, VW, a0 - HA, b0 - 1);
+    const int64_t pitch = P.v.pitch;
+    // colour 1 (Eajacr) on O nodes: rows b0-1 .. b0+TY-1, the lane's column pair
+    for (int b = b0 - 1 + w; b < b0 + TY; b += NW) {
+      T ro0, ro1, va0, va1, vb0, vb1;
+      ld2(RO.at(a, b), ro0, ro1);
+      ld2(VA.at(a, b), va0, va1);
+      ld2(VA.at(a, b + 1), vb0, vb1);
+      T va2 = VA(a + 2, b), vb2 = VA(a + 2, b + 1);
+      bool okb = b >= 0 && b <= W - 1;
+      T v0 = (okb && a <= W - 1) ? jac4(c, ro0, va0, va1, vb1, vb0) : (T)0;
+      T v1 = (okb && a + 1 <= W - 1) ? jac4(c, ro1, va1, va2, vb2, vb1) : (T)0;
+      st2(V.at(a, b), v0, v1);
+      if (okb && b >= b0) {
+        if (a + 1 <= W - 1)
+          st2(&P.v.o[(int64_t)b * pitch + a], v0, v1);
+        else if (a <= W - 1)
+          P.v.o[(int64_t)b * pitch + a] = v0;
+      }
+    }
+    if (w == NW - 1) {   // ring column a0 - 1
+      for (int b = b0 - 1 + lane; b < b0 + TY; b += 32) {
+        int am = a0 - 1;
+        T v = (T)0;
+        if (am >= 0 && am <= W - 1 && b >= 0 && b <= W - 1)
+          v = jac4(c, RO(am, b), VA(am, b), VA(am + 1, b), VA(am + 1, b + 1), VA(am, b + 1));
+        *V.at(am, b) = v;
+      }
+    }
+    __syncthreads();
+    // colour 2 (Eajacb) on E nodes, from the new O values (D(s) residual, reading A10)
+#pragma unroll
+    for (int b = b0 + w; b < b0 + TY; b += NW) {
+      if (b < 1 || b > W - 1) continue;
+      T re0, re1, s0, s1, n0, n1;
+      ld2(RE.at(a, b), re0, re1);
+      ld2(V.at(a, b - 1), s0, s1);
+      ld2(V.at(a, b), n0, n1);
+      T sm = V(a - 1, b - 1), nm = V(a - 1, b);
+      // Eajacb: (i-1,j-1), (i+1,j-1), (i+1,j+1), (i-1,j+1) -> O(a-1,b-1), O(a,b-1), O(a,b), O(a-1,b)
+      T e0 = jac4(c, re0, sm, s0, n0, nm);
+      T e1 = jac4(c, re1, s0, s1, n1, n0);
+      bool ok0 = a >= 1 && a <= W - 1, ok1 = a + 1 <= W - 1;
+      int64_t o = (int64_t)b * pitch + a;
+      if (ok0 && ok1)
+        st2(&P.v.e[o], e0, e1);
+      else {
+        if (ok0) P.v.e[o] = e0;
+        if (ok1) P.v.e[o + 1] = e1;
+      }
+    }
+  }
+  static __device__ void finish(const Params &, Acc &) {}
+};
+
+// ===================== ascent A(s) from D(s): green-only nodes, then D nodes
+// FINE = true: s = 1, r recomputed from (u_old, f) and u_new = u_old + v is
+// written (out of place); FINE = false: r read from r_A(s), v_A(s) written.
+template <class T, int ORDER, bool FINE, int STG>
+struct OpJac2A {
+  static constexpr int NT = mg::NT, STAGES = STG;
+  static constexpr int HU = hx<T>(2), HF = hx<T>(1), HV = hx<T>(1), HG = hx<T>(1);
+  static constexpr int UW = w16<T>(TX + HU + 2), UH = TY + 4;           // u (FINE)
+  static constexpr int FW = w16<T>(TX + HF + 1), FH = TY + 2;           // f (FINE) or r_A (level)
+  static constexpr int VW = w16<T>(TX / 2 + HV + 1), VH = TY / 2 + 2;   // E and O of v_D
+  static constexpr int U_BYTES = FINE ? UW * UH * (int)sizeof(T) : 0;
+  static constexpr int F_BYTES = FW * FH * sizeof(T), V_BYTES = VW * VH * sizeof(T);
+  static constexpr int U_OFF = 0, F_OFF = al128(U_BYTES), VE_OFF = F_OFF + al128(F_BYTES),
+                       VO_OFF = VE_OFF + al128(V_BYTES);
+  static constexpr int STAGE = al128(VO_OFF + V_BYTES);
+  // green values, one per column pair: pair p = (x0-2+2p, x0-1+2p), p = 0..TX/2+1;
+  // which node of the pair is green follows from the row parity
+  static constexpr int GW = TX / 2 + 2, GH = TY + 2;
+  static constexpr int SMEM = STAGES * STAGE + al128(GW * GH * sizeof(T));
+  struct Params {
+    CUtensorMap tu, tf, tve, tvo;   // tu unused when !FINE; tf = f (FINE) or r_A
+    D2<T> out;                      // u_new (FINE) or v_A
+    int M, ntx, ntiles;
+    T c;
+    Coef<T> k;
+  };
+  using Acc = NoAcc;
+  static __device__ void prefetch(const Params &P) {
+    if (FINE) tma_prefetch_desc(&P.tu);
+    tma_prefetch_desc(&P.tf);
+    tma_prefetch_desc(&P.tve);
+    tma_prefetch_desc(&P.tvo);
+  }
+  static __device__ void init(Acc &) {}
+  static __device__ void issue(const Params &P, int t, unsigned char *st, uint64_t *bar) {
+    int x0 = (t % P.ntx) * TX, y0 = (t / P.ntx) * TY;
+    mbar_expect_tx(bar, U_BYTES + F_BYTES + 2 * V_BYTES);
+    if (FINE) tma_load_2d(st + U_OFF, &P.tu, x0 - HU, y0 - 2, bar);
+    tma_load_2d(st + F_OFF, &P.tf, x0 - HF, y0 - 1, bar);
+    tma_load_2d(st + VE_OFF, &P.tve, x0 / 2 - HV, y0 / 2 - 1, bar);
+    tma_load_2d(st + VO_OFF, &P.tvo, x0 / 2 - HV, y0 / 2 - 1, bar);
+  }
+  static __device__ __forceinline__ T rnode(const Params &P, const STile<T> &U, const STile<T> &F, int x, int y) {
+    if (FINE) return res2<T, ORDER>(U, F, x, y, P.k);
+    return F(x, y);
+  }
+  static __device__ void compute(const Params &P, int t, unsigned char *st, unsigned char *scr, Acc &) {
+    const int x0 = (t % P.ntx) * TX, y0 = (t / P.ntx) * TY, M = P.M;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, xl = x0 + 2 * lane, hl = xl >> 1;
+    const T c = P.c;
+    STile<T> U = stile<T>(st + U_OFF, UW, x0 - HU, y0 - 2);
+    STile<T> F = stile<T>(st + F_OFF, FW, x0 - HF, y0 - 1);
+    STile<T> VE = stile<T>(st + VE_OFF, VW, x0 / 2 - HV, y0 / 2 - 1);
+    STile<T> VO = stile<T>(st + VO_OFF, VW, x0 / 2 - HV, y0 / 2 - 1);
+    STile<T> G = stile<T>(scr, GW, 0, y0 - 1);   // G(p, y): the green value of pair p in row y
+    const int p = lane + 1;                       // the lane's pair
+    // colour 1: the green node of the lane's pair in row y ("similarly for a
+    // green grid"): y even -> xl+1, y odd -> xl
+    auto green = [&](int y) {
+      T g = (T)0;
+      if ((y & 1) == 0) {
+        int xg = xl + 1;
+        if (inside(xg, y, M)) {
+          int Y = y >> 1;
+          g = jac4(c, rnode(P, U, F, xg, y), VE(hl, Y), VO(hl, Y - 1), VE(hl + 1, Y), VO(hl, Y));
+        }
+      } else {
+        if (inside(xl, y, M)) {
+          int Y = (y - 1) >> 1;
+          g = jac4(c, rnode(P, U, F, xl, y), VO(hl - 1, Y), VE(hl, Y), VO(hl, Y), VE(hl, Y + 1));
+        }
+      }
+      *G.at(p, y) = g;
+    };
+#pragma unroll
+    for (int y = y0 + w; y < y0 + TY; y += NW) green(y);
+    if (w < 2) {
+      green(w == 0 ? y0 - 1 : y0 + TY);
+    } else if (w < 4) {   // ring columns x0-1 (pair 0) and x0+TX (pair TX/2+1)
+      int idx = (w - 2) * 32 + lane;
+      int x = idx < 32 ? x0 - 1 : x0 + TX, y = y0 + (idx & 31);
+      T g = (T)0;
+      if (((x + y) & 1) && inside(x, y, M)) {
+        SplitTile2<T> VD{VE, VO};
+        g = jac4(c, rnode(P, U, F, x, y), VD(x - 1, y), VD(x, y - 1), VD(x + 1, y), VD(x, y + 1));
+      }
+      *G.at(idx < 32 ? 0 : TX / 2 + 1, y) = g;
+    }
+    __syncthreads();
+    // colour 2: the D(s) node of the pair from the new green values
+#pragma unroll
+    for (int y = y0 + w; y < y0 + TY; y += NW) {
+      if (y < 1 || y > M - 1) continue;
+      T g = G(p, y), v0, v1;
+      if ((y & 1) == 0) {   // D node at xl, green at xl+1
+        v1 = g;
+        v0 = inside(xl, y, M) ? jac4(c, rnode(P, U, F, xl, y), G(p - 1, y), G(p, y - 1), g, G(p, y + 1)) : (T)0;
+      } else {              // D node at xl+1, green at xl
+        v0 = g;
+        v1 = inside(xl + 1, y, M) ? jac4(c, rnode(P, U, F, xl + 1, y), g, G(p, y - 1), G(p + 1, y), G(p, y + 1)) : (T)0;
+      }
+      if (FINE) {   // u <- u + v
+        T u0, u1;
+        ld2(U.at(xl, y), u0, u1);
+        v0 = u0 + v0;
+        v1 = u1 + v1;
+      }
+      bool ok0 = xl >= 1, ok1 = xl + 1 <= M - 1;
+      if (ok0 && ok1)
+        st2(&P.out(xl, y), v0, v1);
+      else {
+        if (ok0 && xl <= M - 1) P.out(xl, y) = v0;
+        if (ok1) P.out(xl + 1, y) = v1;
+      }
+    }
+  }
+  static __device__ void finish(const Params &, Acc &) {}
+};
+
+// ================================================================= launch
+
+static int num_sms() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
+
+// pipeline depth (TMA stages per CTA); MG_STAGES overrides (2, 3 or 4)
+static int stages_cfg() {
+  static int s = 0;
+  if (!s) {
+    s = 2;
+    if (const char *e = getenv("MG_STAGES")) s = atoi(e);
+    if (s < 2 || s > 4) s = 2;
+  }
+  return s;
+}
+
+template <class Op>
+static cudaError_t run_op(const typename Op::Params &P, cudaStream_t st) {
+  cudaError_t e = cudaFuncSetAttribute(tile_pipeline<Op>, cudaFuncAttributeMaxDynamicSharedMemorySize, Op::SMEM);
+  if (e != cudaSuccess) return e;
+  int per_sm = (227 * 1024) / (Op::SMEM + 1024);
+  if (per_sm < 1) per_sm = 1;
+  if (per_sm > 4) per_sm = 4;
+  int grid = num_sms() * per_sm;
+  if (grid > P.ntiles) grid = P.ntiles;
+  if (grid < 1) return cudaSuccess;
+  tile_pipeline<Op><<<grid, Op::NT, Op::SMEM, st>>>(P);
+  return cudaGetLastError();
+}
+
+// run the op with the configured number of stages
+template <template <int> class OpOfStages, class Params>
+static cudaError_t run_staged(const Params &P, cudaStream_t st) {
+  switch (stages_cfg()) {
+    case 3: return run_op<OpOfStages<3>>(reinterpret_cast<const typename OpOfStages<3>::Params &>(P), st);
+    case 4: return run_op<OpOfStages<4>>(reinterpret_cast<const typename OpOfStages<4>::Params &>(P), st);
+    default: return run_op<OpOfStages<2>>(reinterpret_cast<const typename OpOfStages<2>::Params &>(P), st);
+  }
+}
+
+template <class T>
+static bool tm2(CUtensorMap *tm, const void *p, int64_t nx, int64_t ny, int64_t pitch, int bx, int by) {
+  uint64_t dims[2] = {(uint64_t)nx, (uint64_t)ny};
+  uint32_t box[2] = {(uint32_t)bx, (uint32_t)by};
+  return encode_tmap(tm, p, sizeof(T), 2, dims, (uint64_t)pitch, 0, box);
+}
+
+template <class T, int ORDER>
+struct DescS {
+  template <int S>
+  using op = OpDesc2Fine<T, ORDER, S>;
+};
+
+template <class T, int ORDER>
+static cudaError_t desc_impl(const T *u, const T *f, int64_t pitch, const S2<T> &d, int M, const Coef<T> &k,
+                             const NormSink &ns, cudaStream_t st) {
+  using Op = OpDesc2Fine<T, ORDER, 2>;   // Params do not depend on the stage count
+  typename Op::Params P{};
+  if (!tm2<T>(&P.tu, u, M + 1, M + 1, pitch, Op::UW, Op::UH) || !tm2<T>(&P.tf, f, M + 1, M + 1, pitch, Op::FW, Op::FH))
+    return cudaErrorInvalidValue;
+  int ntx = (M + TX - 1) / TX, nty = (M + TY - 1) / TY;
+  P.out = d;
+  P.M = M;
+  P.ntx = ntx;
+  P.ntiles = ntx * nty;
+  P.k = k;
+  P.ns = ns;
+  return run_staged<DescS<T, ORDER>::template op>(P, st);
+}
+
+template <class T>
+cudaError_t fast2_desc_fine(const T *u, const T *f, int64_t pitch, const S2<T> &d, int M, int order, const Coef<T> &k,
+                            const NormSink &ns, cudaStream_t st) {
+  return order == 2 ? desc_impl<T, 2>(u, f, pitch, d, M, k, ns, st) : desc_impl<T, 4>(u, f, pitch, d, M, k, ns, st);
+}
+
+template <class T, int ORDER, bool FINE>
+struct JacAS {
+  template <int S>
+  using op = OpJac2A<T, ORDER, FINE, S>;
+};
+
+template <class T, int ORDER, bool FINE>
+static cudaError_t jac_a_impl(const T *u, const T *f_or_r, int64_t pitch_u, int64_t pitch_f, const S2<T> &vd,
+                              const D2<T> &out, int M, T c, const Coef<T> &k, cudaStream_t st) {
+  using Op = OpJac2A<T, ORDER, FINE, 2>;
+  typename Op::Params P{};
+  int H = M / 2 + 1;
+  if (FINE && !tm2<T>(&P.tu, u, M + 1, M + 1, pitch_u, Op::UW, Op::UH)) return cudaErrorInvalidValue;
+  if (!tm2<T>(&P.tf, f_or_r, M + 1, M + 1, pitch_f, Op::FW, Op::FH) ||
+      !tm2<T>(&P.tve, vd.e, H, H, vd.pitch, Op::VW, Op::VH) || !tm2<T>(&P.tvo, vd.o, H, H, vd.pitch, Op::VW, Op::VH))
+    return cudaErrorInvalidValue;
+  int ntx = (M + TX - 1) / TX, nty = (M + TY - 1) / TY;
+  P.out = out;
+  P.M = M;
+  P.ntx = ntx;
+  P.ntiles = ntx * nty;
+  P.c = c;
+  P.k = k;
+  return run_staged<JacAS<T, ORDER, FINE>::template op>(P, st);
+}
+
+template <class T>
+cudaError_t fast2_asc_fine(const S2<T> &vd, const T *u_old, const T *f, int64_t pitch, T *u_new, int M, int order, T c,
+                           const Coef<T> &k, cudaStream_t st) {
+  D2<T> out{u_new, pitch};
+  if (order == 2) return jac_a_impl<T, 2, true>(u_old, f, pitch, pitch, vd, out, M, c, k, st);
+  return jac_a_impl<T, 4, true>(u_old, f, pitch, pitch, vd, out, M, c, k, st);
+}
+
+template <class T>
+cudaError_t fast2_jac_a(const S2<T> &vd, const D2<T> &r, const D2<T> &v, int M, T c, cudaStream_t st) {
+  Coef<T> k{};
+  return jac_a_impl<T, 2, false>(nullptr, r.p, 0, r.pitch, vd, v, M, c, k, st);
+}
+
+template <class T>
+struct RestADS {
+  template <int S>
+  using op = OpRest2AD<T, S>;
+};
+template <class T>
+struct RestDAS {
+  template <int S>
+  using op = OpRest2DA<T, S>;
+};
+template <class T>
+struct JacDS {
+  template <int S>
+  using op = OpJac2D<T, S>;
+};
+
+template <class T>
+cudaError_t fast2_rest_ad(const D2<T> &r, const S2<T> &d, int M, cudaStream_t st) {
+  using Op = OpRest2AD<T, 2>;
+  typename Op::Params P{};
+  if (!tm2<T>(&P.tr, r.p, M + 1, M + 1, r.pitch, Op::RW, Op::RH)) return cudaErrorInvalidValue;
+  int ntx = (M + TX - 1) / TX, nty = (M + TY - 1) / TY;
+  P.out = d;
+  P.M = M;
+  P.ntx = ntx;
+  P.ntiles = ntx * nty;
+  return run_staged<RestADS<T>::template op>(P, st);
+}
+
+template <class T>
+cudaError_t fast2_rest_da(const S2<T> &d, const D2<T> &r, int Mc, cudaStream_t st) {
+  using Op = OpRest2DA<T, 2>;
+  typename Op::Params P{};
+  int H = Mc + 1;   // E/O arrays of D(s) have M/2 + 1 = Mc + 1 entries per side
+  if (!tm2<T>(&P.te, d.e, H, H, d.pitch, Op::EW, Op::EH) || !tm2<T>(&P.to, d.o, H, H, d.pitch, Op::OW, Op::OH))
+    return cudaErrorInvalidValue;
+  int ntx = (Mc + TX - 1) / TX, nty = (Mc + TY - 1) / TY;
+  P.out = r;
+  P.Mc = Mc;
+  P.ntx = ntx;
+  P.ntiles = ntx * nty;
+  return run_staged<RestDAS<T>::template op>(P, st);
+}
+
+template <class T>
+cudaError_t fast2_jac_d(const D2<T> &vc, const S2<T> &r, const S2<T> &v, int M, T c, cudaStream_t st) {
+  using Op = OpJac2D<T, 2>;
+  typename Op::Params P{};
+  int H = M / 2 + 1;
+  if (!tm2<T>(&P.tva, vc.p, H, H, vc.pitch, Op::AW, Op::AH) || !tm2<T>(&P.tro, r.o, H, H, r.pitch, Op::ROW, Op::ROH) ||
+      !tm2<T>(&P.tre, r.e, H, H, r.pitch, Op::REW, Op::REH))
+    return cudaErrorInvalidValue;
+  int W = M / 2;
+  int ntx = (W + TX - 1) / TX, nty = (W + TY - 1) / TY;
+  P.v = v;
+  P.M = M;
+  P.ntx = ntx;
+  P.ntiles = ntx * nty;
+  P.c = c;
+  return run_staged<JacDS<T>::template op>(P, st);
+}
+
+#define INSTF(T)                                                                                                   \
+  template cudaError_t fast2_desc_fine<T>(const T *, const T *, int64_t, const S2<T> &, int, int, const Coef<T> &, \
+                                          const NormSink &, cudaStream_t);                                         \
+  template cudaError_t fast2_asc_fine<T>(const S2<T> &, const T *, const T *, int64_t, T *, int, int, T,           \
+                                         const Coef<T> &, cudaStream_t);                                           \
+  template cudaError_t fast2_jac_a<T>(const S2<T> &, const D2<T> &, const D2<T> &, int, T, cudaStream_t);          \
+  template cudaError_t fast2_rest_ad<T>(const D2<T> &, const S2<T> &, int, cudaStream_t);                          \
+  template cudaError_t fast2_rest_da<T>(const S2<T> &, const D2<T> &, int, cudaStream_t);                          \
+  template cudaError_t fast2_jac_d<T>(const D2<T> &, const S2<T> &, const S2<T> &, int, T, cudaStream_t);
+
+INSTF(float)
+INSTF(double)
+
+}  // namespace mg

@@ -298,12 +298,12 @@ __global__ void __launch_bounds__(NT3) k3_asc_fine2_ref(D3<const T> u, D3<const 
 }
 
 template <class T>
-__global__ void __launch_bounds__(NT3) k3_update_ref(D3<T> u, D3<const T> v, int M) {
+__global__ void __launch_bounds__(NT3) k3_update_ref(D3<const T> uo, D3<const T> v, D3<T> un, int M) {
   int64_t W = M - 1;
   int64_t t = (int64_t)blockIdx.x * NT3 + threadIdx.x;
   if (t >= W * W * W) return;
   int x = (int)(t % W) + 1, y = (int)((t / W) % W) + 1, z = (int)(t / (W * W)) + 1;
-  u(x, y, z) = u(x, y, z) + v(x, y, z);
+  un(x, y, z) = uo(x, y, z) + v(x, y, z);
 }
 
 template <class T, int ORDER>
@@ -436,8 +436,8 @@ void launch3_jac_g(const S3<T> &vr, const D3<T> &r, const D3<T> &v, int M, T c, 
 }
 
 template <class T>
-void launch3_asc_fine(const S3<T> &vr, const D3<T> &u, const D3<const T> &f, const D3<T> &scratch, int M, int order,
-                      T c, const Coef<T> &k, cudaStream_t st) {
+void launch3_asc_fine(const S3<T> &vr, const D3<T> &u, const D3<const T> &f, const D3<T> &scratch, const D3<T> &un,
+                      int M, int order, T c, const Coef<T> &k, cudaStream_t st) {
   int64_t W = M - 1;
   unsigned g = blocks3(W * W * W);
   if (order == 2) {
@@ -447,7 +447,7 @@ void launch3_asc_fine(const S3<T> &vr, const D3<T> &u, const D3<const T> &f, con
     k3_asc_fine1_ref<T, 4><<<g, NT3, 0, st>>>(cs3(vr), cd3(u), f, scratch, M, c, k);
     k3_asc_fine2_ref<T, 4><<<g, NT3, 0, st>>>(cd3(u), f, scratch, M, c, k);
   }
-  k3_update_ref<T><<<g, NT3, 0, st>>>(u, cd3(scratch), M);
+  k3_update_ref<T><<<g, NT3, 0, st>>>(cd3(u), cd3(scratch), un, M);
 }
 
 template <class T>
@@ -481,7 +481,8 @@ void launch3_norm(const D3<const T> &a, int M, unsigned long long *mx, double *s
   template void launch3_jac_m<T>(const D3<T> &, const S3<T> &, const S3<T> &, int, T, cudaStream_t);               \
   template void launch3_jac_r<T>(const S3<T> &, const S3<T> &, const S3<T> &, int, T, T, cudaStream_t);            \
   template void launch3_jac_g<T>(const S3<T> &, const D3<T> &, const D3<T> &, int, T, cudaStream_t);               \
-  template void launch3_asc_fine<T>(const S3<T> &, const D3<T> &, const D3<const T> &, const D3<T> &, int, int, T, \
+  template void launch3_asc_fine<T>(const S3<T> &, const D3<T> &, const D3<const T> &, const D3<T> &, const D3<T> &, \
+                                    int, int, T,                                                                   \
                                     const Coef<T> &, cudaStream_t);                                                \
   template void launch3_residual<T>(const D3<const T> &, const D3<const T> &, const D3<T> &, int, int,             \
                                     const Coef<T> &, cudaStream_t);                                                \

@@ -20,8 +20,37 @@ void launch2_jac_d(const D2<T> &vc, const S2<T> &r, const S2<T> &v, int M, T c, 
 template <class T>
 void launch2_jac_a(const S2<T> &vd, const D2<T> &r, const D2<T> &v, int M, T c, cudaStream_t st);
 template <class T>
-void launch2_asc_fine(const S2<T> &vd, const D2<T> &u, const D2<const T> &f, const D2<T> &scratch, int M, int order,
-                      T c, const Coef<T> &k, cudaStream_t st);
+void launch2_asc_fine(const S2<T> &vd, const D2<T> &u, const D2<const T> &f, const D2<T> &scratch, const D2<T> &un,
+                      int M, int order, T c, const Coef<T> &k, cudaStream_t st);
+
+// Per-octave level descriptors for the single-CTA coarse kernel.
+template <class T>
+struct Lev2 {
+  S2<T> rD, vD;   // D(s)
+  D2<T> rA, vA;   // A(s)
+  int M;
+  T cD, cA;
+};
+// All octaves o >= oc (oc >= 1) in one CTA: restrictions from r_A(oc) down,
+// the coarsest step, the Jacobi steps back up to v_A(oc).
+template <class T>
+void launch2_coarse(const Lev2<T> *d_lev, int oc, int k, int *counter, cudaStream_t st);
+
+// TMA tile kernels (k2f.cu); every pointer/pitch must be 16-byte aligned.
+template <class T>
+cudaError_t fast2_desc_fine(const T *u, const T *f, int64_t pitch, const S2<T> &d, int M, int order, const Coef<T> &k,
+                            const NormSink &ns, cudaStream_t st);
+template <class T>
+cudaError_t fast2_asc_fine(const S2<T> &vd, const T *u_old, const T *f, int64_t pitch, T *u_new, int M, int order, T c,
+                           const Coef<T> &k, cudaStream_t st);
+template <class T>
+cudaError_t fast2_jac_a(const S2<T> &vd, const D2<T> &r, const D2<T> &v, int M, T c, cudaStream_t st);
+template <class T>
+cudaError_t fast2_rest_ad(const D2<T> &r, const S2<T> &d, int M, cudaStream_t st);
+template <class T>
+cudaError_t fast2_rest_da(const S2<T> &d, const D2<T> &r, int Mc, cudaStream_t st);
+template <class T>
+cudaError_t fast2_jac_d(const D2<T> &vc, const S2<T> &r, const S2<T> &v, int M, T c, cudaStream_t st);
 template <class T>
 void launch2_residual(const D2<const T> &u, const D2<const T> &f, const D2<T> &r, int M, int order, const Coef<T> &k,
                       cudaStream_t st);
@@ -49,8 +78,8 @@ void launch3_jac_r(const S3<T> &vm, const S3<T> &r, const S3<T> &v, int M, T c1,
 template <class T>
 void launch3_jac_g(const S3<T> &vr, const D3<T> &r, const D3<T> &v, int M, T c, cudaStream_t st);
 template <class T>
-void launch3_asc_fine(const S3<T> &vr, const D3<T> &u, const D3<const T> &f, const D3<T> &scratch, int M, int order,
-                      T c, const Coef<T> &k, cudaStream_t st);
+void launch3_asc_fine(const S3<T> &vr, const D3<T> &u, const D3<const T> &f, const D3<T> &scratch, const D3<T> &un,
+                      int M, int order, T c, const Coef<T> &k, cudaStream_t st);
 template <class T>
 void launch3_residual(const D3<const T> &u, const D3<const T> &f, const D3<T> &r, int M, int order, const Coef<T> &k,
                       cudaStream_t st);

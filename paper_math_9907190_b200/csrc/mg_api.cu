@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <cmath>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <memory>
@@ -57,7 +58,14 @@ struct Prof {
   bool first = true;
   std::vector<StepInfo> steps;
   std::vector<cudaEvent_t> evs;   // (nsteps + 1) per cycle
+  bool debug = getenv("MG_DEBUG_SYNC") != nullptr;
+  std::string last;
   void step(const char *name, int level, int launches, double bytes) {
+    if (debug) {
+      cudaError_t e = cudaStreamSynchronize(st);
+      if (e != cudaSuccess) fprintf(stderr, "[mg debug] error after step '%s': %s\n", last.c_str(), cudaGetErrorString(e));
+      last = name;
+    }
     if (first) steps.push_back(StepInfo{name, level, launches, bytes});
     cudaEvent_t e;
     cudaEventCreate(&e);
@@ -65,6 +73,10 @@ struct Prof {
     evs.push_back(e);
   }
   void end_cycle() {
+    if (debug) {
+      cudaError_t er = cudaStreamSynchronize(st);
+      if (er != cudaSuccess) fprintf(stderr, "[mg debug] error after step '%s': %s\n", last.c_str(), cudaGetErrorString(er));
+    }
     cudaEvent_t e;
     cudaEventCreate(&e);
     cudaEventRecord(e, st);
@@ -84,7 +96,12 @@ struct Prof {
 struct ImplBase {
   virtual ~ImplBase() {}
   virtual cudaError_t alloc() = 0;
-  virtual void enqueue_cycle(void *u, const void *f_eff, cudaStream_t st, Prof *prof = nullptr) = 0;
+  // One V-cycle reading u_in and writing u_out = u_in + v (u_out may equal
+  // u_in only when !fast()).
+  virtual void enqueue_cycle(const void *u_in, void *u_out, const void *f_eff, cudaStream_t st,
+                             Prof *prof = nullptr) = 0;
+  // true: the TMA tile kernels run (they update u out of place)
+  virtual bool fast() const { return false; }
   virtual void enqueue_final_norm(void *u, const void *f_eff, cudaStream_t st) = 0;
   virtual void enqueue_residual(const void *u, const void *f, void *r, cudaStream_t st) = 0;
   virtual void enqueue_ftilde(const void *f, void *ft, cudaStream_t st) = 0;
@@ -120,8 +137,12 @@ struct mg_solver {
   double *d_ss = nullptr;
   void *d_ft = nullptr;                    // order-4 f~ (n^d x pitch)
   void *d_u_stage = nullptr, *d_f_stage = nullptr;   // mg_vcycle_host staging
-  cudaGraphExec_t gexec = nullptr;
-  const void *g_u = nullptr, *g_f = nullptr;
+  struct GraphEntry {
+    cudaGraphExec_t exec;
+    const void *uin, *uout, *f;
+  };
+  std::vector<GraphEntry> graphs;   // captured cycles keyed by pointers
+  void *d_ualt = nullptr;            // out-of-place partner of the caller's u
   unsigned long long *h_hist = nullptr;    // pinned
   std::string err;
   size_t field_elems() const { return (size_t)((cfg.dim == 2) ? cfg.n * pitch : cfg.n * cfg.n * pitch); }
@@ -153,7 +174,11 @@ struct Impl2 : ImplBase {
   D2<T> scratch{};
   Coef<T> coef{};
   std::vector<T> cD, cA;   // Jacobi coefficients per octave
+  bool use_fast = false;   // TMA tile kernels for the large levels
+  int oc = 1;              // first octave handled by the single-CTA coarse kernel
+  Lev2<T> *d_lev = nullptr;
   explicit Impl2(const mg_solver *sv) : s(sv), k(sv->k), n(sv->cfg.n), pitch(sv->pitch) {}
+  bool fast() const override { return use_fast; }
 
   int64_t pitch_for(int64_t cnt) const { return round_up(cnt, 128 / (int64_t)sizeof(T)); }
 
@@ -192,23 +217,52 @@ struct Impl2 : ImplBase {
         (*lv)[o] = D2<T>{(T *)q, pa};
       }
     }
-    {
+    coef.invh2 = (T)((double)(n - 1) * (double)(n - 1));
+    coef.c6 = (T)((double)(n - 1) * (double)(n - 1) / 6.0);
+    // TMA needs 16-byte row strides on the caller's arrays (and on ours)
+    use_fast = ((pitch * (int64_t)sizeof(T)) % 16 == 0) && !getenv("MG_FORCE_REF");
+    if (!use_fast) {
       int64_t ps = pitch_for(n);
       void *q;
       cudaError_t st = dalloc(&q, sizeof(T) * n * ps);
       if (st) return st;
       scratch = D2<T>{(T *)q, ps};
     }
-    coef.invh2 = (T)((double)(n - 1) * (double)(n - 1));
-    coef.c6 = (T)((double)(n - 1) * (double)(n - 1) / 6.0);
-    return cudaSuccess;
+    int thresh = 64;
+    if (const char *e = getenv("MG_COARSE_M")) thresh = atoi(e);
+    oc = k - 1;
+    for (int o = 1; o < k; o++)
+      if (M[o] <= thresh) {
+        oc = o;
+        break;
+      }
+    std::vector<Lev2<T>> lv(k);
+    for (int o = 0; o < k; o++) {
+      lv[o].M = M[o];
+      lv[o].cD = cD[o];
+      lv[o].cA = cA[o];
+      if (o + 1 < k) {
+        lv[o].rD = rD[o];
+        lv[o].vD = vD[o];
+      }
+      if (o >= 1) {
+        lv[o].rA = rA[o];
+        lv[o].vA = vA[o];
+      }
+    }
+    void *q;
+    cudaError_t st = dalloc(&q, sizeof(Lev2<T>) * k);
+    if (st) return st;
+    d_lev = (Lev2<T> *)q;
+    return cudaMemcpy(d_lev, lv.data(), sizeof(Lev2<T>) * k, cudaMemcpyHostToDevice);
   }
 
   NormSink sink() const { return NormSink{s->d_hist, s->d_counter, kHistCap}; }
 
-  void enqueue_cycle(void *u, const void *f_eff, cudaStream_t st, Prof *prof) override {
-    D2<const T> uc{(const T *)u, pitch}, fc{(const T *)f_eff, pitch};
-    D2<T> uu{(T *)u, pitch};
+  void enqueue_cycle(const void *u_in, void *u_out, const void *f_eff, cudaStream_t st, Prof *prof) override {
+    if (use_fast) return enqueue_fast(u_in, u_out, f_eff, st, prof);
+    D2<const T> uc{(const T *)u_in, pitch}, fc{(const T *)f_eff, pitch};
+    D2<T> uu{(T *)u_in, pitch}, uo{(T *)u_out, pitch};
     const double w = sizeof(T);
     const int L = 2 * k - 1;
     STEP("desc_fine", 0, 1, w * (2 * Nl[0] + Nl[1]));
@@ -231,11 +285,50 @@ struct Impl2 : ImplBase {
         launch2_jac_a<T>(vD[o], rA[o], vA[o], M[o], cA[o], st);
       } else {
         STEP("asc_fine", 0, 3, w * (Nl[1] + 3 * Nl[0]));
-        launch2_asc_fine<T>(vD[0], uu, fc, scratch, M[0], s->cfg.order, cA[0], coef, st);
+        launch2_asc_fine<T>(vD[0], uu, fc, scratch, uo, M[0], s->cfg.order, cA[0], coef, st);
+      }
+    }
+  }
+
+  // The B200 path: TMA tile kernels on octaves < oc, one CTA below.
+  void enqueue_fast(const void *u_in, void *u_out, const void *f_eff, cudaStream_t st, Prof *prof) {
+    const double w = sizeof(T);
+    const int L = 2 * k - 1;
+    const T *uin = (const T *)u_in, *fe = (const T *)f_eff;
+    STEP("desc_fine", 0, 1, w * (2 * Nl[0] + Nl[1]));
+    fast2_desc_fine<T>(uin, fe, pitch, rD[0], M[0], s->cfg.order, coef, sink(), st);
+    for (int o = 0; o < oc; o++) {
+      if (o >= 1) {
+        STEP("rest_ad", 2 * o, 1, w * (Nl[2 * o] + Nl[2 * o + 1]));
+        fast2_rest_ad<T>(rA[o], rD[o], M[o], st);
+      }
+      STEP("rest_da", 2 * o + 1, 1, w * (Nl[2 * o + 1] + Nl[2 * o + 2]));
+      fast2_rest_da<T>(rD[o], rA[o + 1], M[o + 1], st);
+    }
+    {
+      double b = 0;
+      for (int l = 2 * oc; l < L; l++) b += 5 * Nl[l];
+      b -= Nl[L - 1] + 2 * Nl[2 * oc];   // coarsest: 4 touches; r_A(oc): read twice, written outside
+      STEP("coarse", 2 * oc, 1, w * b);
+    }
+    launch2_coarse<T>(d_lev, oc, k, s->d_counter, st);
+    for (int o = oc - 1; o >= 0; o--) {
+      STEP("jac_d", 2 * o + 1, 1, w * (Nl[2 * o + 2] + 2 * Nl[2 * o + 1]));
+      fast2_jac_d<T>(vA[o + 1], rD[o], vD[o], M[o], cD[o], st);
+      if (o >= 1) {
+        STEP("jac_a", 2 * o, 1, w * (Nl[2 * o + 1] + 2 * Nl[2 * o]));
+        fast2_jac_a<T>(vD[o], rA[o], vA[o], M[o], cA[o], st);
+      } else {
+        STEP("asc_fine", 0, 1, w * (Nl[1] + 3 * Nl[0]));
+        fast2_asc_fine<T>(vD[0], uin, fe, pitch, (T *)u_out, M[0], s->cfg.order, cA[0], coef, st);
       }
     }
   }
   void enqueue_final_norm(void *u, const void *f_eff, cudaStream_t st) override {
+    if (use_fast) {
+      fast2_desc_fine<T>((const T *)u, (const T *)f_eff, pitch, rD[0], M[0], s->cfg.order, coef, sink(), st);
+      return;
+    }
     D2<const T> uc{(const T *)u, pitch}, fc{(const T *)f_eff, pitch};
     launch2_desc_fine<T>(uc, fc, rD[0], M[0], s->cfg.order, coef, sink(), st);
   }
@@ -250,6 +343,7 @@ struct Impl2 : ImplBase {
     launch2_norm<T>(D2<const T>{(const T *)x, pitch}, M[0], mx, ss, st);
   }
   int launches_per_cycle() const override {
+    if (use_fast) return 1 + (oc - 1) + oc + 1 + oc + oc;
     int c = 1;                               // desc fine
     for (int o = 0; o + 1 < k; o++) c += (o >= 1) + 1;
     c += 1;                                  // coarsest
@@ -343,9 +437,10 @@ struct Impl3 : ImplBase {
   D3<const T> cfield(const void *a) const { return D3<const T>{(const T *)a, pitch, pitch * n}; }
   D3<T> field(void *a) const { return D3<T>{(T *)a, pitch, pitch * n}; }
 
-  void enqueue_cycle(void *u, const void *f_eff, cudaStream_t st, Prof *prof) override {
+  void enqueue_cycle(const void *u_in, void *u_out, const void *f_eff, cudaStream_t st, Prof *prof) override {
     const double w = sizeof(T);
     const int L = 3 * k - 2;
+    void *u = const_cast<void *>(u_in);
     STEP("desc_fine", 0, 1, w * (2 * Nl[0] + Nl[1]));
     launch3_desc_fine<T>(cfield(u), cfield(f_eff), rR[0], M[0], s->cfg.order, coef, sink(), st);
     for (int o = 0; o + 1 < k; o++) {
@@ -372,7 +467,8 @@ struct Impl3 : ImplBase {
         launch3_jac_g<T>(vR[o], rG[o], vG[o], M[o], cG[o], st);
       } else {
         STEP("asc_fine", 0, 3, w * (Nl[1] + 3 * Nl[0]));
-        launch3_asc_fine<T>(vR[0], field(u), cfield(f_eff), scratch, M[0], s->cfg.order, cG[0], coef, st);
+        launch3_asc_fine<T>(vR[0], field(u), cfield(f_eff), scratch, field(u_out), M[0], s->cfg.order, cG[0], coef,
+                            st);
       }
     }
   }
@@ -399,20 +495,22 @@ struct Impl3 : ImplBase {
 
 // ------------------------------------------------------------ helpers
 
-static void drop_graph(mg_solver *s) {
-  if (s->gexec) cudaGraphExecDestroy(s->gexec);
-  s->gexec = nullptr;
-  s->g_u = s->g_f = nullptr;
+static void drop_graphs(mg_solver *s) {
+  for (auto &g : s->graphs) cudaGraphExecDestroy(g.exec);
+  s->graphs.clear();
 }
 
-// Launch one V-cycle: replay the captured graph for (u, f_eff), capturing it
-// on first use or when the pointers change.
-static int run_cycle(mg_solver *s, void *u, const void *f_eff) {
-  if (!s->gexec || s->g_u != u || s->g_f != f_eff) {
-    drop_graph(s);
+// Launch one V-cycle u_in -> u_out: replay the CUDA graph captured for these
+// pointers (captured on first use; a few are cached).
+static int run_cycle(mg_solver *s, const void *u_in, void *u_out, const void *f_eff) {
+  cudaGraphExec_t ex = nullptr;
+  for (auto &g : s->graphs)
+    if (g.uin == u_in && g.uout == u_out && g.f == f_eff) ex = g.exec;
+  if (!ex) {
+    if (s->graphs.size() >= 8) drop_graphs(s);
     cudaGraph_t g = nullptr;
     CKS(s, cudaStreamBeginCapture(s->st, cudaStreamCaptureModeThreadLocal));
-    s->impl->enqueue_cycle(u, f_eff, s->st);
+    s->impl->enqueue_cycle(u_in, u_out, f_eff, s->st);
     cudaError_t le = cudaGetLastError();
     cudaError_t e = cudaStreamEndCapture(s->st, &g);
     if (le != cudaSuccess) {
@@ -420,15 +518,16 @@ static int run_cycle(mg_solver *s, void *u, const void *f_eff) {
       return fail(s, MG_ECUDA, std::string("kernel launch during capture: ") + cudaGetErrorString(le));
     }
     CKS(s, e);
-    e = cudaGraphInstantiate(&s->gexec, g, 0);
+    e = cudaGraphInstantiate(&ex, g, 0);
     cudaGraphDestroy(g);
     CKS(s, e);
-    s->g_u = u;
-    s->g_f = f_eff;
+    s->graphs.push_back({ex, u_in, u_out, f_eff});
   }
-  CKS(s, cudaGraphLaunch(s->gexec, s->st));
+  CKS(s, cudaGraphLaunch(ex, s->st));
   return MG_OK;
 }
+
+static bool aligned16(const void *p) { return ((uintptr_t)p & 15) == 0; }
 
 static int begin(mg_solver *s) {
   CKS(s, cudaEventRecord(s->ev_in, s->user));
@@ -544,7 +643,8 @@ int mg_destroy(mg_solver *s) {
   if (!s) return MG_OK;
   DeviceGuard g(s->device);
   if (s->st) cudaStreamSynchronize(s->st);
-  drop_graph(s);
+  drop_graphs(s);
+  cudaFree(s->d_ualt);
   if (s->impl) s->impl->free_all();
   cudaFree(s->d_hist);
   cudaFree(s->d_counter);
@@ -609,10 +709,23 @@ static int vcycle_dev(mg_solver *s, void *u, const void *f, int ncycles, double 
   int nslots = ncycles + 1 < kHistCap ? ncycles + 1 : kHistCap;
   CKS(s, cudaMemsetAsync(s->d_hist, 0, sizeof(unsigned long long) * nslots, s->st));
   CKS(s, cudaMemsetAsync(s->d_counter, 0, sizeof(int), s->st));
-  for (int c = 0; c < ncycles; c++) {
-    int rc = run_cycle(s, u, fe);
-    if (rc) return rc;
+  // TMA path: u alternates between the caller's array and an internal
+  // partner (the ascent reads the old u in a 2-node halo, so it cannot update
+  // in place); an odd cycle count ends with one copy back.
+  bool alt = s->impl->fast() && aligned16(u) && aligned16(fe);
+  if (alt && !s->d_ualt) {
+    size_t bytes = s->field_elems() * s->esz;
+    CKS(s, cudaMalloc(&s->d_ualt, bytes));
+    CKS(s, cudaMemsetAsync(s->d_ualt, 0, bytes, s->st));
   }
+  void *cur = u;
+  for (int c = 0; c < ncycles; c++) {
+    void *dst = alt ? (cur == u ? s->d_ualt : u) : u;
+    int rc = run_cycle(s, cur, dst, fe);
+    if (rc) return rc;
+    cur = dst;
+  }
+  if (cur != u) CKS(s, cudaMemcpyAsync(u, cur, s->field_elems() * s->esz, cudaMemcpyDeviceToDevice, s->st));
   if (res_hist) {
     s->impl->enqueue_final_norm(u, fe, s->st);
     CKS(s, cudaMemcpyAsync(s->h_hist, s->d_hist, sizeof(unsigned long long) * nslots, cudaMemcpyDeviceToHost, s->st));
@@ -704,10 +817,20 @@ int mg_profile(mg_solver *s, void *u, const void *f, int ncycles, mg_step_stat *
   CKS(s, cudaMemsetAsync(s->d_counter, 0, sizeof(int), s->st));
   Prof prof;
   prof.st = s->st;
-  for (int c = 0; c < ncycles; c++) {
-    s->impl->enqueue_cycle(u, fe, s->st, &prof);
-    prof.end_cycle();
+  bool alt = s->impl->fast() && aligned16(u) && aligned16(fe);
+  if (alt && !s->d_ualt) {
+    size_t bytes = s->field_elems() * s->esz;
+    CKS(s, cudaMalloc(&s->d_ualt, bytes));
+    CKS(s, cudaMemsetAsync(s->d_ualt, 0, bytes, s->st));
   }
+  void *cur = u;
+  for (int c = 0; c < ncycles; c++) {
+    void *dst = alt ? (cur == u ? s->d_ualt : u) : u;
+    s->impl->enqueue_cycle(cur, dst, fe, s->st, &prof);
+    prof.end_cycle();
+    cur = dst;
+  }
+  if (cur != u) CKS(s, cudaMemcpyAsync(u, cur, s->field_elems() * s->esz, cudaMemcpyDeviceToDevice, s->st));
   CKS(s, cudaGetLastError());
   CKS(s, cudaStreamSynchronize(s->st));
   size_t ns = prof.steps.size();

@@ -1,0 +1,35 @@
+// tma_host.cu -- host-side tensor-map encoding (cuTensorMapEncodeTiled via the
+// runtime's driver entry point; no link dependency on libcuda).
+#include <cudaTypedefs.h>
+
+#include "tma.cuh"
+
+namespace mg {
+
+static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    void *p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+bool encode_tmap(CUtensorMap *tm, const void *base, int esz, int rank, const uint64_t *dims, uint64_t pitch,
+                 uint64_t plane, const uint32_t *box) {
+  auto fn = encode_fn();
+  if (!fn) return false;
+  cuuint64_t gdim[3] = {dims[0], dims[1], rank > 2 ? dims[2] : 1};
+  cuuint64_t gstr[2] = {pitch * (uint64_t)esz, plane * (uint64_t)esz};
+  cuuint32_t bdim[3] = {box[0], box[1], rank > 2 ? box[2] : 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = fn(tm, esz == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, rank,
+                  const_cast<void *>(base), gdim, gstr, bdim, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                  CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+}  // namespace mg
