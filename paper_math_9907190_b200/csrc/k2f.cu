@@ -102,7 +102,8 @@ __global__ void __launch_bounds__(Op::NT) tile_pipeline(const __grid_constant__ 
       int tn = t + (S - 1) * gridDim.x;
       if (tn < ntiles) {
         int sn = (i + S - 1) % S;   // consumed at iteration i-1 (synchronised below)
-        fence_proxy_async();
+        // WAR on the slot is ordered by the __syncthreads that ended its last use
+        // (no proxy fence: that would wait for the in-flight TMA loads)
         Op::issue(P, tn, smem + sn * Op::STAGE, &bar[sn]);
       }
     }

@@ -4,88 +4,13 @@
 // (FCC: I+J+K even) -> magenta M(s) (BCC: I=J=K mod 2) -> G(2s).
 // Canonical evaluation order and --fmad=false as in k2d.cu.
 #include "kernels.h"
+#include "ops3.cuh"
 
 namespace mg {
 
 constexpr int NT3 = 256;
 
 static inline unsigned blocks3(int64_t n) { return (unsigned)((n + NT3 - 1) / NT3); }
-
-// Axis offsets in the printed order of Erred / Ermagm / Egprolg / Egprolr.
-__constant__ int c_ax6[6][3] = {{1, 0, 0}, {-1, 0, 0}, {0, 1, 0}, {0, -1, 0}, {0, 0, 1}, {0, 0, -1}};
-// Face diagonals in the printed order of Ermagc = Erprolm.
-__constant__ int c_fd12[12][3] = {{1, 1, 0},  {1, -1, 0},  {-1, -1, 0}, {-1, 1, 0}, {1, 0, 1},  {1, 0, -1},
-                                  {-1, 0, -1}, {-1, 0, 1}, {0, 1, 1},   {0, 1, -1}, {0, -1, -1}, {0, -1, 1}};
-// Body diagonals in the printed order of Erblu = Emprolm/b.
-__constant__ int c_bd8[8][3] = {{1, 1, 1},  {1, 1, -1},  {1, -1, 1},  {1, -1, -1},
-                                {-1, 1, 1}, {-1, 1, -1}, {-1, -1, 1}, {-1, -1, -1}};
-// Erprolr for normal axis x, y, z: the normal pair (weight 2)
-// then the 4 in-plane corners; the z table is printed, x and y follow by the
-// cyclic permutation (a,b,c) -> (c,a,b) / (b,c,a) (reading A8).
-__constant__ int c_erp[3][6][3] = {
-    {{1, 0, 0}, {-1, 0, 0}, {0, 1, 1}, {0, 1, -1}, {0, -1, -1}, {0, -1, 1}},
-    {{0, 1, 0}, {0, -1, 0}, {1, 0, 1}, {-1, 0, 1}, {-1, 0, -1}, {1, 0, -1}},
-    {{0, 0, 1}, {0, 0, -1}, {1, 1, 0}, {1, -1, 0}, {-1, -1, 0}, {-1, 1, 0}}};
-
-// ------------------------------------------------------------- residual
-// order 2: 7-point, centre first then i+1,i-1,j+1,j-1,k+1,k-1.
-// order 4: Efos4, f~ precomputed; bracket in printed order.
-template <class T, int ORDER>
-__device__ __forceinline__ T res3(const D3<const T> &u, const D3<const T> &f, int x, int y, int z, const Coef<T> &k) {
-  if (ORDER == 2) {
-    T lap = -((T)6 * u(x, y, z));
-    lap = lap + u(x + 1, y, z);
-    lap = lap + u(x - 1, y, z);
-    lap = lap + u(x, y + 1, z);
-    lap = lap + u(x, y - 1, z);
-    lap = lap + u(x, y, z + 1);
-    lap = lap + u(x, y, z - 1);
-    lap = lap * k.invh2;
-    return f(x, y, z) - lap;
-  } else {
-    T ax = u(x, y - 1, z);
-    ax = ax + u(x, y + 1, z);
-    ax = ax + u(x - 1, y, z);
-    ax = ax + u(x + 1, y, z);
-    ax = ax + u(x, y, z + 1);
-    ax = ax + u(x, y, z - 1);
-    T b = -((T)24 * u(x, y, z));
-    b = b + (T)2 * ax;
-    b = b + u(x + 1, y + 1, z);
-    b = b + u(x - 1, y + 1, z);
-    b = b + u(x - 1, y - 1, z);
-    b = b + u(x + 1, y - 1, z);
-    b = b + u(x, y + 1, z + 1);
-    b = b + u(x, y + 1, z - 1);
-    b = b + u(x, y - 1, z - 1);
-    b = b + u(x, y - 1, z + 1);
-    b = b + u(x + 1, y, z + 1);
-    b = b + u(x - 1, y, z + 1);
-    b = b + u(x - 1, y, z - 1);
-    b = b + u(x + 1, y, z - 1);
-    return f(x, y, z) - b * k.c6;
-  }
-}
-
-template <class T, int ORDER>
-__device__ __forceinline__ T res3z(const D3<const T> &u, const D3<const T> &f, int x, int y, int z, int M,
-                                   const Coef<T> &k) {
-  if (x <= 0 || y <= 0 || z <= 0 || x >= M || y >= M || z >= M) return (T)0;
-  return res3<T, ORDER>(u, f, x, y, z, k);
-}
-
-__device__ __forceinline__ bool inner3(int x, int y, int z, int M) {
-  return x >= 1 && y >= 1 && z >= 1 && x <= M - 1 && y <= M - 1 && z <= M - 1;
-}
-
-// Erred: (1/12)(6r + r_{i+1} + r_{i-1} + r_{j+1} + r_{j-1} + r_{k+1} + r_{k-1}).
-template <class T>
-__device__ __forceinline__ T erred(T c, const T nb[6]) {
-  T t = (T)6 * c;
-#pragma unroll
-  for (int q = 0; q < 6; q++) t = t + nb[q];
-  return t * (T)(1.0 / 12.0);
-}
 
 // -------------------------------------------------- descent, finest level
 // Fused a9+a10: residual recomputed, Erred onto R(1).  Thread (a,b,c) owns

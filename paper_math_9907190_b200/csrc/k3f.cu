@@ -1,0 +1,358 @@
+// k3f.cu -- 3D TMA plane-streaming kernels (sm_100a) for the finest octave.
+//
+// A work unit is an xy tile (TX x TY fine nodes) times a z chunk.  The CTA
+// streams the unit plane by plane: one elected thread keeps the next planes'
+// TMA loads (2D boxes of 3D tensors, out-of-bounds -> 0) in flight into a
+// ring of NS shared-memory slots, one mbarrier per slot; the CTA computes
+// plane p from the slots of the last few planes (2.5D blocking: only the xy
+// halo is re-read, from L2).  Node formulas are the shared ones of
+// ops3.cuh, so results are bit-identical to the reference kernels.
+#include "kernels.h"
+#include "ops3.cuh"
+#include "tma.cuh"
+
+namespace mg {
+
+namespace p3 {
+
+constexpr int al128(int n) { return (n + 127) / 128 * 128; }
+template <class T>
+constexpr int w16(int n) {
+  return (n * (int)sizeof(T) + 15) / 16 * 16 / (int)sizeof(T);
+}
+template <class T>
+constexpr int hx(int h) {
+  return (h * (int)sizeof(T) + 15) / 16 * 16 / (int)sizeof(T);
+}
+
+template <class T>
+struct Vec2;
+template <>
+struct Vec2<double> {
+  using t = double2;
+};
+template <>
+struct Vec2<float> {
+  using t = float2;
+};
+template <class T>
+__device__ __forceinline__ void ld2(const T *p, T &a, T &b) {
+  auto v = *reinterpret_cast<const typename Vec2<T>::t *>(p);
+  a = v.x;
+  b = v.y;
+}
+template <class T>
+__device__ __forceinline__ void st2(T *p, T a, T b) {
+  typename Vec2<T>::t v;
+  v.x = a;
+  v.y = b;
+  *reinterpret_cast<typename Vec2<T>::t *>(p) = v;
+}
+
+template <class T>
+struct STile {
+  T *p;
+  int ld, ox, oy;
+  __device__ __forceinline__ T *at(int x, int y) const { return p + (y - oy) * ld + (x - ox); }
+  __device__ __forceinline__ T operator()(int x, int y) const { return *at(x, y); }
+};
+
+// Three consecutive planes (z = zb-1, zb, zb+1) of a field as a 3D accessor.
+template <class T>
+struct Planes3 {
+  STile<T> m, c, p;
+  int zb;
+  __device__ __forceinline__ T operator()(int x, int y, int z) const {
+    return z < zb ? m(x, y) : (z == zb ? c(x, y) : p(x, y));
+  }
+};
+template <class T>
+struct Plane1 {
+  STile<T> c;
+  __device__ __forceinline__ T operator()(int x, int y, int) const { return c(x, y); }
+};
+
+}  // namespace p3
+
+using namespace p3;
+
+// --------------------------------------------------------------- pipeline
+// Op provides: Unit decode(P, u) with fields pb, pe (plane range of the unit),
+// issue(P, unit, p, slot, bar), step(P, unit, p, slots[3] = {L_p, L_{p-1},
+// L_{p-2}}, scratch, acc).  Slot indices and mbarrier phases are tracked
+// incrementally (no division in the loop).
+template <class Op>
+__global__ void __launch_bounds__(Op::NT, 1) plane_pipeline(const __grid_constant__ typename Op::Params P) {
+  constexpr int NS = Op::NS, D = Op::D;
+  static_assert(NS >= D + 2 + Op::LAFTER, "ring too small for the prefetch distance");
+  extern __shared__ __align__(128) unsigned char smem[];
+  __shared__ __align__(8) uint64_t bar[NS];
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < NS; s++) mbar_init(&bar[s], 1);
+    fence_mbar_init();
+    Op::prefetch(P);
+  }
+  __syncthreads();
+  typename Op::Acc acc;
+  Op::init(acc);
+  const int nunits = P.nunits;
+  // producer cursor (used by thread 0 only)
+  int pu = blockIdx.x, pp = 0, ps = 0;
+  typename Op::Unit pun{};
+  auto produce = [&]() {
+    Op::issue(P, pun, pp, smem + ps * Op::SLOT, &bar[ps]);
+    ps = (ps + 1 == NS) ? 0 : ps + 1;
+    if (++pp >= pun.pe) {
+      pu += gridDim.x;
+      if (pu < nunits) {
+        pun = Op::decode(P, pu);
+        pp = pun.pb;
+      }
+    }
+  };
+  if (threadIdx.x == 0 && pu < nunits) {
+    pun = Op::decode(P, pu);
+    pp = pun.pb;
+    for (int j = 0; j <= D && pu < nunits; j++) produce();
+  }
+  int s0 = 0, s1 = NS - 1, s2 = NS - 2;   // slots of loads g, g-1, g-2
+  uint32_t phase = 0;
+  for (int u = blockIdx.x; u < nunits; u += gridDim.x) {
+    const typename Op::Unit un = Op::decode(P, u);
+    for (int p = un.pb; p < un.pe; p++) {
+      if (threadIdx.x == 0 && pu < nunits) produce();
+      mbar_wait(&bar[s0], phase);
+      unsigned char *sl[3] = {smem + s0 * Op::SLOT, smem + s1 * Op::SLOT, smem + s2 * Op::SLOT};
+      Op::step(P, un, p, sl, smem + NS * Op::SLOT, acc);
+      __syncthreads();
+      s2 = s1;
+      s1 = s0;
+      if (++s0 == NS) {
+        s0 = 0;
+        phase ^= 1;
+      }
+    }
+  }
+  Op::finish(P, acc);
+}
+
+__device__ __forceinline__ bool inside3(int x, int y, int z, int M) {
+  return x >= 1 && y >= 1 && z >= 1 && x <= M - 1 && y <= M - 1 && z <= M - 1;
+}
+
+constexpr int TX3 = 64, TY3 = 16, NT3F = 512, NW3 = NT3F / 32, ZC = 64;
+
+struct Unit3 {
+  int x0, y0, zs, ze, pb, pe;
+};
+
+// ============================================== finest descent a9 + a10
+// r = f - L u (7-point or Efos4) on the tile plus its xy ring, plane by plane,
+// kept in a 3-plane ring; Erred onto the four red sublattices of R(1).
+// Load L_p holds u(p+1) and f(p); step p computes r(p) (needs L_{p-2..p})
+// and writes the red nodes of plane p-1 (needs r(p-2..p)).
+template <class T, int ORDER>
+struct OpDesc3Fine {
+  static constexpr int NT = NT3F, NS = 7, D = 3, LAFTER = 2;
+  static constexpr int HU = hx<T>(2), HF = hx<T>(1);
+  static constexpr int UW = w16<T>(TX3 + HU + 2), UH = TY3 + 4, FW = w16<T>(TX3 + HF + 1), FH = TY3 + 2;
+  // r planes are stored de-interleaved: per row [even x | odd x], each
+  // TX/2 + 2 entries (column pair index -1 .. TX/2), so a lane's node and its
+  // x-neighbours are unit-stride across the warp
+  static constexpr int RH2 = TX3 / 2 + 2, RW = 2 * RH2, RH = TY3 + 2;
+  static constexpr int U_BYTES = UW * UH * sizeof(T), F_BYTES = FW * FH * sizeof(T);
+  static constexpr int U_OFF = 0, F_OFF = al128(U_BYTES);
+  static constexpr int SLOT = al128(F_OFF + F_BYTES);
+  static constexpr int RPL = al128(RW * RH * sizeof(T));
+  static constexpr int NR = 4;   // r planes p-3 .. p
+  static constexpr int SMEM = NS * SLOT + NR * RPL;
+  struct Params {
+    CUtensorMap tu, tf;
+    S3<T> out;
+    int M, ntx, nty, nunits;
+    Coef<T> k;
+    NormSink ns;
+  };
+  using Unit = Unit3;
+  struct Acc {
+    double mx;
+  };
+  static __device__ void prefetch(const Params &P) {
+    tma_prefetch_desc(&P.tu);
+    tma_prefetch_desc(&P.tf);
+  }
+  static __device__ void init(Acc &a) { a.mx = 0.0; }
+  // step p computes r(p) and writes the red nodes of plane p-2 (from r(p-3..p-1))
+  static __device__ __forceinline__ Unit decode(const Params &P, int u) {
+    int tx = u % P.ntx, r = u / P.ntx, ty = r % P.nty, zc = r / P.nty;
+    Unit un;
+    un.x0 = tx * TX3;
+    un.y0 = ty * TY3;
+    un.zs = zc * ZC;
+    un.ze = min(un.zs + ZC, P.M);
+    un.pb = un.zs - 3;
+    un.pe = un.ze + 2;
+    return un;
+  }
+  static __device__ void issue(const Params &P, const Unit &un, int p, unsigned char *slot, uint64_t *bar) {
+    mbar_expect_tx(bar, U_BYTES + F_BYTES);
+    tma_load_3d(slot + U_OFF, &P.tu, un.x0 - HU, un.y0 - 2, p + 1, bar);
+    tma_load_3d(slot + F_OFF, &P.tf, un.x0 - HF, un.y0 - 1, p, bar);
+  }
+  // residuals at (xl, y, z) and (xl+1, y, z); um/uc/up point at u(xl, y) of
+  // planes z-1, z, z+1 in their slots, ff at f(xl, y).
+  static __device__ __forceinline__ void rpair(const T *um, const T *uc, const T *up, const T *ff, bool in0, bool in1,
+                                               const Coef<T> &k, T &r0, T &r1) {
+    Nb19<T> a, b;
+    ld2(uc, a.c, b.c);
+    ld2(uc + UW, a.yp, b.yp);
+    ld2(uc - UW, a.ym, b.ym);
+    ld2(up, a.zp, b.zp);
+    ld2(um, a.zm, b.zm);
+    a.xp = b.c;
+    a.xm = uc[-1];
+    b.xp = uc[2];
+    b.xm = a.c;
+    if (ORDER == 4) {
+      a.xpyp = b.yp;
+      a.xmyp = uc[UW - 1];
+      a.xmym = uc[-UW - 1];
+      a.xpym = b.ym;
+      b.xpyp = uc[UW + 2];
+      b.xmyp = a.yp;
+      b.xmym = a.ym;
+      b.xpym = uc[-UW + 2];
+      ld2(up + UW, a.ypzp, b.ypzp);
+      ld2(um + UW, a.ypzm, b.ypzm);
+      ld2(um - UW, a.ymzm, b.ymzm);
+      ld2(up - UW, a.ymzp, b.ymzp);
+      a.xpzp = b.zp;
+      a.xmzp = up[-1];
+      a.xmzm = um[-1];
+      a.xpzm = b.zm;
+      b.xpzp = up[2];
+      b.xmzp = a.zp;
+      b.xmzm = a.zm;
+      b.xpzm = um[2];
+    }
+    T f0, f1;
+    ld2(ff, f0, f1);
+    r0 = in0 ? res3v<T, ORDER>(a, f0, k) : (T)0;
+    r1 = in1 ? res3v<T, ORDER>(b, f1, k) : (T)0;
+  }
+  static __device__ void step(const Params &P, const Unit &un, int p, unsigned char *const sl[3], unsigned char *scr,
+                              Acc &acc) {
+    const int M = P.M, lane = threadIdx.x & 31, w = threadIdx.x >> 5, xl = un.x0 + 2 * lane;
+    const int x0 = un.x0, y0 = un.y0;
+    auto rbase = [&](int z) { return (T *)(scr + (z & (NR - 1)) * RPL); };   // z >= -3 -> (z & 3) is a valid slot
+    auto uo = [&](int x, int y) { return (y - (y0 - 2)) * UW + (x - (x0 - HU)); };
+    auto fo = [&](int x, int y) { return (y - (y0 - 1)) * FW + (x - (x0 - HF)); };
+    // de-interleaved r: row y, column x -> [ (x&1) * RH2 + (x - x0) / 2 + 1 ]
+    auto rro = [&](int x, int y) { return (y - (y0 - 1)) * RW + (x & 1) * RH2 + ((x - x0) >> 1) + 1; };
+    if (p >= un.zs - 1 && p <= un.ze) {
+      const T *Up = (const T *)(sl[0] + U_OFF), *Uc = (const T *)(sl[1] + U_OFF), *Um = (const T *)(sl[2] + U_OFF);
+      const T *F = (const T *)(sl[0] + F_OFF);
+      T *R = rbase(p + 4);
+      const bool own = p >= un.zs && p < un.ze;
+      const bool zin = p >= 1 && p <= M - 1, xin0 = xl >= 1 && xl <= M - 1, xin1 = xl + 1 <= M - 1;
+      T r0, r1;
+#pragma unroll
+      for (int j = 0; j < TY3 / NW3; j++) {
+        int y = y0 + w + j * NW3;
+        bool yin = zin && y >= 1 && y <= M - 1;
+        int o = uo(xl, y);
+        rpair(Um + o, Uc + o, Up + o, F + fo(xl, y), yin && xin0, yin && xin1, P.k, r0, r1);
+        int ro = rro(xl, y);
+        R[ro] = r0;
+        R[ro + RH2] = r1;
+        if (own) acc.mx = nmax(nmax(acc.mx, absd(r0)), absd(r1));
+      }
+      if (w < 2) {
+        int y = w == 0 ? y0 - 1 : y0 + TY3;
+        bool yin = zin && y >= 1 && y <= M - 1;
+        int o = uo(xl, y);
+        rpair(Um + o, Uc + o, Up + o, F + fo(xl, y), yin && xin0, yin && xin1, P.k, r0, r1);
+        int ro = rro(xl, y);
+        R[ro] = r0;
+        R[ro + RH2] = r1;
+      } else if (w == 2) {
+        int x = lane < 16 ? x0 - 1 : x0 + TX3, y = y0 + (lane & 15);
+        Planes3<T> U3{STile<T>{(T *)Um, UW, x0 - HU, y0 - 2}, STile<T>{(T *)Uc, UW, x0 - HU, y0 - 2},
+                      STile<T>{(T *)Up, UW, x0 - HU, y0 - 2}, p};
+        Plane1<T> F1{STile<T>{(T *)F, FW, x0 - HF, y0 - 1}};
+        R[rro(x, y)] = inside3(x, y, p, M) ? res3<T, ORDER>(U3, F1, x, y, p, P.k) : (T)0;
+      }
+    }
+    const int q = p - 2;   // r(q-1), r(q), r(q+1) were completed in earlier steps
+    if (q >= un.zs && q < un.ze && q >= 1 && q <= M - 1) {
+      const T *Rm = rbase(q + 3), *Rc = rbase(q + 4), *Rp = rbase(q + 5);
+#pragma unroll
+      for (int j = 0; j < TY3 / NW3; j++) {
+        int y = y0 + w + j * NW3;
+        int par = (y + q) & 1, x = xl + par;
+        if (!inside3(x, y, q, M)) continue;
+        int o = rro(x, y);                           // the node
+        int oo = (y - (y0 - 1)) * RW + (1 - par) * RH2 + lane + 1;   // x-neighbour column block
+        // Erred: i+1, i-1, j+1, j-1, k+1, k-1
+        T nb[6] = {Rc[oo + par], Rc[oo + par - 1], Rc[o + RW], Rc[o - RW], Rp[o], Rm[o]};
+        P.out.ref(x, y, q) = erred(Rc[o], nb);
+      }
+    }
+  }
+  static __device__ void finish(const Params &P, Acc &acc) { block_norm_push<NT>(P.ns, acc.mx); }
+};
+
+// ================================================================= launch
+template <class Op>
+static cudaError_t run_plane(const typename Op::Params &P, cudaStream_t st) {
+  cudaError_t e = cudaFuncSetAttribute(plane_pipeline<Op>, cudaFuncAttributeMaxDynamicSharedMemorySize, Op::SMEM);
+  if (e != cudaSuccess) return e;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  int per_sm = (227 * 1024) / (Op::SMEM + 1024);
+  if (per_sm < 1) per_sm = 1;
+  int grid = sms * per_sm;
+  if (grid > P.nunits) grid = P.nunits;
+  if (grid < 1) return cudaSuccess;
+  plane_pipeline<Op><<<grid, Op::NT, Op::SMEM, st>>>(P);
+  return cudaGetLastError();
+}
+
+template <class T>
+static bool tm3(CUtensorMap *tm, const void *p, int64_t n, int64_t pitch, int64_t plane, int bx, int by) {
+  uint64_t dims[3] = {(uint64_t)n, (uint64_t)n, (uint64_t)n};
+  uint32_t box[3] = {(uint32_t)bx, (uint32_t)by, 1};
+  return encode_tmap(tm, p, sizeof(T), 3, dims, (uint64_t)pitch, (uint64_t)plane, box);
+}
+
+template <class T, int ORDER>
+static cudaError_t desc3_impl(const T *u, const T *f, int64_t pitch, const S3<T> &rr, int M, const Coef<T> &k,
+                              const NormSink &ns, cudaStream_t st) {
+  using Op = OpDesc3Fine<T, ORDER>;
+  typename Op::Params P{};
+  int64_t n = M + 1, plane = pitch * n;
+  if (!tm3<T>(&P.tu, u, n, pitch, plane, Op::UW, Op::UH) || !tm3<T>(&P.tf, f, n, pitch, plane, Op::FW, Op::FH))
+    return cudaErrorInvalidValue;
+  P.out = rr;
+  P.M = M;
+  P.ntx = (M + TX3 - 1) / TX3;
+  P.nty = (M + TY3 - 1) / TY3;
+  P.nunits = P.ntx * P.nty * ((M + ZC - 1) / ZC);
+  P.k = k;
+  P.ns = ns;
+  return run_plane<Op>(P, st);
+}
+
+template <class T>
+cudaError_t fast3_desc_fine(const T *u, const T *f, int64_t pitch, const S3<T> &rr, int M, int order, const Coef<T> &k,
+                            const NormSink &ns, cudaStream_t st) {
+  return order == 2 ? desc3_impl<T, 2>(u, f, pitch, rr, M, k, ns, st) : desc3_impl<T, 4>(u, f, pitch, rr, M, k, ns, st);
+}
+
+template cudaError_t fast3_desc_fine<float>(const float *, const float *, int64_t, const S3<float> &, int, int,
+                                            const Coef<float> &, const NormSink &, cudaStream_t);
+template cudaError_t fast3_desc_fine<double>(const double *, const double *, int64_t, const S3<double> &, int, int,
+                                             const Coef<double> &, const NormSink &, cudaStream_t);
+
+}  // namespace mg

@@ -1,0 +1,397 @@
+// k3l.cu -- 3D level kernels on the packed parity sublattices (sm_100a).
+//
+// Every 3D step of the octave (Erred for s > 1, Ermagc/Ermagm, Erblu,
+// Emprolm/b, Erprolr/m, Egprolg/r) is written here in half-index form: the
+// sublattice arrays C, Fx, Fy, Fz (red), C, B (magenta) are dense H^3 arrays
+// (H = M/2 + 1) and every stencil becomes a box stencil with offsets in
+// {-1, 0, 1}.  One thread per half-index (a, b, c), a fastest (coalesced),
+// block (32, 8) over (a, b), grid.z over c; no parity tests at run time.
+// The neighbour order of every sum is the paper's printed order (DESIGN.md
+// canonical arithmetic), so the results are bit-identical to the reference
+// kernels.
+#include "kernels.h"
+#include "ops3.cuh"
+
+namespace mg {
+
+namespace l3 {
+
+// sublattice slots of S3: (x&1) | (y&1)<<1 | (z&1)<<2
+constexpr int C = 0, FX = 6, FY = 5, FZ = 3, B = 7;
+
+template <class T>
+struct Sub {   // one sublattice array of a split level
+  T *p;
+  int64_t pitch, plane;
+  __device__ __forceinline__ T &operator()(int a, int b, int c) const {
+    return p[(int64_t)c * plane + (int64_t)b * pitch + a];
+  }
+};
+template <class T>
+__device__ __forceinline__ Sub<T> sub(const S3<T> &s, int k) {
+  return Sub<T>{s.s[k], s.pitch, s.plane};
+}
+
+template <class T>
+__device__ __forceinline__ T sum6(T v0, T v1, T v2, T v3, T v4, T v5) {
+  T t = v0;
+  t = t + v1;
+  t = t + v2;
+  t = t + v3;
+  t = t + v4;
+  t = t + v5;
+  return t;
+}
+
+}  // namespace l3
+
+using namespace l3;
+
+#define IDX3                                                                             \
+  const int a = blockIdx.x * 32 + threadIdx.x, b = blockIdx.y * 8 + threadIdx.y, c = blockIdx.z; \
+  if (a >= H || b >= H) return;
+
+// --------------------------------------------------------- G(s) -> R(s)
+// Erred from the dense G(s) residual; the 2x2x2 block (a,b,c)
+// holds C (0,0,0), Fx (0,1,1), Fy (1,0,1), Fz (1,1,0).
+template <class T>
+__global__ void __launch_bounds__(256) k3l_rest_gr(D3<const T> r, S3<T> out, int M, int H) {
+  IDX3
+  const int x = 2 * a, y = 2 * b, z = 2 * c;
+  auto er = [&](int X, int Y, int Z) {
+    T nb[6] = {r(X + 1, Y, Z), r(X - 1, Y, Z), r(X, Y + 1, Z), r(X, Y - 1, Z), r(X, Y, Z + 1), r(X, Y, Z - 1)};
+    return erred(r(X, Y, Z), nb);
+  };
+  const bool in_a = x >= 2 && x <= M - 2, in_b = y >= 2 && y <= M - 2, in_c = z >= 2 && z <= M - 2;
+  const bool od_a = x + 1 <= M - 1, od_b = y + 1 <= M - 1, od_c = z + 1 <= M - 1;
+  if (in_a && in_b && in_c) sub(out, C)(a, b, c) = er(x, y, z);
+  if (in_a && od_b && od_c) sub(out, FX)(a, b, c) = er(x, y + 1, z + 1);
+  if (od_a && in_b && od_c) sub(out, FY)(a, b, c) = er(x + 1, y, z + 1);
+  if (od_a && od_b && in_c) sub(out, FZ)(a, b, c) = er(x + 1, y + 1, z);
+}
+
+// --------------------------------------------------------- R(s) -> M(s)
+// corners: Ermagc (1/24)(12 r + 12 face diagonals, printed order);
+// centres: Ermagm (1/6)(6 axis neighbours), zero self weight.
+template <class T>
+__global__ void __launch_bounds__(256) k3l_rest_rm(S3<const T> rr, S3<T> rm, int H) {
+  IDX3
+  Sub<const T> Cr{rr.s[C], rr.pitch, rr.plane}, Fx{rr.s[FX], rr.pitch, rr.plane}, Fy{rr.s[FY], rr.pitch, rr.plane},
+      Fz{rr.s[FZ], rr.pitch, rr.plane};
+  if (a >= 1 && b >= 1 && c >= 1 && a <= H - 2 && b <= H - 2 && c <= H - 2) {
+    T t = (T)12 * Cr(a, b, c);
+    t = t + Fz(a, b, c);              // (+1,+1, 0)
+    t = t + Fz(a, b - 1, c);          // (+1,-1, 0)
+    t = t + Fz(a - 1, b - 1, c);      // (-1,-1, 0)
+    t = t + Fz(a - 1, b, c);          // (-1,+1, 0)
+    t = t + Fy(a, b, c);              // (+1, 0,+1)
+    t = t + Fy(a, b, c - 1);          // (+1, 0,-1)
+    t = t + Fy(a - 1, b, c - 1);      // (-1, 0,-1)
+    t = t + Fy(a - 1, b, c);          // (-1, 0,+1)
+    t = t + Fx(a, b, c);              // ( 0,+1,+1)
+    t = t + Fx(a, b, c - 1);          // ( 0,+1,-1)
+    t = t + Fx(a, b - 1, c - 1);      // ( 0,-1,-1)
+    t = t + Fx(a, b - 1, c);          // ( 0,-1,+1)
+    sub(rm, C)(a, b, c) = t * (T)(1.0 / 24.0);
+  }
+  if (a <= H - 2 && b <= H - 2 && c <= H - 2) {
+    // centre (2a+1, 2b+1, 2c+1): i+1, i-1, j+1, j-1, k+1, k-1
+    T t = sum6(Fx(a + 1, b, c), Fx(a, b, c), Fy(a, b + 1, c), Fy(a, b, c), Fz(a, b, c + 1), Fz(a, b, c));
+    sub(rm, B)(a, b, c) = t * (T)(1.0 / 6.0);
+  }
+}
+
+// ------------------------------------------------------- M(s) -> G(2s)
+// Erblu: (1/16)(8 r + 8 body diagonals, printed order).
+template <class T>
+__global__ void __launch_bounds__(256) k3l_rest_mg(S3<const T> rm, D3<T> g2, int Mc) {
+  const int H = Mc + 1;
+  IDX3
+  if (a < 1 || b < 1 || c < 1 || a > Mc - 1 || b > Mc - 1 || c > Mc - 1) return;
+  Sub<const T> Cm{rm.s[C], rm.pitch, rm.plane}, Bm{rm.s[B], rm.pitch, rm.plane};
+  T t = (T)8 * Cm(a, b, c);
+  t = t + Bm(a, b, c);               // (+,+,+)
+  t = t + Bm(a, b, c - 1);           // (+,+,-)
+  t = t + Bm(a, b - 1, c);           // (+,-,+)
+  t = t + Bm(a, b - 1, c - 1);       // (+,-,-)
+  t = t + Bm(a - 1, b, c);           // (-,+,+)
+  t = t + Bm(a - 1, b, c - 1);       // (-,+,-)
+  t = t + Bm(a - 1, b - 1, c);       // (-,-,+)
+  t = t + Bm(a - 1, b - 1, c - 1);   // (-,-,-)
+  g2(a, b, c) = t * (T)(1.0 / 16.0);
+}
+
+// ----------------------------------------------- M(s) from G(2s): a13
+// Emprolm on the centres, then (second kernel) Emprolb
+// on the corners from the new centres; c = 4 p_m (sh)^2.
+template <class T>
+__global__ void __launch_bounds__(256) k3l_jac_m1(D3<const T> vc, S3<const T> r, S3<T> v, int H, T cc) {
+  IDX3
+  if (a > H - 2 || b > H - 2 || c > H - 2) return;
+  T t = -(cc * r.s[B][(int64_t)c * r.plane + (int64_t)b * r.pitch + a]);
+  t = t + vc(a + 1, b + 1, c + 1);   // (+,+,+)
+  t = t + vc(a + 1, b + 1, c);       // (+,+,-)
+  t = t + vc(a + 1, b, c + 1);       // (+,-,+)
+  t = t + vc(a + 1, b, c);           // (+,-,-)
+  t = t + vc(a, b + 1, c + 1);       // (-,+,+)
+  t = t + vc(a, b + 1, c);           // (-,+,-)
+  t = t + vc(a, b, c + 1);           // (-,-,+)
+  t = t + vc(a, b, c);               // (-,-,-)
+  sub(v, B)(a, b, c) = t * (T)0.125;
+}
+
+template <class T>
+__global__ void __launch_bounds__(256) k3l_jac_m2(S3<const T> r, S3<T> v, int H, T cc) {
+  IDX3
+  if (a < 1 || b < 1 || c < 1 || a > H - 2 || b > H - 2 || c > H - 2) return;
+  Sub<T> Bv = sub(v, B);
+  T t = -(cc * r.s[C][(int64_t)c * r.plane + (int64_t)b * r.pitch + a]);
+  t = t + Bv(a, b, c);
+  t = t + Bv(a, b, c - 1);
+  t = t + Bv(a, b - 1, c);
+  t = t + Bv(a, b - 1, c - 1);
+  t = t + Bv(a - 1, b, c);
+  t = t + Bv(a - 1, b, c - 1);
+  t = t + Bv(a - 1, b - 1, c);
+  t = t + Bv(a - 1, b - 1, c - 1);
+  sub(v, C)(a, b, c) = t * (T)0.125;
+}
+
+// ------------------------------------------------- R(s) from M(s): a14
+// Erprolr on the face centres (normal axis = the even
+// coordinate, reading A8; the x- and y-face sums are the cyclic permutations
+// of the printed z-face sum), c1 = 2 p_r1 (sh)^2; then Erprolm on
+// the corners from the new faces, c2 = 4 p_r2 (sh)^2.
+template <class T>
+__global__ void __launch_bounds__(256) k3l_jac_r1(S3<const T> vm, S3<const T> r, S3<T> v, int H, T c1) {
+  IDX3
+  Sub<const T> Cm{vm.s[C], vm.pitch, vm.plane}, Bm{vm.s[B], vm.pitch, vm.plane};
+  const int64_t o = (int64_t)c * r.plane + (int64_t)b * r.pitch + a;
+  const bool lo_a = a <= H - 2, lo_b = b <= H - 2, lo_c = c <= H - 2;
+  // Fx (2a, 2b+1, 2c+1): normal x; in-plane (0,+1,+1),(0,+1,-1),(0,-1,-1),(0,-1,+1)
+  if (a >= 1 && lo_a && lo_b && lo_c) {
+    T nrm = Bm(a, b, c);
+    nrm = nrm + Bm(a - 1, b, c);
+    T t = -(c1 * r.s[FX][o]);
+    t = t + (T)2 * nrm;
+    t = t + Cm(a, b + 1, c + 1);
+    t = t + Cm(a, b + 1, c);
+    t = t + Cm(a, b, c);
+    t = t + Cm(a, b, c + 1);
+    sub(v, FX)(a, b, c) = t * (T)0.125;
+  }
+  // Fy (2a+1, 2b, 2c+1): normal y; in-plane (+1,0,+1),(-1,0,+1),(-1,0,-1),(+1,0,-1)
+  if (b >= 1 && lo_a && lo_b && lo_c) {
+    T nrm = Bm(a, b, c);
+    nrm = nrm + Bm(a, b - 1, c);
+    T t = -(c1 * r.s[FY][o]);
+    t = t + (T)2 * nrm;
+    t = t + Cm(a + 1, b, c + 1);
+    t = t + Cm(a, b, c + 1);
+    t = t + Cm(a, b, c);
+    t = t + Cm(a + 1, b, c);
+    sub(v, FY)(a, b, c) = t * (T)0.125;
+  }
+  // Fz (2a+1, 2b+1, 2c): normal z; in-plane (+1,+1,0),(+1,-1,0),(-1,-1,0),(-1,+1,0)
+  if (c >= 1 && lo_a && lo_b && lo_c) {
+    T nrm = Bm(a, b, c);
+    nrm = nrm + Bm(a, b, c - 1);
+    T t = -(c1 * r.s[FZ][o]);
+    t = t + (T)2 * nrm;
+    t = t + Cm(a + 1, b + 1, c);
+    t = t + Cm(a + 1, b, c);
+    t = t + Cm(a, b, c);
+    t = t + Cm(a, b + 1, c);
+    sub(v, FZ)(a, b, c) = t * (T)0.125;
+  }
+}
+
+template <class T>
+__global__ void __launch_bounds__(256) k3l_jac_r2(S3<const T> r, S3<T> v, int H, T c2) {
+  IDX3
+  if (a < 1 || b < 1 || c < 1 || a > H - 2 || b > H - 2 || c > H - 2) return;
+  Sub<T> Fx = sub(v, FX), Fy = sub(v, FY), Fz = sub(v, FZ);
+  T t = -(c2 * r.s[C][(int64_t)c * r.plane + (int64_t)b * r.pitch + a]);
+  t = t + Fz(a, b, c);              // (+1,+1, 0)
+  t = t + Fz(a, b - 1, c);          // (+1,-1, 0)
+  t = t + Fz(a - 1, b - 1, c);      // (-1,-1, 0)
+  t = t + Fz(a - 1, b, c);          // (-1,+1, 0)
+  t = t + Fy(a, b, c);              // (+1, 0,+1)
+  t = t + Fy(a, b, c - 1);          // (+1, 0,-1)
+  t = t + Fy(a - 1, b, c - 1);      // (-1, 0,-1)
+  t = t + Fy(a - 1, b, c);          // (-1, 0,+1)
+  t = t + Fx(a, b, c);              // ( 0,+1,+1)
+  t = t + Fx(a, b, c - 1);          // ( 0,+1,-1)
+  t = t + Fx(a, b - 1, c - 1);      // ( 0,-1,-1)
+  t = t + Fx(a, b - 1, c);          // ( 0,-1,+1)
+  sub(v, C)(a, b, c) = t * (T)(1.0 / 12.0);
+}
+
+// ------------------------------------------------- G(s) from R(s): a15
+// Egprolg on the green-only nodes of the block (a,b,c):
+// (1,0,0), (0,1,0), (0,0,1), (1,1,1); neighbours i+1, i-1, j+1, j-1, k+1, k-1.
+// FINE: r recomputed from (u_old, f) and the green v kept in `g`.
+template <class T, int ORDER, bool FINE>
+__global__ void __launch_bounds__(256) k3l_jac_g1(S3<const T> vr, D3<const T> rin, D3<const T> u, D3<const T> f,
+                                                  D3<T> g, int M, int H, T cc, Coef<T> k) {
+  IDX3
+  Sub<const T> Cr{vr.s[C], vr.pitch, vr.plane}, Fx{vr.s[FX], vr.pitch, vr.plane}, Fy{vr.s[FY], vr.pitch, vr.plane},
+      Fz{vr.s[FZ], vr.pitch, vr.plane};
+  const int x = 2 * a, y = 2 * b, z = 2 * c;
+  auto rr = [&](int X, int Y, int Z) -> T {
+    if (FINE) return res3<T, ORDER>(u, f, X, Y, Z, k);
+    return rin(X, Y, Z);
+  };
+  auto jac6 = [&](T r, T v0, T v1, T v2, T v3, T v4, T v5) {
+    T t = -(cc * r);
+    t = t + v0;
+    t = t + v1;
+    t = t + v2;
+    t = t + v3;
+    t = t + v4;
+    t = t + v5;
+    return t * (T)(1.0 / 6.0);
+  };
+  const bool in_a = x >= 2 && x <= M - 2, in_b = y >= 2 && y <= M - 2, in_c = z >= 2 && z <= M - 2;
+  const bool od_a = x + 1 <= M - 1, od_b = y + 1 <= M - 1, od_c = z + 1 <= M - 1;
+  if (od_a && in_b && in_c)   // (2a+1, 2b, 2c)
+    g(x + 1, y, z) = jac6(rr(x + 1, y, z), Cr(a + 1, b, c), Cr(a, b, c), Fz(a, b, c), Fz(a, b - 1, c), Fy(a, b, c),
+                          Fy(a, b, c - 1));
+  if (in_a && od_b && in_c)   // (2a, 2b+1, 2c)
+    g(x, y + 1, z) = jac6(rr(x, y + 1, z), Fz(a, b, c), Fz(a - 1, b, c), Cr(a, b + 1, c), Cr(a, b, c), Fx(a, b, c),
+                          Fx(a, b, c - 1));
+  if (in_a && in_b && od_c)   // (2a, 2b, 2c+1)
+    g(x, y, z + 1) = jac6(rr(x, y, z + 1), Fy(a, b, c), Fy(a - 1, b, c), Fx(a, b, c), Fx(a, b - 1, c), Cr(a, b, c + 1),
+                          Cr(a, b, c));
+  if (od_a && od_b && od_c)   // (2a+1, 2b+1, 2c+1)
+    g(x + 1, y + 1, z + 1) = jac6(rr(x + 1, y + 1, z + 1), Fx(a + 1, b, c), Fx(a, b, c), Fy(a, b + 1, c), Fy(a, b, c),
+                                  Fz(a, b, c + 1), Fz(a, b, c));
+}
+
+// Egprolr on the red nodes of the block from the new green
+// values in `g`; FINE: out = u_old + v at all 8 nodes of the block;
+// otherwise out = v_G(s) at the red nodes (the green ones are already in g = out).
+template <class T, int ORDER, bool FINE>
+__global__ void __launch_bounds__(256) k3l_jac_g2(D3<const T> rin, D3<const T> u, D3<const T> f, D3<const T> g,
+                                                  D3<T> out, int M, int H, T cc, Coef<T> k) {
+  IDX3
+  const int x = 2 * a, y = 2 * b, z = 2 * c;
+  auto rr = [&](int X, int Y, int Z) -> T {
+    if (FINE) return res3<T, ORDER>(u, f, X, Y, Z, k);
+    return rin(X, Y, Z);
+  };
+  auto red = [&](int X, int Y, int Z) {
+    T t = -(cc * rr(X, Y, Z));
+    t = t + g(X + 1, Y, Z);
+    t = t + g(X - 1, Y, Z);
+    t = t + g(X, Y + 1, Z);
+    t = t + g(X, Y - 1, Z);
+    t = t + g(X, Y, Z + 1);
+    t = t + g(X, Y, Z - 1);
+    return t * (T)(1.0 / 6.0);
+  };
+  const bool in_a = x >= 2 && x <= M - 2, in_b = y >= 2 && y <= M - 2, in_c = z >= 2 && z <= M - 2;
+  const bool od_a = x + 1 <= M - 1, od_b = y + 1 <= M - 1, od_c = z + 1 <= M - 1;
+  T vC = (in_a && in_b && in_c) ? red(x, y, z) : (T)0;
+  T vFx = (in_a && od_b && od_c) ? red(x, y + 1, z + 1) : (T)0;
+  T vFy = (od_a && in_b && od_c) ? red(x + 1, y, z + 1) : (T)0;
+  T vFz = (od_a && od_b && in_c) ? red(x + 1, y + 1, z) : (T)0;
+  if (FINE) {
+    // u_new = u_old + v on the whole block (green v from g)
+    if (in_a && in_b && in_c) out(x, y, z) = u(x, y, z) + vC;
+    if (in_a && od_b && od_c) out(x, y + 1, z + 1) = u(x, y + 1, z + 1) + vFx;
+    if (od_a && in_b && od_c) out(x + 1, y, z + 1) = u(x + 1, y, z + 1) + vFy;
+    if (od_a && od_b && in_c) out(x + 1, y + 1, z) = u(x + 1, y + 1, z) + vFz;
+    if (od_a && in_b && in_c) out(x + 1, y, z) = u(x + 1, y, z) + g(x + 1, y, z);
+    if (in_a && od_b && in_c) out(x, y + 1, z) = u(x, y + 1, z) + g(x, y + 1, z);
+    if (in_a && in_b && od_c) out(x, y, z + 1) = u(x, y, z + 1) + g(x, y, z + 1);
+    if (od_a && od_b && od_c) out(x + 1, y + 1, z + 1) = u(x + 1, y + 1, z + 1) + g(x + 1, y + 1, z + 1);
+  } else {
+    if (in_a && in_b && in_c) out(x, y, z) = vC;
+    if (in_a && od_b && od_c) out(x, y + 1, z + 1) = vFx;
+    if (od_a && in_b && od_c) out(x + 1, y, z + 1) = vFy;
+    if (od_a && od_b && in_c) out(x + 1, y + 1, z) = vFz;
+  }
+}
+
+#undef IDX3
+
+// ================================================================ launchers
+static inline dim3 grid3(int H) { return dim3((H + 31) / 32, (H + 7) / 8, H); }
+static const dim3 kBlk(32, 8);
+
+template <class T>
+static D3<const T> cd3(const D3<T> &a) {
+  return D3<const T>{a.p, a.pitch, a.plane};
+}
+template <class T>
+static S3<const T> cs3(const S3<T> &a) {
+  S3<const T> o;
+  for (int i = 0; i < 8; i++) o.s[i] = a.s[i];
+  o.pitch = a.pitch;
+  o.plane = a.plane;
+  return o;
+}
+
+template <class T>
+void lv3_rest_gr(const D3<T> &r, const S3<T> &rr, int M, cudaStream_t st) {
+  int H = M / 2 + 1;
+  k3l_rest_gr<T><<<grid3(H), kBlk, 0, st>>>(cd3(r), rr, M, H);
+}
+template <class T>
+void lv3_rest_rm(const S3<T> &rr, const S3<T> &rm, int M, cudaStream_t st) {
+  int H = M / 2 + 1;
+  k3l_rest_rm<T><<<grid3(H), kBlk, 0, st>>>(cs3(rr), rm, H);
+}
+template <class T>
+void lv3_rest_mg(const S3<T> &rm, const D3<T> &g2, int Mc, cudaStream_t st) {
+  k3l_rest_mg<T><<<grid3(Mc + 1), kBlk, 0, st>>>(cs3(rm), g2, Mc);
+}
+template <class T>
+void lv3_jac_m(const D3<T> &vc, const S3<T> &r, const S3<T> &v, int M, T c, cudaStream_t st) {
+  int H = M / 2 + 1;
+  k3l_jac_m1<T><<<grid3(H), kBlk, 0, st>>>(cd3(vc), cs3(r), v, H, c);
+  k3l_jac_m2<T><<<grid3(H), kBlk, 0, st>>>(cs3(r), v, H, c);
+}
+template <class T>
+void lv3_jac_r(const S3<T> &vm, const S3<T> &r, const S3<T> &v, int M, T c1, T c2, cudaStream_t st) {
+  int H = M / 2 + 1;
+  k3l_jac_r1<T><<<grid3(H), kBlk, 0, st>>>(cs3(vm), cs3(r), v, H, c1);
+  k3l_jac_r2<T><<<grid3(H), kBlk, 0, st>>>(cs3(r), v, H, c2);
+}
+template <class T>
+void lv3_jac_g(const S3<T> &vr, const D3<T> &r, const D3<T> &v, int M, T c, cudaStream_t st) {
+  int H = M / 2 + 1;
+  Coef<T> k{};
+  D3<const T> none{nullptr, 0, 0};
+  k3l_jac_g1<T, 2, false><<<grid3(H), kBlk, 0, st>>>(cs3(vr), cd3(r), none, none, v, M, H, c, k);
+  k3l_jac_g2<T, 2, false><<<grid3(H), kBlk, 0, st>>>(cd3(r), none, none, cd3(v), v, M, H, c, k);
+}
+template <class T>
+void lv3_asc_fine(const S3<T> &vr, const D3<T> &u_old, const D3<const T> &f, const D3<T> &g, const D3<T> &u_new, int M,
+                  int order, T c, const Coef<T> &k, cudaStream_t st) {
+  int H = M / 2 + 1;
+  D3<const T> none{nullptr, 0, 0};
+  if (order == 2) {
+    k3l_jac_g1<T, 2, true><<<grid3(H), kBlk, 0, st>>>(cs3(vr), none, cd3(u_old), f, g, M, H, c, k);
+    k3l_jac_g2<T, 2, true><<<grid3(H), kBlk, 0, st>>>(none, cd3(u_old), f, cd3(g), u_new, M, H, c, k);
+  } else {
+    k3l_jac_g1<T, 4, true><<<grid3(H), kBlk, 0, st>>>(cs3(vr), none, cd3(u_old), f, g, M, H, c, k);
+    k3l_jac_g2<T, 4, true><<<grid3(H), kBlk, 0, st>>>(none, cd3(u_old), f, cd3(g), u_new, M, H, c, k);
+  }
+}
+
+#define INSTL(T)                                                                                                   \
+  template void lv3_rest_gr<T>(const D3<T> &, const S3<T> &, int, cudaStream_t);                                   \
+  template void lv3_rest_rm<T>(const S3<T> &, const S3<T> &, int, cudaStream_t);                                   \
+  template void lv3_rest_mg<T>(const S3<T> &, const D3<T> &, int, cudaStream_t);                                   \
+  template void lv3_jac_m<T>(const D3<T> &, const S3<T> &, const S3<T> &, int, T, cudaStream_t);                   \
+  template void lv3_jac_r<T>(const S3<T> &, const S3<T> &, const S3<T> &, int, T, T, cudaStream_t);                \
+  template void lv3_jac_g<T>(const S3<T> &, const D3<T> &, const D3<T> &, int, T, cudaStream_t);                   \
+  template void lv3_asc_fine<T>(const S3<T> &, const D3<T> &, const D3<const T> &, const D3<T> &, const D3<T> &,   \
+                                int, int, T, const Coef<T> &, cudaStream_t);
+
+INSTL(float)
+INSTL(double)
+
+}  // namespace mg

@@ -85,6 +85,26 @@ void launch3_residual(const D3<const T> &u, const D3<const T> &f, const D3<T> &r
                       cudaStream_t st);
 template <class T>
 void launch3_ftilde(const D3<const T> &f, const D3<T> &ft, int M, cudaStream_t st);
+// TMA plane-streaming kernels (k3f.cu); 16-byte aligned pointers and pitches.
+template <class T>
+cudaError_t fast3_desc_fine(const T *u, const T *f, int64_t pitch, const S3<T> &rr, int M, int order, const Coef<T> &k,
+                            const NormSink &ns, cudaStream_t st);
+// Sublattice level kernels (k3l.cu).
+template <class T>
+void lv3_rest_gr(const D3<T> &r, const S3<T> &rr, int M, cudaStream_t st);
+template <class T>
+void lv3_rest_rm(const S3<T> &rr, const S3<T> &rm, int M, cudaStream_t st);
+template <class T>
+void lv3_rest_mg(const S3<T> &rm, const D3<T> &g2, int Mc, cudaStream_t st);
+template <class T>
+void lv3_jac_m(const D3<T> &vc, const S3<T> &r, const S3<T> &v, int M, T c, cudaStream_t st);
+template <class T>
+void lv3_jac_r(const S3<T> &vm, const S3<T> &r, const S3<T> &v, int M, T c1, T c2, cudaStream_t st);
+template <class T>
+void lv3_jac_g(const S3<T> &vr, const D3<T> &r, const D3<T> &v, int M, T c, cudaStream_t st);
+template <class T>
+void lv3_asc_fine(const S3<T> &vr, const D3<T> &u_old, const D3<const T> &f, const D3<T> &g, const D3<T> &u_new, int M,
+                  int order, T c, const Coef<T> &k, cudaStream_t st);
 template <class T>
 void launch3_norm(const D3<const T> &a, int M, unsigned long long *mx, double *ss, cudaStream_t st);
 

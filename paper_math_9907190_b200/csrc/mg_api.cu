@@ -364,7 +364,9 @@ struct Impl3 : ImplBase {
   D3<T> scratch{};
   Coef<T> coef{};
   std::vector<T> cMg, cR1, cR2, cG;
+  bool use_fast = false;   // TMA plane kernels for the finest octave
   explicit Impl3(const mg_solver *sv) : s(sv), k(sv->k), n(sv->cfg.n), pitch(sv->pitch) {}
+  bool fast() const override { return use_fast; }
   int64_t pitch_for(int64_t cnt) const { return round_up(cnt, 128 / (int64_t)sizeof(T)); }
 
   cudaError_t split(S3<T> &out, int64_t H, std::initializer_list<int> parities) {
@@ -430,10 +432,17 @@ struct Impl3 : ImplBase {
     }
     coef.invh2 = (T)((double)(n - 1) * (double)(n - 1));
     coef.c6 = (T)((double)(n - 1) * (double)(n - 1) / 6.0);
+    use_fast = ((pitch * (int64_t)sizeof(T)) % 16 == 0) && !getenv("MG_FORCE_REF");
     return cudaSuccess;
   }
 
   NormSink sink() const { return NormSink{s->d_hist, s->d_counter, kHistCap}; }
+  void desc_fine(const void *u, const void *f_eff, cudaStream_t st) {
+    if (use_fast && ((uintptr_t)u & 15) == 0 && ((uintptr_t)f_eff & 15) == 0)
+      fast3_desc_fine<T>((const T *)u, (const T *)f_eff, pitch, rR[0], M[0], s->cfg.order, coef, sink(), st);
+    else
+      launch3_desc_fine<T>(cfield(u), cfield(f_eff), rR[0], M[0], s->cfg.order, coef, sink(), st);
+  }
   D3<const T> cfield(const void *a) const { return D3<const T>{(const T *)a, pitch, pitch * n}; }
   D3<T> field(void *a) const { return D3<T>{(T *)a, pitch, pitch * n}; }
 
@@ -442,29 +451,38 @@ struct Impl3 : ImplBase {
     const int L = 3 * k - 2;
     void *u = const_cast<void *>(u_in);
     STEP("desc_fine", 0, 1, w * (2 * Nl[0] + Nl[1]));
-    launch3_desc_fine<T>(cfield(u), cfield(f_eff), rR[0], M[0], s->cfg.order, coef, sink(), st);
+    desc_fine(u, f_eff, st);
     for (int o = 0; o + 1 < k; o++) {
       int g = 3 * o;
       if (o >= 1) {
         STEP("rest_gr", g, 1, w * (Nl[g] + Nl[g + 1]));
-        launch3_rest_gr<T>(rG[o], rR[o], M[o], st);
+        if (use_fast) lv3_rest_gr<T>(rG[o], rR[o], M[o], st);
+        else launch3_rest_gr<T>(rG[o], rR[o], M[o], st);
       }
       STEP("rest_rm", g + 1, 1, w * (Nl[g + 1] + Nl[g + 2]));
-      launch3_rest_rm<T>(rR[o], rM[o], M[o], st);
+      if (use_fast) lv3_rest_rm<T>(rR[o], rM[o], M[o], st);
+      else launch3_rest_rm<T>(rR[o], rM[o], M[o], st);
       STEP("rest_mg", g + 2, 1, w * (Nl[g + 2] + Nl[g + 3]));
-      launch3_rest_mg<T>(rM[o], rG[o + 1], M[o + 1], st);
+      if (use_fast) lv3_rest_mg<T>(rM[o], rG[o + 1], M[o + 1], st);
+      else launch3_rest_mg<T>(rM[o], rG[o + 1], M[o + 1], st);
     }
     STEP("coarsest", L - 1, 1, w * 2);
     launch3_coarsest<T>(rG[k - 1], vG[k - 1], cG[k - 1], s->d_counter, st);
     for (int o = k - 2; o >= 0; o--) {
       int g = 3 * o;
       STEP("jac_m", g + 2, 2, w * (Nl[g + 3] + 2 * Nl[g + 2]));
-      launch3_jac_m<T>(vG[o + 1], rM[o], vM[o], M[o], cMg[o], st);
+      if (use_fast) lv3_jac_m<T>(vG[o + 1], rM[o], vM[o], M[o], cMg[o], st);
+      else launch3_jac_m<T>(vG[o + 1], rM[o], vM[o], M[o], cMg[o], st);
       STEP("jac_r", g + 1, 2, w * (Nl[g + 2] + 2 * Nl[g + 1]));
-      launch3_jac_r<T>(vM[o], rR[o], vR[o], M[o], cR1[o], cR2[o], st);
+      if (use_fast) lv3_jac_r<T>(vM[o], rR[o], vR[o], M[o], cR1[o], cR2[o], st);
+      else launch3_jac_r<T>(vM[o], rR[o], vR[o], M[o], cR1[o], cR2[o], st);
       if (o >= 1) {
         STEP("jac_g", g, 2, w * (Nl[g + 1] + 2 * Nl[g]));
-        launch3_jac_g<T>(vR[o], rG[o], vG[o], M[o], cG[o], st);
+        if (use_fast) lv3_jac_g<T>(vR[o], rG[o], vG[o], M[o], cG[o], st);
+        else launch3_jac_g<T>(vR[o], rG[o], vG[o], M[o], cG[o], st);
+      } else if (use_fast) {
+        STEP("asc_fine", 0, 2, w * (Nl[1] + 3 * Nl[0]));
+        lv3_asc_fine<T>(vR[0], field(u), cfield(f_eff), scratch, field(u_out), M[0], s->cfg.order, cG[0], coef, st);
       } else {
         STEP("asc_fine", 0, 3, w * (Nl[1] + 3 * Nl[0]));
         launch3_asc_fine<T>(vR[0], field(u), cfield(f_eff), scratch, field(u_out), M[0], s->cfg.order, cG[0], coef,
@@ -472,9 +490,7 @@ struct Impl3 : ImplBase {
       }
     }
   }
-  void enqueue_final_norm(void *u, const void *f_eff, cudaStream_t st) override {
-    launch3_desc_fine<T>(cfield(u), cfield(f_eff), rR[0], M[0], s->cfg.order, coef, sink(), st);
-  }
+  void enqueue_final_norm(void *u, const void *f_eff, cudaStream_t st) override { desc_fine(u, f_eff, st); }
   void enqueue_residual(const void *u, const void *f, void *r, cudaStream_t st) override {
     launch3_residual<T>(cfield(u), cfield(f), field(r), M[0], s->cfg.order, coef, st);
   }
@@ -488,7 +504,7 @@ struct Impl3 : ImplBase {
     int c = 1;
     for (int o = 0; o + 1 < k; o++) c += (o >= 1) + 2;
     c += 1;
-    for (int o = k - 2; o >= 0; o--) c += 2 + 2 + ((o >= 1) ? 2 : 3);
+    for (int o = k - 2; o >= 0; o--) c += 2 + 2 + ((o >= 1) ? 2 : (use_fast ? 2 : 3));
     return c;
   }
 };
