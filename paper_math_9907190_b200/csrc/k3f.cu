@@ -140,26 +140,31 @@ __device__ __forceinline__ bool inside3(int x, int y, int z, int M) {
   return x >= 1 && y >= 1 && z >= 1 && x <= M - 1 && y <= M - 1 && z <= M - 1;
 }
 
-constexpr int TX3 = 64, TY3 = 16, NT3F = 512, NW3 = NT3F / 32, ZC = 64;
+// Balanced plane geometry: lane l owns the column pair (x0-2+2l, x0-1+2l), so
+// the 32 lanes cover r on [x0-2, x0+62) and the output tile is the TX3 = 60
+// columns [x0, x0+60); warp w computes r on row y0-1+w (TY3 + 2 = 16 rows,
+// one per warp) and writes the outputs of row y0+w (w < TY3).  Every warp
+// does the same work; no separate ring pass.
+constexpr int TX3 = 60, TY3 = 14, NT3F = 512, NW3 = NT3F / 32, ZC = 64;
+static_assert(TY3 + 2 == NW3, "one r row per warp");
 
 struct Unit3 {
   int x0, y0, zs, ze, pb, pe;
 };
 
 // ============================================== finest descent a9 + a10
-// r = f - L u (7-point or Efos4) on the tile plus its xy ring, plane by plane,
-// kept in a 3-plane ring; Erred onto the four red sublattices of R(1).
+// r = f - L u (7-point or Efos4) on the tile plus its ring, plane by plane,
+// kept in a 4-plane ring; Erred onto the four red sublattices of R(1).
 // Load L_p holds u(p+1) and f(p); step p computes r(p) (needs L_{p-2..p})
-// and writes the red nodes of plane p-1 (needs r(p-2..p)).
+// and writes the red nodes of plane p-2 (from r(p-3..p-1), computed by
+// earlier steps: one barrier per step).
 template <class T, int ORDER>
 struct OpDesc3Fine {
   static constexpr int NT = NT3F, NS = 7, D = 3, LAFTER = 2;
-  static constexpr int HU = hx<T>(2), HF = hx<T>(1);
-  static constexpr int UW = w16<T>(TX3 + HU + 2), UH = TY3 + 4, FW = w16<T>(TX3 + HF + 1), FH = TY3 + 2;
-  // r planes are stored de-interleaved: per row [even x | odd x], each
-  // TX/2 + 2 entries (column pair index -1 .. TX/2), so a lane's node and its
-  // x-neighbours are unit-stride across the warp
-  static constexpr int RH2 = TX3 / 2 + 2, RW = 2 * RH2, RH = TY3 + 2;
+  static constexpr int HX = hx<T>(3);   // u and f boxes start at x0 - HX (16-byte aligned)
+  static constexpr int UW = w16<T>(64 + HX), UH = TY3 + 4, FW = w16<T>(64 + HX), FH = TY3 + 2;
+  // r planes de-interleaved: per row [even columns x0-2+2l | odd columns x0-1+2l], l = 0..31
+  static constexpr int RH2 = 32, RW = 2 * RH2, RH = TY3 + 2;
   static constexpr int U_BYTES = UW * UH * sizeof(T), F_BYTES = FW * FH * sizeof(T);
   static constexpr int U_OFF = 0, F_OFF = al128(U_BYTES);
   static constexpr int SLOT = al128(F_OFF + F_BYTES);
@@ -182,7 +187,6 @@ struct OpDesc3Fine {
     tma_prefetch_desc(&P.tf);
   }
   static __device__ void init(Acc &a) { a.mx = 0.0; }
-  // step p computes r(p) and writes the red nodes of plane p-2 (from r(p-3..p-1))
   static __device__ __forceinline__ Unit decode(const Params &P, int u) {
     int tx = u % P.ntx, r = u / P.ntx, ty = r % P.nty, zc = r / P.nty;
     Unit un;
@@ -196,8 +200,8 @@ struct OpDesc3Fine {
   }
   static __device__ void issue(const Params &P, const Unit &un, int p, unsigned char *slot, uint64_t *bar) {
     mbar_expect_tx(bar, U_BYTES + F_BYTES);
-    tma_load_3d(slot + U_OFF, &P.tu, un.x0 - HU, un.y0 - 2, p + 1, bar);
-    tma_load_3d(slot + F_OFF, &P.tf, un.x0 - HF, un.y0 - 1, p, bar);
+    tma_load_3d(slot + U_OFF, &P.tu, un.x0 - HX, un.y0 - 2, p + 1, bar);
+    tma_load_3d(slot + F_OFF, &P.tf, un.x0 - HX, un.y0 - 1, p, bar);
   }
   // residuals at (xl, y, z) and (xl+1, y, z); um/uc/up point at u(xl, y) of
   // planes z-1, z, z+1 in their slots, ff at f(xl, y).
@@ -242,59 +246,34 @@ struct OpDesc3Fine {
   }
   static __device__ void step(const Params &P, const Unit &un, int p, unsigned char *const sl[3], unsigned char *scr,
                               Acc &acc) {
-    const int M = P.M, lane = threadIdx.x & 31, w = threadIdx.x >> 5, xl = un.x0 + 2 * lane;
-    const int x0 = un.x0, y0 = un.y0;
-    auto rbase = [&](int z) { return (T *)(scr + (z & (NR - 1)) * RPL); };   // z >= -3 -> (z & 3) is a valid slot
-    auto uo = [&](int x, int y) { return (y - (y0 - 2)) * UW + (x - (x0 - HU)); };
-    auto fo = [&](int x, int y) { return (y - (y0 - 1)) * FW + (x - (x0 - HF)); };
-    // de-interleaved r: row y, column x -> [ (x&1) * RH2 + (x - x0) / 2 + 1 ]
-    auto rro = [&](int x, int y) { return (y - (y0 - 1)) * RW + (x & 1) * RH2 + ((x - x0) >> 1) + 1; };
+    const int M = P.M, lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int x0 = un.x0, y0 = un.y0, xl = x0 - 2 + 2 * lane;
+    auto rbase = [&](int z) { return (T *)(scr + (z & (NR - 1)) * RPL); };   // z >= -3: (z & 3) is the slot
     if (p >= un.zs - 1 && p <= un.ze) {
-      const T *Up = (const T *)(sl[0] + U_OFF), *Uc = (const T *)(sl[1] + U_OFF), *Um = (const T *)(sl[2] + U_OFF);
-      const T *F = (const T *)(sl[0] + F_OFF);
-      T *R = rbase(p + 4);
-      const bool own = p >= un.zs && p < un.ze;
-      const bool zin = p >= 1 && p <= M - 1, xin0 = xl >= 1 && xl <= M - 1, xin1 = xl + 1 <= M - 1;
+      const int y = y0 - 1 + w;
+      const int uoff = (y - (y0 - 2)) * UW + (xl - (x0 - HX)), foff = (y - (y0 - 1)) * FW + (xl - (x0 - HX));
+      const T *Up = (const T *)(sl[0] + U_OFF) + uoff, *Uc = (const T *)(sl[1] + U_OFF) + uoff,
+              *Um = (const T *)(sl[2] + U_OFF) + uoff;
+      const T *F = (const T *)(sl[0] + F_OFF) + foff;
+      const bool yin = p >= 1 && p <= M - 1 && y >= 1 && y <= M - 1;
       T r0, r1;
-#pragma unroll
-      for (int j = 0; j < TY3 / NW3; j++) {
-        int y = y0 + w + j * NW3;
-        bool yin = zin && y >= 1 && y <= M - 1;
-        int o = uo(xl, y);
-        rpair(Um + o, Uc + o, Up + o, F + fo(xl, y), yin && xin0, yin && xin1, P.k, r0, r1);
-        int ro = rro(xl, y);
-        R[ro] = r0;
-        R[ro + RH2] = r1;
-        if (own) acc.mx = nmax(nmax(acc.mx, absd(r0)), absd(r1));
-      }
-      if (w < 2) {
-        int y = w == 0 ? y0 - 1 : y0 + TY3;
-        bool yin = zin && y >= 1 && y <= M - 1;
-        int o = uo(xl, y);
-        rpair(Um + o, Uc + o, Up + o, F + fo(xl, y), yin && xin0, yin && xin1, P.k, r0, r1);
-        int ro = rro(xl, y);
-        R[ro] = r0;
-        R[ro + RH2] = r1;
-      } else if (w == 2) {
-        int x = lane < 16 ? x0 - 1 : x0 + TX3, y = y0 + (lane & 15);
-        Planes3<T> U3{STile<T>{(T *)Um, UW, x0 - HU, y0 - 2}, STile<T>{(T *)Uc, UW, x0 - HU, y0 - 2},
-                      STile<T>{(T *)Up, UW, x0 - HU, y0 - 2}, p};
-        Plane1<T> F1{STile<T>{(T *)F, FW, x0 - HF, y0 - 1}};
-        R[rro(x, y)] = inside3(x, y, p, M) ? res3<T, ORDER>(U3, F1, x, y, p, P.k) : (T)0;
-      }
+      rpair(Um, Uc, Up, F, yin && xl >= 1 && xl <= M - 1, yin && xl >= 0 && xl + 1 <= M - 1, P.k, r0, r1);
+      T *R = rbase(p + 4) + w * RW + lane;
+      R[0] = r0;
+      R[RH2] = r1;
+      // norm: every interior node once -- the tile core on the unit's own planes
+      if (p >= un.zs && p < un.ze && w >= 1 && w <= TY3 && lane >= 1 && lane <= TX3 / 2)
+        acc.mx = nmax(nmax(acc.mx, absd(r0)), absd(r1));
     }
     const int q = p - 2;   // r(q-1), r(q), r(q+1) were completed in earlier steps
-    if (q >= un.zs && q < un.ze && q >= 1 && q <= M - 1) {
-      const T *Rm = rbase(q + 3), *Rc = rbase(q + 4), *Rp = rbase(q + 5);
-#pragma unroll
-      for (int j = 0; j < TY3 / NW3; j++) {
-        int y = y0 + w + j * NW3;
-        int par = (y + q) & 1, x = xl + par;
-        if (!inside3(x, y, q, M)) continue;
-        int o = rro(x, y);                           // the node
-        int oo = (y - (y0 - 1)) * RW + (1 - par) * RH2 + lane + 1;   // x-neighbour column block
+    if (w < TY3 && q >= un.zs && q < un.ze && q >= 1 && q <= M - 1) {
+      const int y = y0 + w, par = (y + q) & 1, x = xl + par;
+      if (lane >= 1 && lane <= TX3 / 2 && x >= 1 && x <= M - 1 && y >= 1 && y <= M - 1) {
+        const int row = (w + 1) * RW;   // r row of y
+        const T *Rm = rbase(q + 3) + row, *Rc = rbase(q + 4) + row, *Rp = rbase(q + 5) + row;
+        const int o = par * RH2 + lane, oo = (1 - par) * RH2 + lane + par;
         // Erred: i+1, i-1, j+1, j-1, k+1, k-1
-        T nb[6] = {Rc[oo + par], Rc[oo + par - 1], Rc[o + RW], Rc[o - RW], Rp[o], Rm[o]};
+        T nb[6] = {Rc[oo], Rc[oo - 1], Rc[o + RW], Rc[o - RW], Rp[o], Rm[o]};
         P.out.ref(x, y, q) = erred(Rc[o], nb);
       }
     }
