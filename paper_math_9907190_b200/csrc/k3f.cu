@@ -115,20 +115,25 @@ __global__ void __launch_bounds__(Op::NT, 1) plane_pipeline(const __grid_constan
     pp = pun.pb;
     for (int j = 0; j <= D && pu < nunits; j++) produce();
   }
-  int s0 = 0, s1 = NS - 1, s2 = NS - 2;   // slots of loads g, g-1, g-2
+  constexpr int NB = Op::LAFTER + 1;     // slots of loads g, g-1, ..., g-LAFTER
+  int sidx[NB];
+#pragma unroll
+  for (int j = 0; j < NB; j++) sidx[j] = (NS - j) % NS;
   uint32_t phase = 0;
   for (int u = blockIdx.x; u < nunits; u += gridDim.x) {
     const typename Op::Unit un = Op::decode(P, u);
     for (int p = un.pb; p < un.pe; p++) {
       if (threadIdx.x == 0 && pu < nunits) produce();
-      mbar_wait(&bar[s0], phase);
-      unsigned char *sl[3] = {smem + s0 * Op::SLOT, smem + s1 * Op::SLOT, smem + s2 * Op::SLOT};
+      mbar_wait(&bar[sidx[0]], phase);
+      unsigned char *sl[NB];
+#pragma unroll
+      for (int j = 0; j < NB; j++) sl[j] = smem + sidx[j] * Op::SLOT;
       Op::step(P, un, p, sl, smem + NS * Op::SLOT, acc);
       __syncthreads();
-      s2 = s1;
-      s1 = s0;
-      if (++s0 == NS) {
-        s0 = 0;
+#pragma unroll
+      for (int j = NB - 1; j > 0; j--) sidx[j] = sidx[j - 1];
+      if (++sidx[0] == NS) {
+        sidx[0] = 0;
         phase ^= 1;
       }
     }
@@ -244,7 +249,7 @@ struct OpDesc3Fine {
     r0 = in0 ? res3v<T, ORDER>(a, f0, k) : (T)0;
     r1 = in1 ? res3v<T, ORDER>(b, f1, k) : (T)0;
   }
-  static __device__ void step(const Params &P, const Unit &un, int p, unsigned char *const sl[3], unsigned char *scr,
+  static __device__ void step(const Params &P, const Unit &un, int p, unsigned char *const *sl, unsigned char *scr,
                               Acc &acc) {
     const int M = P.M, lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const int x0 = un.x0, y0 = un.y0, xl = x0 - 2 + 2 * lane;
@@ -279,6 +284,163 @@ struct OpDesc3Fine {
     }
   }
   static __device__ void finish(const Params &P, Acc &acc) { block_norm_push<NT>(P.ns, acc.mx); }
+};
+
+// ============================================== finest ascent a15 (s = 1)
+// Egprolg on the green-only nodes, Egprolr on the red
+// nodes, both with r = f - L u recomputed from u_old, then u_new = u_old + v
+// (P:57-60), in one pass.  Load L_p holds u(p+1), f(p) and the two red
+// sublattices of fine plane p+1; step p computes the green values G(p) (a
+// 4-plane ring) and finishes plane q = p-2 (red values from G(q-1..q+1),
+// u_new of every node).  One barrier per step.
+template <class T, int ORDER>
+struct OpAsc3Fine {
+  static constexpr int NT = NT3F, NS = 8, D = 2, LAFTER = 4;
+  static constexpr int AL = 16 / (int)sizeof(T);   // TMA x alignment in elements
+  static constexpr int HX = hx<T>(3);
+  static constexpr int UW = w16<T>(64 + HX), UH = TY3 + 4, FW = w16<T>(64 + HX), FH = TY3 + 2;
+  static constexpr int VW = w16<T>(34 + AL - 1), VH = TY3 / 2 + 2;
+  static constexpr int U_BYTES = UW * UH * sizeof(T), F_BYTES = FW * FH * sizeof(T), V_BYTES = VW * VH * sizeof(T);
+  static constexpr int U_OFF = 0, F_OFF = al128(U_BYTES), V0_OFF = F_OFF + al128(F_BYTES),
+                       V1_OFF = V0_OFF + al128(V_BYTES);
+  static constexpr int SLOT = al128(V1_OFF + V_BYTES);
+  static constexpr int GH2 = 32, GW = 2 * GH2, GR = TY3 + 2;
+  static constexpr int GPL = al128(GW * GR * sizeof(T));
+  static constexpr int NR = 4;
+  static constexpr int SMEM = NS * SLOT + NR * GPL;
+  struct Params {
+    CUtensorMap tu, tf, tv[4];   // tv: red sublattices C, Fx, Fy, Fz of v_R(1)
+    D3<T> out;
+    int M, ntx, nty, nunits;
+    T c;
+    Coef<T> k;
+  };
+  using Unit = Unit3;
+  struct Acc {};
+  static __device__ void prefetch(const Params &P) {
+    tma_prefetch_desc(&P.tu);
+    tma_prefetch_desc(&P.tf);
+    for (int i = 0; i < 4; i++) tma_prefetch_desc(&P.tv[i]);
+  }
+  static __device__ void init(Acc &) {}
+  static __device__ __forceinline__ Unit decode(const Params &P, int u) {
+    int tx = u % P.ntx, r = u / P.ntx, ty = r % P.nty, zc = r / P.nty;
+    Unit un;
+    un.x0 = tx * TX3;
+    un.y0 = ty * TY3;
+    un.zs = zc * ZC;
+    un.ze = min(un.zs + ZC, P.M);
+    un.pb = un.zs - 3;
+    un.pe = un.ze + 2;
+    return un;
+  }
+  static __device__ __forceinline__ int vx0(int x0) { return (x0 / 2 - 2) & ~(AL - 1); }   // V box x origin
+  static __device__ void issue(const Params &P, const Unit &un, int p, unsigned char *slot, uint64_t *bar) {
+    mbar_expect_tx(bar, U_BYTES + F_BYTES + 2 * V_BYTES);
+    tma_load_3d(slot + U_OFF, &P.tu, un.x0 - HX, un.y0 - 2, p + 1, bar);
+    tma_load_3d(slot + F_OFF, &P.tf, un.x0 - HX, un.y0 - 1, p, bar);
+    // fine plane z = p+1: even z -> C (even x) and Fz (odd x) at half plane z/2;
+    // odd z -> Fx (even x) and Fy (odd x) at half plane (z-1)/2
+    const int z = p + 1, hz = z >> 1;
+    const CUtensorMap *m0 = (z & 1) ? &P.tv[1] : &P.tv[0];
+    const CUtensorMap *m1 = (z & 1) ? &P.tv[2] : &P.tv[3];
+    tma_load_3d(slot + V0_OFF, m0, vx0(un.x0), un.y0 / 2 - 1, hz, bar);
+    tma_load_3d(slot + V1_OFF, m1, vx0(un.x0), un.y0 / 2 - 1, hz, bar);
+  }
+  static __device__ void step(const Params &P, const Unit &un, int p, unsigned char *const *sl, unsigned char *scr,
+                              Acc &) {
+    const int M = P.M, lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int x0 = un.x0, y0 = un.y0, xl = x0 - 2 + 2 * lane, vx = vx0(x0), vy = y0 / 2 - 1;
+    const T c = P.c;
+    auto gbase = [&](int z) { return (T *)(scr + (z & (NR - 1)) * GPL); };
+    // element offset of (x, y) in the u / f boxes, of half-index (a, b) in a V box
+    auto uo = [&](int x, int y) { return (y - (y0 - 2)) * UW + (x - (x0 - HX)); };
+    auto fo = [&](int x, int y) { return (y - (y0 - 1)) * FW + (x - (x0 - HX)); };
+    auto vo = [&](int a, int b) { return (b - vy) * VW + (a - vx); };
+    auto vr = [&](unsigned char *slot, int x, int y) {   // v_R at the red node (x, y) of the slot's plane
+      return ((const T *)(slot + ((x & 1) ? V1_OFF : V0_OFF)))[vo(x >> 1, y >> 1)];
+    };
+    auto resid = [&](const T *um, const T *uc, const T *up, T f) {   // pointers at u(x, y) of planes z-1, z, z+1
+      Nb19<T> q;
+      q.c = uc[0];
+      q.xp = uc[1];
+      q.xm = uc[-1];
+      q.yp = uc[UW];
+      q.ym = uc[-UW];
+      q.zp = up[0];
+      q.zm = um[0];
+      if (ORDER == 4) {
+        q.xpyp = uc[UW + 1];
+        q.xmyp = uc[UW - 1];
+        q.xmym = uc[-UW - 1];
+        q.xpym = uc[-UW + 1];
+        q.ypzp = up[UW];
+        q.ypzm = um[UW];
+        q.ymzm = um[-UW];
+        q.ymzp = up[-UW];
+        q.xpzp = up[1];
+        q.xmzp = up[-1];
+        q.xmzm = um[-1];
+        q.xpzm = um[1];
+      }
+      return res3v<T, ORDER>(q, f, P.k);
+    };
+    auto jac6 = [&](T r, T v0, T v1, T v2, T v3, T v4, T v5) {
+      T t = -(c * r);
+      t = t + v0;
+      t = t + v1;
+      t = t + v2;
+      t = t + v3;
+      t = t + v4;
+      t = t + v5;
+      return t * (T)(1.0 / 6.0);
+    };
+    // ---- colour 1: green values of plane p on rows y0-1 .. y0+TY3
+    if (p >= un.zs - 1 && p <= un.ze) {
+      const int y = y0 - 1 + w, xg = xl + ((y + p + 1) & 1);
+      T g = (T)0;
+      if (p >= 1 && p <= M - 1 && y >= 1 && y <= M - 1 && xg >= 1 && xg <= M - 1) {
+        const int o = uo(xg, y);
+        const T r = resid((const T *)(sl[2] + U_OFF) + o, (const T *)(sl[1] + U_OFF) + o,
+                          (const T *)(sl[0] + U_OFF) + o, ((const T *)(sl[0] + F_OFF))[fo(xg, y)]);
+        // i+1, i-1, j+1, j-1, k+1, k-1: red neighbours; v_R(p) in L_{p-1}, v_R(p+1) in L_p, v_R(p-1) in L_{p-2}
+        g = jac6(r, vr(sl[1], xg + 1, y), vr(sl[1], xg - 1, y), vr(sl[1], xg, y + 1), vr(sl[1], xg, y - 1),
+                 vr(sl[0], xg, y), vr(sl[2], xg, y));
+      }
+      gbase(p + 4)[(xg & 1) * GH2 + w * GW + lane] = g;
+    }
+    // ---- colour 2 + update on plane q = p-2
+    const int q = p - 2;
+    if (w < TY3 && lane >= 1 && lane <= TX3 / 2 && q >= un.zs && q < un.ze && q >= 1 && q <= M - 1) {
+      const int y = y0 + w;
+      if (y >= 1 && y <= M - 1) {
+        const int par = (y + q) & 1, xr = xl + par;   // red node of the pair
+        const int row = (w + 1) * GW;
+        const T *Gm = gbase(q + 3) + row, *Gc = gbase(q + 4) + row, *Gp = gbase(q + 5) + row;
+        const int o = par * GH2 + lane, oo = (1 - par) * GH2 + lane + par;
+        const T vg = Gc[oo - par];   // the pair's green node (x = xl + 1 - par): index lane in block 1-par
+        T vrd = (T)0;
+        if (xr >= 1 && xr <= M - 1) {
+          const int uoff = uo(xr, y);
+          const T r = resid((const T *)(sl[4] + U_OFF) + uoff, (const T *)(sl[3] + U_OFF) + uoff,
+                            (const T *)(sl[2] + U_OFF) + uoff, ((const T *)(sl[2] + F_OFF))[fo(xr, y)]);
+          vrd = jac6(r, Gc[oo], Gc[oo - 1], Gc[o + GW], Gc[o - GW], Gp[o], Gm[o]);
+        }
+        T u0, u1;
+        ld2((const T *)(sl[3] + U_OFF) + uo(xl, y), u0, u1);
+        const T v0 = par ? vg : vrd, v1 = par ? vrd : vg;
+        const bool ok0 = xl >= 1, ok1 = xl + 1 <= M - 1;
+        T *dst = &P.out(xl, y, q);
+        if (ok0 && ok1)
+          st2(dst, u0 + v0, u1 + v1);
+        else {
+          if (ok0 && xl <= M - 1) dst[0] = u0 + v0;
+          if (ok1) dst[1] = u1 + v1;
+        }
+      }
+    }
+  }
+  static __device__ void finish(const Params &, Acc &) {}
 };
 
 // ================================================================= launch
@@ -329,6 +491,43 @@ cudaError_t fast3_desc_fine(const T *u, const T *f, int64_t pitch, const S3<T> &
   return order == 2 ? desc3_impl<T, 2>(u, f, pitch, rr, M, k, ns, st) : desc3_impl<T, 4>(u, f, pitch, rr, M, k, ns, st);
 }
 
+template <class T, int ORDER>
+static cudaError_t asc3_impl(const S3<T> &vr, const T *u_old, const T *f, int64_t pitch, T *u_new, int M, T c,
+                             const Coef<T> &k, cudaStream_t st) {
+  using Op = OpAsc3Fine<T, ORDER>;
+  typename Op::Params P{};
+  int64_t n = M + 1, plane = pitch * n;
+  if (!tm3<T>(&P.tu, u_old, n, pitch, plane, Op::UW, Op::UH) || !tm3<T>(&P.tf, f, n, pitch, plane, Op::FW, Op::FH))
+    return cudaErrorInvalidValue;
+  const int sub[4] = {0, 6, 5, 3};   // C, Fx, Fy, Fz
+  int64_t H = M / 2 + 1;
+  for (int i = 0; i < 4; i++) {
+    uint64_t dims[3] = {(uint64_t)H, (uint64_t)H, (uint64_t)H};
+    uint32_t box[3] = {(uint32_t)Op::VW, (uint32_t)Op::VH, 1};
+    if (!encode_tmap(&P.tv[i], vr.s[sub[i]], sizeof(T), 3, dims, (uint64_t)vr.pitch, (uint64_t)vr.plane, box))
+      return cudaErrorInvalidValue;
+  }
+  P.out = D3<T>{u_new, pitch, plane};
+  P.M = M;
+  P.ntx = (M + TX3 - 1) / TX3;
+  P.nty = (M + TY3 - 1) / TY3;
+  P.nunits = P.ntx * P.nty * ((M + ZC - 1) / ZC);
+  P.c = c;
+  P.k = k;
+  return run_plane<Op>(P, st);
+}
+
+template <class T>
+cudaError_t fast3_asc_fine(const S3<T> &vr, const T *u_old, const T *f, int64_t pitch, T *u_new, int M, int order, T c,
+                           const Coef<T> &k, cudaStream_t st) {
+  return order == 2 ? asc3_impl<T, 2>(vr, u_old, f, pitch, u_new, M, c, k, st)
+                    : asc3_impl<T, 4>(vr, u_old, f, pitch, u_new, M, c, k, st);
+}
+
+template cudaError_t fast3_asc_fine<float>(const S3<float> &, const float *, const float *, int64_t, float *, int, int,
+                                           float, const Coef<float> &, cudaStream_t);
+template cudaError_t fast3_asc_fine<double>(const S3<double> &, const double *, const double *, int64_t, double *, int,
+                                            int, double, const Coef<double> &, cudaStream_t);
 template cudaError_t fast3_desc_fine<float>(const float *, const float *, int64_t, const S3<float> &, int, int,
                                             const Coef<float> &, const NormSink &, cudaStream_t);
 template cudaError_t fast3_desc_fine<double>(const double *, const double *, int64_t, const S3<double> &, int, int,

@@ -55,8 +55,7 @@ using namespace l3;
 // Erred from the dense G(s) residual; the 2x2x2 block (a,b,c)
 // holds C (0,0,0), Fx (0,1,1), Fy (1,0,1), Fz (1,1,0).
 template <class T>
-__global__ void __launch_bounds__(256) k3l_rest_gr(D3<const T> r, S3<T> out, int M, int H) {
-  IDX3
+__device__ __forceinline__ void b3_rest_gr(D3<const T> r, S3<T> out, int M, int H, int a, int b, int c) {
   const int x = 2 * a, y = 2 * b, z = 2 * c;
   auto er = [&](int X, int Y, int Z) {
     T nb[6] = {r(X + 1, Y, Z), r(X - 1, Y, Z), r(X, Y + 1, Z), r(X, Y - 1, Z), r(X, Y, Z + 1), r(X, Y, Z - 1)};
@@ -70,12 +69,17 @@ __global__ void __launch_bounds__(256) k3l_rest_gr(D3<const T> r, S3<T> out, int
   if (od_a && od_b && in_c) sub(out, FZ)(a, b, c) = er(x + 1, y + 1, z);
 }
 
+template <class T>
+__global__ void __launch_bounds__(256) k3l_rest_gr(D3<const T> r, S3<T> out, int M, int H) {
+  IDX3
+  b3_rest_gr(r, out, M, H, a, b, c);
+}
+
 // --------------------------------------------------------- R(s) -> M(s)
 // corners: Ermagc (1/24)(12 r + 12 face diagonals, printed order);
 // centres: Ermagm (1/6)(6 axis neighbours), zero self weight.
 template <class T>
-__global__ void __launch_bounds__(256) k3l_rest_rm(S3<const T> rr, S3<T> rm, int H) {
-  IDX3
+__device__ __forceinline__ void b3_rest_rm(S3<const T> rr, S3<T> rm, int H, int a, int b, int c) {
   Sub<const T> Cr{rr.s[C], rr.pitch, rr.plane}, Fx{rr.s[FX], rr.pitch, rr.plane}, Fy{rr.s[FY], rr.pitch, rr.plane},
       Fz{rr.s[FZ], rr.pitch, rr.plane};
   if (a >= 1 && b >= 1 && c >= 1 && a <= H - 2 && b <= H - 2 && c <= H - 2) {
@@ -101,12 +105,16 @@ __global__ void __launch_bounds__(256) k3l_rest_rm(S3<const T> rr, S3<T> rm, int
   }
 }
 
+template <class T>
+__global__ void __launch_bounds__(256) k3l_rest_rm(S3<const T> rr, S3<T> rm, int H) {
+  IDX3
+  b3_rest_rm(rr, rm, H, a, b, c);
+}
+
 // ------------------------------------------------------- M(s) -> G(2s)
 // Erblu: (1/16)(8 r + 8 body diagonals, printed order).
 template <class T>
-__global__ void __launch_bounds__(256) k3l_rest_mg(S3<const T> rm, D3<T> g2, int Mc) {
-  const int H = Mc + 1;
-  IDX3
+__device__ __forceinline__ void b3_rest_mg(S3<const T> rm, D3<T> g2, int Mc, int a, int b, int c) {
   if (a < 1 || b < 1 || c < 1 || a > Mc - 1 || b > Mc - 1 || c > Mc - 1) return;
   Sub<const T> Cm{rm.s[C], rm.pitch, rm.plane}, Bm{rm.s[B], rm.pitch, rm.plane};
   T t = (T)8 * Cm(a, b, c);
@@ -121,12 +129,18 @@ __global__ void __launch_bounds__(256) k3l_rest_mg(S3<const T> rm, D3<T> g2, int
   g2(a, b, c) = t * (T)(1.0 / 16.0);
 }
 
+template <class T>
+__global__ void __launch_bounds__(256) k3l_rest_mg(S3<const T> rm, D3<T> g2, int Mc) {
+  const int H = Mc + 1;
+  IDX3
+  b3_rest_mg(rm, g2, Mc, a, b, c);
+}
+
 // ----------------------------------------------- M(s) from G(2s): a13
 // Emprolm on the centres, then (second kernel) Emprolb
 // on the corners from the new centres; c = 4 p_m (sh)^2.
 template <class T>
-__global__ void __launch_bounds__(256) k3l_jac_m1(D3<const T> vc, S3<const T> r, S3<T> v, int H, T cc) {
-  IDX3
+__device__ __forceinline__ void b3_jac_m1(D3<const T> vc, S3<const T> r, S3<T> v, int H, T cc, int a, int b, int c) {
   if (a > H - 2 || b > H - 2 || c > H - 2) return;
   T t = -(cc * r.s[B][(int64_t)c * r.plane + (int64_t)b * r.pitch + a]);
   t = t + vc(a + 1, b + 1, c + 1);   // (+,+,+)
@@ -141,8 +155,13 @@ __global__ void __launch_bounds__(256) k3l_jac_m1(D3<const T> vc, S3<const T> r,
 }
 
 template <class T>
-__global__ void __launch_bounds__(256) k3l_jac_m2(S3<const T> r, S3<T> v, int H, T cc) {
+__global__ void __launch_bounds__(256) k3l_jac_m1(D3<const T> vc, S3<const T> r, S3<T> v, int H, T cc) {
   IDX3
+  b3_jac_m1(vc, r, v, H, cc, a, b, c);
+}
+
+template <class T>
+__device__ __forceinline__ void b3_jac_m2(S3<const T> r, S3<T> v, int H, T cc, int a, int b, int c) {
   if (a < 1 || b < 1 || c < 1 || a > H - 2 || b > H - 2 || c > H - 2) return;
   Sub<T> Bv = sub(v, B);
   T t = -(cc * r.s[C][(int64_t)c * r.plane + (int64_t)b * r.pitch + a]);
@@ -157,14 +176,19 @@ __global__ void __launch_bounds__(256) k3l_jac_m2(S3<const T> r, S3<T> v, int H,
   sub(v, C)(a, b, c) = t * (T)0.125;
 }
 
+template <class T>
+__global__ void __launch_bounds__(256) k3l_jac_m2(S3<const T> r, S3<T> v, int H, T cc) {
+  IDX3
+  b3_jac_m2(r, v, H, cc, a, b, c);
+}
+
 // ------------------------------------------------- R(s) from M(s): a14
 // Erprolr on the face centres (normal axis = the even
 // coordinate, reading A8; the x- and y-face sums are the cyclic permutations
 // of the printed z-face sum), c1 = 2 p_r1 (sh)^2; then Erprolm on
 // the corners from the new faces, c2 = 4 p_r2 (sh)^2.
 template <class T>
-__global__ void __launch_bounds__(256) k3l_jac_r1(S3<const T> vm, S3<const T> r, S3<T> v, int H, T c1) {
-  IDX3
+__device__ __forceinline__ void b3_jac_r1(S3<const T> vm, S3<const T> r, S3<T> v, int H, T c1, int a, int b, int c) {
   Sub<const T> Cm{vm.s[C], vm.pitch, vm.plane}, Bm{vm.s[B], vm.pitch, vm.plane};
   const int64_t o = (int64_t)c * r.plane + (int64_t)b * r.pitch + a;
   const bool lo_a = a <= H - 2, lo_b = b <= H - 2, lo_c = c <= H - 2;
@@ -207,8 +231,13 @@ __global__ void __launch_bounds__(256) k3l_jac_r1(S3<const T> vm, S3<const T> r,
 }
 
 template <class T>
-__global__ void __launch_bounds__(256) k3l_jac_r2(S3<const T> r, S3<T> v, int H, T c2) {
+__global__ void __launch_bounds__(256) k3l_jac_r1(S3<const T> vm, S3<const T> r, S3<T> v, int H, T c1) {
   IDX3
+  b3_jac_r1(vm, r, v, H, c1, a, b, c);
+}
+
+template <class T>
+__device__ __forceinline__ void b3_jac_r2(S3<const T> r, S3<T> v, int H, T c2, int a, int b, int c) {
   if (a < 1 || b < 1 || c < 1 || a > H - 2 || b > H - 2 || c > H - 2) return;
   Sub<T> Fx = sub(v, FX), Fy = sub(v, FY), Fz = sub(v, FZ);
   T t = -(c2 * r.s[C][(int64_t)c * r.plane + (int64_t)b * r.pitch + a]);
@@ -227,14 +256,19 @@ __global__ void __launch_bounds__(256) k3l_jac_r2(S3<const T> r, S3<T> v, int H,
   sub(v, C)(a, b, c) = t * (T)(1.0 / 12.0);
 }
 
+template <class T>
+__global__ void __launch_bounds__(256) k3l_jac_r2(S3<const T> r, S3<T> v, int H, T c2) {
+  IDX3
+  b3_jac_r2(r, v, H, c2, a, b, c);
+}
+
 // ------------------------------------------------- G(s) from R(s): a15
 // Egprolg on the green-only nodes of the block (a,b,c):
 // (1,0,0), (0,1,0), (0,0,1), (1,1,1); neighbours i+1, i-1, j+1, j-1, k+1, k-1.
 // FINE: r recomputed from (u_old, f) and the green v kept in `g`.
 template <class T, int ORDER, bool FINE>
-__global__ void __launch_bounds__(256) k3l_jac_g1(S3<const T> vr, D3<const T> rin, D3<const T> u, D3<const T> f,
-                                                  D3<T> g, int M, int H, T cc, Coef<T> k) {
-  IDX3
+__device__ __forceinline__ void b3_jac_g1(S3<const T> vr, D3<const T> rin, D3<const T> u, D3<const T> f,
+                                                  D3<T> g, int M, int H, T cc, Coef<T> k, int a, int b, int c) {
   Sub<const T> Cr{vr.s[C], vr.pitch, vr.plane}, Fx{vr.s[FX], vr.pitch, vr.plane}, Fy{vr.s[FY], vr.pitch, vr.plane},
       Fz{vr.s[FZ], vr.pitch, vr.plane};
   const int x = 2 * a, y = 2 * b, z = 2 * c;
@@ -268,13 +302,19 @@ __global__ void __launch_bounds__(256) k3l_jac_g1(S3<const T> vr, D3<const T> ri
                                   Fz(a, b, c + 1), Fz(a, b, c));
 }
 
+template <class T, int ORDER, bool FINE>
+__global__ void __launch_bounds__(256) k3l_jac_g1(S3<const T> vr, D3<const T> rin, D3<const T> u, D3<const T> f,
+                                                  D3<T> g, int M, int H, T cc, Coef<T> k) {
+  IDX3
+  b3_jac_g1<T, ORDER, FINE>(vr, rin, u, f, g, M, H, cc, k, a, b, c);
+}
+
 // Egprolr on the red nodes of the block from the new green
 // values in `g`; FINE: out = u_old + v at all 8 nodes of the block;
 // otherwise out = v_G(s) at the red nodes (the green ones are already in g = out).
 template <class T, int ORDER, bool FINE>
-__global__ void __launch_bounds__(256) k3l_jac_g2(D3<const T> rin, D3<const T> u, D3<const T> f, D3<const T> g,
-                                                  D3<T> out, int M, int H, T cc, Coef<T> k) {
-  IDX3
+__device__ __forceinline__ void b3_jac_g2(D3<const T> rin, D3<const T> u, D3<const T> f, D3<const T> g,
+                                                  D3<T> out, int M, int H, T cc, Coef<T> k, int a, int b, int c) {
   const int x = 2 * a, y = 2 * b, z = 2 * c;
   auto rr = [&](int X, int Y, int Z) -> T {
     if (FINE) return res3<T, ORDER>(u, f, X, Y, Z, k);
@@ -314,7 +354,66 @@ __global__ void __launch_bounds__(256) k3l_jac_g2(D3<const T> rin, D3<const T> u
   }
 }
 
+template <class T, int ORDER, bool FINE>
+__global__ void __launch_bounds__(256) k3l_jac_g2(D3<const T> rin, D3<const T> u, D3<const T> f, D3<const T> g,
+                                                  D3<T> out, int M, int H, T cc, Coef<T> k) {
+  IDX3
+  b3_jac_g2<T, ORDER, FINE>(rin, u, f, g, out, M, H, cc, k, a, b, c);
+}
+
 #undef IDX3
+
+// ------------------------------------------------------ coarse octaves
+// One CTA runs every octave o >= oc (oc >= 1): the same step bodies in a
+// block-stride loop, __syncthreads between steps (arrays are L1/L2 resident).
+template <class T>
+__global__ void __launch_bounds__(1024) k3l_coarse(const Lev3<T> *lv, int oc, int k, int *counter) {
+  const int tid = threadIdx.x, bs = blockDim.x;
+  D3<const T> none{nullptr, 0, 0};
+  Coef<T> k0{};
+  auto cd = [](const D3<T> &a) { return D3<const T>{a.p, a.pitch, a.plane}; };
+  auto cs = [](const S3<T> &a) {
+    S3<const T> o;
+    for (int i = 0; i < 8; i++) o.s[i] = a.s[i];
+    o.pitch = a.pitch;
+    o.plane = a.plane;
+    return o;
+  };
+#define LOOP3(HH, BODY)                                            \
+  {                                                                \
+    const int H_ = (HH);                                           \
+    const int n_ = H_ * H_ * H_;                                   \
+    for (int t = tid; t < n_; t += bs) {                           \
+      const int a = t % H_, b = (t / H_) % H_, c = t / (H_ * H_); \
+      BODY;                                                        \
+    }                                                              \
+    __syncthreads();                                               \
+  }
+  for (int o = oc; o + 1 < k; o++) {
+    const Lev3<T> L = lv[o], Lc = lv[o + 1];
+    const int H = L.M / 2 + 1;
+    LOOP3(H, b3_rest_gr(cd(L.rG), L.rR, L.M, H, a, b, c));
+    LOOP3(H, b3_rest_rm(cs(L.rR), L.rM, H, a, b, c));
+    LOOP3(Lc.M + 1, b3_rest_mg(cs(L.rM), Lc.rG, Lc.M, a, b, c));
+  }
+  if (tid == 0) {
+    const Lev3<T> L = lv[k - 1];
+    L.vG(1, 1, 1) = (-(L.cG * L.rG(1, 1, 1))) * (T)(1.0 / 6.0);   // reading A4
+    if (counter) *counter += 1;
+  }
+  __syncthreads();
+  for (int o = k - 2; o >= oc; o--) {
+    const Lev3<T> L = lv[o], Lc = lv[o + 1];
+    const int H = L.M / 2 + 1;
+    LOOP3(H, b3_jac_m1(cd(Lc.vG), cs(L.rM), L.vM, H, L.cMg, a, b, c));
+    LOOP3(H, b3_jac_m2(cs(L.rM), L.vM, H, L.cMg, a, b, c));
+    LOOP3(H, b3_jac_r1(cs(L.vM), cs(L.rR), L.vR, H, L.cR1, a, b, c));
+    LOOP3(H, b3_jac_r2(cs(L.rR), L.vR, H, L.cR2, a, b, c));
+    LOOP3(H, (b3_jac_g1<T, 2, false>(cs(L.vR), cd(L.rG), none, none, L.vG, L.M, H, L.cG, k0, a, b, c)));
+    LOOP3(H, (b3_jac_g2<T, 2, false>(cd(L.rG), none, none, cd(L.vG), L.vG, L.M, H, L.cG, k0, a, b, c)));
+  }
+#undef LOOP3
+}
 
 // ================================================================ launchers
 static inline dim3 grid3(int H) { return dim3((H + 31) / 32, (H + 7) / 8, H); }
@@ -381,7 +480,13 @@ void lv3_asc_fine(const S3<T> &vr, const D3<T> &u_old, const D3<const T> &f, con
   }
 }
 
+template <class T>
+void lv3_coarse(const Lev3<T> *d_lev, int oc, int k, int *counter, cudaStream_t st) {
+  k3l_coarse<T><<<1, 1024, 0, st>>>(d_lev, oc, k, counter);
+}
+
 #define INSTL(T)                                                                                                   \
+  template void lv3_coarse<T>(const Lev3<T> *, int, int, int *, cudaStream_t);                                     \
   template void lv3_rest_gr<T>(const D3<T> &, const S3<T> &, int, cudaStream_t);                                   \
   template void lv3_rest_rm<T>(const S3<T> &, const S3<T> &, int, cudaStream_t);                                   \
   template void lv3_rest_mg<T>(const S3<T> &, const D3<T> &, int, cudaStream_t);                                   \

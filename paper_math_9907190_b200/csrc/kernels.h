@@ -89,6 +89,21 @@ void launch3_ftilde(const D3<const T> &f, const D3<T> &ft, int M, cudaStream_t s
 template <class T>
 cudaError_t fast3_desc_fine(const T *u, const T *f, int64_t pitch, const S3<T> &rr, int M, int order, const Coef<T> &k,
                             const NormSink &ns, cudaStream_t st);
+template <class T>
+cudaError_t fast3_asc_fine(const S3<T> &vr, const T *u_old, const T *f, int64_t pitch, T *u_new, int M, int order, T c,
+                           const Coef<T> &k, cudaStream_t st);
+
+// Per-octave level descriptors for the 3D single-CTA coarse kernel.
+template <class T>
+struct Lev3 {
+  S3<T> rR, vR, rM, vM;   // R(s), M(s)
+  D3<T> rG, vG;           // G(s)
+  int M;
+  T cMg, cR1, cR2, cG;
+};
+template <class T>
+void lv3_coarse(const Lev3<T> *d_lev, int oc, int k, int *counter, cudaStream_t st);
+
 // Sublattice level kernels (k3l.cu).
 template <class T>
 void lv3_rest_gr(const D3<T> &r, const S3<T> &rr, int M, cudaStream_t st);

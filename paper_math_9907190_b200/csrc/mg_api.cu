@@ -365,6 +365,8 @@ struct Impl3 : ImplBase {
   Coef<T> coef{};
   std::vector<T> cMg, cR1, cR2, cG;
   bool use_fast = false;   // TMA plane kernels for the finest octave
+  int oc = 1;              // first octave run by the single-CTA coarse kernel
+  Lev3<T> *d_lev = nullptr;
   explicit Impl3(const mg_solver *sv) : s(sv), k(sv->k), n(sv->cfg.n), pitch(sv->pitch) {}
   bool fast() const override { return use_fast; }
   int64_t pitch_for(int64_t cnt) const { return round_up(cnt, 128 / (int64_t)sizeof(T)); }
@@ -433,7 +435,37 @@ struct Impl3 : ImplBase {
     coef.invh2 = (T)((double)(n - 1) * (double)(n - 1));
     coef.c6 = (T)((double)(n - 1) * (double)(n - 1) / 6.0);
     use_fast = ((pitch * (int64_t)sizeof(T)) % 16 == 0) && !getenv("MG_FORCE_REF");
-    return cudaSuccess;
+    int thresh = 16;
+    if (const char *e = getenv("MG_COARSE_M3")) thresh = atoi(e);
+    oc = k - 1;
+    for (int o = 1; o < k; o++)
+      if (M[o] <= thresh) {
+        oc = o;
+        break;
+      }
+    std::vector<Lev3<T>> lv(k);
+    for (int o = 0; o < k; o++) {
+      lv[o].M = M[o];
+      lv[o].cMg = cMg[o];
+      lv[o].cR1 = cR1[o];
+      lv[o].cR2 = cR2[o];
+      lv[o].cG = cG[o];
+      if (o + 1 < k) {
+        lv[o].rR = rR[o];
+        lv[o].vR = vR[o];
+        lv[o].rM = rM[o];
+        lv[o].vM = vM[o];
+      }
+      if (o >= 1) {
+        lv[o].rG = rG[o];
+        lv[o].vG = vG[o];
+      }
+    }
+    void *q;
+    cudaError_t st = dalloc(&q, sizeof(Lev3<T>) * k);
+    if (st) return st;
+    d_lev = (Lev3<T> *)q;
+    return cudaMemcpy(d_lev, lv.data(), sizeof(Lev3<T>) * k, cudaMemcpyHostToDevice);
   }
 
   NormSink sink() const { return NormSink{s->d_hist, s->d_counter, kHistCap}; }
@@ -447,6 +479,7 @@ struct Impl3 : ImplBase {
   D3<T> field(void *a) const { return D3<T>{(T *)a, pitch, pitch * n}; }
 
   void enqueue_cycle(const void *u_in, void *u_out, const void *f_eff, cudaStream_t st, Prof *prof) override {
+    if (use_fast) return enqueue_fast(u_in, u_out, f_eff, st, prof);
     const double w = sizeof(T);
     const int L = 3 * k - 2;
     void *u = const_cast<void *>(u_in);
@@ -490,6 +523,52 @@ struct Impl3 : ImplBase {
       }
     }
   }
+  // The B200 path: TMA plane kernel for the finest descent, sublattice
+  // kernels for the octaves below oc, one CTA for the rest.
+  void enqueue_fast(const void *u_in, void *u_out, const void *f_eff, cudaStream_t st, Prof *prof) {
+    const double w = sizeof(T);
+    const int L = 3 * k - 2;
+    void *u = const_cast<void *>(u_in);
+    STEP("desc_fine", 0, 1, w * (2 * Nl[0] + Nl[1]));
+    desc_fine(u, f_eff, st);
+    for (int o = 0; o < oc; o++) {
+      int g = 3 * o;
+      if (o >= 1) {
+        STEP("rest_gr", g, 1, w * (Nl[g] + Nl[g + 1]));
+        lv3_rest_gr<T>(rG[o], rR[o], M[o], st);
+      }
+      STEP("rest_rm", g + 1, 1, w * (Nl[g + 1] + Nl[g + 2]));
+      lv3_rest_rm<T>(rR[o], rM[o], M[o], st);
+      STEP("rest_mg", g + 2, 1, w * (Nl[g + 2] + Nl[g + 3]));
+      lv3_rest_mg<T>(rM[o], rG[o + 1], M[o + 1], st);
+    }
+    {
+      double b = 0;
+      for (int l = 3 * oc; l < L; l++) b += 5 * Nl[l];
+      b -= Nl[L - 1] + 2 * Nl[3 * oc];
+      STEP("coarse", 3 * oc, 1, w * b);
+    }
+    lv3_coarse<T>(d_lev, oc, k, s->d_counter, st);
+    for (int o = oc - 1; o >= 0; o--) {
+      int g = 3 * o;
+      STEP("jac_m", g + 2, 2, w * (Nl[g + 3] + 2 * Nl[g + 2]));
+      lv3_jac_m<T>(vG[o + 1], rM[o], vM[o], M[o], cMg[o], st);
+      STEP("jac_r", g + 1, 2, w * (Nl[g + 2] + 2 * Nl[g + 1]));
+      lv3_jac_r<T>(vM[o], rR[o], vR[o], M[o], cR1[o], cR2[o], st);
+      if (o >= 1) {
+        STEP("jac_g", g, 2, w * (Nl[g + 1] + 2 * Nl[g]));
+        lv3_jac_g<T>(vR[o], rG[o], vG[o], M[o], cG[o], st);
+      } else if (!getenv("MG_ASC3_DIRECT") && ((uintptr_t)u & 15) == 0 && ((uintptr_t)f_eff & 15) == 0 &&
+                 ((uintptr_t)u_out & 15) == 0) {
+        STEP("asc_fine", 0, 1, w * (Nl[1] + 3 * Nl[0]));
+        fast3_asc_fine<T>(vR[0], (const T *)u, (const T *)f_eff, pitch, (T *)u_out, M[0], s->cfg.order, cG[0], coef,
+                          st);
+      } else {
+        STEP("asc_fine", 0, 2, w * (Nl[1] + 3 * Nl[0]));
+        lv3_asc_fine<T>(vR[0], field(u), cfield(f_eff), scratch, field(u_out), M[0], s->cfg.order, cG[0], coef, st);
+      }
+    }
+  }
   void enqueue_final_norm(void *u, const void *f_eff, cudaStream_t st) override { desc_fine(u, f_eff, st); }
   void enqueue_residual(const void *u, const void *f, void *r, cudaStream_t st) override {
     launch3_residual<T>(cfield(u), cfield(f), field(r), M[0], s->cfg.order, coef, st);
@@ -504,7 +583,14 @@ struct Impl3 : ImplBase {
     int c = 1;
     for (int o = 0; o + 1 < k; o++) c += (o >= 1) + 2;
     c += 1;
-    for (int o = k - 2; o >= 0; o--) c += 2 + 2 + ((o >= 1) ? 2 : (use_fast ? 2 : 3));
+    if (use_fast) {
+      c = 1;
+      for (int o = 0; o < oc; o++) c += (o >= 1) + 2;
+      c += 1;
+      for (int o = oc - 1; o >= 0; o--) c += 2 + 2 + 2;
+      return c;
+    }
+    for (int o = k - 2; o >= 0; o--) c += 2 + 2 + ((o >= 1) ? 2 : 3);
     return c;
   }
 };
