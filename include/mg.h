@@ -38,13 +38,21 @@
  *    the ABI.  mg_last_error() describes the last failure of a handle.
  *  - A handle is not thread-safe; distinct handles are independent.
  *
- * Multi-GPU (cfg.nranks > 1): one process per GPU; the grid is cut into
- * y-slabs (2D) / z-slabs (3D).  Each rank passes only its slab: rows
- * (planes) [lo, hi) of the global grid, stored with `ghost` extra rows
- * (planes) above and below, i.e. a (hi - lo + 2*ghost) x ... array whose row
- * `ghost` is global row lo (see mg_local_extent).  The library fills the
- * ghost rows itself.  Levels coarser than cfg.agglom_points interior nodes
- * are agglomerated on every rank (all-gather + redundant coarse solve).
+ * Multi-GPU (cfg.nranks > 1, dim 2, nranks a power of two, (n-1)/nranks >= 4,
+ * 16-byte row pitch): one process per GPU over NCCL (cfg.nccl_id from
+ * mg_nccl_unique_id on rank 0, broadcast by the caller); the grid is cut into
+ * y-slabs.  Each rank passes only its slab: rows [lo, hi) of
+ * the global grid (lo = rank (n-1)/nranks, hi = lo + (n-1)/nranks) stored
+ * with `ghost` = 2 extra rows below and above, i.e. a (hi - lo + 4) x pitch
+ * array whose row 2 is global row lo (see mg_local_extent); the global
+ * boundary rows 0 and n-1 lie in rank 0's own rows / the last rank's ghost
+ * rows and must be 0.  The library fills the ghost rows itself (halo
+ * exchange per level).  Levels with fewer than cfg.agglom_points interior
+ * nodes (or fewer than 4 rows per rank) are all-gathered and solved
+ * redundantly on every rank; residual norms are max-reduced over ranks.
+ * With cfg.flags = MG_FLAG_LOOPBACK the nranks ranks are virtual (one process,
+ * one GPU, full arrays in and out): the same schedule, halos copied on the
+ * device -- used to test the decomposition bit for bit.
  */
 #ifndef MG_H
 #define MG_H
@@ -69,6 +77,9 @@ typedef enum {
 } mg_status;
 
 enum { MG_F64 = 0, MG_F32 = 1 };
+/* mg_config.flags */
+enum { MG_FLAG_LOOPBACK = 1 };  /* nranks virtual ranks in this process on one GPU (tests the slab
+                                   decomposition; caller passes FULL arrays) */
 enum { MG_NORM_INF = 0, MG_NORM_L2 = 1 };
 
 typedef struct {
@@ -84,7 +95,7 @@ typedef struct {
   int nranks, rank;        /* 1 / 0 for a single GPU */
   const void *nccl_id;     /* 128-byte ncclUniqueId (same on every rank) when nranks > 1 */
   int64_t agglom_points;   /* agglomerate levels with fewer interior nodes; 0 = 1<<18 */
-  int flags;               /* reserved, 0 */
+  int flags;               /* MG_FLAG_* (0 for normal use) */
 } mg_config;
 
 /* Defaults: fp64, pitch = n, NULL stream, current device, 1 rank, p[*] = omega.
@@ -146,6 +157,17 @@ typedef struct {
   double alg_bytes;   /* algorithmic bytes moved per launch of the step */
 } mg_step_stat;
 int mg_profile(mg_solver *s, void *u, const void *f, int ncycles, mg_step_stat *out, int cap);
+
+/* The slab decomposition without a device (host-only planning): rows [lo, hi)
+ * owned by `rank`, ghost rows carried on each side, and the first octave
+ * whose levels are agglomerated (all-gathered).  nranks = 1: the whole grid.
+ * MG_EUNSUPPORTED when the grid cannot be split that way. */
+int mg_slab_plan(int dim, int64_t n, int nranks, int rank, int64_t agglom_points, int64_t *lo, int64_t *hi,
+                 int64_t *ghost, int *agglom_octave);
+
+/* 128-byte NCCL unique id for cfg.nccl_id (call on one rank, broadcast the
+ * bytes to all).  Loads the NCCL library at run time; MG_ENCCL if absent. */
+int mg_nccl_unique_id(void *out128);
 
 const char *mg_strerror(int status);
 const char *mg_last_error(const mg_solver *s);

@@ -13,8 +13,8 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libmg.so")
-SOURCES = ["mg_api.cu", "k2d.cu", "k2f.cu", "k3d.cu", "k3f.cu", "k3l.cu", "tma_host.cu"]
-HEADERS = ["common.cuh", "kernels.h", "ops2.cuh", "ops3.cuh", "tma.cuh"]
+SOURCES = ["mg_api.cu", "k2d.cu", "k2f.cu", "k3d.cu", "k3f.cu", "k3l.cu", "dist2.cu", "tma_host.cu"]
+HEADERS = ["common.cuh", "kernels.h", "ops2.cuh", "ops3.cuh", "tma.cuh", "solver.h"]
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 # --fmad=false: no FMA contraction anywhere (canonical arithmetic)
@@ -58,7 +58,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
         if verbose and out:
             print(out.decode())
     tmp = LIB + ".tmp"
-    cmd = [nvcc(), *ARCH, "-shared", "-o", tmp, *objs, "-Xcompiler", "-fPIC"]
+    cmd = [nvcc(), *ARCH, "-shared", "-o", tmp, *objs, "-Xcompiler", "-fPIC", "-ldl"]
     subprocess.check_call(cmd)
     os.replace(tmp, LIB)
     return LIB

@@ -1,0 +1,613 @@
+// dist2.cu -- the 2D V-cycle on y-slabs over several ranks.
+//
+// Rank q owns the lattice rows [q M_s/P, (q+1) M_s/P) of every level of
+// octave s while M_s/P >= 4 and the level has at least agglom_points
+// interior nodes; each slab array carries 2 ghost rows on each side (global
+// row indices are kept: the device descriptors point at the virtual global
+// row 0).  Before a kernel, the ghost rows it reads are refreshed by a halo
+// exchange (1 or 2 rows); at the first agglomerated octave oa the level's
+// residual is all-gathered into full arrays and every rank runs the coarse
+// octaves redundantly (bit-identical), so the ascent needs no gather back.
+// The per-cycle residual-norm maxima are max-reduced over ranks.
+//
+// Two transports implement the same schedule:
+//  * NCCL (one process per GPU): grouped ncclSend/ncclRecv of whole rows,
+//    in-place ncclAllGather, ncclAllReduce(max); libnccl.so.2 is loaded at run
+//    time (the one torch ships), so a single-GPU build needs no NCCL.
+//  * loopback (MG_FLAG_LOOPBACK): P virtual ranks in one process on one GPU,
+//    halos copied device-to-device between their slabs, coarse arrays shared;
+//    kernels of different virtual ranks never wait on one another.  It tests
+//    the decomposition bit for bit against the single-GPU solver.
+#include <dlfcn.h>
+
+#include "solver.h"
+
+namespace {
+
+// ------------------------------------------------------------------ NCCL
+typedef struct ncclComm *ncclComm_t;
+typedef struct {
+  char internal[128];
+} ncclUniqueId;
+typedef int ncclResult_t;
+enum { ncclFloat32 = 7, ncclFloat64 = 8, ncclUint64 = 5 };
+enum { ncclSum = 0, ncclMax = 2 };
+
+struct NcclApi {
+  bool ok = false;
+  std::string why;
+  ncclResult_t (*GetUniqueId)(ncclUniqueId *) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t *, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*Send)(const void *, size_t, int, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*Recv)(void *, size_t, int, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*GroupStart)() = nullptr;
+  ncclResult_t (*GroupEnd)() = nullptr;
+  ncclResult_t (*AllGather)(const void *, void *, size_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*AllReduce)(const void *, void *, size_t, int, int, ncclComm_t, cudaStream_t) = nullptr;
+  const char *(*GetErrorString)(ncclResult_t) = nullptr;
+  bool load() {
+    if (ok) return true;
+    const char *names[] = {getenv("MG_NCCL_LIB"), "libnccl.so.2", "libnccl.so"};
+    void *h = nullptr;
+    for (const char *nm : names)
+      if (nm && (h = dlopen(nm, RTLD_NOW | RTLD_GLOBAL))) break;
+    if (!h) {
+      why = "libnccl.so.2 not found (set MG_NCCL_LIB)";
+      return false;
+    }
+#define SYM(f, name)                                         \
+  f = reinterpret_cast<decltype(f)>(dlsym(h, name));         \
+  if (!f) {                                                  \
+    why = std::string("missing NCCL symbol ") + name;        \
+    return false;                                            \
+  }
+    SYM(GetUniqueId, "ncclGetUniqueId");
+    SYM(CommInitRank, "ncclCommInitRank");
+    SYM(CommDestroy, "ncclCommDestroy");
+    SYM(Send, "ncclSend");
+    SYM(Recv, "ncclRecv");
+    SYM(GroupStart, "ncclGroupStart");
+    SYM(GroupEnd, "ncclGroupEnd");
+    SYM(AllGather, "ncclAllGather");
+    SYM(AllReduce, "ncclAllReduce");
+    SYM(GetErrorString, "ncclGetErrorString");
+#undef SYM
+    ok = true;
+    return true;
+  }
+};
+NcclApi &nccl() {
+  static NcclApi a;
+  return a;
+}
+
+}  // namespace
+
+// ------------------------------------------------------------ transports
+// An array family is given per local rank as a virtual global-row-0 pointer
+// (bytes) with a pitch in bytes; rows [lo, hi) are owned.
+struct Comm2 {
+  int P = 1;
+  virtual ~Comm2() {}
+  virtual cudaError_t exchange(const std::vector<char *> &p, size_t pitch_b, const std::vector<int> &lo,
+                               const std::vector<int> &hi, int g, cudaStream_t st) = 0;
+  // full array (virtual row 0 pointer): own rows [lo, lo+rows) -> every rank
+  virtual cudaError_t allgather(char *full, size_t pitch_b, int lo, int rows, int esz, cudaStream_t st) = 0;
+  virtual cudaError_t allreduce_max_u64(unsigned long long *d, int n, cudaStream_t st) = 0;
+  virtual cudaError_t allreduce_sum_f64(double *d, int n, cudaStream_t st) = 0;
+  virtual std::string error() const { return ""; }
+};
+
+struct LoopComm : Comm2 {
+  cudaError_t exchange(const std::vector<char *> &p, size_t pb, const std::vector<int> &lo, const std::vector<int> &hi,
+                       int g, cudaStream_t st) override {
+    for (int i = 0; i < P; i++) {
+      if (i > 0) {   // rows [lo_i - g, lo_i) are owned by rank i-1
+        cudaError_t e = cudaMemcpyAsync(p[i] + (int64_t)(lo[i] - g) * pb, p[i - 1] + (int64_t)(lo[i] - g) * pb, g * pb,
+                                        cudaMemcpyDeviceToDevice, st);
+        if (e) return e;
+      }
+      if (i + 1 < P) {   // rows [hi_i, hi_i + g) are owned by rank i+1
+        cudaError_t e = cudaMemcpyAsync(p[i] + (int64_t)hi[i] * pb, p[i + 1] + (int64_t)hi[i] * pb, g * pb,
+                                        cudaMemcpyDeviceToDevice, st);
+        if (e) return e;
+      }
+    }
+    return cudaSuccess;
+  }
+  cudaError_t allgather(char *, size_t, int, int, int, cudaStream_t) override { return cudaSuccess; }
+  cudaError_t allreduce_max_u64(unsigned long long *, int, cudaStream_t) override { return cudaSuccess; }
+  cudaError_t allreduce_sum_f64(double *, int, cudaStream_t) override { return cudaSuccess; }
+};
+
+struct NcclComm : Comm2 {
+  int q = 0;
+  int dtype = ncclFloat64;
+  ncclComm_t comm = nullptr;
+  std::string err;
+  ~NcclComm() override {
+    if (comm) nccl().CommDestroy(comm);
+  }
+  bool init(int P_, int q_, const void *id, int esz) {
+    P = P_;
+    q = q_;
+    dtype = esz == 8 ? ncclFloat64 : ncclFloat32;
+    if (!nccl().load()) {
+      err = nccl().why;
+      return false;
+    }
+    ncclUniqueId uid;
+    std::memcpy(&uid, id, sizeof uid);
+    ncclResult_t r = nccl().CommInitRank(&comm, P, uid, q);
+    if (r != 0) {
+      err = std::string("ncclCommInitRank: ") + nccl().GetErrorString(r);
+      comm = nullptr;
+      return false;
+    }
+    return true;
+  }
+  cudaError_t check(ncclResult_t r, const char *what) {
+    if (r == 0) return cudaSuccess;
+    err = std::string(what) + ": " + nccl().GetErrorString(r);
+    return cudaErrorUnknown;
+  }
+  cudaError_t exchange(const std::vector<char *> &p, size_t pb, const std::vector<int> &lo, const std::vector<int> &hi,
+                       int g, cudaStream_t st) override {
+    const int esz = dtype == ncclFloat64 ? 8 : 4;
+    const size_t cnt = g * pb / esz;
+    char *a = p[0];
+    nccl().GroupStart();
+    if (q > 0) {
+      nccl().Send(a + (int64_t)lo[0] * pb, cnt, dtype, q - 1, comm, st);
+      nccl().Recv(a + (int64_t)(lo[0] - g) * pb, cnt, dtype, q - 1, comm, st);
+    }
+    if (q + 1 < P) {
+      nccl().Send(a + (int64_t)(hi[0] - g) * pb, cnt, dtype, q + 1, comm, st);
+      nccl().Recv(a + (int64_t)hi[0] * pb, cnt, dtype, q + 1, comm, st);
+    }
+    return check(nccl().GroupEnd(), "halo exchange");
+  }
+  cudaError_t allgather(char *full, size_t pb, int lo, int rows, int esz, cudaStream_t st) override {
+    const size_t cnt = rows * pb / esz;
+    return check(nccl().AllGather(full + (int64_t)lo * pb, full + (int64_t)(lo - q * rows) * pb, cnt, dtype, comm, st),
+                 "agglomeration all-gather");
+  }
+  cudaError_t allreduce_max_u64(unsigned long long *d, int n, cudaStream_t st) override {
+    return check(nccl().AllReduce(d, d, n, ncclUint64, ncclMax, comm, st), "norm all-reduce");
+  }
+  cudaError_t allreduce_sum_f64(double *d, int n, cudaStream_t st) override {
+    return check(nccl().AllReduce(d, d, n, ncclFloat64, ncclSum, comm, st), "norm all-reduce");
+  }
+  std::string error() const override { return err; }
+};
+
+// ================================================================ Dist2
+template <class T>
+struct Dist2 : ImplBase {
+  mg_solver *s;
+  int k, P, nloc;   // nloc = local (virtual) ranks: P in loopback, 1 with NCCL
+  bool loop;
+  int64_t n, pitch;
+  std::unique_ptr<Comm2> comm;
+  int oa = 1, oc = 1;
+  std::vector<int> M;
+  std::vector<T> cD, cA;
+  Coef<T> coef{};
+  struct Rk {
+    int q;
+    std::vector<S2<T>> rD, vD;   // octaves o < oa
+    std::vector<D2<T>> rA, vA;   // 1 <= o < oa
+    D2<T> u[2], f;               // loopback: internal slabs of u (pair) and f / f~
+  };
+  std::vector<Rk> rk;
+  std::vector<S2<T>> rDf, vDf;   // full arrays, octaves o >= oa
+  std::vector<D2<T>> rAf, vAf;
+  D2<T> uf_scratch{};            // loopback: full f~ (order 4)
+  Lev2<T> *d_lev = nullptr;
+
+  Dist2(mg_solver *sv, bool loopback) : s(sv), k(sv->k), P(sv->cfg.nranks), loop(loopback), n(sv->cfg.n),
+                                        pitch(sv->pitch) {
+    nloc = loop ? P : 1;
+  }
+  bool fast() const override { return true; }
+  int64_t pitch_for(int64_t cnt) const { return round_up(cnt, 128 / (int64_t)sizeof(T)); }
+  int R(int o) const { return M[o] / P; }                 // A(s) rows per rank at octave o
+  int lo(int o, int q) const { return q * R(o); }
+  int hi(int o, int q) const { return (q + 1) * R(o); }
+
+  // slab of rows [lo-2, hi+2): virtual global-row-0 pointer
+  cudaError_t slab(D2<T> &out, int64_t cols, int lo_, int hi_) {
+    int64_t pt = pitch_for(cols);
+    void *q;
+    cudaError_t e = dalloc(&q, sizeof(T) * pt * (hi_ - lo_ + 4));
+    if (e) return e;
+    out = D2<T>{(T *)q - (int64_t)(lo_ - 2) * pt, pt};
+    return cudaSuccess;
+  }
+  cudaError_t slab_s(S2<T> &out, int64_t cols, int lo_, int hi_) {
+    D2<T> e, o;
+    cudaError_t r = slab(e, cols, lo_, hi_);
+    if (r) return r;
+    r = slab(o, cols, lo_, hi_);
+    if (r) return r;
+    out = S2<T>{e.p, o.p, e.pitch};
+    return cudaSuccess;
+  }
+  // full array of rows [0, rows) with 2 zero rows of padding on each side
+  cudaError_t full(D2<T> &out, int64_t cols, int rows) { return slab(out, cols, 0, rows); }
+  cudaError_t full_s(S2<T> &out, int64_t cols, int rows) { return slab_s(out, cols, 0, rows); }
+
+  cudaError_t alloc() override {
+    const double p = s->cfg.p[0];
+    M.resize(k);
+    cD.resize(k);
+    cA.resize(k);
+    for (int o = 0; o < k; o++) {
+      M[o] = (int)((n - 1) >> o);
+      double hs = std::ldexp(1.0, o) / (double)(n - 1);
+      cD[o] = (T)(2.0 * p * hs * hs);
+      cA[o] = (T)(p * hs * hs);
+    }
+    coef.invh2 = (T)((double)(n - 1) * (double)(n - 1));
+    coef.c6 = (T)((double)(n - 1) * (double)(n - 1) / 6.0);
+    int64_t ag = s->cfg.agglom_points > 0 ? s->cfg.agglom_points : (int64_t(1) << 18);
+    oa = slab_agglom_octave(n, k, P, ag);
+    int thresh = 64;
+    if (const char *e = getenv("MG_COARSE_M")) thresh = atoi(e);
+    oc = k - 1;
+    for (int o = oa; o < k; o++)
+      if (M[o] <= thresh || o == k - 1) {
+        oc = o;
+        break;
+      }
+    if (oc < 1) oc = 1;
+    rk.resize(nloc);
+    for (int i = 0; i < nloc; i++) {
+      Rk &r = rk[i];
+      r.q = loop ? i : s->cfg.rank;
+      r.rD.resize(oa);
+      r.vD.resize(oa);
+      r.rA.resize(oa);
+      r.vA.resize(oa);
+      for (int o = 0; o < oa; o++) {
+        int H = M[o] / 2 + 1, l = lo(o, r.q) / 2, h = hi(o, r.q) / 2;
+        cudaError_t e;
+        if ((e = slab_s(r.rD[o], H, l, h)) || (e = slab_s(r.vD[o], H, l, h))) return e;
+        if (o >= 1 && ((e = slab(r.rA[o], M[o] + 1, lo(o, r.q), hi(o, r.q))) ||
+                       (e = slab(r.vA[o], M[o] + 1, lo(o, r.q), hi(o, r.q)))))
+          return e;
+      }
+      if (loop) {
+        cudaError_t e;
+        if ((e = slab(r.u[0], n, lo(0, r.q), hi(0, r.q))) || (e = slab(r.u[1], n, lo(0, r.q), hi(0, r.q))) ||
+            (e = slab(r.f, n, lo(0, r.q), hi(0, r.q))))
+          return e;
+      }
+    }
+    rDf.resize(k);
+    vDf.resize(k);
+    rAf.resize(k);
+    vAf.resize(k);
+    for (int o = oa; o < k; o++) {
+      cudaError_t e;
+      if ((e = full(rAf[o], M[o] + 1, M[o] + 1)) || (e = full(vAf[o], M[o] + 1, M[o] + 1))) return e;
+      if (o + 1 < k && ((e = full_s(rDf[o], M[o] / 2 + 1, M[o] / 2 + 1)) || (e = full_s(vDf[o], M[o] / 2 + 1, M[o] / 2 + 1))))
+        return e;
+    }
+    if (loop && s->cfg.order == 4) {
+      cudaError_t e = full(uf_scratch, n, n);
+      if (e) return e;
+    }
+    std::vector<Lev2<T>> lv(k);
+    for (int o = oa; o < k; o++) {
+      lv[o].M = M[o];
+      lv[o].cD = cD[o];
+      lv[o].cA = cA[o];
+      lv[o].rA = rAf[o];
+      lv[o].vA = vAf[o];
+      if (o + 1 < k) {
+        lv[o].rD = rDf[o];
+        lv[o].vD = vDf[o];
+      }
+    }
+    void *q;
+    cudaError_t e = dalloc(&q, sizeof(Lev2<T>) * k);
+    if (e) return e;
+    d_lev = (Lev2<T> *)q;
+    return cudaMemcpy(d_lev, lv.data(), sizeof(Lev2<T>) * k, cudaMemcpyHostToDevice);
+  }
+
+  NormSink sink() const { return NormSink{s->d_hist, s->d_counter, kHistCap}; }
+  size_t local_elems() const override { return loop ? 0 : (size_t)(R(0) + 4) * pitch; }
+  bool extent(int64_t *l, int64_t *h, int64_t *g) const override {
+    if (loop) return false;
+    *l = lo(0, s->cfg.rank);
+    *h = hi(0, s->cfg.rank);
+    *g = 2;
+    return true;
+  }
+
+  // ---- exchanges of an array family over the local ranks
+  template <class GetPtr>
+  cudaError_t xchg(int o, bool half, int g, cudaStream_t st, GetPtr get, int64_t pt) {
+    std::vector<char *> p(nloc);
+    std::vector<int> l(nloc), h(nloc);
+    for (int i = 0; i < nloc; i++) {
+      p[i] = (char *)get(i);
+      l[i] = half ? lo(o, rk[i].q) / 2 : lo(o, rk[i].q);
+      h[i] = half ? hi(o, rk[i].q) / 2 : hi(o, rk[i].q);
+    }
+    return comm->exchange(p, (size_t)pt * sizeof(T), l, h, g, st);
+  }
+
+  Rows2 rows_full(int o, int q) const {   // kernels whose output rows are A(s) rows of octave o
+    Rows2 r;
+    r.ylo = lo(o, q);
+    r.yhi = hi(o, q);
+    r.fy0 = lo(o, q) - 2;
+    r.frows = R(o) + 4;
+    r.hy0 = lo(o, q) / 2 - 2;
+    r.hrows = R(o) / 2 + 4;
+    return r;
+  }
+  Rows2 rows_half(int o, int q) const {   // kernels whose output rows are E/O (= A(2s)) rows of octave o
+    Rows2 r;
+    r.ylo = lo(o, q) / 2;
+    r.yhi = hi(o, q) / 2;
+    r.hy0 = lo(o, q) / 2 - 2;
+    r.hrows = R(o) / 2 + 4;
+    return r;
+  }
+
+  cudaError_t cycle(const std::vector<const T *> &uin, const std::vector<T *> &uout, const std::vector<const T *> &fe,
+                    cudaStream_t st, Prof *prof) {
+    const double w = sizeof(T);
+    const int L = 2 * k - 1;
+    cudaError_t e;
+    STEP("halo_u_f", 0, 0, 0);
+    if ((e = xchg(0, false, 2, st, [&](int i) { return uin[i]; }, pitch))) return e;
+    if ((e = xchg(0, false, 1, st, [&](int i) { return fe[i]; }, pitch))) return e;
+    STEP("desc_fine", 0, nloc, w * (2 * Nl[0] + Nl[1]));
+    for (int i = 0; i < nloc; i++)
+      if ((e = fast2_desc_fine<T>(uin[i], fe[i], pitch, rk[i].rD[0], M[0], s->cfg.order, coef, sink(), st,
+                                  rows_full(0, rk[i].q))))
+        return e;
+    for (int o = 0; o < oa; o++) {
+      if (o >= 1) {
+        STEP("rest_ad", 2 * o, nloc, w * (Nl[2 * o] + Nl[2 * o + 1]));
+        if ((e = xchg(o, false, 1, st, [&](int i) { return rk[i].rA[o].p; }, rk[0].rA[o].pitch))) return e;
+        for (int i = 0; i < nloc; i++)
+          if ((e = fast2_rest_ad<T>(rk[i].rA[o], rk[i].rD[o], M[o], st, rows_full(o, rk[i].q)))) return e;
+      }
+      STEP("rest_da", 2 * o + 1, nloc, w * (Nl[2 * o + 1] + Nl[2 * o + 2]));
+      if ((e = xchg(o, true, 1, st, [&](int i) { return rk[i].rD[o].o; }, rk[0].rD[o].pitch))) return e;
+      for (int i = 0; i < nloc; i++) {
+        const D2<T> &out = (o + 1 < oa) ? rk[i].rA[o + 1] : rAf[oa];
+        if ((e = fast2_rest_da<T>(rk[i].rD[o], out, M[o + 1], st, rows_half(o, rk[i].q)))) return e;
+      }
+    }
+    STEP("agglomerate", 2 * oa, 0, 0);
+    if ((e = comm->allgather((char *)rAf[oa].p, rAf[oa].pitch * sizeof(T), lo(oa, rk[0].q), R(oa), sizeof(T), st)))
+      return e;
+    // ---- coarse octaves on full arrays (every NCCL rank; once in loopback)
+    for (int o = oa; o < oc; o++) {
+      if (o > oa) {
+        STEP("rest_ad", 2 * o, 1, w * (Nl[2 * o] + Nl[2 * o + 1]));
+        if ((e = fast2_rest_ad<T>(rAf[o], rDf[o], M[o], st))) return e;
+      } else {
+        STEP("rest_ad", 2 * o, 1, w * (Nl[2 * o] + Nl[2 * o + 1]));
+        if ((e = fast2_rest_ad<T>(rAf[o], rDf[o], M[o], st))) return e;
+      }
+      STEP("rest_da", 2 * o + 1, 1, w * (Nl[2 * o + 1] + Nl[2 * o + 2]));
+      if ((e = fast2_rest_da<T>(rDf[o], rAf[o + 1], M[o + 1], st))) return e;
+    }
+    STEP("coarse", 2 * oc, 1, 0);
+    launch2_coarse<T>(d_lev, oc, k, s->d_counter, st);
+    for (int o = oc - 1; o >= oa; o--) {
+      STEP("jac_d", 2 * o + 1, 1, w * (Nl[2 * o + 2] + 2 * Nl[2 * o + 1]));
+      if ((e = fast2_jac_d<T>(vAf[o + 1], rDf[o], vDf[o], M[o], cD[o], st))) return e;
+      STEP("jac_a", 2 * o, 1, w * (Nl[2 * o + 1] + 2 * Nl[2 * o]));
+      if ((e = fast2_jac_a<T>(vDf[o], rAf[o], vAf[o], M[o], cA[o], st))) return e;
+    }
+    // ---- distributed ascent
+    for (int o = oa - 1; o >= 0; o--) {
+      STEP("jac_d", 2 * o + 1, nloc, w * (Nl[2 * o + 2] + 2 * Nl[2 * o + 1]));
+      if (o + 1 < oa && (e = xchg(o + 1, false, 1, st, [&](int i) { return rk[i].vA[o + 1].p; }, rk[0].vA[o + 1].pitch)))
+        return e;
+      for (int i = 0; i < nloc; i++) {
+        const D2<T> &vc = (o + 1 < oa) ? rk[i].vA[o + 1] : vAf[oa];
+        if ((e = fast2_jac_d<T>(vc, rk[i].rD[o], rk[i].vD[o], M[o], cD[o], st, rows_half(o, rk[i].q)))) return e;
+      }
+      if ((e = xchg(o, true, 1, st, [&](int i) { return rk[i].vD[o].e; }, rk[0].vD[o].pitch)) ||
+          (e = xchg(o, true, 1, st, [&](int i) { return rk[i].vD[o].o; }, rk[0].vD[o].pitch)))
+        return e;
+      if (o >= 1) {
+        STEP("jac_a", 2 * o, nloc, w * (Nl[2 * o + 1] + 2 * Nl[2 * o]));
+        for (int i = 0; i < nloc; i++)
+          if ((e = fast2_jac_a<T>(rk[i].vD[o], rk[i].rA[o], rk[i].vA[o], M[o], cA[o], st, rows_full(o, rk[i].q))))
+            return e;
+      } else {
+        STEP("asc_fine", 0, nloc, w * (Nl[1] + 3 * Nl[0]));
+        for (int i = 0; i < nloc; i++)
+          if ((e = fast2_asc_fine<T>(rk[i].vD[0], uin[i], fe[i], pitch, uout[i], M[0], s->cfg.order, cA[0], coef, st,
+                                     rows_full(0, rk[i].q))))
+            return e;
+      }
+    }
+    (void)L;
+    return cudaSuccess;
+  }
+
+  // virtual global-row-0 pointer of a caller slab (NCCL mode)
+  template <class P_>
+  P_ *vg(P_ *ptr) const {
+    return ptr - (int64_t)(lo(0, s->cfg.rank) - 2) * pitch;
+  }
+
+  void enqueue_cycle(const void *u_in, void *u_out, const void *f_eff, cudaStream_t st, Prof *prof) override {
+    // NCCL mode: one local rank; the caller's arrays are slabs
+    std::vector<const T *> ui{vg((const T *)u_in)}, fe{vg((const T *)f_eff)};
+    std::vector<T *> uo{vg((T *)u_out)};
+    cudaError_t e = cycle(ui, uo, fe, st, prof);
+    if (e) cudaGetLastError(), last = e;
+  }
+  cudaError_t last = cudaSuccess;
+
+  void enqueue_final_norm(void *u, const void *f_eff, cudaStream_t st) override {
+    const T *ui = vg((const T *)u), *fe = vg((const T *)f_eff);
+    xchg(0, false, 2, st, [&](int) { return ui; }, pitch);
+    xchg(0, false, 1, st, [&](int) { return fe; }, pitch);
+    fast2_desc_fine<T>(ui, fe, pitch, rk[0].rD[0], M[0], s->cfg.order, coef, sink(), st, rows_full(0, rk[0].q));
+  }
+  cudaError_t reduce_hist(unsigned long long *d, int nslots, cudaStream_t st) override {
+    return comm->allreduce_max_u64(d, nslots, st);
+  }
+  // f~ (order 4) on the slab: f's ghost row first, then the own rows
+  void enqueue_ftilde(const void *f, void *ft, cudaStream_t st) override {
+    if (loop) {
+      launch2_ftilde<T>(D2<const T>{(const T *)f, pitch}, D2<T>{(T *)ft, pitch}, M[0], st);
+      return;
+    }
+    const T *fv = vg((const T *)f);
+    xchg(0, false, 1, st, [&](int) { return fv; }, pitch);
+    launch2_ftilde_rows<T>(D2<const T>{fv, pitch}, D2<T>{vg((T *)ft), pitch}, M[0], lo(0, rk[0].q), hi(0, rk[0].q), st);
+  }
+  void enqueue_residual(const void *u, const void *f, void *r, cudaStream_t st) override {
+    if (loop) {
+      launch2_residual<T>(D2<const T>{(const T *)u, pitch}, D2<const T>{(const T *)f, pitch}, D2<T>{(T *)r, pitch},
+                          M[0], s->cfg.order, coef, st);
+      return;
+    }
+    const T *uv = vg((const T *)u), *fv = vg((const T *)f);
+    xchg(0, false, 1, st, [&](int) { return uv; }, pitch);
+    launch2_residual_rows<T>(D2<const T>{uv, pitch}, D2<const T>{fv, pitch}, D2<T>{vg((T *)r), pitch}, M[0],
+                             s->cfg.order, coef, lo(0, rk[0].q), hi(0, rk[0].q), st);
+  }
+  void enqueue_norm(const void *x, unsigned long long *mx, double *ss, cudaStream_t st) override {
+    if (loop) {
+      launch2_norm<T>(D2<const T>{(const T *)x, pitch}, M[0], mx, ss, st);
+      return;
+    }
+    launch2_norm_rows<T>(D2<const T>{vg((const T *)x), pitch}, M[0], lo(0, rk[0].q), hi(0, rk[0].q), mx, ss, st);
+    comm->allreduce_max_u64(mx, 1, st);
+    comm->allreduce_sum_f64(ss, 1, st);
+  }
+  int launches_per_cycle() const override {
+    int c = nloc;   // desc
+    for (int o = 0; o < oa; o++) c += ((o >= 1) + 1) * nloc;
+    for (int o = oa; o < oc; o++) c += 2;
+    c += 1;
+    for (int o = oc - 1; o >= oa; o--) c += 2;
+    for (int o = oa - 1; o >= 0; o--) c += 2 * nloc;
+    return c;
+  }
+
+  // ---- loopback: the whole mg_vcycle on full caller arrays
+  int vcycle_all(mg_solver *sv, void *u, const void *f, int ncycles, double *res_hist) override {
+    if (!loop) return 1;
+    cudaStream_t st = sv->st;
+    const size_t pb = pitch * sizeof(T);
+    const T *fsrc = (const T *)f;
+    if (s->cfg.order == 4) {
+      launch2_ftilde<T>(D2<const T>{(const T *)f, pitch}, uf_scratch, M[0], st);
+      fsrc = uf_scratch.p;
+    }
+    // scatter: rows [lo-2, hi+2) clipped to the grid
+    for (int i = 0; i < nloc; i++) {
+      int a = std::max(lo(0, i) - 2, 0), b = std::min(hi(0, i) + 2, (int)n);
+      for (int j = 0; j < 2; j++) cudaMemsetAsync(rk[i].u[j].p + (int64_t)(lo(0, i) - 2) * pitch, 0, (R(0) + 4) * pb, st);
+      cudaMemsetAsync(rk[i].f.p + (int64_t)(lo(0, i) - 2) * pitch, 0, (R(0) + 4) * pb, st);
+      cudaMemcpyAsync(rk[i].u[0].p + (int64_t)a * pitch, (const T *)u + (int64_t)a * pitch, (b - a) * pb,
+                      cudaMemcpyDeviceToDevice, st);
+      cudaMemcpyAsync(rk[i].f.p + (int64_t)a * pitch, fsrc + (int64_t)a * pitch, (b - a) * pb, cudaMemcpyDeviceToDevice,
+                      st);
+    }
+    int nslots = ncycles + 1 < kHistCap ? ncycles + 1 : kHistCap;
+    cudaMemsetAsync(sv->d_hist, 0, sizeof(unsigned long long) * nslots, st);
+    cudaMemsetAsync(sv->d_counter, 0, sizeof(int), st);
+    std::vector<const T *> fe(nloc);
+    for (int i = 0; i < nloc; i++) fe[i] = rk[i].f.p;
+    int cur = 0;
+    for (int c = 0; c < ncycles; c++) {
+      std::vector<const T *> ui(nloc);
+      std::vector<T *> uo(nloc);
+      for (int i = 0; i < nloc; i++) {
+        ui[i] = rk[i].u[cur].p;
+        uo[i] = rk[i].u[cur ^ 1].p;
+      }
+      cudaError_t e = cycle(ui, uo, fe, st, nullptr);
+      if (e) return fail(sv, MG_ECUDA, std::string("loopback cycle: ") + cudaGetErrorString(e));
+      cur ^= 1;
+    }
+    if (res_hist) {
+      std::vector<const T *> ui(nloc);
+      for (int i = 0; i < nloc; i++) ui[i] = rk[i].u[cur].p;
+      xchg(0, false, 2, st, [&](int i) { return ui[i]; }, pitch);
+      xchg(0, false, 1, st, [&](int i) { return fe[i]; }, pitch);
+      for (int i = 0; i < nloc; i++)
+        fast2_desc_fine<T>(ui[i], fe[i], pitch, rk[i].rD[0], M[0], s->cfg.order, coef, sink(), st, rows_full(0, i));
+    }
+    // gather own rows back
+    for (int i = 0; i < nloc; i++)
+      cudaMemcpyAsync((T *)u + (int64_t)lo(0, i) * pitch, rk[i].u[cur].p + (int64_t)lo(0, i) * pitch, R(0) * pb,
+                      cudaMemcpyDeviceToDevice, st);
+    CKS(sv, cudaGetLastError());
+    if (res_hist) {
+      CKS(sv, cudaMemcpyAsync(sv->h_hist, sv->d_hist, sizeof(unsigned long long) * nslots, cudaMemcpyDeviceToHost, st));
+      CKS(sv, cudaStreamSynchronize(st));
+      bool finite = true;
+      for (int i = 0; i <= ncycles; i++) {
+        double v;
+        unsigned long long bb = sv->h_hist[i < kHistCap ? i : kHistCap - 1];
+        std::memcpy(&v, &bb, sizeof v);
+        res_hist[i] = v;
+        if (!std::isfinite(v)) finite = false;
+      }
+      if (!finite) return fail(sv, MG_EDIVERGED, "non-finite residual norm");
+    }
+    return MG_OK;
+  }
+};
+
+// factory used by mg_create_ex
+ImplBase *make_dist2(mg_solver *s, bool loopback, std::string *err) {
+  ImplBase *impl = nullptr;
+  Comm2 *c = nullptr;
+  if (loopback) {
+    c = new LoopComm();
+    c->P = s->cfg.nranks;
+  } else {
+    NcclComm *nc = new NcclComm();
+    if (!nc->init(s->cfg.nranks, s->cfg.rank, s->cfg.nccl_id, s->esz)) {
+      *err = nc->err;
+      delete nc;
+      return nullptr;
+    }
+    c = nc;
+  }
+  if (s->cfg.dtype == MG_F64) {
+    auto *d = new Dist2<double>(s, loopback);
+    d->comm.reset(c);
+    impl = d;
+  } else {
+    auto *d = new Dist2<float>(s, loopback);
+    d->comm.reset(c);
+    impl = d;
+  }
+  return impl;
+}
+
+int nccl_unique_id(void *out, std::string *err) {
+  if (!nccl().load()) {
+    *err = nccl().why;
+    return MG_ENCCL;
+  }
+  ncclUniqueId id;
+  if (nccl().GetUniqueId(&id) != 0) {
+    *err = "ncclGetUniqueId failed";
+    return MG_ENCCL;
+  }
+  std::memcpy(out, &id, sizeof id);
+  return MG_OK;
+}

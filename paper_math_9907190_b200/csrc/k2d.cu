@@ -234,7 +234,89 @@ __global__ void __launch_bounds__(NT) k2_norm(D2<const T> a, int M, unsigned lon
   }
 }
 
+// Row-ranged variants for slabs (multi-GPU): rows [ylo, yhi) only.
+template <class T>
+__global__ void __launch_bounds__(NT) k2_ftilde_rows(D2<const T> f, D2<T> ft, int M, int ylo, int yhi) {
+  int W = M - 1;
+  int64_t t = (int64_t)blockIdx.x * NT + threadIdx.x;
+  if (t >= (int64_t)W * (yhi - ylo)) return;
+  int x = (int)(t % W) + 1, y = (int)(t / W) + ylo;
+  if (y < 1 || y > M - 1) return;
+  T s = (T)8 * f(x, y);
+  s = s + f(x + 1, y);
+  s = s + f(x, y + 1);
+  s = s + f(x - 1, y);
+  s = s + f(x, y - 1);
+  ft(x, y) = s * (T)(1.0 / 12.0);
+}
+
+template <class T, int ORDER>
+__global__ void __launch_bounds__(NT) k2_residual_rows(D2<const T> u, D2<const T> f, D2<T> r, int M, Coef<T> k, int ylo,
+                                                       int yhi) {
+  int64_t t = (int64_t)blockIdx.x * NT + threadIdx.x;
+  int Wd = M + 1;
+  if (t >= (int64_t)Wd * (yhi - ylo)) return;
+  int x = (int)(t % Wd), y = (int)(t / Wd) + ylo;
+  r(x, y) = res2z<T, ORDER>(u, f, x, y, M, k);
+}
+
+template <class T>
+__global__ void __launch_bounds__(NT) k2_norm_rows(D2<const T> a, int M, int ylo, int yhi, unsigned long long *mx_out,
+                                                   double *ss_out) {
+  int W = M - 1;
+  double mx = 0.0, ss = 0.0;
+  for (int64_t t = (int64_t)blockIdx.x * NT + threadIdx.x; t < (int64_t)W * (yhi - ylo); t += (int64_t)gridDim.x * NT) {
+    int x = (int)(t % W) + 1, y = (int)(t / W) + ylo;
+    if (y < 1 || y > M - 1) continue;
+    double v = (double)a(x, y);
+    mx = nmax(mx, fabs(v));
+    ss += v * v;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    ss += __shfl_xor_sync(0xffffffffu, ss, o);
+    mx = nmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  }
+  __shared__ double rs[NT / 32], rm[NT / 32];
+  int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  if (lane == 0) {
+    rs[wid] = ss;
+    rm[wid] = mx;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s2 = 0.0, m2 = 0.0;
+    for (int i = 0; i < NT / 32; i++) {
+      s2 += rs[i];
+      m2 = nmax(m2, rm[i]);
+    }
+    atomicAdd(ss_out, s2);
+    atomicMax(mx_out, (unsigned long long)__double_as_longlong(m2));
+  }
+}
+
 // ================================================================ launchers
+
+template <class T>
+void launch2_ftilde_rows(const D2<const T> &f, const D2<T> &ft, int M, int ylo, int yhi, cudaStream_t st) {
+  int64_t W = M - 1;
+  if (yhi > ylo) k2_ftilde_rows<T><<<blocks_for(W * (yhi - ylo)), NT, 0, st>>>(f, ft, M, ylo, yhi);
+}
+template <class T>
+void launch2_residual_rows(const D2<const T> &u, const D2<const T> &f, const D2<T> &r, int M, int order,
+                           const Coef<T> &k, int ylo, int yhi, cudaStream_t st) {
+  int64_t W = M + 1;
+  if (yhi <= ylo) return;
+  if (order == 2)
+    k2_residual_rows<T, 2><<<blocks_for(W * (yhi - ylo)), NT, 0, st>>>(u, f, r, M, k, ylo, yhi);
+  else
+    k2_residual_rows<T, 4><<<blocks_for(W * (yhi - ylo)), NT, 0, st>>>(u, f, r, M, k, ylo, yhi);
+}
+template <class T>
+void launch2_norm_rows(const D2<const T> &a, int M, int ylo, int yhi, unsigned long long *mx, double *ss,
+                       cudaStream_t st) {
+  k2_norm_rows<T><<<148 * 4, NT, 0, st>>>(a, M, ylo, yhi, mx, ss);
+}
 
 template <class T>
 static D2<const T> cd(const D2<T> &a) {
@@ -327,6 +409,11 @@ void launch2_norm(const D2<const T> &a, int M, unsigned long long *mx, double *s
 }
 
 #define INST(T)                                                                                                     \
+  template void launch2_ftilde_rows<T>(const D2<const T> &, const D2<T> &, int, int, int, cudaStream_t);           \
+  template void launch2_residual_rows<T>(const D2<const T> &, const D2<const T> &, const D2<T> &, int, int,        \
+                                         const Coef<T> &, int, int, cudaStream_t);                                 \
+  template void launch2_norm_rows<T>(const D2<const T> &, int, int, int, unsigned long long *, double *,           \
+                                     cudaStream_t);                                                                \
   template void launch2_desc_fine<T>(const D2<const T> &, const D2<const T> &, const S2<T> &, int, int,            \
                                      const Coef<T> &, const NormSink &, cudaStream_t);                             \
   template void launch2_rest_ad<T>(const D2<T> &, const S2<T> &, int, cudaStream_t);                               \

@@ -139,6 +139,7 @@ struct OpDesc2Fine {
     int M, ntx, ntiles;
     Coef<T> k;
     NormSink ns;
+    int ylo, yhi, yo, yh;   // output rows [ylo, yhi); TMA y = global y - yo (full rows) / - yh (half rows)
   };
   struct Acc {
     double mx;
@@ -149,10 +150,10 @@ struct OpDesc2Fine {
   }
   static __device__ void init(Acc &a) { a.mx = 0.0; }
   static __device__ void issue(const Params &P, int t, unsigned char *st, uint64_t *bar) {
-    int x0 = (t % P.ntx) * TX, y0 = (t / P.ntx) * TY;
+    int x0 = (t % P.ntx) * TX, y0 = P.ylo + (t / P.ntx) * TY;
     mbar_expect_tx(bar, U_BYTES + F_BYTES);
-    tma_load_2d(st + U_OFF, &P.tu, x0 - HU, y0 - 2, bar);
-    tma_load_2d(st + F_OFF, &P.tf, x0 - HF, y0 - 1, bar);
+    tma_load_2d(st + U_OFF, &P.tu, x0 - HU, y0 - 2 - P.yo, bar);
+    tma_load_2d(st + F_OFF, &P.tf, x0 - HF, y0 - 1 - P.yo, bar);
   }
   // residual at (xl, y) and (xl + 1, y), 0 outside the interior
   static __device__ __forceinline__ void rpair(const STile<T> &U, const STile<T> &F, int xl, int y, int M,
@@ -181,7 +182,7 @@ struct OpDesc2Fine {
     r1 = inside(xl + 1, y, M) ? res2v<T, ORDER>(q1, f1, k) : (T)0;
   }
   static __device__ void compute(const Params &P, int t, unsigned char *st, unsigned char *scr, Acc &acc) {
-    const int x0 = (t % P.ntx) * TX, y0 = (t / P.ntx) * TY, M = P.M;
+    const int x0 = (t % P.ntx) * TX, y0 = P.ylo + (t / P.ntx) * TY, M = P.M, yhi = P.yhi;
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, xl = x0 + 2 * lane;
     STile<T> U = stile<T>(st + U_OFF, UW, x0 - HU, y0 - 2);
     STile<T> F = stile<T>(st + F_OFF, FW, x0 - HF, y0 - 1);
@@ -191,7 +192,7 @@ struct OpDesc2Fine {
     for (int y = y0 + w; y < y0 + TY; y += NW) {
       rpair(U, F, xl, y, M, P.k, r0, r1);
       st2(R.at(xl, y), r0, r1);
-      acc.mx = nmax(nmax(acc.mx, absd(r0)), absd(r1));
+      if (y < yhi) acc.mx = nmax(nmax(acc.mx, absd(r0)), absd(r1));
     }
     if (w < 2) {   // ring rows
       int y = w == 0 ? y0 - 1 : y0 + TY;
@@ -210,6 +211,7 @@ struct OpDesc2Fine {
       T rc, rE, rN, ro;
       ld2(R.at(xl, y), rc, rE);
       ld2(R.at(xl, y + 1), rN, ro);
+      if (y >= yhi) continue;
       int64_t o = (int64_t)(y / 2) * pitch + xl / 2;
       if (xl >= 2 && xl <= M - 2 && y >= 2 && y <= M - 2)
         P.out.e[o] = erest2r(rc, R(xl - 1, y), R(xl, y - 1), rE, rN);
@@ -232,17 +234,18 @@ struct OpRest2AD {
     CUtensorMap tr;
     S2<T> out;
     int M, ntx, ntiles;
+    int ylo, yhi, yo, yh;
   };
   using Acc = NoAcc;
   static __device__ void prefetch(const Params &P) { tma_prefetch_desc(&P.tr); }
   static __device__ void init(Acc &) {}
   static __device__ void issue(const Params &P, int t, unsigned char *st, uint64_t *bar) {
-    int x0 = (t % P.ntx) * TX, y0 = (t / P.ntx) * TY;
+    int x0 = (t % P.ntx) * TX, y0 = P.ylo + (t / P.ntx) * TY;
     mbar_expect_tx(bar, R_BYTES);
-    tma_load_2d(st, &P.tr, x0 - HR, y0 - 1, bar);
+    tma_load_2d(st, &P.tr, x0 - HR, y0 - 1 - P.yo, bar);
   }
   static __device__ void compute(const Params &P, int t, unsigned char *st, unsigned char *, Acc &) {
-    const int x0 = (t % P.ntx) * TX, y0 = (t / P.ntx) * TY, M = P.M;
+    const int x0 = (t % P.ntx) * TX, y0 = P.ylo + (t / P.ntx) * TY, M = P.M, yhi = P.yhi;
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, xl = x0 + 2 * lane;
     STile<T> R = stile<T>(st, RW, x0 - HR, y0 - 1);
     const int64_t pitch = P.out.pitch;
@@ -252,6 +255,7 @@ struct OpRest2AD {
       T rc, rE, rN, ro;
       ld2(R.at(xl, y), rc, rE);
       ld2(R.at(xl, y + 1), rN, ro);
+      if (y >= yhi) continue;
       int64_t o = (int64_t)(y / 2) * pitch + xl / 2;
       if (xl >= 2 && xl <= M - 2 && y >= 2 && y <= M - 2)
         P.out.e[o] = erest2r(rc, R(xl - 1, y), R(xl, y - 1), rE, rN);
@@ -276,6 +280,7 @@ struct OpRest2DA {
     CUtensorMap te, to;
     D2<T> out;
     int Mc, ntx, ntiles;
+    int ylo, yhi, yo, yh;
   };
   using Acc = NoAcc;
   static __device__ void prefetch(const Params &P) {
@@ -284,19 +289,19 @@ struct OpRest2DA {
   }
   static __device__ void init(Acc &) {}
   static __device__ void issue(const Params &P, int t, unsigned char *st, uint64_t *bar) {
-    int X0 = (t % P.ntx) * TX, Y0 = (t / P.ntx) * TY;
+    int X0 = (t % P.ntx) * TX, Y0 = P.ylo + (t / P.ntx) * TY;
     mbar_expect_tx(bar, E_BYTES + O_BYTES);
-    tma_load_2d(st + E_OFF, &P.te, X0, Y0, bar);
-    tma_load_2d(st + O_OFF, &P.to, X0 - HO, Y0 - 1, bar);
+    tma_load_2d(st + E_OFF, &P.te, X0, Y0 - P.yh, bar);
+    tma_load_2d(st + O_OFF, &P.to, X0 - HO, Y0 - 1 - P.yh, bar);
   }
   static __device__ void compute(const Params &P, int t, unsigned char *st, unsigned char *, Acc &) {
-    const int X0 = (t % P.ntx) * TX, Y0 = (t / P.ntx) * TY, Mc = P.Mc;
+    const int X0 = (t % P.ntx) * TX, Y0 = P.ylo + (t / P.ntx) * TY, Mc = P.Mc, yhi = P.yhi;
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, X = X0 + 2 * lane;
     STile<T> E = stile<T>(st + E_OFF, EW, X0, Y0);
     STile<T> O = stile<T>(st + O_OFF, OW, X0 - HO, Y0 - 1);
 #pragma unroll
     for (int Y = Y0 + w; Y < Y0 + TY; Y += NW) {
-      if (Y < 1 || Y > Mc - 1) continue;
+      if (Y < 1 || Y > Mc - 1 || Y >= yhi) continue;
       T e0, e1, s0, s1, n0, n1;
       ld2(E.at(X, Y), e0, e1);
       ld2(O.at(X, Y - 1), s0, s1);
@@ -337,6 +342,7 @@ struct OpJac2D {
     S2<T> v;
     int M, ntx, ntiles;
     T c;
+    int ylo, yhi, yo, yh;
   };
   using Acc = NoAcc;
   static __device__ void prefetch(const Params &P) {
@@ -346,14 +352,14 @@ struct OpJac2D {
   }
   static __device__ void init(Acc &) {}
   static __device__ void issue(const Params &P, int t, unsigned char *st, uint64_t *bar) {
-    int a0 = (t % P.ntx) * TX, b0 = (t / P.ntx) * TY;
+    int a0 = (t % P.ntx) * TX, b0 = P.ylo + (t / P.ntx) * TY;
     mbar_expect_tx(bar, A_BYTES + RO_BYTES + RE_BYTES);
-    tma_load_2d(st + A_OFF, &P.tva, a0 - HA, b0 - 1, bar);
-    tma_load_2d(st + RO_OFF, &P.tro, a0 - HA, b0 - 1, bar);
-    tma_load_2d(st + RE_OFF, &P.tre, a0, b0, bar);
+    tma_load_2d(st + A_OFF, &P.tva, a0 - HA, b0 - 1 - P.yh, bar);
+    tma_load_2d(st + RO_OFF, &P.tro, a0 - HA, b0 - 1 - P.yh, bar);
+    tma_load_2d(st + RE_OFF, &P.tre, a0, b0 - P.yh, bar);
   }
   static __device__ void compute(const Params &P, int t, unsigned char *st, unsigned char *scr, Acc &) {
-    const int a0 = (t % P.ntx) * TX, b0 = (t / P.ntx) * TY, W = P.M / 2;
+    const int a0 = (t % P.ntx) * TX, b0 = P.ylo + (t / P.ntx) * TY, W = P.M / 2, yhi = P.yhi;
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, a = a0 + 2 * lane;
     const T c = P.c;
     STile<T> VA = stile<T>(st + A_OFF, AW, a0 - HA, b0 - 1);
@@ -372,7 +378,7 @@ struct OpJac2D {
       T v0 = (okb && a <= W - 1) ? jac4(c, ro0, va0, va1, vb1, vb0) : (T)0;
       T v1 = (okb && a + 1 <= W - 1) ? jac4(c, ro1, va1, va2, vb2, vb1) : (T)0;
       st2(V.at(a, b), v0, v1);
-      if (okb && b >= b0) {
+      if (okb && b >= b0 && b < yhi) {
         if (a + 1 <= W - 1)
           st2(&P.v.o[(int64_t)b * pitch + a], v0, v1);
         else if (a <= W - 1)
@@ -392,7 +398,7 @@ struct OpJac2D {
     // colour 2 (Eajacb) on E nodes, from the new O values (D(s) residual, reading A10)
 #pragma unroll
     for (int b = b0 + w; b < b0 + TY; b += NW) {
-      if (b < 1 || b > W - 1) continue;
+      if (b < 1 || b > W - 1 || b >= yhi) continue;
       T re0, re1, s0, s1, n0, n1;
       ld2(RE.at(a, b), re0, re1);
       ld2(V.at(a, b - 1), s0, s1);
@@ -439,6 +445,7 @@ struct OpJac2A {
     int M, ntx, ntiles;
     T c;
     Coef<T> k;
+    int ylo, yhi, yo, yh;
   };
   using Acc = NoAcc;
   static __device__ void prefetch(const Params &P) {
@@ -449,19 +456,19 @@ struct OpJac2A {
   }
   static __device__ void init(Acc &) {}
   static __device__ void issue(const Params &P, int t, unsigned char *st, uint64_t *bar) {
-    int x0 = (t % P.ntx) * TX, y0 = (t / P.ntx) * TY;
+    int x0 = (t % P.ntx) * TX, y0 = P.ylo + (t / P.ntx) * TY;
     mbar_expect_tx(bar, U_BYTES + F_BYTES + 2 * V_BYTES);
-    if (FINE) tma_load_2d(st + U_OFF, &P.tu, x0 - HU, y0 - 2, bar);
-    tma_load_2d(st + F_OFF, &P.tf, x0 - HF, y0 - 1, bar);
-    tma_load_2d(st + VE_OFF, &P.tve, x0 / 2 - HV, y0 / 2 - 1, bar);
-    tma_load_2d(st + VO_OFF, &P.tvo, x0 / 2 - HV, y0 / 2 - 1, bar);
+    if (FINE) tma_load_2d(st + U_OFF, &P.tu, x0 - HU, y0 - 2 - P.yo, bar);
+    tma_load_2d(st + F_OFF, &P.tf, x0 - HF, y0 - 1 - P.yo, bar);
+    tma_load_2d(st + VE_OFF, &P.tve, x0 / 2 - HV, y0 / 2 - 1 - P.yh, bar);
+    tma_load_2d(st + VO_OFF, &P.tvo, x0 / 2 - HV, y0 / 2 - 1 - P.yh, bar);
   }
   static __device__ __forceinline__ T rnode(const Params &P, const STile<T> &U, const STile<T> &F, int x, int y) {
     if (FINE) return res2<T, ORDER>(U, F, x, y, P.k);
     return F(x, y);
   }
   static __device__ void compute(const Params &P, int t, unsigned char *st, unsigned char *scr, Acc &) {
-    const int x0 = (t % P.ntx) * TX, y0 = (t / P.ntx) * TY, M = P.M;
+    const int x0 = (t % P.ntx) * TX, y0 = P.ylo + (t / P.ntx) * TY, M = P.M, yhi = P.yhi;
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, xl = x0 + 2 * lane, hl = xl >> 1;
     const T c = P.c;
     STile<T> U = stile<T>(st + U_OFF, UW, x0 - HU, y0 - 2);
@@ -506,7 +513,7 @@ struct OpJac2A {
     // colour 2: the D(s) node of the pair from the new green values
 #pragma unroll
     for (int y = y0 + w; y < y0 + TY; y += NW) {
-      if (y < 1 || y > M - 1) continue;
+      if (y < 1 || y > M - 1 || y >= yhi) continue;
       T g = G(p, y), v0, v1;
       if ((y & 1) == 0) {   // D node at xl, green at xl+1
         v1 = g;
@@ -588,6 +595,12 @@ static bool tm2(CUtensorMap *tm, const void *p, int64_t nx, int64_t ny, int64_t 
   return encode_tmap(tm, p, sizeof(T), 2, dims, (uint64_t)pitch, 0, box);
 }
 
+// Row ranges for slab-decomposed (multi-GPU) levels; the default is the
+// whole level.  Output rows [ylo, yhi) are written; inputs are local
+// allocations whose row 0 is global row fy0 (full-resolution rows) or hy0
+// (half rows, E/O and coarser), with frows / hrows rows.
+static inline int tiles_y(int ylo, int yhi) { return yhi > ylo ? (yhi - ylo + TY - 1) / TY : 0; }
+
 template <class T, int ORDER>
 struct DescS {
   template <int S>
@@ -596,25 +609,32 @@ struct DescS {
 
 template <class T, int ORDER>
 static cudaError_t desc_impl(const T *u, const T *f, int64_t pitch, const S2<T> &d, int M, const Coef<T> &k,
-                             const NormSink &ns, cudaStream_t st) {
+                             const NormSink &ns, cudaStream_t st, const Rows2 &rw) {
   using Op = OpDesc2Fine<T, ORDER, 2>;   // Params do not depend on the stage count
   typename Op::Params P{};
-  if (!tm2<T>(&P.tu, u, M + 1, M + 1, pitch, Op::UW, Op::UH) || !tm2<T>(&P.tf, f, M + 1, M + 1, pitch, Op::FW, Op::FH))
+  const int yhi = rw.yhi < 0 ? M : rw.yhi, frows = rw.frows < 0 ? M + 1 : rw.frows;
+  if (!tm2<T>(&P.tu, u + (int64_t)rw.fy0 * pitch, M + 1, frows, pitch, Op::UW, Op::UH) ||
+      !tm2<T>(&P.tf, f + (int64_t)rw.fy0 * pitch, M + 1, frows, pitch, Op::FW, Op::FH))
     return cudaErrorInvalidValue;
-  int ntx = (M + TX - 1) / TX, nty = (M + TY - 1) / TY;
+  int ntx = (M + TX - 1) / TX, nty = tiles_y(rw.ylo, yhi);
   P.out = d;
   P.M = M;
   P.ntx = ntx;
   P.ntiles = ntx * nty;
   P.k = k;
   P.ns = ns;
+  P.ylo = rw.ylo;
+  P.yhi = yhi;
+  P.yo = rw.fy0;
+  P.yh = rw.hy0;
   return run_staged<DescS<T, ORDER>::template op>(P, st);
 }
 
 template <class T>
 cudaError_t fast2_desc_fine(const T *u, const T *f, int64_t pitch, const S2<T> &d, int M, int order, const Coef<T> &k,
-                            const NormSink &ns, cudaStream_t st) {
-  return order == 2 ? desc_impl<T, 2>(u, f, pitch, d, M, k, ns, st) : desc_impl<T, 4>(u, f, pitch, d, M, k, ns, st);
+                            const NormSink &ns, cudaStream_t st, const Rows2 &rw) {
+  return order == 2 ? desc_impl<T, 2>(u, f, pitch, d, M, k, ns, st, rw)
+                    : desc_impl<T, 4>(u, f, pitch, d, M, k, ns, st, rw);
 }
 
 template <class T, int ORDER, bool FINE>
@@ -625,36 +645,44 @@ struct JacAS {
 
 template <class T, int ORDER, bool FINE>
 static cudaError_t jac_a_impl(const T *u, const T *f_or_r, int64_t pitch_u, int64_t pitch_f, const S2<T> &vd,
-                              const D2<T> &out, int M, T c, const Coef<T> &k, cudaStream_t st) {
+                              const D2<T> &out, int M, T c, const Coef<T> &k, cudaStream_t st, const Rows2 &rw) {
   using Op = OpJac2A<T, ORDER, FINE, 2>;
   typename Op::Params P{};
-  int H = M / 2 + 1;
-  if (FINE && !tm2<T>(&P.tu, u, M + 1, M + 1, pitch_u, Op::UW, Op::UH)) return cudaErrorInvalidValue;
-  if (!tm2<T>(&P.tf, f_or_r, M + 1, M + 1, pitch_f, Op::FW, Op::FH) ||
-      !tm2<T>(&P.tve, vd.e, H, H, vd.pitch, Op::VW, Op::VH) || !tm2<T>(&P.tvo, vd.o, H, H, vd.pitch, Op::VW, Op::VH))
+  const int H = M / 2 + 1;
+  const int yhi = rw.yhi < 0 ? M : rw.yhi, frows = rw.frows < 0 ? M + 1 : rw.frows,
+            hrows = rw.hrows < 0 ? H : rw.hrows;
+  if (FINE && !tm2<T>(&P.tu, u + (int64_t)rw.fy0 * pitch_u, M + 1, frows, pitch_u, Op::UW, Op::UH))
     return cudaErrorInvalidValue;
-  int ntx = (M + TX - 1) / TX, nty = (M + TY - 1) / TY;
+  if (!tm2<T>(&P.tf, f_or_r + (int64_t)rw.fy0 * pitch_f, M + 1, frows, pitch_f, Op::FW, Op::FH) ||
+      !tm2<T>(&P.tve, vd.e + (int64_t)rw.hy0 * vd.pitch, H, hrows, vd.pitch, Op::VW, Op::VH) ||
+      !tm2<T>(&P.tvo, vd.o + (int64_t)rw.hy0 * vd.pitch, H, hrows, vd.pitch, Op::VW, Op::VH))
+    return cudaErrorInvalidValue;
+  int ntx = (M + TX - 1) / TX, nty = tiles_y(rw.ylo, yhi);
   P.out = out;
   P.M = M;
   P.ntx = ntx;
   P.ntiles = ntx * nty;
   P.c = c;
   P.k = k;
+  P.ylo = rw.ylo;
+  P.yhi = yhi;
+  P.yo = rw.fy0;
+  P.yh = rw.hy0;
   return run_staged<JacAS<T, ORDER, FINE>::template op>(P, st);
 }
 
 template <class T>
 cudaError_t fast2_asc_fine(const S2<T> &vd, const T *u_old, const T *f, int64_t pitch, T *u_new, int M, int order, T c,
-                           const Coef<T> &k, cudaStream_t st) {
+                           const Coef<T> &k, cudaStream_t st, const Rows2 &rw) {
   D2<T> out{u_new, pitch};
-  if (order == 2) return jac_a_impl<T, 2, true>(u_old, f, pitch, pitch, vd, out, M, c, k, st);
-  return jac_a_impl<T, 4, true>(u_old, f, pitch, pitch, vd, out, M, c, k, st);
+  if (order == 2) return jac_a_impl<T, 2, true>(u_old, f, pitch, pitch, vd, out, M, c, k, st, rw);
+  return jac_a_impl<T, 4, true>(u_old, f, pitch, pitch, vd, out, M, c, k, st, rw);
 }
 
 template <class T>
-cudaError_t fast2_jac_a(const S2<T> &vd, const D2<T> &r, const D2<T> &v, int M, T c, cudaStream_t st) {
+cudaError_t fast2_jac_a(const S2<T> &vd, const D2<T> &r, const D2<T> &v, int M, T c, cudaStream_t st, const Rows2 &rw) {
   Coef<T> k{};
-  return jac_a_impl<T, 2, false>(nullptr, r.p, 0, r.pitch, vd, v, M, c, k, st);
+  return jac_a_impl<T, 2, false>(nullptr, r.p, 0, r.pitch, vd, v, M, c, k, st, rw);
 }
 
 template <class T>
@@ -674,60 +702,80 @@ struct JacDS {
 };
 
 template <class T>
-cudaError_t fast2_rest_ad(const D2<T> &r, const S2<T> &d, int M, cudaStream_t st) {
+cudaError_t fast2_rest_ad(const D2<T> &r, const S2<T> &d, int M, cudaStream_t st, const Rows2 &rw) {
   using Op = OpRest2AD<T, 2>;
   typename Op::Params P{};
-  if (!tm2<T>(&P.tr, r.p, M + 1, M + 1, r.pitch, Op::RW, Op::RH)) return cudaErrorInvalidValue;
-  int ntx = (M + TX - 1) / TX, nty = (M + TY - 1) / TY;
+  const int yhi = rw.yhi < 0 ? M : rw.yhi, frows = rw.frows < 0 ? M + 1 : rw.frows;
+  if (!tm2<T>(&P.tr, r.p + (int64_t)rw.fy0 * r.pitch, M + 1, frows, r.pitch, Op::RW, Op::RH))
+    return cudaErrorInvalidValue;
+  int ntx = (M + TX - 1) / TX, nty = tiles_y(rw.ylo, yhi);
   P.out = d;
   P.M = M;
   P.ntx = ntx;
   P.ntiles = ntx * nty;
+  P.ylo = rw.ylo;
+  P.yhi = yhi;
+  P.yo = rw.fy0;
+  P.yh = rw.hy0;
   return run_staged<RestADS<T>::template op>(P, st);
 }
 
 template <class T>
-cudaError_t fast2_rest_da(const S2<T> &d, const D2<T> &r, int Mc, cudaStream_t st) {
+cudaError_t fast2_rest_da(const S2<T> &d, const D2<T> &r, int Mc, cudaStream_t st, const Rows2 &rw) {
   using Op = OpRest2DA<T, 2>;
   typename Op::Params P{};
-  int H = Mc + 1;   // E/O arrays of D(s) have M/2 + 1 = Mc + 1 entries per side
-  if (!tm2<T>(&P.te, d.e, H, H, d.pitch, Op::EW, Op::EH) || !tm2<T>(&P.to, d.o, H, H, d.pitch, Op::OW, Op::OH))
+  const int H = Mc + 1;   // E/O arrays of D(s) have M/2 + 1 = Mc + 1 entries per side
+  const int yhi = rw.yhi < 0 ? Mc : rw.yhi, hrows = rw.hrows < 0 ? H : rw.hrows;
+  if (!tm2<T>(&P.te, d.e + (int64_t)rw.hy0 * d.pitch, H, hrows, d.pitch, Op::EW, Op::EH) ||
+      !tm2<T>(&P.to, d.o + (int64_t)rw.hy0 * d.pitch, H, hrows, d.pitch, Op::OW, Op::OH))
     return cudaErrorInvalidValue;
-  int ntx = (Mc + TX - 1) / TX, nty = (Mc + TY - 1) / TY;
+  int ntx = (Mc + TX - 1) / TX, nty = tiles_y(rw.ylo, yhi);
   P.out = r;
   P.Mc = Mc;
   P.ntx = ntx;
   P.ntiles = ntx * nty;
+  P.ylo = rw.ylo;
+  P.yhi = yhi;
+  P.yo = rw.fy0;
+  P.yh = rw.hy0;
   return run_staged<RestDAS<T>::template op>(P, st);
 }
 
 template <class T>
-cudaError_t fast2_jac_d(const D2<T> &vc, const S2<T> &r, const S2<T> &v, int M, T c, cudaStream_t st) {
+cudaError_t fast2_jac_d(const D2<T> &vc, const S2<T> &r, const S2<T> &v, int M, T c, cudaStream_t st,
+                        const Rows2 &rw) {
   using Op = OpJac2D<T, 2>;
   typename Op::Params P{};
-  int H = M / 2 + 1;
-  if (!tm2<T>(&P.tva, vc.p, H, H, vc.pitch, Op::AW, Op::AH) || !tm2<T>(&P.tro, r.o, H, H, r.pitch, Op::ROW, Op::ROH) ||
-      !tm2<T>(&P.tre, r.e, H, H, r.pitch, Op::REW, Op::REH))
+  const int H = M / 2 + 1, W = M / 2;
+  const int yhi = rw.yhi < 0 ? W : rw.yhi, hrows = rw.hrows < 0 ? H : rw.hrows;
+  if (!tm2<T>(&P.tva, vc.p + (int64_t)rw.hy0 * vc.pitch, H, hrows, vc.pitch, Op::AW, Op::AH) ||
+      !tm2<T>(&P.tro, r.o + (int64_t)rw.hy0 * r.pitch, H, hrows, r.pitch, Op::ROW, Op::ROH) ||
+      !tm2<T>(&P.tre, r.e + (int64_t)rw.hy0 * r.pitch, H, hrows, r.pitch, Op::REW, Op::REH))
     return cudaErrorInvalidValue;
-  int W = M / 2;
-  int ntx = (W + TX - 1) / TX, nty = (W + TY - 1) / TY;
+  int ntx = (W + TX - 1) / TX, nty = tiles_y(rw.ylo, yhi);
   P.v = v;
   P.M = M;
   P.ntx = ntx;
   P.ntiles = ntx * nty;
   P.c = c;
+  P.ylo = rw.ylo;
+  P.yhi = yhi;
+  P.yo = rw.fy0;
+  P.yh = rw.hy0;
   return run_staged<JacDS<T>::template op>(P, st);
 }
 
 #define INSTF(T)                                                                                                   \
   template cudaError_t fast2_desc_fine<T>(const T *, const T *, int64_t, const S2<T> &, int, int, const Coef<T> &, \
-                                          const NormSink &, cudaStream_t);                                         \
+                                          const NormSink &, cudaStream_t, const Rows2 &);                          \
   template cudaError_t fast2_asc_fine<T>(const S2<T> &, const T *, const T *, int64_t, T *, int, int, T,           \
-                                         const Coef<T> &, cudaStream_t);                                           \
-  template cudaError_t fast2_jac_a<T>(const S2<T> &, const D2<T> &, const D2<T> &, int, T, cudaStream_t);          \
-  template cudaError_t fast2_rest_ad<T>(const D2<T> &, const S2<T> &, int, cudaStream_t);                          \
-  template cudaError_t fast2_rest_da<T>(const S2<T> &, const D2<T> &, int, cudaStream_t);                          \
-  template cudaError_t fast2_jac_d<T>(const D2<T> &, const S2<T> &, const S2<T> &, int, T, cudaStream_t);
+                                         const Coef<T> &, cudaStream_t, const Rows2 &);                            \
+  template cudaError_t fast2_jac_a<T>(const S2<T> &, const D2<T> &, const D2<T> &, int, T, cudaStream_t,           \
+                                      const Rows2 &);                                                              \
+  template cudaError_t fast2_rest_ad<T>(const D2<T> &, const S2<T> &, int, cudaStream_t, const Rows2 &);           \
+  template cudaError_t fast2_rest_da<T>(const S2<T> &, const D2<T> &, int, cudaStream_t, const Rows2 &);           \
+  template cudaError_t fast2_jac_d<T>(const D2<T> &, const S2<T> &, const S2<T> &, int, T, cudaStream_t,           \
+                                      const Rows2 &);
 
 INSTF(float)
 INSTF(double)

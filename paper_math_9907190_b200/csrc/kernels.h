@@ -37,20 +37,29 @@ template <class T>
 void launch2_coarse(const Lev2<T> *d_lev, int oc, int k, int *counter, cudaStream_t st);
 
 // TMA tile kernels (k2f.cu); every pointer/pitch must be 16-byte aligned.
+// Rows2: the output rows a launch writes and the local allocations of its
+// inputs (multi-GPU slabs); the default (all -1 / 0) is the whole level.
+struct Rows2 {
+  int ylo = 0, yhi = -1;    // output rows [ylo, yhi) in the output array's row units (-1: all)
+  int fy0 = 0, frows = -1;  // full-resolution inputs: global row of local row 0, local rows (-1: all)
+  int hy0 = 0, hrows = -1;  // half-resolution inputs (E/O of D(s), A(2s))
+};
 template <class T>
 cudaError_t fast2_desc_fine(const T *u, const T *f, int64_t pitch, const S2<T> &d, int M, int order, const Coef<T> &k,
-                            const NormSink &ns, cudaStream_t st);
+                            const NormSink &ns, cudaStream_t st, const Rows2 &rw = Rows2());
 template <class T>
 cudaError_t fast2_asc_fine(const S2<T> &vd, const T *u_old, const T *f, int64_t pitch, T *u_new, int M, int order, T c,
-                           const Coef<T> &k, cudaStream_t st);
+                           const Coef<T> &k, cudaStream_t st, const Rows2 &rw = Rows2());
 template <class T>
-cudaError_t fast2_jac_a(const S2<T> &vd, const D2<T> &r, const D2<T> &v, int M, T c, cudaStream_t st);
+cudaError_t fast2_jac_a(const S2<T> &vd, const D2<T> &r, const D2<T> &v, int M, T c, cudaStream_t st,
+                        const Rows2 &rw = Rows2());
 template <class T>
-cudaError_t fast2_rest_ad(const D2<T> &r, const S2<T> &d, int M, cudaStream_t st);
+cudaError_t fast2_rest_ad(const D2<T> &r, const S2<T> &d, int M, cudaStream_t st, const Rows2 &rw = Rows2());
 template <class T>
-cudaError_t fast2_rest_da(const S2<T> &d, const D2<T> &r, int Mc, cudaStream_t st);
+cudaError_t fast2_rest_da(const S2<T> &d, const D2<T> &r, int Mc, cudaStream_t st, const Rows2 &rw = Rows2());
 template <class T>
-cudaError_t fast2_jac_d(const D2<T> &vc, const S2<T> &r, const S2<T> &v, int M, T c, cudaStream_t st);
+cudaError_t fast2_jac_d(const D2<T> &vc, const S2<T> &r, const S2<T> &v, int M, T c, cudaStream_t st,
+                        const Rows2 &rw = Rows2());
 template <class T>
 void launch2_residual(const D2<const T> &u, const D2<const T> &f, const D2<T> &r, int M, int order, const Coef<T> &k,
                       cudaStream_t st);
@@ -58,6 +67,15 @@ template <class T>
 void launch2_ftilde(const D2<const T> &f, const D2<T> &ft, int M, cudaStream_t st);
 template <class T>
 void launch2_norm(const D2<const T> &a, int M, unsigned long long *mx, double *ss, cudaStream_t st);
+
+template <class T>
+void launch2_ftilde_rows(const D2<const T> &f, const D2<T> &ft, int M, int ylo, int yhi, cudaStream_t st);
+template <class T>
+void launch2_residual_rows(const D2<const T> &u, const D2<const T> &f, const D2<T> &r, int M, int order,
+                           const Coef<T> &k, int ylo, int yhi, cudaStream_t st);
+template <class T>
+void launch2_norm_rows(const D2<const T> &a, int M, int ylo, int yhi, unsigned long long *mx, double *ss,
+                       cudaStream_t st);
 
 // ----------------------------------------------------------------- 3D
 template <class T>

@@ -1,165 +1,10 @@
 // mg_api.cu -- the C ABI of include/mg.h: argument checking, the level plan
 // (buffers in HBM), the per-cycle launch schedule captured in a CUDA graph,
 // norms, staging.  Host code only; the kernels live in k2d.cu / k3d.cu.
-#include <cuda_runtime.h>
+#include "solver.h"
 
-#include <cmath>
-#include <cstdlib>
-#include <cstdio>
-#include <cstring>
-#include <memory>
-#include <string>
-#include <vector>
-
-#include "../../include/mg.h"
-#include "kernels.h"
-
-using namespace mg;
-
-namespace {
-
-constexpr int kHistCap = 4096;
-
-int log2_exact(int64_t v) {
-  if (v < 1) return -1;
-  int k = 0;
-  while ((int64_t(1) << k) < v) k++;
-  return ((int64_t(1) << k) == v) ? k : -1;
-}
-
-int64_t round_up(int64_t v, int64_t m) { return (v + m - 1) / m * m; }
-
-struct DeviceGuard {
-  int prev = -1;
-  explicit DeviceGuard(int dev) {
-    if (dev >= 0) {
-      cudaGetDevice(&prev);
-      if (prev != dev) cudaSetDevice(dev);
-      else prev = -1;
-    }
-  }
-  ~DeviceGuard() {
-    if (prev >= 0) cudaSetDevice(prev);
-  }
-};
-
-}  // namespace
-
-// ---------------------------------------------------------------- profiler
-// Step markers: in profile mode every step of the cycle is preceded by a CUDA
-// event on the solver's stream; otherwise the markers cost nothing.
-struct StepInfo {
-  std::string name;
-  int level, launches;
-  double bytes;
-};
-struct Prof {
-  cudaStream_t st = nullptr;
-  bool first = true;
-  std::vector<StepInfo> steps;
-  std::vector<cudaEvent_t> evs;   // (nsteps + 1) per cycle
-  bool debug = getenv("MG_DEBUG_SYNC") != nullptr;
-  std::string last;
-  void step(const char *name, int level, int launches, double bytes) {
-    if (debug) {
-      cudaError_t e = cudaStreamSynchronize(st);
-      if (e != cudaSuccess) fprintf(stderr, "[mg debug] error after step '%s': %s\n", last.c_str(), cudaGetErrorString(e));
-      last = name;
-    }
-    if (first) steps.push_back(StepInfo{name, level, launches, bytes});
-    cudaEvent_t e;
-    cudaEventCreate(&e);
-    cudaEventRecord(e, st);
-    evs.push_back(e);
-  }
-  void end_cycle() {
-    if (debug) {
-      cudaError_t er = cudaStreamSynchronize(st);
-      if (er != cudaSuccess) fprintf(stderr, "[mg debug] error after step '%s': %s\n", last.c_str(), cudaGetErrorString(er));
-    }
-    cudaEvent_t e;
-    cudaEventCreate(&e);
-    cudaEventRecord(e, st);
-    evs.push_back(e);
-    first = false;
-  }
-  ~Prof() {
-    for (auto e : evs) cudaEventDestroy(e);
-  }
-};
-#define STEP(name, lev, nl, bytes) \
-  do {                              \
-    if (prof) prof->step(name, lev, nl, bytes); \
-  } while (0)
-
-// ---------------------------------------------------------------- solver
-struct ImplBase {
-  virtual ~ImplBase() {}
-  virtual cudaError_t alloc() = 0;
-  // One V-cycle reading u_in and writing u_out = u_in + v (u_out may equal
-  // u_in only when !fast()).
-  virtual void enqueue_cycle(const void *u_in, void *u_out, const void *f_eff, cudaStream_t st,
-                             Prof *prof = nullptr) = 0;
-  // true: the TMA tile kernels run (they update u out of place)
-  virtual bool fast() const { return false; }
-  virtual void enqueue_final_norm(void *u, const void *f_eff, cudaStream_t st) = 0;
-  virtual void enqueue_residual(const void *u, const void *f, void *r, cudaStream_t st) = 0;
-  virtual void enqueue_ftilde(const void *f, void *ft, cudaStream_t st) = 0;
-  virtual void enqueue_norm(const void *x, unsigned long long *mx, double *ss, cudaStream_t st) = 0;
-  virtual int launches_per_cycle() const = 0;
-  std::vector<void *> bufs;
-  size_t bytes = 0;
-  std::vector<double> Nl;   // interior nodes per level
-  cudaError_t dalloc(void **p, size_t n) {
-    cudaError_t e = cudaMalloc(p, n);
-    if (e != cudaSuccess) return e;
-    bufs.push_back(*p);
-    bytes += n;
-    return cudaMemset(*p, 0, n);
-  }
-  void free_all() {
-    for (void *p : bufs) cudaFree(p);
-    bufs.clear();
-  }
-};
-
-struct mg_solver {
-  mg_config cfg{};
-  int k = 0, L = 0, esz = 8;
-  int64_t pitch = 0;
-  int device = 0;
-  cudaStream_t user = nullptr, st = nullptr;
-  cudaEvent_t ev_in = nullptr, ev_out = nullptr;
-  std::unique_ptr<ImplBase> impl;
-  unsigned long long *d_hist = nullptr;   // kHistCap slots
-  int *d_counter = nullptr;
-  unsigned long long *d_mx = nullptr;
-  double *d_ss = nullptr;
-  void *d_ft = nullptr;                    // order-4 f~ (n^d x pitch)
-  void *d_u_stage = nullptr, *d_f_stage = nullptr;   // mg_vcycle_host staging
-  struct GraphEntry {
-    cudaGraphExec_t exec;
-    const void *uin, *uout, *f;
-  };
-  std::vector<GraphEntry> graphs;   // captured cycles keyed by pointers
-  void *d_ualt = nullptr;            // out-of-place partner of the caller's u
-  unsigned long long *h_hist = nullptr;    // pinned
-  std::string err;
-  size_t field_elems() const { return (size_t)((cfg.dim == 2) ? cfg.n * pitch : cfg.n * cfg.n * pitch); }
-};
-
-static int fail(mg_solver *s, int code, const std::string &msg) {
-  if (s) s->err = msg;
-  return code;
-}
-
-#define CKS(s, call)                                                                          \
-  do {                                                                                        \
-    cudaError_t e_ = (call);                                                                  \
-    if (e_ != cudaSuccess)                                                                    \
-      return fail((s), e_ == cudaErrorMemoryAllocation ? MG_ENOMEM : MG_ECUDA,                \
-                  std::string(#call) + ": " + cudaGetErrorString(e_));                        \
-  } while (0)
+ImplBase *make_dist2(mg_solver *s, bool loopback, std::string *err);
+int nccl_unique_id(void *out, std::string *err);
 
 // ------------------------------------------------------------------ 2D
 template <class T>
@@ -657,7 +502,14 @@ static int check_config(const mg_config *c, int *k_out) {
     if (!(c->p[i] > 0.0 && c->p[i] <= 3.0)) return MG_EINVAL;
   if (c->pitch != 0 && c->pitch < c->n) return MG_EINVAL;
   if (c->nranks < 0 || (c->nranks > 1 && (c->rank < 0 || c->rank >= c->nranks))) return MG_EINVAL;
-  if (c->nranks > 1) return MG_EUNSUPPORTED;   // multi-GPU lives in the comm layer
+  if (c->nranks > 1) {
+    // y-slabs of the 2D hierarchy (dist2.cu); 3D slabs are not in this build
+    if (c->dim != 2) return MG_EUNSUPPORTED;
+    if (log2_exact(c->nranks) < 0 || ((c->n - 1) / c->nranks) < 4) return MG_EUNSUPPORTED;
+    int64_t pt = c->pitch ? c->pitch : c->n;
+    if ((pt * (c->dtype == MG_F64 ? 8 : 4)) % 16 != 0) return MG_EUNSUPPORTED;
+    if (!(c->flags & MG_FLAG_LOOPBACK) && !c->nccl_id) return MG_EINVAL;
+  }
   *k_out = k;
   return MG_OK;
 }
@@ -703,7 +555,16 @@ int mg_create_ex(const mg_config *cfg, mg_solver **out) {
   CKS(sp, cudaMemset(s->d_hist, 0, sizeof(unsigned long long) * kHistCap));
   CKS(sp, cudaMemset(s->d_counter, 0, sizeof(int)));
   CKS(sp, cudaMallocHost(&s->h_hist, sizeof(unsigned long long) * kHistCap));
-  if (cfg->dim == 2) {
+  if (cfg->nranks > 1) {
+    std::string why;
+    ImplBase *d = make_dist2(sp, (cfg->flags & MG_FLAG_LOOPBACK) != 0, &why);
+    if (!d) {
+      fprintf(stderr, "[libmg] multi-GPU init failed: %s\n", why.c_str());
+      mg_destroy(s.release());
+      return MG_ENCCL;
+    }
+    s->impl.reset(d);
+  } else if (cfg->dim == 2) {
     if (cfg->dtype == MG_F64) s->impl.reset(new Impl2<double>(sp));
     else s->impl.reset(new Impl2<float>(sp));
   } else {
@@ -765,6 +626,13 @@ int mg_destroy(mg_solver *s) {
 
 int mg_local_extent(const mg_solver *s, int64_t *lo, int64_t *hi, int64_t *ghost) {
   if (!s) return MG_EINVAL;
+  int64_t l, h, g;
+  if (s->impl && s->impl->extent(&l, &h, &g)) {
+    if (lo) *lo = l;
+    if (hi) *hi = h;
+    if (ghost) *ghost = g;
+    return MG_OK;
+  }
   if (lo) *lo = 0;
   if (hi) *hi = s->cfg.n;
   if (ghost) *ghost = 0;
@@ -830,6 +698,7 @@ static int vcycle_dev(mg_solver *s, void *u, const void *f, int ncycles, double 
   if (cur != u) CKS(s, cudaMemcpyAsync(u, cur, s->field_elems() * s->esz, cudaMemcpyDeviceToDevice, s->st));
   if (res_hist) {
     s->impl->enqueue_final_norm(u, fe, s->st);
+    CKS(s, s->impl->reduce_hist(s->d_hist, nslots, s->st));
     CKS(s, cudaMemcpyAsync(s->h_hist, s->d_hist, sizeof(unsigned long long) * nslots, cudaMemcpyDeviceToHost, s->st));
     CKS(s, cudaStreamSynchronize(s->st));
     bool finite = true;
@@ -853,6 +722,11 @@ int mg_vcycle(mg_solver *s, void *u, const void *f, int ncycles, double *res_his
   DeviceGuard g(s->device);
   int rc = begin(s);
   if (rc) return rc;
+  rc = s->impl->vcycle_all(s, u, f, ncycles, res_hist);
+  if (rc != 1) {
+    int rc2 = end(s);
+    return rc ? rc : rc2;
+  }
   rc = vcycle_dev(s, u, f, ncycles, res_hist);
   int rc2 = end(s);
   return rc ? rc : rc2;
@@ -953,6 +827,36 @@ int mg_profile(mg_solver *s, void *u, const void *f, int ncycles, mg_step_stat *
   }
   rc = end(s);
   return rc ? rc : (int)ns;
+}
+
+int mg_slab_plan(int dim, int64_t n, int nranks, int rank, int64_t agglom_points, int64_t *lo, int64_t *hi,
+                 int64_t *ghost, int *agglom_octave) {
+  int k = log2_exact(n - 1);
+  if (k < 2 || nranks < 1 || rank < 0 || rank >= nranks) return MG_EINVAL;
+  if (dim != 2) return MG_EUNSUPPORTED;
+  if (nranks == 1) {
+    if (lo) *lo = 0;
+    if (hi) *hi = n;
+    if (ghost) *ghost = 0;
+    if (agglom_octave) *agglom_octave = 0;
+    return MG_OK;
+  }
+  if (log2_exact(nranks) < 0 || (n - 1) / nranks < 4) return MG_EUNSUPPORTED;
+  int64_t R = (n - 1) / nranks;
+  if (lo) *lo = rank * R;
+  if (hi) *hi = (rank + 1) * R;
+  if (ghost) *ghost = 2;
+  if (agglom_octave)
+    *agglom_octave = slab_agglom_octave(n, k, nranks, agglom_points > 0 ? agglom_points : (int64_t(1) << 18));
+  return MG_OK;
+}
+
+int mg_nccl_unique_id(void *out) {
+  if (!out) return MG_EINVAL;
+  std::string err;
+  int rc = nccl_unique_id(out, &err);
+  if (rc) fprintf(stderr, "[libmg] %s\n", err.c_str());
+  return rc;
 }
 
 const char *mg_strerror(int status) {

@@ -1,0 +1,187 @@
+// solver.h -- internal host-side types shared by the C ABI (mg_api.cu) and
+// the multi-GPU slab solver (dist2.cu).  Not part of the public ABI.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "../../include/mg.h"
+#include "kernels.h"
+
+using namespace mg;
+
+namespace {
+
+constexpr int kHistCap = 4096;
+
+int log2_exact(int64_t v) {
+  if (v < 1) return -1;
+  int k = 0;
+  while ((int64_t(1) << k) < v) k++;
+  return ((int64_t(1) << k) == v) ? k : -1;
+}
+
+int64_t round_up(int64_t v, int64_t m) { return (v + m - 1) / m * m; }
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    if (dev >= 0) {
+      cudaGetDevice(&prev);
+      if (prev != dev) cudaSetDevice(dev);
+      else prev = -1;
+    }
+  }
+  ~DeviceGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
+
+}  // namespace
+
+// Slab plan (2D y-slabs): the first octave whose levels are agglomerated:
+// fewer than `ag` interior nodes on A(s), or fewer than 4 rows per rank.
+static inline int slab_agglom_octave(int64_t n, int k, int P, int64_t ag) {
+  for (int o = 1; o < k; o++) {
+    int64_t M = (n - 1) >> o;
+    if ((M - 1) * (M - 1) < ag || M / P < 4) return o;
+  }
+  return k - 1;
+}
+
+// ---------------------------------------------------------------- profiler
+// Step markers: in profile mode every step of the cycle is preceded by a CUDA
+// event on the solver's stream; otherwise the markers cost nothing.
+struct StepInfo {
+  std::string name;
+  int level, launches;
+  double bytes;
+};
+struct Prof {
+  cudaStream_t st = nullptr;
+  bool first = true;
+  std::vector<StepInfo> steps;
+  std::vector<cudaEvent_t> evs;   // (nsteps + 1) per cycle
+  bool debug = getenv("MG_DEBUG_SYNC") != nullptr;
+  std::string last;
+  void step(const char *name, int level, int launches, double bytes) {
+    if (debug) {
+      cudaError_t e = cudaStreamSynchronize(st);
+      if (e != cudaSuccess) fprintf(stderr, "[mg debug] error after step '%s': %s\n", last.c_str(), cudaGetErrorString(e));
+      last = name;
+    }
+    if (first) steps.push_back(StepInfo{name, level, launches, bytes});
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    cudaEventRecord(e, st);
+    evs.push_back(e);
+  }
+  void end_cycle() {
+    if (debug) {
+      cudaError_t er = cudaStreamSynchronize(st);
+      if (er != cudaSuccess) fprintf(stderr, "[mg debug] error after step '%s': %s\n", last.c_str(), cudaGetErrorString(er));
+    }
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    cudaEventRecord(e, st);
+    evs.push_back(e);
+    first = false;
+  }
+  ~Prof() {
+    for (auto e : evs) cudaEventDestroy(e);
+  }
+};
+#define STEP(name, lev, nl, bytes) \
+  do {                              \
+    if (prof) prof->step(name, lev, nl, bytes); \
+  } while (0)
+
+// ---------------------------------------------------------------- solver
+struct ImplBase {
+  virtual ~ImplBase() {}
+  virtual cudaError_t alloc() = 0;
+  // One V-cycle reading u_in and writing u_out = u_in + v (u_out may equal
+  // u_in only when !fast()).
+  virtual void enqueue_cycle(const void *u_in, void *u_out, const void *f_eff, cudaStream_t st,
+                             Prof *prof = nullptr) = 0;
+  // true: the TMA tile kernels run (they update u out of place)
+  virtual bool fast() const { return false; }
+  virtual void enqueue_final_norm(void *u, const void *f_eff, cudaStream_t st) = 0;
+  virtual void enqueue_residual(const void *u, const void *f, void *r, cudaStream_t st) = 0;
+  virtual void enqueue_ftilde(const void *f, void *ft, cudaStream_t st) = 0;
+  virtual void enqueue_norm(const void *x, unsigned long long *mx, double *ss, cudaStream_t st) = 0;
+  virtual int launches_per_cycle() const = 0;
+  // ---- multi-GPU hooks (single-GPU defaults)
+  // elements of one caller field (u, f, r) as this rank holds it
+  virtual size_t local_elems() const { return 0; }
+  // rows/planes [lo, hi) owned and ghost rows carried by the caller's arrays
+  virtual bool extent(int64_t *, int64_t *, int64_t *) const { return false; }
+  // loopback (virtual ranks in one process): the whole mg_vcycle; 1 = not handled
+  virtual int vcycle_all(mg_solver *, void *, const void *, int, double *) { return 1; }
+  // combine the per-cycle residual-norm maxima over ranks
+  virtual cudaError_t reduce_hist(unsigned long long *, int, cudaStream_t) { return cudaSuccess; }
+  // before the cycles of one call: ghost rows of f (or f~)
+  virtual cudaError_t prepare_rhs(const void *, cudaStream_t) { return cudaSuccess; }
+  std::vector<void *> bufs;
+  size_t bytes = 0;
+  std::vector<double> Nl;   // interior nodes per level
+  cudaError_t dalloc(void **p, size_t n) {
+    cudaError_t e = cudaMalloc(p, n);
+    if (e != cudaSuccess) return e;
+    bufs.push_back(*p);
+    bytes += n;
+    return cudaMemset(*p, 0, n);
+  }
+  void free_all() {
+    for (void *p : bufs) cudaFree(p);
+    bufs.clear();
+  }
+};
+
+struct mg_solver {
+  mg_config cfg{};
+  int k = 0, L = 0, esz = 8;
+  int64_t pitch = 0;
+  int device = 0;
+  cudaStream_t user = nullptr, st = nullptr;
+  cudaEvent_t ev_in = nullptr, ev_out = nullptr;
+  std::unique_ptr<ImplBase> impl;
+  unsigned long long *d_hist = nullptr;   // kHistCap slots
+  int *d_counter = nullptr;
+  unsigned long long *d_mx = nullptr;
+  double *d_ss = nullptr;
+  void *d_ft = nullptr;                    // order-4 f~ (n^d x pitch)
+  void *d_u_stage = nullptr, *d_f_stage = nullptr;   // mg_vcycle_host staging
+  struct GraphEntry {
+    cudaGraphExec_t exec;
+    const void *uin, *uout, *f;
+  };
+  std::vector<GraphEntry> graphs;   // captured cycles keyed by pointers
+  void *d_ualt = nullptr;            // out-of-place partner of the caller's u
+  unsigned long long *h_hist = nullptr;    // pinned
+  std::string err;
+  size_t field_elems() const {
+    size_t le = impl ? impl->local_elems() : 0;
+    return le ? le : (size_t)((cfg.dim == 2) ? cfg.n * pitch : cfg.n * cfg.n * pitch);
+  }
+};
+
+static int fail(mg_solver *s, int code, const std::string &msg) {
+  if (s) s->err = msg;
+  return code;
+}
+
+#define CKS(s, call)                                                                          \
+  do {                                                                                        \
+    cudaError_t e_ = (call);                                                                  \
+    if (e_ != cudaSuccess)                                                                    \
+      return fail((s), e_ == cudaErrorMemoryAllocation ? MG_ENOMEM : MG_ECUDA,                \
+                  std::string(#call) + ": " + cudaGetErrorString(e_));                        \
+  } while (0)
+

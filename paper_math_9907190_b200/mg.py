@@ -24,6 +24,7 @@ LIB_PATH = os.path.join(HERE, "libmg.so")
 MG_OK, MG_EINVAL, MG_ENOMEM, MG_ECUDA, MG_ENCCL, MG_EUNSUPPORTED, MG_EDIVERGED, MG_ENODEV = 0, -1, -2, -3, -4, -5, -6, -7
 MG_F64, MG_F32 = 0, 1
 MG_NORM_INF, MG_NORM_L2 = 0, 1
+MG_FLAG_LOOPBACK = 1
 
 
 class MGError(RuntimeError):
@@ -72,6 +73,10 @@ EXPORTS = {
     "mg_launches_per_cycle": (ctypes.c_int, [ctypes.c_void_p]),
     "mg_profile": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int,
                                   ctypes.POINTER(mg_step_stat), ctypes.c_int]),
+    "mg_slab_plan": (ctypes.c_int, [ctypes.c_int, ctypes.c_int64, ctypes.c_int, ctypes.c_int, ctypes.c_int64,
+                                    ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_int64),
+                                    ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_int)]),
+    "mg_nccl_unique_id": (ctypes.c_int, [ctypes.c_void_p]),
     "mg_strerror": (ctypes.c_char_p, [ctypes.c_int]),
     "mg_last_error": (ctypes.c_char_p, [ctypes.c_void_p]),
 }
@@ -175,6 +180,46 @@ def mg_profile(h, u_ptr: int, f_ptr: int, ncycles: int, cap: int = 256):
             for b in buf[: min(rc, cap)]]
 
 
+def mg_slab_plan(dim: int, n: int, nranks: int, rank: int, agglom_points: int = 0):
+    """Host-only slab plan: (lo, hi, ghost, agglomeration octave)."""
+    lo, hi, g, oa = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int()
+    _check(load().mg_slab_plan(dim, n, nranks, rank, agglom_points, ctypes.byref(lo), ctypes.byref(hi),
+                               ctypes.byref(g), ctypes.byref(oa)), None, "mg_slab_plan")
+    return lo.value, hi.value, g.value, oa.value
+
+
+def mg_nccl_unique_id() -> bytes:
+    buf = ctypes.create_string_buffer(128)
+    _check(load().mg_nccl_unique_id(buf), None, "mg_nccl_unique_id")
+    return buf.raw
+
+
+def broadcast_nccl_id(group=None) -> bytes:
+    """Rank 0 of the torch.distributed group makes the NCCL id; every rank gets it."""
+    import torch
+    import torch.distributed as dist
+    rank = dist.get_rank(group)
+    t = torch.zeros(128, dtype=torch.uint8)
+    if rank == 0:
+        t.copy_(torch.frombuffer(bytearray(mg_nccl_unique_id()), dtype=torch.uint8))
+    backend = dist.get_backend(group)
+    if backend == "nccl":
+        t = t.cuda()
+    dist.broadcast(t, src=dist.get_global_rank(group, 0) if group is not None else 0, group=group)
+    return bytes(t.cpu().numpy().tobytes())
+
+
+def split_rows(full, lo: int, hi: int, ghost: int):
+    """The slab a rank passes in multi-GPU mode: rows [lo - ghost, hi + ghost)
+    of a full (n, pitch) array (rows outside the grid are zero)."""
+    import numpy as _np
+    n = full.shape[0]
+    out = _np.zeros((hi - lo + 2 * ghost,) + tuple(full.shape[1:]), dtype=full.dtype)
+    a, b = max(lo - ghost, 0), min(hi + ghost, n)
+    out[a - (lo - ghost): b - (lo - ghost)] = full[a:b]
+    return out
+
+
 def mg_last_error(h) -> str:
     return (load().mg_last_error(h) or b"").decode()
 
@@ -196,7 +241,8 @@ class Solver:
     """
 
     def __init__(self, dim: int, n: int, order: int = 2, p=None, dtype=None, device=None,
-                 pitch: int | None = None, stream=None):
+                 pitch: int | None = None, stream=None, nranks: int = 1, rank: int = 0, group=None,
+                 loopback: bool = False, agglom_points: int = 0):
         import torch
         if not torch.cuda.is_available():
             raise MGError(MG_ENODEV, "no CUDA device (libmg has no CPU path)")
@@ -221,8 +267,21 @@ class Solver:
         cfg.pitch = self.pitch
         cfg.stream = self.stream.cuda_stream
         cfg.device = self.device.index
-        cfg.nranks, cfg.rank = 1, 0
+        if group is not None:
+            import torch.distributed as dist
+            nranks, rank = dist.get_world_size(group), dist.get_rank(group)
+        cfg.nranks, cfg.rank = nranks, rank
+        cfg.agglom_points = agglom_points
+        self._id = None
+        if loopback:
+            cfg.flags = MG_FLAG_LOOPBACK
+        elif nranks > 1:
+            self._id = ctypes.create_string_buffer(broadcast_nccl_id(group), 128)
+            cfg.nccl_id = ctypes.cast(self._id, ctypes.c_void_p)
+        self.nranks, self.rank, self.loopback = nranks, rank, loopback
         self.h = mg_create_ex(cfg)
+        lo, hi, g = mg_local_extent(self.h)
+        self.lo, self.hi, self.ghost = lo, hi, g
 
     def __del__(self):
         h = getattr(self, "h", None)
@@ -233,6 +292,9 @@ class Solver:
     # -- layout helpers
     @property
     def shape(self):
+        """Shape of a field as this rank passes it (the slab with ghost rows in multi-GPU mode)."""
+        if self.nranks > 1 and not self.loopback:
+            return (self.hi - self.lo + 2 * self.ghost, self.pitch)
         return (self.n, self.pitch) if self.dim == 2 else (self.n, self.n, self.pitch)
 
     def alloc(self, like=None):
