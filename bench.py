@@ -176,11 +176,20 @@ def main():
     tdt = torch.float64 if args.dtype == "f64" else torch.float32
     npdt = np.float64 if args.dtype == "f64" else np.float32
 
-    # Multi-GPU: the slab-decomposed solver is not in this round's build, so
-    # every rank runs the whole problem as an independent replica (weak
-    # scaling, no collective on the data path).
-    s = Solver(w.dim, w.n, order=w.order, p=w.p, dtype=tdt)
-    f_host = W.workload_rhs(w.name, npdt)
+    # Multi-GPU: 2D workloads run the y-slab solver over NCCL (strong scaling:
+    # the one global grid is split over the ranks); 3D workloads run one
+    # replica per GPU (3D slabs are not in this build; weak scaling).
+    dist_2d = ws > 1 and w.dim == 2
+    if dist_2d:
+        s = Solver(w.dim, w.n, order=w.order, p=w.p, dtype=tdt, group=dist.group.WORLD)
+    else:
+        s = Solver(w.dim, w.n, order=w.order, p=w.p, dtype=tdt)
+    f_full = W.workload_rhs(w.name, npdt)
+    if dist_2d:
+        from paper_math_9907190_b200.mg import split_rows
+        f_host = split_rows(f_full, s.lo, s.hi, s.ghost)
+    else:
+        f_host = f_full
     u = s.alloc()
     f = s.alloc(f_host)
     N = (w.n - 2) ** w.dim
@@ -222,7 +231,8 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
     ms_per_step = ms / args.steps
-    value = ws * N * args.steps / (ms / 1e3) / 1e9
+    units = N if dist_2d else ws * N   # strong scaling: one grid; replicas: ws grids
+    value = units * args.steps / (ms / 1e3) / 1e9
     clocks = sampler.summary(t0, t1)
 
     # per-step CUDA-event profile (separate, un-graphed pass) for the roofline
@@ -257,7 +267,7 @@ def main():
         # cycles, copy u out -- all inside the CUDA-event timed region
         uh = torch.zeros(s.shape, dtype=tdt).pin_memory()
         fh = torch.zeros(s.shape, dtype=tdt).pin_memory()
-        s.view(fh).copy_(torch.from_numpy(f_host))
+        s.view(fh).copy_(torch.from_numpy(np.ascontiguousarray(f_host)))
         s.vcycle_host(uh, fh, w.cycles)
         times = []
         for _ in range(3):
@@ -270,8 +280,12 @@ def main():
             times.append(e0.elapsed_time(e1))
         t_e2e = float(np.median(times))
         fb = uh.numel() * uh.element_size()
-        e2e = {"value": ws * N * w.cycles / (t_e2e / 1e3) / 1e9, "unit": UNIT,
-               "h2d_bytes_per_step": 2 * fb, "d2h_bytes_per_step": fb,
+        if ws > 1:
+            t = torch.tensor([t_e2e], device="cuda", dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            t_e2e = float(t.item())
+        e2e = {"value": units * w.cycles / (t_e2e / 1e3) / 1e9, "unit": UNIT,
+               "h2d_bytes_per_step": 2 * fb * ws, "d2h_bytes_per_step": fb * ws,
                "step": f"one mg_vcycle_host call: H2D u,f (pinned) + {w.cycles} V-cycles + D2H u",
                "ms_per_step": t_e2e}
 
@@ -282,9 +296,11 @@ def main():
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": args.dtype, "data": "synthetic",
+        "scaling": "strong" if dist_2d else "weak", "vs_baseline": None, "dtype": args.dtype, "data": "synthetic",
         "config": {"workload": w.name, "dim": w.dim, "n": w.n, "order": w.order, "p": list(w.p),
-                   "unknowns": N, "rhs": w.note, "parallelism": "replicas" if ws > 1 else "single",
+                   "unknowns": N, "rhs": w.note,
+                   "parallelism": (f"y-slabs x{ws} (NCCL halo exchange, all-gather agglomeration)" if dist_2d
+                                   else ("replicas" if ws > 1 else "single")),
                    "l2": "inputs larger than L2 (u and f are %.0f MB each vs 126 MB L2)" %
                          (s.view(u).numel() * u.element_size() / 1e6),
                    "levels": s.levels},
