@@ -231,22 +231,24 @@ __global__ void __launch_bounds__(NT3) k3_update_ref(D3<const T> uo, D3<const T>
   un(x, y, z) = uo(x, y, z) + v(x, y, z);
 }
 
+// planes [z0, z0 + nz) (multi-GPU slabs; the whole grid by default)
 template <class T, int ORDER>
-__global__ void __launch_bounds__(NT3) k3_residual(D3<const T> u, D3<const T> f, D3<T> r, int M, Coef<T> k) {
+__global__ void __launch_bounds__(NT3) k3_residual(D3<const T> u, D3<const T> f, D3<T> r, int M, Coef<T> k, int z0,
+                                                   int nz) {
   int64_t W = M + 1;
   int64_t t = (int64_t)blockIdx.x * NT3 + threadIdx.x;
-  if (t >= W * W * W) return;
-  int x = (int)(t % W), y = (int)((t / W) % W), z = (int)(t / (W * W));
+  if (t >= W * W * nz) return;
+  int x = (int)(t % W), y = (int)((t / W) % W), z = (int)(t / (W * W)) + z0;
   r(x, y, z) = res3z<T, ORDER>(u, f, x, y, z, M, k);
 }
 
 // f~ of Efos4: (1/12)(6f + f_{i+1} + f_{j+1} + f_{i-1} + f_{j-1} + f_{k+1} + f_{k-1}).
 template <class T>
-__global__ void __launch_bounds__(NT3) k3_ftilde(D3<const T> f, D3<T> ft, int M) {
+__global__ void __launch_bounds__(NT3) k3_ftilde(D3<const T> f, D3<T> ft, int M, int z0, int nz) {
   int64_t W = M - 1;
   int64_t t = (int64_t)blockIdx.x * NT3 + threadIdx.x;
-  if (t >= W * W * W) return;
-  int x = (int)(t % W) + 1, y = (int)((t / W) % W) + 1, z = (int)(t / (W * W)) + 1;
+  if (t >= W * W * nz) return;
+  int x = (int)(t % W) + 1, y = (int)((t / W) % W) + 1, z = (int)(t / (W * W)) + z0;
   T s = (T)6 * f(x, y, z);
   s = s + f(x + 1, y, z);
   s = s + f(x, y + 1, z);
@@ -258,11 +260,12 @@ __global__ void __launch_bounds__(NT3) k3_ftilde(D3<const T> f, D3<T> ft, int M)
 }
 
 template <class T>
-__global__ void __launch_bounds__(NT3) k3_norm(D3<const T> a, int M, unsigned long long *mx_out, double *ss_out) {
+__global__ void __launch_bounds__(NT3) k3_norm(D3<const T> a, int M, unsigned long long *mx_out, double *ss_out, int z0,
+                                               int nz) {
   int64_t W = M - 1;
   double mx = 0.0, ss = 0.0;
-  for (int64_t t = (int64_t)blockIdx.x * NT3 + threadIdx.x; t < W * W * W; t += (int64_t)gridDim.x * NT3) {
-    int x = (int)(t % W) + 1, y = (int)((t / W) % W) + 1, z = (int)(t / (W * W)) + 1;
+  for (int64_t t = (int64_t)blockIdx.x * NT3 + threadIdx.x; t < W * W * nz; t += (int64_t)gridDim.x * NT3) {
+    int x = (int)(t % W) + 1, y = (int)((t / W) % W) + 1, z = (int)(t / (W * W)) + z0;
     double v = (double)a(x, y, z);
     mx = nmax(mx, fabs(v));
     ss += v * v;
@@ -375,25 +378,37 @@ void launch3_asc_fine(const S3<T> &vr, const D3<T> &u, const D3<const T> &f, con
   k3_update_ref<T><<<g, NT3, 0, st>>>(cd3(u), cd3(scratch), un, M);
 }
 
+// [zlo, zhi) clipped to the planes the kernel covers (residual: 0..M, the
+// others: the interior 1..M-1)
 template <class T>
 void launch3_residual(const D3<const T> &u, const D3<const T> &f, const D3<T> &r, int M, int order, const Coef<T> &k,
-                      cudaStream_t st) {
+                      cudaStream_t st, int zlo, int zhi) {
   int64_t W = M + 1;
+  if (zhi < 0 || zhi > M + 1) zhi = M + 1;
+  if (zlo < 0) zlo = 0;
+  const int nz = zhi - zlo;
+  if (nz <= 0) return;
   if (order == 2)
-    k3_residual<T, 2><<<blocks3(W * W * W), NT3, 0, st>>>(u, f, r, M, k);
+    k3_residual<T, 2><<<blocks3(W * W * nz), NT3, 0, st>>>(u, f, r, M, k, zlo, nz);
   else
-    k3_residual<T, 4><<<blocks3(W * W * W), NT3, 0, st>>>(u, f, r, M, k);
+    k3_residual<T, 4><<<blocks3(W * W * nz), NT3, 0, st>>>(u, f, r, M, k, zlo, nz);
 }
 
 template <class T>
-void launch3_ftilde(const D3<const T> &f, const D3<T> &ft, int M, cudaStream_t st) {
+void launch3_ftilde(const D3<const T> &f, const D3<T> &ft, int M, cudaStream_t st, int zlo, int zhi) {
   int64_t W = M - 1;
-  k3_ftilde<T><<<blocks3(W * W * W), NT3, 0, st>>>(f, ft, M);
+  if (zhi < 0 || zhi > M) zhi = M;
+  if (zlo < 1) zlo = 1;
+  const int nz = zhi - zlo;
+  if (nz > 0) k3_ftilde<T><<<blocks3(W * W * nz), NT3, 0, st>>>(f, ft, M, zlo, nz);
 }
 
 template <class T>
-void launch3_norm(const D3<const T> &a, int M, unsigned long long *mx, double *ss, cudaStream_t st) {
-  k3_norm<T><<<148 * 4, NT3, 0, st>>>(a, M, mx, ss);
+void launch3_norm(const D3<const T> &a, int M, unsigned long long *mx, double *ss, cudaStream_t st, int zlo, int zhi) {
+  if (zhi < 0 || zhi > M) zhi = M;
+  if (zlo < 1) zlo = 1;
+  const int nz = zhi - zlo;
+  if (nz > 0) k3_norm<T><<<148 * 4, NT3, 0, st>>>(a, M, mx, ss, zlo, nz);
 }
 
 #define INST3(T)                                                                                                    \
@@ -410,9 +425,9 @@ void launch3_norm(const D3<const T> &a, int M, unsigned long long *mx, double *s
                                     int, int, T,                                                                   \
                                     const Coef<T> &, cudaStream_t);                                                \
   template void launch3_residual<T>(const D3<const T> &, const D3<const T> &, const D3<T> &, int, int,             \
-                                    const Coef<T> &, cudaStream_t);                                                \
-  template void launch3_ftilde<T>(const D3<const T> &, const D3<T> &, int, cudaStream_t);                          \
-  template void launch3_norm<T>(const D3<const T> &, int, unsigned long long *, double *, cudaStream_t);
+                                    const Coef<T> &, cudaStream_t, int, int);                                      \
+  template void launch3_ftilde<T>(const D3<const T> &, const D3<T> &, int, cudaStream_t, int, int);                \
+  template void launch3_norm<T>(const D3<const T> &, int, unsigned long long *, double *, cudaStream_t, int, int);
 
 INST3(float)
 INST3(double)

@@ -180,6 +180,7 @@ struct OpDesc3Fine {
     CUtensorMap tu, tf;
     S3<T> out;
     int M, ntx, nty, nunits;
+    int zlo, zhi, fz0;   // output planes [zlo, zhi); global plane of the u/f maps' plane 0
     Coef<T> k;
     NormSink ns;
   };
@@ -197,16 +198,16 @@ struct OpDesc3Fine {
     Unit un;
     un.x0 = tx * TX3;
     un.y0 = ty * TY3;
-    un.zs = zc * ZC;
-    un.ze = min(un.zs + ZC, P.M);
+    un.zs = P.zlo + zc * ZC;
+    un.ze = min(un.zs + ZC, P.zhi);
     un.pb = un.zs - 3;
     un.pe = un.ze + 2;
     return un;
   }
   static __device__ void issue(const Params &P, const Unit &un, int p, unsigned char *slot, uint64_t *bar) {
     mbar_expect_tx(bar, U_BYTES + F_BYTES);
-    tma_load_3d(slot + U_OFF, &P.tu, un.x0 - HX, un.y0 - 2, p + 1, bar);
-    tma_load_3d(slot + F_OFF, &P.tf, un.x0 - HX, un.y0 - 1, p, bar);
+    tma_load_3d(slot + U_OFF, &P.tu, un.x0 - HX, un.y0 - 2, p + 1 - P.fz0, bar);
+    tma_load_3d(slot + F_OFF, &P.tf, un.x0 - HX, un.y0 - 1, p - P.fz0, bar);
   }
   // residuals at (xl, y, z) and (xl+1, y, z); um/uc/up point at u(xl, y) of
   // planes z-1, z, z+1 in their slots, ff at f(xl, y).
@@ -312,6 +313,7 @@ struct OpAsc3Fine {
     CUtensorMap tu, tf, tv[4];   // tv: red sublattices C, Fx, Fy, Fz of v_R(1)
     D3<T> out;
     int M, ntx, nty, nunits;
+    int zlo, zhi, fz0, hz0;   // output planes [zlo, zhi); global (half-)plane of the maps' plane 0
     T c;
     Coef<T> k;
   };
@@ -328,8 +330,8 @@ struct OpAsc3Fine {
     Unit un;
     un.x0 = tx * TX3;
     un.y0 = ty * TY3;
-    un.zs = zc * ZC;
-    un.ze = min(un.zs + ZC, P.M);
+    un.zs = P.zlo + zc * ZC;
+    un.ze = min(un.zs + ZC, P.zhi);
     un.pb = un.zs - 3;
     un.pe = un.ze + 2;
     return un;
@@ -337,15 +339,15 @@ struct OpAsc3Fine {
   static __device__ __forceinline__ int vx0(int x0) { return (x0 / 2 - 2) & ~(AL - 1); }   // V box x origin
   static __device__ void issue(const Params &P, const Unit &un, int p, unsigned char *slot, uint64_t *bar) {
     mbar_expect_tx(bar, U_BYTES + F_BYTES + 2 * V_BYTES);
-    tma_load_3d(slot + U_OFF, &P.tu, un.x0 - HX, un.y0 - 2, p + 1, bar);
-    tma_load_3d(slot + F_OFF, &P.tf, un.x0 - HX, un.y0 - 1, p, bar);
+    tma_load_3d(slot + U_OFF, &P.tu, un.x0 - HX, un.y0 - 2, p + 1 - P.fz0, bar);
+    tma_load_3d(slot + F_OFF, &P.tf, un.x0 - HX, un.y0 - 1, p - P.fz0, bar);
     // fine plane z = p+1: even z -> C (even x) and Fz (odd x) at half plane z/2;
     // odd z -> Fx (even x) and Fy (odd x) at half plane (z-1)/2
     const int z = p + 1, hz = z >> 1;
     const CUtensorMap *m0 = (z & 1) ? &P.tv[1] : &P.tv[0];
     const CUtensorMap *m1 = (z & 1) ? &P.tv[2] : &P.tv[3];
-    tma_load_3d(slot + V0_OFF, m0, vx0(un.x0), un.y0 / 2 - 1, hz, bar);
-    tma_load_3d(slot + V1_OFF, m1, vx0(un.x0), un.y0 / 2 - 1, hz, bar);
+    tma_load_3d(slot + V0_OFF, m0, vx0(un.x0), un.y0 / 2 - 1, hz - P.hz0, bar);
+    tma_load_3d(slot + V1_OFF, m1, vx0(un.x0), un.y0 / 2 - 1, hz - P.hz0, bar);
   }
   static __device__ void step(const Params &P, const Unit &un, int p, unsigned char *const *sl, unsigned char *scr,
                               Acc &) {
@@ -460,26 +462,40 @@ static cudaError_t run_plane(const typename Op::Params &P, cudaStream_t st) {
   return cudaGetLastError();
 }
 
+// map of planes [z0, z0 + nz) of an n x n x (any) field given by its
+// virtual plane-0 pointer p (nz = -1: all n planes)
 template <class T>
-static bool tm3(CUtensorMap *tm, const void *p, int64_t n, int64_t pitch, int64_t plane, int bx, int by) {
-  uint64_t dims[3] = {(uint64_t)n, (uint64_t)n, (uint64_t)n};
+static bool tm3(CUtensorMap *tm, const T *p, int64_t n, int64_t pitch, int64_t plane, int bx, int by, int z0 = 0,
+                int nz = -1) {
+  if (nz < 0) nz = (int)n;
+  p += (int64_t)z0 * plane;
+  uint64_t dims[3] = {(uint64_t)n, (uint64_t)n, (uint64_t)nz};
   uint32_t box[3] = {(uint32_t)bx, (uint32_t)by, 1};
   return encode_tmap(tm, p, sizeof(T), 3, dims, (uint64_t)pitch, (uint64_t)plane, box);
 }
 
+static inline void zrange(const ZRange3 &pz, int M, int &zlo, int &zhi) {
+  zlo = pz.zlo;
+  zhi = pz.zhi < 0 ? M : pz.zhi;
+}
+
 template <class T, int ORDER>
 static cudaError_t desc3_impl(const T *u, const T *f, int64_t pitch, const S3<T> &rr, int M, const Coef<T> &k,
-                              const NormSink &ns, cudaStream_t st) {
+                              const NormSink &ns, cudaStream_t st, const ZRange3 &pz) {
   using Op = OpDesc3Fine<T, ORDER>;
   typename Op::Params P{};
   int64_t n = M + 1, plane = pitch * n;
-  if (!tm3<T>(&P.tu, u, n, pitch, plane, Op::UW, Op::UH) || !tm3<T>(&P.tf, f, n, pitch, plane, Op::FW, Op::FH))
+  if (!tm3<T>(&P.tu, u, n, pitch, plane, Op::UW, Op::UH, pz.fz0, pz.fplanes) ||
+      !tm3<T>(&P.tf, f, n, pitch, plane, Op::FW, Op::FH, pz.fz0, pz.fplanes))
     return cudaErrorInvalidValue;
   P.out = rr;
   P.M = M;
+  zrange(pz, M, P.zlo, P.zhi);
+  P.fz0 = pz.fz0;
+  if (P.zhi <= P.zlo) return cudaSuccess;
   P.ntx = (M + TX3 - 1) / TX3;
   P.nty = (M + TY3 - 1) / TY3;
-  P.nunits = P.ntx * P.nty * ((M + ZC - 1) / ZC);
+  P.nunits = P.ntx * P.nty * ((P.zhi - P.zlo + ZC - 1) / ZC);
   P.k = k;
   P.ns = ns;
   return run_plane<Op>(P, st);
@@ -487,31 +503,39 @@ static cudaError_t desc3_impl(const T *u, const T *f, int64_t pitch, const S3<T>
 
 template <class T>
 cudaError_t fast3_desc_fine(const T *u, const T *f, int64_t pitch, const S3<T> &rr, int M, int order, const Coef<T> &k,
-                            const NormSink &ns, cudaStream_t st) {
-  return order == 2 ? desc3_impl<T, 2>(u, f, pitch, rr, M, k, ns, st) : desc3_impl<T, 4>(u, f, pitch, rr, M, k, ns, st);
+                            const NormSink &ns, cudaStream_t st, const ZRange3 &pz) {
+  return order == 2 ? desc3_impl<T, 2>(u, f, pitch, rr, M, k, ns, st, pz)
+                    : desc3_impl<T, 4>(u, f, pitch, rr, M, k, ns, st, pz);
 }
 
 template <class T, int ORDER>
 static cudaError_t asc3_impl(const S3<T> &vr, const T *u_old, const T *f, int64_t pitch, T *u_new, int M, T c,
-                             const Coef<T> &k, cudaStream_t st) {
+                             const Coef<T> &k, cudaStream_t st, const ZRange3 &pz) {
   using Op = OpAsc3Fine<T, ORDER>;
   typename Op::Params P{};
   int64_t n = M + 1, plane = pitch * n;
-  if (!tm3<T>(&P.tu, u_old, n, pitch, plane, Op::UW, Op::UH) || !tm3<T>(&P.tf, f, n, pitch, plane, Op::FW, Op::FH))
+  if (!tm3<T>(&P.tu, u_old, n, pitch, plane, Op::UW, Op::UH, pz.fz0, pz.fplanes) ||
+      !tm3<T>(&P.tf, f, n, pitch, plane, Op::FW, Op::FH, pz.fz0, pz.fplanes))
     return cudaErrorInvalidValue;
   const int sub[4] = {0, 6, 5, 3};   // C, Fx, Fy, Fz
   int64_t H = M / 2 + 1;
+  const int hpl = pz.hplanes < 0 ? (int)H : pz.hplanes;
   for (int i = 0; i < 4; i++) {
-    uint64_t dims[3] = {(uint64_t)H, (uint64_t)H, (uint64_t)H};
+    uint64_t dims[3] = {(uint64_t)H, (uint64_t)H, (uint64_t)hpl};
     uint32_t box[3] = {(uint32_t)Op::VW, (uint32_t)Op::VH, 1};
-    if (!encode_tmap(&P.tv[i], vr.s[sub[i]], sizeof(T), 3, dims, (uint64_t)vr.pitch, (uint64_t)vr.plane, box))
+    if (!encode_tmap(&P.tv[i], vr.s[sub[i]] + (int64_t)pz.hz0 * vr.plane, sizeof(T), 3, dims, (uint64_t)vr.pitch,
+                     (uint64_t)vr.plane, box))
       return cudaErrorInvalidValue;
   }
   P.out = D3<T>{u_new, pitch, plane};
   P.M = M;
+  zrange(pz, M, P.zlo, P.zhi);
+  P.fz0 = pz.fz0;
+  P.hz0 = pz.hz0;
+  if (P.zhi <= P.zlo) return cudaSuccess;
   P.ntx = (M + TX3 - 1) / TX3;
   P.nty = (M + TY3 - 1) / TY3;
-  P.nunits = P.ntx * P.nty * ((M + ZC - 1) / ZC);
+  P.nunits = P.ntx * P.nty * ((P.zhi - P.zlo + ZC - 1) / ZC);
   P.c = c;
   P.k = k;
   return run_plane<Op>(P, st);
@@ -519,18 +543,18 @@ static cudaError_t asc3_impl(const S3<T> &vr, const T *u_old, const T *f, int64_
 
 template <class T>
 cudaError_t fast3_asc_fine(const S3<T> &vr, const T *u_old, const T *f, int64_t pitch, T *u_new, int M, int order, T c,
-                           const Coef<T> &k, cudaStream_t st) {
-  return order == 2 ? asc3_impl<T, 2>(vr, u_old, f, pitch, u_new, M, c, k, st)
-                    : asc3_impl<T, 4>(vr, u_old, f, pitch, u_new, M, c, k, st);
+                           const Coef<T> &k, cudaStream_t st, const ZRange3 &pz) {
+  return order == 2 ? asc3_impl<T, 2>(vr, u_old, f, pitch, u_new, M, c, k, st, pz)
+                    : asc3_impl<T, 4>(vr, u_old, f, pitch, u_new, M, c, k, st, pz);
 }
 
 template cudaError_t fast3_asc_fine<float>(const S3<float> &, const float *, const float *, int64_t, float *, int, int,
-                                           float, const Coef<float> &, cudaStream_t);
+                                           float, const Coef<float> &, cudaStream_t, const ZRange3 &);
 template cudaError_t fast3_asc_fine<double>(const S3<double> &, const double *, const double *, int64_t, double *, int,
-                                            int, double, const Coef<double> &, cudaStream_t);
+                                            int, double, const Coef<double> &, cudaStream_t, const ZRange3 &);
 template cudaError_t fast3_desc_fine<float>(const float *, const float *, int64_t, const S3<float> &, int, int,
-                                            const Coef<float> &, const NormSink &, cudaStream_t);
+                                            const Coef<float> &, const NormSink &, cudaStream_t, const ZRange3 &);
 template cudaError_t fast3_desc_fine<double>(const double *, const double *, int64_t, const S3<double> &, int, int,
-                                             const Coef<double> &, const NormSink &, cudaStream_t);
+                                             const Coef<double> &, const NormSink &, cudaStream_t, const ZRange3 &);
 
 }  // namespace mg

@@ -47,8 +47,8 @@ __device__ __forceinline__ T sum6(T v0, T v1, T v2, T v3, T v4, T v5) {
 
 using namespace l3;
 
-#define IDX3                                                                             \
-  const int a = blockIdx.x * 32 + threadIdx.x, b = blockIdx.y * 8 + threadIdx.y, c = blockIdx.z; \
+#define IDX3                                                                                    \
+  const int a = blockIdx.x * 32 + threadIdx.x, b = blockIdx.y * 8 + threadIdx.y, c = blockIdx.z + c0; \
   if (a >= H || b >= H) return;
 
 // --------------------------------------------------------- G(s) -> R(s)
@@ -70,7 +70,7 @@ __device__ __forceinline__ void b3_rest_gr(D3<const T> r, S3<T> out, int M, int 
 }
 
 template <class T>
-__global__ void __launch_bounds__(256) k3l_rest_gr(D3<const T> r, S3<T> out, int M, int H) {
+__global__ void __launch_bounds__(256) k3l_rest_gr(D3<const T> r, S3<T> out, int M, int H, int c0) {
   IDX3
   b3_rest_gr(r, out, M, H, a, b, c);
 }
@@ -106,7 +106,7 @@ __device__ __forceinline__ void b3_rest_rm(S3<const T> rr, S3<T> rm, int H, int 
 }
 
 template <class T>
-__global__ void __launch_bounds__(256) k3l_rest_rm(S3<const T> rr, S3<T> rm, int H) {
+__global__ void __launch_bounds__(256) k3l_rest_rm(S3<const T> rr, S3<T> rm, int H, int c0) {
   IDX3
   b3_rest_rm(rr, rm, H, a, b, c);
 }
@@ -130,7 +130,7 @@ __device__ __forceinline__ void b3_rest_mg(S3<const T> rm, D3<T> g2, int Mc, int
 }
 
 template <class T>
-__global__ void __launch_bounds__(256) k3l_rest_mg(S3<const T> rm, D3<T> g2, int Mc) {
+__global__ void __launch_bounds__(256) k3l_rest_mg(S3<const T> rm, D3<T> g2, int Mc, int c0) {
   const int H = Mc + 1;
   IDX3
   b3_rest_mg(rm, g2, Mc, a, b, c);
@@ -155,7 +155,7 @@ __device__ __forceinline__ void b3_jac_m1(D3<const T> vc, S3<const T> r, S3<T> v
 }
 
 template <class T>
-__global__ void __launch_bounds__(256) k3l_jac_m1(D3<const T> vc, S3<const T> r, S3<T> v, int H, T cc) {
+__global__ void __launch_bounds__(256) k3l_jac_m1(D3<const T> vc, S3<const T> r, S3<T> v, int H, T cc, int c0) {
   IDX3
   b3_jac_m1(vc, r, v, H, cc, a, b, c);
 }
@@ -177,7 +177,7 @@ __device__ __forceinline__ void b3_jac_m2(S3<const T> r, S3<T> v, int H, T cc, i
 }
 
 template <class T>
-__global__ void __launch_bounds__(256) k3l_jac_m2(S3<const T> r, S3<T> v, int H, T cc) {
+__global__ void __launch_bounds__(256) k3l_jac_m2(S3<const T> r, S3<T> v, int H, T cc, int c0) {
   IDX3
   b3_jac_m2(r, v, H, cc, a, b, c);
 }
@@ -231,7 +231,7 @@ __device__ __forceinline__ void b3_jac_r1(S3<const T> vm, S3<const T> r, S3<T> v
 }
 
 template <class T>
-__global__ void __launch_bounds__(256) k3l_jac_r1(S3<const T> vm, S3<const T> r, S3<T> v, int H, T c1) {
+__global__ void __launch_bounds__(256) k3l_jac_r1(S3<const T> vm, S3<const T> r, S3<T> v, int H, T c1, int c0) {
   IDX3
   b3_jac_r1(vm, r, v, H, c1, a, b, c);
 }
@@ -257,7 +257,7 @@ __device__ __forceinline__ void b3_jac_r2(S3<const T> r, S3<T> v, int H, T c2, i
 }
 
 template <class T>
-__global__ void __launch_bounds__(256) k3l_jac_r2(S3<const T> r, S3<T> v, int H, T c2) {
+__global__ void __launch_bounds__(256) k3l_jac_r2(S3<const T> r, S3<T> v, int H, T c2, int c0) {
   IDX3
   b3_jac_r2(r, v, H, c2, a, b, c);
 }
@@ -304,7 +304,7 @@ __device__ __forceinline__ void b3_jac_g1(S3<const T> vr, D3<const T> rin, D3<co
 
 template <class T, int ORDER, bool FINE>
 __global__ void __launch_bounds__(256) k3l_jac_g1(S3<const T> vr, D3<const T> rin, D3<const T> u, D3<const T> f,
-                                                  D3<T> g, int M, int H, T cc, Coef<T> k) {
+                                                  D3<T> g, int M, int H, T cc, Coef<T> k, int c0) {
   IDX3
   b3_jac_g1<T, ORDER, FINE>(vr, rin, u, f, g, M, H, cc, k, a, b, c);
 }
@@ -356,7 +356,7 @@ __device__ __forceinline__ void b3_jac_g2(D3<const T> rin, D3<const T> u, D3<con
 
 template <class T, int ORDER, bool FINE>
 __global__ void __launch_bounds__(256) k3l_jac_g2(D3<const T> rin, D3<const T> u, D3<const T> f, D3<const T> g,
-                                                  D3<T> out, int M, int H, T cc, Coef<T> k) {
+                                                  D3<T> out, int M, int H, T cc, Coef<T> k, int c0) {
   IDX3
   b3_jac_g2<T, ORDER, FINE>(rin, u, f, g, out, M, H, cc, k, a, b, c);
 }
@@ -416,8 +416,13 @@ __global__ void __launch_bounds__(1024) k3l_coarse(const Lev3<T> *lv, int oc, in
 }
 
 // ================================================================ launchers
-static inline dim3 grid3(int H) { return dim3((H + 31) / 32, (H + 7) / 8, H); }
+// grid.z covers the half-index planes [c0, c1) (c1 = -1: all H).
+static inline dim3 grid3(int H, int nz) { return dim3((H + 31) / 32, (H + 7) / 8, nz); }
 static const dim3 kBlk(32, 8);
+static inline int zcount(int H, int c0, int &c1) {
+  if (c1 < 0 || c1 > H) c1 = H;
+  return c1 - c0;
+}
 
 template <class T>
 static D3<const T> cd3(const D3<T> &a) {
@@ -433,38 +438,47 @@ static S3<const T> cs3(const S3<T> &a) {
 }
 
 template <class T>
-void lv3_rest_gr(const D3<T> &r, const S3<T> &rr, int M, cudaStream_t st) {
-  int H = M / 2 + 1;
-  k3l_rest_gr<T><<<grid3(H), kBlk, 0, st>>>(cd3(r), rr, M, H);
+void lv3_rest_gr(const D3<T> &r, const S3<T> &rr, int M, cudaStream_t st, int c0, int c1) {
+  int H = M / 2 + 1, nz = zcount(H, c0, c1);
+  if (nz > 0) k3l_rest_gr<T><<<grid3(H, nz), kBlk, 0, st>>>(cd3(r), rr, M, H, c0);
 }
 template <class T>
-void lv3_rest_rm(const S3<T> &rr, const S3<T> &rm, int M, cudaStream_t st) {
-  int H = M / 2 + 1;
-  k3l_rest_rm<T><<<grid3(H), kBlk, 0, st>>>(cs3(rr), rm, H);
+void lv3_rest_rm(const S3<T> &rr, const S3<T> &rm, int M, cudaStream_t st, int c0, int c1) {
+  int H = M / 2 + 1, nz = zcount(H, c0, c1);
+  if (nz > 0) k3l_rest_rm<T><<<grid3(H, nz), kBlk, 0, st>>>(cs3(rr), rm, H, c0);
 }
 template <class T>
-void lv3_rest_mg(const S3<T> &rm, const D3<T> &g2, int Mc, cudaStream_t st) {
-  k3l_rest_mg<T><<<grid3(Mc + 1), kBlk, 0, st>>>(cs3(rm), g2, Mc);
+void lv3_rest_mg(const S3<T> &rm, const D3<T> &g2, int Mc, cudaStream_t st, int c0, int c1) {
+  int nz = zcount(Mc + 1, c0, c1);
+  if (nz > 0) k3l_rest_mg<T><<<grid3(Mc + 1, nz), kBlk, 0, st>>>(cs3(rm), g2, Mc, c0);
 }
 template <class T>
-void lv3_jac_m(const D3<T> &vc, const S3<T> &r, const S3<T> &v, int M, T c, cudaStream_t st) {
-  int H = M / 2 + 1;
-  k3l_jac_m1<T><<<grid3(H), kBlk, 0, st>>>(cd3(vc), cs3(r), v, H, c);
-  k3l_jac_m2<T><<<grid3(H), kBlk, 0, st>>>(cs3(r), v, H, c);
+void lv3_jac_m(const D3<T> &vc, const S3<T> &r, const S3<T> &v, int M, T c, cudaStream_t st, int c0, int c1,
+               int phase) {
+  int H = M / 2 + 1, nz = zcount(H, c0, c1);
+  if (nz <= 0) return;
+  if (phase != 2) k3l_jac_m1<T><<<grid3(H, nz), kBlk, 0, st>>>(cd3(vc), cs3(r), v, H, c, c0);
+  if (phase != 1) k3l_jac_m2<T><<<grid3(H, nz), kBlk, 0, st>>>(cs3(r), v, H, c, c0);
 }
 template <class T>
-void lv3_jac_r(const S3<T> &vm, const S3<T> &r, const S3<T> &v, int M, T c1, T c2, cudaStream_t st) {
-  int H = M / 2 + 1;
-  k3l_jac_r1<T><<<grid3(H), kBlk, 0, st>>>(cs3(vm), cs3(r), v, H, c1);
-  k3l_jac_r2<T><<<grid3(H), kBlk, 0, st>>>(cs3(r), v, H, c2);
+void lv3_jac_r(const S3<T> &vm, const S3<T> &r, const S3<T> &v, int M, T c1, T c2, cudaStream_t st, int cz0, int cz1,
+               int phase) {
+  int H = M / 2 + 1, nz = zcount(H, cz0, cz1);
+  if (nz <= 0) return;
+  if (phase != 2) k3l_jac_r1<T><<<grid3(H, nz), kBlk, 0, st>>>(cs3(vm), cs3(r), v, H, c1, cz0);
+  if (phase != 1) k3l_jac_r2<T><<<grid3(H, nz), kBlk, 0, st>>>(cs3(r), v, H, c2, cz0);
 }
 template <class T>
-void lv3_jac_g(const S3<T> &vr, const D3<T> &r, const D3<T> &v, int M, T c, cudaStream_t st) {
-  int H = M / 2 + 1;
+void lv3_jac_g(const S3<T> &vr, const D3<T> &r, const D3<T> &v, int M, T c, cudaStream_t st, int c0, int c1,
+               int phase) {
+  int H = M / 2 + 1, nz = zcount(H, c0, c1);
+  if (nz <= 0) return;
   Coef<T> k{};
   D3<const T> none{nullptr, 0, 0};
-  k3l_jac_g1<T, 2, false><<<grid3(H), kBlk, 0, st>>>(cs3(vr), cd3(r), none, none, v, M, H, c, k);
-  k3l_jac_g2<T, 2, false><<<grid3(H), kBlk, 0, st>>>(cd3(r), none, none, cd3(v), v, M, H, c, k);
+  if (phase != 2)
+    k3l_jac_g1<T, 2, false><<<grid3(H, nz), kBlk, 0, st>>>(cs3(vr), cd3(r), none, none, v, M, H, c, k, c0);
+  if (phase != 1)
+    k3l_jac_g2<T, 2, false><<<grid3(H, nz), kBlk, 0, st>>>(cd3(r), none, none, cd3(v), v, M, H, c, k, c0);
 }
 template <class T>
 void lv3_asc_fine(const S3<T> &vr, const D3<T> &u_old, const D3<const T> &f, const D3<T> &g, const D3<T> &u_new, int M,
@@ -472,11 +486,11 @@ void lv3_asc_fine(const S3<T> &vr, const D3<T> &u_old, const D3<const T> &f, con
   int H = M / 2 + 1;
   D3<const T> none{nullptr, 0, 0};
   if (order == 2) {
-    k3l_jac_g1<T, 2, true><<<grid3(H), kBlk, 0, st>>>(cs3(vr), none, cd3(u_old), f, g, M, H, c, k);
-    k3l_jac_g2<T, 2, true><<<grid3(H), kBlk, 0, st>>>(none, cd3(u_old), f, cd3(g), u_new, M, H, c, k);
+    k3l_jac_g1<T, 2, true><<<grid3(H, H), kBlk, 0, st>>>(cs3(vr), none, cd3(u_old), f, g, M, H, c, k, 0);
+    k3l_jac_g2<T, 2, true><<<grid3(H, H), kBlk, 0, st>>>(none, cd3(u_old), f, cd3(g), u_new, M, H, c, k, 0);
   } else {
-    k3l_jac_g1<T, 4, true><<<grid3(H), kBlk, 0, st>>>(cs3(vr), none, cd3(u_old), f, g, M, H, c, k);
-    k3l_jac_g2<T, 4, true><<<grid3(H), kBlk, 0, st>>>(none, cd3(u_old), f, cd3(g), u_new, M, H, c, k);
+    k3l_jac_g1<T, 4, true><<<grid3(H, H), kBlk, 0, st>>>(cs3(vr), none, cd3(u_old), f, g, M, H, c, k, 0);
+    k3l_jac_g2<T, 4, true><<<grid3(H, H), kBlk, 0, st>>>(none, cd3(u_old), f, cd3(g), u_new, M, H, c, k, 0);
   }
 }
 
@@ -487,12 +501,12 @@ void lv3_coarse(const Lev3<T> *d_lev, int oc, int k, int *counter, cudaStream_t 
 
 #define INSTL(T)                                                                                                   \
   template void lv3_coarse<T>(const Lev3<T> *, int, int, int *, cudaStream_t);                                     \
-  template void lv3_rest_gr<T>(const D3<T> &, const S3<T> &, int, cudaStream_t);                                   \
-  template void lv3_rest_rm<T>(const S3<T> &, const S3<T> &, int, cudaStream_t);                                   \
-  template void lv3_rest_mg<T>(const S3<T> &, const D3<T> &, int, cudaStream_t);                                   \
-  template void lv3_jac_m<T>(const D3<T> &, const S3<T> &, const S3<T> &, int, T, cudaStream_t);                   \
-  template void lv3_jac_r<T>(const S3<T> &, const S3<T> &, const S3<T> &, int, T, T, cudaStream_t);                \
-  template void lv3_jac_g<T>(const S3<T> &, const D3<T> &, const D3<T> &, int, T, cudaStream_t);                   \
+  template void lv3_rest_gr<T>(const D3<T> &, const S3<T> &, int, cudaStream_t, int, int);                         \
+  template void lv3_rest_rm<T>(const S3<T> &, const S3<T> &, int, cudaStream_t, int, int);                         \
+  template void lv3_rest_mg<T>(const S3<T> &, const D3<T> &, int, cudaStream_t, int, int);                         \
+  template void lv3_jac_m<T>(const D3<T> &, const S3<T> &, const S3<T> &, int, T, cudaStream_t, int, int, int);    \
+  template void lv3_jac_r<T>(const S3<T> &, const S3<T> &, const S3<T> &, int, T, T, cudaStream_t, int, int, int); \
+  template void lv3_jac_g<T>(const S3<T> &, const D3<T> &, const D3<T> &, int, T, cudaStream_t, int, int, int);    \
   template void lv3_asc_fine<T>(const S3<T> &, const D3<T> &, const D3<const T> &, const D3<T> &, const D3<T> &,   \
                                 int, int, T, const Coef<T> &, cudaStream_t);
 

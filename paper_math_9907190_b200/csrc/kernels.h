@@ -98,18 +98,26 @@ void launch3_jac_g(const S3<T> &vr, const D3<T> &r, const D3<T> &v, int M, T c, 
 template <class T>
 void launch3_asc_fine(const S3<T> &vr, const D3<T> &u, const D3<const T> &f, const D3<T> &scratch, const D3<T> &un,
                       int M, int order, T c, const Coef<T> &k, cudaStream_t st);
+// z ranges [zlo, zhi) of global planes (multi-GPU z-slabs); zhi = -1: all.
 template <class T>
 void launch3_residual(const D3<const T> &u, const D3<const T> &f, const D3<T> &r, int M, int order, const Coef<T> &k,
-                      cudaStream_t st);
+                      cudaStream_t st, int zlo = 0, int zhi = -1);
 template <class T>
-void launch3_ftilde(const D3<const T> &f, const D3<T> &ft, int M, cudaStream_t st);
+void launch3_ftilde(const D3<const T> &f, const D3<T> &ft, int M, cudaStream_t st, int zlo = 0, int zhi = -1);
 // TMA plane-streaming kernels (k3f.cu); 16-byte aligned pointers and pitches.
+// ZRange3: the fine planes a launch writes and the local allocations of its
+// inputs (multi-GPU slabs); the default is the whole grid.
+struct ZRange3 {
+  int zlo = 0, zhi = -1;      // output fine planes [zlo, zhi) (-1: all)
+  int fz0 = 0, fplanes = -1;  // fine inputs (u, f): global plane of local plane 0, local planes (-1: all)
+  int hz0 = 0, hplanes = -1;  // half-resolution sublattice inputs (v_R(1))
+};
 template <class T>
 cudaError_t fast3_desc_fine(const T *u, const T *f, int64_t pitch, const S3<T> &rr, int M, int order, const Coef<T> &k,
-                            const NormSink &ns, cudaStream_t st);
+                            const NormSink &ns, cudaStream_t st, const ZRange3 &pz = ZRange3());
 template <class T>
 cudaError_t fast3_asc_fine(const S3<T> &vr, const T *u_old, const T *f, int64_t pitch, T *u_new, int M, int order, T c,
-                           const Coef<T> &k, cudaStream_t st);
+                           const Coef<T> &k, cudaStream_t st, const ZRange3 &pz = ZRange3());
 
 // Per-octave level descriptors for the 3D single-CTA coarse kernel.
 template <class T>
@@ -122,23 +130,30 @@ struct Lev3 {
 template <class T>
 void lv3_coarse(const Lev3<T> *d_lev, int oc, int k, int *counter, cudaStream_t st);
 
-// Sublattice level kernels (k3l.cu).
+// Sublattice level kernels (k3l.cu).  [c0, c1): the half-index planes
+// (2x2x2 blocks; for rest_mg the G(2s) planes) a launch writes; c1 = -1: all.
+// jac_m, jac_r, jac_g run two kernels (the paper's two colours); phase 1 or 2
+// launches only that one (multi-GPU: a halo exchange goes in between), 0 both.
 template <class T>
-void lv3_rest_gr(const D3<T> &r, const S3<T> &rr, int M, cudaStream_t st);
+void lv3_rest_gr(const D3<T> &r, const S3<T> &rr, int M, cudaStream_t st, int c0 = 0, int c1 = -1);
 template <class T>
-void lv3_rest_rm(const S3<T> &rr, const S3<T> &rm, int M, cudaStream_t st);
+void lv3_rest_rm(const S3<T> &rr, const S3<T> &rm, int M, cudaStream_t st, int c0 = 0, int c1 = -1);
 template <class T>
-void lv3_rest_mg(const S3<T> &rm, const D3<T> &g2, int Mc, cudaStream_t st);
+void lv3_rest_mg(const S3<T> &rm, const D3<T> &g2, int Mc, cudaStream_t st, int c0 = 0, int c1 = -1);
 template <class T>
-void lv3_jac_m(const D3<T> &vc, const S3<T> &r, const S3<T> &v, int M, T c, cudaStream_t st);
+void lv3_jac_m(const D3<T> &vc, const S3<T> &r, const S3<T> &v, int M, T c, cudaStream_t st, int c0 = 0, int c1 = -1,
+               int phase = 0);
 template <class T>
-void lv3_jac_r(const S3<T> &vm, const S3<T> &r, const S3<T> &v, int M, T c1, T c2, cudaStream_t st);
+void lv3_jac_r(const S3<T> &vm, const S3<T> &r, const S3<T> &v, int M, T c1, T c2, cudaStream_t st, int cz0 = 0,
+               int cz1 = -1, int phase = 0);
 template <class T>
-void lv3_jac_g(const S3<T> &vr, const D3<T> &r, const D3<T> &v, int M, T c, cudaStream_t st);
+void lv3_jac_g(const S3<T> &vr, const D3<T> &r, const D3<T> &v, int M, T c, cudaStream_t st, int c0 = 0, int c1 = -1,
+               int phase = 0);
 template <class T>
 void lv3_asc_fine(const S3<T> &vr, const D3<T> &u_old, const D3<const T> &f, const D3<T> &g, const D3<T> &u_new, int M,
                   int order, T c, const Coef<T> &k, cudaStream_t st);
 template <class T>
-void launch3_norm(const D3<const T> &a, int M, unsigned long long *mx, double *ss, cudaStream_t st);
+void launch3_norm(const D3<const T> &a, int M, unsigned long long *mx, double *ss, cudaStream_t st, int zlo = 0,
+                  int zhi = -1);
 
 }  // namespace mg

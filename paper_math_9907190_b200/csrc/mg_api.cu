@@ -1,10 +1,11 @@
 // mg_api.cu -- the C ABI of include/mg.h: argument checking, the level plan
 // (buffers in HBM), the per-cycle launch schedule captured in a CUDA graph,
 // norms, staging.  Host code only; the kernels live in k2d.cu / k3d.cu.
+#include "comm.h"
 #include "solver.h"
 
 ImplBase *make_dist2(mg_solver *s, bool loopback, std::string *err);
-int nccl_unique_id(void *out, std::string *err);
+ImplBase *make_dist3(mg_solver *s, bool loopback, std::string *err);
 
 // ------------------------------------------------------------------ 2D
 template <class T>
@@ -503,8 +504,7 @@ static int check_config(const mg_config *c, int *k_out) {
   if (c->pitch != 0 && c->pitch < c->n) return MG_EINVAL;
   if (c->nranks < 0 || (c->nranks > 1 && (c->rank < 0 || c->rank >= c->nranks))) return MG_EINVAL;
   if (c->nranks > 1) {
-    // y-slabs of the 2D hierarchy (dist2.cu); 3D slabs are not in this build
-    if (c->dim != 2) return MG_EUNSUPPORTED;
+    // y-slabs (2D, dist2.cu) / z-slabs (3D, dist3.cu) of the hierarchy
     if (log2_exact(c->nranks) < 0 || ((c->n - 1) / c->nranks) < 4) return MG_EUNSUPPORTED;
     int64_t pt = c->pitch ? c->pitch : c->n;
     if ((pt * (c->dtype == MG_F64 ? 8 : 4)) % 16 != 0) return MG_EUNSUPPORTED;
@@ -557,7 +557,8 @@ int mg_create_ex(const mg_config *cfg, mg_solver **out) {
   CKS(sp, cudaMallocHost(&s->h_hist, sizeof(unsigned long long) * kHistCap));
   if (cfg->nranks > 1) {
     std::string why;
-    ImplBase *d = make_dist2(sp, (cfg->flags & MG_FLAG_LOOPBACK) != 0, &why);
+    const bool lb = (cfg->flags & MG_FLAG_LOOPBACK) != 0;
+    ImplBase *d = cfg->dim == 2 ? make_dist2(sp, lb, &why) : make_dist3(sp, lb, &why);
     if (!d) {
       fprintf(stderr, "[libmg] multi-GPU init failed: %s\n", why.c_str());
       mg_destroy(s.release());
@@ -833,7 +834,7 @@ int mg_slab_plan(int dim, int64_t n, int nranks, int rank, int64_t agglom_points
                  int64_t *ghost, int *agglom_octave) {
   int k = log2_exact(n - 1);
   if (k < 2 || nranks < 1 || rank < 0 || rank >= nranks) return MG_EINVAL;
-  if (dim != 2) return MG_EUNSUPPORTED;
+  if (dim != 2 && dim != 3) return MG_EINVAL;
   if (nranks == 1) {
     if (lo) *lo = 0;
     if (hi) *hi = n;
@@ -847,7 +848,8 @@ int mg_slab_plan(int dim, int64_t n, int nranks, int rank, int64_t agglom_points
   if (hi) *hi = (rank + 1) * R;
   if (ghost) *ghost = 2;
   if (agglom_octave)
-    *agglom_octave = slab_agglom_octave(n, k, nranks, agglom_points > 0 ? agglom_points : (int64_t(1) << 18));
+    *agglom_octave =
+        slab_agglom_octave(n, k, nranks, agglom_points > 0 ? agglom_points : (int64_t(1) << 18), dim);
   return MG_OK;
 }
 

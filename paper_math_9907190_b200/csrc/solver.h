@@ -47,10 +47,11 @@ struct DeviceGuard {
 
 // Slab plan (2D y-slabs): the first octave whose levels are agglomerated:
 // fewer than `ag` interior nodes on A(s), or fewer than 4 rows per rank.
-static inline int slab_agglom_octave(int64_t n, int k, int P, int64_t ag) {
+static inline int slab_agglom_octave(int64_t n, int k, int P, int64_t ag, int dim = 2) {
   for (int o = 1; o < k; o++) {
-    int64_t M = (n - 1) >> o;
-    if ((M - 1) * (M - 1) < ag || M / P < 4) return o;
+    int64_t M = (n - 1) >> o, m = M - 1;
+    int64_t pts = dim == 2 ? m * m : m * m * m;
+    if (pts < ag || M / P < 4) return o;
   }
   return k - 1;
 }

@@ -210,8 +210,8 @@ def broadcast_nccl_id(group=None) -> bytes:
 
 
 def split_rows(full, lo: int, hi: int, ghost: int):
-    """The slab a rank passes in multi-GPU mode: rows [lo - ghost, hi + ghost)
-    of a full (n, pitch) array (rows outside the grid are zero)."""
+    """The slab a rank passes in multi-GPU mode: rows (2D) or planes (3D)
+    [lo - ghost, hi + ghost) of a full array (those outside the grid are zero)."""
     import numpy as _np
     n = full.shape[0]
     out = _np.zeros((hi - lo + 2 * ghost,) + tuple(full.shape[1:]), dtype=full.dtype)
@@ -294,7 +294,8 @@ class Solver:
     def shape(self):
         """Shape of a field as this rank passes it (the slab with ghost rows in multi-GPU mode)."""
         if self.nranks > 1 and not self.loopback:
-            return (self.hi - self.lo + 2 * self.ghost, self.pitch)
+            rows = self.hi - self.lo + 2 * self.ghost
+            return (rows, self.pitch) if self.dim == 2 else (rows, self.n, self.pitch)
         return (self.n, self.pitch) if self.dim == 2 else (self.n, self.n, self.pitch)
 
     def alloc(self, like=None):

@@ -56,13 +56,14 @@ def _plan_body(rank, world):
     from paper_math_9907190_b200 import build, mg
     build.build()
     res = []
-    for n in (65, 129, 1025, 8193):
-        for ag in (0, 16, 1 << 30):
-            lo, hi, g, oa = mg.mg_slab_plan(2, n, world, rank, ag)
-            t = torch.tensor([lo, hi, g, oa], dtype=torch.int64)
-            allt = [torch.zeros(4, dtype=torch.int64) for _ in range(world)]
-            dist.all_gather(allt, t)
-            res.append((n, ag, [x.tolist() for x in allt]))
+    for dim, sizes in ((2, (65, 129, 1025, 8193)), (3, (33, 65, 513))):
+        for n in sizes:
+            for ag in (0, 16, 1 << 30):
+                lo, hi, g, oa = mg.mg_slab_plan(dim, n, world, rank, ag)
+                t = torch.tensor([lo, hi, g, oa], dtype=torch.int64)
+                allt = [torch.zeros(4, dtype=torch.int64) for _ in range(world)]
+                dist.all_gather(allt, t)
+                res.append((dim, n, ag, [x.tolist() for x in allt]))
     return res
 
 
@@ -99,14 +100,18 @@ def _slab_body(rank, world):
 def test_slab_plan_is_consistent_across_ranks():
     out = _spawn("_plan_body")
     assert not isinstance(out[0], str), out
-    for (n, ag, rows), (_, _, rows1) in zip(out[0], out[1]):
+    for (dim, n, ag, rows), (_, _, _, rows1) in zip(out[0], out[1]):
         assert rows == rows1
         (lo0, hi0, g0, oa0), (lo1, hi1, g1, oa1) = rows
-        assert lo0 == 0 and hi0 == lo1 and hi1 == n - 1          # the slabs tile rows [0, n-1)
+        assert lo0 == 0 and hi0 == lo1 and hi1 == n - 1          # the slabs tile rows/planes [0, n-1)
         assert hi0 - lo0 == hi1 - lo1 >= 4 and g0 == g1 == 2      # ghosts owned by the neighbour
         assert oa0 == oa1 >= 1                                    # same agglomeration octave
-        m = (n - 1) >> oa0
-        assert (m - 1) ** 2 < max(ag, 1) or m // 2 < 4 or oa0 == int(np.log2(n - 1)) - 1 or ag == 0
+        k = int(np.log2(n - 1))
+        agp = ag if ag > 0 else 1 << 18
+        # oa is the first octave whose level is below the threshold or too thin to split
+        first = next(o for o in range(1, k) if (((n - 1) >> o) - 1) ** dim < agp or ((n - 1) >> o) // 2 < 4) \
+            if any((((n - 1) >> o) - 1) ** dim < agp or ((n - 1) >> o) // 2 < 4 for o in range(1, k)) else k - 1
+        assert oa0 == first, (dim, n, ag, oa0, first)
 
 
 def test_nccl_id_reaches_every_rank():
