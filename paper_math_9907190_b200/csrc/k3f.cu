@@ -7,6 +7,8 @@
 // plane p from the slots of the last few planes (2.5D blocking: only the xy
 // halo is re-read, from L2).  Node formulas are the shared ones of
 // ops3.cuh, so results are bit-identical to the reference kernels.
+#include <cstdlib>
+
 #include "kernels.h"
 #include "ops3.cuh"
 #include "tma.cuh"
@@ -504,6 +506,8 @@ static cudaError_t desc3_impl(const T *u, const T *f, int64_t pitch, const S3<T>
 template <class T>
 cudaError_t fast3_desc_fine(const T *u, const T *f, int64_t pitch, const S3<T> &rr, int M, int order, const Coef<T> &k,
                             const NormSink &ns, cudaStream_t st, const ZRange3 &pz) {
+  static const bool gen1 = getenv("MG_K3_GEN1") != nullptr;   // A/B switch to the first-generation kernel
+  if (order == 2 && !gen1) return fast3p_desc_fine<T>(u, f, pitch, rr, M, k, ns, st, pz);
   return order == 2 ? desc3_impl<T, 2>(u, f, pitch, rr, M, k, ns, st, pz)
                     : desc3_impl<T, 4>(u, f, pitch, rr, M, k, ns, st, pz);
 }
@@ -544,6 +548,8 @@ static cudaError_t asc3_impl(const S3<T> &vr, const T *u_old, const T *f, int64_
 template <class T>
 cudaError_t fast3_asc_fine(const S3<T> &vr, const T *u_old, const T *f, int64_t pitch, T *u_new, int M, int order, T c,
                            const Coef<T> &k, cudaStream_t st, const ZRange3 &pz) {
+  static const bool gen1 = getenv("MG_K3_GEN1") != nullptr;
+  if (order == 2 && !gen1) return fast3p_asc_fine<T>(vr, u_old, f, pitch, u_new, M, c, k, st, pz);
   return order == 2 ? asc3_impl<T, 2>(vr, u_old, f, pitch, u_new, M, c, k, st, pz)
                     : asc3_impl<T, 4>(vr, u_old, f, pitch, u_new, M, c, k, st, pz);
 }

@@ -119,6 +119,15 @@ template <class T>
 cudaError_t fast3_asc_fine(const S3<T> &vr, const T *u_old, const T *f, int64_t pitch, T *u_new, int M, int order, T c,
                            const Coef<T> &k, cudaStream_t st, const ZRange3 &pz = ZRange3());
 
+// Second-generation register-streaming plane pipelines (k3p.cu), order 2 only;
+// fast3_desc_fine / fast3_asc_fine dispatch to them for order 2.
+template <class T>
+cudaError_t fast3p_desc_fine(const T *u, const T *f, int64_t pitch, const S3<T> &rr, int M, const Coef<T> &k,
+                             const NormSink &ns, cudaStream_t st, const ZRange3 &pz);
+template <class T>
+cudaError_t fast3p_asc_fine(const S3<T> &vr, const T *u_old, const T *f, int64_t pitch, T *u_new, int M, T c,
+                            const Coef<T> &k, cudaStream_t st, const ZRange3 &pz);
+
 // Per-octave level descriptors for the 3D single-CTA coarse kernel.
 template <class T>
 struct Lev3 {
