@@ -21,6 +21,8 @@
 // ops3.cuh, so the results are bit-identical to the oracle.
 // Order 4 (Efos4) keeps the first-generation kernels of k3f.cu: its face
 // diagonals reach the neighbours of the z +- 1 planes.
+#include <type_traits>
+
 #include "kernels.h"
 #include "ops3.cuh"
 #include "tma.cuh"
@@ -62,11 +64,11 @@ __device__ __forceinline__ void ld2(const T *p, T &a, T &b) {
   b = v.y;
 }
 template <class T>
-__device__ __forceinline__ void st2(T *p, T a, T b) {
+__device__ __forceinline__ void st2(T *p, T a, T b) {   // streaming (evict-first) vector store
   typename V2t<T>::t v;
   v.x = a;
   v.y = b;
-  *reinterpret_cast<typename V2t<T>::t *>(p) = v;
+  __stcs(reinterpret_cast<typename V2t<T>::t *>(p), v);
 }
 
 // r = f - (-(6c) + xp + xm + yp + ym + zp + zm) * (n-1)^2   (res3v, order 2)
@@ -117,9 +119,13 @@ struct Sched {
 using namespace zp;
 
 // ------------------------------------------------------------ pipeline
-// Op: NS (slots), SLOT (bytes), SMEM, Params (with .sc, .nunits unused),
-// issue(P, it, j, slot, bar), State, begin(State&, it), step(P, State&, it, j,
-// Lc, Lp, gring) -- step must not touch Lp / the ring after its barrier.
+// Op: NS (slots), SLOT (bytes), SMEM, Params (with .sc), issue(P, it, j,
+// slot, bar), State, Ctx, begin(P, Ctx&, it), step<PH>(P, State&, Ctx&, it,
+// j, Lc, Lp, gz, gq).  PH = j & 1: every parity the step needs (tile origins
+// y0 and x0 are even) is a compile-time function of PH, and the register
+// state is double-buffered by PH, so no selects or register moves remain.
+// The ring of green planes is addressed by byte offsets gz (plane j-1) and
+// gq (plane j-2).
 template <class Op>
 __global__ void __launch_bounds__(NT, 1) zpipe(const __grid_constant__ typename Op::Params P) {
   constexpr int NS = Op::NS, D = NS - 2;
@@ -145,7 +151,7 @@ __global__ void __launch_bounds__(NT, 1) zpipe(const __grid_constant__ typename 
       if (it.ze > it.zs) {
         pk = k;
         pit = it;
-        pj = it.zs - 2;
+        pj = it.zs - Op::PRO;
         pmore = true;
         return;
       }
@@ -170,35 +176,77 @@ __global__ void __launch_bounds__(NT, 1) zpipe(const __grid_constant__ typename 
   for (int k = 0; k < nit; k++) {
     const Item it = P.sc.get(k, b, G);
     if (it.ze <= it.zs) continue;
-    for (int j = it.zs - 2; j <= it.ze + 1; j++) {
+    typename Op::Ctx C;
+    Op::begin(P, C, it);
+    // ring planes rotate by one per step; greens are written and read within one item
+    int gz = 0, gq = 0;
+    auto one = [&](auto ph, int j) {
+      constexpr int PH = decltype(ph)::value;
+      gq = gz;
+      gz = (gz == 2 * Op::GPL) ? 0 : gz + Op::GPL;
       if (threadIdx.x == 0) produce();
       mbar_wait(&bar[cs], phase);
-      Op::step(P, S, it, j, smem + cs * Op::SLOT, smem + cprev * Op::SLOT, gring);
+      Op::template step<PH>(P, S, C, it, j, smem + cs * Op::SLOT, smem + cprev * Op::SLOT, gring + gz, gring + gq);
       __syncthreads();
       cprev = cs;
       if (++cs == NS) {
         cs = 0;
         phase ^= 1;
       }
+    };
+    // unrolled by two so the PH-indexed register state never moves
+    const int jb = it.zs - Op::PRO, je = it.ze + 1;
+    int j = jb;
+    if (j & 1) one(std::integral_constant<int, 1>(), j++);
+    for (; j + 1 <= je; j += 2) {
+      one(std::integral_constant<int, 0>(), j);
+      one(std::integral_constant<int, 1>(), j + 1);
     }
+    if (j <= je) one(std::integral_constant<int, 0>(), j);
   }
   Op::finish(P, S);
 }
 
+// own-node interior masks of an item (x: columns xl, xl+1; y: rows yA, yA+1)
+struct Masks {
+  bool full;             // every own node of every thread is interior in x and y
+  bool c0, c1, rA, rB;   // this thread's columns / rows interior
+};
+__device__ __forceinline__ Masks item_masks(const Item &it, int M, int xl, int yA) {
+  Masks m;
+  m.full = it.x0 - 2 >= 1 && it.x0 + 61 <= M - 1 && it.y0 - 1 >= 1 && it.y0 + 30 <= M - 1;
+  m.c0 = xl >= 1 && xl <= M - 1;
+  m.c1 = xl + 1 >= 1 && xl + 1 <= M - 1;
+  m.rA = yA >= 1 && yA <= M - 1;
+  m.rB = yA + 1 >= 1 && yA + 1 <= M - 1;
+  return m;
+}
+
+// exact max of |r| as the bit pattern of a non-negative double (NaN-safe:
+// NaN patterns sort above +inf, so a diverged residual is never lost)
 template <class T>
-__device__ __forceinline__ T *gptr(unsigned char *gring, int z, int row, int lane) {
-  // green value of ring plane z (z >= -2) at own row index row (-1..32), lane (-1..32)
-  return (T *)(gring + ((z + 3) % 3) * Geo<T>::GPL) + (row + 1) * GS + (lane + 1);
+__device__ __forceinline__ unsigned long long absbits(T v) {
+  return (unsigned long long)__double_as_longlong((double)v) & 0x7fffffffffffffffull;
+}
+__device__ __forceinline__ unsigned long long umax64(unsigned long long a, unsigned long long b) { return a > b ? a : b; }
+
+template <class T>
+__device__ __forceinline__ void sel0(T &v, bool keep) {
+  v = keep ? v : (T)0;
 }
 
 // =================================================== finest descent a9 + a10
-// Step j: r(j-1) at the thread's 4 nodes (registers, greens also to the
-// ring); then Erred at the red nodes of plane q = j-2.
-template <class T>
+// Step j: r(j-1) at the thread's 4 nodes (registers; the green ones also to
+// the ring); then Erred at the red nodes of plane q = j-2.
+// Parities (yA odd, xl even): the red column of row A at plane z is (z+1) & 1,
+// i.e. PH at z = j-1 and Q = 1-PH at q = j-2; row B the other way round.
+// FINE = false: the same pass one octave down (G(s) -> R(s), s > 1): r is
+// read from the dense level array (the "f" box) instead of computed, no norm.
+template <class T, bool FINE = true>
 struct OpDesc3P {
   using Gm = Geo<T>;
-  static constexpr int NS = sizeof(T) == 8 ? 5 : 8;
-  static constexpr int U_OFF = 0, F_OFF = al128(Gm::U_BYTES), SLOT = al128(F_OFF + Gm::F_BYTES);
+  static constexpr int NS = FINE ? (sizeof(T) == 8 ? 5 : 8) : 8, GPL = Gm::GPL, PRO = FINE ? 2 : 0;
+  static constexpr int U_OFF = 0, F_OFF = FINE ? al128(Gm::U_BYTES) : 0, SLOT = al128(F_OFF + Gm::F_BYTES);
   static constexpr int SMEM = NS * SLOT + 3 * Gm::GPL;
   struct Params {
     CUtensorMap tu, tf;
@@ -209,37 +257,66 @@ struct OpDesc3P {
     NormSink ns;
   };
   struct State {
-    T um[2][2], uc[2][2];   // own u(j-2), u(j-1): [row A/B][col 0/1]
-    T r0[2][2], r1[2][2];   // own r(j-3), r(j-2)
-    double mx;
+    T u[2][2][2];   // [z & 1][row A/B][col 0/1]: own u of the two latest planes
+    T r[2][2][2];   // own r of the two latest planes
+    unsigned long long mx;
+  };
+  struct Ctx {
+    Masks m;
+    bool oA[2], oB[2];   // Erred output at row A / B, by PH
+    int64_t bA, bB;      // sublattice offsets (y >> 1) * pitch + (xl >> 1) of rows A, B
   };
   static __device__ void prefetch(const Params &P) {
-    tma_prefetch_desc(&P.tu);
+    if (FINE) tma_prefetch_desc(&P.tu);
     tma_prefetch_desc(&P.tf);
   }
-  static __device__ void init(State &S) { S.mx = 0.0; }
+  static __device__ void init(State &S) { S.mx = 0ull; }
+  static __device__ void begin(const Params &P, Ctx &C, const Item &it) {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int xl = it.x0 - 2 + 2 * lane, yA = it.y0 - 1 + 2 * w;
+    C.m = item_masks(it, P.M, xl, yA);
+    const bool lk = lane >= 1 && lane <= TX / 2;
+    // PH = 0: row A red at col 1, row B at col 0; PH = 1: the other way round
+    C.oA[0] = lk && w >= 1 && C.m.rA && C.m.c1;
+    C.oA[1] = lk && w >= 1 && C.m.rA && C.m.c0;
+    C.oB[0] = lk && w <= 14 && C.m.rB && C.m.c0;
+    C.oB[1] = lk && w <= 14 && C.m.rB && C.m.c1;
+    C.bA = (int64_t)(yA >> 1) * P.out.pitch + (xl >> 1);
+    C.bB = (int64_t)((yA + 1) >> 1) * P.out.pitch + (xl >> 1);
+  }
   static __device__ void issue(const Params &P, const Item &it, int j, unsigned char *slot, uint64_t *bar) {
     const bool wf = j >= it.zs;
-    mbar_expect_tx(bar, Gm::U_BYTES + (wf ? Gm::F_BYTES : 0));
-    tma_load_3d(slot + U_OFF, &P.tu, it.x0 - Gm::UXO, it.y0 - 2, j - P.fz0, bar);
+    mbar_expect_tx(bar, (FINE ? Gm::U_BYTES : 0) + (wf ? Gm::F_BYTES : 0));
+    if (FINE) tma_load_3d(slot + U_OFF, &P.tu, it.x0 - Gm::UXO, it.y0 - 2, j - P.fz0, bar);
     if (wf) tma_load_3d(slot + F_OFF, &P.tf, it.x0 - 2, it.y0 - 1, j - 1 - P.fz0, bar);
   }
-  static __device__ __forceinline__ void step(const Params &P, State &S, const Item &it, int j, unsigned char *Lc,
-                                              unsigned char *Lp, unsigned char *gring) {
+  template <int PH>
+  static __device__ __forceinline__ void step(const Params &P, State &S, const Ctx &C, const Item &it, int j,
+                                              unsigned char *Lc, unsigned char *Lp, unsigned char *gz,
+                                              unsigned char *gq) {
+    constexpr int Q = PH ^ 1;   // slot of planes j-1, j-3
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, M = P.M;
-    const int xl = it.x0 - 2 + 2 * lane, yA = it.y0 - 1 + 2 * w;
     const int uo = (2 * w + 1) * Gm::UW + 2 * lane - 2 + Gm::UXO;   // u box offset of (xl, yA)
     const int fo = 2 * w * Gm::FW + 2 * lane;                         // f box offset of (xl, yA)
     T un[2][2];
-    {
+    if (FINE) {
       const T *U = (const T *)(Lc + U_OFF);
       ld2(U + uo, un[0][0], un[0][1]);
       ld2(U + uo + Gm::UW, un[1][0], un[1][1]);
     }
     if (j >= it.zs) {
-      // ---- r(j-1) at the own nodes
-      const T *U = (const T *)(Lp + U_OFF) + uo;   // u(j-1) at (xl, yA)
-      const T *F = (const T *)(Lc + F_OFF) + fo;   // f(j-1)
+      T rn[2][2];
+      const int z = j - 1;
+      if constexpr (!FINE) {
+        const T *F = (const T *)(Lc + F_OFF) + fo;   // r(z) from the level array (zero outside the interior)
+        ld2(F, rn[0][0], rn[0][1]);
+        ld2(F + Gm::FW, rn[1][0], rn[1][1]);
+      } else {
+      // ---- r(z), z = j-1: centre u(j-1) = S.u[Q], z-1 = S.u[PH] (u(j-2)), z+1 = un
+      const T(&uc)[2][2] = S.u[Q];
+      const T(&um)[2][2] = S.u[PH];
+      const T *U = (const T *)(Lp + U_OFF) + uo;
+      const T *F = (const T *)(Lc + F_OFF) + fo;
       T ymA0, ymA1, ypB0, ypB1, t, lA, rA, lB, rB, fA0, fA1, fB0, fB1;
       ld2(U - Gm::UW, ymA0, ymA1);
       ld2(U + 2 * Gm::UW, ypB0, ypB1);
@@ -250,113 +327,112 @@ struct OpDesc3P {
       ld2(F, fA0, fA1);
       ld2(F + Gm::FW, fB0, fB1);
       const T h = P.invh2;
-      T rn[2][2];
       // i+1, i-1, j+1, j-1, k+1, k-1
-      rn[0][0] = res7(S.uc[0][0], S.uc[0][1], lA, S.uc[1][0], ymA0, un[0][0], S.um[0][0], fA0, h);
-      rn[0][1] = res7(S.uc[0][1], rA, S.uc[0][0], S.uc[1][1], ymA1, un[0][1], S.um[0][1], fA1, h);
-      rn[1][0] = res7(S.uc[1][0], S.uc[1][1], lB, ypB0, S.uc[0][0], un[1][0], S.um[1][0], fB0, h);
-      rn[1][1] = res7(S.uc[1][1], rB, S.uc[1][0], ypB1, S.uc[0][1], un[1][1], S.um[1][1], fB1, h);
-      const int z = j - 1;
+      rn[0][0] = res7(uc[0][0], uc[0][1], lA, uc[1][0], ymA0, un[0][0], um[0][0], fA0, h);
+      rn[0][1] = res7(uc[0][1], rA, uc[0][0], uc[1][1], ymA1, un[0][1], um[0][1], fA1, h);
+      rn[1][0] = res7(uc[1][0], uc[1][1], lB, ypB0, uc[0][0], un[1][0], um[1][0], fB0, h);
+      rn[1][1] = res7(uc[1][1], rB, uc[1][0], ypB1, uc[0][1], un[1][1], um[1][1], fB1, h);
       const bool zin = z >= 1 && z <= M - 1;
-      const bool c0 = xl >= 1 && xl <= M - 1, c1 = xl + 1 >= 1 && xl + 1 <= M - 1;
-      const bool a = zin && yA >= 1 && yA <= M - 1, bb = zin && yA + 1 >= 1 && yA + 1 <= M - 1;
-      rn[0][0] = (a && c0) ? rn[0][0] : (T)0;
-      rn[0][1] = (a && c1) ? rn[0][1] : (T)0;
-      rn[1][0] = (bb && c0) ? rn[1][0] : (T)0;
-      rn[1][1] = (bb && c1) ? rn[1][1] : (T)0;
+      if (!(C.m.full && zin)) {
+        sel0(rn[0][0], zin && C.m.rA && C.m.c0);
+        sel0(rn[0][1], zin && C.m.rA && C.m.c1);
+        sel0(rn[1][0], zin && C.m.rB && C.m.c0);
+        sel0(rn[1][1], zin && C.m.rB && C.m.c1);
+      }
       // every computed r is a true residual (or 0): max over all of them
-      S.mx = nmax(S.mx, nmax(nmax(absd(rn[0][0]), absd(rn[0][1])), nmax(absd(rn[1][0]), absd(rn[1][1]))));
-      // green (x+y+z odd) values to the ring; red column offset of row A = (yA + z) & 1
-      const int pA = (yA + z) & 1;
-      *gptr<T>(gring, z, 2 * w, lane) = pA ? rn[0][0] : rn[0][1];
-      *gptr<T>(gring, z, 2 * w + 1, lane) = pA ? rn[1][1] : rn[1][0];
-      // ---- Erred at the red nodes of q = j-2: r(q-1) = S.r0, r(q) = S.r1, r(q+1) = rn
+      S.mx = umax64(S.mx, umax64(umax64(absbits(rn[0][0]), absbits(rn[0][1])),
+                                 umax64(absbits(rn[1][0]), absbits(rn[1][1]))));
+      }
+      // greens of plane z to the ring: red column of row A at z is PH, so its
+      // green is column Q; row B (even y) the other way round
+      {
+        T *g = (T *)gz + (2 * w + 1) * GS + (lane + 1);
+        g[0] = rn[0][Q];
+        g[GS] = rn[1][PH];
+      }
+      // ---- Erred at the red nodes of q = j-2: r(q-1) = S.r[Q], r(q) = S.r[PH], r(q+1) = rn.
+      // Red column of row A at q is Q, of row B is PH.
       const int q = j - 2;
-      if (q >= it.zs && q >= 1 && q <= M - 1 && lane >= 1 && lane <= TX / 2) {
-        const int qA = (yA + q) & 1;   // red column of row A (row B: 1 - qA)
-        const T *g = gptr<T>(gring, q, 2 * w, lane);
+      if (q >= it.zs && q >= 1 && q <= M - 1 && (C.oA[PH] || C.oB[PH])) {
+        const T(&R1)[2][2] = S.r[PH];
+        const T(&R0)[2][2] = S.r[Q];
+        const T *g = (const T *)gq + (2 * w + 1) * GS + (lane + 1);
+        const T ymA = g[-GS], ypB = g[2 * GS];
         T sA, sB;
-        if (qA == 0) {
+        if (Q == 0) {
           // row A red at col 0: i+1 own col 1, i-1 lane-1; row B red at col 1: i+1 lane+1, i-1 own col 0
-          const T xmA = g[-1], xpB = g[GS + 1], ymA = g[-GS], ypB = g[2 * GS];
-          T t1 = (T)6 * S.r1[0][0];
-          t1 = t1 + S.r1[0][1];
-          t1 = t1 + xmA;
-          t1 = t1 + S.r1[1][0];
+          T t1 = (T)6 * R1[0][0];
+          t1 = t1 + R1[0][1];
+          t1 = t1 + g[-1];
+          t1 = t1 + R1[1][0];
           t1 = t1 + ymA;
           t1 = t1 + rn[0][0];
-          t1 = t1 + S.r0[0][0];
+          t1 = t1 + R0[0][0];
           sA = t1 * (T)(1.0 / 12.0);
-          T t2 = (T)6 * S.r1[1][1];
-          t2 = t2 + xpB;
-          t2 = t2 + S.r1[1][0];
+          T t2 = (T)6 * R1[1][1];
+          t2 = t2 + g[GS + 1];
+          t2 = t2 + R1[1][0];
           t2 = t2 + ypB;
-          t2 = t2 + S.r1[0][1];
+          t2 = t2 + R1[0][1];
           t2 = t2 + rn[1][1];
-          t2 = t2 + S.r0[1][1];
+          t2 = t2 + R0[1][1];
           sB = t2 * (T)(1.0 / 12.0);
         } else {
           // row A red at col 1: i+1 lane+1, i-1 own col 0; row B red at col 0: i+1 own col 1, i-1 lane-1
-          const T xpA = g[1], xmB = g[GS - 1], ymA = g[-GS], ypB = g[2 * GS];
-          T t1 = (T)6 * S.r1[0][1];
-          t1 = t1 + xpA;
-          t1 = t1 + S.r1[0][0];
-          t1 = t1 + S.r1[1][1];
+          T t1 = (T)6 * R1[0][1];
+          t1 = t1 + g[1];
+          t1 = t1 + R1[0][0];
+          t1 = t1 + R1[1][1];
           t1 = t1 + ymA;
           t1 = t1 + rn[0][1];
-          t1 = t1 + S.r0[0][1];
+          t1 = t1 + R0[0][1];
           sA = t1 * (T)(1.0 / 12.0);
-          T t2 = (T)6 * S.r1[1][0];
-          t2 = t2 + S.r1[1][1];
-          t2 = t2 + xmB;
+          T t2 = (T)6 * R1[1][0];
+          t2 = t2 + R1[1][1];
+          t2 = t2 + g[GS - 1];
           t2 = t2 + ypB;
-          t2 = t2 + S.r1[0][0];
+          t2 = t2 + R1[0][0];
           t2 = t2 + rn[1][0];
-          t2 = t2 + S.r0[1][0];
+          t2 = t2 + R0[1][0];
           sB = t2 * (T)(1.0 / 12.0);
         }
-        const int hx = xl >> 1;
+        // sublattice (x&1 | (y&1)<<1 | (q&1)<<2): row A (odd y) x&1 = Q; row B (even y) x&1 = PH
         const int64_t zoff = (int64_t)(q >> 1) * P.out.plane;
-        // row A: x = xl + qA; row B: x = xl + 1 - qA
-        if (w >= 1 && yA <= M - 1 && yA >= 1 && xl + qA <= M - 1 && xl + qA >= 1) {
-          const int sl = qA | ((yA & 1) << 1) | ((q & 1) << 2);
-          P.out.s[sl][zoff + (int64_t)(yA >> 1) * P.out.pitch + hx] = sA;
-        }
-        const int yB = yA + 1, xb = xl + 1 - qA;
-        if (w <= 14 && yB <= M - 1 && yB >= 1 && xb <= M - 1 && xb >= 1) {
-          const int sl = (1 - qA) | ((yB & 1) << 1) | ((q & 1) << 2);
-          P.out.s[sl][zoff + (int64_t)(yB >> 1) * P.out.pitch + hx] = sB;
-        }
+        // streaming stores: r_R(1) is not re-read in this pass, keep L2 for the halos
+        if (C.oA[PH]) __stcs(&P.out.s[Q | 2 | (PH << 2)][zoff + C.bA], sA);
+        if (C.oB[PH]) __stcs(&P.out.s[PH | (PH << 2)][zoff + C.bB], sB);
       }
 #pragma unroll
       for (int r = 0; r < 2; r++)
 #pragma unroll
-        for (int c = 0; c < 2; c++) {
-          S.r0[r][c] = S.r1[r][c];
-          S.r1[r][c] = rn[r][c];
-        }
+        for (int c = 0; c < 2; c++) S.r[Q][r][c] = rn[r][c];
     }
+    if (FINE) {
 #pragma unroll
-    for (int r = 0; r < 2; r++)
+      for (int r = 0; r < 2; r++)
 #pragma unroll
-      for (int c = 0; c < 2; c++) {
-        S.um[r][c] = S.uc[r][c];
-        S.uc[r][c] = un[r][c];
-      }
+        for (int c = 0; c < 2; c++) S.u[PH][r][c] = un[r][c];
+    }
   }
-  static __device__ void finish(const Params &P, State &S) { block_norm_push<NT>(P.ns, S.mx); }
+  static __device__ void finish(const Params &P, State &S) {
+    if (FINE) block_norm_push<NT>(P.ns, __longlong_as_double((long long)S.mx));
+  }
 };
 
 // ================================================== finest ascent a15 (s = 1)
 // Step j: r(j-1) at the 4 own nodes; Egprolg at the green node of
-// each own row of plane j-1 (red neighbours from v_R(j-1) in shared memory,
-// v_R(j), v_R(j-2) own); then Egprolr at the red nodes of plane
+// each own row of plane z = j-1 (red neighbours from v_R(z) in shared memory,
+// v_R(z+1), v_R(z-1) own); then Egprolr at the red nodes of plane
 // q = j-2 from the green values, and u_new = u_old + v there.
-template <class T>
+// Green column of row A at plane z = j-1 is Q = 1-PH (row B: PH); the red
+// column of row A at plane q = j-2 is Q as well.
+// FINE = false: Egprolg/Egprolr one octave down (G(s) from R(s), s > 1): r is
+// read from the dense level array (the "f" box) and v_G(s) is written.
+template <class T, bool FINE = true>
 struct OpAsc3P {
   using Gm = Geo<T>;
-  static constexpr int NS = sizeof(T) == 8 ? 4 : 7;
-  static constexpr int U_OFF = 0, F_OFF = al128(Gm::U_BYTES), V0_OFF = F_OFF + al128(Gm::F_BYTES),
+  static constexpr int NS = FINE ? (sizeof(T) == 8 ? 4 : 7) : (sizeof(T) == 8 ? 7 : 10), GPL = Gm::GPL, PRO = 2;
+  static constexpr int U_OFF = 0, F_OFF = FINE ? al128(Gm::U_BYTES) : 0, V0_OFF = F_OFF + al128(Gm::F_BYTES),
                        V1_OFF = V0_OFF + al128(Gm::V_BYTES), SLOT = al128(V1_OFF + Gm::V_BYTES);
   static constexpr int SMEM = NS * SLOT + 3 * Gm::GPL;
   struct Params {
@@ -367,22 +443,36 @@ struct OpAsc3P {
     T c, invh2;
   };
   struct State {
-    T um[2][2], uc[2][2];   // own u(j-2), u(j-1)
-    T r1[2][2];             // own r(j-2)
-    T g0[2], g1[2];         // own green v of planes j-3, j-2 (one per row)
-    T vr0[2], vr1[2];       // own v_R of planes j-2, j-1 (at the green column of the plane below)
+    T u[2][2][2];   // [z & 1][row][col] own u
+    T rq[2];        // own r(j-2) at the red node of rows A, B
+    T g[2][2];      // [z & 1][row] own green v
+    T vr[2][2];     // [z & 1][row] own v_R(z) at the green column of plane z-1
+  };
+  struct Ctx {
+    Masks m;
+    bool oA, oB;   // u_new rows written (lane, warp, y interior)
+    int hx;        // half-index column of xl in the V boxes
   };
   static __device__ void prefetch(const Params &P) {
-    tma_prefetch_desc(&P.tu);
+    if (FINE) tma_prefetch_desc(&P.tu);
     tma_prefetch_desc(&P.tf);
     for (int i = 0; i < 4; i++) tma_prefetch_desc(&P.tv[i]);
   }
   static __device__ void init(State &) {}
   static __device__ __forceinline__ int vx0(int x0) { return (x0 / 2 - 2) & ~(Gm::AL - 1); }
+  static __device__ void begin(const Params &P, Ctx &C, const Item &it) {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int xl = it.x0 - 2 + 2 * lane, yA = it.y0 - 1 + 2 * w;
+    C.m = item_masks(it, P.M, xl, yA);
+    const bool lk = lane >= 1 && lane <= TX / 2;
+    C.oA = lk && w >= 1 && C.m.rA;
+    C.oB = lk && w <= 14 && C.m.rB;
+    C.hx = (xl >> 1) - vx0(it.x0);
+  }
   static __device__ void issue(const Params &P, const Item &it, int j, unsigned char *slot, uint64_t *bar) {
     const bool wf = j >= it.zs;
-    mbar_expect_tx(bar, Gm::U_BYTES + 2 * Gm::V_BYTES + (wf ? Gm::F_BYTES : 0));
-    tma_load_3d(slot + U_OFF, &P.tu, it.x0 - Gm::UXO, it.y0 - 2, j - P.fz0, bar);
+    mbar_expect_tx(bar, (FINE ? Gm::U_BYTES : 0) + 2 * Gm::V_BYTES + (wf ? Gm::F_BYTES : 0));
+    if (FINE) tma_load_3d(slot + U_OFF, &P.tu, it.x0 - Gm::UXO, it.y0 - 2, j - P.fz0, bar);
     if (wf) tma_load_3d(slot + F_OFF, &P.tf, it.x0 - 2, it.y0 - 1, j - 1 - P.fz0, bar);
     // red nodes of fine plane j: even j -> C (even x), Fz (odd x); odd j -> Fx (even x), Fy (odd x)
     const int hz = j >> 1;
@@ -401,31 +491,37 @@ struct OpAsc3P {
     t = t + v5;
     return t * (T)(1.0 / 6.0);
   }
-  static __device__ __forceinline__ void step(const Params &P, State &S, const Item &it, int j, unsigned char *Lc,
-                                              unsigned char *Lp, unsigned char *gring) {
+  template <int PH>
+  static __device__ __forceinline__ void step(const Params &P, State &S, const Ctx &C, const Item &it, int j,
+                                              unsigned char *Lc, unsigned char *Lp, unsigned char *gz,
+                                              unsigned char *gq) {
+    constexpr int Q = PH ^ 1;
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, M = P.M;
-    const int xl = it.x0 - 2 + 2 * lane, yA = it.y0 - 1 + 2 * w;
     const int uo = (2 * w + 1) * Gm::UW + 2 * lane - 2 + Gm::UXO;
     const int fo = 2 * w * Gm::FW + 2 * lane;
-    const int vxo = vx0(it.x0), vyo = it.y0 / 2 - 1;
-    const int z = j - 1;
-    // green column of plane z in row A (row B: the other one); red column = 1 - that
-    const int gA = 1 - ((yA + z) & 1);
     T un[2][2];
-    {
+    if (FINE) {
       const T *U = (const T *)(Lc + U_OFF);
       ld2(U + uo, un[0][0], un[0][1]);
       ld2(U + uo + Gm::UW, un[1][0], un[1][1]);
     }
-    // own v_R(j) at the green column of plane j-1 (x = xl + gA / xl + 1 - gA; half index xl/2)
+    // own v_R(j) at the green column of plane j-1: row A col Q (parity Q -> V box Q), row B col PH
+    // (V rows: half row of yA is w, of yA+1 is w+1 in the box)
     T vrn[2];
     {
-      const int ho = (yA >> 1) - vyo, hb = ((yA + 1) >> 1) - vyo, hx = (xl >> 1) - vxo;
-      const T *V0 = (const T *)(Lc + V0_OFF), *V1 = (const T *)(Lc + V1_OFF);
-      vrn[0] = (gA ? V1 : V0)[ho * Gm::VW + hx];
-      vrn[1] = (gA ? V0 : V1)[hb * Gm::VW + hx];
+      const T *VA = (const T *)(Lc + (Q ? V1_OFF : V0_OFF)), *VB = (const T *)(Lc + (PH ? V1_OFF : V0_OFF));
+      vrn[0] = VA[w * Gm::VW + C.hx];
+      vrn[1] = VB[(w + 1) * Gm::VW + C.hx];
     }
     if (j >= it.zs) {
+      T rn[2][2];
+      if constexpr (!FINE) {
+        const T *F = (const T *)(Lc + F_OFF) + fo;   // r(j-1) from the level array
+        ld2(F, rn[0][0], rn[0][1]);
+        ld2(F + Gm::FW, rn[1][0], rn[1][1]);
+      } else {
+      const T(&uc)[2][2] = S.u[Q];
+      const T(&um)[2][2] = S.u[PH];
       const T *U = (const T *)(Lp + U_OFF) + uo;
       const T *F = (const T *)(Lc + F_OFF) + fo;
       T ymA0, ymA1, ypB0, ypB1, t, lA, rA, lB, rB, fA0, fA1, fB0, fB1;
@@ -438,93 +534,104 @@ struct OpAsc3P {
       ld2(F, fA0, fA1);
       ld2(F + Gm::FW, fB0, fB1);
       const T h = P.invh2;
-      T rn[2][2];
-      rn[0][0] = res7(S.uc[0][0], S.uc[0][1], lA, S.uc[1][0], ymA0, un[0][0], S.um[0][0], fA0, h);
-      rn[0][1] = res7(S.uc[0][1], rA, S.uc[0][0], S.uc[1][1], ymA1, un[0][1], S.um[0][1], fA1, h);
-      rn[1][0] = res7(S.uc[1][0], S.uc[1][1], lB, ypB0, S.uc[0][0], un[1][0], S.um[1][0], fB0, h);
-      rn[1][1] = res7(S.uc[1][1], rB, S.uc[1][0], ypB1, S.uc[0][1], un[1][1], S.um[1][1], fB1, h);
-      // ---- Egprolg at the green node of rows A, B of plane z
+      rn[0][0] = res7(uc[0][0], uc[0][1], lA, uc[1][0], ymA0, un[0][0], um[0][0], fA0, h);
+      rn[0][1] = res7(uc[0][1], rA, uc[0][0], uc[1][1], ymA1, un[0][1], um[0][1], fA1, h);
+      rn[1][0] = res7(uc[1][0], uc[1][1], lB, ypB0, uc[0][0], un[1][0], um[1][0], fB0, h);
+      rn[1][1] = res7(uc[1][1], rB, uc[1][0], ypB1, uc[0][1], un[1][1], um[1][1], fB1, h);
+      }
+      // ---- Egprolg at the green nodes (row A col Q, row B col PH) of plane z = j-1
+      const int z = j - 1;
       const bool zin = z >= 1 && z <= M - 1;
       T gn[2];
       {
         const T *V0 = (const T *)(Lp + V0_OFF), *V1 = (const T *)(Lp + V1_OFF);   // v_R(z)
-        const int hx = (xl >> 1) - vxo;
-#pragma unroll
-        for (int R = 0; R < 2; R++) {
-          const int y = yA + R, gc = R ? 1 - gA : gA, xg = xl + gc;
-          const int hy = (y >> 1) - vyo;
-          // x neighbours xg +- 1 have parity 1 - gc; y neighbours parity gc
-          const T *VX = gc ? V0 : V1, *VY = gc ? V1 : V0;
-          T xp, xm;
-          if (gc) {   // xg odd: xg+1 -> half hx+1, xg-1 -> hx
-            xp = VX[hy * Gm::VW + hx + 1];
-            xm = VX[hy * Gm::VW + hx];
-          } else {    // xg even: xg+1 -> hx, xg-1 -> hx-1
-            xp = VX[hy * Gm::VW + hx];
-            xm = VX[hy * Gm::VW + hx - 1];
-          }
-          const T yp = VY[(((y + 1) >> 1) - vyo) * Gm::VW + hx];
-          const T ym = VY[(((y - 1) >> 1) - vyo) * Gm::VW + hx];
-          const T r = gc ? rn[R][1] : rn[R][0];
-          const bool in = zin && y >= 1 && y <= M - 1 && xg >= 1 && xg <= M - 1;
-          gn[R] = in ? jac6(P.c, r, xp, xm, yp, ym, vrn[R], S.vr0[R]) : (T)0;
-        }
-      }
-      *gptr<T>(gring, z, 2 * w, lane) = gn[0];
-      *gptr<T>(gring, z, 2 * w + 1, lane) = gn[1];
-      // ---- Egprolr at the red nodes of q = j-2, then u_new = u_old + v
-      const int q = j - 2;
-      if (q >= it.zs && q >= 1 && q <= M - 1 && lane >= 1 && lane <= TX / 2) {
-        // red column of row A at plane q = green column of row A at plane z = gA
-        const T *g = gptr<T>(gring, q, 2 * w, lane);
-        const T ymA = g[-GS], ypB = g[2 * GS];
-        T vA, vB;
-        if (gA == 0) {
-          // row A red col 0: i+1 own green (col 1), i-1 lane-1; row B red col 1: i+1 lane+1, i-1 own green
-          vA = jac6(P.c, S.r1[0][0], S.g1[0], g[-1], S.g1[1], ymA, gn[0], S.g0[0]);
-          vB = jac6(P.c, S.r1[1][1], g[GS + 1], S.g1[1], ypB, S.g1[0], gn[1], S.g0[1]);
+        const int hx = C.hx;
+        // row A (half row w): green col Q; x neighbours have parity PH, y neighbours parity Q
+        const T *XA = PH ? V1 : V0, *YA = Q ? V1 : V0;
+        // row B (half row w+1): green col PH; x neighbours parity Q, y neighbours parity PH
+        const T *XB = Q ? V1 : V0, *YB = PH ? V1 : V0;
+        T xpA, xmA, xpB, xmB;
+        if (Q) {   // row A green at odd x: xg+1 -> hx+1, xg-1 -> hx; row B green at even x
+          xpA = XA[w * Gm::VW + hx + 1];
+          xmA = XA[w * Gm::VW + hx];
+          xpB = XB[(w + 1) * Gm::VW + hx];
+          xmB = XB[(w + 1) * Gm::VW + hx - 1];
         } else {
-          vA = jac6(P.c, S.r1[0][1], g[1], S.g1[0], S.g1[1], ymA, gn[0], S.g0[0]);
-          vB = jac6(P.c, S.r1[1][0], S.g1[1], g[GS - 1], ypB, S.g1[0], gn[1], S.g0[1]);
+          xpA = XA[w * Gm::VW + hx];
+          xmA = XA[w * Gm::VW + hx - 1];
+          xpB = XB[(w + 1) * Gm::VW + hx + 1];
+          xmB = XB[(w + 1) * Gm::VW + hx];
         }
-        // u_new = u(q) + v: u(q) = S.um; row A: red col gA, green col 1-gA
-        const T a0 = S.um[0][0] + (gA ? S.g1[0] : vA), a1 = S.um[0][1] + (gA ? vA : S.g1[0]);
-        const T b0 = S.um[1][0] + (gA ? vB : S.g1[1]), b1 = S.um[1][1] + (gA ? S.g1[1] : vB);
-        const bool k0 = xl >= 1 && xl <= M - 1, k1 = xl + 1 >= 1 && xl + 1 <= M - 1;
+        // y neighbours: row A (yA odd): yA+1 -> half row w+1, yA-1 -> w; row B (even): yB+1 -> w+1, yB-1 -> w
+        const T ypA = YA[(w + 1) * Gm::VW + hx], ymA = YA[w * Gm::VW + hx];
+        const T ypB2 = YB[(w + 1) * Gm::VW + hx], ymB2 = YB[w * Gm::VW + hx];
+        gn[0] = jac6(P.c, rn[0][Q], xpA, xmA, ypA, ymA, vrn[0], S.vr[PH][0]);
+        gn[1] = jac6(P.c, rn[1][PH], xpB, xmB, ypB2, ymB2, vrn[1], S.vr[PH][1]);
+        if (!(C.m.full && zin)) {
+          sel0(gn[0], zin && C.m.rA && (Q ? C.m.c1 : C.m.c0));
+          sel0(gn[1], zin && C.m.rB && (PH ? C.m.c1 : C.m.c0));
+        }
+      }
+      {
+        T *g = (T *)gz + (2 * w + 1) * GS + (lane + 1);
+        g[0] = gn[0];
+        g[GS] = gn[1];
+      }
+      // ---- Egprolr at the red nodes of q = j-2 (row A col Q, row B col PH), then u_new
+      const int q = j - 2;
+      if (q >= it.zs && q >= 1 && q <= M - 1 && (C.oA || C.oB)) {
+        const T *g = (const T *)gq + (2 * w + 1) * GS + (lane + 1);
+        const T ymA = g[-GS], ypB = g[2 * GS];
+        const T(&g1)[2] = S.g[PH];   // greens of plane q
+        const T(&g0)[2] = S.g[Q];    // greens of plane q-1
+        T vA, vB, a0, a1, b0, b1;
+        if (Q == 0) {
+          // row A red col 0: i+1 own green, i-1 lane-1; row B red col 1: i+1 lane+1, i-1 own green
+          vA = jac6(P.c, S.rq[0], g1[0], g[-1], g1[1], ymA, gn[0], g0[0]);
+          vB = jac6(P.c, S.rq[1], g[GS + 1], g1[1], ypB, g1[0], gn[1], g0[1]);
+          a0 = vA;
+          a1 = g1[0];
+          b0 = g1[1];
+          b1 = vB;
+        } else {
+          // row A red col 1: i+1 lane+1, i-1 own green; row B red col 0: i+1 own green, i-1 lane-1
+          vA = jac6(P.c, S.rq[0], g[1], g1[0], g1[1], ymA, gn[0], g0[0]);
+          vB = jac6(P.c, S.rq[1], g1[1], g[GS - 1], ypB, g1[0], gn[1], g0[1]);
+          a0 = g1[0];
+          a1 = vA;
+          b0 = vB;
+          b1 = g1[1];
+        }
+        if (FINE) {   // u_new = u_old + v
+          a0 = S.u[PH][0][0] + a0;
+          a1 = S.u[PH][0][1] + a1;
+          b0 = S.u[PH][1][0] + b0;
+          b1 = S.u[PH][1][1] + b1;
+        }
+        const int xl = it.x0 - 2 + 2 * lane, yA = it.y0 - 1 + 2 * w;
         T *dst = &P.out(xl, yA, q);
-        if (w >= 1 && yA >= 1 && yA <= M - 1) {
-          if (k0 && k1) st2(dst, a0, a1);
-          else {
-            if (k0) dst[0] = a0;
-            if (k1) dst[1] = a1;
-          }
-        }
-        dst += P.out.pitch;
-        if (w <= 14 && yA + 1 >= 1 && yA + 1 <= M - 1) {
-          if (k0 && k1) st2(dst, b0, b1);
-          else {
-            if (k0) dst[0] = b0;
-            if (k1) dst[1] = b1;
-          }
+        if (C.m.c0 && C.m.c1) {
+          if (C.oA) st2(dst, a0, a1);
+          if (C.oB) st2(dst + P.out.pitch, b0, b1);
+        } else {
+          if (C.oA && C.m.c0) __stcs(dst, a0);
+          if (C.oA && C.m.c1) __stcs(dst + 1, a1);
+          if (C.oB && C.m.c0) __stcs(dst + P.out.pitch, b0);
+          if (C.oB && C.m.c1) __stcs(dst + P.out.pitch + 1, b1);
         }
       }
-#pragma unroll
-      for (int R = 0; R < 2; R++) {
-        S.g0[R] = S.g1[R];
-        S.g1[R] = gn[R];
-#pragma unroll
-        for (int c = 0; c < 2; c++) S.r1[R][c] = rn[R][c];
-      }
+      // red r of plane z for the next step (row A red col PH, row B col Q)
+      S.rq[0] = rn[0][PH];
+      S.rq[1] = rn[1][Q];
+      S.g[Q][0] = gn[0];
+      S.g[Q][1] = gn[1];
     }
 #pragma unroll
     for (int R = 0; R < 2; R++) {
-      S.vr0[R] = S.vr1[R];
-      S.vr1[R] = vrn[R];
+      S.vr[PH][R] = vrn[R];
+      if (FINE)
 #pragma unroll
-      for (int c = 0; c < 2; c++) {
-        S.um[R][c] = S.uc[R][c];
-        S.uc[R][c] = un[R][c];
-      }
+        for (int c = 0; c < 2; c++) S.u[PH][R][c] = un[R][c];
     }
   }
   static __device__ void finish(const Params &, State &) {}
@@ -601,6 +708,40 @@ cudaError_t fast3p_asc_fine(const S3<T> &vr, const T *u_old, const T *f, int64_t
   return run_zpipe<Op>(P, M, pz.zlo, pz.zhi < 0 ? M : pz.zhi, st);
 }
 
+template <class T>
+cudaError_t fast3p_rest_gr(const D3<T> &r, const S3<T> &rr, int M, cudaStream_t st) {
+  using Op = OpDesc3P<T, false>;
+  using Gm = Geo<T>;
+  typename Op::Params P{};
+  const int64_t n = M + 1;
+  if (!tmap3<T>(&P.tf, r.p, n, n, n, r.pitch, r.plane, Gm::FW, Gm::FH)) return cudaErrorInvalidValue;
+  P.out = rr;
+  P.M = M;
+  return run_zpipe<Op>(P, M, 0, M, st);
+}
+
+template <class T>
+cudaError_t fast3p_jac_g(const S3<T> &vr, const D3<T> &r, const D3<T> &v, int M, T c, cudaStream_t st) {
+  using Op = OpAsc3P<T, false>;
+  using Gm = Geo<T>;
+  typename Op::Params P{};
+  const int64_t n = M + 1, H = M / 2 + 1;
+  if (!tmap3<T>(&P.tf, r.p, n, n, n, r.pitch, r.plane, Gm::FW, Gm::FH)) return cudaErrorInvalidValue;
+  const int sub[4] = {0, 6, 5, 3};   // C, Fx, Fy, Fz
+  for (int i = 0; i < 4; i++)
+    if (!tmap3<T>(&P.tv[i], vr.s[sub[i]], H, H, H, vr.pitch, vr.plane, Gm::VW, Gm::VH)) return cudaErrorInvalidValue;
+  P.out = v;
+  P.M = M;
+  P.c = c;
+  return run_zpipe<Op>(P, M, 0, M, st);
+}
+
+template cudaError_t fast3p_rest_gr<double>(const D3<double> &, const S3<double> &, int, cudaStream_t);
+template cudaError_t fast3p_rest_gr<float>(const D3<float> &, const S3<float> &, int, cudaStream_t);
+template cudaError_t fast3p_jac_g<double>(const S3<double> &, const D3<double> &, const D3<double> &, int, double,
+                                          cudaStream_t);
+template cudaError_t fast3p_jac_g<float>(const S3<float> &, const D3<float> &, const D3<float> &, int, float,
+                                         cudaStream_t);
 template cudaError_t fast3p_desc_fine<double>(const double *, const double *, int64_t, const S3<double> &, int,
                                               const Coef<double> &, const NormSink &, cudaStream_t, const ZRange3 &);
 template cudaError_t fast3p_desc_fine<float>(const float *, const float *, int64_t, const S3<float> &, int,

@@ -128,6 +128,14 @@ template <class T>
 cudaError_t fast3p_asc_fine(const S3<T> &vr, const T *u_old, const T *f, int64_t pitch, T *u_new, int M, T c,
                             const Coef<T> &k, cudaStream_t st, const ZRange3 &pz);
 
+// The same pipelines one octave down (s > 1, single GPU): G(s) -> R(s)
+// (Erred from the dense r_G(s)) and G(s) from R(s) (Egprolg + Egprolr, both
+// colours in one pass).
+template <class T>
+cudaError_t fast3p_rest_gr(const D3<T> &r, const S3<T> &rr, int M, cudaStream_t st);
+template <class T>
+cudaError_t fast3p_jac_g(const S3<T> &vr, const D3<T> &r, const D3<T> &v, int M, T c, cudaStream_t st);
+
 // Per-octave level descriptors for the 3D single-CTA coarse kernel.
 template <class T>
 struct Lev3 {

@@ -374,6 +374,7 @@ struct Impl3 : ImplBase {
   void enqueue_fast(const void *u_in, void *u_out, const void *f_eff, cudaStream_t st, Prof *prof) {
     const double w = sizeof(T);
     const int L = 3 * k - 2;
+    static const bool gen2 = getenv("MG_K3_GEN1") == nullptr;   // plane pipelines for the G(s) levels
     void *u = const_cast<void *>(u_in);
     STEP("desc_fine", 0, 1, w * (2 * Nl[0] + Nl[1]));
     desc_fine(u, f_eff, st);
@@ -381,7 +382,8 @@ struct Impl3 : ImplBase {
       int g = 3 * o;
       if (o >= 1) {
         STEP("rest_gr", g, 1, w * (Nl[g] + Nl[g + 1]));
-        lv3_rest_gr<T>(rG[o], rR[o], M[o], st);
+        if (gen2) fast3p_rest_gr<T>(rG[o], rR[o], M[o], st);
+        else lv3_rest_gr<T>(rG[o], rR[o], M[o], st);
       }
       STEP("rest_rm", g + 1, 1, w * (Nl[g + 1] + Nl[g + 2]));
       lv3_rest_rm<T>(rR[o], rM[o], M[o], st);
@@ -402,8 +404,13 @@ struct Impl3 : ImplBase {
       STEP("jac_r", g + 1, 2, w * (Nl[g + 2] + 2 * Nl[g + 1]));
       lv3_jac_r<T>(vM[o], rR[o], vR[o], M[o], cR1[o], cR2[o], st);
       if (o >= 1) {
-        STEP("jac_g", g, 2, w * (Nl[g + 1] + 2 * Nl[g]));
-        lv3_jac_g<T>(vR[o], rG[o], vG[o], M[o], cG[o], st);
+        if (gen2) {
+          STEP("jac_g", g, 1, w * (Nl[g + 1] + 2 * Nl[g]));
+          fast3p_jac_g<T>(vR[o], rG[o], vG[o], M[o], cG[o], st);
+        } else {
+          STEP("jac_g", g, 2, w * (Nl[g + 1] + 2 * Nl[g]));
+          lv3_jac_g<T>(vR[o], rG[o], vG[o], M[o], cG[o], st);
+        }
       } else if (!getenv("MG_ASC3_DIRECT") && ((uintptr_t)u & 15) == 0 && ((uintptr_t)f_eff & 15) == 0 &&
                  ((uintptr_t)u_out & 15) == 0) {
         STEP("asc_fine", 0, 1, w * (Nl[1] + 3 * Nl[0]));
@@ -433,7 +440,8 @@ struct Impl3 : ImplBase {
       c = 1;
       for (int o = 0; o < oc; o++) c += (o >= 1) + 2;
       c += 1;
-      for (int o = oc - 1; o >= 0; o--) c += 2 + 2 + 2;
+      const bool gen2 = getenv("MG_K3_GEN1") == nullptr;
+      for (int o = oc - 1; o >= 0; o--) c += 2 + 2 + (o >= 1 ? (gen2 ? 1 : 2) : 1);
       return c;
     }
     for (int o = k - 2; o >= 0; o--) c += 2 + 2 + ((o >= 1) ? 2 : 3);
