@@ -21,191 +21,10 @@
 // ops3.cuh, so the results are bit-identical to the oracle.
 // Order 4 (Efos4) keeps the first-generation kernels of k3f.cu: its face
 // diagonals reach the neighbours of the z +- 1 planes.
-#include <type_traits>
-
-#include "kernels.h"
 #include "ops3.cuh"
-#include "tma.cuh"
+#include "zpipe.cuh"
 
 namespace mg {
-
-namespace zp {
-
-constexpr int TX = 60, TY = 30, NT = 512;
-constexpr int GS = 34;                       // green-plane ring: 34 x 34 (rows/lanes -1 .. 32)
-constexpr int al128(int n) { return (n + 127) / 128 * 128; }
-
-template <class T>
-struct Geo {
-  static constexpr int AL = 16 / (int)sizeof(T);       // TMA x alignment (elements)
-  static constexpr int UXO = (AL == 2) ? 4 : 6;         // u box starts at x0 - UXO (>= 3, aligned)
-  static constexpr int UW = (UXO + 63 + AL - 1) / AL * AL, UH = TY + 4;
-  static constexpr int FW = 64, FH = TY + 2;            // f box: x0-2 .., y0-1 ..
-  static constexpr int VW = (34 + AL - 1 + AL - 1) / AL * AL, VH = TY / 2 + 2;
-  static constexpr int U_BYTES = UW * UH * (int)sizeof(T), F_BYTES = FW * FH * (int)sizeof(T);
-  static constexpr int V_BYTES = VW * VH * (int)sizeof(T);
-  static constexpr int GPL = al128(GS * GS * (int)sizeof(T));
-};
-
-template <class T>
-struct V2t;
-template <>
-struct V2t<double> {
-  using t = double2;
-};
-template <>
-struct V2t<float> {
-  using t = float2;
-};
-template <class T>
-__device__ __forceinline__ void ld2(const T *p, T &a, T &b) {
-  auto v = *reinterpret_cast<const typename V2t<T>::t *>(p);
-  a = v.x;
-  b = v.y;
-}
-template <class T>
-__device__ __forceinline__ void st2(T *p, T a, T b) {   // streaming (evict-first) vector store
-  typename V2t<T>::t v;
-  v.x = a;
-  v.y = b;
-  __stcs(reinterpret_cast<typename V2t<T>::t *>(p), v);
-}
-
-// r = f - (-(6c) + xp + xm + yp + ym + zp + zm) * (n-1)^2   (res3v, order 2)
-template <class T>
-__device__ __forceinline__ T res7(T c, T xp, T xm, T yp, T ym, T zp, T zm, T f, T invh2) {
-  T lap = -((T)6 * c);
-  lap = lap + xp;
-  lap = lap + xm;
-  lap = lap + yp;
-  lap = lap + ym;
-  lap = lap + zp;
-  lap = lap + zm;
-  lap = lap * invh2;
-  return f - lap;
-}
-
-// Balanced work list: items k < W are whole tiles b + k*G over [zlo, zhi);
-// item W (when R = T mod G > 0) is one z segment of tail tile W*G + b mod R.
-struct Item {
-  int x0, y0, zs, ze;
-};
-struct Sched {
-  int T, ntx, zlo, zhi;
-  __device__ __forceinline__ int count(int G) const { return T / G + (T % G ? 1 : 0); }
-  __device__ __forceinline__ Item get(int k, int b, int G) const {
-    const int W = T / G, R = T % G;
-    int t, zs = zlo, ze = zhi;
-    if (k < W) {
-      t = b + k * G;
-    } else {
-      const int r = b % R, nseg = G / R + (r < G % R ? 1 : 0), sg = b / R;
-      const long long Z = zhi - zlo;
-      t = W * G + r;
-      zs = zlo + (int)(Z * sg / nseg);
-      ze = zlo + (int)(Z * (sg + 1) / nseg);
-    }
-    Item it;
-    it.x0 = (t % ntx) * TX - 2;
-    it.y0 = (t / ntx) * TY;
-    it.zs = zs;
-    it.ze = ze;
-    return it;
-  }
-};
-
-}  // namespace zp
-
-using namespace zp;
-
-// ------------------------------------------------------------ pipeline
-// Op: NS (slots), SLOT (bytes), SMEM, Params (with .sc), issue(P, it, j,
-// slot, bar), State, Ctx, begin(P, Ctx&, it), step<PH>(P, State&, Ctx&, it,
-// j, Lc, Lp, gz, gq).  PH = j & 1: every parity the step needs (tile origins
-// y0 and x0 are even) is a compile-time function of PH, and the register
-// state is double-buffered by PH, so no selects or register moves remain.
-// The ring of green planes is addressed by byte offsets gz (plane j-1) and
-// gq (plane j-2).
-template <class Op>
-__global__ void __launch_bounds__(NT, 1) zpipe(const __grid_constant__ typename Op::Params P) {
-  constexpr int NS = Op::NS, D = NS - 2;
-  extern __shared__ __align__(128) unsigned char smem[];
-  __shared__ __align__(8) uint64_t bar[NS];
-  const int G = gridDim.x, b = blockIdx.x;
-  const int nit = P.sc.count(G);
-  if (threadIdx.x == 0) {
-    for (int s = 0; s < NS; s++) mbar_init(&bar[s], 1);
-    fence_mbar_init();
-    Op::prefetch(P);
-  }
-  __syncthreads();
-  unsigned char *gring = smem + NS * Op::SLOT;
-
-  // producer cursor (thread 0): item pk, plane pj, slot ps
-  int pk = 0, pj = 0, ps = 0;
-  Item pit{};
-  bool pmore = false;
-  auto pseek = [&](int k) {   // first non-empty item >= k
-    for (; k < nit; k++) {
-      Item it = P.sc.get(k, b, G);
-      if (it.ze > it.zs) {
-        pk = k;
-        pit = it;
-        pj = it.zs - Op::PRO;
-        pmore = true;
-        return;
-      }
-    }
-    pmore = false;
-  };
-  auto produce = [&]() {
-    if (!pmore) return;
-    Op::issue(P, pit, pj, smem + ps * Op::SLOT, &bar[ps]);
-    ps = (ps + 1 == NS) ? 0 : ps + 1;
-    if (++pj > pit.ze + 1) pseek(pk + 1);
-  };
-  if (threadIdx.x == 0) {
-    pseek(0);
-    for (int d = 0; d < D; d++) produce();
-  }
-
-  typename Op::State S;
-  Op::init(S);
-  int cs = 0, cprev = NS - 1;
-  uint32_t phase = 0;
-  for (int k = 0; k < nit; k++) {
-    const Item it = P.sc.get(k, b, G);
-    if (it.ze <= it.zs) continue;
-    typename Op::Ctx C;
-    Op::begin(P, C, it);
-    // ring planes rotate by one per step; greens are written and read within one item
-    int gz = 0, gq = 0;
-    auto one = [&](auto ph, int j) {
-      constexpr int PH = decltype(ph)::value;
-      gq = gz;
-      gz = (gz == 2 * Op::GPL) ? 0 : gz + Op::GPL;
-      if (threadIdx.x == 0) produce();
-      mbar_wait(&bar[cs], phase);
-      Op::template step<PH>(P, S, C, it, j, smem + cs * Op::SLOT, smem + cprev * Op::SLOT, gring + gz, gring + gq);
-      __syncthreads();
-      cprev = cs;
-      if (++cs == NS) {
-        cs = 0;
-        phase ^= 1;
-      }
-    };
-    // unrolled by two so the PH-indexed register state never moves
-    const int jb = it.zs - Op::PRO, je = it.ze + 1;
-    int j = jb;
-    if (j & 1) one(std::integral_constant<int, 1>(), j++);
-    for (; j + 1 <= je; j += 2) {
-      one(std::integral_constant<int, 0>(), j);
-      one(std::integral_constant<int, 1>(), j + 1);
-    }
-    if (j <= je) one(std::integral_constant<int, 0>(), j);
-  }
-  Op::finish(P, S);
-}
 
 // own-node interior masks of an item (x: columns xl, xl+1; y: rows yA, yA+1)
 struct Masks {
@@ -245,7 +64,7 @@ __device__ __forceinline__ void sel0(T &v, bool keep) {
 template <class T, bool FINE = true>
 struct OpDesc3P {
   using Gm = Geo<T>;
-  static constexpr int NS = FINE ? (sizeof(T) == 8 ? 5 : 8) : 8, GPL = Gm::GPL, PRO = FINE ? 2 : 0;
+  static constexpr int NS = FINE ? (sizeof(T) == 8 ? 5 : 8) : 8, GPL = Gm::GPL, PRO = FINE ? 2 : 0, EPI = 2;
   static constexpr int U_OFF = 0, F_OFF = FINE ? al128(Gm::U_BYTES) : 0, SLOT = al128(F_OFF + Gm::F_BYTES);
   static constexpr int SMEM = NS * SLOT + 3 * Gm::GPL;
   struct Params {
@@ -293,7 +112,7 @@ struct OpDesc3P {
   template <int PH>
   static __device__ __forceinline__ void step(const Params &P, State &S, const Ctx &C, const Item &it, int j,
                                               unsigned char *Lc, unsigned char *Lp, unsigned char *gz,
-                                              unsigned char *gq) {
+                                              unsigned char *gq, unsigned char *) {
     constexpr int Q = PH ^ 1;   // slot of planes j-1, j-3
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, M = P.M;
     const int uo = (2 * w + 1) * Gm::UW + 2 * lane - 2 + Gm::UXO;   // u box offset of (xl, yA)
@@ -431,7 +250,7 @@ struct OpDesc3P {
 template <class T, bool FINE = true>
 struct OpAsc3P {
   using Gm = Geo<T>;
-  static constexpr int NS = FINE ? (sizeof(T) == 8 ? 4 : 7) : (sizeof(T) == 8 ? 7 : 10), GPL = Gm::GPL, PRO = 2;
+  static constexpr int NS = FINE ? (sizeof(T) == 8 ? 4 : 7) : (sizeof(T) == 8 ? 7 : 10), GPL = Gm::GPL, PRO = 2, EPI = 2;
   static constexpr int U_OFF = 0, F_OFF = FINE ? al128(Gm::U_BYTES) : 0, V0_OFF = F_OFF + al128(Gm::F_BYTES),
                        V1_OFF = V0_OFF + al128(Gm::V_BYTES), SLOT = al128(V1_OFF + Gm::V_BYTES);
   static constexpr int SMEM = NS * SLOT + 3 * Gm::GPL;
@@ -494,7 +313,7 @@ struct OpAsc3P {
   template <int PH>
   static __device__ __forceinline__ void step(const Params &P, State &S, const Ctx &C, const Item &it, int j,
                                               unsigned char *Lc, unsigned char *Lp, unsigned char *gz,
-                                              unsigned char *gq) {
+                                              unsigned char *gq, unsigned char *) {
     constexpr int Q = PH ^ 1;
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, M = P.M;
     const int uo = (2 * w + 1) * Gm::UW + 2 * lane - 2 + Gm::UXO;
@@ -640,30 +459,8 @@ struct OpAsc3P {
 // ================================================================= launch
 template <class Op>
 static cudaError_t run_zpipe(typename Op::Params &P, int M, int zlo, int zhi, cudaStream_t st) {
-  if (zhi <= zlo) return cudaSuccess;
-  cudaError_t e = cudaFuncSetAttribute(zpipe<Op>, cudaFuncAttributeMaxDynamicSharedMemorySize, Op::SMEM);
-  if (e != cudaSuccess) return e;
-  int dev = 0, sms = 148;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  P.sc.ntx = (M + 1) / TX + 1;   // tiles start at x0 = 60 t - 2; outputs x = 1 .. M-1
-  const int nty = (M + TY - 1) / TY;
-  P.sc.T = P.sc.ntx * nty;
-  P.sc.zlo = zlo;
-  P.sc.zhi = zhi;
-  const int Z = zhi - zlo;
-  int grid = sms;
-  if ((long long)P.sc.T * Z < grid) grid = (int)((long long)P.sc.T * Z);
-  zpipe<Op><<<grid, NT, Op::SMEM, st>>>(P);
-  return cudaGetLastError();
-}
-
-template <class T>
-static bool tmap3(CUtensorMap *tm, const T *p, int64_t nx, int64_t ny, int64_t nz, int64_t pitch, int64_t plane, int bx,
-                  int by) {
-  uint64_t dims[3] = {(uint64_t)nx, (uint64_t)ny, (uint64_t)nz};
-  uint32_t box[3] = {(uint32_t)bx, (uint32_t)by, 1};
-  return encode_tmap(tm, p, sizeof(T), 3, dims, (uint64_t)pitch, (uint64_t)plane, box);
+  // tiles start at x0 = 60 t - 2 (outputs x = 1 .. M-1), y0 = 30 t
+  return launch_zpipe<Op>(P, TX, TY, -2, 0, (M + 1) / TX + 1, (M + TY - 1) / TY, zlo, zhi, st);
 }
 
 template <class T>

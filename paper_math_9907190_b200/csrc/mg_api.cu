@@ -199,6 +199,27 @@ struct Impl2 : ImplBase {
 };
 
 // ------------------------------------------------------------------ 3D
+// fp64 sublattice pipelines (k3s.cu); the fp32 overloads are never reached
+// (Impl3 keeps the k3l.cu kernels for fp32).
+static void sub3_rest_rm(const S3<double> &rr, const S3<double> &rm, int M, cudaStream_t st) {
+  fast3s_rest_rm(rr, rm, M, st);
+}
+static void sub3_rest_mg(const S3<double> &rm, const D3<double> &g2, int Mc, cudaStream_t st) {
+  fast3s_rest_mg(rm, g2, Mc, st);
+}
+static void sub3_jac_m(const D3<double> &vc, const S3<double> &r, const S3<double> &v, int M, double c,
+                       cudaStream_t st) {
+  fast3s_jac_m(vc, r, v, M, c, st);
+}
+static void sub3_jac_r(const S3<double> &vm, const S3<double> &r, const S3<double> &v, int M, double c1, double c2,
+                       cudaStream_t st) {
+  fast3s_jac_r(vm, r, v, M, c1, c2, st);
+}
+static void sub3_rest_rm(const S3<float> &, const S3<float> &, int, cudaStream_t) {}
+static void sub3_rest_mg(const S3<float> &, const D3<float> &, int, cudaStream_t) {}
+static void sub3_jac_m(const D3<float> &, const S3<float> &, const S3<float> &, int, float, cudaStream_t) {}
+static void sub3_jac_r(const S3<float> &, const S3<float> &, const S3<float> &, int, float, float, cudaStream_t) {}
+
 template <class T>
 struct Impl3 : ImplBase {
   const mg_solver *s;
@@ -375,6 +396,7 @@ struct Impl3 : ImplBase {
     const double w = sizeof(T);
     const int L = 3 * k - 2;
     static const bool gen2 = getenv("MG_K3_GEN1") == nullptr;   // plane pipelines for the G(s) levels
+    const bool gen2s = gen2 && sizeof(T) == 8;                    // and for the sublattice levels (fp64)
     void *u = const_cast<void *>(u_in);
     STEP("desc_fine", 0, 1, w * (2 * Nl[0] + Nl[1]));
     desc_fine(u, f_eff, st);
@@ -386,9 +408,11 @@ struct Impl3 : ImplBase {
         else lv3_rest_gr<T>(rG[o], rR[o], M[o], st);
       }
       STEP("rest_rm", g + 1, 1, w * (Nl[g + 1] + Nl[g + 2]));
-      lv3_rest_rm<T>(rR[o], rM[o], M[o], st);
+      if (gen2s) sub3_rest_rm(rR[o], rM[o], M[o], st);
+      else lv3_rest_rm<T>(rR[o], rM[o], M[o], st);
       STEP("rest_mg", g + 2, 1, w * (Nl[g + 2] + Nl[g + 3]));
-      lv3_rest_mg<T>(rM[o], rG[o + 1], M[o + 1], st);
+      if (gen2s) sub3_rest_mg(rM[o], rG[o + 1], M[o + 1], st);
+      else lv3_rest_mg<T>(rM[o], rG[o + 1], M[o + 1], st);
     }
     {
       double b = 0;
@@ -399,10 +423,12 @@ struct Impl3 : ImplBase {
     lv3_coarse<T>(d_lev, oc, k, s->d_counter, st);
     for (int o = oc - 1; o >= 0; o--) {
       int g = 3 * o;
-      STEP("jac_m", g + 2, 2, w * (Nl[g + 3] + 2 * Nl[g + 2]));
-      lv3_jac_m<T>(vG[o + 1], rM[o], vM[o], M[o], cMg[o], st);
-      STEP("jac_r", g + 1, 2, w * (Nl[g + 2] + 2 * Nl[g + 1]));
-      lv3_jac_r<T>(vM[o], rR[o], vR[o], M[o], cR1[o], cR2[o], st);
+      STEP("jac_m", g + 2, gen2s ? 1 : 2, w * (Nl[g + 3] + 2 * Nl[g + 2]));
+      if (gen2s) sub3_jac_m(vG[o + 1], rM[o], vM[o], M[o], cMg[o], st);
+      else lv3_jac_m<T>(vG[o + 1], rM[o], vM[o], M[o], cMg[o], st);
+      STEP("jac_r", g + 1, gen2s ? 1 : 2, w * (Nl[g + 2] + 2 * Nl[g + 1]));
+      if (gen2s) sub3_jac_r(vM[o], rR[o], vR[o], M[o], cR1[o], cR2[o], st);
+      else lv3_jac_r<T>(vM[o], rR[o], vR[o], M[o], cR1[o], cR2[o], st);
       if (o >= 1) {
         if (gen2) {
           STEP("jac_g", g, 1, w * (Nl[g + 1] + 2 * Nl[g]));
@@ -440,8 +466,8 @@ struct Impl3 : ImplBase {
       c = 1;
       for (int o = 0; o < oc; o++) c += (o >= 1) + 2;
       c += 1;
-      const bool gen2 = getenv("MG_K3_GEN1") == nullptr;
-      for (int o = oc - 1; o >= 0; o--) c += 2 + 2 + (o >= 1 ? (gen2 ? 1 : 2) : 1);
+      const bool gen2 = getenv("MG_K3_GEN1") == nullptr, gen2s = gen2 && sizeof(T) == 8;
+      for (int o = oc - 1; o >= 0; o--) c += (gen2s ? 2 : 4) + (o >= 1 ? (gen2 ? 1 : 2) : 1);
       return c;
     }
     for (int o = k - 2; o >= 0; o--) c += 2 + 2 + ((o >= 1) ? 2 : 3);

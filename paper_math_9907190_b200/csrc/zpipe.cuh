@@ -1,0 +1,234 @@
+// zpipe.cuh -- the persistent TMA plane pipeline shared by the 3D stencil
+// passes (k3p.cu: fine-resolution passes; k3s.cu: sublattice level passes).
+//
+// One CTA per SM walks a balanced list of work items (an xy tile times a z
+// range); one thread keeps NS-2 planes of TMA loads in flight in a ring of NS
+// shared-memory slots (one mbarrier each); step j of an item consumes load
+// L_j (and the older slots the Op declares), then one __syncthreads.
+#pragma once
+#include <type_traits>
+
+#include "kernels.h"
+#include "tma.cuh"
+
+namespace mg {
+
+namespace zp {
+
+constexpr int TX = 60, TY = 30, NT = 512;
+constexpr int GS = 34;                       // green-plane ring: 34 x 34 (rows/lanes -1 .. 32)
+constexpr int al128(int n) { return (n + 127) / 128 * 128; }
+
+template <class T>
+struct Geo {
+  static constexpr int AL = 16 / (int)sizeof(T);       // TMA x alignment (elements)
+  static constexpr int UXO = (AL == 2) ? 4 : 6;         // u box starts at x0 - UXO (>= 3, aligned)
+  static constexpr int UW = (UXO + 63 + AL - 1) / AL * AL, UH = TY + 4;
+  static constexpr int FW = 64, FH = TY + 2;            // f box: x0-2 .., y0-1 ..
+  static constexpr int VW = (34 + AL - 1 + AL - 1) / AL * AL, VH = TY / 2 + 2;
+  static constexpr int U_BYTES = UW * UH * (int)sizeof(T), F_BYTES = FW * FH * (int)sizeof(T);
+  static constexpr int V_BYTES = VW * VH * (int)sizeof(T);
+  static constexpr int GPL = al128(GS * GS * (int)sizeof(T));
+};
+
+template <class T>
+struct V2t;
+template <>
+struct V2t<double> {
+  using t = double2;
+};
+template <>
+struct V2t<float> {
+  using t = float2;
+};
+template <class T>
+__device__ __forceinline__ void ld2(const T *p, T &a, T &b) {
+  auto v = *reinterpret_cast<const typename V2t<T>::t *>(p);
+  a = v.x;
+  b = v.y;
+}
+template <class T>
+__device__ __forceinline__ void st2(T *p, T a, T b) {   // streaming (evict-first) vector store
+  typename V2t<T>::t v;
+  v.x = a;
+  v.y = b;
+  __stcs(reinterpret_cast<typename V2t<T>::t *>(p), v);
+}
+
+// r = f - (-(6c) + xp + xm + yp + ym + zp + zm) * (n-1)^2   (res3v, order 2)
+template <class T>
+__device__ __forceinline__ T res7(T c, T xp, T xm, T yp, T ym, T zp, T zm, T f, T invh2) {
+  T lap = -((T)6 * c);
+  lap = lap + xp;
+  lap = lap + xm;
+  lap = lap + yp;
+  lap = lap + ym;
+  lap = lap + zp;
+  lap = lap + zm;
+  lap = lap * invh2;
+  return f - lap;
+}
+
+// Balanced work list: items k < W are whole tiles b + k*G over [zlo, zhi);
+// item W (when R = T mod G > 0) is one z segment of tail tile W*G + b mod R.
+struct Item {
+  int x0, y0, zs, ze;
+};
+struct Sched {
+  int T, ntx, zlo, zhi;
+  int tx, ty, xoff, yoff;   // tile extents and origin offsets: x0 = tx * (t % ntx) + xoff
+  __device__ __forceinline__ int count(int G) const { return T / G + (T % G ? 1 : 0); }
+  __device__ __forceinline__ Item get(int k, int b, int G) const {
+    const int W = T / G, R = T % G;
+    int t, zs = zlo, ze = zhi;
+    if (k < W) {
+      t = b + k * G;
+    } else {
+      const int r = b % R, nseg = G / R + (r < G % R ? 1 : 0), sg = b / R;
+      const long long Z = zhi - zlo;
+      t = W * G + r;
+      zs = zlo + (int)(Z * sg / nseg);
+      ze = zlo + (int)(Z * (sg + 1) / nseg);
+    }
+    Item it;
+    it.x0 = (t % ntx) * tx + xoff;
+    it.y0 = (t / ntx) * ty + yoff;
+    it.zs = zs;
+    it.ze = ze;
+    return it;
+  }
+};
+
+}  // namespace zp
+
+using namespace zp;
+
+// ------------------------------------------------------------ pipeline
+// Op: NS (slots), SLOT (bytes), SMEM, GPL (bytes of one ring plane), PRO /
+// EPI (steps before zs / after ze-1), Params (with .sc), issue(P, it, j,
+// slot, bar), State, Ctx, begin(P, Ctx&, it), step<PH>(P, State&, Ctx&, it,
+// j, Lc, Lp, gz, gq, gr): item steps run j = zs-PRO .. ze-1+EPI.  PH = j & 1: every parity the step needs (tile origins
+// y0 and x0 are even) is a compile-time function of PH, and the register
+// state is double-buffered by PH, so no selects or register moves remain.
+// A 3-plane ring after the slots is addressed by gz (plane j-1), gq (plane
+// j-2) and gr (plane j-3).
+template <class Op>
+__global__ void __launch_bounds__(NT, 1) zpipe(const __grid_constant__ typename Op::Params P) {
+  constexpr int NS = Op::NS, D = NS - 2;
+  extern __shared__ __align__(128) unsigned char smem[];
+  __shared__ __align__(8) uint64_t bar[NS];
+  const int G = gridDim.x, b = blockIdx.x;
+  const int nit = P.sc.count(G);
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < NS; s++) mbar_init(&bar[s], 1);
+    fence_mbar_init();
+    Op::prefetch(P);
+  }
+  __syncthreads();
+  unsigned char *gring = smem + NS * Op::SLOT;
+
+  // producer cursor (thread 0): item pk, plane pj, slot ps
+  int pk = 0, pj = 0, ps = 0;
+  Item pit{};
+  bool pmore = false;
+  auto pseek = [&](int k) {   // first non-empty item >= k
+    for (; k < nit; k++) {
+      Item it = P.sc.get(k, b, G);
+      if (it.ze > it.zs) {
+        pk = k;
+        pit = it;
+        pj = it.zs - Op::PRO;
+        pmore = true;
+        return;
+      }
+    }
+    pmore = false;
+  };
+  auto produce = [&]() {
+    if (!pmore) return;
+    Op::issue(P, pit, pj, smem + ps * Op::SLOT, &bar[ps]);
+    ps = (ps + 1 == NS) ? 0 : ps + 1;
+    if (++pj > pit.ze - 1 + Op::EPI) pseek(pk + 1);
+  };
+  if (threadIdx.x == 0) {
+    pseek(0);
+    for (int d = 0; d < D; d++) produce();
+  }
+
+  typename Op::State S;
+  Op::init(S);
+  int cs = 0, cprev = NS - 1;
+  uint32_t phase = 0;
+  for (int k = 0; k < nit; k++) {
+    const Item it = P.sc.get(k, b, G);
+    if (it.ze <= it.zs) continue;
+    typename Op::Ctx C;
+    Op::begin(P, C, it);
+    // ring planes rotate by one per step; greens are written and read within one item
+    int gz = 0, gq = 0;
+    auto one = [&](auto ph, int j) {
+      constexpr int PH = decltype(ph)::value;
+      gq = gz;
+      gz = (gz == 2 * Op::GPL) ? 0 : gz + Op::GPL;
+      if (threadIdx.x == 0) produce();
+      mbar_wait(&bar[cs], phase);
+      const int gr = (gz == 2 * Op::GPL) ? 0 : gz + Op::GPL;   // plane j-3
+      Op::template step<PH>(P, S, C, it, j, smem + cs * Op::SLOT, smem + cprev * Op::SLOT, gring + gz, gring + gq,
+                            gring + gr);
+      __syncthreads();
+      cprev = cs;
+      if (++cs == NS) {
+        cs = 0;
+        phase ^= 1;
+      }
+    };
+    // unrolled by two so the PH-indexed register state never moves
+    const int jb = it.zs - Op::PRO, je = it.ze - 1 + Op::EPI;
+    int j = jb;
+    if (j & 1) one(std::integral_constant<int, 1>(), j++);
+    for (; j + 1 <= je; j += 2) {
+      one(std::integral_constant<int, 0>(), j);
+      one(std::integral_constant<int, 1>(), j + 1);
+    }
+    if (j <= je) one(std::integral_constant<int, 0>(), j);
+  }
+  Op::finish(P, S);
+}
+
+// Launch one persistent CTA per SM (fewer for tiny problems) over ntx x nty
+// tiles of tx x ty nodes (x0 = tx * i + xoff, y0 = ty * j + yoff) and the
+// z range [zlo, zhi).
+template <class Op>
+static cudaError_t launch_zpipe(typename Op::Params &P, int tx, int ty, int xoff, int yoff, int ntx, int nty, int zlo,
+                                int zhi, cudaStream_t st) {
+  if (zhi <= zlo) return cudaSuccess;
+  cudaError_t e = cudaFuncSetAttribute(zpipe<Op>, cudaFuncAttributeMaxDynamicSharedMemorySize, Op::SMEM);
+  if (e != cudaSuccess) return e;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  P.sc.tx = tx;
+  P.sc.ty = ty;
+  P.sc.xoff = xoff;
+  P.sc.yoff = yoff;
+  P.sc.ntx = ntx;
+  P.sc.T = ntx * nty;
+  P.sc.zlo = zlo;
+  P.sc.zhi = zhi;
+  const long long work = (long long)P.sc.T * (zhi - zlo);
+  const int grid = work < sms ? (int)work : sms;
+  zpipe<Op><<<grid, NT, Op::SMEM, st>>>(P);
+  return cudaGetLastError();
+}
+
+// 3D tensor map over nx x ny x nz elements (row pitch, plane stride in
+// elements), box bx x by x 1; out-of-bounds reads return zeros.
+template <class T>
+static bool tmap3(CUtensorMap *tm, const T *p, int64_t nx, int64_t ny, int64_t nz, int64_t pitch, int64_t plane, int bx,
+                  int by) {
+  uint64_t dims[3] = {(uint64_t)nx, (uint64_t)ny, (uint64_t)nz};
+  uint32_t box[3] = {(uint32_t)bx, (uint32_t)by, 1};
+  return encode_tmap(tm, p, sizeof(T), 3, dims, (uint64_t)pitch, (uint64_t)plane, box);
+}
+
+}  // namespace mg
