@@ -7,7 +7,10 @@
 //
 // Level kernels in this file work on lattice coordinates of one octave
 // s = 2^o (x = i/s, y = j/s), M = (n-1)/s.
+#include <cstdlib>
+
 #include "kernels.h"
+#include "tma.cuh"
 #include "ops2.cuh"
 
 namespace mg {
@@ -103,7 +106,73 @@ __global__ void __launch_bounds__(NT) k2_jac_a2_ref(D2<const T> r, D2<T> v, int 
 // resident), so the cost is latency; __syncthreads orders the steps.
 template <class T>
 __global__ void __launch_bounds__(1024) k2_coarse(const Lev2<T> *lv, int oc, int k, int *counter) {
+  pdl_trigger();
+  pdl_wait();
   const int tid = threadIdx.x, bs = blockDim.x;
+  for (int o = oc; o + 1 < k; o++) {
+    const Lev2<T> L = lv[o];
+    const Lev2<T> Lc = lv[o + 1];
+    int64_t n = (int64_t)(L.M / 2 + 1) * (L.M / 2 + 1);
+    for (int64_t t = tid; t < n; t += bs) node_rest_ad(D2<const T>{L.rA.p, L.rA.pitch}, L.rD, L.M, t);
+    __syncthreads();
+    n = (int64_t)(Lc.M - 1) * (Lc.M - 1);
+    for (int64_t t = tid; t < n; t += bs) node_rest_da(S2<const T>{L.rD.e, L.rD.o, L.rD.pitch}, Lc.rA, Lc.M, t);
+    __syncthreads();
+  }
+  if (tid == 0) {
+    const Lev2<T> L = lv[k - 1];
+    node_coarsest(D2<const T>{L.rA.p, L.rA.pitch}, L.vA, L.cA, counter);
+  }
+  __syncthreads();
+  for (int o = k - 2; o >= oc; o--) {
+    const Lev2<T> L = lv[o];
+    const Lev2<T> Lc = lv[o + 1];
+    const int M = L.M;
+    S2<const T> rD{L.rD.e, L.rD.o, L.rD.pitch};
+    int64_t n = (int64_t)(M / 2) * (M / 2);
+    for (int64_t t = tid; t < n; t += bs) node_jac_d1(D2<const T>{Lc.vA.p, Lc.vA.pitch}, rD, L.vD, M, L.cD, t);
+    __syncthreads();
+    n = (int64_t)(M / 2 - 1) * (M / 2 - 1);
+    for (int64_t t = tid; t < n; t += bs) node_jac_d2(rD, L.vD, M, L.cD, t);
+    __syncthreads();
+    n = (int64_t)(M - 1) * (M - 1);
+    S2<const T> vD{L.vD.e, L.vD.o, L.vD.pitch};
+    D2<const T> rA{L.rA.p, L.rA.pitch};
+    for (int64_t t = tid; t < n; t += bs) node_jac_a1(vD, rA, L.vA, M, L.cA, t);
+    __syncthreads();
+    for (int64_t t = tid; t < n; t += bs) node_jac_a2(rA, L.vA, M, L.cA, t);
+    __syncthreads();
+  }
+}
+
+// Shared-memory variant of k2_coarse: the levels below octave oc live in
+// shared memory (zero-filled per launch), only r_A(oc) is read from and
+// v_A(oc) written to global memory; same node bodies and order.
+template <class T>
+__global__ void __launch_bounds__(1024) k2_coarse_smem(const Lev2<T> *lvg, int oc, int k, int *counter, int elems) {
+  pdl_trigger();
+  extern __shared__ __align__(16) unsigned char dsm[];
+  T *arena = (T *)dsm;
+  __shared__ Lev2<T> lv[32];
+  const int tid = threadIdx.x, bs = blockDim.x;
+  for (int t = tid; t < elems; t += bs) arena[t] = (T)0;
+  if (tid == 0) {
+    T *p = arena;
+    for (int o = oc; o < k; o++) lv[o] = lvg[o];
+    for (int o = oc; o + 1 < k; o++) {
+      const int W = lv[o].M / 2 + 1, n2 = W * W;
+      lv[o].rD = S2<T>{p, p + n2, W};
+      p += 2 * n2;
+      lv[o].vD = S2<T>{p, p + n2, W};
+      p += 2 * n2;
+      lv[o + 1].rA = D2<T>{p, W};
+      p += n2;
+      lv[o + 1].vA = D2<T>{p, W};
+      p += n2;
+    }
+  }
+  __syncthreads();
+  pdl_wait();
   for (int o = oc; o + 1 < k; o++) {
     const Lev2<T> L = lv[o];
     const Lev2<T> Lc = lv[o + 1];
@@ -384,7 +453,21 @@ void launch2_asc_fine(const S2<T> &vd, const D2<T> &u, const D2<const T> &f, con
 
 template <class T>
 void launch2_coarse(const Lev2<T> *d_lev, int oc, int k, int *counter, cudaStream_t st) {
-  k2_coarse<T><<<1, 1024, 0, st>>>(d_lev, oc, k, counter);
+  static const bool global = getenv("MG_COARSE_GLOBAL") != nullptr;
+  if (!global && oc >= 1 && k <= 32) {
+    size_t elems = 0;
+    for (int o = oc; o + 1 < k; o++) {
+      const size_t W = (size_t(1) << (k - o - 1)) + 1;   // M_o / 2 + 1 for n = 2^k + 1
+      elems += 6 * W * W;
+    }
+    const size_t bytes = elems * sizeof(T);
+    if (bytes <= 200 * 1024) {
+      cudaFuncSetAttribute(k2_coarse_smem<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+      launch_pdl(k2_coarse_smem<T>, dim3(1), dim3(1024), bytes, st, d_lev, oc, k, counter, (int)elems);
+      return;
+    }
+  }
+  launch_pdl(k2_coarse<T>, dim3(1), dim3(1024), 0, st, d_lev, oc, k, counter);
 }
 
 template <class T>

@@ -81,12 +81,14 @@ __global__ void __launch_bounds__(Op::NT) tile_pipeline(const __grid_constant__ 
   constexpr int S = Op::STAGES;
   extern __shared__ __align__(128) unsigned char smem[];
   __shared__ __align__(8) uint64_t bar[S];
+  pdl_trigger();
   if (threadIdx.x == 0) {
     for (int s = 0; s < S; s++) mbar_init(&bar[s], 1);
     fence_mbar_init();
     Op::prefetch(P);
   }
   __syncthreads();
+  pdl_wait();
   typename Op::Acc acc;
   Op::init(acc);
   const int ntiles = P.ntiles;
@@ -574,8 +576,7 @@ static cudaError_t run_op(const typename Op::Params &P, cudaStream_t st) {
   int grid = num_sms() * per_sm;
   if (grid > P.ntiles) grid = P.ntiles;
   if (grid < 1) return cudaSuccess;
-  tile_pipeline<Op><<<grid, Op::NT, Op::SMEM, st>>>(P);
-  return cudaGetLastError();
+  return launch_pdl(tile_pipeline<Op>, dim3(grid), dim3(Op::NT), Op::SMEM, st, P);
 }
 
 // run the op with the configured number of stages

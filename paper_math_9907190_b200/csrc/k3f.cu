@@ -89,12 +89,14 @@ __global__ void __launch_bounds__(Op::NT, 1) plane_pipeline(const __grid_constan
   static_assert(NS >= D + 2 + Op::LAFTER, "ring too small for the prefetch distance");
   extern __shared__ __align__(128) unsigned char smem[];
   __shared__ __align__(8) uint64_t bar[NS];
+  pdl_trigger();
   if (threadIdx.x == 0) {
     for (int s = 0; s < NS; s++) mbar_init(&bar[s], 1);
     fence_mbar_init();
     Op::prefetch(P);
   }
   __syncthreads();
+  pdl_wait();
   typename Op::Acc acc;
   Op::init(acc);
   const int nunits = P.nunits;
@@ -460,8 +462,7 @@ static cudaError_t run_plane(const typename Op::Params &P, cudaStream_t st) {
   int grid = sms * per_sm;
   if (grid > P.nunits) grid = P.nunits;
   if (grid < 1) return cudaSuccess;
-  plane_pipeline<Op><<<grid, Op::NT, Op::SMEM, st>>>(P);
-  return cudaGetLastError();
+  return launch_pdl(plane_pipeline<Op>, dim3(grid), dim3(Op::NT), Op::SMEM, st, P);
 }
 
 // map of planes [z0, z0 + nz) of an n x n x (any) field given by its

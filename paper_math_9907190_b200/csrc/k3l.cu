@@ -9,7 +9,11 @@
 // The neighbour order of every sum is the paper's printed order (DESIGN.md
 // canonical arithmetic), so the results are bit-identical to the reference
 // kernels.
+#include <cstdlib>
+#include <initializer_list>
+
 #include "kernels.h"
+#include "tma.cuh"
 #include "ops3.cuh"
 
 namespace mg {
@@ -368,7 +372,105 @@ __global__ void __launch_bounds__(256) k3l_jac_g2(D3<const T> rin, D3<const T> u
 // block-stride loop, __syncthreads between steps (arrays are L1/L2 resident).
 template <class T>
 __global__ void __launch_bounds__(1024) k3l_coarse(const Lev3<T> *lv, int oc, int k, int *counter) {
+  pdl_trigger();
+  pdl_wait();
   const int tid = threadIdx.x, bs = blockDim.x;
+  D3<const T> none{nullptr, 0, 0};
+  Coef<T> k0{};
+  auto cd = [](const D3<T> &a) { return D3<const T>{a.p, a.pitch, a.plane}; };
+  auto cs = [](const S3<T> &a) {
+    S3<const T> o;
+    for (int i = 0; i < 8; i++) o.s[i] = a.s[i];
+    o.pitch = a.pitch;
+    o.plane = a.plane;
+    return o;
+  };
+#define LOOP3(HH, BODY)                                            \
+  {                                                                \
+    const int H_ = (HH);                                           \
+    const int n_ = H_ * H_ * H_;                                   \
+    for (int t = tid; t < n_; t += bs) {                           \
+      const int a = t % H_, b = (t / H_) % H_, c = t / (H_ * H_); \
+      BODY;                                                        \
+    }                                                              \
+    __syncthreads();                                               \
+  }
+  for (int o = oc; o + 1 < k; o++) {
+    const Lev3<T> L = lv[o], Lc = lv[o + 1];
+    const int H = L.M / 2 + 1;
+    LOOP3(H, b3_rest_gr(cd(L.rG), L.rR, L.M, H, a, b, c));
+    LOOP3(H, b3_rest_rm(cs(L.rR), L.rM, H, a, b, c));
+    LOOP3(Lc.M + 1, b3_rest_mg(cs(L.rM), Lc.rG, Lc.M, a, b, c));
+  }
+  if (tid == 0) {
+    const Lev3<T> L = lv[k - 1];
+    L.vG(1, 1, 1) = (-(L.cG * L.rG(1, 1, 1))) * (T)(1.0 / 6.0);   // reading A4
+    if (counter) *counter += 1;
+  }
+  __syncthreads();
+  for (int o = k - 2; o >= oc; o--) {
+    const Lev3<T> L = lv[o], Lc = lv[o + 1];
+    const int H = L.M / 2 + 1;
+    LOOP3(H, b3_jac_m1(cd(Lc.vG), cs(L.rM), L.vM, H, L.cMg, a, b, c));
+    LOOP3(H, b3_jac_m2(cs(L.rM), L.vM, H, L.cMg, a, b, c));
+    LOOP3(H, b3_jac_r1(cs(L.vM), cs(L.rR), L.vR, H, L.cR1, a, b, c));
+    LOOP3(H, b3_jac_r2(cs(L.rR), L.vR, H, L.cR2, a, b, c));
+    LOOP3(H, (b3_jac_g1<T, 2, false>(cs(L.vR), cd(L.rG), none, none, L.vG, L.M, H, L.cG, k0, a, b, c)));
+    LOOP3(H, (b3_jac_g2<T, 2, false>(cd(L.rG), none, none, cd(L.vG), L.vG, L.M, H, L.cG, k0, a, b, c)));
+  }
+#undef LOOP3
+}
+
+// Shared-memory variant: every level below octave oc lives in shared memory
+// (zero-filled per launch; boundary entries stay zero), only r_G(oc) is read
+// from and v_G(oc) written to global memory.  Same node bodies and order as
+// k3l_coarse, so the results are identical; the steps cost shared-memory
+// instead of L2 latency.
+template <class T>
+static __host__ __device__ size_t coarse3_smem_elems(const int *Ms, int oc, int k) {
+  size_t e = 0;
+  for (int o = oc; o + 1 < k; o++) {
+    const size_t H = Ms[o] / 2 + 1;
+    e += 14 * H * H * H;   // r_R, v_R (4), r_M, v_M (2), r_G(2s), v_G(2s) (1 each)
+  }
+  return e;
+}
+
+template <class T>
+__global__ void __launch_bounds__(1024) k3l_coarse_smem(const Lev3<T> *lvg, int oc, int k, int *counter, size_t elems) {
+  pdl_trigger();
+  extern __shared__ __align__(16) unsigned char dsm[];
+  T *arena = (T *)dsm;
+  __shared__ Lev3<T> lv[32];
+  const int tid = threadIdx.x, bs = blockDim.x;
+  for (size_t t = tid; t < elems; t += bs) arena[t] = (T)0;
+  if (tid == 0) {
+    T *p = arena;
+    for (int o = oc; o < k; o++) lv[o] = lvg[o];
+    for (int o = oc; o + 1 < k; o++) {
+      const int H = lv[o].M / 2 + 1;
+      const int64_t n3 = (int64_t)H * H * H;
+      auto split = [&](S3<T> &a, std::initializer_list<int> subs) {
+        for (int q = 0; q < 8; q++) a.s[q] = nullptr;
+        for (int q : subs) {
+          a.s[q] = p;
+          p += n3;
+        }
+        a.pitch = H;
+        a.plane = (int64_t)H * H;
+      };
+      split(lv[o].rR, {0, 3, 5, 6});
+      split(lv[o].vR, {0, 3, 5, 6});
+      split(lv[o].rM, {0, 7});
+      split(lv[o].vM, {0, 7});
+      lv[o + 1].rG = D3<T>{p, H, (int64_t)H * H};
+      p += n3;
+      lv[o + 1].vG = D3<T>{p, H, (int64_t)H * H};
+      p += n3;
+    }
+  }
+  __syncthreads();
+  pdl_wait();
   D3<const T> none{nullptr, 0, 0};
   Coef<T> k0{};
   auto cd = [](const D3<T> &a) { return D3<const T>{a.p, a.pitch, a.plane}; };
@@ -496,7 +598,18 @@ void lv3_asc_fine(const S3<T> &vr, const D3<T> &u_old, const D3<const T> &f, con
 
 template <class T>
 void lv3_coarse(const Lev3<T> *d_lev, int oc, int k, int *counter, cudaStream_t st) {
-  k3l_coarse<T><<<1, 1024, 0, st>>>(d_lev, oc, k, counter);
+  static const bool global = getenv("MG_COARSE_GLOBAL") != nullptr;
+  if (!global && oc >= 1 && k <= 32) {
+    int Ms[32];
+    for (int o = 0; o < k; o++) Ms[o] = 1 << (k - o);   // M of octave o for n = 2^k + 1
+    const size_t elems = coarse3_smem_elems<T>(Ms, oc, k), bytes = elems * sizeof(T);
+    if (bytes <= 200 * 1024) {
+      cudaFuncSetAttribute(k3l_coarse_smem<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+      launch_pdl(k3l_coarse_smem<T>, dim3(1), dim3(1024), bytes, st, d_lev, oc, k, counter, elems);
+      return;
+    }
+  }
+  launch_pdl(k3l_coarse<T>, dim3(1), dim3(1024), 0, st, d_lev, oc, k, counter);
 }
 
 #define INSTL(T)                                                                                                   \

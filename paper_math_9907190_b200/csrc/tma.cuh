@@ -6,6 +6,8 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
+#include <utility>
 
 namespace mg {
 
@@ -61,6 +63,15 @@ __device__ __forceinline__ void tma_prefetch_desc(const CUtensorMap *tm) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(tm)) : "memory");
 }
 
+// Programmatic dependent launch (sm_90+): a kernel launched with the
+// programmatic-serialization attribute may start while its predecessor in the
+// stream drains; pdl_wait() blocks until the predecessor grid has completed
+// and its memory is visible, so it must precede every global access that
+// depends on (or is read by) earlier kernels.  pdl_trigger() lets the next
+// kernel launch as soon as every CTA of this grid has started.
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 // ------------------------------------------------------------- host side
 // Encode a 2D (rank 2) or 3D (rank 3) tiled tensor map over a pitched array
 // of T: dims {nx, ny[, nz]} elements, row pitch `pitch` elements, plane
@@ -68,5 +79,24 @@ __device__ __forceinline__ void tma_prefetch_desc(const CUtensorMap *tm) {
 // (negative coordinates included) are filled with zeros.
 bool encode_tmap(CUtensorMap *tm, const void *base, int esz, int rank, const uint64_t *dims, uint64_t pitch,
                  uint64_t plane, const uint32_t *box);
+
+// Launch a kernel that calls pdl_wait() before its first dependent global
+// access with the programmatic-stream-serialization attribute (captured into
+// CUDA graphs as a programmatic edge) when MG_PDL=1; plainly otherwise.
+bool pdl_enabled();
+template <class... KArgs, class... Args>
+cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args &&...args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
 
 }  // namespace mg

@@ -32,4 +32,14 @@ bool encode_tmap(CUtensorMap *tm, const void *base, int esz, int rank, const uin
   return r == CUDA_SUCCESS;
 }
 
+// Off by default: measured on B200 it gained nothing (the next pass's CTAs
+// cannot become resident before the previous pass's 200 KB-smem CTAs exit).
+bool pdl_enabled() {
+  static const bool on = [] {
+    const char *e = getenv("MG_PDL");
+    return e && *e && *e != '0';
+  }();
+  return on;
+}
+
 }  // namespace mg

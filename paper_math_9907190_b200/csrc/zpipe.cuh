@@ -119,12 +119,14 @@ __global__ void __launch_bounds__(NT, 1) zpipe(const __grid_constant__ typename 
   __shared__ __align__(8) uint64_t bar[NS];
   const int G = gridDim.x, b = blockIdx.x;
   const int nit = P.sc.count(G);
+  pdl_trigger();
   if (threadIdx.x == 0) {
     for (int s = 0; s < NS; s++) mbar_init(&bar[s], 1);
     fence_mbar_init();
     Op::prefetch(P);
   }
   __syncthreads();
+  pdl_wait();   // the predecessor's outputs (and its reads of what this pass writes) are done
   unsigned char *gring = smem + NS * Op::SLOT;
 
   // producer cursor (thread 0): item pk, plane pj, slot ps
@@ -217,8 +219,7 @@ static cudaError_t launch_zpipe(typename Op::Params &P, int tx, int ty, int xoff
   P.sc.zhi = zhi;
   const long long work = (long long)P.sc.T * (zhi - zlo);
   const int grid = work < sms ? (int)work : sms;
-  zpipe<Op><<<grid, NT, Op::SMEM, st>>>(P);
-  return cudaGetLastError();
+  return launch_pdl(zpipe<Op>, dim3(grid), dim3(NT), Op::SMEM, st, P);
 }
 
 // 3D tensor map over nx x ny x nz elements (row pitch, plane stride in
