@@ -176,16 +176,16 @@ def main():
     tdt = torch.float64 if args.dtype == "f64" else torch.float32
     npdt = np.float64 if args.dtype == "f64" else np.float32
 
-    # Multi-GPU: 2D workloads run the y-slab solver over NCCL (strong scaling:
-    # the one global grid is split over the ranks); 3D workloads run one
-    # replica per GPU (3D slabs are not in this build; weak scaling).
-    dist_2d = ws > 1 and w.dim == 2
-    if dist_2d:
+    # Multi-GPU: the slab solver over NCCL -- 2D y-slabs, 3D z-slabs, per-level
+    # halo exchange, all-gather agglomeration of the coarse octaves (strong
+    # scaling: the one global grid is split over the ranks).
+    slabs = ws > 1
+    if slabs:
         s = Solver(w.dim, w.n, order=w.order, p=w.p, dtype=tdt, group=dist.group.WORLD)
     else:
         s = Solver(w.dim, w.n, order=w.order, p=w.p, dtype=tdt)
     f_full = W.workload_rhs(w.name, npdt)
-    if dist_2d:
+    if slabs:
         from paper_math_9907190_b200.mg import split_rows
         f_host = split_rows(f_full, s.lo, s.hi, s.ghost)
     else:
@@ -236,7 +236,7 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
     ms_per_step = ms / args.steps
-    units = N if dist_2d else ws * N   # strong scaling: one grid; replicas: ws grids
+    units = N if slabs else ws * N   # strong scaling: one grid; replicas: ws grids
     value = units * args.steps / (ms / 1e3) / 1e9
     clocks = sampler.summary(t0, t1)
 
@@ -301,10 +301,10 @@ def main():
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
-        "scaling": "strong" if dist_2d else "weak", "vs_baseline": None, "dtype": args.dtype, "data": "synthetic",
+        "scaling": "strong" if slabs else "weak", "vs_baseline": None, "dtype": args.dtype, "data": "synthetic",
         "config": {"workload": w.name, "dim": w.dim, "n": w.n, "order": w.order, "p": list(w.p),
                    "unknowns": N, "rhs": w.note,
-                   "parallelism": (f"y-slabs x{ws} (NCCL halo exchange, all-gather agglomeration)" if dist_2d
+                   "parallelism": (f"{'y' if w.dim == 2 else 'z'}-slabs x{ws} (NCCL halo exchange, all-gather agglomeration)" if slabs
                                    else ("replicas" if ws > 1 else "single")),
                    "l2": "inputs larger than L2 (u and f are %.0f MB each vs 126 MB L2)" %
                          (s.view(u).numel() * u.element_size() / 1e6),

@@ -38,15 +38,16 @@
  *    the ABI.  mg_last_error() describes the last failure of a handle.
  *  - A handle is not thread-safe; distinct handles are independent.
  *
- * Multi-GPU (cfg.nranks > 1, dim 2, nranks a power of two, (n-1)/nranks >= 4,
+ * Multi-GPU (cfg.nranks > 1, nranks a power of two, (n-1)/nranks >= 4,
  * 16-byte row pitch): one process per GPU over NCCL (cfg.nccl_id from
  * mg_nccl_unique_id on rank 0, broadcast by the caller); the grid is cut into
- * y-slabs.  Each rank passes only its slab: rows [lo, hi) of
- * the global grid (lo = rank (n-1)/nranks, hi = lo + (n-1)/nranks) stored
- * with `ghost` = 2 extra rows below and above, i.e. a (hi - lo + 4) x pitch
- * array whose row 2 is global row lo (see mg_local_extent); the global
- * boundary rows 0 and n-1 lie in rank 0's own rows / the last rank's ghost
- * rows and must be 0.  The library fills the ghost rows itself (halo
+ * y-slabs (dim 2) or z-slabs (dim 3).  Each rank passes only
+ * its slab: rows (2D) / planes (3D) [lo, hi) of the global grid
+ * (lo = rank (n-1)/nranks, hi = lo + (n-1)/nranks) stored with `ghost` = 2
+ * extra rows / planes below and above, i.e. a (hi - lo + 4) x pitch (2D) or
+ * (hi - lo + 4) x n x pitch (3D) array whose row / plane 2 is global lo (see
+ * mg_local_extent); the global boundary rows / planes 0 and n-1 lie in rank
+ * 0's own rows / the last rank's ghost rows and must be 0.  The library fills the ghost rows itself (halo
  * exchange per level).  Levels with fewer than cfg.agglom_points interior
  * nodes (or fewer than 4 rows per rank) are all-gathered and solved
  * redundantly on every rank; residual norms are max-reduced over ranks.

@@ -189,15 +189,22 @@ struct OpJacR3 {
   static __device__ void finish(const Params &, State &) {}
 };
 
+// Two half-index rows per thread for the single-colour-ring passes below:
+// warp w owns rows b = b0 + 2w (+ ring offset) and the next one.
+constexpr int RH2 = 32, RBOX2 = RW * RH2 * 8;                  // 8192 B
+constexpr int BOX34x33 = al128(34 * 33 * 8), BOX36x33 = al128(36 * 33 * 8);
+
 // ===================================================== G(2s) -> M(s): a13
-// Same thread map as OpJacR3.  L_j = {v_G(2s)(j), r_B(j-1), r_C(j-2)}.
-// Step j: centres of plane j-1 (Emprolm), corners of plane j-2
-// from the new centres (Emprolb).
+// Thread columns (a0-2+l, b0-1+2w+R), R = 0, 1: core a in [a0, a0+30)
+// (l >= 2), b in [b0, b0+31) (not the first row of warp 0).
+// L_j = {v_G(2s)(j), r_B(j-1), r_C(j-2)}.  Step j: centres of plane j-1
+// (Emprolm), corners of plane j-2 from the new centres
+// (Emprolb).
 struct OpJacM3 {
-  static constexpr int NS = 10, PRO = 1, EPI = 2;
-  static constexpr int OG = 0, OR = BOX34;   // v_G box, r boxes (B, C)
-  static constexpr int SLOT = OR + 2 * RBOX;
-  static constexpr int GPL = RBOX;           // centre ring plane
+  static constexpr int NS = 7, PRO = 1, EPI = 2;
+  static constexpr int OG = 0, OR = BOX34x33;   // v_G box, r boxes (B, C)
+  static constexpr int SLOT = OR + 2 * RBOX2;
+  static constexpr int GPL = RBOX2;             // centre ring plane
   static constexpr int SMEM = NS * SLOT + 3 * GPL;
   struct Params {
     CUtensorMap tg, tr[2];   // v_G(2s); r_M B, C
@@ -207,10 +214,10 @@ struct OpJacM3 {
     T cc;
   };
   struct State {
-    T bo[2];   // own new centre values by plane parity
+    T bo[2][2];   // [plane parity][row] own new centre values
   };
   struct Ctx {
-    bool b0k, b1k, core;   // (a, b) in [0,H-2]^2 / [1,H-2]^2, core column
+    bool b0k[2], b1k[2], core[2];   // per row: (a, b) in [0,H-2]^2 / [1,H-2]^2, core node
   };
   static __device__ void prefetch(const Params &P) {
     tma_prefetch_desc(&P.tg);
@@ -220,18 +227,22 @@ struct OpJacM3 {
   static __device__ void init(State &) {}
   static __device__ void begin(const Params &P, Ctx &C, const Item &it) {
     const int l = threadIdx.x & 31, w = threadIdx.x >> 5;
-    const int a = it.x0 - 2 + l, b = it.y0 - 1 + w;
+    const int a = it.x0 - 2 + l;
     const HM m{P.H};
-    C.b0k = m.z0(a) && m.z0(b);
-    C.b1k = m.z1(a) && m.z1(b);
-    C.core = l >= 2 && w >= 1;
+#pragma unroll
+    for (int R = 0; R < 2; R++) {
+      const int b = it.y0 - 1 + 2 * w + R;
+      C.b0k[R] = m.z0(a) && m.z0(b);
+      C.b1k[R] = m.z1(a) && m.z1(b);
+      C.core[R] = l >= 2 && (w >= 1 || R == 1);
+    }
   }
   static __device__ void issue(const Params &P, const Item &it, int j, unsigned char *slot, uint64_t *bar) {
     const bool wf = j >= it.zs, wc = j >= it.zs + 2;
-    mbar_expect_tx(bar, 34 * 17 * 8 + (wf ? RBOX : 0) + (wc ? RBOX : 0));
+    mbar_expect_tx(bar, 34 * 33 * 8 + (wf ? RBOX2 : 0) + (wc ? RBOX2 : 0));
     tma_load_3d(slot + OG, &P.tg, it.x0 - 2, it.y0 - 1, j, bar);
     if (wf) tma_load_3d(slot + OR, &P.tr[0], it.x0 - 2, it.y0 - 1, j - 1, bar);
-    if (wc) tma_load_3d(slot + OR + RBOX, &P.tr[1], it.x0 - 2, it.y0 - 1, j - 2, bar);
+    if (wc) tma_load_3d(slot + OR + RBOX2, &P.tr[1], it.x0 - 2, it.y0 - 1, j - 2, bar);
   }
   template <int PH>
   static __device__ __forceinline__ void step(const Params &P, State &S, const Ctx &Cx, const Item &it, int j,
@@ -240,53 +251,58 @@ struct OpJacM3 {
     constexpr int Q = PH ^ 1;
     if (j < it.zs) return;
     const int l = threadIdx.x & 31, w = threadIdx.x >> 5;
-    const int a = it.x0 - 2 + l, b = it.y0 - 1 + w;
-    const int og = w * 34 + l, orr = w * RW + l;
+    const int a = it.x0 - 2 + l;
     const HM m{P.H};
-    const int c = j - 1;
-    const T *Gc = (const T *)(Lp + OG) + og, *Gn = (const T *)(Lc + OG) + og;   // v_G planes c, c+1
-    const T *R = (const T *)(Lc + OR) + orr;
-    T t = -(P.cc * R[0]);
-    t = t + Gn[35];   // (+,+,+)
-    t = t + Gc[35];   // (+,+,-)
-    t = t + Gn[1];    // (+,-,+)
-    t = t + Gc[1];    // (+,-,-)
-    t = t + Gn[34];   // (-,+,+)
-    t = t + Gc[34];   // (-,+,-)
-    t = t + Gn[0];    // (-,-,+)
-    t = t + Gc[0];    // (-,-,-)
-    const bool ok = Cx.b0k && m.z0(c);
-    const T bn = ok ? t * (T)0.125 : (T)0;
-    ((T *)gz)[orr] = bn;
-    if (ok && Cx.core && c >= it.zs && c < it.ze)
-      __stcs(P.v.s[B] + (int64_t)c * P.v.plane + (int64_t)b * P.v.pitch + a, bn);
-    const int q = j - 2;
-    if (q >= it.zs && Cx.core && Cx.b1k && m.z1(q)) {
-      const T *G0 = (const T *)gq + orr, *G1 = (const T *)gr + orr;   // centres of planes q, q-1
-      T u = -(P.cc * R[RBOX / 8]);
-      u = u + S.bo[PH];        // (a, b, c)
-      u = u + S.bo[Q];         // (a, b, c-1)
-      u = u + G0[-RW];         // (a, b-1, c)
-      u = u + G1[-RW];         // (a, b-1, c-1)
-      u = u + G0[-1];          // (a-1, b, c)
-      u = u + G1[-1];          // (a-1, b, c-1)
-      u = u + G0[-RW - 1];     // (a-1, b-1, c)
-      u = u + G1[-RW - 1];     // (a-1, b-1, c-1)
-      __stcs(P.v.s[C] + (int64_t)q * P.v.plane + (int64_t)b * P.v.pitch + a, u * (T)0.125);
+    const int c = j - 1, q = j - 2;
+    const bool czin = m.z0(c), cout = c >= it.zs && c < it.ze, qok = q >= it.zs && m.z1(q);
+    T bn[2];
+#pragma unroll
+    for (int R = 0; R < 2; R++) {
+      const int og = (2 * w + R) * 34 + l, orr = (2 * w + R) * RW + l;
+      const T *Gc = (const T *)(Lp + OG) + og, *Gn = (const T *)(Lc + OG) + og;   // v_G planes c, c+1
+      const T *Rb = (const T *)(Lc + OR) + orr;
+      T t = -(P.cc * Rb[0]);
+      t = t + Gn[35];   // (+,+,+)
+      t = t + Gc[35];   // (+,+,-)
+      t = t + Gn[1];    // (+,-,+)
+      t = t + Gc[1];    // (+,-,-)
+      t = t + Gn[34];   // (-,+,+)
+      t = t + Gc[34];   // (-,+,-)
+      t = t + Gn[0];    // (-,-,+)
+      t = t + Gc[0];    // (-,-,-)
+      const bool ok = Cx.b0k[R] && czin;
+      bn[R] = ok ? t * (T)0.125 : (T)0;
+      ((T *)gz)[orr] = bn[R];
+      const int b = it.y0 - 1 + 2 * w + R;
+      if (ok && Cx.core[R] && cout) __stcs(P.v.s[B] + (int64_t)c * P.v.plane + (int64_t)b * P.v.pitch + a, bn[R]);
+      if (qok && Cx.core[R] && Cx.b1k[R]) {
+        const T *G0 = (const T *)gq + orr, *G1 = (const T *)gr + orr;   // centres of planes q, q-1
+        T u = -(P.cc * Rb[RBOX2 / 8]);
+        u = u + S.bo[PH][R];     // (a, b, c)
+        u = u + S.bo[Q][R];      // (a, b, c-1)
+        u = u + G0[-RW];         // (a, b-1, c)
+        u = u + G1[-RW];         // (a, b-1, c-1)
+        u = u + G0[-1];          // (a-1, b, c)
+        u = u + G1[-1];          // (a-1, b, c-1)
+        u = u + G0[-RW - 1];     // (a-1, b-1, c)
+        u = u + G1[-RW - 1];     // (a-1, b-1, c-1)
+        __stcs(P.v.s[C] + (int64_t)q * P.v.plane + (int64_t)b * P.v.pitch + a, u * (T)0.125);
+      }
     }
-    S.bo[Q] = bn;
+    S.bo[Q][0] = bn[0];
+    S.bo[Q][1] = bn[1];
   }
   static __device__ void finish(const Params &, State &) {}
 };
 
 // ===================================================== R(s) -> M(s): a11
-// Thread column (a, b) = (a0+l, b0+w), tiles 32 x 16, no ring.
+// Thread columns (a0+l, b0+2w+R), tiles 32 x 32, no ring.
 // L_j = {Fx(j), Fy(j), Fz(j+1), C_R(j)}; step j: corners (Ermagc)
 // and centres (Ermagm) of plane j.
 struct OpRestRM3 {
-  static constexpr int NS = 10, PRO = 1, EPI = 0;
-  static constexpr int OX = 0, OY = BOX36, OZ = BOX36 + BOX34, OCR = BOX36 + 2 * BOX34;
-  static constexpr int SLOT = OCR + RBOX;
+  static constexpr int NS = 6, PRO = 1, EPI = 0;
+  static constexpr int OX = 0, OY = BOX36x33, OZ = BOX36x33 + BOX34x33, OCR = BOX36x33 + 2 * BOX34x33;
+  static constexpr int SLOT = OCR + RBOX2;
   static constexpr int GPL = 0;
   static constexpr int SMEM = NS * SLOT + 128;
   struct Params {
@@ -297,7 +313,7 @@ struct OpRestRM3 {
   };
   struct State {};
   struct Ctx {
-    bool k0, k1;   // (a, b) in [0,H-2]^2 / [1,H-2]^2
+    bool k0[2], k1[2];   // per row: (a, b) in [0,H-2]^2 / [1,H-2]^2
   };
   static __device__ void prefetch(const Params &P) {
     tma_prefetch_desc(&P.tx);
@@ -309,12 +325,15 @@ struct OpRestRM3 {
   static __device__ void begin(const Params &P, Ctx &C, const Item &it) {
     const int l = threadIdx.x & 31, w = threadIdx.x >> 5;
     const HM m{P.H};
-    C.k0 = m.z0(it.x0 + l) && m.z0(it.y0 + w);
-    C.k1 = m.z1(it.x0 + l) && m.z1(it.y0 + w);
+#pragma unroll
+    for (int R = 0; R < 2; R++) {
+      C.k0[R] = m.z0(it.x0 + l) && m.z0(it.y0 + 2 * w + R);
+      C.k1[R] = m.z1(it.x0 + l) && m.z1(it.y0 + 2 * w + R);
+    }
   }
   static __device__ void issue(const Params &P, const Item &it, int j, unsigned char *slot, uint64_t *bar) {
     const bool wc = j >= it.zs;
-    mbar_expect_tx(bar, 36 * 17 * 8 + 2 * 34 * 17 * 8 + (wc ? RBOX : 0));
+    mbar_expect_tx(bar, 36 * 33 * 8 + 2 * 34 * 33 * 8 + (wc ? RBOX2 : 0));
     tma_load_3d(slot + OX, &P.tx, it.x0 - 2, it.y0 - 1, j, bar);
     tma_load_3d(slot + OY, &P.ty, it.x0 - 2, it.y0, j, bar);
     tma_load_3d(slot + OZ, &P.tz, it.x0 - 2, it.y0 - 1, j + 1, bar);
@@ -326,49 +345,55 @@ struct OpRestRM3 {
                                               unsigned char *, unsigned char *) {
     if (j < it.zs) return;
     const int l = threadIdx.x & 31, w = threadIdx.x >> 5;
-    const int a = it.x0 + l, b = it.y0 + w, c = j;
+    const int a = it.x0 + l, c = j;
     const HM m{P.H};
-    const int ox = (w + 1) * 36 + l + 2, oy = w * 34 + l + 2, oz = (w + 1) * 34 + l + 2;
-    const T *Xc = (const T *)(Lc + OX) + ox, *Xp = (const T *)(Lp + OX) + ox;   // Fx planes c, c-1
-    const T *Yc = (const T *)(Lc + OY) + oy, *Yp = (const T *)(Lp + OY) + oy;   // Fy planes c, c-1
-    const T *Zn = (const T *)(Lc + OZ) + oz, *Zc = (const T *)(Lp + OZ) + oz;   // Fz planes c+1, c
-    const int64_t o = (int64_t)c * P.out.plane + (int64_t)b * P.out.pitch + a;
-    if (Cx.k1 && m.z1(c)) {
-      T t = (T)12 * ((const T *)(Lc + OCR))[w * RW + l];
-      t = t + Zc[0];         // (+1,+1, 0)
-      t = t + Zc[-34];       // (+1,-1, 0)
-      t = t + Zc[-35];       // (-1,-1, 0)
-      t = t + Zc[-1];        // (-1,+1, 0)
-      t = t + Yc[0];         // (+1, 0,+1)
-      t = t + Yp[0];         // (+1, 0,-1)
-      t = t + Yp[-1];        // (-1, 0,-1)
-      t = t + Yc[-1];        // (-1, 0,+1)
-      t = t + Xc[0];         // ( 0,+1,+1)
-      t = t + Xp[0];         // ( 0,+1,-1)
-      t = t + Xp[-36];       // ( 0,-1,-1)
-      t = t + Xc[-36];       // ( 0,-1,+1)
-      __stcs(P.out.s[C] + o, t * (T)(1.0 / 24.0));
-    }
-    if (Cx.k0 && m.z0(c)) {
-      // centre (2a+1, 2b+1, 2c+1): i+1, i-1, j+1, j-1, k+1, k-1
-      T t = Xc[1];
-      t = t + Xc[0];
-      t = t + Yc[34];
-      t = t + Yc[0];
-      t = t + Zn[0];
-      t = t + Zc[0];
-      __stcs(P.out.s[B] + o, t * (T)(1.0 / 6.0));
+    const bool c0 = m.z0(c), c1 = m.z1(c);
+#pragma unroll
+    for (int R = 0; R < 2; R++) {
+      const int b = it.y0 + 2 * w + R, rr = 2 * w + R;
+      const int ox = (rr + 1) * 36 + l + 2, oy = rr * 34 + l + 2, oz = (rr + 1) * 34 + l + 2;
+      const T *Xc = (const T *)(Lc + OX) + ox, *Xp = (const T *)(Lp + OX) + ox;   // Fx planes c, c-1
+      const T *Yc = (const T *)(Lc + OY) + oy, *Yp = (const T *)(Lp + OY) + oy;   // Fy planes c, c-1
+      const T *Zn = (const T *)(Lc + OZ) + oz, *Zc = (const T *)(Lp + OZ) + oz;   // Fz planes c+1, c
+      const int64_t o = (int64_t)c * P.out.plane + (int64_t)b * P.out.pitch + a;
+      if (Cx.k1[R] && c1) {
+        T t = (T)12 * ((const T *)(Lc + OCR))[rr * RW + l];
+        t = t + Zc[0];         // (+1,+1, 0)
+        t = t + Zc[-34];       // (+1,-1, 0)
+        t = t + Zc[-35];       // (-1,-1, 0)
+        t = t + Zc[-1];        // (-1,+1, 0)
+        t = t + Yc[0];         // (+1, 0,+1)
+        t = t + Yp[0];         // (+1, 0,-1)
+        t = t + Yp[-1];        // (-1, 0,-1)
+        t = t + Yc[-1];        // (-1, 0,+1)
+        t = t + Xc[0];         // ( 0,+1,+1)
+        t = t + Xp[0];         // ( 0,+1,-1)
+        t = t + Xp[-36];       // ( 0,-1,-1)
+        t = t + Xc[-36];       // ( 0,-1,+1)
+        __stcs(P.out.s[C] + o, t * (T)(1.0 / 24.0));
+      }
+      if (Cx.k0[R] && c0) {
+        // centre (2a+1, 2b+1, 2c+1): i+1, i-1, j+1, j-1, k+1, k-1
+        T t = Xc[1];
+        t = t + Xc[0];
+        t = t + Yc[34];
+        t = t + Yc[0];
+        t = t + Zn[0];
+        t = t + Zc[0];
+        __stcs(P.out.s[B] + o, t * (T)(1.0 / 6.0));
+      }
     }
   }
   static __device__ void finish(const Params &, State &) {}
 };
 
 // ===================================================== M(s) -> G(2s): a12
-// Erblu.  L_j = {C_M(j), B_M(j)}; step j: plane j.
+// Erblu.  Tiles 32 x 32, two rows per thread.
+// L_j = {C_M(j), B_M(j)}; step j: plane j.
 struct OpRestMG3 {
   static constexpr int NS = 12, PRO = 1, EPI = 0;
-  static constexpr int OB = 0, OCM = BOX34;
-  static constexpr int SLOT = OCM + RBOX;
+  static constexpr int OB = 0, OCM = BOX34x33;
+  static constexpr int SLOT = OCM + RBOX2;
   static constexpr int GPL = 0;
   static constexpr int SMEM = NS * SLOT + 128;
   struct Params {
@@ -379,7 +404,7 @@ struct OpRestMG3 {
   };
   struct State {};
   struct Ctx {
-    bool k1;
+    bool k1[2];
   };
   static __device__ void prefetch(const Params &P) {
     tma_prefetch_desc(&P.tb);
@@ -389,11 +414,12 @@ struct OpRestMG3 {
   static __device__ void begin(const Params &P, Ctx &C, const Item &it) {
     const int l = threadIdx.x & 31, w = threadIdx.x >> 5;
     const HM m{P.H};
-    C.k1 = m.z1(it.x0 + l) && m.z1(it.y0 + w);
+    C.k1[0] = m.z1(it.x0 + l) && m.z1(it.y0 + 2 * w);
+    C.k1[1] = m.z1(it.x0 + l) && m.z1(it.y0 + 2 * w + 1);
   }
   static __device__ void issue(const Params &P, const Item &it, int j, unsigned char *slot, uint64_t *bar) {
     const bool wc = j >= it.zs;
-    mbar_expect_tx(bar, 34 * 17 * 8 + (wc ? RBOX : 0));
+    mbar_expect_tx(bar, 34 * 33 * 8 + (wc ? RBOX2 : 0));
     tma_load_3d(slot + OB, &P.tb, it.x0 - 2, it.y0 - 1, j, bar);
     if (wc) tma_load_3d(slot + OCM, &P.tc, it.x0, it.y0, j, bar);
   }
@@ -403,21 +429,26 @@ struct OpRestMG3 {
                                               unsigned char *, unsigned char *) {
     if (j < it.zs) return;
     const int l = threadIdx.x & 31, w = threadIdx.x >> 5;
-    const int a = it.x0 + l, b = it.y0 + w, c = j;
+    const int a = it.x0 + l, c = j;
     const HM m{P.H};
-    if (!(Cx.k1 && m.z1(c))) return;
-    const int ob = (w + 1) * 34 + l + 2;
-    const T *Bc = (const T *)(Lc + OB) + ob, *Bp = (const T *)(Lp + OB) + ob;   // B planes c, c-1
-    T t = (T)8 * ((const T *)(Lc + OCM))[w * RW + l];
-    t = t + Bc[0];         // (+,+,+)
-    t = t + Bp[0];         // (+,+,-)
-    t = t + Bc[-34];       // (+,-,+)
-    t = t + Bp[-34];       // (+,-,-)
-    t = t + Bc[-1];        // (-,+,+)
-    t = t + Bp[-1];        // (-,+,-)
-    t = t + Bc[-35];       // (-,-,+)
-    t = t + Bp[-35];       // (-,-,-)
-    __stcs(&P.out(a, b, c), t * (T)(1.0 / 16.0));
+    if (!m.z1(c)) return;
+#pragma unroll
+    for (int R = 0; R < 2; R++) {
+      if (!Cx.k1[R]) continue;
+      const int b = it.y0 + 2 * w + R, rr = 2 * w + R;
+      const int ob = (rr + 1) * 34 + l + 2;
+      const T *Bc = (const T *)(Lc + OB) + ob, *Bp = (const T *)(Lp + OB) + ob;   // B planes c, c-1
+      T t = (T)8 * ((const T *)(Lc + OCM))[rr * RW + l];
+      t = t + Bc[0];         // (+,+,+)
+      t = t + Bp[0];         // (+,+,-)
+      t = t + Bc[-34];       // (+,-,+)
+      t = t + Bp[-34];       // (+,-,-)
+      t = t + Bc[-1];        // (-,+,+)
+      t = t + Bp[-1];        // (-,+,-)
+      t = t + Bc[-35];       // (-,-,+)
+      t = t + Bp[-35];       // (-,-,-)
+      __stcs(&P.out(a, b, c), t * (T)(1.0 / 16.0));
+    }
   }
   static __device__ void finish(const Params &, State &) {}
 };
@@ -448,35 +479,35 @@ cudaError_t fast3s_jac_m(const D3<double> &vc, const S3<double> &r, const S3<dou
   using Op = OpJacM3;
   Op::Params P{};
   const int H = M / 2 + 1;
-  if (!tmap3<T>(&P.tg, vc.p, H, H, H, vc.pitch, vc.plane, 34, 17) || !tsub(&P.tr[0], r, B, H, RW, RH) ||
-      !tsub(&P.tr[1], r, C, H, RW, RH))
+  if (!tmap3<T>(&P.tg, vc.p, H, H, H, vc.pitch, vc.plane, 34, 33) || !tsub(&P.tr[0], r, B, H, RW, RH2) ||
+      !tsub(&P.tr[1], r, C, H, RW, RH2))
     return cudaErrorInvalidValue;
   P.v = v;
   P.H = H;
   P.cc = cc;
-  return launch_zpipe<Op>(P, 30, 15, 0, 0, cdiv(H - 1, 30), cdiv(H - 1, 15), 0, H - 1, st);
+  return launch_zpipe<Op>(P, 30, 31, 0, 0, cdiv(H - 1, 30), cdiv(H - 1, 31), 0, H - 1, st);
 }
 
 cudaError_t fast3s_rest_rm(const S3<double> &rr, const S3<double> &rm, int M, cudaStream_t st) {
   using Op = OpRestRM3;
   Op::Params P{};
   const int H = M / 2 + 1;
-  if (!tsub(&P.tx, rr, FX, H, 36, 17) || !tsub(&P.ty, rr, FY, H, 34, 17) || !tsub(&P.tz, rr, FZ, H, 34, 17) ||
-      !tsub(&P.tc, rr, C, H, RW, RH))
+  if (!tsub(&P.tx, rr, FX, H, 36, 33) || !tsub(&P.ty, rr, FY, H, 34, 33) || !tsub(&P.tz, rr, FZ, H, 34, 33) ||
+      !tsub(&P.tc, rr, C, H, RW, RH2))
     return cudaErrorInvalidValue;
   P.out = rm;
   P.H = H;
-  return launch_zpipe<Op>(P, 32, 16, 0, 0, cdiv(H - 1, 32), cdiv(H - 1, 16), 0, H - 1, st);
+  return launch_zpipe<Op>(P, 32, 32, 0, 0, cdiv(H - 1, 32), cdiv(H - 1, 32), 0, H - 1, st);
 }
 
 cudaError_t fast3s_rest_mg(const S3<double> &rm, const D3<double> &g2, int Mc, cudaStream_t st) {
   using Op = OpRestMG3;
   Op::Params P{};
   const int H = Mc + 1;
-  if (!tsub(&P.tb, rm, B, H, 34, 17) || !tsub(&P.tc, rm, C, H, RW, RH)) return cudaErrorInvalidValue;
+  if (!tsub(&P.tb, rm, B, H, 34, 33) || !tsub(&P.tc, rm, C, H, RW, RH2)) return cudaErrorInvalidValue;
   P.out = g2;
   P.H = H;
-  return launch_zpipe<Op>(P, 32, 16, 0, 0, cdiv(H - 1, 32), cdiv(H - 1, 16), 1, H - 1, st);
+  return launch_zpipe<Op>(P, 32, 32, 0, 0, cdiv(H - 1, 32), cdiv(H - 1, 32), 1, H - 1, st);
 }
 
 }  // namespace mg

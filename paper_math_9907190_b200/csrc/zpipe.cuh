@@ -69,32 +69,37 @@ __device__ __forceinline__ T res7(T c, T xp, T xm, T yp, T ym, T zp, T zm, T f, 
   return f - lap;
 }
 
-// Balanced work list: items k < W are whole tiles b + k*G over [zlo, zhi);
-// item W (when R = T mod G > 0) is one z segment of tail tile W*G + b mod R.
+// Balanced work list.  Each of the T tiles is cut into S z pieces (S = 1
+// unless T < G) giving U = T*S units; units k*G + b (k < W = U / G) are
+// whole; the R = U mod G remaining units are each split into ~G/R z segments,
+// one per CTA, so every CTA streams the same number of planes and tiles that
+// are neighbours in xy are streamed concurrently (their halos hit in L2).
 struct Item {
   int x0, y0, zs, ze;
 };
 struct Sched {
-  int T, ntx, zlo, zhi;
+  int T, ntx, zlo, zhi, S;
   int tx, ty, xoff, yoff;   // tile extents and origin offsets: x0 = tx * (t % ntx) + xoff
-  __device__ __forceinline__ int count(int G) const { return T / G + (T % G ? 1 : 0); }
+  __device__ __forceinline__ int count(int G) const { return (T * S) / G + ((T * S) % G ? 1 : 0); }
   __device__ __forceinline__ Item get(int k, int b, int G) const {
-    const int W = T / G, R = T % G;
-    int t, zs = zlo, ze = zhi;
+    const int U = T * S, W = U / G, R = U % G;
+    const long long Z = zhi - zlo;
+    int u, sg = 0, nseg = 1;
     if (k < W) {
-      t = b + k * G;
+      u = b + k * G;
     } else {
-      const int r = b % R, nseg = G / R + (r < G % R ? 1 : 0), sg = b / R;
-      const long long Z = zhi - zlo;
-      t = W * G + r;
-      zs = zlo + (int)(Z * sg / nseg);
-      ze = zlo + (int)(Z * (sg + 1) / nseg);
+      const int r = b % R;
+      u = W * G + r;
+      nseg = G / R + (r < G % R ? 1 : 0);
+      sg = b / R;
     }
+    const int t = u % T, p = u / T;
+    const int z0 = zlo + (int)(Z * p / S), z1 = zlo + (int)(Z * (p + 1) / S);
     Item it;
     it.x0 = (t % ntx) * tx + xoff;
     it.y0 = (t / ntx) * ty + yoff;
-    it.zs = zs;
-    it.ze = ze;
+    it.zs = z0 + (int)((long long)(z1 - z0) * sg / nseg);
+    it.ze = z0 + (int)((long long)(z1 - z0) * (sg + 1) / nseg);
     return it;
   }
 };
@@ -217,6 +222,8 @@ static cudaError_t launch_zpipe(typename Op::Params &P, int tx, int ty, int xoff
   P.sc.T = ntx * nty;
   P.sc.zlo = zlo;
   P.sc.zhi = zhi;
+  P.sc.S = P.sc.T >= sms ? 1 : (sms + P.sc.T - 1) / P.sc.T;
+  if (P.sc.S > zhi - zlo) P.sc.S = zhi - zlo;
   const long long work = (long long)P.sc.T * (zhi - zlo);
   const int grid = work < sms ? (int)work : sms;
   return launch_pdl(zpipe<Op>, dim3(grid), dim3(NT), Op::SMEM, st, P);
