@@ -7,6 +7,7 @@
 //
 // Level kernels in this file work on lattice coordinates of one octave
 // s = 2^o (x = i/s, y = j/s), M = (n-1)/s.
+#include <cooperative_groups.h>
 #include <cstdlib>
 
 #include "kernels.h"
@@ -206,6 +207,110 @@ __global__ void __launch_bounds__(1024) k2_coarse_smem(const Lev2<T> *lvg, int o
     __syncthreads();
     for (int64_t t = tid; t < n; t += bs) node_jac_a2(rA, L.vA, M, L.cA, t);
     __syncthreads();
+  }
+}
+
+// Cooperative tail (as k3l_tail): octaves om .. oc-1 grid-wide with a grid
+// barrier between steps, octaves >= oc in CTA 0's shared memory; one launch.
+template <class T>
+struct Tail2 {
+  Lev2<T> lv[40];
+  int om, oc, k;
+  int *counter;
+};
+
+template <class T>
+__device__ __forceinline__ void coarse2_block(const Tail2<T> &P, T *arena) {
+  const int tid = threadIdx.x, bs = blockDim.x, oc = P.oc, k = P.k;
+  // octave o's arrays: r_E, r_O, v_E, v_O of D(s), r, v of A(2s) -- 6 consecutive W^2 arrays
+  auto off = [&](int o) {
+    size_t e = 0;
+    for (int q = oc; q < o; q++) {
+      const size_t W = P.lv[q].M / 2 + 1;
+      e += 6 * W * W;
+    }
+    return arena + e;
+  };
+  auto aa = [&](int o, int which) -> D2<T> {   // A(s) of octave o (global at oc)
+    if (o == oc) return which ? P.lv[o].vA : P.lv[o].rA;
+    const int W = P.lv[o - 1].M / 2 + 1;
+    return D2<T>{off(o - 1) + (int64_t)(4 + which) * W * W, W};
+  };
+  for (size_t t = tid, n = off(k - 1) - arena; t < n; t += bs) arena[t] = (T)0;
+  __syncthreads();
+  for (int o = oc; o + 1 < k; o++) {
+    const int M = P.lv[o].M, W = M / 2 + 1, n2 = W * W;
+    T *b = off(o);
+    const S2<T> rD{b, b + n2, W};
+    const D2<T> rA = aa(o, 0), rA2 = aa(o + 1, 0);
+    for (int64_t t = tid; t < (int64_t)n2; t += bs) node_rest_ad(D2<const T>{rA.p, rA.pitch}, rD, M, t);
+    __syncthreads();
+    const int64_t n = (int64_t)(M / 2 - 1) * (M / 2 - 1);
+    for (int64_t t = tid; t < n; t += bs) node_rest_da(S2<const T>{rD.e, rD.o, rD.pitch}, rA2, M / 2, t);
+    __syncthreads();
+  }
+  if (tid == 0) {
+    const D2<T> rA = aa(k - 1, 0), vA = aa(k - 1, 1);
+    node_coarsest(D2<const T>{rA.p, rA.pitch}, vA, P.lv[k - 1].cA, P.counter);
+  }
+  __syncthreads();
+  for (int o = k - 2; o >= oc; o--) {
+    const Lev2<T> &L = P.lv[o];
+    const int M = L.M, W = M / 2 + 1, n2 = W * W;
+    T *b = off(o);
+    const S2<const T> rD{b, b + n2, W};
+    const S2<T> vD{b + 2 * n2, b + 3 * n2, W};
+    const D2<T> rA = aa(o, 0), vA = aa(o, 1), vA2 = aa(o + 1, 1);
+    int64_t n = (int64_t)(M / 2) * (M / 2);
+    for (int64_t t = tid; t < n; t += bs) node_jac_d1(D2<const T>{vA2.p, vA2.pitch}, rD, vD, M, L.cD, t);
+    __syncthreads();
+    n = (int64_t)(M / 2 - 1) * (M / 2 - 1);
+    for (int64_t t = tid; t < n; t += bs) node_jac_d2(rD, vD, M, L.cD, t);
+    __syncthreads();
+    n = (int64_t)(M - 1) * (M - 1);
+    const S2<const T> vDc{vD.e, vD.o, vD.pitch};
+    const D2<const T> rAc{rA.p, rA.pitch};
+    for (int64_t t = tid; t < n; t += bs) node_jac_a1(vDc, rAc, vA, M, L.cA, t);
+    __syncthreads();
+    for (int64_t t = tid; t < n; t += bs) node_jac_a2(rAc, vA, M, L.cA, t);
+    __syncthreads();
+  }
+}
+
+template <class T>
+__global__ void __launch_bounds__(512, 1) k2_tail(const __grid_constant__ Tail2<T> P) {
+  namespace cg = cooperative_groups;
+  cg::grid_group grid = cg::this_grid();
+  extern __shared__ __align__(16) unsigned char dsm[];
+  const int64_t gt = (int64_t)blockIdx.x * blockDim.x + threadIdx.x, gs = (int64_t)gridDim.x * blockDim.x;
+  for (int o = P.om; o < P.oc; o++) {
+    const Lev2<T> &L = P.lv[o], &Lc = P.lv[o + 1];
+    int64_t n = (int64_t)(L.M / 2 + 1) * (L.M / 2 + 1);
+    for (int64_t t = gt; t < n; t += gs) node_rest_ad(D2<const T>{L.rA.p, L.rA.pitch}, L.rD, L.M, t);
+    grid.sync();
+    n = (int64_t)(Lc.M - 1) * (Lc.M - 1);
+    for (int64_t t = gt; t < n; t += gs) node_rest_da(S2<const T>{L.rD.e, L.rD.o, L.rD.pitch}, Lc.rA, Lc.M, t);
+    grid.sync();
+  }
+  if (blockIdx.x == 0) coarse2_block(P, (T *)dsm);
+  grid.sync();
+  for (int o = P.oc - 1; o >= P.om; o--) {
+    const Lev2<T> &L = P.lv[o], &Lc = P.lv[o + 1];
+    const int M = L.M;
+    const S2<const T> rD{L.rD.e, L.rD.o, L.rD.pitch};
+    int64_t n = (int64_t)(M / 2) * (M / 2);
+    for (int64_t t = gt; t < n; t += gs) node_jac_d1(D2<const T>{Lc.vA.p, Lc.vA.pitch}, rD, L.vD, M, L.cD, t);
+    grid.sync();
+    n = (int64_t)(M / 2 - 1) * (M / 2 - 1);
+    for (int64_t t = gt; t < n; t += gs) node_jac_d2(rD, L.vD, M, L.cD, t);
+    grid.sync();
+    n = (int64_t)(M - 1) * (M - 1);
+    const S2<const T> vD{L.vD.e, L.vD.o, L.vD.pitch};
+    const D2<const T> rA{L.rA.p, L.rA.pitch};
+    for (int64_t t = gt; t < n; t += gs) node_jac_a1(vD, rA, L.vA, M, L.cA, t);
+    grid.sync();
+    for (int64_t t = gt; t < n; t += gs) node_jac_a2(rA, L.vA, M, L.cA, t);
+    grid.sync();
   }
 }
 
@@ -515,5 +620,42 @@ void launch2_norm(const D2<const T> &a, int M, unsigned long long *mx, double *s
 
 INST(float)
 INST(double)
+
+
+template <class T>
+bool launch2_tail(const Lev2<T> *h_lev, int om, int oc, int k, int *counter, cudaStream_t st) {
+  if (k > 40 || om < 1 || om > oc || oc >= k) return false;
+  Tail2<T> P;
+  for (int o = 0; o < k; o++) P.lv[o] = h_lev[o];
+  P.om = om;
+  P.oc = oc;
+  P.k = k;
+  P.counter = counter;
+  size_t elems = 0;
+  for (int o = oc; o + 1 < k; o++) {
+    const size_t W = h_lev[o].M / 2 + 1;
+    elems += 6 * W * W;
+  }
+  const size_t bytes = elems * sizeof(T);
+  if (bytes > 200 * 1024) return false;
+  if (cudaFuncSetAttribute(k2_tail<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes) != cudaSuccess)
+    return false;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(sms);
+  cfg.blockDim = dim3(512);
+  cfg.dynamicSmemBytes = bytes;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeCooperative;
+  at[0].val.cooperative = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, k2_tail<T>, P) == cudaSuccess;
+}
+template bool launch2_tail<float>(const Lev2<float> *, int, int, int, int *, cudaStream_t);
+template bool launch2_tail<double>(const Lev2<double> *, int, int, int, int *, cudaStream_t);
 
 }  // namespace mg

@@ -9,6 +9,8 @@
 // The neighbour order of every sum is the paper's printed order (DESIGN.md
 // canonical arithmetic), so the results are bit-identical to the reference
 // kernels.
+#include <cooperative_groups.h>
+#include <cstdio>
 #include <cstdlib>
 #include <initializer_list>
 
@@ -517,6 +519,161 @@ __global__ void __launch_bounds__(1024) k3l_coarse_smem(const Lev3<T> *lvg, int 
 #undef LOOP3
 }
 
+// ------------------------------------------------------ cooperative tail
+// One cooperative launch for every octave o >= om: the octaves om .. oc-1 run
+// grid-wide (each step a grid-stride loop over its blocks, one grid barrier
+// between steps; the level arrays are L2 resident), the octaves >= oc run in
+// CTA 0's shared memory with __syncthreads between steps (the other CTAs wait
+// at the next grid barrier).  Same node bodies, same order as the per-level
+// kernels, so the results are identical.  Level descriptors come in the
+// kernel parameter block (uniform, constant-cached).
+template <class T>
+struct Tail3 {
+  Lev3<T> lv[20];
+  int om, oc, k;
+  int *counter;
+  unsigned long long *dbg;   // MG_TAIL_DEBUG: globaltimer stamps of CTA 0's phases (else null)
+};
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
+// coarse octaves in shared memory: level arrays at fixed offsets of one arena
+template <class T>
+__device__ __forceinline__ void coarse3_block(const Tail3<T> &P, T *arena) {
+  const int tid = threadIdx.x, bs = blockDim.x, oc = P.oc, k = P.k;
+  // octave o's arrays: 14 consecutive H^3 arrays starting at off(o)
+  auto off = [&](int o) {
+    size_t e = 0;
+    for (int q = oc; q < o; q++) {
+      const size_t H = P.lv[q].M / 2 + 1;
+      e += 14 * H * H * H;
+    }
+    return arena + e;
+  };
+  auto sub = [&](T *base, int H, std::initializer_list<int> subs, std::initializer_list<int> idx) {
+    S3<T> a;
+    for (int q = 0; q < 8; q++) a.s[q] = nullptr;
+    const int64_t n3 = (int64_t)H * H * H;
+    auto it = idx.begin();
+    for (int q : subs) a.s[q] = base + (*it++) * n3;
+    a.pitch = H;
+    a.plane = (int64_t)H * H;
+    return a;
+  };
+  auto cs = [](const S3<T> &a) {
+    S3<const T> o;
+    for (int i = 0; i < 8; i++) o.s[i] = a.s[i];
+    o.pitch = a.pitch;
+    o.plane = a.plane;
+    return o;
+  };
+  auto cd = [](const D3<T> &a) { return D3<const T>{a.p, a.pitch, a.plane}; };
+  // G(s) of octave o: global at o = oc, else the G(2s) arrays of octave o-1
+  auto gr = [&](int o, int which) -> D3<T> {
+    if (o == oc) return which ? P.lv[o].vG : P.lv[o].rG;
+    const int H = P.lv[o - 1].M / 2 + 1;
+    return D3<T>{off(o - 1) + (int64_t)(12 + which) * H * H * H, H, (int64_t)H * H};
+  };
+  D3<const T> none{nullptr, 0, 0};
+  Coef<T> k0{};
+  for (size_t t = tid, n = off(k - 1) - arena; t < n; t += bs) arena[t] = (T)0;
+  __syncthreads();
+#define LOOPB(HH, BODY)                                            \
+  {                                                                \
+    const int H_ = (HH);                                           \
+    const int n_ = H_ * H_ * H_;                                   \
+    for (int t = tid; t < n_; t += bs) {                           \
+      const int a = t % H_, b = (t / H_) % H_, c = t / (H_ * H_); \
+      BODY;                                                        \
+    }                                                              \
+    __syncthreads();                                               \
+    if (P.dbg && tid == 0) P.dbg[1 + (nph++)] = gtimer();          \
+  }
+  int nph = 0;
+  if (P.dbg && tid == 0) P.dbg[0] = gtimer();
+  for (int o = oc; o + 1 < k; o++) {
+    const int M = P.lv[o].M, H = M / 2 + 1;
+    T *base = off(o);
+    const S3<T> rR = sub(base, H, {0, 3, 5, 6}, {0, 1, 2, 3}), rM = sub(base, H, {0, 7}, {8, 9});
+    const D3<T> rG = gr(o, 0), rG2 = gr(o + 1, 0);
+    LOOPB(H, b3_rest_gr(cd(rG), rR, M, H, a, b, c));
+    LOOPB(H, b3_rest_rm(cs(rR), rM, H, a, b, c));
+    LOOPB(M / 2 + 1, b3_rest_mg(cs(rM), rG2, M / 2, a, b, c));
+  }
+  if (tid == 0) {
+    const D3<T> rG = gr(k - 1, 0), vG = gr(k - 1, 1);
+    vG(1, 1, 1) = (-(P.lv[k - 1].cG * rG(1, 1, 1))) * (T)(1.0 / 6.0);   // reading A4
+    if (P.counter) *P.counter += 1;
+  }
+  __syncthreads();
+  for (int o = k - 2; o >= oc; o--) {
+    const Lev3<T> &L = P.lv[o];
+    const int M = L.M, H = M / 2 + 1;
+    T *base = off(o);
+    const S3<T> rR = sub(base, H, {0, 3, 5, 6}, {0, 1, 2, 3}), vR = sub(base, H, {0, 3, 5, 6}, {4, 5, 6, 7});
+    const S3<T> rM = sub(base, H, {0, 7}, {8, 9}), vM = sub(base, H, {0, 7}, {10, 11});
+    const D3<T> rG = gr(o, 0), vG = gr(o, 1), vG2 = gr(o + 1, 1);
+    LOOPB(H, b3_jac_m1(cd(vG2), cs(rM), vM, H, L.cMg, a, b, c));
+    LOOPB(H, b3_jac_m2(cs(rM), vM, H, L.cMg, a, b, c));
+    LOOPB(H, b3_jac_r1(cs(vM), cs(rR), vR, H, L.cR1, a, b, c));
+    LOOPB(H, b3_jac_r2(cs(rR), vR, H, L.cR2, a, b, c));
+    LOOPB(H, (b3_jac_g1<T, 2, false>(cs(vR), cd(rG), none, none, vG, M, H, L.cG, k0, a, b, c)));
+    LOOPB(H, (b3_jac_g2<T, 2, false>(cd(rG), none, none, cd(vG), vG, M, H, L.cG, k0, a, b, c)));
+  }
+#undef LOOPB
+}
+
+template <class T>
+__global__ void __launch_bounds__(512, 1) k3l_tail(const __grid_constant__ Tail3<T> P) {
+  namespace cg = cooperative_groups;
+  cg::grid_group grid = cg::this_grid();
+  extern __shared__ __align__(16) unsigned char dsm[];
+  const int gt = blockIdx.x * blockDim.x + threadIdx.x, gs = gridDim.x * blockDim.x;
+  auto cd = [](const D3<T> &a) { return D3<const T>{a.p, a.pitch, a.plane}; };
+  auto cs = [](const S3<T> &a) {
+    S3<const T> o;
+    for (int i = 0; i < 8; i++) o.s[i] = a.s[i];
+    o.pitch = a.pitch;
+    o.plane = a.plane;
+    return o;
+  };
+#define LOOPG(HH, BODY)                                            \
+  {                                                                \
+    const int H_ = (HH);                                           \
+    const int n_ = H_ * H_ * H_;                                   \
+    for (int t = gt; t < n_; t += gs) {                            \
+      const int a = t % H_, b = (t / H_) % H_, c = t / (H_ * H_); \
+      BODY;                                                        \
+    }                                                              \
+    grid.sync();                                                   \
+  }
+  for (int o = P.om; o < P.oc; o++) {
+    const Lev3<T> &L = P.lv[o], &Lc = P.lv[o + 1];
+    const int H = L.M / 2 + 1;
+    LOOPG(H, b3_rest_gr(cd(L.rG), L.rR, L.M, H, a, b, c));
+    LOOPG(H, b3_rest_rm(cs(L.rR), L.rM, H, a, b, c));
+    LOOPG(Lc.M + 1, b3_rest_mg(cs(L.rM), Lc.rG, Lc.M, a, b, c));
+  }
+  if (blockIdx.x == 0) coarse3_block(P, (T *)dsm);
+  grid.sync();
+  D3<const T> none{nullptr, 0, 0};
+  Coef<T> k0{};
+  for (int o = P.oc - 1; o >= P.om; o--) {
+    const Lev3<T> &L = P.lv[o], &Lc = P.lv[o + 1];
+    const int H = L.M / 2 + 1;
+    LOOPG(H, b3_jac_m1(cd(Lc.vG), cs(L.rM), L.vM, H, L.cMg, a, b, c));
+    LOOPG(H, b3_jac_m2(cs(L.rM), L.vM, H, L.cMg, a, b, c));
+    LOOPG(H, b3_jac_r1(cs(L.vM), cs(L.rR), L.vR, H, L.cR1, a, b, c));
+    LOOPG(H, b3_jac_r2(cs(L.rR), L.vR, H, L.cR2, a, b, c));
+    LOOPG(H, (b3_jac_g1<T, 2, false>(cs(L.vR), cd(L.rG), none, none, L.vG, L.M, H, L.cG, k0, a, b, c)));
+    LOOPG(H, (b3_jac_g2<T, 2, false>(cd(L.rG), none, none, cd(L.vG), L.vG, L.M, H, L.cG, k0, a, b, c)));
+  }
+#undef LOOPG
+}
+
 // ================================================================ launchers
 // grid.z covers the half-index planes [c0, c1) (c1 = -1: all H).
 static inline dim3 grid3(int H, int nz) { return dim3((H + 31) / 32, (H + 7) / 8, nz); }
@@ -625,5 +782,60 @@ void lv3_coarse(const Lev3<T> *d_lev, int oc, int k, int *counter, cudaStream_t 
 
 INSTL(float)
 INSTL(double)
+
+
+// Octaves om .. k-1 in one cooperative launch (om <= oc; oc >= 1).  Returns
+// false (nothing launched) when the tail does not fit.
+template <class T>
+bool lv3_tail(const Lev3<T> *h_lev, int om, int oc, int k, int *counter, cudaStream_t st) {
+  if (k > 20 || om < 1 || om > oc || oc >= k) return false;
+  Tail3<T> P;
+  for (int o = 0; o < k; o++) P.lv[o] = h_lev[o];
+  P.om = om;
+  P.oc = oc;
+  P.k = k;
+  P.counter = counter;
+  static unsigned long long *dbg = nullptr;
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  cudaStreamIsCapturing(st, &cap);
+  const bool debug = getenv("MG_TAIL_DEBUG") != nullptr && cap == cudaStreamCaptureStatusNone;
+  if (debug && !dbg) cudaMalloc(&dbg, 256 * sizeof(unsigned long long));
+  P.dbg = debug ? dbg : nullptr;
+  size_t elems = 0;
+  for (int o = oc; o + 1 < k; o++) {
+    const size_t H = h_lev[o].M / 2 + 1;
+    elems += 14 * H * H * H;
+  }
+  const size_t bytes = elems * sizeof(T);
+  if (bytes > 200 * 1024) return false;
+  if (cudaFuncSetAttribute(k3l_tail<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes) != cudaSuccess)
+    return false;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(sms);
+  cfg.blockDim = dim3(512);
+  cfg.dynamicSmemBytes = bytes;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeCooperative;
+  at[0].val.cooperative = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  const bool ok = cudaLaunchKernelEx(&cfg, k3l_tail<T>, P) == cudaSuccess;
+  if (debug && ok) {
+    unsigned long long h[256] = {};
+    cudaMemcpyAsync(h, dbg, sizeof h, cudaMemcpyDeviceToHost, st);
+    cudaStreamSynchronize(st);
+    fprintf(stderr, "[tail] CTA0 coarse phases (us):");
+    for (int i = 1; i < 64 && h[i] > h[0] && h[i] - h[0] < 1000000000ull; i++)
+      fprintf(stderr, " %.2f", (h[i] - h[i - 1]) * 1e-3);
+    fprintf(stderr, "\n");
+  }
+  return ok;
+}
+template bool lv3_tail<float>(const Lev3<float> *, int, int, int, int *, cudaStream_t);
+template bool lv3_tail<double>(const Lev3<double> *, int, int, int, int *, cudaStream_t);
 
 }  // namespace mg

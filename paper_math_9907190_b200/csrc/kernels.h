@@ -35,6 +35,10 @@ struct Lev2 {
 // the coarsest step, the Jacobi steps back up to v_A(oc).
 template <class T>
 void launch2_coarse(const Lev2<T> *d_lev, int oc, int k, int *counter, cudaStream_t st);
+// Octaves om .. oc-1 grid-wide and oc .. k-1 in one CTA's shared memory, one
+// cooperative launch (h_lev: host copy of the descriptors).  false: not launched.
+template <class T>
+bool launch2_tail(const Lev2<T> *h_lev, int om, int oc, int k, int *counter, cudaStream_t st);
 
 // TMA tile kernels (k2f.cu); every pointer/pitch must be 16-byte aligned.
 // Rows2: the output rows a launch writes and the local allocations of its
@@ -156,6 +160,10 @@ struct Lev3 {
 };
 template <class T>
 void lv3_coarse(const Lev3<T> *d_lev, int oc, int k, int *counter, cudaStream_t st);
+// Octaves om .. oc-1 grid-wide and oc .. k-1 in one CTA's shared memory, one
+// cooperative launch (h_lev: host copy of the descriptors).  false: not launched.
+template <class T>
+bool lv3_tail(const Lev3<T> *h_lev, int om, int oc, int k, int *counter, cudaStream_t st);
 
 // Sublattice level kernels (k3l.cu).  [c0, c1): the half-index planes
 // (2x2x2 blocks; for rest_mg the G(2s) planes) a launch writes; c1 = -1: all.

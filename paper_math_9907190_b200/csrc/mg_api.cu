@@ -22,7 +22,10 @@ struct Impl2 : ImplBase {
   std::vector<T> cD, cA;   // Jacobi coefficients per octave
   bool use_fast = false;   // TMA tile kernels for the large levels
   int oc = 1;              // first octave handled by the single-CTA coarse kernel
+  int om = 1;              // first octave of the cooperative tail kernel (om <= oc)
+  bool use_tail = false;
   Lev2<T> *d_lev = nullptr;
+  std::vector<Lev2<T>> h_lev;   // host copy of the level descriptors (tail kernel parameters)
   explicit Impl2(const mg_solver *sv) : s(sv), k(sv->k), n(sv->cfg.n), pitch(sv->pitch) {}
   bool fast() const override { return use_fast; }
 
@@ -100,6 +103,18 @@ struct Impl2 : ImplBase {
     cudaError_t st = dalloc(&q, sizeof(Lev2<T>) * k);
     if (st) return st;
     d_lev = (Lev2<T> *)q;
+    h_lev = lv;
+    // cooperative tail: octaves with M <= MG_TAIL_M2 in one launch; off by
+    // default in 2D (measured on B200: no gain over the per-level kernels)
+    int tm = 0;
+    if (const char *e = getenv("MG_TAIL_M2")) tm = atoi(e);
+    om = oc;
+    for (int o = 1; o < oc; o++)
+      if (M[o] <= tm) {
+        om = o;
+        break;
+      }
+    use_tail = use_fast && tm > 0 && k <= 40;
     return cudaMemcpy(d_lev, lv.data(), sizeof(Lev2<T>) * k, cudaMemcpyHostToDevice);
   }
 
@@ -143,22 +158,15 @@ struct Impl2 : ImplBase {
     const T *uin = (const T *)u_in, *fe = (const T *)f_eff;
     STEP("desc_fine", 0, 1, w * (2 * Nl[0] + Nl[1]));
     fast2_desc_fine<T>(uin, fe, pitch, rD[0], M[0], s->cfg.order, coef, sink(), st);
-    for (int o = 0; o < oc; o++) {
+    auto descent = [&](int o) {
       if (o >= 1) {
         STEP("rest_ad", 2 * o, 1, w * (Nl[2 * o] + Nl[2 * o + 1]));
         fast2_rest_ad<T>(rA[o], rD[o], M[o], st);
       }
       STEP("rest_da", 2 * o + 1, 1, w * (Nl[2 * o + 1] + Nl[2 * o + 2]));
       fast2_rest_da<T>(rD[o], rA[o + 1], M[o + 1], st);
-    }
-    {
-      double b = 0;
-      for (int l = 2 * oc; l < L; l++) b += 5 * Nl[l];
-      b -= Nl[L - 1] + 2 * Nl[2 * oc];   // coarsest: 4 touches; r_A(oc): read twice, written outside
-      STEP("coarse", 2 * oc, 1, w * b);
-    }
-    launch2_coarse<T>(d_lev, oc, k, s->d_counter, st);
-    for (int o = oc - 1; o >= 0; o--) {
+    };
+    auto ascent = [&](int o) {
       STEP("jac_d", 2 * o + 1, 1, w * (Nl[2 * o + 2] + 2 * Nl[2 * o + 1]));
       fast2_jac_d<T>(vA[o + 1], rD[o], vD[o], M[o], cD[o], st);
       if (o >= 1) {
@@ -168,7 +176,32 @@ struct Impl2 : ImplBase {
         STEP("asc_fine", 0, 1, w * (Nl[1] + 3 * Nl[0]));
         fast2_asc_fine<T>(vD[0], uin, fe, pitch, (T *)u_out, M[0], s->cfg.order, cA[0], coef, st);
       }
+    };
+    const int od = use_tail ? om : oc;   // first octave not run by per-level kernels
+    for (int o = 0; o < od; o++) descent(o);
+    bool tail_done = false;
+    if (use_tail) {
+      double b = 0;
+      for (int l = 2 * om; l < L; l++) b += 5 * Nl[l];
+      b -= Nl[L - 1] + 2 * Nl[2 * om];
+      STEP("tail", 2 * om, 1, w * b);
+      tail_done = launch2_tail<T>(h_lev.data(), om, oc, k, s->d_counter, st);
+      if (!tail_done) {
+        static bool warned = false;
+        if (!warned) fprintf(stderr, "[mg] cooperative tail kernel not launched; per-level kernels instead\n");
+        warned = true;
+      }
     }
+    if (!tail_done) {
+      for (int o = od; o < oc; o++) descent(o);
+      double b = 0;
+      for (int l = 2 * oc; l < L; l++) b += 5 * Nl[l];
+      b -= Nl[L - 1] + 2 * Nl[2 * oc];   // coarsest: 4 touches; r_A(oc): read twice, written outside
+      STEP("coarse", 2 * oc, 1, w * b);
+      launch2_coarse<T>(d_lev, oc, k, s->d_counter, st);
+      for (int o = oc - 1; o >= od; o--) ascent(o);
+    }
+    for (int o = od - 1; o >= 0; o--) ascent(o);
   }
   void enqueue_final_norm(void *u, const void *f_eff, cudaStream_t st) override {
     if (use_fast) {
@@ -189,7 +222,11 @@ struct Impl2 : ImplBase {
     launch2_norm<T>(D2<const T>{(const T *)x, pitch}, M[0], mx, ss, st);
   }
   int launches_per_cycle() const override {
-    if (use_fast) return 1 + (oc - 1) + oc + 1 + oc + oc;
+    if (use_fast) {
+      const int od = use_tail ? om : oc;
+      // desc_fine, rest_ad (o >= 1) + rest_da per descent octave, tail or coarse, jac_d + jac_a/asc per ascent octave
+      return 1 + (od - 1) + od + 1 + 2 * od + (use_tail ? 0 : 3 * (oc - od));
+    }
     int c = 1;                               // desc fine
     for (int o = 0; o + 1 < k; o++) c += (o >= 1) + 1;
     c += 1;                                  // coarsest
@@ -233,7 +270,10 @@ struct Impl3 : ImplBase {
   std::vector<T> cMg, cR1, cR2, cG;
   bool use_fast = false;   // TMA plane kernels for the finest octave
   int oc = 1;              // first octave run by the single-CTA coarse kernel
+  int om = 1;              // first octave of the cooperative tail kernel (om <= oc)
+  bool use_tail = false;
   Lev3<T> *d_lev = nullptr;
+  std::vector<Lev3<T>> h_lev;   // host copy of the level descriptors (tail kernel parameters)
   explicit Impl3(const mg_solver *sv) : s(sv), k(sv->k), n(sv->cfg.n), pitch(sv->pitch) {}
   bool fast() const override { return use_fast; }
   int64_t pitch_for(int64_t cnt) const { return round_up(cnt, 128 / (int64_t)sizeof(T)); }
@@ -332,6 +372,17 @@ struct Impl3 : ImplBase {
     cudaError_t st = dalloc(&q, sizeof(Lev3<T>) * k);
     if (st) return st;
     d_lev = (Lev3<T> *)q;
+    h_lev = lv;
+    // cooperative tail: octaves with M <= MG_TAIL_M3 (default 64) in one launch
+    int tm = 64;
+    if (const char *e = getenv("MG_TAIL_M3")) tm = atoi(e);
+    om = oc;
+    for (int o = 1; o < oc; o++)
+      if (M[o] <= tm) {
+        om = o;
+        break;
+      }
+    use_tail = use_fast && tm > 0 && k <= 20;
     return cudaMemcpy(d_lev, lv.data(), sizeof(Lev3<T>) * k, cudaMemcpyHostToDevice);
   }
 
@@ -400,7 +451,7 @@ struct Impl3 : ImplBase {
     void *u = const_cast<void *>(u_in);
     STEP("desc_fine", 0, 1, w * (2 * Nl[0] + Nl[1]));
     desc_fine(u, f_eff, st);
-    for (int o = 0; o < oc; o++) {
+    auto descent = [&](int o) {
       int g = 3 * o;
       if (o >= 1) {
         STEP("rest_gr", g, 1, w * (Nl[g] + Nl[g + 1]));
@@ -413,15 +464,8 @@ struct Impl3 : ImplBase {
       STEP("rest_mg", g + 2, 1, w * (Nl[g + 2] + Nl[g + 3]));
       if (gen2s) sub3_rest_mg(rM[o], rG[o + 1], M[o + 1], st);
       else lv3_rest_mg<T>(rM[o], rG[o + 1], M[o + 1], st);
-    }
-    {
-      double b = 0;
-      for (int l = 3 * oc; l < L; l++) b += 5 * Nl[l];
-      b -= Nl[L - 1] + 2 * Nl[3 * oc];
-      STEP("coarse", 3 * oc, 1, w * b);
-    }
-    lv3_coarse<T>(d_lev, oc, k, s->d_counter, st);
-    for (int o = oc - 1; o >= 0; o--) {
+    };
+    auto ascent = [&](int o) {   // o >= 1
       int g = 3 * o;
       STEP("jac_m", g + 2, gen2s ? 1 : 2, w * (Nl[g + 3] + 2 * Nl[g + 2]));
       if (gen2s) sub3_jac_m(vG[o + 1], rM[o], vM[o], M[o], cMg[o], st);
@@ -429,15 +473,51 @@ struct Impl3 : ImplBase {
       STEP("jac_r", g + 1, gen2s ? 1 : 2, w * (Nl[g + 2] + 2 * Nl[g + 1]));
       if (gen2s) sub3_jac_r(vM[o], rR[o], vR[o], M[o], cR1[o], cR2[o], st);
       else lv3_jac_r<T>(vM[o], rR[o], vR[o], M[o], cR1[o], cR2[o], st);
+      if (gen2) {
+        STEP("jac_g", g, 1, w * (Nl[g + 1] + 2 * Nl[g]));
+        fast3p_jac_g<T>(vR[o], rG[o], vG[o], M[o], cG[o], st);
+      } else {
+        STEP("jac_g", g, 2, w * (Nl[g + 1] + 2 * Nl[g]));
+        lv3_jac_g<T>(vR[o], rG[o], vG[o], M[o], cG[o], st);
+      }
+    };
+    const int od = use_tail ? om : oc;   // first octave not run by per-level kernels
+    for (int o = 0; o < od; o++) descent(o);
+    bool tail_done = false;
+    if (use_tail) {
+      double b = 0;
+      for (int l = 3 * om; l < L; l++) b += 5 * Nl[l];
+      b -= Nl[L - 1] + 2 * Nl[3 * om];
+      STEP("tail", 3 * om, 1, w * b);
+      tail_done = lv3_tail<T>(h_lev.data(), om, oc, k, s->d_counter, st);
+      if (!tail_done) {
+        static bool warned = false;
+        if (!warned) fprintf(stderr, "[mg] cooperative tail kernel not launched; per-level kernels instead\n");
+        warned = true;
+      }
+    }
+    if (!tail_done) {
+      for (int o = od; o < oc; o++) descent(o);
+      double b = 0;
+      for (int l = 3 * oc; l < L; l++) b += 5 * Nl[l];
+      b -= Nl[L - 1] + 2 * Nl[3 * oc];
+      STEP("coarse", 3 * oc, 1, w * b);
+      lv3_coarse<T>(d_lev, oc, k, s->d_counter, st);
+      for (int o = oc - 1; o >= od && o >= 1; o--) ascent(o);
+    }
+    for (int o = od - 1; o >= 0; o--) {
       if (o >= 1) {
-        if (gen2) {
-          STEP("jac_g", g, 1, w * (Nl[g + 1] + 2 * Nl[g]));
-          fast3p_jac_g<T>(vR[o], rG[o], vG[o], M[o], cG[o], st);
-        } else {
-          STEP("jac_g", g, 2, w * (Nl[g + 1] + 2 * Nl[g]));
-          lv3_jac_g<T>(vR[o], rG[o], vG[o], M[o], cG[o], st);
-        }
-      } else if (!getenv("MG_ASC3_DIRECT") && ((uintptr_t)u & 15) == 0 && ((uintptr_t)f_eff & 15) == 0 &&
+        ascent(o);
+        continue;
+      }
+      int g = 3 * o;
+      STEP("jac_m", g + 2, gen2s ? 1 : 2, w * (Nl[g + 3] + 2 * Nl[g + 2]));
+      if (gen2s) sub3_jac_m(vG[o + 1], rM[o], vM[o], M[o], cMg[o], st);
+      else lv3_jac_m<T>(vG[o + 1], rM[o], vM[o], M[o], cMg[o], st);
+      STEP("jac_r", g + 1, gen2s ? 1 : 2, w * (Nl[g + 2] + 2 * Nl[g + 1]));
+      if (gen2s) sub3_jac_r(vM[o], rR[o], vR[o], M[o], cR1[o], cR2[o], st);
+      else lv3_jac_r<T>(vM[o], rR[o], vR[o], M[o], cR1[o], cR2[o], st);
+      if (!getenv("MG_ASC3_DIRECT") && ((uintptr_t)u & 15) == 0 && ((uintptr_t)f_eff & 15) == 0 &&
                  ((uintptr_t)u_out & 15) == 0) {
         STEP("asc_fine", 0, 1, w * (Nl[1] + 3 * Nl[0]));
         fast3_asc_fine<T>(vR[0], (const T *)u, (const T *)f_eff, pitch, (T *)u_out, M[0], s->cfg.order, cG[0], coef,
@@ -467,7 +547,13 @@ struct Impl3 : ImplBase {
       for (int o = 0; o < oc; o++) c += (o >= 1) + 2;
       c += 1;
       const bool gen2 = getenv("MG_K3_GEN1") == nullptr, gen2s = gen2 && sizeof(T) == 8;
-      for (int o = oc - 1; o >= 0; o--) c += (gen2s ? 2 : 4) + (o >= 1 ? (gen2 ? 1 : 2) : 1);
+      const int od = use_tail ? om : oc;
+      c = 1;
+      for (int o = 0; o < od; o++) c += (o >= 1) + 2;
+      c += 1;   // tail or coarse
+      if (!use_tail)
+        for (int o = oc - 1; o >= od; o--) c += (gen2s ? 2 : 4) + (gen2 ? 1 : 2);
+      for (int o = od - 1; o >= 0; o--) c += (gen2s ? 2 : 4) + (o >= 1 ? (gen2 ? 1 : 2) : 1);
       return c;
     }
     for (int o = k - 2; o >= 0; o--) c += 2 + 2 + ((o >= 1) ? 2 : 3);
