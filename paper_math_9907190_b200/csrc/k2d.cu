@@ -558,7 +558,7 @@ void launch2_asc_fine(const S2<T> &vd, const D2<T> &u, const D2<const T> &f, con
 
 template <class T>
 void launch2_coarse(const Lev2<T> *d_lev, int oc, int k, int *counter, cudaStream_t st) {
-  static const bool global = getenv("MG_COARSE_GLOBAL") != nullptr;
+  static const bool global = env_flag("MG_COARSE_GLOBAL");
   if (!global && oc >= 1 && k <= 32) {
     size_t elems = 0;
     for (int o = oc; o + 1 < k; o++) {

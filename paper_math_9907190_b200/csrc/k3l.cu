@@ -755,7 +755,7 @@ void lv3_asc_fine(const S3<T> &vr, const D3<T> &u_old, const D3<const T> &f, con
 
 template <class T>
 void lv3_coarse(const Lev3<T> *d_lev, int oc, int k, int *counter, cudaStream_t st) {
-  static const bool global = getenv("MG_COARSE_GLOBAL") != nullptr;
+  static const bool global = env_flag("MG_COARSE_GLOBAL");
   if (!global && oc >= 1 && k <= 32) {
     int Ms[32];
     for (int o = 0; o < k; o++) Ms[o] = 1 << (k - o);   // M of octave o for n = 2^k + 1
@@ -798,7 +798,7 @@ bool lv3_tail(const Lev3<T> *h_lev, int om, int oc, int k, int *counter, cudaStr
   static unsigned long long *dbg = nullptr;
   cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
   cudaStreamIsCapturing(st, &cap);
-  const bool debug = getenv("MG_TAIL_DEBUG") != nullptr && cap == cudaStreamCaptureStatusNone;
+  const bool debug = env_flag("MG_TAIL_DEBUG") && cap == cudaStreamCaptureStatusNone;
   if (debug && !dbg) cudaMalloc(&dbg, 256 * sizeof(unsigned long long));
   P.dbg = debug ? dbg : nullptr;
   size_t elems = 0;

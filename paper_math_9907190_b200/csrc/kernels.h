@@ -1,9 +1,17 @@
 // kernels.h -- internal launcher interface between the host plan (mg_api.cpp)
 // and the sm_100a kernels (k2d.cu, k3d.cu).  Not part of the public ABI.
 #pragma once
+#include <cstdlib>
+
 #include "common.cuh"
 
 namespace mg {
+
+// A boolean environment switch: set and not "0".
+inline bool env_flag(const char *name) {
+  const char *e = std::getenv(name);
+  return e && *e && !(e[0] == '0' && e[1] == 0);
+}
 
 // ----------------------------------------------------------------- 2D
 template <class T>
@@ -145,10 +153,15 @@ cudaError_t fast3p_jac_g(const S3<T> &vr, const D3<T> &r, const D3<T> &v, int M,
 // of each Jacobi level in one pass).
 cudaError_t fast3s_rest_rm(const S3<double> &rr, const S3<double> &rm, int M, cudaStream_t st);
 cudaError_t fast3s_rest_mg(const S3<double> &rm, const D3<double> &g2, int Mc, cudaStream_t st);
+// R(s) -> M(s) -> G(2s) in one pass (r_M written, not re-read): rest_rm and rest_mg fused.
+cudaError_t fast3s_rest_rmg(const S3<double> &rr, const S3<double> &rm, const D3<double> &g2, int M, cudaStream_t st);
 cudaError_t fast3s_jac_m(const D3<double> &vc, const S3<double> &r, const S3<double> &v, int M, double cc,
                          cudaStream_t st);
 cudaError_t fast3s_jac_r(const S3<double> &vm, const S3<double> &r, const S3<double> &v, int M, double c1, double c2,
                          cudaStream_t st);
+// G(2s) -> M(s) -> R(s) in one pass (v_M(s) stays on chip): jac_m and jac_r fused.
+cudaError_t fast3s_jac_mr(const D3<double> &vc, const S3<double> &rm, const S3<double> &rr, const S3<double> &v, int M,
+                          double cm, double c1, double c2, cudaStream_t st);
 
 // Per-octave level descriptors for the 3D single-CTA coarse kernel.
 template <class T>

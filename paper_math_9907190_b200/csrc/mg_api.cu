@@ -69,7 +69,7 @@ struct Impl2 : ImplBase {
     coef.invh2 = (T)((double)(n - 1) * (double)(n - 1));
     coef.c6 = (T)((double)(n - 1) * (double)(n - 1) / 6.0);
     // TMA needs 16-byte row strides on the caller's arrays (and on ours)
-    use_fast = ((pitch * (int64_t)sizeof(T)) % 16 == 0) && !getenv("MG_FORCE_REF");
+    use_fast = ((pitch * (int64_t)sizeof(T)) % 16 == 0) && !env_flag("MG_FORCE_REF");
     if (!use_fast) {
       int64_t ps = pitch_for(n);
       void *q;
@@ -252,6 +252,16 @@ static void sub3_jac_r(const S3<double> &vm, const S3<double> &r, const S3<doubl
                        cudaStream_t st) {
   fast3s_jac_r(vm, r, v, M, c1, c2, st);
 }
+static void sub3_jac_mr(const D3<double> &vc, const S3<double> &rm, const S3<double> &rr, const S3<double> &v, int M,
+                        double cm, double c1, double c2, cudaStream_t st) {
+  fast3s_jac_mr(vc, rm, rr, v, M, cm, c1, c2, st);
+}
+static void sub3_jac_mr(const D3<float> &, const S3<float> &, const S3<float> &, const S3<float> &, int, float, float,
+                        float, cudaStream_t) {}
+static void sub3_rest_rmg(const S3<double> &rr, const S3<double> &rm, const D3<double> &g2, int M, cudaStream_t st) {
+  fast3s_rest_rmg(rr, rm, g2, M, st);
+}
+static void sub3_rest_rmg(const S3<float> &, const S3<float> &, const D3<float> &, int, cudaStream_t) {}
 static void sub3_rest_rm(const S3<float> &, const S3<float> &, int, cudaStream_t) {}
 static void sub3_rest_mg(const S3<float> &, const D3<float> &, int, cudaStream_t) {}
 static void sub3_jac_m(const D3<float> &, const S3<float> &, const S3<float> &, int, float, cudaStream_t) {}
@@ -341,7 +351,7 @@ struct Impl3 : ImplBase {
     }
     coef.invh2 = (T)((double)(n - 1) * (double)(n - 1));
     coef.c6 = (T)((double)(n - 1) * (double)(n - 1) / 6.0);
-    use_fast = ((pitch * (int64_t)sizeof(T)) % 16 == 0) && !getenv("MG_FORCE_REF");
+    use_fast = ((pitch * (int64_t)sizeof(T)) % 16 == 0) && !env_flag("MG_FORCE_REF");
     int thresh = 16;
     if (const char *e = getenv("MG_COARSE_M3")) thresh = atoi(e);
     oc = k - 1;
@@ -446,9 +456,10 @@ struct Impl3 : ImplBase {
   void enqueue_fast(const void *u_in, void *u_out, const void *f_eff, cudaStream_t st, Prof *prof) {
     const double w = sizeof(T);
     const int L = 3 * k - 2;
-    static const bool gen2 = getenv("MG_K3_GEN1") == nullptr;   // plane pipelines for the G(s) levels
+    static const bool gen2 = !env_flag("MG_K3_GEN1");   // plane pipelines for the G(s) levels
     const bool gen2s = gen2 && sizeof(T) == 8;                    // and for the sublattice levels (fp64)
     void *u = const_cast<void *>(u_in);
+    static const bool fuse_rmg = !getenv("MG_K3_RMG") || atoi(getenv("MG_K3_RMG")) != 0;
     STEP("desc_fine", 0, 1, w * (2 * Nl[0] + Nl[1]));
     desc_fine(u, f_eff, st);
     auto descent = [&](int o) {
@@ -458,6 +469,11 @@ struct Impl3 : ImplBase {
         if (gen2) fast3p_rest_gr<T>(rG[o], rR[o], M[o], st);
         else lv3_rest_gr<T>(rG[o], rR[o], M[o], st);
       }
+      if (gen2s && fuse_rmg) {   // R(s) -> M(s) -> G(2s) in one pass (r_M written, not re-read)
+        STEP("rest_rmg", g + 1, 1, w * (Nl[g + 1] + Nl[g + 2] + Nl[g + 3]));
+        sub3_rest_rmg(rR[o], rM[o], rG[o + 1], M[o], st);
+        return;
+      }
       STEP("rest_rm", g + 1, 1, w * (Nl[g + 1] + Nl[g + 2]));
       if (gen2s) sub3_rest_rm(rR[o], rM[o], M[o], st);
       else lv3_rest_rm<T>(rR[o], rM[o], M[o], st);
@@ -465,14 +481,27 @@ struct Impl3 : ImplBase {
       if (gen2s) sub3_rest_mg(rM[o], rG[o + 1], M[o + 1], st);
       else lv3_rest_mg<T>(rM[o], rG[o + 1], M[o + 1], st);
     };
-    auto ascent = [&](int o) {   // o >= 1
+    // G(2s) -> M(s) -> R(s): one fused pass (v_M(s) stays on chip) or the two level kernels.
+    // Measured on B200: the fused pass wins on the octaves o >= 1 (2 launches -> 1) but loses at
+    // o = 0 (0.41 vs 0.39 ms: its 29 x 13 core tile recomputes 26 % ring and is issue-bound there).
+    static const bool fuse_mr = !env_flag("MG_K3_NOFUSE");
+    auto jac_mr = [&](int o) {
       int g = 3 * o;
+      if (gen2s && fuse_mr && o >= 1) {
+        STEP("jac_mr", g + 1, 1, w * (Nl[g + 3] + Nl[g + 2] + 2 * Nl[g + 1]));
+        sub3_jac_mr(vG[o + 1], rM[o], rR[o], vR[o], M[o], cMg[o], cR1[o], cR2[o], st);
+        return;
+      }
       STEP("jac_m", g + 2, gen2s ? 1 : 2, w * (Nl[g + 3] + 2 * Nl[g + 2]));
       if (gen2s) sub3_jac_m(vG[o + 1], rM[o], vM[o], M[o], cMg[o], st);
       else lv3_jac_m<T>(vG[o + 1], rM[o], vM[o], M[o], cMg[o], st);
       STEP("jac_r", g + 1, gen2s ? 1 : 2, w * (Nl[g + 2] + 2 * Nl[g + 1]));
       if (gen2s) sub3_jac_r(vM[o], rR[o], vR[o], M[o], cR1[o], cR2[o], st);
       else lv3_jac_r<T>(vM[o], rR[o], vR[o], M[o], cR1[o], cR2[o], st);
+    };
+    auto ascent = [&](int o) {   // o >= 1
+      int g = 3 * o;
+      jac_mr(o);
       if (gen2) {
         STEP("jac_g", g, 1, w * (Nl[g + 1] + 2 * Nl[g]));
         fast3p_jac_g<T>(vR[o], rG[o], vG[o], M[o], cG[o], st);
@@ -511,13 +540,8 @@ struct Impl3 : ImplBase {
         continue;
       }
       int g = 3 * o;
-      STEP("jac_m", g + 2, gen2s ? 1 : 2, w * (Nl[g + 3] + 2 * Nl[g + 2]));
-      if (gen2s) sub3_jac_m(vG[o + 1], rM[o], vM[o], M[o], cMg[o], st);
-      else lv3_jac_m<T>(vG[o + 1], rM[o], vM[o], M[o], cMg[o], st);
-      STEP("jac_r", g + 1, gen2s ? 1 : 2, w * (Nl[g + 2] + 2 * Nl[g + 1]));
-      if (gen2s) sub3_jac_r(vM[o], rR[o], vR[o], M[o], cR1[o], cR2[o], st);
-      else lv3_jac_r<T>(vM[o], rR[o], vR[o], M[o], cR1[o], cR2[o], st);
-      if (!getenv("MG_ASC3_DIRECT") && ((uintptr_t)u & 15) == 0 && ((uintptr_t)f_eff & 15) == 0 &&
+      jac_mr(o);
+      if (!env_flag("MG_ASC3_DIRECT") && ((uintptr_t)u & 15) == 0 && ((uintptr_t)f_eff & 15) == 0 &&
                  ((uintptr_t)u_out & 15) == 0) {
         STEP("asc_fine", 0, 1, w * (Nl[1] + 3 * Nl[0]));
         fast3_asc_fine<T>(vR[0], (const T *)u, (const T *)f_eff, pitch, (T *)u_out, M[0], s->cfg.order, cG[0], coef,
@@ -546,14 +570,17 @@ struct Impl3 : ImplBase {
       c = 1;
       for (int o = 0; o < oc; o++) c += (o >= 1) + 2;
       c += 1;
-      const bool gen2 = getenv("MG_K3_GEN1") == nullptr, gen2s = gen2 && sizeof(T) == 8;
+      const bool gen2 = !env_flag("MG_K3_GEN1"), gen2s = gen2 && sizeof(T) == 8;
+      const bool fz = gen2s && !env_flag("MG_K3_NOFUSE");
+      auto per_mr_o = [&](int o) { return gen2s ? (fz && o >= 1 ? 1 : 2) : 4; };
       const int od = use_tail ? om : oc;
+      const bool frmg = gen2s && (!getenv("MG_K3_RMG") || atoi(getenv("MG_K3_RMG")) != 0);
       c = 1;
-      for (int o = 0; o < od; o++) c += (o >= 1) + 2;
+      for (int o = 0; o < od; o++) c += (o >= 1) + (frmg ? 1 : 2);
       c += 1;   // tail or coarse
       if (!use_tail)
-        for (int o = oc - 1; o >= od; o--) c += (gen2s ? 2 : 4) + (gen2 ? 1 : 2);
-      for (int o = od - 1; o >= 0; o--) c += (gen2s ? 2 : 4) + (o >= 1 ? (gen2 ? 1 : 2) : 1);
+        for (int o = oc - 1; o >= od; o--) c += per_mr_o(o) + (gen2 ? 1 : 2);
+      for (int o = od - 1; o >= 0; o--) c += per_mr_o(o) + (o >= 1 ? (gen2 ? 1 : 2) : 1);
       return c;
     }
     for (int o = k - 2; o >= 0; o--) c += 2 + 2 + ((o >= 1) ? 2 : 3);

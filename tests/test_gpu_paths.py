@@ -1,0 +1,75 @@
+"""Every alternative code path of the library is bit-identical to the oracle.
+
+The library chooses between kernel variants once per process from environment
+switches (fused vs separate level passes, cooperative tail on/off, first- vs
+second-generation 3D kernels, the reference kernels).  Each case below runs a
+small problem in a fresh subprocess with one switch set and asserts the
+iterates and the residual history equal the CPU oracle's bit for bit.
+"""
+import json
+import os
+import subprocess
+import sys
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+CHILD = r"""
+import json, sys
+import numpy as np
+sys.path.insert(0, {root!r})
+import oracle
+from paper_math_9907190_b200 import workloads as W
+from paper_math_9907190_b200.mg import Solver
+import torch
+dim, n, order, dtype = {dim}, {n}, {order}, np.{dtype}
+p = (1.052,) if dim == 2 else (1.11, 1.42, 1.08, 0.99)
+if order == 4 and dim == 2:
+    p = (1.20,)
+f = W.random_field(dim, n, seed=7).astype(dtype)
+u0 = (W.random_field(dim, n, seed=8) * 0.1).astype(dtype)
+s = Solver(dim, n, order=order, p=p, dtype=torch.float64 if dtype == np.float64 else torch.float32)
+u = s.alloc(u0)
+ft = s.alloc(f)
+h = s.vcycle(u, ft, 3, hist=True)
+ug = s.view(u).cpu().numpy()
+uo = u0.copy()
+ho = oracle.vcycle(uo, f, p, 3, order=order, hist=True)
+print(json.dumps({{"bitwise": bool(np.array_equal(ug, uo)), "hist": bool(np.array_equal(h, ho)),
+                  "rel": float(np.max(np.abs(ug.astype(np.float64) - uo)) / np.max(np.abs(uo)))}}))
+"""
+
+CASES = [
+    # (env, dim, n, order, dtype)
+    ({}, 3, 129, 2, "float64"),
+    ({"MG_K3_RMG": "0"}, 3, 129, 2, "float64"),
+    ({"MG_K3_NOFUSE": "1"}, 3, 129, 2, "float64"),
+    ({"MG_TAIL_M3": "0"}, 3, 129, 2, "float64"),
+    ({"MG_TAIL_M3": "128"}, 3, 129, 2, "float64"),
+    ({"MG_K3_GEN1": "1"}, 3, 65, 2, "float64"),
+    ({"MG_FORCE_REF": "1"}, 3, 33, 2, "float64"),
+    ({"MG_COARSE_GLOBAL": "1", "MG_TAIL_M3": "0"}, 3, 65, 2, "float64"),
+    ({"MG_TAIL_M2": "128"}, 2, 513, 2, "float64"),
+    ({"MG_STAGES": "3"}, 2, 513, 2, "float64"),
+    ({"MG_COARSE_GLOBAL": "1"}, 2, 257, 2, "float64"),
+    ({"MG_FORCE_REF": "1"}, 2, 129, 4, "float64"),
+    ({"MG_PDL": "1"}, 2, 257, 2, "float64"),
+    ({"MG_PDL": "1"}, 3, 65, 2, "float64"),
+]
+
+
+@pytest.mark.parametrize("env,dim,n,order,dtype", CASES,
+                         ids=[f"{'+'.join(f'{k}={v}' for k, v in e.items()) or 'default'}-{d}d{n}o{o}"
+                              for e, d, n, o, _ in CASES])
+def test_path_is_bit_identical(env, dim, n, order, dtype):
+    code = CHILD.format(root=ROOT, dim=dim, n=n, order=order, dtype=dtype)
+    full_env = dict(os.environ)
+    full_env.update(env)
+    out = subprocess.run([sys.executable, "-c", code], env=full_env, capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stderr[-2000:]
+    res = json.loads(out.stdout.strip().splitlines()[-1])
+    assert res["bitwise"], res
+    assert res["hist"], res
