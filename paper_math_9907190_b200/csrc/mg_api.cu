@@ -459,7 +459,9 @@ struct Impl3 : ImplBase {
     static const bool gen2 = !env_flag("MG_K3_GEN1");   // plane pipelines for the G(s) levels
     const bool gen2s = gen2 && sizeof(T) == 8;                    // and for the sublattice levels (fp64)
     void *u = const_cast<void *>(u_in);
-    static const bool fuse_rmg = !getenv("MG_K3_RMG") || atoi(getenv("MG_K3_RMG")) != 0;
+    // fused octave passes: bit-identical, but no measurable gain in graph replay on B200 (A/B in
+    // DESIGN.md), so opt-in (MG_K3_FUSE=1)
+    static const bool fuse_rmg = env_flag("MG_K3_FUSE");
     STEP("desc_fine", 0, 1, w * (2 * Nl[0] + Nl[1]));
     desc_fine(u, f_eff, st);
     auto descent = [&](int o) {
@@ -484,7 +486,7 @@ struct Impl3 : ImplBase {
     // G(2s) -> M(s) -> R(s): one fused pass (v_M(s) stays on chip) or the two level kernels.
     // Measured on B200: the fused pass wins on the octaves o >= 1 (2 launches -> 1) but loses at
     // o = 0 (0.41 vs 0.39 ms: its 29 x 13 core tile recomputes 26 % ring and is issue-bound there).
-    static const bool fuse_mr = !env_flag("MG_K3_NOFUSE");
+    static const bool fuse_mr = env_flag("MG_K3_FUSE");
     auto jac_mr = [&](int o) {
       int g = 3 * o;
       if (gen2s && fuse_mr && o >= 1) {
@@ -571,10 +573,10 @@ struct Impl3 : ImplBase {
       for (int o = 0; o < oc; o++) c += (o >= 1) + 2;
       c += 1;
       const bool gen2 = !env_flag("MG_K3_GEN1"), gen2s = gen2 && sizeof(T) == 8;
-      const bool fz = gen2s && !env_flag("MG_K3_NOFUSE");
+      const bool fz = gen2s && env_flag("MG_K3_FUSE");
       auto per_mr_o = [&](int o) { return gen2s ? (fz && o >= 1 ? 1 : 2) : 4; };
       const int od = use_tail ? om : oc;
-      const bool frmg = gen2s && (!getenv("MG_K3_RMG") || atoi(getenv("MG_K3_RMG")) != 0);
+      const bool frmg = gen2s && env_flag("MG_K3_FUSE");
       c = 1;
       for (int o = 0; o < od; o++) c += (o >= 1) + (frmg ? 1 : 2);
       c += 1;   // tail or coarse

@@ -45,8 +45,8 @@ print(json.dumps({{"bitwise": bool(np.array_equal(ug, uo)), "hist": bool(np.arra
 CASES = [
     # (env, dim, n, order, dtype)
     ({}, 3, 129, 2, "float64"),
-    ({"MG_K3_RMG": "0"}, 3, 129, 2, "float64"),
-    ({"MG_K3_NOFUSE": "1"}, 3, 129, 2, "float64"),
+    ({"MG_K3_FUSE": "1"}, 3, 129, 2, "float64"),
+    ({"MG_K3_FUSE": "1"}, 3, 257, 2, "float64"),
     ({"MG_TAIL_M3": "0"}, 3, 129, 2, "float64"),
     ({"MG_TAIL_M3": "128"}, 3, 129, 2, "float64"),
     ({"MG_K3_GEN1": "1"}, 3, 65, 2, "float64"),
