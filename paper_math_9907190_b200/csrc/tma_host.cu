@@ -2,6 +2,8 @@
 // runtime's driver entry point; no link dependency on libcuda).
 #include <cudaTypedefs.h>
 
+#include <cstdlib>
+
 #include "tma.cuh"
 
 namespace mg {
@@ -18,6 +20,20 @@ static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   return fn;
 }
 
+// L2 sector promotion of the TMA loads (MG_L2_PROMO = 0 / 64 / 128 / 256).  Default none:
+// measured on B200 (interleaved A/B, tools/ab.py) 256 B promotion cost 1.2 % (3D) and 0.8 %
+// (2D) per cycle -- the halo boxes' edges pulled in sectors nobody reads.
+static CUtensorMapL2promotion l2_promotion() {
+  static const CUtensorMapL2promotion p = [] {
+    const char *e = getenv("MG_L2_PROMO");
+    const int v = e ? atoi(e) : 0;
+    return v == 0 ? CU_TENSOR_MAP_L2_PROMOTION_NONE
+                  : v == 64 ? CU_TENSOR_MAP_L2_PROMOTION_L2_64B
+                            : v == 128 ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B : CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
+  }();
+  return p;
+}
+
 bool encode_tmap(CUtensorMap *tm, const void *base, int esz, int rank, const uint64_t *dims, uint64_t pitch,
                  uint64_t plane, const uint32_t *box) {
   auto fn = encode_fn();
@@ -28,7 +44,7 @@ bool encode_tmap(CUtensorMap *tm, const void *base, int esz, int rank, const uin
   cuuint32_t estr[3] = {1, 1, 1};
   CUresult r = fn(tm, esz == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, rank,
                   const_cast<void *>(base), gdim, gstr, bdim, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                  CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                  CU_TENSOR_MAP_SWIZZLE_NONE, l2_promotion(), CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
 }
 
