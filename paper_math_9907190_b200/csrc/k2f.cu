@@ -95,7 +95,7 @@ __global__ void __launch_bounds__(Op::NT) tile_pipeline(const __grid_constant__ 
   if (threadIdx.x == 0)
     for (int j = 0; j + 1 < S; j++) {
       int tj = blockIdx.x + j * gridDim.x;
-      if (tj < ntiles) Op::issue(P, tj, smem + j * Op::STAGE, &bar[j]);
+      if (tj < ntiles) Op::issue(P, P.rev ? ntiles - 1 - tj : tj, smem + j * Op::STAGE, &bar[j]);
     }
   int i = 0;
   for (int t = blockIdx.x; t < ntiles; t += gridDim.x, i++) {
@@ -106,11 +106,11 @@ __global__ void __launch_bounds__(Op::NT) tile_pipeline(const __grid_constant__ 
         int sn = (i + S - 1) % S;   // consumed at iteration i-1 (synchronised below)
         // WAR on the slot is ordered by the __syncthreads that ended its last use
         // (no proxy fence: that would wait for the in-flight TMA loads)
-        Op::issue(P, tn, smem + sn * Op::STAGE, &bar[sn]);
+        Op::issue(P, P.rev ? ntiles - 1 - tn : tn, smem + sn * Op::STAGE, &bar[sn]);
       }
     }
     mbar_wait(&bar[st], (i / S) & 1);
-    Op::compute(P, t, smem + st * Op::STAGE, smem + S * Op::STAGE, acc);
+    Op::compute(P, P.rev ? ntiles - 1 - t : t, smem + st * Op::STAGE, smem + S * Op::STAGE, acc);
     __syncthreads();
   }
   Op::finish(P, acc);
@@ -139,6 +139,7 @@ struct OpDesc2Fine {
     CUtensorMap tu, tf;
     S2<T> out;
     int M, ntx, ntiles;
+    int rev;   // 1: tiles in descending order (Rows2::rev)
     Coef<T> k;
     NormSink ns;
     int ylo, yhi, yo, yh;   // output rows [ylo, yhi); TMA y = global y - yo (full rows) / - yh (half rows)
@@ -236,6 +237,7 @@ struct OpRest2AD {
     CUtensorMap tr;
     S2<T> out;
     int M, ntx, ntiles;
+    int rev;   // 1: tiles in descending order (Rows2::rev)
     int ylo, yhi, yo, yh;
   };
   using Acc = NoAcc;
@@ -282,6 +284,7 @@ struct OpRest2DA {
     CUtensorMap te, to;
     D2<T> out;
     int Mc, ntx, ntiles;
+    int rev;   // 1: tiles in descending order (Rows2::rev)
     int ylo, yhi, yo, yh;
   };
   using Acc = NoAcc;
@@ -343,6 +346,7 @@ struct OpJac2D {
     CUtensorMap tva, tro, tre;
     S2<T> v;
     int M, ntx, ntiles;
+    int rev;   // 1: tiles in descending order (Rows2::rev)
     T c;
     int ylo, yhi, yo, yh;
   };
@@ -445,6 +449,7 @@ struct OpJac2A {
     CUtensorMap tu, tf, tve, tvo;   // tu unused when !FINE; tf = f (FINE) or r_A
     D2<T> out;                      // u_new (FINE) or v_A
     int M, ntx, ntiles;
+    int rev;   // 1: tiles in descending order (Rows2::rev)
     T c;
     Coef<T> k;
     int ylo, yhi, yo, yh;
@@ -622,6 +627,7 @@ static cudaError_t desc_impl(const T *u, const T *f, int64_t pitch, const S2<T> 
   P.M = M;
   P.ntx = ntx;
   P.ntiles = ntx * nty;
+  P.rev = rw.rev;
   P.k = k;
   P.ns = ns;
   P.ylo = rw.ylo;
@@ -663,6 +669,7 @@ static cudaError_t jac_a_impl(const T *u, const T *f_or_r, int64_t pitch_u, int6
   P.M = M;
   P.ntx = ntx;
   P.ntiles = ntx * nty;
+  P.rev = rw.rev;
   P.c = c;
   P.k = k;
   P.ylo = rw.ylo;
@@ -714,6 +721,7 @@ cudaError_t fast2_rest_ad(const D2<T> &r, const S2<T> &d, int M, cudaStream_t st
   P.M = M;
   P.ntx = ntx;
   P.ntiles = ntx * nty;
+  P.rev = rw.rev;
   P.ylo = rw.ylo;
   P.yhi = yhi;
   P.yo = rw.fy0;
@@ -735,6 +743,7 @@ cudaError_t fast2_rest_da(const S2<T> &d, const D2<T> &r, int Mc, cudaStream_t s
   P.Mc = Mc;
   P.ntx = ntx;
   P.ntiles = ntx * nty;
+  P.rev = rw.rev;
   P.ylo = rw.ylo;
   P.yhi = yhi;
   P.yo = rw.fy0;
@@ -758,6 +767,7 @@ cudaError_t fast2_jac_d(const D2<T> &vc, const S2<T> &r, const S2<T> &v, int M, 
   P.M = M;
   P.ntx = ntx;
   P.ntiles = ntx * nty;
+  P.rev = rw.rev;
   P.c = c;
   P.ylo = rw.ylo;
   P.yhi = yhi;

@@ -52,6 +52,7 @@ bool launch2_tail(const Lev2<T> *h_lev, int om, int oc, int k, int *counter, cud
 // Rows2: the output rows a launch writes and the local allocations of its
 // inputs (multi-GPU slabs); the default (all -1 / 0) is the whole level.
 struct Rows2 {
+  bool rev = false;         // walk the tiles in descending order (reuse the L2-resident tail of the producer's output)
   int ylo = 0, yhi = -1;    // output rows [ylo, yhi) in the output array's row units (-1: all)
   int fy0 = 0, frows = -1;  // full-resolution inputs: global row of local row 0, local rows (-1: all)
   int hy0 = 0, hrows = -1;  // half-resolution inputs (E/O of D(s), A(2s))

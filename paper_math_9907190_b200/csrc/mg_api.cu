@@ -24,6 +24,7 @@ struct Impl2 : ImplBase {
   int oc = 1;              // first octave handled by the single-CTA coarse kernel
   int om = 1;              // first octave of the cooperative tail kernel (om <= oc)
   bool use_tail = false;
+  bool serp = !env_flag("MG_2D_NOSERP");   // serpentine tile order across passes
   Lev2<T> *d_lev = nullptr;
   std::vector<Lev2<T>> h_lev;   // host copy of the level descriptors (tail kernel parameters)
   explicit Impl2(const mg_solver *sv) : s(sv), k(sv->k), n(sv->cfg.n), pitch(sv->pitch) {}
@@ -157,24 +158,28 @@ struct Impl2 : ImplBase {
     const int L = 2 * k - 1;
     const T *uin = (const T *)u_in, *fe = (const T *)f_eff;
     STEP("desc_fine", 0, 1, w * (2 * Nl[0] + Nl[1]));
-    fast2_desc_fine<T>(uin, fe, pitch, rD[0], M[0], s->cfg.order, coef, sink(), st);
+    // Serpentine tile order: each pass starts where its producer finished,
+    // so the last ~100 MB the producer wrote are still in L2.
+    Rows2 fwd, bwd;
+    bwd.rev = serp;
+    fast2_desc_fine<T>(uin, fe, pitch, rD[0], M[0], s->cfg.order, coef, sink(), st, fwd);
     auto descent = [&](int o) {
       if (o >= 1) {
         STEP("rest_ad", 2 * o, 1, w * (Nl[2 * o] + Nl[2 * o + 1]));
-        fast2_rest_ad<T>(rA[o], rD[o], M[o], st);
+        fast2_rest_ad<T>(rA[o], rD[o], M[o], st, fwd);
       }
       STEP("rest_da", 2 * o + 1, 1, w * (Nl[2 * o + 1] + Nl[2 * o + 2]));
-      fast2_rest_da<T>(rD[o], rA[o + 1], M[o + 1], st);
+      fast2_rest_da<T>(rD[o], rA[o + 1], M[o + 1], st, bwd);
     };
     auto ascent = [&](int o) {
       STEP("jac_d", 2 * o + 1, 1, w * (Nl[2 * o + 2] + 2 * Nl[2 * o + 1]));
-      fast2_jac_d<T>(vA[o + 1], rD[o], vD[o], M[o], cD[o], st);
+      fast2_jac_d<T>(vA[o + 1], rD[o], vD[o], M[o], cD[o], st, fwd);
       if (o >= 1) {
         STEP("jac_a", 2 * o, 1, w * (Nl[2 * o + 1] + 2 * Nl[2 * o]));
-        fast2_jac_a<T>(vD[o], rA[o], vA[o], M[o], cA[o], st);
+        fast2_jac_a<T>(vD[o], rA[o], vA[o], M[o], cA[o], st, bwd);
       } else {
         STEP("asc_fine", 0, 1, w * (Nl[1] + 3 * Nl[0]));
-        fast2_asc_fine<T>(vD[0], uin, fe, pitch, (T *)u_out, M[0], s->cfg.order, cA[0], coef, st);
+        fast2_asc_fine<T>(vD[0], uin, fe, pitch, (T *)u_out, M[0], s->cfg.order, cA[0], coef, st, bwd);
       }
     };
     const int od = use_tail ? om : oc;   // first octave not run by per-level kernels

@@ -58,6 +58,7 @@ CASES = [
     ({"MG_FORCE_REF": "1"}, 2, 129, 4, "float64"),
     ({"MG_PDL": "1"}, 2, 257, 2, "float64"),
     ({"MG_PDL": "1"}, 3, 65, 2, "float64"),
+    ({"MG_2D_NOSERP": "1"}, 2, 513, 2, "float64"),
 ]
 
 

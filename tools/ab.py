@@ -19,13 +19,13 @@ import sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-def run(env_kv, workload, steps):
+def run(env_kv, workload, steps, dtype):
     env = dict(os.environ)
     for kv in env_kv.split():
         k, v = kv.split("=", 1)
         env[k] = v
     out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--workload", workload, "--steps",
-                          str(steps), "--warmup", "5", "--no-cpu", "--no-e2e"], env=env, capture_output=True,
+                          str(steps), "--warmup", "5", "--no-cpu", "--no-e2e", "--dtype", dtype], env=env, capture_output=True,
                          text=True, timeout=900)
     d = json.loads(out.stdout.strip().splitlines()[-1])
     return d["ms_per_step"], d["clocks"]["sm_mhz"]
@@ -38,11 +38,12 @@ def main():
     ap.add_argument("--workload", default="3d_513")
     ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--rounds", type=int, default=4)
+    ap.add_argument("--dtype", default="f64")
     args = ap.parse_args()
     res = {args.a: [], args.b: []}
     for _ in range(args.rounds):
         for arm in (args.a, args.b):
-            ms, mhz = run(arm, args.workload, args.steps)
+            ms, mhz = run(arm, args.workload, args.steps, args.dtype)
             res[arm].append(ms)
             print(f"[{arm}] {ms:.4f} ms  {mhz} MHz", flush=True)
     for arm, v in res.items():
