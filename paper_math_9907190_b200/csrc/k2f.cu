@@ -547,6 +547,7 @@ struct OpJac2A {
   static __device__ void finish(const Params &, Acc &) {}
 };
 
+
 // ================================================================= launch
 
 static int num_sms() {
@@ -775,6 +776,7 @@ cudaError_t fast2_jac_d(const D2<T> &vc, const S2<T> &r, const S2<T> &v, int M, 
   P.yh = rw.hy0;
   return run_staged<JacDS<T>::template op>(P, st);
 }
+
 
 #define INSTF(T)                                                                                                   \
   template cudaError_t fast2_desc_fine<T>(const T *, const T *, int64_t, const S2<T> &, int, int, const Coef<T> &, \

@@ -1,0 +1,389 @@
+// k2x.cu -- cross-cycle fusion in 2D: the finest ascent of
+// one V-cycle and the finest descent of the next in one pass over the grid.
+//
+//   ascent  (OpJac2A<FINE>): greens of A(1) from r(u_old) and v_D(1), then the
+//            D(1) nodes from the greens, u_new = u_old + v_A(1)  (P:57-60,
+//            Eajacr/Eajacb P:350-360);
+//   descent (OpDesc2Fine):   r = f - L u_new, Erest2r onto D(1),
+//            max|r| for the residual history.
+//
+// Separately the two passes read u and f twice per cycle (10 N words in all
+// per cycle); fused they read them once (8 N).  The tile
+// kernels of k2f.cu would need a 4-node halo for this (r_new needs u_new on
+// ring 1, u_new needs greens on ring 2, greens need u_old on ring 4), and
+// their shared-memory phases turned out instruction-bound.  This kernel is a
+// register pipeline instead: one warp streams down a strip of 56 output
+// columns (lane l owns the column pair x = x0 - 4 + 2l, the 4-column halo on
+// both sides is the outer lanes), one row per step, x neighbours by warp
+// shuffles, no shared memory and no barriers.  At input row j a step computes
+//     r_old(j-1) -> green(j-1) -> D node(j-2) -> u_new(j-2) -> r_new(j-3)
+// and, every second row, the Erest2r pair of rows (j-5, j-4).  Rows are
+// prefetched four steps ahead (plain 16/8-byte vector loads, 512 B per warp
+// row).  A strip is cut into row segments (9 rows of warm-up each) so that
+// the grid fills every SM once.  Same node formulas, same evaluation order:
+// bit-identical to the two separate passes.
+#include "kernels.h"
+#include "ops2.cuh"
+
+namespace mg {
+namespace xf {
+
+constexpr int SW = 56;    // output columns per strip: 32 lanes x 2 minus 2 x 4 halo
+constexpr int DEPTH = 8;  // rows in flight per warp (power of 2)
+
+template <class T>
+struct V2;
+template <>
+struct V2<double> {
+  using t = double2;
+};
+template <>
+struct V2<float> {
+  using t = float2;
+};
+
+template <class T>
+__device__ __forceinline__ T shup(T v) {   // value of lane - 1
+  return __shfl_up_sync(0xffffffffu, v, 1);
+}
+template <class T>
+__device__ __forceinline__ T shdn(T v) {   // value of lane + 1
+  return __shfl_down_sync(0xffffffffu, v, 1);
+}
+
+// per-lane asynchronous global -> shared copies (cp.async, sm_80+): the lane
+// later reads back only what it copied itself, so no barrier is involved
+template <int BYTES>
+__device__ __forceinline__ void cpa(void *s, const void *g) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(s);
+  if (BYTES == 16)
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(g) : "memory");
+  else
+    asm volatile("cp.async.ca.shared.global [%0], [%1], %2;\n" ::"r"(sa), "l"(g), "n"(BYTES) : "memory");
+}
+__device__ __forceinline__ void cpa_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cpa_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
+}
+
+// one grid row at the lane's pair: a = (x, y), b = (x+1, y), w = (x-1, y), e = (x+2, y)
+template <class T>
+struct Row {
+  T a, b, w, e;
+};
+template <class T>
+__device__ __forceinline__ Row<T> mkrow(T a, T b) {
+  return Row<T>{a, b, shup(b), shdn(a)};
+}
+
+template <class T>
+struct Pair {
+  T a, b;
+};
+
+template <class T>
+struct XParams {
+  const T *u, *f;     // u_old, f (row pitch `pitch`)
+  const T *ve, *vo;   // v_D(1), E and O (row pitch vp)
+  T *un;              // u_new (pitch)
+  T *re, *ro;         // the next cycle's r_D(1), E and O (pitch rp)
+  int64_t pitch, vp, rp;
+  int M, nstrips, seg;
+  T c;
+  Coef<T> k;
+  NormSink ns;
+};
+
+// prefetched inputs of one row
+template <class T>
+struct In {
+  T ua, ub, fa, fb, d;
+};
+
+// One warp's strip segment.  Pipeline state lives in 4-slot arrays indexed
+// by row & 3 (statically, the step body is unrolled 4 times), so nothing is
+// shifted between steps.  Loads are unconditional from clamped addresses:
+// rows outside [0, M] and columns outside [0, M] only feed nodes that are
+// not interior, whose results are all selected away (inside() is false).
+template <class T, int ORDER>
+struct Strip {
+  const T *pu, *pf, *pve, *pvo;
+  T *pun, *pre, *pro;
+  int64_t pitch, vp, rp;
+  Coef<T> k;
+  T c;
+  int x, xc, M, ys, ye;
+  bool ca, cb, outl;   // (x, y) / (x+1, y) interior columns; lane writes output
+  unsigned char *ring;  // this warp's DEPTH-slot input ring in shared memory, offset to the lane
+  Row<T> U[4];         // u_old
+  Pair<T> F[4];        // f
+  T Dv[4];             // v_D at the row's D node
+  Pair<T> RO[4];       // r(u_old)
+  T G[4];              // green value of the row
+  Row<T> N[4];         // u_new
+  Pair<T> R[4];        // r(u_new)
+  double mx;
+
+  __device__ __forceinline__ Strip(const XParams<T> &P, int x_, int ys_, int ye_, unsigned char *ring_) {
+    ring = ring_;
+    pu = P.u;
+    pf = P.f;
+    pve = P.ve;
+    pvo = P.vo;
+    pun = P.un;
+    pre = P.re;
+    pro = P.ro;
+    pitch = P.pitch;
+    vp = P.vp;
+    rp = P.rp;
+    k = P.k;
+    c = P.c;
+    M = P.M;
+    x = x_;
+    ys = ys_;
+    ye = ye_;
+    xc = min(max(x, 0), M);
+    ca = x >= 1 && x <= M - 1;
+    cb = x + 1 >= 1 && x + 1 <= M - 1;
+    const int lane = threadIdx.x & 31;
+    outl = lane >= 2 && lane < 30;
+#pragma unroll
+    for (int i = 0; i < 4; i++) {
+      U[i] = N[i] = Row<T>{0, 0, 0, 0};
+      F[i] = RO[i] = R[i] = Pair<T>{0, 0};
+      Dv[i] = G[i] = (T)0;
+    }
+    mx = 0.0;
+  }
+  __device__ __forceinline__ bool rin(int y) const { return (unsigned)(y - 1) < (unsigned)(M - 1); }
+
+  // slot layout: 32 u pairs, 32 f pairs, 32 v_D values (lane l at pair /
+  // value l); `ring` already points at the lane's u pair of slot 0
+  static constexpr int SLOT = 32 * 5 * sizeof(T), FO = 32 * 2 * sizeof(T), DO = 32 * 4 * sizeof(T);
+  // start the copies of row y into slot y % DEPTH (one commit group per row)
+  __device__ __forceinline__ void issue(int y) const {
+    const int yc = min(max(y, 0), M);
+    const int64_t o = (int64_t)yc * pitch + xc;
+    unsigned char *q = ring + (y & (DEPTH - 1)) * SLOT;
+    cpa<2 * sizeof(T)>(q, pu + o);
+    cpa<2 * sizeof(T)>(q + FO, pf + o);
+    // the D(1) node of row y in the pair: (x, y) on even rows (E), (x+1, y) on odd rows (O)
+    cpa<sizeof(T)>(q + DO - (threadIdx.x & 31) * sizeof(T),
+                   ((y & 1) ? pvo : pve) + (int64_t)(yc >> 1) * vp + (xc >> 1));
+    cpa_commit();
+  }
+  __device__ __forceinline__ In<T> fetch(int y) const {
+    const unsigned char *q = ring + (y & (DEPTH - 1)) * SLOT;
+    const auto u = *reinterpret_cast<const typename V2<T>::t *>(q);
+    const auto f = *reinterpret_cast<const typename V2<T>::t *>(q + FO);
+    const T d = *reinterpret_cast<const T *>(q + DO - (threadIdx.x & 31) * sizeof(T));
+    return In<T>{u.x, u.y, f.x, f.y, d};
+  }
+
+  // r = f - L u at the pair of row y (inside-masked)
+  __device__ __forceinline__ Pair<T> res(const Row<T> &dn, const Row<T> &cr, const Row<T> &up, const Pair<T> &f,
+                                         bool ry) const {
+    Nb9<T> q0, q1;
+    q0.c = cr.a;
+    q0.w = cr.w;
+    q0.s = dn.a;
+    q0.e = cr.b;
+    q0.n = up.a;
+    q1.c = cr.b;
+    q1.w = cr.a;
+    q1.s = dn.b;
+    q1.e = cr.e;
+    q1.n = up.b;
+    if (ORDER == 4) {
+      q0.ne = up.b;
+      q0.nw = up.w;
+      q0.sw = dn.w;
+      q0.se = dn.b;
+      q1.ne = up.e;
+      q1.nw = up.a;
+      q1.sw = dn.a;
+      q1.se = dn.e;
+    } else {
+      q0.ne = q0.nw = q0.sw = q0.se = q1.ne = q1.nw = q1.sw = q1.se = (T)0;
+    }
+    Pair<T> r;
+    r.a = (ry && ca) ? res2v<T, ORDER>(q0, f.a, k) : (T)0;
+    r.b = (ry && cb) ? res2v<T, ORDER>(q1, f.b, k) : (T)0;
+    return r;
+  }
+
+  // one step at input row j, j & 3 == K (j - ys is a multiple of 4 at K = 0)
+  template <int K>
+  __device__ __forceinline__ void step(int j) {
+    constexpr int PAR = K & 1;
+    constexpr int s0 = K, s1 = (K + 3) & 3, s2 = (K + 2) & 3, s3 = (K + 1) & 3;   // rows j, j-1, j-2, j-3 (j-4: s0)
+    // row j: wait for its copies (DEPTH - 2 younger groups may stay in flight),
+    // then refill the slot row j-1 used with row j + DEPTH - 1
+    cpa_wait<DEPTH - 2>();
+    const In<T> in = fetch(j);
+    issue(j + DEPTH - 1);
+    U[s0] = mkrow(in.ua, in.ub);
+    F[s0] = Pair<T>{in.fa, in.fb};
+    Dv[s0] = in.d;
+    const bool r1 = rin(j - 1), r2 = rin(j - 2), r3 = rin(j - 3);
+    // r_old at row j-1
+    RO[s1] = res(U[s2], U[s1], U[s0], F[s1], r1);
+    // green at row j-1: (x+1) on even rows, x on odd rows
+    if (PAR == 1) {   // j-1 even: W = (x, y), S = (x+1, y-1), E = (x+2, y), N = (x+1, y+1)
+      const T dE = shdn(Dv[s1]);
+      G[s1] = (r1 && cb) ? jac4(c, RO[s1].b, Dv[s1], Dv[s2], dE, Dv[s0]) : (T)0;
+    } else {          // j-1 odd: W = (x-1, y), S = (x, y-1), E = (x+1, y), N = (x, y+1)
+      const T dW = shup(Dv[s1]);
+      G[s1] = (r1 && ca) ? jac4(c, RO[s1].a, dW, Dv[s2], Dv[s1], Dv[s0]) : (T)0;
+    }
+    // D node at row j-2 from the greens; u_new = u_old + v there
+    {
+      const int y = j - 2;
+      T va, vb;
+      if (PAR == 0) {   // y even: D node x; W = (x-1, y), S = (x, y-1), E = (x+1, y), N = (x, y+1)
+        const T gW = shup(G[s2]);
+        va = (r2 && ca) ? jac4(c, RO[s2].a, gW, G[s3], G[s2], G[s1]) : (T)0;
+        vb = G[s2];
+      } else {          // y odd: D node x+1; W = (x, y), S = (x+1, y-1), E = (x+2, y), N = (x+1, y+1)
+        const T gE = shdn(G[s2]);
+        va = G[s2];
+        vb = (r2 && cb) ? jac4(c, RO[s2].b, G[s2], G[s3], gE, G[s1]) : (T)0;
+      }
+      const bool i0 = r2 && ca, i1 = r2 && cb;
+      const T na = i0 ? U[s2].a + va : U[s2].a, nb = i1 ? U[s2].b + vb : U[s2].b;
+      N[s2] = mkrow(na, nb);
+      if (outl && y >= ys && y < ye) {
+        T *p = pun + (int64_t)y * pitch + x;
+        if (i0 && i1) {
+          typename V2<T>::t v;
+          v.x = na;
+          v.y = nb;
+          *reinterpret_cast<typename V2<T>::t *>(p) = v;
+        } else if (i1) {   // x = 0
+          p[1] = nb;
+        }
+      }
+    }
+    // r_new at row j-3 (rows j-4, j-3, j-2 of u_new)
+    R[s3] = res(N[s0], N[s3], N[s2], F[s3], r3);
+    if (outl && j - 3 >= ys && j - 3 < ye) mx = nmax(nmax(mx, absd(R[s3].a)), absd(R[s3].b));
+    // Erest2r of the row pair (y, y+1) = (j-5, j-4) when y is even
+    if (PAR == 1) {
+      const int y = j - 5;
+      const Pair<T> R6 = R[s2], R5 = R[s1], R4 = R[s0], R3 = R[s3];
+      const T rW = shup(R5.b), rE = shdn(R4.a);
+      if (outl && y >= ys && y < ye) {
+        const int64_t o = (int64_t)(y >> 1) * rp + (x >> 1);
+        if (x >= 2 && x <= M - 2 && y >= 2 && y <= M - 2) pre[o] = erest2r(R5.a, rW, R6.a, R5.b, R4.a);
+        if (x + 1 <= M - 1 && y + 1 <= M - 1) pro[o] = erest2r(R4.b, R4.a, R5.b, rE, R3.b);
+      }
+    }
+  }
+};
+
+template <class T, int ORDER, int WPB, int MINB>
+__global__ void __launch_bounds__(WPB * 32, MINB) asc_desc_stream(const __grid_constant__ XParams<T> P) {
+  const int lane = threadIdx.x & 31;
+  const int item = blockIdx.x * WPB + (threadIdx.x >> 5);
+  const int nseg = (P.M + P.seg - 1) / P.seg;
+  double mx = 0.0;
+  if (item < P.nstrips * nseg) {   // warp-uniform
+    const int strip = item % P.nstrips, sg = item / P.nstrips;
+    const int ys = sg * P.seg, ye = min(ys + P.seg, P.M);
+    extern __shared__ __align__(16) unsigned char xsm[];
+    Strip<T, ORDER> S(P, strip * SW - 4 + 2 * lane, ys, ye,
+                      xsm + (threadIdx.x >> 5) * (DEPTH * 32 * 5 * sizeof(T)) + lane * (2 * sizeof(T)));
+    const int j0 = ys - 4, jend = ye + 3;   // steps j0 .. jend: ye - ys + 8 of them, a multiple of 4
+#pragma unroll
+    for (int i = 0; i < DEPTH - 1; i++) S.issue(j0 + i);
+    for (int j = j0; j <= jend; j += 4) {
+      S.template step<0>(j);
+      S.template step<1>(j + 1);
+      S.template step<2>(j + 2);
+      S.template step<3>(j + 3);
+    }
+    mx = S.mx;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) mx = nmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  if (lane == 0 && item < P.nstrips * nseg) norm_push(P.ns, mx);
+}
+
+}  // namespace xf
+
+template <class T, int ORDER, int WPB, int MINB>
+static cudaError_t asc_desc_launch_w(const xf::XParams<T> &P0, cudaStream_t st) {
+  constexpr int SMEM = WPB * xf::DEPTH * 32 * 5 * sizeof(T);
+  static int wres = 0, sms = 0;
+  if (!wres) {
+    int dev = 0, nb = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, xf::asc_desc_stream<T, ORDER, WPB, MINB>, WPB * 32, SMEM);
+    wres = nb > 0 ? nb * WPB : WPB;
+    if (sms <= 0) sms = 148;
+  }
+  xf::XParams<T> P = P0;
+  // one wave: about sms * wres warps, a segment of >= 32 rows (multiple of 4) each
+  const int S = (sms * wres + P.nstrips - 1) / P.nstrips;
+  int seg = (P.M + S - 1) / S;
+  seg = (seg + 3) / 4 * 4;
+  if (seg < 32) seg = 32;
+  P.seg = seg;
+  const int nitems = P.nstrips * ((P.M + seg - 1) / seg);
+  const int grid = (nitems + WPB - 1) / WPB;
+  xf::asc_desc_stream<T, ORDER, WPB, MINB><<<grid, WPB * 32, SMEM, st>>>(P);
+  return cudaGetLastError();
+}
+
+// one warp per block (registers are allocated per block); MG_XF_MINB caps
+// the registers so that 12 / 14 / 16 warps fit on an SM
+template <class T, int ORDER>
+static cudaError_t asc_desc_launch(const xf::XParams<T> &P, cudaStream_t st) {
+  static int mb = -1;
+  if (mb < 0) {
+    mb = 0;
+    if (const char *e = getenv("MG_XF_MINB")) mb = atoi(e);
+  }
+  if (mb == 12) return asc_desc_launch_w<T, ORDER, 1, 12>(P, st);
+  if (mb == 14) return asc_desc_launch_w<T, ORDER, 1, 14>(P, st);
+  if (mb == 16) return asc_desc_launch_w<T, ORDER, 1, 16>(P, st);
+  return asc_desc_launch_w<T, ORDER, 1, 1>(P, st);
+}
+
+template <class T>
+cudaError_t fast2_asc_desc(const S2<T> &vd, const T *u_old, const T *f, int64_t pitch, T *u_new, const S2<T> &d,
+                           int M, int order, T c, const Coef<T> &k, const NormSink &ns, cudaStream_t st, bool rev) {
+  (void)rev;   // the strips are walked top-down; no serpentine variant
+  // vector loads of the pair (x, x+1), x even, may touch column M+1: the row
+  // pitch must leave a padding word and rows must be 2-word aligned
+  if (((uintptr_t)u_old | (uintptr_t)f | (uintptr_t)u_new) % (2 * sizeof(T)) || pitch % 2 || pitch < M + 2)
+    return cudaErrorInvalidValue;
+  xf::XParams<T> P{};
+  P.u = u_old;
+  P.f = f;
+  P.ve = vd.e;
+  P.vo = vd.o;
+  P.un = u_new;
+  P.re = d.e;
+  P.ro = d.o;
+  P.pitch = pitch;
+  P.vp = vd.pitch;
+  P.rp = d.pitch;
+  P.M = M;
+  P.nstrips = (M + xf::SW - 1) / xf::SW;
+  P.c = c;
+  P.k = k;
+  P.ns = ns;
+  return order == 2 ? asc_desc_launch<T, 2>(P, st) : asc_desc_launch<T, 4>(P, st);
+}
+
+template cudaError_t fast2_asc_desc<float>(const S2<float> &, const float *, const float *, int64_t, float *,
+                                           const S2<float> &, int, int, float, const Coef<float> &, const NormSink &,
+                                           cudaStream_t, bool);
+template cudaError_t fast2_asc_desc<double>(const S2<double> &, const double *, const double *, int64_t, double *,
+                                            const S2<double> &, int, int, double, const Coef<double> &,
+                                            const NormSink &, cudaStream_t, bool);
+
+}  // namespace mg

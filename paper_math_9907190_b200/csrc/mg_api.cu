@@ -25,6 +25,7 @@ struct Impl2 : ImplBase {
   int om = 1;              // first octave of the cooperative tail kernel (om <= oc)
   bool use_tail = false;
   bool serp = !env_flag("MG_2D_NOSERP");   // serpentine tile order across passes
+  bool xfuse = !env_flag("MG_2D_NOXFUSE");   // cross-cycle fusion of the finest ascent and descent
   Lev2<T> *d_lev = nullptr;
   std::vector<Lev2<T>> h_lev;   // host copy of the level descriptors (tail kernel parameters)
   explicit Impl2(const mg_solver *sv) : s(sv), k(sv->k), n(sv->cfg.n), pitch(sv->pitch) {}
@@ -121,6 +122,12 @@ struct Impl2 : ImplBase {
 
   NormSink sink() const { return NormSink{s->d_hist, s->d_counter, kHistCap}; }
 
+  bool fuses_cycles() const override { return use_fast && xfuse; }
+  void enqueue_cycle_mode(const void *u_in, void *u_out, const void *f_eff, cudaStream_t st, Prof *prof,
+                          int mode) override {
+    if (use_fast) return enqueue_fast(u_in, u_out, f_eff, st, prof, mode);
+    enqueue_cycle(u_in, u_out, f_eff, st, prof);
+  }
   void enqueue_cycle(const void *u_in, void *u_out, const void *f_eff, cudaStream_t st, Prof *prof) override {
     if (use_fast) return enqueue_fast(u_in, u_out, f_eff, st, prof);
     D2<const T> uc{(const T *)u_in, pitch}, fc{(const T *)f_eff, pitch};
@@ -153,23 +160,29 @@ struct Impl2 : ImplBase {
   }
 
   // The B200 path: TMA tile kernels on octaves < oc, one CTA below.
-  void enqueue_fast(const void *u_in, void *u_out, const void *f_eff, cudaStream_t st, Prof *prof) {
+  void enqueue_fast(const void *u_in, void *u_out, const void *f_eff, cudaStream_t st, Prof *prof, int mode = 0) {
     const double w = sizeof(T);
     const int L = 2 * k - 1;
     const T *uin = (const T *)u_in, *fe = (const T *)f_eff;
-    STEP("desc_fine", 0, 1, w * (2 * Nl[0] + Nl[1]));
     // Serpentine tile order: each pass starts where its producer finished,
     // so the last ~100 MB the producer wrote are still in L2.
+    // The finest descent runs forwards; the fused ascent+descent backwards,
+    // and the restrictions follow whichever produced r_D(1).
     Rows2 fwd, bwd;
     bwd.rev = serp;
-    fast2_desc_fine<T>(uin, fe, pitch, rD[0], M[0], s->cfg.order, coef, sink(), st, fwd);
+    const bool skip = mode & kSkipDesc;
+    Rows2 dA = skip ? bwd : fwd, dD = skip ? fwd : bwd;   // rest_ad, rest_da
+    if (!skip) {
+      STEP("desc_fine", 0, 1, w * (2 * Nl[0] + Nl[1]));
+      fast2_desc_fine<T>(uin, fe, pitch, rD[0], M[0], s->cfg.order, coef, sink(), st, fwd);
+    }
     auto descent = [&](int o) {
       if (o >= 1) {
         STEP("rest_ad", 2 * o, 1, w * (Nl[2 * o] + Nl[2 * o + 1]));
-        fast2_rest_ad<T>(rA[o], rD[o], M[o], st, fwd);
+        fast2_rest_ad<T>(rA[o], rD[o], M[o], st, dA);
       }
       STEP("rest_da", 2 * o + 1, 1, w * (Nl[2 * o + 1] + Nl[2 * o + 2]));
-      fast2_rest_da<T>(rD[o], rA[o + 1], M[o + 1], st, bwd);
+      fast2_rest_da<T>(rD[o], rA[o + 1], M[o + 1], st, dD);
     };
     auto ascent = [&](int o) {
       STEP("jac_d", 2 * o + 1, 1, w * (Nl[2 * o + 2] + 2 * Nl[2 * o + 1]));
@@ -177,6 +190,10 @@ struct Impl2 : ImplBase {
       if (o >= 1) {
         STEP("jac_a", 2 * o, 1, w * (Nl[2 * o + 1] + 2 * Nl[2 * o]));
         fast2_jac_a<T>(vD[o], rA[o], vA[o], M[o], cA[o], st, bwd);
+      } else if (mode & kFuseNext) {
+        STEP("asc_desc", 0, 1, w * (2 * Nl[1] + 3 * Nl[0]));
+        fast2_asc_desc<T>(vD[0], uin, fe, pitch, (T *)u_out, rD[0], M[0], s->cfg.order, cA[0], coef, sink(), st,
+                          serp);
       } else {
         STEP("asc_fine", 0, 1, w * (Nl[1] + 3 * Nl[0]));
         fast2_asc_fine<T>(vD[0], uin, fe, pitch, (T *)u_out, M[0], s->cfg.order, cA[0], coef, st, bwd);
@@ -604,15 +621,15 @@ static void drop_graphs(mg_solver *s) {
 
 // Launch one V-cycle u_in -> u_out: replay the CUDA graph captured for these
 // pointers (captured on first use; a few are cached).
-static int run_cycle(mg_solver *s, const void *u_in, void *u_out, const void *f_eff) {
+static int run_cycle(mg_solver *s, const void *u_in, void *u_out, const void *f_eff, int mode) {
   cudaGraphExec_t ex = nullptr;
   for (auto &g : s->graphs)
-    if (g.uin == u_in && g.uout == u_out && g.f == f_eff) ex = g.exec;
+    if (g.uin == u_in && g.uout == u_out && g.f == f_eff && g.mode == mode) ex = g.exec;
   if (!ex) {
-    if (s->graphs.size() >= 8) drop_graphs(s);
+    if (s->graphs.size() >= 16) drop_graphs(s);
     cudaGraph_t g = nullptr;
     CKS(s, cudaStreamBeginCapture(s->st, cudaStreamCaptureModeThreadLocal));
-    s->impl->enqueue_cycle(u_in, u_out, f_eff, s->st);
+    s->impl->enqueue_cycle_mode(u_in, u_out, f_eff, s->st, nullptr, mode);
     cudaError_t le = cudaGetLastError();
     cudaError_t e = cudaStreamEndCapture(s->st, &g);
     if (le != cudaSuccess) {
@@ -623,7 +640,7 @@ static int run_cycle(mg_solver *s, const void *u_in, void *u_out, const void *f_
     e = cudaGraphInstantiate(&ex, g, 0);
     cudaGraphDestroy(g);
     CKS(s, e);
-    s->graphs.push_back({ex, u_in, u_out, f_eff});
+    s->graphs.push_back({ex, u_in, u_out, f_eff, mode});
   }
   CKS(s, cudaGraphLaunch(ex, s->st));
   return MG_OK;
@@ -843,16 +860,23 @@ static int vcycle_dev(mg_solver *s, void *u, const void *f, int ncycles, double 
     CKS(s, cudaMalloc(&s->d_ualt, bytes));
     CKS(s, cudaMemsetAsync(s->d_ualt, 0, bytes, s->st));
   }
+  // Cross-cycle fusion: every cycle but the first skips its finest descent,
+  // which the previous cycle's last pass computed (and the final residual
+  // norm comes from the last cycle's when it is wanted).
+  const bool xf = alt && s->impl->fuses_cycles();
   void *cur = u;
   for (int c = 0; c < ncycles; c++) {
     void *dst = alt ? (cur == u ? s->d_ualt : u) : u;
-    int rc = run_cycle(s, cur, dst, fe);
+    int mode = 0;
+    if (xf && c > 0) mode |= ImplBase::kSkipDesc;
+    if (xf && (c + 1 < ncycles || res_hist)) mode |= ImplBase::kFuseNext;
+    int rc = run_cycle(s, cur, dst, fe, mode);
     if (rc) return rc;
     cur = dst;
   }
   if (cur != u) CKS(s, cudaMemcpyAsync(u, cur, s->field_elems() * s->esz, cudaMemcpyDeviceToDevice, s->st));
   if (res_hist) {
-    s->impl->enqueue_final_norm(u, fe, s->st);
+    if (!xf || ncycles == 0) s->impl->enqueue_final_norm(u, fe, s->st);
     CKS(s, s->impl->reduce_hist(s->d_hist, nslots, s->st));
     CKS(s, cudaMemcpyAsync(s->h_hist, s->d_hist, sizeof(unsigned long long) * nslots, cudaMemcpyDeviceToHost, s->st));
     CKS(s, cudaStreamSynchronize(s->st));
@@ -954,10 +978,15 @@ int mg_profile(mg_solver *s, void *u, const void *f, int ncycles, mg_step_stat *
     CKS(s, cudaMalloc(&s->d_ualt, bytes));
     CKS(s, cudaMemsetAsync(s->d_ualt, 0, bytes, s->st));
   }
+  // with cross-cycle fusion every profiled cycle is a steady-state one: the
+  // descent of the first runs unprofiled before the loop
+  const bool xf = alt && s->impl->fuses_cycles();
+  const int mode = xf ? ImplBase::kSkipDesc | ImplBase::kFuseNext : 0;
+  if (xf) s->impl->enqueue_final_norm(u, fe, s->st);
   void *cur = u;
   for (int c = 0; c < ncycles; c++) {
     void *dst = alt ? (cur == u ? s->d_ualt : u) : u;
-    s->impl->enqueue_cycle(cur, dst, fe, s->st, &prof);
+    s->impl->enqueue_cycle_mode(cur, dst, fe, s->st, &prof, mode);
     prof.end_cycle();
     cur = dst;
   }

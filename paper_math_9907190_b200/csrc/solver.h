@@ -113,6 +113,17 @@ struct ImplBase {
                              Prof *prof = nullptr) = 0;
   // true: the TMA tile kernels run (they update u out of place)
   virtual bool fast() const { return false; }
+  // Cross-cycle fusion.  Mode bits of enqueue_cycle_mode:
+  // kSkipDesc -- this cycle's finest descent already ran (fused into the
+  // previous cycle's ascent, which also pushed its residual norm);
+  // kFuseNext -- the finest ascent also runs the next cycle's descent.
+  enum { kSkipDesc = 1, kFuseNext = 2 };
+  virtual bool fuses_cycles() const { return false; }
+  virtual void enqueue_cycle_mode(const void *u_in, void *u_out, const void *f_eff, cudaStream_t st, Prof *prof,
+                                  int mode) {
+    (void)mode;
+    enqueue_cycle(u_in, u_out, f_eff, st, prof);
+  }
   virtual void enqueue_final_norm(void *u, const void *f_eff, cudaStream_t st) = 0;
   virtual void enqueue_residual(const void *u, const void *f, void *r, cudaStream_t st) = 0;
   virtual void enqueue_ftilde(const void *f, void *ft, cudaStream_t st) = 0;
@@ -162,6 +173,7 @@ struct mg_solver {
   struct GraphEntry {
     cudaGraphExec_t exec;
     const void *uin, *uout, *f;
+    int mode;
   };
   std::vector<GraphEntry> graphs;   // captured cycles keyed by pointers
   void *d_ualt = nullptr;            // out-of-place partner of the caller's u

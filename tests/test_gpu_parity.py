@@ -105,6 +105,33 @@ def test_parity_2d_8193_full_size():
         assert np.array_equal(hg, ho)
 
 
+@pytest.mark.parametrize("dtype", [np.float64, np.float32], ids=["f64", "f32"])
+@pytest.mark.parametrize("order", [2, 4])
+def test_cycle_fusion_call_patterns(order, dtype):
+    """Cross-cycle fusion: 1, 2 and 5 cycles per call, with and
+    without the residual history, and a run split over several calls all
+    equal the oracle bit for bit."""
+    import torch
+    n, p = 513, (P2 if order == 2 else P2_4)
+    f = W.random_field(2, n, seed=31).astype(dtype)
+    u0 = (W.random_field(2, n, seed=32) * 0.1).astype(dtype)
+    for cycles in (1, 2, 5):
+        uo, ho = _oracle_run(2, n, order, p, f, u0, cycles, dtype)
+        for hist in (False, True):
+            ug, hg = _gpu_run(2, n, order, p, f, u0, cycles, dtype, hist=hist)
+            assert np.array_equal(ug, uo), (cycles, hist, _rel(ug, uo))
+            if hist:
+                assert np.array_equal(hg, ho), cycles
+    s = _solver(2, n, order, p, dtype)
+    u = s.alloc(u0)
+    ft = s.alloc(f)
+    for c in (2, 1, 3):
+        s.vcycle(u, ft, c)
+    torch.cuda.synchronize()
+    uo, _ = _oracle_run(2, n, order, p, f, u0, 6, dtype)
+    assert np.array_equal(s.view(u).cpu().numpy(), uo)
+
+
 @pytest.mark.slow
 def test_parity_3d_513_full_size():
     """BASELINE configs[4] at full size, one cycle compared element by element."""
