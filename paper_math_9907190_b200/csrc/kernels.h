@@ -51,6 +51,15 @@ bool launch2_tail(const Lev2<T> *h_lev, int om, int oc, int k, int *counter, cud
 // TMA tile kernels (k2f.cu); every pointer/pitch must be 16-byte aligned.
 // Rows2: the output rows a launch writes and the local allocations of its
 // inputs (multi-GPU slabs); the default (all -1 / 0) is the whole level.
+// Direction of the next 3D plane-pipeline launch on this host thread
+// (zpipe Sched::rev, items walked in reverse): the 3D V-cycle alternates it
+// so that every pass first reads what its producer wrote last (still in L2).
+// launch_zpipe resets it to 0.
+inline int &zp_next_rev() {
+  static thread_local int r = 0;
+  return r;
+}
+
 struct Rows2 {
   bool rev = false;         // walk the tiles in descending order (reuse the L2-resident tail of the producer's output)
   int ylo = 0, yhi = -1;    // output rows [ylo, yhi) in the output array's row units (-1: all)

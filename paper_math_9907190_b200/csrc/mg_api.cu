@@ -484,12 +484,20 @@ struct Impl3 : ImplBase {
     // fused octave passes: bit-identical, but no measurable gain in graph replay on B200 (A/B in
     // DESIGN.md), so opt-in (MG_K3_FUSE=1)
     static const bool fuse_rmg = env_flag("MG_K3_FUSE");
+    // Serpentine item order (zpipe Sched::rev): descent pass d (desc_fine = 0,
+    // then rest_rm, rest_mg, rest_gr, ...) runs reversed when d is odd; ascent
+    // passes alternate backwards from asc_fine (reversed), so the next
+    // cycle's desc_fine (forward) starts where asc_fine ended.
+    static const bool serp = !env_flag("MG_3D_NOSERP");
+    auto dir = [&](int pass) { zp_next_rev() = serp ? (pass & 1) : 0; };
     STEP("desc_fine", 0, 1, w * (2 * Nl[0] + Nl[1]));
+    dir(0);
     desc_fine(u, f_eff, st);
     auto descent = [&](int o) {
       int g = 3 * o;
       if (o >= 1) {
         STEP("rest_gr", g, 1, w * (Nl[g] + Nl[g + 1]));
+        dir(3 * o);
         if (gen2) fast3p_rest_gr<T>(rG[o], rR[o], M[o], st);
         else lv3_rest_gr<T>(rG[o], rR[o], M[o], st);
       }
@@ -499,9 +507,11 @@ struct Impl3 : ImplBase {
         return;
       }
       STEP("rest_rm", g + 1, 1, w * (Nl[g + 1] + Nl[g + 2]));
+      dir(3 * o + 1);
       if (gen2s) sub3_rest_rm(rR[o], rM[o], M[o], st);
       else lv3_rest_rm<T>(rR[o], rM[o], M[o], st);
       STEP("rest_mg", g + 2, 1, w * (Nl[g + 2] + Nl[g + 3]));
+      dir(3 * o + 2);
       if (gen2s) sub3_rest_mg(rM[o], rG[o + 1], M[o + 1], st);
       else lv3_rest_mg<T>(rM[o], rG[o + 1], M[o + 1], st);
     };
@@ -517,9 +527,11 @@ struct Impl3 : ImplBase {
         return;
       }
       STEP("jac_m", g + 2, gen2s ? 1 : 2, w * (Nl[g + 3] + 2 * Nl[g + 2]));
+      dir(3 * o + 3);
       if (gen2s) sub3_jac_m(vG[o + 1], rM[o], vM[o], M[o], cMg[o], st);
       else lv3_jac_m<T>(vG[o + 1], rM[o], vM[o], M[o], cMg[o], st);
       STEP("jac_r", g + 1, gen2s ? 1 : 2, w * (Nl[g + 2] + 2 * Nl[g + 1]));
+      dir(3 * o + 2);
       if (gen2s) sub3_jac_r(vM[o], rR[o], vR[o], M[o], cR1[o], cR2[o], st);
       else lv3_jac_r<T>(vM[o], rR[o], vR[o], M[o], cR1[o], cR2[o], st);
     };
@@ -528,6 +540,7 @@ struct Impl3 : ImplBase {
       jac_mr(o);
       if (gen2) {
         STEP("jac_g", g, 1, w * (Nl[g + 1] + 2 * Nl[g]));
+        dir(3 * o + 1);
         fast3p_jac_g<T>(vR[o], rG[o], vG[o], M[o], cG[o], st);
       } else {
         STEP("jac_g", g, 2, w * (Nl[g + 1] + 2 * Nl[g]));
@@ -568,6 +581,7 @@ struct Impl3 : ImplBase {
       if (!env_flag("MG_ASC3_DIRECT") && ((uintptr_t)u & 15) == 0 && ((uintptr_t)f_eff & 15) == 0 &&
                  ((uintptr_t)u_out & 15) == 0) {
         STEP("asc_fine", 0, 1, w * (Nl[1] + 3 * Nl[0]));
+        dir(1);
         fast3_asc_fine<T>(vR[0], (const T *)u, (const T *)f_eff, pitch, (T *)u_out, M[0], s->cfg.order, cG[0], coef,
                           st);
       } else {
@@ -575,6 +589,7 @@ struct Impl3 : ImplBase {
         lv3_asc_fine<T>(vR[0], field(u), cfield(f_eff), scratch, field(u_out), M[0], s->cfg.order, cG[0], coef, st);
       }
     }
+    zp_next_rev() = 0;
   }
   void enqueue_final_norm(void *u, const void *f_eff, cudaStream_t st) override { desc_fine(u, f_eff, st); }
   void enqueue_residual(const void *u, const void *f, void *r, cudaStream_t st) override {

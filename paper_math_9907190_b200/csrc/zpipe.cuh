@@ -80,9 +80,11 @@ struct Item {
 struct Sched {
   int T, ntx, zlo, zhi, S;
   int tx, ty, xoff, yoff;   // tile extents and origin offsets: x0 = tx * (t % ntx) + xoff
+  int rev;                  // 1: every CTA walks its items in reverse order (serpentine across passes)
   __device__ __forceinline__ int count(int G) const { return (T * S) / G + ((T * S) % G ? 1 : 0); }
   __device__ __forceinline__ Item get(int k, int b, int G) const {
     const int U = T * S, W = U / G, R = U % G;
+    if (rev) k = count(G) - 1 - k;
     const long long Z = zhi - zlo;
     int u, sg = 0, nseg = 1;
     if (k < W) {
@@ -222,6 +224,8 @@ static cudaError_t launch_zpipe(typename Op::Params &P, int tx, int ty, int xoff
   P.sc.T = ntx * nty;
   P.sc.zlo = zlo;
   P.sc.zhi = zhi;
+  P.sc.rev = zp_next_rev();
+  zp_next_rev() = 0;
   P.sc.S = P.sc.T >= sms ? 1 : (sms + P.sc.T - 1) / P.sc.T;
   if (P.sc.S > zhi - zlo) P.sc.S = zhi - zlo;
   const long long work = (long long)P.sc.T * (zhi - zlo);
