@@ -15,13 +15,17 @@
 // register pipeline instead: one warp streams down a strip of 56 output
 // columns (lane l owns the column pair x = x0 - 4 + 2l, the 4-column halo on
 // both sides is the outer lanes), one row per step, x neighbours by warp
-// shuffles, no shared memory and no barriers.  At input row j a step computes
+// shuffles, no barriers.  At input row j a step computes
 //     r_old(j-1) -> green(j-1) -> D node(j-2) -> u_new(j-2) -> r_new(j-3)
-// and, every second row, the Erest2r pair of rows (j-5, j-4).  Rows are
-// prefetched four steps ahead (plain 16/8-byte vector loads, 512 B per warp
-// row).  A strip is cut into row segments (9 rows of warm-up each) so that
-// the grid fills every SM once.  Same node formulas, same evaluation order:
-// bit-identical to the two separate passes.
+// and, every second row, the Erest2r pair of rows (j-5, j-4).  Input rows
+// (u, f pairs and the v_D value of each lane) arrive DEPTH - 1 steps ahead
+// through per-lane cp.async copies into a shared-memory ring (each lane reads
+// back only its own bytes); register prefetch instead stalled on the
+// zero-masking of the loads and cost 40 registers.  A strip is cut into row
+// segments (8 rows of warm-up each) so that
+// the grid fills every SM once; warps whose segment touches no boundary row
+// or column run a mask-free instance of the step.  Same node formulas, same
+// evaluation order: bit-identical to the two separate passes.
 #include "kernels.h"
 #include "ops2.cuh"
 
@@ -182,6 +186,9 @@ struct Strip {
   }
 
   // r = f - L u at the pair of row y (inside-masked)
+  // EDGE = false: the warp's strip segment touches no boundary row or column
+  // (every node it computes is interior), so all masks are compile-time true
+  template <bool EDGE>
   __device__ __forceinline__ Pair<T> res(const Row<T> &dn, const Row<T> &cr, const Row<T> &up, const Pair<T> &f,
                                          bool ry) const {
     Nb9<T> q0, q1;
@@ -208,13 +215,13 @@ struct Strip {
       q0.ne = q0.nw = q0.sw = q0.se = q1.ne = q1.nw = q1.sw = q1.se = (T)0;
     }
     Pair<T> r;
-    r.a = (ry && ca) ? res2v<T, ORDER>(q0, f.a, k) : (T)0;
-    r.b = (ry && cb) ? res2v<T, ORDER>(q1, f.b, k) : (T)0;
+    r.a = (!EDGE || (ry && ca)) ? res2v<T, ORDER>(q0, f.a, k) : (T)0;
+    r.b = (!EDGE || (ry && cb)) ? res2v<T, ORDER>(q1, f.b, k) : (T)0;
     return r;
   }
 
   // one step at input row j, j & 3 == K (j - ys is a multiple of 4 at K = 0)
-  template <int K>
+  template <int K, bool EDGE>
   __device__ __forceinline__ void step(int j) {
     constexpr int PAR = K & 1;
     constexpr int s0 = K, s1 = (K + 3) & 3, s2 = (K + 2) & 3, s3 = (K + 1) & 3;   // rows j, j-1, j-2, j-3 (j-4: s0)
@@ -226,16 +233,17 @@ struct Strip {
     U[s0] = mkrow(in.ua, in.ub);
     F[s0] = Pair<T>{in.fa, in.fb};
     Dv[s0] = in.d;
-    const bool r1 = rin(j - 1), r2 = rin(j - 2), r3 = rin(j - 3);
+    const bool r1 = !EDGE || rin(j - 1), r2 = !EDGE || rin(j - 2), r3 = !EDGE || rin(j - 3);
+    const bool ka = !EDGE || ca, kb = !EDGE || cb;
     // r_old at row j-1
-    RO[s1] = res(U[s2], U[s1], U[s0], F[s1], r1);
+    RO[s1] = res<EDGE>(U[s2], U[s1], U[s0], F[s1], r1);
     // green at row j-1: (x+1) on even rows, x on odd rows
     if (PAR == 1) {   // j-1 even: W = (x, y), S = (x+1, y-1), E = (x+2, y), N = (x+1, y+1)
       const T dE = shdn(Dv[s1]);
-      G[s1] = (r1 && cb) ? jac4(c, RO[s1].b, Dv[s1], Dv[s2], dE, Dv[s0]) : (T)0;
+      G[s1] = (r1 && kb) ? jac4(c, RO[s1].b, Dv[s1], Dv[s2], dE, Dv[s0]) : (T)0;
     } else {          // j-1 odd: W = (x-1, y), S = (x, y-1), E = (x+1, y), N = (x, y+1)
       const T dW = shup(Dv[s1]);
-      G[s1] = (r1 && ca) ? jac4(c, RO[s1].a, dW, Dv[s2], Dv[s1], Dv[s0]) : (T)0;
+      G[s1] = (r1 && ka) ? jac4(c, RO[s1].a, dW, Dv[s2], Dv[s1], Dv[s0]) : (T)0;
     }
     // D node at row j-2 from the greens; u_new = u_old + v there
     {
@@ -243,14 +251,14 @@ struct Strip {
       T va, vb;
       if (PAR == 0) {   // y even: D node x; W = (x-1, y), S = (x, y-1), E = (x+1, y), N = (x, y+1)
         const T gW = shup(G[s2]);
-        va = (r2 && ca) ? jac4(c, RO[s2].a, gW, G[s3], G[s2], G[s1]) : (T)0;
+        va = (r2 && ka) ? jac4(c, RO[s2].a, gW, G[s3], G[s2], G[s1]) : (T)0;
         vb = G[s2];
       } else {          // y odd: D node x+1; W = (x, y), S = (x+1, y-1), E = (x+2, y), N = (x+1, y+1)
         const T gE = shdn(G[s2]);
         va = G[s2];
-        vb = (r2 && cb) ? jac4(c, RO[s2].b, G[s2], G[s3], gE, G[s1]) : (T)0;
+        vb = (r2 && kb) ? jac4(c, RO[s2].b, G[s2], G[s3], gE, G[s1]) : (T)0;
       }
-      const bool i0 = r2 && ca, i1 = r2 && cb;
+      const bool i0 = r2 && ka, i1 = r2 && kb;
       const T na = i0 ? U[s2].a + va : U[s2].a, nb = i1 ? U[s2].b + vb : U[s2].b;
       N[s2] = mkrow(na, nb);
       if (outl && y >= ys && y < ye) {
@@ -266,7 +274,7 @@ struct Strip {
       }
     }
     // r_new at row j-3 (rows j-4, j-3, j-2 of u_new)
-    R[s3] = res(N[s0], N[s3], N[s2], F[s3], r3);
+    R[s3] = res<EDGE>(N[s0], N[s3], N[s2], F[s3], r3);
     if (outl && j - 3 >= ys && j - 3 < ye) mx = nmax(nmax(mx, absd(R[s3].a)), absd(R[s3].b));
     // Erest2r of the row pair (y, y+1) = (j-5, j-4) when y is even
     if (PAR == 1) {
@@ -275,8 +283,8 @@ struct Strip {
       const T rW = shup(R5.b), rE = shdn(R4.a);
       if (outl && y >= ys && y < ye) {
         const int64_t o = (int64_t)(y >> 1) * rp + (x >> 1);
-        if (x >= 2 && x <= M - 2 && y >= 2 && y <= M - 2) pre[o] = erest2r(R5.a, rW, R6.a, R5.b, R4.a);
-        if (x + 1 <= M - 1 && y + 1 <= M - 1) pro[o] = erest2r(R4.b, R4.a, R5.b, rE, R3.b);
+        if (!EDGE || (x >= 2 && x <= M - 2 && y >= 2 && y <= M - 2)) pre[o] = erest2r(R5.a, rW, R6.a, R5.b, R4.a);
+        if (!EDGE || (x + 1 <= M - 1 && y + 1 <= M - 1)) pro[o] = erest2r(R4.b, R4.a, R5.b, rE, R3.b);
       }
     }
   }
@@ -297,11 +305,23 @@ __global__ void __launch_bounds__(WPB * 32, MINB) asc_desc_stream(const __grid_c
     const int j0 = ys - 4, jend = ye + 3;   // steps j0 .. jend: ye - ys + 8 of them, a multiple of 4
 #pragma unroll
     for (int i = 0; i < DEPTH - 1; i++) S.issue(j0 + i);
-    for (int j = j0; j <= jend; j += 4) {
-      S.template step<0>(j);
-      S.template step<1>(j + 1);
-      S.template step<2>(j + 2);
-      S.template step<3>(j + 3);
+    // rows computed: [ys-7, ye+2]; columns: [x0-4, x0+59]
+    const int x0 = strip * SW;
+    const bool edge = ys - 7 < 1 || ye + 2 > P.M - 1 || x0 - 4 < 1 || x0 + 59 > P.M - 1;
+    if (edge) {
+      for (int j = j0; j <= jend; j += 4) {
+        S.template step<0, true>(j);
+        S.template step<1, true>(j + 1);
+        S.template step<2, true>(j + 2);
+        S.template step<3, true>(j + 3);
+      }
+    } else {
+      for (int j = j0; j <= jend; j += 4) {
+        S.template step<0, false>(j);
+        S.template step<1, false>(j + 1);
+        S.template step<2, false>(j + 2);
+        S.template step<3, false>(j + 3);
+      }
     }
     mx = S.mx;
   }
@@ -337,18 +357,12 @@ static cudaError_t asc_desc_launch_w(const xf::XParams<T> &P0, cudaStream_t st) 
   return cudaGetLastError();
 }
 
-// one warp per block (registers are allocated per block); MG_XF_MINB caps
-// the registers so that 12 / 14 / 16 warps fit on an SM
+// one warp per block: registers are allocated per block, so 1-warp blocks
+// fill an SM to the register limit (measured: 2- and 4-warp blocks leave
+// 3-4 warps per SM unused and run 60 % slower; capping the registers at 128
+// to fit 16 warps spills the pipeline state and is slower still)
 template <class T, int ORDER>
 static cudaError_t asc_desc_launch(const xf::XParams<T> &P, cudaStream_t st) {
-  static int mb = -1;
-  if (mb < 0) {
-    mb = 0;
-    if (const char *e = getenv("MG_XF_MINB")) mb = atoi(e);
-  }
-  if (mb == 12) return asc_desc_launch_w<T, ORDER, 1, 12>(P, st);
-  if (mb == 14) return asc_desc_launch_w<T, ORDER, 1, 14>(P, st);
-  if (mb == 16) return asc_desc_launch_w<T, ORDER, 1, 16>(P, st);
   return asc_desc_launch_w<T, ORDER, 1, 1>(P, st);
 }
 
