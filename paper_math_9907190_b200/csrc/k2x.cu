@@ -33,7 +33,6 @@ namespace mg {
 namespace xf {
 
 constexpr int SW = 56;    // output columns per strip: 32 lanes x 2 minus 2 x 4 halo
-constexpr int DEPTH = 8;  // rows in flight per warp (power of 2)
 
 template <class T>
 struct V2;
@@ -110,7 +109,7 @@ struct In {
 // shifted between steps.  Loads are unconditional from clamped addresses:
 // rows outside [0, M] and columns outside [0, M] only feed nodes that are
 // not interior, whose results are all selected away (inside() is false).
-template <class T, int ORDER>
+template <class T, int ORDER, int DEPTH>   // DEPTH: rows in flight per warp (power of 2)
 struct Strip {
   const T *pu, *pf, *pve, *pvo;
   T *pun, *pre, *pro;
@@ -127,7 +126,12 @@ struct Strip {
   T G[4];              // green value of the row
   Row<T> N[4];         // u_new
   Pair<T> R[4];        // r(u_new)
-  double mx;
+  unsigned long long mx;   // max |r| as the bit pattern of a non-negative double (NaN sorts above inf)
+  // interior warps address by increments: next load row offset, next E / O
+  // v_D load pointers, u_new store pointer of row j-2, next Erest2r offset
+  int64_t lo, rso;
+  const T *ldE, *ldO;
+  T *stp;
 
   __device__ __forceinline__ Strip(const XParams<T> &P, int x_, int ys_, int ye_, unsigned char *ring_) {
     ring = ring_;
@@ -158,7 +162,18 @@ struct Strip {
       F[i] = RO[i] = R[i] = Pair<T>{0, 0};
       Dv[i] = G[i] = (T)0;
     }
-    mx = 0.0;
+    mx = 0ull;
+  }
+  // incremental addressing from step j0 on (row-interior blocks only)
+  __device__ __forceinline__ void start(int j0) {
+    lo = (int64_t)(j0 + DEPTH - 1) * pitch + xc;   // the first row issued inside the loop (odd)
+    ldO = pvo + (int64_t)((j0 + DEPTH - 1) >> 1) * vp + (xc >> 1);
+    ldE = pve + (int64_t)((j0 + DEPTH) >> 1) * vp + (xc >> 1);
+    stp = pun + (int64_t)(j0 - 2) * pitch + x;
+    rso = (int64_t)((j0 - 4) >> 1) * rp + (x >> 1);
+  }
+  static __device__ __forceinline__ unsigned long long absbits(T v) {
+    return (unsigned long long)__double_as_longlong((double)v) & 0x7fffffffffffffffull;
   }
   __device__ __forceinline__ bool rin(int y) const { return (unsigned)(y - 1) < (unsigned)(M - 1); }
 
@@ -177,6 +192,22 @@ struct Strip {
                    ((y & 1) ? pvo : pve) + (int64_t)(yc >> 1) * vp + (xc >> 1));
     cpa_commit();
   }
+  // the same for an interior warp (row y in [0, M], parity YP = y & 1)
+  template <int YP>
+  __device__ __forceinline__ void issue_inc(int y) {
+    unsigned char *q = ring + (y & (DEPTH - 1)) * SLOT;
+    cpa<2 * sizeof(T)>(q, pu + lo);
+    cpa<2 * sizeof(T)>(q + FO, pf + lo);
+    lo += pitch;
+    if (YP) {
+      cpa<sizeof(T)>(q + DO - (threadIdx.x & 31) * sizeof(T), ldO);
+      ldO += vp;
+    } else {
+      cpa<sizeof(T)>(q + DO - (threadIdx.x & 31) * sizeof(T), ldE);
+      ldE += vp;
+    }
+    cpa_commit();
+  }
   __device__ __forceinline__ In<T> fetch(int y) const {
     const unsigned char *q = ring + (y & (DEPTH - 1)) * SLOT;
     const auto u = *reinterpret_cast<const typename V2<T>::t *>(q);
@@ -186,11 +217,10 @@ struct Strip {
   }
 
   // r = f - L u at the pair of row y (inside-masked)
-  // EDGE = false: the warp's strip segment touches no boundary row or column
-  // (every node it computes is interior), so all masks are compile-time true
-  template <bool EDGE>
+  // r at the pair of row y; ry, ka, kb: row y / column x / column x+1
+  // interior (compile-time true away from the boundary)
   __device__ __forceinline__ Pair<T> res(const Row<T> &dn, const Row<T> &cr, const Row<T> &up, const Pair<T> &f,
-                                         bool ry) const {
+                                         bool ry, bool ka, bool kb) const {
     Nb9<T> q0, q1;
     q0.c = cr.a;
     q0.w = cr.w;
@@ -215,13 +245,15 @@ struct Strip {
       q0.ne = q0.nw = q0.sw = q0.se = q1.ne = q1.nw = q1.sw = q1.se = (T)0;
     }
     Pair<T> r;
-    r.a = (!EDGE || (ry && ca)) ? res2v<T, ORDER>(q0, f.a, k) : (T)0;
-    r.b = (!EDGE || (ry && cb)) ? res2v<T, ORDER>(q1, f.b, k) : (T)0;
+    r.a = (ry && ka) ? res2v<T, ORDER>(q0, f.a, k) : (T)0;
+    r.b = (ry && kb) ? res2v<T, ORDER>(q1, f.b, k) : (T)0;
     return r;
   }
 
   // one step at input row j, j & 3 == K (j - ys is a multiple of 4 at K = 0)
-  template <int K, bool EDGE>
+  // RE: a row of this step (computed, restricted or loaded) may lie outside
+  // the interior (masks and clamped loads); CE: the same for the warp's columns
+  template <int K, bool RE, bool CE>
   __device__ __forceinline__ void step(int j) {
     constexpr int PAR = K & 1;
     constexpr int s0 = K, s1 = (K + 3) & 3, s2 = (K + 2) & 3, s3 = (K + 1) & 3;   // rows j, j-1, j-2, j-3 (j-4: s0)
@@ -229,14 +261,17 @@ struct Strip {
     // then refill the slot row j-1 used with row j + DEPTH - 1
     cpa_wait<DEPTH - 2>();
     const In<T> in = fetch(j);
-    issue(j + DEPTH - 1);
+    if (RE)
+      issue(j + DEPTH - 1);
+    else
+      issue_inc<(K + DEPTH - 1) & 1>(j + DEPTH - 1);
     U[s0] = mkrow(in.ua, in.ub);
     F[s0] = Pair<T>{in.fa, in.fb};
     Dv[s0] = in.d;
-    const bool r1 = !EDGE || rin(j - 1), r2 = !EDGE || rin(j - 2), r3 = !EDGE || rin(j - 3);
-    const bool ka = !EDGE || ca, kb = !EDGE || cb;
+    const bool r1 = !RE || rin(j - 1), r2 = !RE || rin(j - 2), r3 = !RE || rin(j - 3);
+    const bool ka = !CE || ca, kb = !CE || cb;
     // r_old at row j-1
-    RO[s1] = res<EDGE>(U[s2], U[s1], U[s0], F[s1], r1);
+    RO[s1] = res(U[s2], U[s1], U[s0], F[s1], r1, ka, kb);
     // green at row j-1: (x+1) on even rows, x on odd rows
     if (PAR == 1) {   // j-1 even: W = (x, y), S = (x+1, y-1), E = (x+2, y), N = (x+1, y+1)
       const T dE = shdn(Dv[s1]);
@@ -262,7 +297,7 @@ struct Strip {
       const T na = i0 ? U[s2].a + va : U[s2].a, nb = i1 ? U[s2].b + vb : U[s2].b;
       N[s2] = mkrow(na, nb);
       if (outl && y >= ys && y < ye) {
-        T *p = pun + (int64_t)y * pitch + x;
+        T *p = RE ? pun + (int64_t)y * pitch + x : stp;
         if (i0 && i1) {
           typename V2<T>::t v;
           v.x = na;
@@ -274,96 +309,113 @@ struct Strip {
       }
     }
     // r_new at row j-3 (rows j-4, j-3, j-2 of u_new)
-    R[s3] = res<EDGE>(N[s0], N[s3], N[s2], F[s3], r3);
-    if (outl && j - 3 >= ys && j - 3 < ye) mx = nmax(nmax(mx, absd(R[s3].a)), absd(R[s3].b));
+    R[s3] = res(N[s0], N[s3], N[s2], F[s3], r3, ka, kb);
+    if (outl && j - 3 >= ys && j - 3 < ye) {
+      const unsigned long long a = absbits(R[s3].a), b = absbits(R[s3].b), m = a > b ? a : b;
+      mx = m > mx ? m : mx;
+    }
     // Erest2r of the row pair (y, y+1) = (j-5, j-4) when y is even
     if (PAR == 1) {
       const int y = j - 5;
       const Pair<T> R6 = R[s2], R5 = R[s1], R4 = R[s0], R3 = R[s3];
       const T rW = shup(R5.b), rE = shdn(R4.a);
       if (outl && y >= ys && y < ye) {
-        const int64_t o = (int64_t)(y >> 1) * rp + (x >> 1);
-        if (!EDGE || (x >= 2 && x <= M - 2 && y >= 2 && y <= M - 2)) pre[o] = erest2r(R5.a, rW, R6.a, R5.b, R4.a);
-        if (!EDGE || (x + 1 <= M - 1 && y + 1 <= M - 1)) pro[o] = erest2r(R4.b, R4.a, R5.b, rE, R3.b);
+        const int64_t o = RE ? (int64_t)(y >> 1) * rp + (x >> 1) : rso;
+        if ((!CE || (x >= 2 && x <= M - 2)) && (!RE || (y >= 2 && y <= M - 2)))
+          pre[o] = erest2r(R5.a, rW, R6.a, R5.b, R4.a);
+        if ((!CE || x + 1 <= M - 1) && (!RE || y + 1 <= M - 1)) pro[o] = erest2r(R4.b, R4.a, R5.b, rE, R3.b);
       }
+      if (!RE) rso += rp;
     }
+    if (!RE) stp += pitch;
+  }
+  template <bool RE, bool CE>
+  __device__ __forceinline__ void steps(int j) {
+    step<0, RE, CE>(j);
+    step<1, RE, CE>(j + 1);
+    step<2, RE, CE>(j + 2);
+    step<3, RE, CE>(j + 3);
   }
 };
 
-template <class T, int ORDER, int WPB, int MINB>
-__global__ void __launch_bounds__(WPB * 32, MINB) asc_desc_stream(const __grid_constant__ XParams<T> P) {
+template <class T, int ORDER, int DEPTH, int MINB>
+__global__ void __launch_bounds__(32, MINB) asc_desc_stream(const __grid_constant__ XParams<T> P) {
   const int lane = threadIdx.x & 31;
-  const int item = blockIdx.x * WPB + (threadIdx.x >> 5);
+  const int item = blockIdx.x;
   const int nseg = (P.M + P.seg - 1) / P.seg;
-  double mx = 0.0;
+  unsigned long long mx = 0ull;
   if (item < P.nstrips * nseg) {   // warp-uniform
     const int strip = item % P.nstrips, sg = item / P.nstrips;
     const int ys = sg * P.seg, ye = min(ys + P.seg, P.M);
     extern __shared__ __align__(16) unsigned char xsm[];
-    Strip<T, ORDER> S(P, strip * SW - 4 + 2 * lane, ys, ye,
-                      xsm + (threadIdx.x >> 5) * (DEPTH * 32 * 5 * sizeof(T)) + lane * (2 * sizeof(T)));
+    Strip<T, ORDER, DEPTH> S(P, strip * SW - 4 + 2 * lane, ys, ye,
+                      xsm + lane * (2 * sizeof(T)));
     const int j0 = ys - 4, jend = ye + 3;   // steps j0 .. jend: ye - ys + 8 of them, a multiple of 4
 #pragma unroll
     for (int i = 0; i < DEPTH - 1; i++) S.issue(j0 + i);
-    // rows computed: [ys-7, ye+2]; columns: [x0-4, x0+59]
+    // A block of 4 steps j..j+3 is row-interior when every row it computes,
+    // restricts or loads lies inside: j >= 8 and j + 3 + DEPTH - 1 <= M.
+    // Column-interior warps: lanes' columns x0-4 .. x0+59 inside [1, M-1].
     const int x0 = strip * SW;
-    const bool edge = ys - 7 < 1 || ye + 2 > P.M - 1 || x0 - 4 < 1 || x0 + 59 > P.M - 1;
-    if (edge) {
-      for (int j = j0; j <= jend; j += 4) {
-        S.template step<0, true>(j);
-        S.template step<1, true>(j + 1);
-        S.template step<2, true>(j + 2);
-        S.template step<3, true>(j + 3);
-      }
-    } else {
-      for (int j = j0; j <= jend; j += 4) {
-        S.template step<0, false>(j);
-        S.template step<1, false>(j + 1);
-        S.template step<2, false>(j + 2);
-        S.template step<3, false>(j + 3);
+    const bool ce = x0 - 4 < 1 || x0 + 59 > P.M - 1;
+    auto rowin = [&](int j) { return j >= 8 && j + 3 + DEPTH - 1 <= P.M; };
+    int j = j0;
+    for (; j <= jend && !rowin(j); j += 4) S.template steps<true, true>(j);
+    if (j <= jend) {
+      S.start(j);
+      if (ce) {
+        for (; j <= jend && rowin(j); j += 4) S.template steps<false, true>(j);
+      } else {
+        for (; j <= jend && rowin(j); j += 4) S.template steps<false, false>(j);
       }
     }
+    for (; j <= jend; j += 4) S.template steps<true, true>(j);
     mx = S.mx;
   }
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) mx = nmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-  if (lane == 0 && item < P.nstrips * nseg) norm_push(P.ns, mx);
+  for (int o = 16; o > 0; o >>= 1) {
+    const unsigned long long w = __shfl_xor_sync(0xffffffffu, mx, o);
+    mx = w > mx ? w : mx;
+  }
+  if (lane == 0 && item < P.nstrips * nseg) norm_push(P.ns, __longlong_as_double((long long)mx));
 }
 
 }  // namespace xf
 
-template <class T, int ORDER, int WPB, int MINB>
+template <class T, int ORDER, int DEPTH, int MINB>
 static cudaError_t asc_desc_launch_w(const xf::XParams<T> &P0, cudaStream_t st) {
-  constexpr int SMEM = WPB * xf::DEPTH * 32 * 5 * sizeof(T);
+  constexpr int SMEM = DEPTH * 32 * 5 * sizeof(T);
   static int wres = 0, sms = 0;
   if (!wres) {
     int dev = 0, nb = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, xf::asc_desc_stream<T, ORDER, WPB, MINB>, WPB * 32, SMEM);
-    wres = nb > 0 ? nb * WPB : WPB;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, xf::asc_desc_stream<T, ORDER, DEPTH, MINB>, 32, SMEM);
+    wres = nb > 0 ? nb : 1;
     if (sms <= 0) sms = 148;
   }
   xf::XParams<T> P = P0;
-  // one wave: about sms * wres warps, a segment of >= 32 rows (multiple of 4) each
-  const int S = (sms * wres + P.nstrips - 1) / P.nstrips;
+  // exactly one wave: at most sms * wres warps (a second, partial wave would
+  // double the tail), a segment of >= 32 rows (multiple of 4) each
+  const int S = max(1, (sms * wres) / P.nstrips);
   int seg = (P.M + S - 1) / S;
   seg = (seg + 3) / 4 * 4;
   if (seg < 32) seg = 32;
   P.seg = seg;
   const int nitems = P.nstrips * ((P.M + seg - 1) / seg);
-  const int grid = (nitems + WPB - 1) / WPB;
-  xf::asc_desc_stream<T, ORDER, WPB, MINB><<<grid, WPB * 32, SMEM, st>>>(P);
+  xf::asc_desc_stream<T, ORDER, DEPTH, MINB><<<nitems, 32, SMEM, st>>>(P);
   return cudaGetLastError();
 }
 
-// one warp per block: registers are allocated per block, so 1-warp blocks
-// fill an SM to the register limit (measured: 2- and 4-warp blocks leave
-// 3-4 warps per SM unused and run 60 % slower; capping the registers at 128
-// to fit 16 warps spills the pipeline state and is slower still)
+// One warp per block: registers are allocated per block, so 1-warp blocks
+// fill an SM to the register limit (2- and 4-warp blocks left 3-4 warps per
+// SM unused and ran 60 % slower).  Order 2 caps the registers at 128 (16
+// warps per SM, no spills); measured alternatives: a 16-row ring (fp64 +5 %,
+// fp32 +4 % time), 24 warps per SM with 80 registers (spills: fp64 +50 %,
+// fp32 +2 %).
 template <class T, int ORDER>
 static cudaError_t asc_desc_launch(const xf::XParams<T> &P, cudaStream_t st) {
-  return asc_desc_launch_w<T, ORDER, 1, 1>(P, st);
+  return asc_desc_launch_w<T, ORDER, 8, (ORDER == 2 ? 16 : 1)>(P, st);
 }
 
 template <class T>
