@@ -114,10 +114,10 @@ __global__ void __launch_bounds__(1024) k2_coarse(const Lev2<T> *lv, int oc, int
     const Lev2<T> L = lv[o];
     const Lev2<T> Lc = lv[o + 1];
     int64_t n = (int64_t)(L.M / 2 + 1) * (L.M / 2 + 1);
-    for (int64_t t = tid; t < n; t += bs) node_rest_ad(D2<const T>{L.rA.p, L.rA.pitch}, L.rD, L.M, t);
+    for (int t = tid; t < (int)n; t += bs) node_rest_ad(D2<const T>{L.rA.p, L.rA.pitch}, L.rD, L.M, t);
     __syncthreads();
     n = (int64_t)(Lc.M - 1) * (Lc.M - 1);
-    for (int64_t t = tid; t < n; t += bs) node_rest_da(S2<const T>{L.rD.e, L.rD.o, L.rD.pitch}, Lc.rA, Lc.M, t);
+    for (int t = tid; t < (int)n; t += bs) node_rest_da(S2<const T>{L.rD.e, L.rD.o, L.rD.pitch}, Lc.rA, Lc.M, t);
     __syncthreads();
   }
   if (tid == 0) {
@@ -131,17 +131,17 @@ __global__ void __launch_bounds__(1024) k2_coarse(const Lev2<T> *lv, int oc, int
     const int M = L.M;
     S2<const T> rD{L.rD.e, L.rD.o, L.rD.pitch};
     int64_t n = (int64_t)(M / 2) * (M / 2);
-    for (int64_t t = tid; t < n; t += bs) node_jac_d1(D2<const T>{Lc.vA.p, Lc.vA.pitch}, rD, L.vD, M, L.cD, t);
+    for (int t = tid; t < (int)n; t += bs) node_jac_d1(D2<const T>{Lc.vA.p, Lc.vA.pitch}, rD, L.vD, M, L.cD, t);
     __syncthreads();
     n = (int64_t)(M / 2 - 1) * (M / 2 - 1);
-    for (int64_t t = tid; t < n; t += bs) node_jac_d2(rD, L.vD, M, L.cD, t);
+    for (int t = tid; t < (int)n; t += bs) node_jac_d2(rD, L.vD, M, L.cD, t);
     __syncthreads();
     n = (int64_t)(M - 1) * (M - 1);
     S2<const T> vD{L.vD.e, L.vD.o, L.vD.pitch};
     D2<const T> rA{L.rA.p, L.rA.pitch};
-    for (int64_t t = tid; t < n; t += bs) node_jac_a1(vD, rA, L.vA, M, L.cA, t);
+    for (int t = tid; t < (int)n; t += bs) node_jac_a1(vD, rA, L.vA, M, L.cA, t);
     __syncthreads();
-    for (int64_t t = tid; t < n; t += bs) node_jac_a2(rA, L.vA, M, L.cA, t);
+    for (int t = tid; t < (int)n; t += bs) node_jac_a2(rA, L.vA, M, L.cA, t);
     __syncthreads();
   }
 }
@@ -178,10 +178,10 @@ __global__ void __launch_bounds__(1024) k2_coarse_smem(const Lev2<T> *lvg, int o
     const Lev2<T> L = lv[o];
     const Lev2<T> Lc = lv[o + 1];
     int64_t n = (int64_t)(L.M / 2 + 1) * (L.M / 2 + 1);
-    for (int64_t t = tid; t < n; t += bs) node_rest_ad(D2<const T>{L.rA.p, L.rA.pitch}, L.rD, L.M, t);
+    for (int t = tid; t < (int)n; t += bs) node_rest_ad(D2<const T>{L.rA.p, L.rA.pitch}, L.rD, L.M, t);
     __syncthreads();
     n = (int64_t)(Lc.M - 1) * (Lc.M - 1);
-    for (int64_t t = tid; t < n; t += bs) node_rest_da(S2<const T>{L.rD.e, L.rD.o, L.rD.pitch}, Lc.rA, Lc.M, t);
+    for (int t = tid; t < (int)n; t += bs) node_rest_da(S2<const T>{L.rD.e, L.rD.o, L.rD.pitch}, Lc.rA, Lc.M, t);
     __syncthreads();
   }
   if (tid == 0) {
@@ -195,17 +195,17 @@ __global__ void __launch_bounds__(1024) k2_coarse_smem(const Lev2<T> *lvg, int o
     const int M = L.M;
     S2<const T> rD{L.rD.e, L.rD.o, L.rD.pitch};
     int64_t n = (int64_t)(M / 2) * (M / 2);
-    for (int64_t t = tid; t < n; t += bs) node_jac_d1(D2<const T>{Lc.vA.p, Lc.vA.pitch}, rD, L.vD, M, L.cD, t);
+    for (int t = tid; t < (int)n; t += bs) node_jac_d1(D2<const T>{Lc.vA.p, Lc.vA.pitch}, rD, L.vD, M, L.cD, t);
     __syncthreads();
     n = (int64_t)(M / 2 - 1) * (M / 2 - 1);
-    for (int64_t t = tid; t < n; t += bs) node_jac_d2(rD, L.vD, M, L.cD, t);
+    for (int t = tid; t < (int)n; t += bs) node_jac_d2(rD, L.vD, M, L.cD, t);
     __syncthreads();
     n = (int64_t)(M - 1) * (M - 1);
     S2<const T> vD{L.vD.e, L.vD.o, L.vD.pitch};
     D2<const T> rA{L.rA.p, L.rA.pitch};
-    for (int64_t t = tid; t < n; t += bs) node_jac_a1(vD, rA, L.vA, M, L.cA, t);
+    for (int t = tid; t < (int)n; t += bs) node_jac_a1(vD, rA, L.vA, M, L.cA, t);
     __syncthreads();
-    for (int64_t t = tid; t < n; t += bs) node_jac_a2(rA, L.vA, M, L.cA, t);
+    for (int t = tid; t < (int)n; t += bs) node_jac_a2(rA, L.vA, M, L.cA, t);
     __syncthreads();
   }
 }
@@ -243,10 +243,10 @@ __device__ __forceinline__ void coarse2_block(const Tail2<T> &P, T *arena) {
     T *b = off(o);
     const S2<T> rD{b, b + n2, W};
     const D2<T> rA = aa(o, 0), rA2 = aa(o + 1, 0);
-    for (int64_t t = tid; t < (int64_t)n2; t += bs) node_rest_ad(D2<const T>{rA.p, rA.pitch}, rD, M, t);
+    for (int t = tid; t < (int)n2; t += bs) node_rest_ad(D2<const T>{rA.p, rA.pitch}, rD, M, t);
     __syncthreads();
     const int64_t n = (int64_t)(M / 2 - 1) * (M / 2 - 1);
-    for (int64_t t = tid; t < n; t += bs) node_rest_da(S2<const T>{rD.e, rD.o, rD.pitch}, rA2, M / 2, t);
+    for (int t = tid; t < (int)n; t += bs) node_rest_da(S2<const T>{rD.e, rD.o, rD.pitch}, rA2, M / 2, t);
     __syncthreads();
   }
   if (tid == 0) {
@@ -262,17 +262,17 @@ __device__ __forceinline__ void coarse2_block(const Tail2<T> &P, T *arena) {
     const S2<T> vD{b + 2 * n2, b + 3 * n2, W};
     const D2<T> rA = aa(o, 0), vA = aa(o, 1), vA2 = aa(o + 1, 1);
     int64_t n = (int64_t)(M / 2) * (M / 2);
-    for (int64_t t = tid; t < n; t += bs) node_jac_d1(D2<const T>{vA2.p, vA2.pitch}, rD, vD, M, L.cD, t);
+    for (int t = tid; t < (int)n; t += bs) node_jac_d1(D2<const T>{vA2.p, vA2.pitch}, rD, vD, M, L.cD, t);
     __syncthreads();
     n = (int64_t)(M / 2 - 1) * (M / 2 - 1);
-    for (int64_t t = tid; t < n; t += bs) node_jac_d2(rD, vD, M, L.cD, t);
+    for (int t = tid; t < (int)n; t += bs) node_jac_d2(rD, vD, M, L.cD, t);
     __syncthreads();
     n = (int64_t)(M - 1) * (M - 1);
     const S2<const T> vDc{vD.e, vD.o, vD.pitch};
     const D2<const T> rAc{rA.p, rA.pitch};
-    for (int64_t t = tid; t < n; t += bs) node_jac_a1(vDc, rAc, vA, M, L.cA, t);
+    for (int t = tid; t < (int)n; t += bs) node_jac_a1(vDc, rAc, vA, M, L.cA, t);
     __syncthreads();
-    for (int64_t t = tid; t < n; t += bs) node_jac_a2(rAc, vA, M, L.cA, t);
+    for (int t = tid; t < (int)n; t += bs) node_jac_a2(rAc, vA, M, L.cA, t);
     __syncthreads();
   }
 }
@@ -286,10 +286,10 @@ __global__ void __launch_bounds__(512, 1) k2_tail(const __grid_constant__ Tail2<
   for (int o = P.om; o < P.oc; o++) {
     const Lev2<T> &L = P.lv[o], &Lc = P.lv[o + 1];
     int64_t n = (int64_t)(L.M / 2 + 1) * (L.M / 2 + 1);
-    for (int64_t t = gt; t < n; t += gs) node_rest_ad(D2<const T>{L.rA.p, L.rA.pitch}, L.rD, L.M, t);
+    for (int t = gt; t < (int)n; t += gs) node_rest_ad(D2<const T>{L.rA.p, L.rA.pitch}, L.rD, L.M, t);
     grid.sync();
     n = (int64_t)(Lc.M - 1) * (Lc.M - 1);
-    for (int64_t t = gt; t < n; t += gs) node_rest_da(S2<const T>{L.rD.e, L.rD.o, L.rD.pitch}, Lc.rA, Lc.M, t);
+    for (int t = gt; t < (int)n; t += gs) node_rest_da(S2<const T>{L.rD.e, L.rD.o, L.rD.pitch}, Lc.rA, Lc.M, t);
     grid.sync();
   }
   if (blockIdx.x == 0) coarse2_block(P, (T *)dsm);
@@ -299,17 +299,17 @@ __global__ void __launch_bounds__(512, 1) k2_tail(const __grid_constant__ Tail2<
     const int M = L.M;
     const S2<const T> rD{L.rD.e, L.rD.o, L.rD.pitch};
     int64_t n = (int64_t)(M / 2) * (M / 2);
-    for (int64_t t = gt; t < n; t += gs) node_jac_d1(D2<const T>{Lc.vA.p, Lc.vA.pitch}, rD, L.vD, M, L.cD, t);
+    for (int t = gt; t < (int)n; t += gs) node_jac_d1(D2<const T>{Lc.vA.p, Lc.vA.pitch}, rD, L.vD, M, L.cD, t);
     grid.sync();
     n = (int64_t)(M / 2 - 1) * (M / 2 - 1);
-    for (int64_t t = gt; t < n; t += gs) node_jac_d2(rD, L.vD, M, L.cD, t);
+    for (int t = gt; t < (int)n; t += gs) node_jac_d2(rD, L.vD, M, L.cD, t);
     grid.sync();
     n = (int64_t)(M - 1) * (M - 1);
     const S2<const T> vD{L.vD.e, L.vD.o, L.vD.pitch};
     const D2<const T> rA{L.rA.p, L.rA.pitch};
-    for (int64_t t = gt; t < n; t += gs) node_jac_a1(vD, rA, L.vA, M, L.cA, t);
+    for (int t = gt; t < (int)n; t += gs) node_jac_a1(vD, rA, L.vA, M, L.cA, t);
     grid.sync();
-    for (int64_t t = gt; t < n; t += gs) node_jac_a2(rA, L.vA, M, L.cA, t);
+    for (int t = gt; t < (int)n; t += gs) node_jac_a2(rA, L.vA, M, L.cA, t);
     grid.sync();
   }
 }

@@ -118,8 +118,8 @@ __device__ __forceinline__ T jac4(T c, T r, T v1, T v2, T v3, T v4) {
 
 // a2: Erest2r from the dense A(s) residual onto D(s); t over (M/2+1)^2,
 // writes E(a,b) = node (2a,2b) and O(a,b) = node (2a+1,2b+1) when interior.
-template <class T>
-__device__ __forceinline__ void node_rest_ad(const D2<const T> &r, const S2<T> &d, int M, int64_t t) {
+template <class T, class I>
+__device__ __forceinline__ void node_rest_ad(const D2<const T> &r, const S2<T> &d, int M, I t) {
   int H = M / 2 + 1;
   int a = (int)(t % H), b = (int)(t / H);
   int x = 2 * a, y = 2 * b;
@@ -133,8 +133,8 @@ __device__ __forceinline__ void node_rest_ad(const D2<const T> &r, const S2<T> &
 
 // a3: Erest2b from D(s) onto A(2s); coarse node (X,Y) is lattice node
 // (2X,2Y); t over (Mc-1)^2.
-template <class T>
-__device__ __forceinline__ void node_rest_da(const S2<const T> &d, const D2<T> &r, int Mc, int64_t t) {
+template <class T, class I>
+__device__ __forceinline__ void node_rest_da(const S2<const T> &d, const D2<T> &r, int Mc, I t) {
   int W = Mc - 1;
   int X = (int)(t % W) + 1, Y = (int)(t / W) + 1;
   int x = 2 * X, y = 2 * Y;
@@ -150,9 +150,9 @@ __device__ __forceinline__ void node_coarsest(const D2<const T> &r, const D2<T> 
 
 // a5: colour 1 on O (nodes of D(s) not on A(2s)): Eajacr from
 // the coarse A(2s) values at the 4 diagonal neighbours; t over (M/2)^2.
-template <class T>
+template <class T, class I>
 __device__ __forceinline__ void node_jac_d1(const D2<const T> &vc, const S2<const T> &r, const S2<T> &v, int M, T c,
-                                            int64_t t) {
+                                            I t) {
   int W = M / 2;
   int a = (int)(t % W), b = (int)(t / W);
   int x = 2 * a + 1, y = 2 * b + 1;
@@ -163,8 +163,8 @@ __device__ __forceinline__ void node_jac_d1(const D2<const T> &vc, const S2<cons
 
 // a6: colour 2 on E (= A(2s) positions): Eajacb from the new O
 // values; uses the D(s) residual at that node (reading A10); t over (M/2-1)^2.
-template <class T>
-__device__ __forceinline__ void node_jac_d2(const S2<const T> &r, const S2<T> &v, int M, T c, int64_t t) {
+template <class T, class I>
+__device__ __forceinline__ void node_jac_d2(const S2<const T> &r, const S2<T> &v, int M, T c, I t) {
   int W = M / 2 - 1;
   int a = (int)(t % W) + 1, b = (int)(t / W) + 1;
   int x = 2 * a, y = 2 * b;
@@ -175,17 +175,17 @@ __device__ __forceinline__ void node_jac_d2(const S2<const T> &r, const S2<T> &v
 // a7 (s > 1): colour 1 on the green-only nodes (x+y odd) from D(s), colour 2
 // on the D(s) nodes from the new green values ("similarly for a green grid",
 // P:228-230; reading A5), c = p (sh)^2; t over (M-1)^2.
-template <class T>
+template <class T, class I>
 __device__ __forceinline__ void node_jac_a1(const S2<const T> &vd, const D2<const T> &r, const D2<T> &v, int M, T c,
-                                            int64_t t) {
+                                            I t) {
   int W = M - 1;
   int x = (int)(t % W) + 1, y = (int)(t / W) + 1;
   if (((x + y) & 1) == 0) return;
   v(x, y) = jac4(c, r(x, y), vd.get(x - 1, y), vd.get(x, y - 1), vd.get(x + 1, y), vd.get(x, y + 1));
 }
 
-template <class T>
-__device__ __forceinline__ void node_jac_a2(const D2<const T> &r, const D2<T> &v, int M, T c, int64_t t) {
+template <class T, class I>
+__device__ __forceinline__ void node_jac_a2(const D2<const T> &r, const D2<T> &v, int M, T c, I t) {
   int W = M - 1;
   int x = (int)(t % W) + 1, y = (int)(t / W) + 1;
   if (((x + y) & 1) == 1) return;
