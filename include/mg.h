@@ -159,6 +159,19 @@ typedef struct {
 } mg_step_stat;
 int mg_profile(mg_solver *s, void *u, const void *f, int ncycles, mg_step_stat *out, int cap);
 
+/* Convergence factor of the V-cycle (the paper's rho-bar,
+ * "the largest eigenvalue" of the iteration operator, reading A12):
+ * power iteration on the error equation.  e is a DEVICE array (layout of u,
+ * boundary 0, not all zero) holding the start error; it is normalised, then
+ * `iters` times replaced by one V-cycle of it with f = 0, rescaled to unit
+ * L2 norm on the device.  ratios (NULL or room for iters doubles) receives
+ * ||e_k|| / ||e_{k-1}|| per iteration; *rho = their geometric mean over the
+ * second half of the iterations (-> the spectral radius when the dominant
+ * eigenvalue is separated; a complex pair still gives its modulus).  On
+ * return e holds the normalised last iterate (the slowest error mode).
+ * Single GPU (MG_EUNSUPPORTED for nranks > 1); iters >= 2.  Synchronises. */
+int mg_convergence_factor(mg_solver *s, void *e, int iters, double *rho, double *ratios);
+
 /* The slab decomposition without a device (host-only planning): rows [lo, hi)
  * owned by `rank`, ghost rows carried on each side, and the first octave
  * whose levels are agglomerated (all-gathered).  nranks = 1: the whole grid.

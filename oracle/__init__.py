@@ -159,3 +159,24 @@ def vcycle(u: np.ndarray, f: np.ndarray, p, ncycles: int, order: int = 2, hist: 
     if rc != 0:
         raise RuntimeError(f"orc_vcycle failed rc={rc}")
     return np.array(list(h)) if hist else None
+
+
+def convergence_factor(e: np.ndarray, p, iters: int, order: int = 2):
+    """The paper's convergence factor rho-bar, "the largest eigenvalue" of the
+    V-cycle iteration operator (reading A12: spectral radius), by
+    power iteration on the error equation (f = 0): normalise e (L2 over all
+    nodes; the boundary is zero), then ``iters`` times: one V-cycle of e with
+    f = 0, ratio_k = ||e||_2, e <- e * (1 / ratio_k) (the factor formed in
+    fp64, the product in e's precision).  Returns (rho, ratios), rho = the
+    geometric mean of the ratios of the second half.  In place on e."""
+    f = np.zeros_like(e)
+    nrm = float(np.sqrt(np.sum(e.astype(np.float64) ** 2)))
+    e[...] = e * e.dtype.type(1.0 / nrm)
+    ratios = np.empty(iters)
+    for k in range(iters):
+        vcycle(e, f, p, 1, order=order)
+        nrm = float(np.sqrt(np.sum(e.astype(np.float64) ** 2)))
+        ratios[k] = nrm
+        e[...] = e * e.dtype.type(1.0 / nrm)
+    tail = ratios[iters // 2:]
+    return float(np.exp(np.mean(np.log(tail)))), ratios

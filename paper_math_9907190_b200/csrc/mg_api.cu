@@ -701,6 +701,19 @@ static int check_config(const mg_config *c, int *k_out) {
 }
 
 // =================================================================== ABI
+__global__ void k_rate_norm(const double *ss, double *ratios, int k, double *prev, double *inv) {
+  const double nrm = sqrt(*ss);
+  ratios[k] = nrm / *prev;
+  *inv = nrm > 0.0 ? 1.0 / nrm : 0.0;
+  *prev = 1.0;
+}
+template <class T>
+__global__ void k_rate_scale(const T *src, T *dst, size_t n, const double *inv) {
+  const T f = (T)*inv;
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
+    dst[i] = src[i] * f;
+}
+
 extern "C" {
 
 int mg_create_ex(const mg_config *cfg, mg_solver **out) {
@@ -799,6 +812,7 @@ int mg_destroy(mg_solver *s) {
   cudaFree(s->d_hist);
   cudaFree(s->d_counter);
   cudaFree(s->d_mx);
+  if (s->d_zero) cudaFree(s->d_zero);
   cudaFree(s->d_ss);
   cudaFree(s->d_ft);
   cudaFree(s->d_u_stage);
@@ -945,6 +959,77 @@ int mg_vcycle_host(mg_solver *s, void *u_host, const void *f_host, int ncycles, 
   CKS(s, cudaMemcpyAsync(u_host, s->d_u_stage, bytes, cudaMemcpyDeviceToHost, s->st));
   CKS(s, cudaStreamSynchronize(s->st));
   return end(s);
+}
+
+// ---------------------------------------------------- convergence factor
+// power iteration on the error equation (f = 0), every
+// step on the device.  One iteration: one V-cycle e -> e' (no cross-cycle
+// fusion: e is rescaled between cycles), ss = sum e'^2 over the interior
+// (the norm kernel), then k_rate_scale: ratio_k = sqrt(ss) / prev, e = e' /
+// sqrt(ss), prev = 1.
+int mg_convergence_factor(mg_solver *s, void *e, int iters, double *rho, double *ratios) {
+  if (!s) return MG_EINVAL;
+  if (!e || iters < 2 || !rho) return fail(s, MG_EINVAL, "mg_convergence_factor: bad argument");
+  if (s->cfg.nranks > 1) return fail(s, MG_EUNSUPPORTED, "mg_convergence_factor: single GPU only");
+  DeviceGuard g(s->device);
+  int rc = begin(s);
+  if (rc) return rc;
+  const size_t ne = s->field_elems(), bytes = ne * s->esz;
+  if (!s->d_zero) {
+    CKS(s, cudaMalloc(&s->d_zero, bytes));
+    CKS(s, cudaMemsetAsync(s->d_zero, 0, bytes, s->st));
+  }
+  const bool alt = s->impl->fast() && aligned16(e);
+  if (alt && !s->d_ualt) {
+    CKS(s, cudaMalloc(&s->d_ualt, bytes));
+    CKS(s, cudaMemsetAsync(s->d_ualt, 0, bytes, s->st));
+  }
+  double *d_rate = nullptr;   // [0] prev, [1] 1/norm, [2 ..] ratios
+  CKS(s, cudaMalloc(&d_rate, sizeof(double) * (iters + 3)));
+  const double one = 1.0;
+  // normalise the start vector first (ratio 0 of the history is its norm)
+  CKS(s, cudaMemcpyAsync(d_rate, &one, sizeof one, cudaMemcpyHostToDevice, s->st));
+  CKS(s, cudaMemsetAsync(s->d_mx, 0, sizeof(unsigned long long), s->st));
+  CKS(s, cudaMemsetAsync(s->d_ss, 0, sizeof(double), s->st));
+  s->impl->enqueue_norm(e, s->d_mx, s->d_ss, s->st);
+  k_rate_norm<<<1, 1, 0, s->st>>>(s->d_ss, d_rate + 2, 0, d_rate, d_rate + 1);
+  const int nb = 148 * 8;
+  if (s->esz == 8)
+    k_rate_scale<double><<<nb, 256, 0, s->st>>>((const double *)e, (double *)e, ne, d_rate + 1);
+  else
+    k_rate_scale<float><<<nb, 256, 0, s->st>>>((const float *)e, (float *)e, ne, d_rate + 1);
+  CKS(s, cudaMemsetAsync(s->d_counter, 0, sizeof(int), s->st));
+  for (int it = 1; it <= iters; it++) {
+    void *dst = alt ? s->d_ualt : e;
+    rc = run_cycle(s, e, dst, s->d_zero, 0);
+    if (rc) {
+      cudaFree(d_rate);
+      return rc;
+    }
+    CKS(s, cudaMemsetAsync(s->d_mx, 0, sizeof(unsigned long long), s->st));
+    CKS(s, cudaMemsetAsync(s->d_ss, 0, sizeof(double), s->st));
+    s->impl->enqueue_norm(dst, s->d_mx, s->d_ss, s->st);
+    k_rate_norm<<<1, 1, 0, s->st>>>(s->d_ss, d_rate + 2, it, d_rate, d_rate + 1);
+    if (s->esz == 8)
+      k_rate_scale<double><<<nb, 256, 0, s->st>>>((const double *)dst, (double *)e, ne, d_rate + 1);
+    else
+      k_rate_scale<float><<<nb, 256, 0, s->st>>>((const float *)dst, (float *)e, ne, d_rate + 1);
+  }
+  std::vector<double> h(iters + 1);
+  CKS(s, cudaMemcpyAsync(h.data(), d_rate + 2, sizeof(double) * (iters + 1), cudaMemcpyDeviceToHost, s->st));
+  CKS(s, cudaStreamSynchronize(s->st));
+  cudaFree(d_rate);
+  rc = end(s);
+  if (rc) return rc;
+  // geometric mean of the ratios of the second half of the iterations
+  double lg = 0.0;
+  int m = 0;
+  for (int it = iters / 2 + 1; it <= iters; it++, m++) lg += std::log(h[it]);
+  *rho = std::exp(lg / m);
+  if (ratios)
+    for (int it = 0; it < iters; it++) ratios[it] = h[it + 1];
+  if (!std::isfinite(*rho)) return fail(s, MG_EDIVERGED, "mg_convergence_factor: non-finite ratio");
+  return MG_OK;
 }
 
 int mg_norm(mg_solver *s, const void *x, int kind, double *out) {

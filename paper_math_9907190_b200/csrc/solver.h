@@ -177,6 +177,7 @@ struct mg_solver {
   };
   std::vector<GraphEntry> graphs;   // captured cycles keyed by pointers
   void *d_ualt = nullptr;            // out-of-place partner of the caller's u
+  void *d_zero = nullptr;            // zero right-hand side (mg_convergence_factor)
   unsigned long long *h_hist = nullptr;    // pinned
   std::string err;
   size_t field_elems() const {

@@ -73,6 +73,8 @@ EXPORTS = {
     "mg_launches_per_cycle": (ctypes.c_int, [ctypes.c_void_p]),
     "mg_profile": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int,
                                   ctypes.POINTER(mg_step_stat), ctypes.c_int]),
+    "mg_convergence_factor": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int,
+                                             ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double)]),
     "mg_slab_plan": (ctypes.c_int, [ctypes.c_int, ctypes.c_int64, ctypes.c_int, ctypes.c_int, ctypes.c_int64,
                                     ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_int64),
                                     ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_int)]),
@@ -178,6 +180,15 @@ def mg_profile(h, u_ptr: int, f_ptr: int, ncycles: int, cap: int = 256):
         _check(rc, h, "mg_profile")
     return [dict(name=b.name.decode(), level=b.level, launches=b.launches, ms=b.ms, alg_bytes=b.alg_bytes)
             for b in buf[: min(rc, cap)]]
+
+
+def mg_convergence_factor(h, e_ptr: int, iters: int):
+    """Power iteration of the V-cycle on the error equation (include/mg.h):
+    returns (rho, per-iteration ratios)."""
+    rho = ctypes.c_double()
+    buf = (ctypes.c_double * iters)()
+    _check(load().mg_convergence_factor(h, e_ptr, iters, ctypes.byref(rho), buf), h, "mg_convergence_factor")
+    return rho.value, np.array(list(buf))
 
 
 def mg_slab_plan(dim: int, n: int, nranks: int, rank: int, agglom_points: int = 0):
@@ -331,6 +342,11 @@ class Solver:
 
     def profile(self, u, f, ncycles: int = 5):
         return mg_profile(self.h, self._chk(u), self._chk(f), ncycles)
+
+    def convergence_factor(self, e, iters: int = 100):
+        """rho-bar of the V-cycle by power iteration from the start error e
+        (a device tensor of ``self.shape``, overwritten by the slowest mode)."""
+        return mg_convergence_factor(self.h, self._chk(e), iters)
 
     @property
     def levels(self) -> int:

@@ -81,3 +81,8 @@ def test_no_cpu_fallback_without_gpu(lib):
         pytest.skip("GPU present")
     h = ctypes.c_void_p()
     assert lib.mg_create(2, 17, 2, 1.0, ctypes.byref(h)) == mg.MG_ENODEV
+
+
+def test_convergence_factor_rejects_null_handle(lib):
+    rho = ctypes.c_double()
+    assert lib.mg_convergence_factor(None, None, 10, ctypes.byref(rho), None) == mg.MG_EINVAL

@@ -444,6 +444,28 @@ def test_convergence_factor_matches_paper(row):
     assert _rho(dim, n, p, order) == pytest.approx(want, abs=tol)
 
 
+@pytest.mark.parametrize("row", _load("paper_tables.txt"), ids=lambda r: "-".join(r[:4]))
+def test_power_iteration_matches_paper(row):
+    """The oracle's power iteration (oracle.convergence_factor, the reference
+    of the GPU's mg_convergence_factor) reproduces Tables 1-3 (P:292-298,
+    709-712, 786-792) within the same windows as the ARPACK eigenvalue."""
+    dim, n, order = int(row[0]), int(row[1]), int(row[2])
+    p = [float(t) for t in row[3].split(",")]
+    p = p[0] if dim == 2 else tuple(p)
+    want, tol = float(row[4]), float(row[5])
+    rho, ratios = oracle.convergence_factor(W.random_field(dim, n, seed=3), p, 200, order=order)
+    assert rho == pytest.approx(want, abs=tol)
+    assert len(ratios) == 200 and np.all(ratios > 0)
+
+
+def test_power_iteration_agrees_with_arpack():
+    """Where the dominant eigenvalue is real and separated, the power-iteration
+    ratio converges to ARPACK's spectral radius (an independent route)."""
+    for dim, n, p, order in [(2, 33, 1.0, 2), (3, 9, (1.0, 1.0, 1.0, 1.0), 2)]:
+        rho, _ = oracle.convergence_factor(W.random_field(dim, n, seed=4), p, 300, order=order)
+        assert rho == pytest.approx(_rho(dim, n, p, order), rel=5e-3)
+
+
 def test_optimal_p_is_linear_in_p():
     """the correction is exactly p times the p = 1 correction
     (every v is created by one -c r injection), so the error operator is
