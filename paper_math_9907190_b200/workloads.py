@@ -86,6 +86,12 @@ def discrete_laplacian(u: np.ndarray) -> np.ndarray:
     return out
 
 
+def smooth_rhs(dim: int, n: int) -> np.ndarray:
+    """Problem data for accuracy studies: f = continuous Laplacian of
+    u* = prod sin(pi x_d), i.e. -dim pi^2 u*, at every node (0 on the boundary)."""
+    return -dim * np.pi ** 2 * manufactured_u(dim, n)
+
+
 def make_rhs(dim: int, n: int, kind: str, seed: int, noise: float = 1e-3) -> np.ndarray:
     """Right-hand side f (float64)."""
     rng = np.random.default_rng(seed)
