@@ -81,6 +81,13 @@ enum { MG_F64 = 0, MG_F32 = 1 };
 /* mg_config.flags */
 enum { MG_FLAG_LOOPBACK = 1 };  /* nranks virtual ranks in this process on one GPU (tests the slab
                                    decomposition; caller passes FULL arrays) */
+enum { MG_FLAG_CONVENTIONAL = 2 };  /* the paper's "usual" multigrid instead of the diagonal one (SURVEY
+                                       8(f) NEXT-3): V(0,1) on
+                                       the factor-2 hierarchy, full weighting (9-/27-point), bi/trilinear
+                                       interpolation, one two-colour Jacobi sweep per level (DESIGN.md
+                                       reading A18), over-relaxation p = p[0] (2D) / p[3] (3D) on the
+                                       residual term.  Single GPU; every call of this header applies
+                                       (mg_num_levels / mg_level_points describe the diagonal hierarchy). */
 enum { MG_NORM_INF = 0, MG_NORM_L2 = 1 };
 
 typedef struct {

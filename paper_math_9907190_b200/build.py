@@ -13,7 +13,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libmg.so")
-SOURCES = ["mg_api.cu", "k2d.cu", "k2f.cu", "k2x.cu", "k3d.cu", "k3f.cu", "k3p.cu", "k3s.cu", "k3l.cu", "comm.cu", "dist2.cu", "dist3.cu", "tma_host.cu"]
+SOURCES = ["mg_api.cu", "conv.cu", "k2d.cu", "k2f.cu", "k2x.cu", "k3d.cu", "k3f.cu", "k3p.cu", "k3s.cu", "k3l.cu", "comm.cu", "dist2.cu", "dist3.cu", "tma_host.cu"]
 HEADERS = ["zpipe.cuh", "common.cuh", "kernels.h", "ops2.cuh", "ops3.cuh", "tma.cuh", "solver.h", "comm.h"]
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

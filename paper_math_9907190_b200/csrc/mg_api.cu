@@ -754,7 +754,13 @@ int mg_create_ex(const mg_config *cfg, mg_solver **out) {
   CKS(sp, cudaMemset(s->d_hist, 0, sizeof(unsigned long long) * kHistCap));
   CKS(sp, cudaMemset(s->d_counter, 0, sizeof(int)));
   CKS(sp, cudaMallocHost(&s->h_hist, sizeof(unsigned long long) * kHistCap));
-  if (cfg->nranks > 1) {
+  if (cfg->flags & MG_FLAG_CONVENTIONAL) {
+    if (cfg->nranks > 1) {
+      mg_destroy(s.release());
+      return MG_EUNSUPPORTED;
+    }
+    s->impl.reset(make_conv(sp));
+  } else if (cfg->nranks > 1) {
     std::string why;
     const bool lb = (cfg->flags & MG_FLAG_LOOPBACK) != 0;
     ImplBase *d = cfg->dim == 2 ? make_dist2(sp, lb, &why) : make_dist3(sp, lb, &why);

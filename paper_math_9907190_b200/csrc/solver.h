@@ -186,6 +186,11 @@ struct mg_solver {
   }
 };
 
+// conv.cu: the paper's "usual" V(0,1) multigrid (MG_FLAG_CONVENTIONAL, NEXT-3)
+namespace mg {
+ImplBase *make_conv(const mg_solver *s);
+}
+
 static int fail(mg_solver *s, int code, const std::string &msg) {
   if (s) s->err = msg;
   return code;
@@ -198,4 +203,3 @@ static int fail(mg_solver *s, int code, const std::string &msg) {
       return fail((s), e_ == cudaErrorMemoryAllocation ? MG_ENOMEM : MG_ECUDA,                \
                   std::string(#call) + ": " + cudaGetErrorString(e_));                        \
   } while (0)
-

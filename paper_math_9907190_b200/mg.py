@@ -25,6 +25,7 @@ MG_OK, MG_EINVAL, MG_ENOMEM, MG_ECUDA, MG_ENCCL, MG_EUNSUPPORTED, MG_EDIVERGED, 
 MG_F64, MG_F32 = 0, 1
 MG_NORM_INF, MG_NORM_L2 = 0, 1
 MG_FLAG_LOOPBACK = 1
+MG_FLAG_CONVENTIONAL = 2
 
 
 class MGError(RuntimeError):
@@ -245,7 +246,9 @@ def _round_pitch(n: int, itemsize: int) -> int:
 class Solver:
     """One libmg handle bound to torch tensors on one CUDA device.
 
-    ``Solver(dim, n, order=2, p=1.052 | (p_m, p_r1, p_r2, p_g), dtype=torch.float64)``.
+    ``Solver(dim, n, order=2, p=1.052 | (p_m, p_r1, p_r2, p_g), dtype=torch.float64)``;
+    ``conventional=True`` selects the paper's "usual" V(0,1) multigrid (p: one
+    value, 3D uses p_g).
     Fields are tensors of shape ``(n, pitch)`` (2D) or ``(n, n, pitch)`` (3D)
     whose first ``n`` columns are the grid; :meth:`alloc` makes them and
     :meth:`view` strips the padding.
@@ -253,7 +256,7 @@ class Solver:
 
     def __init__(self, dim: int, n: int, order: int = 2, p=None, dtype=None, device=None,
                  pitch: int | None = None, stream=None, nranks: int = 1, rank: int = 0, group=None,
-                 loopback: bool = False, agglom_points: int = 0):
+                 loopback: bool = False, agglom_points: int = 0, conventional: bool = False):
         import torch
         if not torch.cuda.is_available():
             raise MGError(MG_ENODEV, "no CUDA device (libmg has no CPU path)")
@@ -284,6 +287,8 @@ class Solver:
         cfg.nranks, cfg.rank = nranks, rank
         cfg.agglom_points = agglom_points
         self._id = None
+        if conventional:
+            cfg.flags = MG_FLAG_CONVENTIONAL   # the paper's "usual" V(0,1) multigrid (NEXT-3)
         if loopback:
             cfg.flags = MG_FLAG_LOOPBACK
         elif nranks > 1:
