@@ -146,7 +146,8 @@ int mg_num_levels(const mg_solver *s);
 int64_t mg_level_points(const mg_solver *s, int lev);
 
 /* Kernel launches queued by one V-cycle on this handle (for the bench's
- * gpu_launches count). */
+ * gpu_launches count); with the 2D cross-cycle fusion, a steady-state cycle
+ * of a multi-cycle call (the first cycle of a call queues one more). */
 int mg_launches_per_cycle(const mg_solver *s);
 
 /* Per-step timing of the V-cycle, for the roofline report.  Runs `ncycles`

@@ -246,8 +246,9 @@ struct Impl2 : ImplBase {
   int launches_per_cycle() const override {
     if (use_fast) {
       const int od = use_tail ? om : oc;
-      // desc_fine, rest_ad (o >= 1) + rest_da per descent octave, tail or coarse, jac_d + jac_a/asc per ascent octave
-      return 1 + (od - 1) + od + 1 + 2 * od + (use_tail ? 0 : 3 * (oc - od));
+      // desc_fine, rest_ad (o >= 1) + rest_da per descent octave, tail or coarse, jac_d + jac_a/asc per ascent
+      // octave; with cross-cycle fusion a steady-state cycle has no desc_fine (the previous cycle's asc_desc ran it)
+      return 1 + (od - 1) + od + 1 + 2 * od + (use_tail ? 0 : 3 * (oc - od)) - (fuses_cycles() ? 1 : 0);
     }
     int c = 1;                               // desc fine
     for (int o = 0; o + 1 < k; o++) c += (o >= 1) + 1;
