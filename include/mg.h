@@ -104,6 +104,11 @@ typedef struct {
   const void *nccl_id;     /* 128-byte ncclUniqueId (same on every rank) when nranks > 1 */
   int64_t agglom_points;   /* agglomerate levels with fewer interior nodes; 0 = 1<<18 */
   int flags;               /* MG_FLAG_* (0 for normal use) */
+  int sweeps;              /* two-colour Jacobi steps per level on the ascent (0 or 1: the paper's V-cycle).
+                              > 1 (2D, single GPU, diagonal scheme; at most 8): the paper's open question of
+                              "extra Jacobi iterations at each level" (DESIGN.md
+                              reading A19) -- every level, the finest included, repeats its step with its own
+                              values in place of the coarser level's.  Runs the plain (non-TMA) kernels. */
 } mg_config;
 
 /* Defaults: fp64, pitch = n, NULL stream, current device, 1 rank, p[*] = omega.

@@ -62,6 +62,7 @@ def _lib(dtype):
             ("orc_coarsest", I, [I, L, D, P, P]),
             ("orc_norm_inf", ctypes.c_double, [I, L, P]),
             ("orc_vcycle", I, [I, L, I, D, P, P, I, D]),
+            ("orc_vcycle_sweeps", I, [I, L, I, D, P, P, I, D, I]),
             ("orc_real_size", I, []),
         ]:
             fn = getattr(lib, name)
@@ -147,21 +148,23 @@ def norm_inf(x: np.ndarray) -> float:
     return _lib(x.dtype).orc_norm_inf(x.ndim, x.shape[0], _ptr(np.ascontiguousarray(x)))
 
 
-def vcycle(u: np.ndarray, f: np.ndarray, p, ncycles: int, order: int = 2, hist: bool = False):
+def vcycle(u: np.ndarray, f: np.ndarray, p, ncycles: int, order: int = 2, hist: bool = False, sweeps: int = 1):
     """Run ``ncycles`` V-cycles in place on ``u``; return the L-inf residual
-    history (ncycles+1 values) if ``hist``."""
+    history (ncycles+1 values) if ``hist``.  ``sweeps`` > 1 (2D): that many
+    two-colour Jacobi steps on every level (reading A19
+    of DESIGN.md)."""
     dim, n = u.ndim, u.shape[0]
     assert u.dtype == f.dtype and u.shape == f.shape and u.flags.c_contiguous
     f = np.ascontiguousarray(f)
     h = (ctypes.c_double * (ncycles + 1))() if hist else None
-    rc = _lib(u.dtype).orc_vcycle(dim, n, order, _params(dim, p), _ptr(u), _ptr(f), ncycles,
-                                  h if hist else None)
+    rc = _lib(u.dtype).orc_vcycle_sweeps(dim, n, order, _params(dim, p), _ptr(u), _ptr(f), ncycles,
+                                         h if hist else None, sweeps)
     if rc != 0:
         raise RuntimeError(f"orc_vcycle failed rc={rc}")
     return np.array(list(h)) if hist else None
 
 
-def convergence_factor(e: np.ndarray, p, iters: int, order: int = 2):
+def convergence_factor(e: np.ndarray, p, iters: int, order: int = 2, sweeps: int = 1):
     """The paper's convergence factor rho-bar, "the largest eigenvalue" of the
     V-cycle iteration operator (reading A12: spectral radius), by
     power iteration on the error equation (f = 0): normalise e (L2 over all
@@ -174,7 +177,7 @@ def convergence_factor(e: np.ndarray, p, iters: int, order: int = 2):
     e[...] = e * e.dtype.type(1.0 / nrm)
     ratios = np.empty(iters)
     for k in range(iters):
-        vcycle(e, f, p, 1, order=order)
+        vcycle(e, f, p, 1, order=order, sweeps=sweeps)
         nrm = float(np.sqrt(np.sum(e.astype(np.float64) ** 2)))
         ratios[k] = nrm
         e[...] = e * e.dtype.type(1.0 / nrm)

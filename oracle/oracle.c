@@ -611,6 +611,30 @@ double orc_norm_inf(int dim, long n, const real *x) {
   return mx;
 }
 
+/* ------------------------------------------------- extra Jacobi sweeps
+ * SURVEY 8(f) NEXT-4, the paper's open question "the effect of extra Jacobi
+ * iterations at each level of the diagonal grid".  Reading A19:
+ * an extra sweep on a 2D level repeats that level's two-colour step with
+ * the level's own values in place of the coarser level's -- on D(s) colour 1
+ * takes its four diagonal neighbours from the A(2s)-coincident (E) nodes of
+ * v_{D(s)}; on A(s) the green nodes take their four axis neighbours from the
+ * D(s) nodes of v_{A(s)} -- then colour 2 as before; on every level,
+ * the finest included (u <- u + v_0 after its last sweep).  Only 2D: in 3D
+ * the red level's first colour reads magenta B nodes, which the red level
+ * does not hold. */
+static void jac_2d_again(long m, int cls, double p, double hsq, real *v, const real *r, real *src) {
+  if (cls == 1) {   /* D(s): the E nodes as a coarse (m/2+1)^2 grid */
+    long mc = m / 2;
+    for (long Y = 0; Y <= mc; Y++)
+      for (long X = 0; X <= mc; X++) AT2(src, mc, X, Y) = AT2(v, m, 2 * X, 2 * Y);
+    jac_2d_diag(m, p, hsq, src, r, v);
+  } else {          /* A(s): colour 1 from v's own D nodes */
+    for (long J = 0; J <= m; J++)
+      for (long I = 0; I <= m; I++) AT2(src, m, I, J) = AT2(v, m, I, J);
+    jac_2d_axis(m, p, hsq, src, r, v);
+  }
+}
+
 /* ------------------------------------------------------------- V-cycle */
 
 static size_t lev_size(int dim, long n, int lev) {
@@ -626,9 +650,19 @@ static size_t lev_size(int dim, long n, int lev) {
  *   u <- u + v_0 at the interior.
  * hist (may be NULL): ncycles+1 values, ||f - L u||_inf before each cycle
  * and after the last one.  Returns 0, -1 bad arguments, -2 out of memory. */
+int orc_vcycle_sweeps(int dim, long n, int order, const double *p, real *u, const real *f, int ncycles, double *hist,
+                      int sweeps);
 int orc_vcycle(int dim, long n, int order, const double *p, real *u, const real *f, int ncycles, double *hist) {
+  return orc_vcycle_sweeps(dim, n, order, p, u, f, ncycles, hist, 1);
+}
+
+/* The same with `sweeps` two-colour Jacobi steps on every level (reading
+ * A19; 2D only for sweeps > 1). */
+int orc_vcycle_sweeps(int dim, long n, int order, const double *p, real *u, const real *f, int ncycles, double *hist,
+                      int sweeps) {
   int L = orc_levels(dim, n);
-  if (L < 0 || (order != 2 && order != 4) || ncycles < 0) return -1;
+  if (L < 0 || (order != 2 && order != 4) || ncycles < 0 || sweeps < 1 || (dim == 3 && sweeps > 1)) return -1;
+  real *tmp = NULL;
   real **r = (real **)calloc((size_t)L, sizeof(real *));
   real **v = (real **)calloc((size_t)L, sizeof(real *));
   real *ft = NULL;
@@ -655,7 +689,15 @@ int orc_vcycle(int dim, long n, int order, const double *p, real *u, const real 
     if (cyc == ncycles) break;
     for (int l = 0; l + 1 < L; l++) orc_restrict(dim, n, l, r[l], r[l + 1]);
     orc_coarsest(dim, n, p, r[L - 1], v[L - 1]);
-    for (int l = L - 2; l >= 0; l--) orc_jacobi(dim, n, l, p, v[l + 1], r[l], v[l]);
+    for (int l = L - 2; l >= 0; l--) {
+      orc_jacobi(dim, n, l, p, v[l + 1], r[l], v[l]);
+      if (sweeps > 1) {
+        if (!tmp && !(tmp = (real *)calloc(lev_size(dim, n, 0), sizeof(real)))) { rc = -2; goto done; }
+        long m = orc_lattice(dim, n, l);
+        for (int sw = 1; sw < sweeps; sw++)
+          jac_2d_again(m, lev_class(dim, l), p[0], hs2(n, lev_octave(dim, l)), v[l], r[l], tmp);
+      }
+    }
     if (dim == 2) {
       for (long J = 1; J < m0; J++)
         for (long I = 1; I < m0; I++) AT2(u, m0, I, J) = AT2(u, m0, I, J) + AT2(v[0], m0, I, J);
@@ -666,6 +708,7 @@ int orc_vcycle(int dim, long n, int order, const double *p, real *u, const real 
     }
   }
 done:
+  free(tmp);
   if (r) for (int l = 0; l < L; l++) free(r[l]);
   if (v) for (int l = 0; l < L; l++) free(v[l]);
   free(r);

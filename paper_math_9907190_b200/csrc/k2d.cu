@@ -556,6 +556,45 @@ void launch2_asc_fine(const S2<T> &vd, const D2<T> &u, const D2<const T> &f, con
   k2_update_ref<T><<<blocks_for(W * W), NT, 0, st>>>(cd(u), cd(scratch), un, M);
 }
 
+// D(s) nodes of a dense A(s) field into split E/O arrays (extra sweeps,
+// reading A19): E(a,b) = v(2a, 2b), O(a,b) = v(2a+1, 2b+1).
+template <class T>
+__global__ void __launch_bounds__(NT) k2_gather_d(D2<const T> v, S2<T> d, int M) {
+  const int H = M / 2 + 1;
+  int64_t t = (int64_t)blockIdx.x * NT + threadIdx.x;
+  if (t >= (int64_t)H * H) return;
+  const int a = (int)(t % H), b = (int)(t / H);
+  d.e[(int64_t)b * d.pitch + a] = v(2 * a, 2 * b);
+  d.o[(int64_t)b * d.pitch + a] = (2 * a + 1 <= M && 2 * b + 1 <= M) ? v(2 * a + 1, 2 * b + 1) : (T)0;
+}
+
+template <class T>
+void launch2_gather_d(const D2<T> &v, const S2<T> &d, int M, cudaStream_t st) {
+  const int64_t H = M / 2 + 1;
+  k2_gather_d<T><<<blocks_for(H * H), NT, 0, st>>>(cd(v), d, M);
+}
+
+// finest ascent with `sweeps` two-colour steps: the first from v_D(1), the
+// others from the D nodes of v itself (gathered into tmp), then u_new = u + v
+template <class T>
+void launch2_asc_fine_sweeps(const S2<T> &vd, const D2<T> &u, const D2<const T> &f, const D2<T> &scratch,
+                             const D2<T> &un, int M, int order, T c, const Coef<T> &k, int sweeps, const S2<T> &tmp,
+                             cudaStream_t st) {
+  int64_t W = M - 1;
+  for (int sw = 0; sw < sweeps; sw++) {
+    const S2<T> &src = sw == 0 ? vd : tmp;
+    if (sw > 0) launch2_gather_d<T>(scratch, tmp, M, st);
+    if (order == 2) {
+      k2_asc_fine1_ref<T, 2><<<blocks_for(W * W), NT, 0, st>>>(cs(src), cd(u), f, scratch, M, c, k);
+      k2_asc_fine2_ref<T, 2><<<blocks_for(W * W), NT, 0, st>>>(cd(u), f, scratch, M, c, k);
+    } else {
+      k2_asc_fine1_ref<T, 4><<<blocks_for(W * W), NT, 0, st>>>(cs(src), cd(u), f, scratch, M, c, k);
+      k2_asc_fine2_ref<T, 4><<<blocks_for(W * W), NT, 0, st>>>(cd(u), f, scratch, M, c, k);
+    }
+  }
+  k2_update_ref<T><<<blocks_for(W * W), NT, 0, st>>>(cd(u), cd(scratch), un, M);
+}
+
 template <class T>
 void launch2_coarse(const Lev2<T> *d_lev, int oc, int k, int *counter, cudaStream_t st) {
   static const bool global = env_flag("MG_COARSE_GLOBAL");
@@ -613,6 +652,10 @@ void launch2_norm(const D2<const T> &a, int M, unsigned long long *mx, double *s
                                     int, int, T,                                                                   \
                                     const Coef<T> &, cudaStream_t);                                                \
   template void launch2_coarse<T>(const Lev2<T> *, int, int, int *, cudaStream_t);                                \
+  template void launch2_gather_d<T>(const D2<T> &, const S2<T> &, int, cudaStream_t);                              \
+  template void launch2_asc_fine_sweeps<T>(const S2<T> &, const D2<T> &, const D2<const T> &, const D2<T> &,        \
+                                           const D2<T> &, int, int, T, const Coef<T> &, int, const S2<T> &,        \
+                                           cudaStream_t);                                                           \
   template void launch2_residual<T>(const D2<const T> &, const D2<const T> &, const D2<T> &, int, int,             \
                                     const Coef<T> &, cudaStream_t);                                                \
   template void launch2_ftilde<T>(const D2<const T> &, const D2<T> &, int, cudaStream_t);                          \

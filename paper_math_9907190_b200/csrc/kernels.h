@@ -89,6 +89,12 @@ template <class T>
 cudaError_t fast2_jac_d(const D2<T> &vc, const S2<T> &r, const S2<T> &v, int M, T c, cudaStream_t st,
                         const Rows2 &rw = Rows2());
 template <class T>
+void launch2_gather_d(const D2<T> &v, const S2<T> &d, int M, cudaStream_t st);
+template <class T>
+void launch2_asc_fine_sweeps(const S2<T> &vd, const D2<T> &u, const D2<const T> &f, const D2<T> &scratch,
+                             const D2<T> &un, int M, int order, T c, const Coef<T> &k, int sweeps, const S2<T> &tmp,
+                             cudaStream_t st);
+template <class T>
 void launch2_residual(const D2<const T> &u, const D2<const T> &f, const D2<T> &r, int M, int order, const Coef<T> &k,
                       cudaStream_t st);
 template <class T>

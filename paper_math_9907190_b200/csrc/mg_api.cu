@@ -25,6 +25,9 @@ struct Impl2 : ImplBase {
   int om = 1;              // first octave of the cooperative tail kernel (om <= oc)
   bool use_tail = false;
   bool serp = !env_flag("MG_2D_NOSERP");   // serpentine tile order across passes
+  int sweeps = 1;          // two-colour steps per level (> 1: NEXT-4, plain kernels)
+  D2<T> tmpA{};            // sweeps > 1: E nodes of v_D(s) as a dense A(2s)-shaped array
+  S2<T> tmpD{};            //             D nodes of v_A(s) as split E/O arrays
   bool xfuse = !env_flag("MG_2D_NOXFUSE");   // cross-cycle fusion of the finest ascent and descent
   Lev2<T> *d_lev = nullptr;
   std::vector<Lev2<T>> h_lev;   // host copy of the level descriptors (tail kernel parameters)
@@ -71,7 +74,18 @@ struct Impl2 : ImplBase {
     coef.invh2 = (T)((double)(n - 1) * (double)(n - 1));
     coef.c6 = (T)((double)(n - 1) * (double)(n - 1) / 6.0);
     // TMA needs 16-byte row strides on the caller's arrays (and on ours)
-    use_fast = ((pitch * (int64_t)sizeof(T)) % 16 == 0) && !env_flag("MG_FORCE_REF");
+    sweeps = s->cfg.sweeps > 1 ? s->cfg.sweeps : 1;
+    use_fast = ((pitch * (int64_t)sizeof(T)) % 16 == 0) && !env_flag("MG_FORCE_REF") && sweeps == 1;
+    if (sweeps > 1) {
+      const int64_t H = M[0] / 2 + 1, ph = pitch_for(H);
+      void *a, *e, *o;
+      cudaError_t st = dalloc(&a, sizeof(T) * H * ph);
+      if (!st) st = dalloc(&e, sizeof(T) * H * ph);
+      if (!st) st = dalloc(&o, sizeof(T) * H * ph);
+      if (st) return st;
+      tmpA = D2<T>{(T *)a, ph};
+      tmpD = S2<T>{(T *)e, (T *)o, ph};
+    }
     if (!use_fast) {
       int64_t ps = pitch_for(n);
       void *q;
@@ -149,9 +163,23 @@ struct Impl2 : ImplBase {
     for (int o = k - 2; o >= 0; o--) {
       STEP("jac_d", 2 * o + 1, 2, w * (Nl[2 * o + 2] + 2 * Nl[2 * o + 1]));
       launch2_jac_d<T>(vA[o + 1], rD[o], vD[o], M[o], cD[o], st);
+      for (int sw = 1; sw < sweeps; sw++) {   // again, from the E nodes of v_D itself (reading A19)
+        const int64_t H = M[o] / 2 + 1;
+        cudaMemcpy2DAsync(tmpA.p, tmpA.pitch * sizeof(T), vD[o].e, vD[o].pitch * sizeof(T), H * sizeof(T), H,
+                          cudaMemcpyDeviceToDevice, st);
+        launch2_jac_d<T>(tmpA, rD[o], vD[o], M[o], cD[o], st);
+      }
       if (o >= 1) {
         STEP("jac_a", 2 * o, 2, w * (Nl[2 * o + 1] + 2 * Nl[2 * o]));
         launch2_jac_a<T>(vD[o], rA[o], vA[o], M[o], cA[o], st);
+        for (int sw = 1; sw < sweeps; sw++) {   // again, from the D nodes of v_A itself
+          const S2<T> td{tmpD.e, tmpD.o, tmpD.pitch};
+          launch2_gather_d<T>(vA[o], td, M[o], st);
+          launch2_jac_a<T>(td, rA[o], vA[o], M[o], cA[o], st);
+        }
+      } else if (sweeps > 1) {
+        STEP("asc_fine", 0, 3 * sweeps, w * (Nl[1] + 3 * Nl[0]));
+        launch2_asc_fine_sweeps<T>(vD[0], uu, fc, scratch, uo, M[0], s->cfg.order, cA[0], coef, sweeps, tmpD, st);
       } else {
         STEP("asc_fine", 0, 3, w * (Nl[1] + 3 * Nl[0]));
         launch2_asc_fine<T>(vD[0], uu, fc, scratch, uo, M[0], s->cfg.order, cA[0], coef, st);
@@ -689,6 +717,8 @@ static int check_config(const mg_config *c, int *k_out) {
   for (int i = 0; i < np; i++)
     if (!(c->p[i] > 0.0 && c->p[i] <= 3.0)) return MG_EINVAL;
   if (c->pitch != 0 && c->pitch < c->n) return MG_EINVAL;
+  if (c->sweeps < 0 || c->sweeps > 8) return MG_EINVAL;
+  if (c->sweeps > 1 && (c->dim != 2 || c->nranks > 1 || (c->flags & MG_FLAG_CONVENTIONAL))) return MG_EUNSUPPORTED;
   if (c->nranks < 0 || (c->nranks > 1 && (c->rank < 0 || c->rank >= c->nranks))) return MG_EINVAL;
   if (c->nranks > 1) {
     // y-slabs (2D, dist2.cu) / z-slabs (3D, dist3.cu) of the hierarchy

@@ -49,6 +49,7 @@ class mg_config(ctypes.Structure):
         ("nccl_id", ctypes.c_void_p),
         ("agglom_points", ctypes.c_int64),
         ("flags", ctypes.c_int),
+        ("sweeps", ctypes.c_int),
     ]
 
 
@@ -256,7 +257,7 @@ class Solver:
 
     def __init__(self, dim: int, n: int, order: int = 2, p=None, dtype=None, device=None,
                  pitch: int | None = None, stream=None, nranks: int = 1, rank: int = 0, group=None,
-                 loopback: bool = False, agglom_points: int = 0, conventional: bool = False):
+                 loopback: bool = False, agglom_points: int = 0, conventional: bool = False, sweeps: int = 1):
         import torch
         if not torch.cuda.is_available():
             raise MGError(MG_ENODEV, "no CUDA device (libmg has no CPU path)")
@@ -286,6 +287,7 @@ class Solver:
             nranks, rank = dist.get_world_size(group), dist.get_rank(group)
         cfg.nranks, cfg.rank = nranks, rank
         cfg.agglom_points = agglom_points
+        cfg.sweeps = sweeps
         self._id = None
         if conventional:
             cfg.flags = MG_FLAG_CONVENTIONAL   # the paper's "usual" V(0,1) multigrid (NEXT-3)

@@ -19,18 +19,18 @@ from .mg import Solver
 
 
 def convergence_factor(dim: int, n: int, p, order: int = 2, iters: int = 200, dtype=None, seed: int = 3,
-                       solver: Solver | None = None):
-    """rho-bar of the V-cycle with parameters p, from a seeded random start
-    error; returns (rho, ratios)."""
+                       solver: Solver | None = None, sweeps: int = 1):
+    """rho-bar of the V-cycle with parameters p (and `sweeps` Jacobi steps
+    per level, NEXT-4), from a seeded random start error; returns (rho, ratios)."""
     import torch
     dtype = dtype or torch.float64
-    s = solver or Solver(dim, n, order=order, p=p, dtype=dtype)
+    s = solver or Solver(dim, n, order=order, p=p, dtype=dtype, sweeps=sweeps)
     e = s.alloc(W.random_field(dim, n, seed=seed))
     return s.convergence_factor(e, iters)
 
 
 def tune(dim: int, n: int, order: int = 2, p0=None, iters: int = 120, dtype=None, xatol: float = 2e-3,
-         maxfev: int = 200):
+         maxfev: int = 200, sweeps: int = 1):
     """Nelder-Mead over the relaxation parameters minimising rho-bar (P:345-348,
     P:800-811).  Returns dict(p=..., rho=..., nfev=...)."""
     from scipy.optimize import minimize
@@ -44,7 +44,7 @@ def tune(dim: int, n: int, order: int = 2, p0=None, iters: int = 120, dtype=None
         key = tuple(np.round(x, 12))
         if key not in cache:
             p = float(x[0]) if dim == 2 else tuple(float(v) for v in x)
-            cache[key] = convergence_factor(dim, n, p, order, iters, dtype)[0]
+            cache[key] = convergence_factor(dim, n, p, order, iters, dtype, sweeps=sweeps)[0]
         return cache[key]
 
     simplex = None

@@ -466,6 +466,33 @@ def test_power_iteration_agrees_with_arpack():
         assert rho == pytest.approx(_rho(dim, n, p, order), rel=5e-3)
 
 
+def test_extra_sweeps_variant():
+    """NEXT-4 oracle variant (reading A19): sweeps = 1 is the V-cycle itself;
+    more sweeps keep the cycle linear, leave the exact discrete solution a
+    fixed point, and at p = 1 lower rho-bar (0.099 -> ~0.047, 2D 65^2)."""
+    n = 33
+    f = W.random_field(2, n, seed=4)
+    u1, u2 = np.zeros_like(f), np.zeros_like(f)
+    oracle.vcycle(u1, f, 1.052, 3)
+    oracle.vcycle(u2, f, 1.052, 3, sweeps=1)
+    assert np.array_equal(u1, u2)
+    a, b = W.random_field(2, n, seed=1), W.random_field(2, n, seed=2)
+    z = np.zeros_like(a)
+    ua, ub, uab = a.copy(), b.copy(), 2 * a + 3 * b
+    for u in (ua, ub, uab):
+        oracle.vcycle(u, z, 1.0, 1, sweeps=3)
+    np.testing.assert_allclose(uab, 2 * ua + 3 * ub, atol=1e-12)
+    ustar = _exact.exact_solution(f)
+    u = ustar.copy()
+    oracle.vcycle(u, f, 1.0, 1, sweeps=2)
+    np.testing.assert_allclose(u, ustar, atol=1e-12 * np.max(np.abs(ustar)))
+    r1, _ = oracle.convergence_factor(W.random_field(2, 65, seed=3), 1.0, 150, sweeps=1)
+    r2, _ = oracle.convergence_factor(W.random_field(2, 65, seed=3), 1.0, 150, sweeps=2)
+    assert r1 == pytest.approx(0.099, abs=0.003) and r2 < 0.6 * r1
+    with pytest.raises(RuntimeError):
+        oracle.vcycle(np.zeros((9, 9, 9)), np.zeros((9, 9, 9)), (1.0,) * 4, 1, sweeps=2)
+
+
 def test_optimal_p_is_linear_in_p():
     """the correction is exactly p times the p = 1 correction
     (every v is created by one -c r injection), so the error operator is
