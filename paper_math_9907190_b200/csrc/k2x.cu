@@ -18,20 +18,22 @@
 // shuffles, no barriers.  At input row j a step computes
 //     r_old(j-1) -> green(j-1) -> D node(j-2) -> u_new(j-2) -> r_new(j-3)
 // and, every second row, the Erest2r pair of rows (j-5, j-4).  Input rows
-// (u, f pairs and the v_D value of each lane) arrive DEPTH - 1 steps ahead
-// through per-lane cp.async copies into a shared-memory ring (each lane reads
-// back only its own bytes); register prefetch instead stalled on the
-// zero-masking of the loads and cost 40 registers.  A strip is cut into row
-// segments (8 rows of warm-up each) so that
-// the grid fills every SM once; warps whose segment touches no boundary row
-// or column run a mask-free instance of the step.  Same node formulas, same
-// evaluation order: bit-identical to the two separate passes.
+// (u, f pairs and the v_D value of each lane) arrive LA = 4 steps ahead
+// through per-lane cp.async copies into an 8-slot shared-memory ring (each
+// lane reads back only its own bytes); f stays in the ring for the two steps
+// that read it instead of in registers (register prefetch instead stalled on
+// the zero-masking of the loads and cost 40 registers; a 7-row lookahead with
+// f in registers was 4 % slower).  A strip is cut into row segments (8 rows
+// of warm-up each) so that the grid fills every SM once; blocks of steps whose
+// rows all lie inside run a mask-free instance of the step.  Same node
+// formulas, same evaluation order: bit-identical to the two separate passes.
 #include "kernels.h"
 #include "ops2.cuh"
 
 namespace mg {
 namespace xf {
 
+constexpr int LA = 4;     // rows issued ahead (cp.async ring of 8 slots: f of a row stays 3 more steps)
 constexpr int SW = 56;    // output columns per strip: 32 lanes x 2 minus 2 x 4 halo
 
 template <class T>
@@ -120,7 +122,6 @@ struct Strip {
   bool ca, cb, outl;   // (x, y) / (x+1, y) interior columns; lane writes output
   unsigned char *ring;  // this warp's DEPTH-slot input ring in shared memory, offset to the lane
   Row<T> U[4];         // u_old
-  Pair<T> F[4];        // f
   T Dv[4];             // v_D at the row's D node
   Pair<T> RO[4];       // r(u_old)
   T G[4];              // green value of the row
@@ -159,16 +160,16 @@ struct Strip {
 #pragma unroll
     for (int i = 0; i < 4; i++) {
       U[i] = N[i] = Row<T>{0, 0, 0, 0};
-      F[i] = RO[i] = R[i] = Pair<T>{0, 0};
+      RO[i] = R[i] = Pair<T>{0, 0};
       Dv[i] = G[i] = (T)0;
     }
     mx = 0ull;
   }
   // incremental addressing from step j0 on (row-interior blocks only)
   __device__ __forceinline__ void start(int j0) {
-    lo = (int64_t)(j0 + DEPTH - 1) * pitch + xc;   // the first row issued inside the loop (odd)
-    ldO = pvo + (int64_t)((j0 + DEPTH - 1) >> 1) * vp + (xc >> 1);
-    ldE = pve + (int64_t)((j0 + DEPTH) >> 1) * vp + (xc >> 1);
+    lo = (int64_t)(j0 + LA) * pitch + xc;   // the first row issued inside the loop (even)
+    ldE = pve + (int64_t)((j0 + LA) >> 1) * vp + (xc >> 1);
+    ldO = pvo + (int64_t)((j0 + LA + 1) >> 1) * vp + (xc >> 1);
     stp = pun + (int64_t)(j0 - 2) * pitch + x;
     rso = (int64_t)((j0 - 4) >> 1) * rp + (x >> 1);
   }
@@ -207,6 +208,10 @@ struct Strip {
       ldE += vp;
     }
     cpa_commit();
+  }
+  __device__ __forceinline__ Pair<T> fpair(int y) const {   // f at the lane's pair of row y (in the ring)
+    const auto f = *reinterpret_cast<const typename V2<T>::t *>(ring + (y & (DEPTH - 1)) * SLOT + FO);
+    return Pair<T>{f.x, f.y};
   }
   __device__ __forceinline__ In<T> fetch(int y) const {
     const unsigned char *q = ring + (y & (DEPTH - 1)) * SLOT;
@@ -257,21 +262,22 @@ struct Strip {
   __device__ __forceinline__ void step(int j) {
     constexpr int PAR = K & 1;
     constexpr int s0 = K, s1 = (K + 3) & 3, s2 = (K + 2) & 3, s3 = (K + 1) & 3;   // rows j, j-1, j-2, j-3 (j-4: s0)
-    // row j: wait for its copies (DEPTH - 2 younger groups may stay in flight),
-    // then refill the slot row j-1 used with row j + DEPTH - 1
-    cpa_wait<DEPTH - 2>();
+    // row j: wait for its copies (the LA - 1 younger groups may stay in flight),
+    // then issue row j + LA into the slot of row j + LA - DEPTH, whose f was
+    // last read at step j - 1 (f of row r is read at steps r+1 and r+3, from
+    // the ring: it is not kept in registers)
+    cpa_wait<LA - 1>();
     const In<T> in = fetch(j);
     if (RE)
-      issue(j + DEPTH - 1);
+      issue(j + LA);
     else
-      issue_inc<(K + DEPTH - 1) & 1>(j + DEPTH - 1);
+      issue_inc<(K + LA) & 1>(j + LA);
     U[s0] = mkrow(in.ua, in.ub);
-    F[s0] = Pair<T>{in.fa, in.fb};
     Dv[s0] = in.d;
     const bool r1 = !RE || rin(j - 1), r2 = !RE || rin(j - 2), r3 = !RE || rin(j - 3);
     const bool ka = !CE || ca, kb = !CE || cb;
     // r_old at row j-1
-    RO[s1] = res(U[s2], U[s1], U[s0], F[s1], r1, ka, kb);
+    RO[s1] = res(U[s2], U[s1], U[s0], fpair(j - 1), r1, ka, kb);
     // green at row j-1: (x+1) on even rows, x on odd rows
     if (PAR == 1) {   // j-1 even: W = (x, y), S = (x+1, y-1), E = (x+2, y), N = (x+1, y+1)
       const T dE = shdn(Dv[s1]);
@@ -309,7 +315,7 @@ struct Strip {
       }
     }
     // r_new at row j-3 (rows j-4, j-3, j-2 of u_new)
-    R[s3] = res(N[s0], N[s3], N[s2], F[s3], r3, ka, kb);
+    R[s3] = res(N[s0], N[s3], N[s2], fpair(j - 3), r3, ka, kb);
     if (outl && j - 3 >= ys && j - 3 < ye) {
       const unsigned long long a = absbits(R[s3].a), b = absbits(R[s3].b), m = a > b ? a : b;
       mx = m > mx ? m : mx;
@@ -352,13 +358,13 @@ __global__ void __launch_bounds__(32, MINB) asc_desc_stream(const __grid_constan
                       xsm + lane * (2 * sizeof(T)));
     const int j0 = ys - 4, jend = ye + 3;   // steps j0 .. jend: ye - ys + 8 of them, a multiple of 4
 #pragma unroll
-    for (int i = 0; i < DEPTH - 1; i++) S.issue(j0 + i);
+    for (int i = 0; i < LA; i++) S.issue(j0 + i);
     // A block of 4 steps j..j+3 is row-interior when every row it computes,
-    // restricts or loads lies inside: j >= 8 and j + 3 + DEPTH - 1 <= M.
+    // restricts or loads lies inside: j >= 8 and j + 3 + LA <= M.
     // Column-interior warps: lanes' columns x0-4 .. x0+59 inside [1, M-1].
     const int x0 = strip * SW;
     const bool ce = x0 - 4 < 1 || x0 + 59 > P.M - 1;
-    auto rowin = [&](int j) { return j >= 8 && j + 3 + DEPTH - 1 <= P.M; };
+    auto rowin = [&](int j) { return j >= 8 && j + 3 + LA <= P.M; };
     int j = j0;
     for (; j <= jend && !rowin(j); j += 4) S.template steps<true, true>(j);
     if (j <= jend) {
