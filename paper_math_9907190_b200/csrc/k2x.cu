@@ -18,7 +18,7 @@
 // shuffles, no barriers.  At input row j a step computes
 //     r_old(j-1) -> green(j-1) -> D node(j-2) -> u_new(j-2) -> r_new(j-3)
 // and, every second row, the Erest2r pair of rows (j-5, j-4).  Input rows
-// (u, f pairs and the v_D value of each lane) arrive LA = 4 steps ahead
+// (u, f pairs and the v_D value of each lane) arrive 2 (fp64) / 3 (fp32) steps ahead
 // through per-lane cp.async copies into an 8-slot shared-memory ring (each
 // lane reads back only its own bytes); f stays in the ring for the two steps
 // that read it instead of in registers (register prefetch instead stalled on
@@ -33,7 +33,13 @@
 namespace mg {
 namespace xf {
 
-constexpr int LA = 4;     // rows issued ahead (cp.async ring of 8 slots: f of a row stays 3 more steps)
+// rows issued ahead (cp.async ring of 8 slots, LA + 4 <= 8: f of a row stays 3 more steps); measured on
+// B200 (2D 8193^2, ms per fused pass): fp64 LA = 1 / 2 / 3 / 4: 0.477 / 0.361 / 0.379 / 0.409; fp32 LA = 2 / 3 / 4:
+// 0.234 / 0.223 / 0.236
+template <class T>
+__host__ __device__ constexpr int lookahead() {
+  return sizeof(T) == 8 ? 2 : 3;
+}
 constexpr int SW = 56;    // output columns per strip: 32 lanes x 2 minus 2 x 4 halo
 
 template <class T>
@@ -111,8 +117,9 @@ struct In {
 // shifted between steps.  Loads are unconditional from clamped addresses:
 // rows outside [0, M] and columns outside [0, M] only feed nodes that are
 // not interior, whose results are all selected away (inside() is false).
-template <class T, int ORDER, int DEPTH>   // DEPTH: rows in flight per warp (power of 2)
+template <class T, int ORDER, int DEPTH>   // DEPTH: ring slots per lane (power of 2)
 struct Strip {
+  static constexpr int LA = lookahead<T>();
   const T *pu, *pf, *pve, *pvo;
   T *pun, *pre, *pro;
   int64_t pitch, vp, rp;
@@ -167,9 +174,10 @@ struct Strip {
   }
   // incremental addressing from step j0 on (row-interior blocks only)
   __device__ __forceinline__ void start(int j0) {
-    lo = (int64_t)(j0 + LA) * pitch + xc;   // the first row issued inside the loop (even)
-    ldE = pve + (int64_t)((j0 + LA) >> 1) * vp + (xc >> 1);
-    ldO = pvo + (int64_t)((j0 + LA + 1) >> 1) * vp + (xc >> 1);
+    const int r = j0 + LA;   // the first row issued inside the loop
+    lo = (int64_t)r * pitch + xc;
+    ldE = pve + (int64_t)((r + 1) >> 1) * vp + (xc >> 1);   // first even row >= r
+    ldO = pvo + (int64_t)(r >> 1) * vp + (xc >> 1);         // first odd row >= r
     stp = pun + (int64_t)(j0 - 2) * pitch + x;
     rso = (int64_t)((j0 - 4) >> 1) * rp + (x >> 1);
   }
@@ -358,6 +366,7 @@ __global__ void __launch_bounds__(32, MINB) asc_desc_stream(const __grid_constan
                       xsm + lane * (2 * sizeof(T)));
     const int j0 = ys - 4, jend = ye + 3;   // steps j0 .. jend: ye - ys + 8 of them, a multiple of 4
 #pragma unroll
+    constexpr int LA = lookahead<T>();
     for (int i = 0; i < LA; i++) S.issue(j0 + i);
     // A block of 4 steps j..j+3 is row-interior when every row it computes,
     // restricts or loads lies inside: j >= 8 and j + 3 + LA <= M.
