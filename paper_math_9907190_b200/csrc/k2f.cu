@@ -575,14 +575,14 @@ static int stages_cfg() {
 template <class Op>
 static cudaError_t run_op(const typename Op::Params &P, cudaStream_t st) {
   cudaError_t e = cudaFuncSetAttribute(tile_pipeline<Op>, cudaFuncAttributeMaxDynamicSharedMemorySize, Op::SMEM);
-  if (e != cudaSuccess) return e;
+  if (e != cudaSuccess) return note_launch(e);
   int per_sm = (227 * 1024) / (Op::SMEM + 1024);
   if (per_sm < 1) per_sm = 1;
   if (per_sm > 4) per_sm = 4;
   int grid = num_sms() * per_sm;
   if (grid > P.ntiles) grid = P.ntiles;
   if (grid < 1) return cudaSuccess;
-  return launch_pdl(tile_pipeline<Op>, dim3(grid), dim3(Op::NT), Op::SMEM, st, P);
+  return note_launch(launch_pdl(tile_pipeline<Op>, dim3(grid), dim3(Op::NT), Op::SMEM, st, P));
 }
 
 // run the op with the configured number of stages
@@ -599,7 +599,9 @@ template <class T>
 static bool tm2(CUtensorMap *tm, const void *p, int64_t nx, int64_t ny, int64_t pitch, int bx, int by) {
   uint64_t dims[2] = {(uint64_t)nx, (uint64_t)ny};
   uint32_t box[2] = {(uint32_t)bx, (uint32_t)by};
-  return encode_tmap(tm, p, sizeof(T), 2, dims, (uint64_t)pitch, 0, box);
+  const bool ok = encode_tmap(tm, p, sizeof(T), 2, dims, (uint64_t)pitch, 0, box);
+  if (!ok) note_launch(cudaErrorInvalidValue);
+  return ok;
 }
 
 // Row ranges for slab-decomposed (multi-GPU) levels; the default is the

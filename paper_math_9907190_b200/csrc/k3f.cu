@@ -453,7 +453,7 @@ struct OpAsc3Fine {
 template <class Op>
 static cudaError_t run_plane(const typename Op::Params &P, cudaStream_t st) {
   cudaError_t e = cudaFuncSetAttribute(plane_pipeline<Op>, cudaFuncAttributeMaxDynamicSharedMemorySize, Op::SMEM);
-  if (e != cudaSuccess) return e;
+  if (e != cudaSuccess) return note_launch(e);
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -462,7 +462,7 @@ static cudaError_t run_plane(const typename Op::Params &P, cudaStream_t st) {
   int grid = sms * per_sm;
   if (grid > P.nunits) grid = P.nunits;
   if (grid < 1) return cudaSuccess;
-  return launch_pdl(plane_pipeline<Op>, dim3(grid), dim3(Op::NT), Op::SMEM, st, P);
+  return note_launch(launch_pdl(plane_pipeline<Op>, dim3(grid), dim3(Op::NT), Op::SMEM, st, P));
 }
 
 // map of planes [z0, z0 + nz) of an n x n x (any) field given by its
@@ -474,7 +474,9 @@ static bool tm3(CUtensorMap *tm, const T *p, int64_t n, int64_t pitch, int64_t p
   p += (int64_t)z0 * plane;
   uint64_t dims[3] = {(uint64_t)n, (uint64_t)n, (uint64_t)nz};
   uint32_t box[3] = {(uint32_t)bx, (uint32_t)by, 1};
-  return encode_tmap(tm, p, sizeof(T), 3, dims, (uint64_t)pitch, (uint64_t)plane, box);
+  const bool ok = encode_tmap(tm, p, sizeof(T), 3, dims, (uint64_t)pitch, (uint64_t)plane, box);
+  if (!ok) note_launch(cudaErrorInvalidValue);
+  return ok;
 }
 
 static inline void zrange(const ZRange3 &pz, int M, int &zlo, int &zhi) {

@@ -201,7 +201,7 @@ constexpr int BOX34x33 = al128(34 * 33 * 8), BOX36x33 = al128(36 * 33 * 8);
 // (Emprolm), corners of plane j-2 from the new centres
 // (Emprolb).
 struct OpJacM3 {
-  static constexpr int NS = 7, PRO = 1, EPI = 2;
+  static constexpr int NS = 5, PRO = 1, EPI = 2;
   static constexpr int OG = 0, OR = BOX34x33;   // v_G box, r boxes (B, C)
   static constexpr int SLOT = OR + 2 * RBOX2;
   static constexpr int GPL = RBOX2;             // centre ring plane

@@ -51,6 +51,25 @@ bool launch2_tail(const Lev2<T> *h_lev, int om, int oc, int k, int *counter, cud
 // TMA tile kernels (k2f.cu); every pointer/pitch must be 16-byte aligned.
 // Rows2: the output rows a launch writes and the local allocations of its
 // inputs (multi-GPU slabs); the default (all -1 / 0) is the whole level.
+// First configuration failure of a kernel launch on this host thread (a
+// rejected dynamic shared-memory size, an unencodable tensor map, a launch
+// error): the generic launchers record it here, and the ABI checks and clears
+// it after enqueueing a cycle, so a pass that could not be launched is an
+// MG_ECUDA error, never a silently skipped pass.
+inline cudaError_t &sticky_launch_error() {
+  static thread_local cudaError_t e = cudaSuccess;
+  return e;
+}
+inline cudaError_t note_launch(cudaError_t e) {
+  if (e != cudaSuccess && sticky_launch_error() == cudaSuccess) sticky_launch_error() = e;
+  return e;
+}
+inline cudaError_t take_launch_error() {
+  cudaError_t e = sticky_launch_error();
+  sticky_launch_error() = cudaSuccess;
+  return e;
+}
+
 // Direction of the next 3D plane-pipeline launch on this host thread
 // (zpipe Sched::rev, items walked in reverse): the 3D V-cycle alternates it
 // so that every pass first reads what its producer wrote last (still in L2).

@@ -673,8 +673,10 @@ static int run_cycle(mg_solver *s, const void *u_in, void *u_out, const void *f_
     if (s->graphs.size() >= 16) drop_graphs(s);
     cudaGraph_t g = nullptr;
     CKS(s, cudaStreamBeginCapture(s->st, cudaStreamCaptureModeThreadLocal));
+    take_launch_error();
     s->impl->enqueue_cycle_mode(u_in, u_out, f_eff, s->st, nullptr, mode);
     cudaError_t le = cudaGetLastError();
+    if (le == cudaSuccess) le = take_launch_error();
     cudaError_t e = cudaStreamEndCapture(s->st, &g);
     if (le != cudaSuccess) {
       if (g) cudaGraphDestroy(g);
@@ -699,6 +701,7 @@ static int begin(mg_solver *s) {
 }
 static int end(mg_solver *s) {
   CKS(s, cudaGetLastError());
+  CKS(s, take_launch_error());   // a pass whose launch was rejected (kernels.h)
   CKS(s, cudaEventRecord(s->ev_out, s->st));
   CKS(s, cudaStreamWaitEvent(s->user, s->ev_out, 0));
   return MG_OK;
@@ -1129,6 +1132,7 @@ int mg_profile(mg_solver *s, void *u, const void *f, int ncycles, mg_step_stat *
   }
   if (cur != u) CKS(s, cudaMemcpyAsync(u, cur, s->field_elems() * s->esz, cudaMemcpyDeviceToDevice, s->st));
   CKS(s, cudaGetLastError());
+  CKS(s, take_launch_error());
   CKS(s, cudaStreamSynchronize(s->st));
   size_t ns = prof.steps.size();
   std::vector<double> acc(ns, 0.0);

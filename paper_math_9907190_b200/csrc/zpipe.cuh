@@ -212,7 +212,7 @@ static cudaError_t launch_zpipe(typename Op::Params &P, int tx, int ty, int xoff
                                 int zhi, cudaStream_t st) {
   if (zhi <= zlo) return cudaSuccess;
   cudaError_t e = cudaFuncSetAttribute(zpipe<Op>, cudaFuncAttributeMaxDynamicSharedMemorySize, Op::SMEM);
-  if (e != cudaSuccess) return e;
+  if (e != cudaSuccess) return note_launch(e);
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -230,7 +230,7 @@ static cudaError_t launch_zpipe(typename Op::Params &P, int tx, int ty, int xoff
   if (P.sc.S > zhi - zlo) P.sc.S = zhi - zlo;
   const long long work = (long long)P.sc.T * (zhi - zlo);
   const int grid = work < sms ? (int)work : sms;
-  return launch_pdl(zpipe<Op>, dim3(grid), dim3(NT), Op::SMEM, st, P);
+  return note_launch(launch_pdl(zpipe<Op>, dim3(grid), dim3(NT), Op::SMEM, st, P));
 }
 
 // 3D tensor map over nx x ny x nz elements (row pitch, plane stride in
@@ -240,7 +240,9 @@ static bool tmap3(CUtensorMap *tm, const T *p, int64_t nx, int64_t ny, int64_t n
                   int by) {
   uint64_t dims[3] = {(uint64_t)nx, (uint64_t)ny, (uint64_t)nz};
   uint32_t box[3] = {(uint32_t)bx, (uint32_t)by, 1};
-  return encode_tmap(tm, p, sizeof(T), 3, dims, (uint64_t)pitch, (uint64_t)plane, box);
+  const bool ok = encode_tmap(tm, p, sizeof(T), 3, dims, (uint64_t)pitch, (uint64_t)plane, box);
+  if (!ok) note_launch(cudaErrorInvalidValue);
+  return ok;
 }
 
 }  // namespace mg
