@@ -27,6 +27,8 @@
 // of warm-up each) so that the grid fills every SM once; blocks of steps whose
 // rows all lie inside run a mask-free instance of the step.  Same node
 // formulas, same evaluation order: bit-identical to the two separate passes.
+#include <type_traits>
+
 #include "kernels.h"
 #include "ops2.cuh"
 
@@ -395,6 +397,234 @@ __global__ void __launch_bounds__(32, MINB) asc_desc_stream(const __grid_constan
   if (lane == 0 && item < P.nstrips * nseg) norm_push(P.ns, __longlong_as_double((long long)mx));
 }
 
+
+// ---------------------------------------------------------------- fp32
+// Four columns per lane (fp32, order 2): lane l owns x = x0 - 4 + 4l .. x+3,
+// so a warp streams a strip of 120 output columns; a row of u or f is one
+// 16-byte vector per lane, the x neighbours of the quad are the neighbouring
+// lanes' outer values (two shuffles per row instead of four), and the halo
+// costs 8 of 128 columns instead of 8 of 64.  The nodes, their formulas and
+// their order are those of the pair strip above (node by node), so the results
+// are bit-identical to it and to the two separate passes.
+constexpr int SWQ = 120;
+
+struct Q4 {
+  float a, b, c, d;   // x, x+1, x+2, x+3
+};
+struct RowQ {
+  Q4 q;
+  float w, e;   // x-1, x+4
+};
+__device__ __forceinline__ RowQ mkrowq(const Q4 &q) { return RowQ{q, shup(q.d), shdn(q.a)}; }
+
+struct XParamsQ {
+  const float *u, *f, *ve, *vo;
+  float *un, *re, *ro;
+  int64_t pitch, vp, rp;
+  int M, nstrips, seg;
+  float c;
+  Coef<float> k;
+  NormSink ns;
+};
+
+template <int DEPTH, int LA>
+struct StripQ {
+  const float *pu, *pf, *pve, *pvo;
+  float *pun, *pre, *pro;
+  int64_t pitch, vp, rp;
+  Coef<float> kk;
+  float c;
+  int x, xc, M, ys, ye;
+  bool k0, k1, k2, k3, outl;   // interior columns x..x+3; lane writes output
+  unsigned char *ring;
+  RowQ U[4];
+  Q4 N4[4];                    // u_new (quad only; w/e shuffled when a row becomes the centre)
+  float Nw[4], Ne[4];
+  float D0[4], D1[4];          // v_D at the two D nodes of the row (x, x+2 even rows; x+1, x+3 odd rows)
+  Q4 RO[4];
+  float G0[4], G1[4];          // the two greens of the row (x+1, x+3 even rows; x, x+2 odd rows)
+  Q4 R[4];
+  unsigned long long mx;
+  static constexpr int SLOT = 32 * 40, FO = 32 * 16, DO = 32 * 32;
+
+  __device__ __forceinline__ StripQ(const XParamsQ &P, int x_, int ys_, int ye_, unsigned char *ring_) {
+    pu = P.u; pf = P.f; pve = P.ve; pvo = P.vo; pun = P.un; pre = P.re; pro = P.ro;
+    pitch = P.pitch; vp = P.vp; rp = P.rp; kk = P.k; c = P.c; M = P.M;
+    x = x_; ys = ys_; ye = ye_; ring = ring_;
+    xc = min(max(x, 0), M);
+    k0 = x >= 1 && x <= M - 1;
+    k1 = x + 1 >= 1 && x + 1 <= M - 1;
+    k2 = x + 2 >= 1 && x + 2 <= M - 1;
+    k3 = x + 3 >= 1 && x + 3 <= M - 1;
+    const int lane = threadIdx.x & 31;
+    outl = lane >= 1 && lane < 31;
+#pragma unroll
+    for (int i = 0; i < 4; i++) {
+      U[i] = RowQ{{0, 0, 0, 0}, 0, 0};
+      N4[i] = RO[i] = R[i] = Q4{0, 0, 0, 0};
+      Nw[i] = Ne[i] = D0[i] = D1[i] = G0[i] = G1[i] = 0.f;
+    }
+    mx = 0ull;
+  }
+  __device__ __forceinline__ bool rin(int y) const { return (unsigned)(y - 1) < (unsigned)(M - 1); }
+  __device__ __forceinline__ void issue(int y) const {
+    const int yc = min(max(y, 0), M);
+    const int64_t o = (int64_t)yc * pitch + xc;
+    unsigned char *q = ring + (y & (DEPTH - 1)) * SLOT;
+    cpa<16>(q, pu + o);
+    cpa<16>(q + FO, pf + o);
+    // the two D(1) nodes of row y in the quad: E at x, x+2 (even rows), O at x+1, x+3 (odd rows)
+    cpa<8>(q + DO - (threadIdx.x & 31) * 8, ((y & 1) ? pvo : pve) + (int64_t)(yc >> 1) * vp + (xc >> 1));
+    cpa_commit();
+  }
+  __device__ __forceinline__ Q4 ld4(const unsigned char *p) const {
+    const float4 v = *reinterpret_cast<const float4 *>(p);
+    return Q4{v.x, v.y, v.z, v.w};
+  }
+  // r = f - L u at the quad of row y (gather9 roles, order 2), masked
+  __device__ __forceinline__ Q4 res(const Q4 &dn, const RowQ &cr, const Q4 &up, const Q4 &f, bool ry) const {
+    auto one = [&](float cc, float w, float s, float e, float n, float ff, bool k) {
+      Nb9<float> q;
+      q.c = cc; q.w = w; q.s = s; q.e = e; q.n = n;
+      q.ne = q.nw = q.sw = q.se = 0.f;
+      return (ry && k) ? res2v<float, 2>(q, ff, kk) : 0.f;
+    };
+    Q4 r;
+    r.a = one(cr.q.a, cr.w, dn.a, cr.q.b, up.a, f.a, k0);
+    r.b = one(cr.q.b, cr.q.a, dn.b, cr.q.c, up.b, f.b, k1);
+    r.c = one(cr.q.c, cr.q.b, dn.c, cr.q.d, up.c, f.c, k2);
+    r.d = one(cr.q.d, cr.q.c, dn.d, cr.e, up.d, f.d, k3);
+    return r;
+  }
+  template <int K>
+  __device__ __forceinline__ void step(int j) {
+    constexpr int PAR = K & 1;
+    constexpr int s0 = K, s1 = (K + 3) & 3, s2 = (K + 2) & 3, s3 = (K + 1) & 3;
+    cpa_wait<LA - 1>();
+    const unsigned char *q = ring + (j & (DEPTH - 1)) * SLOT;
+    const Q4 u = ld4(q);
+    const float2 dd = *reinterpret_cast<const float2 *>(q + DO - (threadIdx.x & 31) * 8);
+    issue(j + LA);
+    U[s0] = mkrowq(u);
+    D0[s0] = dd.x;
+    D1[s0] = dd.y;
+    const bool r1 = rin(j - 1), r2 = rin(j - 2), r3 = rin(j - 3);
+    const Q4 f1 = ld4(ring + ((j - 1) & (DEPTH - 1)) * SLOT + FO);
+    RO[s1] = res(U[s2].q, U[s1], U[s0].q, f1, r1);
+    // greens of row j-1
+    if (PAR == 1) {   // y even: greens at x+1, x+3
+      const float dE = shdn(D0[s1]);   // E at x+4
+      G0[s1] = (r1 && k1) ? jac4(c, RO[s1].b, D0[s1], D0[s2], D1[s1], D0[s0]) : 0.f;
+      G1[s1] = (r1 && k3) ? jac4(c, RO[s1].d, D1[s1], D1[s2], dE, D1[s0]) : 0.f;
+    } else {          // y odd: greens at x, x+2
+      const float dW = shup(D1[s1]);   // O at x-1
+      G0[s1] = (r1 && k0) ? jac4(c, RO[s1].a, dW, D0[s2], D0[s1], D0[s0]) : 0.f;
+      G1[s1] = (r1 && k2) ? jac4(c, RO[s1].c, D0[s1], D1[s2], D1[s1], D1[s0]) : 0.f;
+    }
+    // D nodes of row j-2 and u_new there
+    {
+      const int y = j - 2;
+      float va, vb, vc, vd;
+      if (PAR == 0) {   // y even: D at x, x+2; greens at x+1 (G0), x+3 (G1)
+        const float gW = shup(G1[s2]);   // green at x-1
+        va = (r2 && k0) ? jac4(c, RO[s2].a, gW, G0[s3], G0[s2], G0[s1]) : 0.f;
+        vb = G0[s2];
+        vc = (r2 && k2) ? jac4(c, RO[s2].c, G0[s2], G1[s3], G1[s2], G1[s1]) : 0.f;
+        vd = G1[s2];
+      } else {          // y odd: D at x+1, x+3; greens at x (G0), x+2 (G1)
+        const float gE = shdn(G0[s2]);   // green at x+4
+        va = G0[s2];
+        vb = (r2 && k1) ? jac4(c, RO[s2].b, G0[s2], G0[s3], G1[s2], G0[s1]) : 0.f;
+        vc = G1[s2];
+        vd = (r2 && k3) ? jac4(c, RO[s2].d, G1[s2], G1[s3], gE, G1[s1]) : 0.f;
+      }
+      const Q4 &uo = U[s2].q;
+      Q4 n;
+      n.a = (r2 && k0) ? uo.a + va : uo.a;
+      n.b = (r2 && k1) ? uo.b + vb : uo.b;
+      n.c = (r2 && k2) ? uo.c + vc : uo.c;
+      n.d = (r2 && k3) ? uo.d + vd : uo.d;
+      N4[s2] = n;
+      Nw[s2] = shup(n.d);
+      Ne[s2] = shdn(n.a);
+      if (outl && y >= ys && y < ye && r2) {
+        float *p = pun + (int64_t)y * pitch + x;
+        if (k0 && k1 && k2 && k3) {
+          *reinterpret_cast<float4 *>(p) = make_float4(n.a, n.b, n.c, n.d);
+        } else {
+          if (k0) p[0] = n.a;
+          if (k1) p[1] = n.b;
+          if (k2) p[2] = n.c;
+          if (k3) p[3] = n.d;
+        }
+      }
+    }
+    // r_new at row j-3
+    {
+      const Q4 f3 = ld4(ring + ((j - 3) & (DEPTH - 1)) * SLOT + FO);
+      const RowQ cr{N4[s3], Nw[s3], Ne[s3]};
+      R[s3] = res(N4[s0], cr, N4[s2], f3, r3);
+      if (outl && j - 3 >= ys && j - 3 < ye) {
+        auto ab = [](float v) { return (unsigned long long)__double_as_longlong((double)v) & 0x7fffffffffffffffull; };
+        unsigned long long m = ab(R[s3].a);
+        m = max(m, ab(R[s3].b));
+        m = max(m, ab(R[s3].c));
+        m = max(m, ab(R[s3].d));
+        mx = max(mx, m);
+      }
+    }
+    // Erest2r of rows (j-5, j-4) when j-5 is even
+    if (PAR == 1) {
+      const int y = j - 5;
+      const Q4 R6 = R[s2], R5 = R[s1], R4 = R[s0], R3 = R[s3];
+      const float rW = shup(R5.d), rE = shdn(R4.a);
+      if (outl && y >= ys && y < ye) {
+        const int64_t o = (int64_t)(y >> 1) * rp + (x >> 1);
+        const bool ye_ = y >= 2 && y <= M - 2, yo_ = y + 1 <= M - 1;
+        const float e0 = erest2r(R5.a, rW, R6.a, R5.b, R4.a);
+        const float e2 = erest2r(R5.c, R5.b, R6.c, R5.d, R4.c);
+        const float o1 = erest2r(R4.b, R4.a, R5.b, R4.c, R3.b);
+        const float o3 = erest2r(R4.d, R4.c, R5.d, rE, R3.d);
+        if (ye_ && x >= 2 && x <= M - 2) pre[o] = e0;
+        if (ye_ && x + 2 >= 2 && x + 2 <= M - 2) pre[o + 1] = e2;
+        if (yo_ && x + 1 <= M - 1) pro[o] = o1;
+        if (yo_ && x + 3 <= M - 1) pro[o + 1] = o3;
+      }
+    }
+  }
+};
+
+template <int DEPTH, int LA>
+__global__ void __launch_bounds__(32, 16) asc_desc_stream_q(const __grid_constant__ XParamsQ P) {
+  const int lane = threadIdx.x & 31;
+  const int item = blockIdx.x;
+  const int nseg = (P.M + P.seg - 1) / P.seg;
+  unsigned long long mx = 0ull;
+  if (item < P.nstrips * nseg) {
+    const int strip = item % P.nstrips, sg = item / P.nstrips;
+    const int ys = sg * P.seg, ye = min(ys + P.seg, P.M);
+    extern __shared__ __align__(16) unsigned char xsm[];
+    StripQ<DEPTH, LA> S(P, strip * SWQ - 4 + 4 * lane, ys, ye, xsm + lane * 16);
+    const int j0 = ys - 4, jend = ye + 3;
+#pragma unroll
+    for (int i = 0; i < LA; i++) S.issue(j0 + i);
+    // (a mask-free instance for interior blocks, as in the pair strip, measured 7 % slower here)
+    for (int j = j0; j <= jend; j += 4) {
+      S.template step<0>(j);
+      S.template step<1>(j + 1);
+      S.template step<2>(j + 2);
+      S.template step<3>(j + 3);
+    }
+    mx = S.mx;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const unsigned long long w = __shfl_xor_sync(0xffffffffu, mx, o);
+    mx = w > mx ? w : mx;
+  }
+  if (lane == 0 && item < P.nstrips * nseg) norm_push(P.ns, __longlong_as_double((long long)mx));
+}
+
 }  // namespace xf
 
 template <class T, int ORDER, int DEPTH, int MINB>
@@ -422,6 +652,33 @@ static cudaError_t asc_desc_launch_w(const xf::XParams<T> &P0, cudaStream_t st) 
   return cudaGetLastError();
 }
 
+// fp32 order 2: the four-columns-per-lane strip (MG_XF_PAIRS=1: the pair strip)
+template <int LA>
+static cudaError_t asc_desc_launch_q(const xf::XParams<float> &P0, cudaStream_t st) {
+  constexpr int DEPTH = 8, SMEM = DEPTH * 32 * 40;
+  static int wres = 0, sms = 0;
+  if (!wres) {
+    int dev = 0, nb = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, xf::asc_desc_stream_q<DEPTH, LA>, 32, SMEM);
+    wres = nb > 0 ? nb : 1;
+    if (sms <= 0) sms = 148;
+  }
+  xf::XParamsQ P{};
+  P.u = P0.u; P.f = P0.f; P.ve = P0.ve; P.vo = P0.vo; P.un = P0.un; P.re = P0.re; P.ro = P0.ro;
+  P.pitch = P0.pitch; P.vp = P0.vp; P.rp = P0.rp; P.M = P0.M; P.c = P0.c; P.k = P0.k; P.ns = P0.ns;
+  P.nstrips = (P.M + xf::SWQ - 1) / xf::SWQ;
+  const int S = max(1, (sms * wres) / P.nstrips);
+  int seg = (P.M + S - 1) / S;
+  seg = (seg + 3) / 4 * 4;
+  if (seg < 32) seg = 32;
+  P.seg = seg;
+  const int nitems = P.nstrips * ((P.M + seg - 1) / seg);
+  xf::asc_desc_stream_q<DEPTH, LA><<<nitems, 32, SMEM, st>>>(P);
+  return cudaGetLastError();
+}
+
 // One warp per block: registers are allocated per block, so 1-warp blocks
 // fill an SM to the register limit (2- and 4-warp blocks left 3-4 warps per
 // SM unused and ran 60 % slower).  Order 2 caps the registers at 128 (16
@@ -430,6 +687,10 @@ static cudaError_t asc_desc_launch_w(const xf::XParams<T> &P0, cudaStream_t st) 
 // fp32 +2 %).
 template <class T, int ORDER>
 static cudaError_t asc_desc_launch(const xf::XParams<T> &P, cudaStream_t st) {
+  if constexpr (std::is_same<T, float>::value && ORDER == 2) {
+    static const bool pairs = env_flag("MG_XF_PAIRS");
+    if (!pairs) return asc_desc_launch_q<3>(P, st);   // lookahead 2 / 3 / 4 rows: 0.459 / 0.457 / 0.461 ms
+  }
   return asc_desc_launch_w<T, ORDER, 8, (ORDER == 2 ? 16 : 1)>(P, st);
 }
 
