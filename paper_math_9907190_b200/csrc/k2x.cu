@@ -23,10 +23,13 @@
 // lane reads back only its own bytes); f stays in the ring for the two steps
 // that read it instead of in registers (register prefetch instead stalled on
 // the zero-masking of the loads and cost 40 registers; a 7-row lookahead with
-// f in registers was 4 % slower).  A strip is cut into row segments (8 rows
-// of warm-up each) so that the grid fills every SM once; blocks of steps whose
-// rows all lie inside run a mask-free instance of the step.  Same node
-// formulas, same evaluation order: bit-identical to the two separate passes.
+// f in registers was 17 % slower: with a short ring the halo columns and rows
+// that neighbouring strips share are re-read while still in L2).  A strip is
+// cut into row segments (8 rows of warm-up each) so that the grid fills every
+// SM exactly once; blocks of steps whose rows all lie inside run a mask-free
+// instance of the step.  fp32 order 2 uses a four-columns-per-lane variant of
+// the same pipeline (StripQ, below).  Same node formulas, same evaluation
+// order: bit-identical to the two separate passes.
 #include <type_traits>
 
 #include "kernels.h"
