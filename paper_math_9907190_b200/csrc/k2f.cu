@@ -547,6 +547,163 @@ struct OpJac2A {
   static __device__ void finish(const Params &, Acc &) {}
 };
 
+// ============ ascent A(s) then D(s-1) in one pass: v_A(s) never reaches HBM
+// The tile is [a0, a0+TX) x [b0, b0+TY) of D(s-1)'s E/O index space, which is
+// A(s)'s node space.  v_A(s) is computed (OpJac2A's two colours, same node
+// formulas and operand order) on the ring [a0-1, a0+TX] x [b0-1, b0+TY] that
+// the O update needs, then OpJac2D's two colours run from shared memory.
+template <class T, int STG, int NTH>
+struct OpJac2AD {
+  static constexpr int NT = NTH, STAGES = STG, NW = NT / 32;
+  static constexpr int H2 = hx<T>(2), H1 = hx<T>(1);
+  static constexpr int RAW = w16<T>(TX + 2 + H2), RAH = TY + 4;            // r_A(s): [a0-2, a0+TX+2) x [b0-2, b0+TY+2)
+  static constexpr int VDW = w16<T>(TX / 2 + 2 + H2), VDH = TY / 2 + 4;    // v_D(s) E/O: the D(s) ring of those greens
+  static constexpr int ROW = w16<T>(TX + H1), ROH = TY + 1, REW = w16<T>(TX), REH = TY;   // r_D(s-1) O / E
+  static constexpr int RA_BYTES = RAW * RAH * sizeof(T), VD_BYTES = VDW * VDH * sizeof(T),
+                       RO_BYTES = ROW * ROH * sizeof(T), RE_BYTES = REW * REH * sizeof(T);
+  static constexpr int RA_OFF = 0, VE_OFF = al128(RA_BYTES), VO_OFF = VE_OFF + al128(VD_BYTES),
+                       RO_OFF = VO_OFF + al128(VD_BYTES), RE_OFF = RO_OFF + al128(RO_BYTES);
+  static constexpr int STAGE = al128(RE_OFF + RE_BYTES);
+  // scratch: v_A(s) on [a0-2, a0+TX+2) x [b0-2, b0+TY+2); O of v_D(s-1) on [a0-2, a0+TX) x [b0-1, b0+TY)
+  static constexpr int VAW = TX + 4, VAH = TY + 4, OSW = TX + 2, OSH = TY + 1;
+  static constexpr int VA_BYTES = al128(VAW * VAH * (int)sizeof(T));
+  static constexpr int SMEM = STAGES * STAGE + VA_BYTES + al128(OSW * OSH * sizeof(T));
+  struct Params {
+    CUtensorMap tra, tve, tvo, tro, tre;
+    S2<T> v;
+    int M, ntx, ntiles;
+    int rev;
+    T ca, cd;
+  };
+  using Acc = NoAcc;
+  static __device__ void prefetch(const Params &P) {
+    tma_prefetch_desc(&P.tra);
+    tma_prefetch_desc(&P.tve);
+    tma_prefetch_desc(&P.tvo);
+    tma_prefetch_desc(&P.tro);
+    tma_prefetch_desc(&P.tre);
+  }
+  static __device__ void init(Acc &) {}
+  static __device__ void issue(const Params &P, int t, unsigned char *st, uint64_t *bar) {
+    const int a0 = (t % P.ntx) * TX, b0 = (t / P.ntx) * TY;
+    mbar_expect_tx(bar, RA_BYTES + 2 * VD_BYTES + RO_BYTES + RE_BYTES);
+    tma_load_2d(st + RA_OFF, &P.tra, a0 - H2, b0 - 2, bar);
+    tma_load_2d(st + VE_OFF, &P.tve, a0 / 2 - H2, b0 / 2 - 2, bar);
+    tma_load_2d(st + VO_OFF, &P.tvo, a0 / 2 - H2, b0 / 2 - 2, bar);
+    tma_load_2d(st + RO_OFF, &P.tro, a0 - H1, b0 - 1, bar);
+    tma_load_2d(st + RE_OFF, &P.tre, a0, b0, bar);
+  }
+  static __device__ void compute(const Params &P, int t, unsigned char *st, unsigned char *scr, Acc &) {
+    const int a0 = (t % P.ntx) * TX, b0 = (t / P.ntx) * TY, W = P.M / 2;   // A(s) nodes 0 .. W
+    STile<T> RA = stile<T>(st + RA_OFF, RAW, a0 - H2, b0 - 2);
+    STile<T> VE = stile<T>(st + VE_OFF, VDW, a0 / 2 - H2, b0 / 2 - 2);
+    STile<T> VO = stile<T>(st + VO_OFF, VDW, a0 / 2 - H2, b0 / 2 - 2);
+    STile<T> RO = stile<T>(st + RO_OFF, ROW, a0 - H1, b0 - 1);
+    STile<T> RE = stile<T>(st + RE_OFF, REW, a0, b0);
+    STile<T> VA = stile<T>(scr, VAW, a0 - 2, b0 - 2);
+    STile<T> OS = stile<T>(scr + VA_BYTES, OSW, a0 - 2, b0 - 1);
+    const SplitTile2<T> VD{VE, VO};
+    const T ca = P.ca, cd = P.cd;
+    auto in = [&](int x, int y) { return x >= 1 && y >= 1 && x <= W - 1 && y <= W - 1; };
+    // A(s) colour 1: the green node (x + y odd) of each column pair (a0-2+2p, a0-1+2p), rows
+    // b0-2 .. b0+TY+1 taken two at a time (even, odd) so every E/O choice is static
+    const T *Eb = (const T *)(st + VE_OFF), *Ob = (const T *)(st + VO_OFF), *Rb = (const T *)(st + RA_OFF);
+    T *Vb = (T *)scr;
+    constexpr int GP = TX / 2 + 2, GR = TY / 2 + 2;
+#pragma unroll
+    for (int k = 0; k < (GP * GR + NT - 1) / NT; k++) {
+      const int i = threadIdx.x + k * NT;
+      if (GP * GR % NT && i >= GP * GR) break;
+      const int p = i % GP, m = i / GP;
+      {   // y = b0-2+2m even: green at x = a0-1+2p; E(i-1,J), O(i-1,J-1), E(i,J), O(i-1,J) with i = x/2+1, J = y/2
+        const int y = b0 - 2 + 2 * m, x = a0 - 1 + 2 * p;
+        const T *e = Eb + (m + 1) * VDW + p + H2, *o = Ob + m * VDW + p + H2 - 1;
+        T g = (T)0;
+        if (in(x, y)) g = jac4(ca, Rb[2 * m * RAW + 2 * p + 1 - 2 + H2], e[-1], o[0], e[0], o[VDW]);
+        Vb[2 * m * VAW + 2 * p + 1] = g;
+      }
+      {   // y = b0-1+2m odd: green at x = a0-2+2p; O(i-1,J), E(i,J), O(i,J), E(i,J+1) with i = x/2, J = y/2
+        const int y = b0 - 1 + 2 * m, x = a0 - 2 + 2 * p;
+        const T *e = Eb + (m + 1) * VDW + p - 1 + H2, *o = Ob + (m + 1) * VDW + p - 1 + H2;
+        T g = (T)0;
+        if (in(x, y)) g = jac4(ca, Rb[(2 * m + 1) * RAW + 2 * p - 2 + H2], o[-1], e[0], o[0], e[VDW]);
+        Vb[(2 * m + 1) * VAW + 2 * p] = g;
+      }
+    }
+    __syncthreads();
+    // A(s) colour 2: the D(s) node (x + y even) of each pair (a0-1+2p, a0+2p), rows b0-1 .. b0+TY
+    constexpr int DP = TX / 2 + 1, DR = TY / 2 + 1;
+#pragma unroll
+    for (int k = 0; k < (DP * DR + NT - 1) / NT; k++) {
+      const int i = threadIdx.x + k * NT;
+      if (DP * DR % NT && i >= DP * DR) break;
+      const int p = i % DP, m = i / DP;
+      {   // y = b0-1+2m odd: x = a0-1+2p
+        const int y = b0 - 1 + 2 * m, x = a0 - 1 + 2 * p;
+        T *q = Vb + (2 * m + 1) * VAW + 2 * p + 1;
+        T v = (T)0;
+        if (in(x, y)) v = jac4(ca, Rb[(2 * m + 1) * RAW + 2 * p + 1 - 2 + H2], q[-1], q[-VAW], q[1], q[VAW]);
+        *q = v;
+      }
+      {   // y = b0+2m even: x = a0+2p
+        const int y = b0 + 2 * m, x = a0 + 2 * p;
+        T *q = Vb + (2 * m + 2) * VAW + 2 * p + 2;
+        T v = (T)0;
+        if (in(x, y)) v = jac4(ca, Rb[(2 * m + 2) * RAW + 2 * p - 2 + H2 + 2], q[-1], q[-VAW], q[1], q[VAW]);
+        *q = v;
+      }
+    }
+    __syncthreads();
+    // D(s-1) colour 1 (Eajacr) on O nodes, pairs (a, a+1) = (a0-2+2p, a0-1+2p), rows b0-1 .. b0+TY-1
+    const int64_t pitch = P.v.pitch;
+#pragma unroll
+    for (int k = 0; k < (DP * (TY + 1) + NT - 1) / NT; k++) {
+      const int i = threadIdx.x + k * NT;
+      if (DP * (TY + 1) % NT && i >= DP * (TY + 1)) break;
+      const int b = b0 - 1 + i / DP, a = a0 - 2 + 2 * (i % DP);
+      T ro0, ro1, va0, va1, vb0, vb1;
+      ld2(RO.at(a, b), ro0, ro1);
+      ld2(VA.at(a, b), va0, va1);
+      ld2(VA.at(a, b + 1), vb0, vb1);
+      const T va2 = VA(a + 2, b), vb2 = VA(a + 2, b + 1);
+      const bool okb = b >= 0 && b <= W - 1;
+      const bool ok0 = okb && a >= a0 - 1 && a >= 0 && a <= W - 1, ok1 = okb && a + 1 >= 0 && a + 1 <= W - 1;
+      const T v0 = ok0 ? jac4(cd, ro0, va0, va1, vb1, vb0) : (T)0;
+      const T v1 = ok1 ? jac4(cd, ro1, va1, va2, vb2, vb1) : (T)0;
+      st2(OS.at(a, b), v0, v1);
+      if (okb && b >= b0 && a >= a0) {
+        if (ok1)
+          st2(&P.v.o[(int64_t)b * pitch + a], v0, v1);
+        else if (ok0)
+          P.v.o[(int64_t)b * pitch + a] = v0;
+      }
+    }
+    __syncthreads();
+    // D(s-1) colour 2 (Eajacb) on E nodes, from the new O values
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, a = a0 + 2 * lane;
+#pragma unroll
+    for (int b = b0 + w; b < b0 + TY; b += NW) {
+      if (b < 1 || b > W - 1) continue;
+      T re0, re1, s0, s1, n0, n1;
+      ld2(RE.at(a, b), re0, re1);
+      ld2(OS.at(a, b - 1), s0, s1);
+      ld2(OS.at(a, b), n0, n1);
+      const T sm = OS(a - 1, b - 1), nm = OS(a - 1, b);
+      const T e0 = jac4(cd, re0, sm, s0, n0, nm);
+      const T e1 = jac4(cd, re1, s0, s1, n1, n0);
+      const bool ok0 = a >= 1 && a <= W - 1, ok1 = a + 1 <= W - 1;
+      const int64_t o = (int64_t)b * pitch + a;
+      if (ok0 && ok1)
+        st2(&P.v.e[o], e0, e1);
+      else {
+        if (ok0) P.v.e[o] = e0;
+        if (ok1) P.v.e[o + 1] = e1;
+      }
+    }
+  }
+  static __device__ void finish(const Params &, Acc &) {}
+};
+
 
 // ================================================================= launch
 
@@ -779,6 +936,32 @@ cudaError_t fast2_jac_d(const D2<T> &vc, const S2<T> &r, const S2<T> &v, int M, 
   return run_staged<JacDS<T>::template op>(P, st);
 }
 
+template <class T>
+cudaError_t fast2_jac_ad(const S2<T> &vd, const D2<T> &ra, T ca, const S2<T> &rd, const S2<T> &v, int M, T cd,
+                         cudaStream_t st, bool rev) {
+  using Op = OpJac2AD<T, 2, 256>;   // two stages: a third does not fit next to the scratch tiles
+  typename Op::Params P{};
+  const int W = M / 2, H = W + 1, Hs = W / 2 + 1;
+  if (!tm2<T>(&P.tra, ra.p, H, H, ra.pitch, Op::RAW, Op::RAH) ||
+      !tm2<T>(&P.tve, vd.e, Hs, Hs, vd.pitch, Op::VDW, Op::VDH) ||
+      !tm2<T>(&P.tvo, vd.o, Hs, Hs, vd.pitch, Op::VDW, Op::VDH) ||
+      !tm2<T>(&P.tro, rd.o, H, H, rd.pitch, Op::ROW, Op::ROH) ||
+      !tm2<T>(&P.tre, rd.e, H, H, rd.pitch, Op::REW, Op::REH))
+    return cudaErrorInvalidValue;
+  const int ntx = (W + TX - 1) / TX, nty = (W + TY - 1) / TY;
+  P.v = v;
+  P.M = M;
+  P.ntx = ntx;
+  P.ntiles = ntx * nty;
+  P.rev = rev;
+  P.ca = ca;
+  P.cd = cd;
+  static const int nt = getenv("MG_AD_NT") ? atoi(getenv("MG_AD_NT")) : 512;
+  if (nt != 256)
+    return run_op<OpJac2AD<T, 2, 512>>(reinterpret_cast<const typename OpJac2AD<T, 2, 512>::Params &>(P), st);
+  return run_op<Op>(P, st);
+}
+
 
 #define INSTF(T)                                                                                                   \
   template cudaError_t fast2_desc_fine<T>(const T *, const T *, int64_t, const S2<T> &, int, int, const Coef<T> &, \
@@ -790,7 +973,9 @@ cudaError_t fast2_jac_d(const D2<T> &vc, const S2<T> &r, const S2<T> &v, int M, 
   template cudaError_t fast2_rest_ad<T>(const D2<T> &, const S2<T> &, int, cudaStream_t, const Rows2 &);           \
   template cudaError_t fast2_rest_da<T>(const S2<T> &, const D2<T> &, int, cudaStream_t, const Rows2 &);           \
   template cudaError_t fast2_jac_d<T>(const D2<T> &, const S2<T> &, const S2<T> &, int, T, cudaStream_t,           \
-                                      const Rows2 &);
+                                      const Rows2 &);                                                              \
+  template cudaError_t fast2_jac_ad<T>(const S2<T> &, const D2<T> &, T, const S2<T> &, const S2<T> &, int, T,      \
+                                       cudaStream_t, bool);
 
 INSTF(float)
 INSTF(double)

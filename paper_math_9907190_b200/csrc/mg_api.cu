@@ -29,6 +29,11 @@ struct Impl2 : ImplBase {
   D2<T> tmpA{};            // sweeps > 1: E nodes of v_D(s) as a dense A(2s)-shaped array
   S2<T> tmpD{};            //             D nodes of v_A(s) as split E/O arrays
   bool xfuse = !env_flag("MG_2D_NOXFUSE");   // cross-cycle fusion of the finest ascent and descent
+  bool adfuse = !env_flag("MG_2D_NOADFUSE");  // jac_a(s) fused with jac_d(s-1): v_A(s) stays on chip
+  // ... for octaves s >= ad_min (MG_AD_MINO, default 2): measured on B200 at 8193^2 the fused pass beats the
+  // two separate ones from s = 2 down (0.052 vs 0.055 ms at s = 2) but not at s = 1 (0.183 vs 0.170 ms: the
+  // pass is issue-bound there, one 163 KB-shared-memory CTA per SM)
+  int ad_min = getenv("MG_AD_MINO") && atoi(getenv("MG_AD_MINO")) > 1 ? atoi(getenv("MG_AD_MINO")) : 2;
   Lev2<T> *d_lev = nullptr;
   std::vector<Lev2<T>> h_lev;   // host copy of the level descriptors (tail kernel parameters)
   explicit Impl2(const mg_solver *sv) : s(sv), k(sv->k), n(sv->cfg.n), pitch(sv->pitch) {}
@@ -212,10 +217,18 @@ struct Impl2 : ImplBase {
       STEP("rest_da", 2 * o + 1, 1, w * (Nl[2 * o + 1] + Nl[2 * o + 2]));
       fast2_rest_da<T>(rD[o], rA[o + 1], M[o + 1], st, dD);
     };
+    bool d_done = false;   // jac_d(o) already ran inside the fused pass of octave o + 1
     auto ascent = [&](int o) {
-      STEP("jac_d", 2 * o + 1, 1, w * (Nl[2 * o + 2] + 2 * Nl[2 * o + 1]));
-      fast2_jac_d<T>(vA[o + 1], rD[o], vD[o], M[o], cD[o], st, fwd);
-      if (o >= 1) {
+      if (!d_done) {
+        STEP("jac_d", 2 * o + 1, 1, w * (Nl[2 * o + 2] + 2 * Nl[2 * o + 1]));
+        fast2_jac_d<T>(vA[o + 1], rD[o], vD[o], M[o], cD[o], st, fwd);
+      }
+      d_done = false;
+      if (o >= 1 && adfuse && o >= ad_min) {
+        STEP("jac_ad", 2 * o, 1, w * (Nl[2 * o + 1] + Nl[2 * o] + 2 * Nl[2 * o - 1]));
+        fast2_jac_ad<T>(vD[o], rA[o], cA[o], rD[o - 1], vD[o - 1], M[o - 1], cD[o - 1], st, serp);
+        d_done = true;
+      } else if (o >= 1) {
         STEP("jac_a", 2 * o, 1, w * (Nl[2 * o + 1] + 2 * Nl[2 * o]));
         fast2_jac_a<T>(vD[o], rA[o], vA[o], M[o], cA[o], st, bwd);
       } else if (mode & kFuseNext) {
@@ -276,7 +289,9 @@ struct Impl2 : ImplBase {
       const int od = use_tail ? om : oc;
       // desc_fine, rest_ad (o >= 1) + rest_da per descent octave, tail or coarse, jac_d + jac_a/asc per ascent
       // octave; with cross-cycle fusion a steady-state cycle has no desc_fine (the previous cycle's asc_desc ran it)
-      return 1 + (od - 1) + od + 1 + 2 * od + (use_tail ? 0 : 3 * (oc - od)) - (fuses_cycles() ? 1 : 0);
+      // jac_a(o) and jac_d(o - 1) share one pass for o >= 1
+      return 1 + (od - 1) + od + 1 + 2 * od + (use_tail ? 0 : 3 * (oc - od)) - (fuses_cycles() ? 1 : 0) -
+             (adfuse && od > ad_min ? od - ad_min : 0);
     }
     int c = 1;                               // desc fine
     for (int o = 0; o + 1 < k; o++) c += (o >= 1) + 1;
