@@ -552,9 +552,9 @@ struct OpJac2A {
 // A(s)'s node space.  v_A(s) is computed (OpJac2A's two colours, same node
 // formulas and operand order) on the ring [a0-1, a0+TX] x [b0-1, b0+TY] that
 // the O update needs, then OpJac2D's two colours run from shared memory.
-template <class T, int STG, int NTH>
+template <class T, int STG, int NTH, int TYA>
 struct OpJac2AD {
-  static constexpr int NT = NTH, STAGES = STG, NW = NT / 32;
+  static constexpr int NT = NTH, STAGES = STG, NW = NT / 32, TY = TYA;
   static constexpr int H2 = hx<T>(2), H1 = hx<T>(1);
   static constexpr int RAW = w16<T>(TX + 2 + H2), RAH = TY + 4;            // r_A(s): [a0-2, a0+TX+2) x [b0-2, b0+TY+2)
   static constexpr int VDW = w16<T>(TX / 2 + 2 + H2), VDH = TY / 2 + 4;    // v_D(s) E/O: the D(s) ring of those greens
@@ -939,16 +939,20 @@ cudaError_t fast2_jac_d(const D2<T> &vc, const S2<T> &r, const S2<T> &v, int M, 
 template <class T>
 cudaError_t fast2_jac_ad(const S2<T> &vd, const D2<T> &ra, T ca, const S2<T> &rd, const S2<T> &v, int M, T cd,
                          cudaStream_t st, bool rev) {
-  using Op = OpJac2AD<T, 2, 256>;   // two stages: a third does not fit next to the scratch tiles
+  using Op = OpJac2AD<T, 2, 512, 32>;   // Params and tile widths do not depend on NT / TY
   typename Op::Params P{};
   const int W = M / 2, H = W + 1, Hs = W / 2 + 1;
-  if (!tm2<T>(&P.tra, ra.p, H, H, ra.pitch, Op::RAW, Op::RAH) ||
-      !tm2<T>(&P.tve, vd.e, Hs, Hs, vd.pitch, Op::VDW, Op::VDH) ||
-      !tm2<T>(&P.tvo, vd.o, Hs, Hs, vd.pitch, Op::VDW, Op::VDH) ||
-      !tm2<T>(&P.tro, rd.o, H, H, rd.pitch, Op::ROW, Op::ROH) ||
-      !tm2<T>(&P.tre, rd.e, H, H, rd.pitch, Op::REW, Op::REH))
+  static const int nt = getenv("MG_AD_NT") ? atoi(getenv("MG_AD_NT")) : 512;
+  static const int ty = getenv("MG_AD_TY") ? atoi(getenv("MG_AD_TY")) : 16;
+  const int tyv = (ty == 32 || ty == 8) ? ty : 16;   // 16 rows: two CTAs per SM (measured best)
+  const int ryh = tyv + 4, vdh = tyv / 2 + 4;
+  if (!tm2<T>(&P.tra, ra.p, H, H, ra.pitch, Op::RAW, ryh) ||
+      !tm2<T>(&P.tve, vd.e, Hs, Hs, vd.pitch, Op::VDW, vdh) ||
+      !tm2<T>(&P.tvo, vd.o, Hs, Hs, vd.pitch, Op::VDW, vdh) ||
+      !tm2<T>(&P.tro, rd.o, H, H, rd.pitch, Op::ROW, tyv + 1) ||
+      !tm2<T>(&P.tre, rd.e, H, H, rd.pitch, Op::REW, tyv))
     return cudaErrorInvalidValue;
-  const int ntx = (W + TX - 1) / TX, nty = (W + TY - 1) / TY;
+  const int ntx = (W + TX - 1) / TX, nty = (W + tyv - 1) / tyv;
   P.v = v;
   P.M = M;
   P.ntx = ntx;
@@ -956,10 +960,19 @@ cudaError_t fast2_jac_ad(const S2<T> &vd, const D2<T> &ra, T ca, const S2<T> &rd
   P.rev = rev;
   P.ca = ca;
   P.cd = cd;
-  static const int nt = getenv("MG_AD_NT") ? atoi(getenv("MG_AD_NT")) : 512;
-  if (nt != 256)
-    return run_op<OpJac2AD<T, 2, 512>>(reinterpret_cast<const typename OpJac2AD<T, 2, 512>::Params &>(P), st);
-  return run_op<Op>(P, st);
+#define AD_RUN(NTV, TYV) \
+  return run_op<OpJac2AD<T, 2, NTV, TYV>>(reinterpret_cast<const typename OpJac2AD<T, 2, NTV, TYV>::Params &>(P), st)
+  if (tyv == 8) {
+    if (nt == 512) AD_RUN(512, 8);
+    AD_RUN(256, 8);
+  }
+  if (tyv == 16) {
+    if (nt == 256) AD_RUN(256, 16);
+    AD_RUN(512, 16);
+  }
+  if (nt == 256) AD_RUN(256, 32);
+  AD_RUN(512, 32);
+#undef AD_RUN
 }
 
 

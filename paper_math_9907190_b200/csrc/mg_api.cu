@@ -30,10 +30,8 @@ struct Impl2 : ImplBase {
   S2<T> tmpD{};            //             D nodes of v_A(s) as split E/O arrays
   bool xfuse = !env_flag("MG_2D_NOXFUSE");   // cross-cycle fusion of the finest ascent and descent
   bool adfuse = !env_flag("MG_2D_NOADFUSE");  // jac_a(s) fused with jac_d(s-1): v_A(s) stays on chip
-  // ... for octaves s >= ad_min (MG_AD_MINO, default 2): measured on B200 at 8193^2 the fused pass beats the
-  // two separate ones from s = 2 down (0.052 vs 0.055 ms at s = 2) but not at s = 1 (0.183 vs 0.170 ms: the
-  // pass is issue-bound there, one 163 KB-shared-memory CTA per SM)
-  int ad_min = getenv("MG_AD_MINO") && atoi(getenv("MG_AD_MINO")) > 1 ? atoi(getenv("MG_AD_MINO")) : 2;
+  // ... for octaves s >= ad_min (MG_AD_MINO, default 1): 16-row tiles, two 90 KB CTAs of 512 threads per SM
+  int ad_min = getenv("MG_AD_MINO") && atoi(getenv("MG_AD_MINO")) >= 1 ? atoi(getenv("MG_AD_MINO")) : 1;
   Lev2<T> *d_lev = nullptr;
   std::vector<Lev2<T>> h_lev;   // host copy of the level descriptors (tail kernel parameters)
   explicit Impl2(const mg_solver *sv) : s(sv), k(sv->k), n(sv->cfg.n), pitch(sv->pitch) {}

@@ -64,8 +64,9 @@ CASES = [
     ({"MG_XF_PAIRS": "1"}, 2, 513, 2, "float32"),
     ({"MG_2D_NOADFUSE": "1"}, 2, 513, 2, "float64"),
     ({"MG_2D_NOADFUSE": "1"}, 2, 257, 4, "float32"),
-    ({"MG_AD_MINO": "1"}, 2, 513, 2, "float64"),
-    ({"MG_AD_MINO": "1", "MG_AD_NT": "256"}, 2, 1025, 4, "float32"),
+    ({"MG_AD_MINO": "2"}, 2, 513, 2, "float64"),
+    ({"MG_AD_TY": "32", "MG_AD_NT": "256"}, 2, 1025, 4, "float32"),
+    ({"MG_AD_TY": "8"}, 2, 513, 2, "float64"),
     ({"MG_3D_NOSERP": "1"}, 3, 129, 2, "float64"),
 ]
 
