@@ -733,7 +733,10 @@ template <class Op>
 static cudaError_t run_op(const typename Op::Params &P, cudaStream_t st) {
   cudaError_t e = cudaFuncSetAttribute(tile_pipeline<Op>, cudaFuncAttributeMaxDynamicSharedMemorySize, Op::SMEM);
   if (e != cudaSuccess) return note_launch(e);
-  int per_sm = (227 * 1024) / (Op::SMEM + 1024);
+  // persistent CTAs: never more than can be resident at once (shared memory, registers and threads)
+  int per_sm = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tile_pipeline<Op>, Op::NT, Op::SMEM) != cudaSuccess)
+    per_sm = (227 * 1024) / (Op::SMEM + 1024);
   if (per_sm < 1) per_sm = 1;
   if (per_sm > 4) per_sm = 4;
   int grid = num_sms() * per_sm;
@@ -942,7 +945,7 @@ cudaError_t fast2_jac_ad(const S2<T> &vd, const D2<T> &ra, T ca, const S2<T> &rd
   using Op = OpJac2AD<T, 2, 512, 32>;   // Params and tile widths do not depend on NT / TY
   typename Op::Params P{};
   const int W = M / 2, H = W + 1, Hs = W / 2 + 1;
-  static const int nt = getenv("MG_AD_NT") ? atoi(getenv("MG_AD_NT")) : 512;
+  static const int nt = getenv("MG_AD_NT") ? atoi(getenv("MG_AD_NT")) : 576;
   static const int ty = getenv("MG_AD_TY") ? atoi(getenv("MG_AD_TY")) : 16;
   const int tyv = (ty == 32 || ty == 8) ? ty : 16;   // 16 rows: two CTAs per SM (measured best)
   const int ryh = tyv + 4, vdh = tyv / 2 + 4;
@@ -968,7 +971,8 @@ cudaError_t fast2_jac_ad(const S2<T> &vd, const D2<T> &ra, T ca, const S2<T> &rd
   }
   if (tyv == 16) {
     if (nt == 256) AD_RUN(256, 16);
-    AD_RUN(512, 16);
+    if (nt == 512) AD_RUN(512, 16);
+    AD_RUN(576, 16);   // 18 warps: the O colour (33 x 17 pairs) in one round
   }
   if (nt == 256) AD_RUN(256, 32);
   AD_RUN(512, 32);
