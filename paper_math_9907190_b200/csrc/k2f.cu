@@ -327,6 +327,101 @@ struct OpRest2DA {
   static __device__ void finish(const Params &, Acc &) {}
 };
 
+// ========== restriction D(s) -> A(s+1) -> D(s+1) in one pass (Erest2b, Erest2r)
+// Tile [X0, X0+TX) x [Y0, Y0+TYA) of A(s+1): r_A(s+1) is formed (OpRest2DA's
+// formula) on the tile and its one-node ring in shared memory, written for the
+// tile, and restricted onto D(s+1) (OpRest2AD's formulas) from shared memory.
+template <class T, int STG, int NTH, int TYA>
+struct OpRest2DAD {
+  static constexpr int NT = NTH, STAGES = STG, NW = NT / 32, TY = TYA;
+  static constexpr int H1 = hx<T>(1), H2 = hx<T>(2);
+  static constexpr int EW = w16<T>(TX + 1 + H1), EH = TY + 2;   // E of r_D(s): [X0-1, X0+TX] x [Y0-1, Y0+TY]
+  static constexpr int OW = w16<T>(TX + 1 + H2), OH = TY + 3;   // O of r_D(s): [X0-2, X0+TX] x [Y0-2, Y0+TY]
+  static constexpr int E_BYTES = EW * EH * sizeof(T), O_BYTES = OW * OH * sizeof(T);
+  static constexpr int E_OFF = 0, O_OFF = al128(E_BYTES);
+  static constexpr int STAGE = al128(O_OFF + O_BYTES);
+  static constexpr int RSW = TX + 4, RSH = TY + 2;              // r_A(s+1) on [X0-2, X0+TX+2) x [Y0-1, Y0+TY]
+  static constexpr int SMEM = STAGES * STAGE + al128(RSW * RSH * sizeof(T));
+  struct Params {
+    CUtensorMap te, to;
+    D2<T> ra;    // r_A(s+1)
+    S2<T> rd;    // r_D(s+1)
+    int Mc, ntx, ntiles;
+    int rev;
+  };
+  using Acc = NoAcc;
+  static __device__ void prefetch(const Params &P) {
+    tma_prefetch_desc(&P.te);
+    tma_prefetch_desc(&P.to);
+  }
+  static __device__ void init(Acc &) {}
+  static __device__ void issue(const Params &P, int t, unsigned char *st, uint64_t *bar) {
+    const int X0 = (t % P.ntx) * TX, Y0 = (t / P.ntx) * TY;
+    mbar_expect_tx(bar, E_BYTES + O_BYTES);
+    tma_load_2d(st + E_OFF, &P.te, X0 - H1, Y0 - 1, bar);
+    tma_load_2d(st + O_OFF, &P.to, X0 - H2, Y0 - 2, bar);
+  }
+  static __device__ void compute(const Params &P, int t, unsigned char *st, unsigned char *scr, Acc &) {
+    const int X0 = (t % P.ntx) * TX, Y0 = (t / P.ntx) * TY, Mc = P.Mc;
+    const T *Eb = (const T *)(st + E_OFF), *Ob = (const T *)(st + O_OFF);
+    T *Rb = (T *)scr;
+    // r_A(s+1) at (X, Y), X = X0-1 .. X0+TX, Y = Y0-1 .. Y0+TY: pairs (X0-1+2p, X0+2p)
+    constexpr int RP = TX / 2 + 1, RR = TY + 2;
+#pragma unroll
+    for (int k = 0; k < (RP * RR + NT - 1) / NT; k++) {
+      const int i = threadIdx.x + k * NT;
+      if (RP * RR % NT && i >= RP * RR) break;
+      const int p = i % RP, r = i / RP, Y = Y0 - 1 + r;
+      // E(X, Y) at Eb[r * EW + X - X0 + H1]; O(X, Y) at Ob[(r + 1) * OW + X - X0 + H2]
+      const T *e = Eb + r * EW + 2 * p - 1 + H1, *o = Ob + (r + 1) * OW + 2 * p - 1 + H2;
+      const bool oky = Y >= 1 && Y <= Mc - 1;
+#pragma unroll
+      for (int q = 0; q < 2; q++) {
+        const int X = X0 - 1 + 2 * p + q;
+        // Erest2b: E(X,Y), O(X-1,Y-1), O(X,Y-1), O(X,Y), O(X-1,Y)
+        const T v = (oky && X >= 1 && X <= Mc - 1) ? erest2b(e[q], o[q - 1 - OW], o[q - OW], o[q], o[q - 1]) : (T)0;
+        Rb[r * RSW + 2 * p + 1 + q] = v;
+      }
+    }
+    __syncthreads();
+    // the tile's r_A(s+1) (aligned pairs) and Erest2r onto D(s+1): rows (y, y+1), y = Y0 + 2b
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, xl = X0 + 2 * lane;
+    STile<T> R = stile<T>(scr, RSW, X0 - 2, Y0 - 1);
+    const int64_t pitch = P.rd.pitch;
+#pragma unroll
+    for (int b = w; b < TY / 2; b += NW) {
+      const int y = Y0 + 2 * b;
+      T rc, rE, rN, ro;
+      ld2(R.at(xl, y), rc, rE);
+      ld2(R.at(xl, y + 1), rN, ro);
+      if (y <= Mc - 1) {
+        const bool ok0 = xl >= 1 && xl <= Mc - 1, ok1 = xl + 1 <= Mc - 1;
+        if (y >= 1) {
+          if (ok0 && ok1)
+            st2(&P.ra(xl, y), rc, rE);
+          else {
+            if (ok0) P.ra(xl, y) = rc;
+            if (ok1) P.ra(xl + 1, y) = rE;
+          }
+        }
+        if (y + 1 <= Mc - 1) {
+          if (ok0 && ok1)
+            st2(&P.ra(xl, y + 1), rN, ro);
+          else {
+            if (ok0) P.ra(xl, y + 1) = rN;
+            if (ok1) P.ra(xl + 1, y + 1) = ro;
+          }
+        }
+        const int64_t o = (int64_t)(y / 2) * pitch + xl / 2;
+        if (xl >= 2 && xl <= Mc - 2 && y >= 2 && y <= Mc - 2)
+          P.rd.e[o] = erest2r(rc, R(xl - 1, y), R(xl, y - 1), rE, rN);
+        if (xl + 1 <= Mc - 1 && y + 1 <= Mc - 1) P.rd.o[o] = erest2r(ro, rN, rE, R(xl + 2, y + 1), R(xl + 1, y + 2));
+      }
+    }
+  }
+  static __device__ void finish(const Params &, Acc &) {}
+};
+
 // ================================ ascent D(s) from A(2s): Eajacr then Eajacb
 // tile in E/O index space [a0, a0+TX) x [b0, b0+TY); the O values are also
 // computed on the one-node ring below/left that the E update needs.
@@ -940,6 +1035,23 @@ cudaError_t fast2_jac_d(const D2<T> &vc, const S2<T> &r, const S2<T> &v, int M, 
 }
 
 template <class T>
+cudaError_t fast2_rest_dad(const S2<T> &d, const D2<T> &ra, const S2<T> &rd, int Mc, cudaStream_t st, bool rev) {
+  using Op = OpRest2DAD<T, 2, 576, 32>;
+  typename Op::Params P{};
+  const int H = Mc + 1;   // E/O arrays of D(s) have Mc + 1 entries per side
+  if (!tm2<T>(&P.te, d.e, H, H, d.pitch, Op::EW, Op::EH) || !tm2<T>(&P.to, d.o, H, H, d.pitch, Op::OW, Op::OH))
+    return cudaErrorInvalidValue;
+  const int ntx = (Mc + TX - 1) / TX, nty = (Mc + Op::TY - 1) / Op::TY;
+  P.ra = ra;
+  P.rd = rd;
+  P.Mc = Mc;
+  P.ntx = ntx;
+  P.ntiles = ntx * nty;
+  P.rev = rev;
+  return run_op<Op>(P, st);
+}
+
+template <class T>
 cudaError_t fast2_jac_ad(const S2<T> &vd, const D2<T> &ra, T ca, const S2<T> &rd, const S2<T> &v, int M, T cd,
                          cudaStream_t st, bool rev) {
   using Op = OpJac2AD<T, 2, 512, 32>;   // Params and tile widths do not depend on NT / TY
@@ -991,6 +1103,7 @@ cudaError_t fast2_jac_ad(const S2<T> &vd, const D2<T> &ra, T ca, const S2<T> &rd
   template cudaError_t fast2_rest_da<T>(const S2<T> &, const D2<T> &, int, cudaStream_t, const Rows2 &);           \
   template cudaError_t fast2_jac_d<T>(const D2<T> &, const S2<T> &, const S2<T> &, int, T, cudaStream_t,           \
                                       const Rows2 &);                                                              \
+  template cudaError_t fast2_rest_dad<T>(const S2<T> &, const D2<T> &, const S2<T> &, int, cudaStream_t, bool);   \
   template cudaError_t fast2_jac_ad<T>(const S2<T> &, const D2<T> &, T, const S2<T> &, const S2<T> &, int, T,      \
                                        cudaStream_t, bool);
 

@@ -107,6 +107,10 @@ cudaError_t fast2_asc_desc(const S2<T> &vd, const T *u_old, const T *f, int64_t 
 template <class T>
 cudaError_t fast2_jac_d(const D2<T> &vc, const S2<T> &r, const S2<T> &v, int M, T c, cudaStream_t st,
                         const Rows2 &rw = Rows2());
+// rest_da of D(s) (r_A(s+1), written) fused with rest_ad of A(s+1) (r_D(s+1));
+// Mc = the size of A(s+1); whole level only (single GPU).
+template <class T>
+cudaError_t fast2_rest_dad(const S2<T> &d, const D2<T> &ra, const S2<T> &rd, int Mc, cudaStream_t st, bool rev);
 // jac_a on A(s) (v_A(s) from v_D(s), r_A(s); M = the fine size of D(s-1))
 // fused with jac_d on D(s-1) (v_D(s-1) from v_A(s), r_D(s-1)): v_A(s) stays in
 // shared memory; whole level only (single GPU).

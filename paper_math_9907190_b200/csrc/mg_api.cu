@@ -31,6 +31,10 @@ struct Impl2 : ImplBase {
   bool xfuse = !env_flag("MG_2D_NOXFUSE");   // cross-cycle fusion of the finest ascent and descent
   bool adfuse = !env_flag("MG_2D_NOADFUSE");  // jac_a(s) fused with jac_d(s-1): v_A(s) stays on chip
   // ... for octaves s >= ad_min (MG_AD_MINO, default 1): 16-row tiles, two 90 KB CTAs of 512 threads per SM
+  bool dafuse = !env_flag("MG_2D_NODAFUSE");  // rest_da(s) fused with rest_ad(s+1): r_A(s+1) not re-read
+  // ... for octaves s >= da_min (MG_DA_MINO); measured on B200 at 8193^2: fp64 gains from s = 0 (0.089 vs
+  // 0.066 + 0.033 ms), fp32 loses there (0.056 vs 0.034 + 0.021 ms) and gains from s = 1
+  int da_min = getenv("MG_DA_MINO") ? atoi(getenv("MG_DA_MINO")) : (sizeof(T) == 4 ? 1 : 0);
   int ad_min = getenv("MG_AD_MINO") && atoi(getenv("MG_AD_MINO")) >= 1 ? atoi(getenv("MG_AD_MINO")) : 1;
   Lev2<T> *d_lev = nullptr;
   std::vector<Lev2<T>> h_lev;   // host copy of the level descriptors (tail kernel parameters)
@@ -207,10 +211,19 @@ struct Impl2 : ImplBase {
       STEP("desc_fine", 0, 1, w * (2 * Nl[0] + Nl[1]));
       fast2_desc_fine<T>(uin, fe, pitch, rD[0], M[0], s->cfg.order, coef, sink(), st, fwd);
     }
+    const int od = use_tail ? om : oc;   // first octave not run by per-level kernels
+    bool a_done = false;                 // rest_ad(o) already ran inside the fused pass of octave o - 1
     auto descent = [&](int o) {
-      if (o >= 1) {
+      if (o >= 1 && !a_done) {
         STEP("rest_ad", 2 * o, 1, w * (Nl[2 * o] + Nl[2 * o + 1]));
         fast2_rest_ad<T>(rA[o], rD[o], M[o], st, dA);
+      }
+      a_done = false;
+      if (dafuse && o >= da_min && o + 1 < od) {
+        STEP("rest_dad", 2 * o + 1, 1, w * (Nl[2 * o + 1] + Nl[2 * o + 2] + Nl[2 * o + 3]));
+        fast2_rest_dad<T>(rD[o], rA[o + 1], rD[o + 1], M[o + 1], st, dD.rev);
+        a_done = true;
+        return;
       }
       STEP("rest_da", 2 * o + 1, 1, w * (Nl[2 * o + 1] + Nl[2 * o + 2]));
       fast2_rest_da<T>(rD[o], rA[o + 1], M[o + 1], st, dD);
@@ -238,7 +251,6 @@ struct Impl2 : ImplBase {
         fast2_asc_fine<T>(vD[0], uin, fe, pitch, (T *)u_out, M[0], s->cfg.order, cA[0], coef, st, bwd);
       }
     };
-    const int od = use_tail ? om : oc;   // first octave not run by per-level kernels
     for (int o = 0; o < od; o++) descent(o);
     bool tail_done = false;
     if (use_tail) {
@@ -289,7 +301,8 @@ struct Impl2 : ImplBase {
       // octave; with cross-cycle fusion a steady-state cycle has no desc_fine (the previous cycle's asc_desc ran it)
       // jac_a(o) and jac_d(o - 1) share one pass for o >= 1
       return 1 + (od - 1) + od + 1 + 2 * od + (use_tail ? 0 : 3 * (oc - od)) - (fuses_cycles() ? 1 : 0) -
-             (adfuse && od > ad_min ? od - ad_min : 0);
+             (adfuse && od > ad_min ? od - ad_min : 0) -
+             (dafuse && od - 1 > da_min ? od - 1 - da_min : 0);
     }
     int c = 1;                               // desc fine
     for (int o = 0; o + 1 < k; o++) c += (o >= 1) + 1;
