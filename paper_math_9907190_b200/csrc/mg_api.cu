@@ -221,7 +221,8 @@ struct Impl2 : ImplBase {
       a_done = false;
       if (dafuse && o >= da_min && o + 1 < od) {
         STEP("rest_dad", 2 * o + 1, 1, w * (Nl[2 * o + 1] + Nl[2 * o + 2] + Nl[2 * o + 3]));
-        fast2_rest_dad<T>(rD[o], rA[o + 1], rD[o + 1], M[o + 1], st, dD.rev);
+        // serpentine: consecutive octave-pair passes walk in opposite directions
+        fast2_rest_dad<T>(rD[o], rA[o + 1], rD[o + 1], M[o + 1], st, dD.rev ^ (serp && (o & 1)));
         a_done = true;
         return;
       }
@@ -237,7 +238,8 @@ struct Impl2 : ImplBase {
       d_done = false;
       if (o >= 1 && adfuse && o >= ad_min) {
         STEP("jac_ad", 2 * o, 1, w * (Nl[2 * o + 1] + Nl[2 * o] + 2 * Nl[2 * o - 1]));
-        fast2_jac_ad<T>(vD[o], rA[o], cA[o], rD[o - 1], vD[o - 1], M[o - 1], cD[o - 1], st, serp);
+        fast2_jac_ad<T>(vD[o], rA[o], cA[o], rD[o - 1], vD[o - 1], M[o - 1], cD[o - 1], st,
+                        serp && !((o - 1) & 1));   // alternating, backwards at s = 1
         d_done = true;
       } else if (o >= 1) {
         STEP("jac_a", 2 * o, 1, w * (Nl[2 * o + 1] + 2 * Nl[2 * o]));
