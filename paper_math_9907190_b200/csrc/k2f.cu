@@ -1057,7 +1057,8 @@ cudaError_t fast2_jac_ad(const S2<T> &vd, const D2<T> &ra, T ca, const S2<T> &rd
   using Op = OpJac2AD<T, 2, 512, 32>;   // Params and tile widths do not depend on NT / TY
   typename Op::Params P{};
   const int W = M / 2, H = W + 1, Hs = W / 2 + 1;
-  static const int nt = getenv("MG_AD_NT") ? atoi(getenv("MG_AD_NT")) : 576;
+  // measured: fp64 576 threads (two CTAs per SM), fp32 256 (four)
+  static const int nt = getenv("MG_AD_NT") ? atoi(getenv("MG_AD_NT")) : (sizeof(T) == 4 ? 256 : 576);
   static const int ty = getenv("MG_AD_TY") ? atoi(getenv("MG_AD_TY")) : 16;
   const int tyv = (ty == 32 || ty == 8) ? ty : 16;   // 16 rows: two CTAs per SM (measured best)
   const int ryh = tyv + 4, vdh = tyv / 2 + 4;
