@@ -1048,6 +1048,10 @@ cudaError_t fast2_rest_dad(const S2<T> &d, const D2<T> &ra, const S2<T> &rd, int
   P.ntx = ntx;
   P.ntiles = ntx * nty;
   P.rev = rev;
+  // measured: fp64 576 threads (two CTAs per SM), fp32 256 (four; with 576 the fp32 pass is issue-bound)
+  static const int nt = getenv("MG_DA_NT") ? atoi(getenv("MG_DA_NT")) : (sizeof(T) == 4 ? 256 : 576);
+  if (nt == 256)
+    return run_op<OpRest2DAD<T, 2, 256, 32>>(reinterpret_cast<const typename OpRest2DAD<T, 2, 256, 32>::Params &>(P), st);
   return run_op<Op>(P, st);
 }
 

@@ -32,9 +32,9 @@ struct Impl2 : ImplBase {
   bool adfuse = !env_flag("MG_2D_NOADFUSE");  // jac_a(s) fused with jac_d(s-1): v_A(s) stays on chip
   // ... for octaves s >= ad_min (MG_AD_MINO, default 1): 16-row tiles, two 90 KB CTAs of 512 threads per SM
   bool dafuse = !env_flag("MG_2D_NODAFUSE");  // rest_da(s) fused with rest_ad(s+1): r_A(s+1) not re-read
-  // ... for octaves s >= da_min (MG_DA_MINO); measured on B200 at 8193^2: fp64 gains from s = 0 (0.089 vs
-  // 0.066 + 0.033 ms), fp32 loses there (0.056 vs 0.034 + 0.021 ms) and gains from s = 1
-  int da_min = getenv("MG_DA_MINO") ? atoi(getenv("MG_DA_MINO")) : (sizeof(T) == 4 ? 1 : 0);
+  // ... for octaves s >= da_min (MG_DA_MINO, default 0); measured on B200 at 8193^2 fp64 s = 0: 0.089 vs
+  // 0.066 + 0.033 ms; fp32 (256-thread CTAs) 0.052 vs 0.034 + 0.021 ms
+  int da_min = getenv("MG_DA_MINO") ? atoi(getenv("MG_DA_MINO")) : 0;
   int ad_min = getenv("MG_AD_MINO") && atoi(getenv("MG_AD_MINO")) >= 1 ? atoi(getenv("MG_AD_MINO")) : 1;
   Lev2<T> *d_lev = nullptr;
   std::vector<Lev2<T>> h_lev;   // host copy of the level descriptors (tail kernel parameters)

@@ -70,7 +70,9 @@ CASES = [
     ({"MG_AD_NT": "576"}, 2, 513, 2, "float32"),
     ({"MG_2D_NODAFUSE": "1"}, 2, 513, 2, "float64"),
     ({"MG_2D_NODAFUSE": "1"}, 2, 257, 4, "float32"),
-    ({"MG_DA_MINO": "0"}, 2, 513, 2, "float32"),
+    ({"MG_DA_MINO": "1"}, 2, 513, 2, "float32"),
+    ({"MG_DA_NT": "576"}, 2, 513, 2, "float32"),
+    ({"MG_DA_NT": "256"}, 2, 513, 4, "float64"),
     ({"MG_DA_MINO": "2", "MG_AD_MINO": "3"}, 2, 1025, 2, "float64"),
     ({"MG_3D_NOSERP": "1"}, 3, 129, 2, "float64"),
 ]
