@@ -312,7 +312,10 @@ def main():
         "roofline": roofline,
         "cpu_baseline": cpu,
         "e2e": e2e,
-        "gpu_launches": s.launches_per_cycle * args.steps,
+        # per call: K steady-state cycles, plus the first cycle's finest descent when the 2D single-GPU cycles
+        # are fused; tests/test_gpu_launches.py checks this count against the CUDA profiler
+        "gpu_launches": s.launches_per_cycle * args.steps + (
+            1 if (w.dim == 2 and not slabs and os.environ.get("MG_2D_NOXFUSE", "0") in ("", "0")) else 0),
         "clocks": clocks,
     }
     if rank == 0:
