@@ -59,6 +59,7 @@ CASES = [
     ({"MG_PDL": "1"}, 2, 257, 2, "float64"),
     ({"MG_PDL": "1"}, 3, 65, 2, "float64"),
     ({"MG_2D_NOSERP": "1"}, 2, 513, 2, "float64"),
+    ({"MG_PDL_SMALL": "0"}, 2, 513, 2, "float64"),
     ({"MG_2D_NOXFUSE": "1"}, 2, 513, 2, "float64"),
     ({"MG_2D_NOXFUSE": "1"}, 2, 257, 4, "float32"),
     ({"MG_XF_PAIRS": "1"}, 2, 513, 2, "float32"),
