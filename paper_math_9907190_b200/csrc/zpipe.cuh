@@ -230,7 +230,10 @@ static cudaError_t launch_zpipe(typename Op::Params &P, int tx, int ty, int xoff
   if (P.sc.S > zhi - zlo) P.sc.S = zhi - zlo;
   const long long work = (long long)P.sc.T * (zhi - zlo);
   const int grid = work < sms ? (int)work : sms;
-  return note_launch(launch_pdl(zpipe<Op>, dim3(grid), dim3(NT), Op::SMEM, st, P));
+  // small levels (at most one work unit per CTA): programmatic launch (MG_PDL_SMALL3=1)
+  static const bool pdl_small = env_flag("MG_PDL_SMALL3");
+  const bool pdl = pdl_enabled() || (pdl_small && (long long)P.sc.T * P.sc.S <= grid);
+  return note_launch(launch_pdl_if(pdl, zpipe<Op>, dim3(grid), dim3(NT), Op::SMEM, st, P));
 }
 
 // 3D tensor map over nx x ny x nz elements (row pitch, plane stride in
