@@ -95,91 +95,133 @@ def _dist():
     return ws, rank, local
 
 
+def _cpu_model():
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for line in fh:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+class _OneCore:
+    """Pin this process to one host core for the oracle timing (SURVEY 8(d):
+    single thread pinned with os.sched_setaffinity); restore afterwards."""
+
+    def __enter__(self):
+        self.prev = os.sched_getaffinity(0)
+        self.core = min(self.prev)
+        os.sched_setaffinity(0, {self.core})
+        return self
+
+    def __exit__(self, *exc):
+        os.sched_setaffinity(0, self.prev)
+
+
+def _oracle_rate(w, dtype, budget_s, max_cycles):
+    """Oracle cycles of the full workload within ~budget_s on one pinned core."""
+    import oracle
+    oracle.build()
+    f = W.workload_rhs(w.name, dtype)
+    u = np.zeros_like(f)
+    N = (w.n - 2) ** w.dim
+    with _OneCore() as pin:
+        t0 = time.perf_counter()
+        oracle.vcycle(u, f, w.p, 1, order=w.order)       # one warm-up cycle (allocation, page faults)
+        t_one = time.perf_counter() - t0
+        cyc = max(1, min(max_cycles, int(budget_s / max(t_one, 1e-3))))
+        t0 = time.perf_counter()
+        oracle.vcycle(u, f, w.p, cyc, order=w.order)
+        dt = time.perf_counter() - t0
+    sample = (f"{cyc} V-cycle(s) of the full {w.name} workload ({N} unknowns), single-threaded C oracle pinned "
+              f"to host core {pin.core} ({dt:.1f} s; host: {os.cpu_count()} cores, {_cpu_model()})")
+    return N * cyc / dt / 1e9, cyc, dt, sample
+
+
 def run_reference(args, w, ws, rank):
     """The oracle (plain single-threaded C) as the reference arm, on the host."""
     if rank != 0:
         return
-    import oracle
-    oracle.build()
     dtype = np.float64 if args.dtype == "f64" else np.float32
-    f = W.workload_rhs(w.name, dtype)
-    u = np.zeros_like(f)
-    N = (w.n - 2) ** w.dim
-    t0 = time.perf_counter()
-    oracle.vcycle(u, f, w.p, 1, order=w.order)       # one warm-up cycle (allocation, page faults)
-    t_one = time.perf_counter() - t0
-    budget = 150.0
-    steps = max(1, min(args.steps, int(budget / max(t_one, 1e-3))))
-    t0 = time.perf_counter()
-    oracle.vcycle(u, f, w.p, steps, order=w.order)
-    dt = time.perf_counter() - t0
-    value = N * steps / dt / 1e9
-    sample = f"{steps} V-cycle(s) of the full {w.name} workload (requested {args.steps}; capped to ~{budget:.0f} s)"
+    value, steps, dt, sample = _oracle_rate(w, dtype, 150.0, args.steps)
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": steps, "warmup": 1, "ms_per_step": dt / steps * 1e3, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": args.dtype, "data": "synthetic",
         "config": {"workload": w.name, "dim": w.dim, "n": w.n, "order": w.order, "p": list(w.p),
-                   "unknowns": N},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample},
+                   "unknowns": (w.n - 2) ** w.dim},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle",
+                         "sample": sample + f" (requested {args.steps} steps; capped to ~150 s)"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
 
 
 def cpu_baseline(w, dtype, seconds=20.0):
-    """Oracle throughput on a bounded sample of the same workload (1 host core)."""
-    import oracle
-    oracle.build()
-    f = W.workload_rhs(w.name, dtype)
-    u = np.zeros_like(f)
-    N = (w.n - 2) ** w.dim
-    t0 = time.perf_counter()
-    oracle.vcycle(u, f, w.p, 1, order=w.order)
-    t1 = time.perf_counter() - t0
-    cyc = max(1, min(w.cycles, int(seconds / max(t1, 1e-3))))
-    t0 = time.perf_counter()
-    oracle.vcycle(u, f, w.p, cyc, order=w.order)
-    dt = time.perf_counter() - t0
-    return {"value": N * cyc / dt / 1e9, "unit": UNIT, "cores": 1, "kind": "oracle",
-            "sample": f"{cyc} V-cycle(s) of the full {w.name} workload, single-threaded C oracle "
-                      f"({dt:.1f} s; host has {os.cpu_count()} cores)"}
+    """Oracle throughput on a bounded sample of the same workload (1 pinned host core)."""
+    value, _, _, sample = _oracle_rate(w, dtype, seconds, w.cycles)
+    return {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample}
 
 
-def main():
-    ap = argparse.ArgumentParser()
-    ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=400)
-    ap.add_argument("--warmup", type=int, default=20)
-    ap.add_argument("--impl", default="libmg", choices=["libmg", "reference"])
-    ap.add_argument("--workload", default="2d_8193", choices=sorted(W.WORKLOADS))
-    ap.add_argument("--dtype", default="f64", choices=["f64", "f32"])
-    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
-    ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--profile-only", action="store_true", help="short run for ncu (no sampler/e2e/cpu)")
-    args = ap.parse_args()
-    args.warmup = max(args.warmup, 3)
-    w = W.WORKLOADS[args.workload]
-    ws, rank, local = _dist()
-
-    if args.impl == "reference":
-        run_reference(args, w, ws, rank)
-        return
-
+def _spawn(args):
+    """--gpus N without a launcher: re-run this command under torch.distributed.run
+    (one rank per GPU, rendezvous on 127.0.0.1) and pass its exit code on."""
     import torch
-    import torch.distributed as dist
+    have = torch.cuda.device_count()
+    if have < args.gpus:
+        sys.exit(f"bench.py: --gpus {args.gpus} requested but only {have} CUDA device(s) are visible")
+    import socket
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    sys.exit(subprocess.call(cmd))
+
+
+def _roofline(s, u, f, ms_per_step, w, dtype_tag):
+    """Dominant step of a separate, un-graphed per-step profile (CUDA events)."""
+    prof = s.profile(u, f, 10)
+    peak, peak_src = _peaks()
+    top = max(prof, key=lambda r: r["ms"])
+    achieved = top["alg_bytes"] / (top["ms"] / top["launches"] * 1e-3) / 1e9 / top["launches"]
+    total_bytes = sum(r["alg_bytes"] for r in prof)
+    cycle_gbs = total_bytes / (ms_per_step * 1e-3) / 1e9
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tpath):
+        with open(tpath) as fh:
+            tr = json.load(fh)
+        traffic = tr.get(f"{w.name}/{dtype_tag}/{top['name']}")
+    prof_ms = sum(r["ms"] for r in prof)
+    return {
+        "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+        "traffic": traffic, "kernel": top["name"], "kernel_launches": top["launches"],
+        "kernel_ms": top["ms"], "kernel_alg_bytes": top["alg_bytes"],
+        "kernel_share_of_step": top["ms"] / prof_ms,
+        "peak_source": peak_src,
+        "cycle": {"alg_bytes": total_bytes, "achieved": cycle_gbs, "frac": cycle_gbs / peak},
+        "steps": [{k: (round(v, 5) if isinstance(v, float) else v) for k, v in r.items()} for r in prof],
+    }
+
+
+def _b_alg(s, itemsize):
+    """SURVEY 8(d) B_alg per V-cycle: w [5 N_0 + 5 sum_{l=1}^{L-2} N_l + 4 N_{L-1}]
+    (every array once per producer/consumer, interior nodes only)."""
+    L = s.levels
+    pts = [s.level_points(l) for l in range(L)]
+    return itemsize * (5 * pts[0] + 5 * sum(pts[1:L - 1]) + 4 * pts[L - 1])
+
+
+def measure(args, w, tdt, ws, rank, local, slabs, dist, sampler_ok=True):
+    """Time args.steps V-cycles of workload w in one mg_vcycle call (CUDA events
+    on the calling stream, barrier + synchronize on both sides, max over ranks)."""
+    import torch
     from paper_math_9907190_b200.mg import Solver
-
-    torch.cuda.set_device(local)
-    if ws > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    tdt = torch.float64 if args.dtype == "f64" else torch.float32
-    npdt = np.float64 if args.dtype == "f64" else np.float32
-
-    # Multi-GPU: the slab solver over NCCL -- 2D y-slabs, 3D z-slabs, per-level
-    # halo exchange, all-gather agglomeration of the coarse octaves (strong
-    # scaling: the one global grid is split over the ranks).
-    slabs = ws > 1
+    npdt = np.float64 if tdt == torch.float64 else np.float32
+    dtag = "f64" if tdt == torch.float64 else "f32"
     if slabs:
         s = Solver(w.dim, w.n, order=w.order, p=w.p, dtype=tdt, group=dist.group.WORLD)
     else:
@@ -203,9 +245,7 @@ def main():
         s.vcycle(u, f, args.steps)
         torch.cuda.synchronize()
         torch.cuda.profiler.stop()
-        if rank == 0:
-            print(json.dumps({"profile_only": True, "workload": w.name, "steps": args.steps}))
-        return
+        return None
 
     sampler = ClockSampler(local)
     sampler.start()
@@ -238,33 +278,57 @@ def main():
     ms_per_step = ms / args.steps
     units = N if slabs else ws * N   # strong scaling: one grid; replicas: ws grids
     value = units * args.steps / (ms / 1e3) / 1e9
-    clocks = sampler.summary(t0, t1)
+    # SURVEY 8(d) headline fraction: B_alg per cycle (~10 values per unknown) over nominal 8 TB/s per GPU
+    b_alg = _b_alg(s, u.element_size()) * (1 if slabs else ws)
+    res = {"s": s, "u": u, "f": f, "f_host": f_host, "N": N, "units": units, "ms_per_step": ms_per_step,
+           "value": value, "clocks": sampler.summary(t0, t1), "launches": s.launches_per_cycle,
+           "levels": s.levels, "survey_frac_nominal": b_alg / (ms_per_step * 1e-3) / (8.0e12 * ws),
+           "b_alg_per_cycle": b_alg}
+    res["roofline"] = _roofline(s, u, f, ms_per_step, w, dtag)
+    return res
 
-    # per-step CUDA-event profile (separate, un-graphed pass) for the roofline
-    prof = s.profile(u, f, 10)
-    peak, peak_src = _peaks()
-    top = max(prof, key=lambda r: r["ms"])
-    achieved = top["alg_bytes"] / (top["ms"] / top["launches"] * 1e-3) / 1e9 / top["launches"]
-    total_bytes = sum(r["alg_bytes"] for r in prof)
-    cycle_gbs = total_bytes / (ms_per_step * 1e-3) / 1e9
-    traffic = None
-    tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
-    if os.path.exists(tpath):
-        with open(tpath) as fh:
-            tr = json.load(fh)
-        key = f"{w.name}/{args.dtype}/{top['name']}"
-        if key in tr:
-            traffic = tr[key]
-    prof_ms = sum(r["ms"] for r in prof)
-    roofline = {
-        "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-        "traffic": traffic, "kernel": top["name"], "kernel_launches": top["launches"],
-        "kernel_ms": top["ms"], "kernel_alg_bytes": top["alg_bytes"],
-        "kernel_share_of_step": top["ms"] / prof_ms,
-        "peak_source": peak_src,
-        "cycle": {"alg_bytes": total_bytes, "achieved": cycle_gbs, "frac": cycle_gbs / peak},
-        "steps": [{k: (round(v, 5) if isinstance(v, float) else v) for k, v in r.items()} for r in prof],
-    }
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=400)
+    ap.add_argument("--warmup", type=int, default=20)
+    ap.add_argument("--impl", default="libmg", choices=["libmg", "reference"])
+    ap.add_argument("--workload", default="2d_8193", choices=sorted(W.WORKLOADS))
+    ap.add_argument("--dtype", default="f64", choices=["f64", "f32"])
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-sub", action="store_true", help="skip the 3D 513^3 sub-record")
+    ap.add_argument("--profile-only", action="store_true", help="short run for ncu (no sampler/e2e/cpu)")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    w = W.WORKLOADS[args.workload]
+    ws, rank, local = _dist()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ and args.impl != "reference":
+        _spawn(args)
+    if args.impl == "reference":
+        run_reference(args, w, ws, rank)
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    torch.cuda.set_device(local)
+    if ws > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    tdt = torch.float64 if args.dtype == "f64" else torch.float32
+
+    # Multi-GPU: the slab solver over NCCL -- 2D y-slabs, 3D z-slabs, per-level
+    # halo exchange, all-gather agglomeration of the coarse octaves (strong
+    # scaling: the one global grid is split over the ranks).
+    slabs = ws > 1
+    m = measure(args, w, tdt, ws, rank, local, slabs, dist)
+    if m is None:
+        if rank == 0:
+            print(json.dumps({"profile_only": True, "workload": w.name, "steps": args.steps}))
+        return
+    s, u, f, f_host, units = m["s"], m["u"], m["f"], m["f_host"], m["units"]
+    stream = torch.cuda.current_stream()
 
     e2e = None
     if not args.no_e2e:
@@ -294,34 +358,105 @@ def main():
                "step": f"one mg_vcycle_host call: H2D u,f (pinned) + {w.cycles} V-cycles + D2H u",
                "ms_per_step": t_e2e}
 
+    pitch_n = None
+    if not slabs and not args.no_e2e:
+        pitch_n = _pitch_n_rate(s, w, tdt, args)
+
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu:
-        cpu = cpu_baseline(w, npdt)
+        cpu = cpu_baseline(w, np.float64 if args.dtype == "f64" else np.float32)
+
+    # BASELINE configs[4] (3D 513^3 fp64) rides along as a sub-record on one GPU, so
+    # the driver's single line carries both north-star workloads
+    sub = []
+    if not slabs and not args.no_sub and w.name != "3d_513":
+        for key in ("s", "u", "f"):
+            m.pop(key)
+        del s, u, f
+        torch.cuda.empty_cache()
+        w3 = W.WORKLOADS["3d_513"]
+        m3 = measure(args, w3, torch.float64, ws, rank, local, False, dist)
+        sub.append({"workload": w3.name, "dtype": "f64", "value": m3["value"], "unit": UNIT,
+                    "ms_per_step": m3["ms_per_step"], "steps": args.steps, "warmup": args.warmup,
+                    "unknowns": m3["N"], "survey_frac_of_nominal_8tbs": m3["survey_frac_nominal"],
+                    "gpu_launches": m3["s"].launches_per_cycle * args.steps,
+                    "roofline": m3["roofline"], "clocks": m3["clocks"]})
+        del m3
 
     line = {
-        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+        "metric": METRIC, "value": m["value"], "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": m["ms_per_step"], "higher_is_better": True,
         "scaling": "strong" if slabs else "weak", "vs_baseline": None, "dtype": args.dtype, "data": "synthetic",
         "config": {"workload": w.name, "dim": w.dim, "n": w.n, "order": w.order, "p": list(w.p),
-                   "unknowns": N, "rhs": w.note,
+                   "unknowns": m["N"], "rhs": w.note,
                    "parallelism": (f"{'y' if w.dim == 2 else 'z'}-slabs x{ws} (NCCL halo exchange, all-gather agglomeration)" if slabs
                                    else ("replicas" if ws > 1 else "single")),
                    "l2": "inputs larger than L2 (u and f are %.0f MB each vs 126 MB L2)" %
-                         (s.view(u).numel() * u.element_size() / 1e6),
-                   "levels": s.levels},
-        "roofline": roofline,
+                         (s_bytes(w, tdt) / 1e6),
+                   "levels": m["levels"]},
+        "survey_frac_of_nominal_8tbs": m["survey_frac_nominal"],
+        "roofline": m["roofline"],
         "cpu_baseline": cpu,
         "e2e": e2e,
+        "pitch_n": pitch_n,
         # per call: K steady-state cycles, plus the first cycle's finest descent when the 2D single-GPU cycles
         # are fused; tests/test_gpu_launches.py checks this count against the CUDA profiler
-        "gpu_launches": s.launches_per_cycle * args.steps + (
+        "gpu_launches": m["launches"] * args.steps + (
             1 if (w.dim == 2 and not slabs and os.environ.get("MG_2D_NOXFUSE", "0") in ("", "0")) else 0),
-        "clocks": clocks,
+        "clocks": m["clocks"],
+        "sub": sub or None,
     }
     if rank == 0:
         print(json.dumps(line), flush=True)
     if ws > 1:
         dist.destroy_process_group()
+
+
+def s_bytes(w, tdt):
+    import torch
+    return w.n ** w.dim * (8 if tdt == torch.float64 else 4)
+
+
+def _pitch_n_rate(s, w, tdt, args):
+    """The C-ABI default layout (mg_create: pitch = n, unpadded device arrays):
+    same cycles through the same kernels, u and f staged into the work layout
+    once per call (include/mg.h).  One call of the workload's cycle count, timed
+    with CUDA events; reported next to the headline."""
+    import torch
+    from paper_math_9907190_b200 import mg as M
+    npdt = np.float64 if tdt == torch.float64 else np.float32
+    cfg = M.mg_config()
+    cfg.dim, cfg.n, cfg.order = w.dim, w.n, w.order
+    cfg.dtype = M.MG_F64 if tdt == torch.float64 else M.MG_F32
+    pp = list(w.p) + [0.0] * (4 - len(w.p))
+    cfg.p = (M.ctypes.c_double * 4)(*pp)
+    cfg.pitch = 0
+    stream = torch.cuda.current_stream()
+    cfg.stream = stream.cuda_stream
+    cfg.device = torch.cuda.current_device()
+    cfg.nranks, cfg.rank = 1, 0
+    h = M.mg_create_ex(cfg)
+    try:
+        shape = (w.n,) * w.dim
+        u = torch.zeros(shape, dtype=tdt, device="cuda")
+        f = torch.from_numpy(W.workload_rhs(w.name, npdt)).cuda()
+        M.mg_vcycle(h, u.data_ptr(), f.data_ptr(), 3)
+        times = []
+        for _ in range(3):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            M.mg_vcycle(h, u.data_ptr(), f.data_ptr(), w.cycles)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            times.append(e0.elapsed_time(e1))
+        t = float(np.median(times))
+        N = (w.n - 2) ** w.dim
+        return {"value": N * w.cycles / (t / 1e3) / 1e9, "unit": UNIT, "ms_per_call": t, "cycles_per_call": w.cycles,
+                "call": "mg_create(dim, n, order, p) + mg_vcycle on (n, n[, n]) device arrays: pitch = n, staged"}
+    finally:
+        M.mg_destroy(h)
+        del u, f
+        torch.cuda.empty_cache()
 
 
 if __name__ == "__main__":

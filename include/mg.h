@@ -20,10 +20,17 @@
  *  - Arrays are row-major with x fastest: 2D element (i, j) at
  *    base[j * pitch + i]; 3D element (i, j, k) at
  *    base[(k * n + j) * pitch + i] (single GPU).  `pitch` is in elements,
- *    fixed at mg_create_ex time (cfg.pitch; 0 means n).  A pitch whose byte
- *    size is a multiple of 16 lets the library read the caller's arrays
- *    directly; otherwise each call stages them through internal pitched
- *    copies (correct, slower).
+ *    fixed at mg_create_ex time (cfg.pitch; 0 means n, as mg_create uses).
+ *    The V-cycle kernels (TMA tiles) read u and f in a "work layout": rows a
+ *    multiple of 16 bytes, base 16-byte aligned.  Caller arrays already in
+ *    that layout (a pitch whose byte size is a multiple of 16 and aligned
+ *    pointers) are read and updated in place.  Otherwise -- e.g. pitch = n,
+ *    since n = 2^k + 1 never gives 16-byte rows -- each mg_vcycle /
+ *    mg_profile / mg_convergence_factor call copies u and f into library-owned
+ *    work arrays (row pitch n rounded up to 128 bytes; one cudaMemcpy2DAsync
+ *    per array, 2 x 2 N element moves per call), runs the same kernels there
+ *    and copies u back (2 N more).  mg_vcycle_host copies the host arrays
+ *    straight into the work layout.  mg_residual and mg_norm read any pitch.
  *  - u, f, r, x are DEVICE pointers on the solver's device unless the name
  *    says _host.  The caller owns them; the library never frees them.  They
  *    must stay alive until the work queued on the solver's stream completes.
@@ -132,8 +139,9 @@ int mg_residual(mg_solver *s, const void *u, const void *f, void *r);
 
 /* ncycles V-cycles in place on u (ncycles = 0: no-op).  res_hist: NULL, or
  * room for ncycles+1 doubles that receive ||f - L u||_inf before every cycle
- * and after the last; a non-NULL res_hist synchronises the stream and
- * returns MG_EDIVERGED if any entry is not finite. */
+ * and after the last; a non-NULL res_hist synchronises the stream, needs
+ * ncycles < 4096 (MG_EINVAL otherwise; run longer histories in several
+ * calls) and returns MG_EDIVERGED if any entry is not finite. */
 int mg_vcycle(mg_solver *s, void *u, const void *f, int ncycles, double *res_hist);
 
 /* Same as mg_vcycle on HOST arrays (pitch as configured): copies u and f to

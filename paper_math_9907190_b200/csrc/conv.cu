@@ -323,7 +323,7 @@ struct ImplConv : ImplBase {
     residual0(u, f_eff, st);
     push_norm(st);
   }
-  void enqueue_residual(const void *u, const void *f, void *rr, cudaStream_t st) override {
+  void enqueue_residual(const void *u, const void *f, void *rr, cudaStream_t st, int64_t) override {
     if (DIM == 2)
       launch2_residual<T>(D2<const T>{(const T *)u, pitch}, D2<const T>{(const T *)f, pitch}, D2<T>{(T *)rr, pitch},
                           M[0], s->cfg.order, coef, st);
@@ -331,13 +331,13 @@ struct ImplConv : ImplBase {
       launch3_residual<T>(D3<const T>{(const T *)u, pitch, pitch * n}, D3<const T>{(const T *)f, pitch, pitch * n},
                           D3<T>{(T *)rr, pitch, pitch * n}, M[0], s->cfg.order, coef, st);
   }
-  void enqueue_ftilde(const void *f, void *ft, cudaStream_t st) override {
+  void enqueue_ftilde(const void *f, void *ft, cudaStream_t st, int64_t) override {
     if (DIM == 2)
       launch2_ftilde<T>(D2<const T>{(const T *)f, pitch}, D2<T>{(T *)ft, pitch}, M[0], st);
     else
       launch3_ftilde<T>(D3<const T>{(const T *)f, pitch, pitch * n}, D3<T>{(T *)ft, pitch, pitch * n}, M[0], st);
   }
-  void enqueue_norm(const void *x, unsigned long long *mx, double *ss, cudaStream_t st) override {
+  void enqueue_norm(const void *x, unsigned long long *mx, double *ss, cudaStream_t st, int64_t) override {
     if (DIM == 2)
       launch2_norm<T>(D2<const T>{(const T *)x, pitch}, M[0], mx, ss, st);
     else

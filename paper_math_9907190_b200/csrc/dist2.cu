@@ -299,7 +299,7 @@ struct Dist2 : ImplBase {
     return comm->allreduce_max_u64(d, nslots, st);
   }
   // f~ (order 4) on the slab: f's ghost row first, then the own rows
-  void enqueue_ftilde(const void *f, void *ft, cudaStream_t st) override {
+  void enqueue_ftilde(const void *f, void *ft, cudaStream_t st, int64_t) override {
     if (loop) {
       launch2_ftilde<T>(D2<const T>{(const T *)f, pitch}, D2<T>{(T *)ft, pitch}, M[0], st);
       return;
@@ -308,7 +308,7 @@ struct Dist2 : ImplBase {
     xchg(0, false, 1, st, [&](int) { return fv; }, pitch);
     launch2_ftilde_rows<T>(D2<const T>{fv, pitch}, D2<T>{vg((T *)ft), pitch}, M[0], lo(0, rk[0].q), hi(0, rk[0].q), st);
   }
-  void enqueue_residual(const void *u, const void *f, void *r, cudaStream_t st) override {
+  void enqueue_residual(const void *u, const void *f, void *r, cudaStream_t st, int64_t) override {
     if (loop) {
       launch2_residual<T>(D2<const T>{(const T *)u, pitch}, D2<const T>{(const T *)f, pitch}, D2<T>{(T *)r, pitch},
                           M[0], s->cfg.order, coef, st);
@@ -319,7 +319,7 @@ struct Dist2 : ImplBase {
     launch2_residual_rows<T>(D2<const T>{uv, pitch}, D2<const T>{fv, pitch}, D2<T>{vg((T *)r), pitch}, M[0],
                              s->cfg.order, coef, lo(0, rk[0].q), hi(0, rk[0].q), st);
   }
-  void enqueue_norm(const void *x, unsigned long long *mx, double *ss, cudaStream_t st) override {
+  void enqueue_norm(const void *x, unsigned long long *mx, double *ss, cudaStream_t st, int64_t) override {
     if (loop) {
       launch2_norm<T>(D2<const T>{(const T *)x, pitch}, M[0], mx, ss, st);
       return;

@@ -352,7 +352,7 @@ struct Dist3 : ImplBase {
   cudaError_t reduce_hist(unsigned long long *d, int nslots, cudaStream_t st) override {
     return comm->allreduce_max_u64(d, nslots, st);
   }
-  void enqueue_ftilde(const void *f, void *ft, cudaStream_t st) override {
+  void enqueue_ftilde(const void *f, void *ft, cudaStream_t st, int64_t) override {
     if (loop) {
       launch3_ftilde<T>(D3<const T>{(const T *)f, pitch, fplane()}, D3<T>{(T *)ft, pitch, fplane()}, M[0], st);
       return;
@@ -361,7 +361,7 @@ struct Dist3 : ImplBase {
     xchg(0, false, 1, st, [&](int) { return fvp; }, fplane());
     launch3_ftilde<T>(cfv(f), fv(ft), M[0], st, lo(0, rk[0].q), hi(0, rk[0].q));
   }
-  void enqueue_residual(const void *u, const void *f, void *r, cudaStream_t st) override {
+  void enqueue_residual(const void *u, const void *f, void *r, cudaStream_t st, int64_t) override {
     if (loop) {
       launch3_residual<T>(D3<const T>{(const T *)u, pitch, fplane()}, D3<const T>{(const T *)f, pitch, fplane()},
                           D3<T>{(T *)r, pitch, fplane()}, M[0], s->cfg.order, coef, st);
@@ -371,7 +371,7 @@ struct Dist3 : ImplBase {
     xchg(0, false, 1, st, [&](int) { return uvp; }, fplane());
     launch3_residual<T>(cfv(u), cfv(f), fv(r), M[0], s->cfg.order, coef, st, lo(0, rk[0].q), hi(0, rk[0].q));
   }
-  void enqueue_norm(const void *x, unsigned long long *mx, double *ss, cudaStream_t st) override {
+  void enqueue_norm(const void *x, unsigned long long *mx, double *ss, cudaStream_t st, int64_t) override {
     if (loop) {
       launch3_norm<T>(D3<const T>{(const T *)x, pitch, fplane()}, M[0], mx, ss, st);
       return;

@@ -686,6 +686,15 @@ bool launch2_tail(const Lev2<T> *h_lev, int om, int oc, int k, int *counter, cud
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  // a cooperative launch that cannot be co-resident (MPS / green-context SM
+  // limits) would be rejected -- inside a stream capture that invalidates the
+  // capture, so decide on the host first and let the caller run per-level kernels
+  int per_sm = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k2_tail<T>, 512, bytes) != cudaSuccess ||
+      per_sm < 1) {
+    cudaGetLastError();
+    return false;
+  }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(sms);
   cfg.blockDim = dim3(512);

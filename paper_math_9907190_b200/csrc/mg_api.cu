@@ -12,7 +12,8 @@ template <class T>
 struct Impl2 : ImplBase {
   const mg_solver *s;
   int k;
-  int64_t n, pitch;
+  int64_t n, pitch;   // pitch: the work layout of u, f~ in the cycle (mg_solver::wpitch)
+  int64_t cpitch;     // the caller's layout (mg_residual / mg_norm operands)
   // per octave o: D level (o = 0..k-2), A level (o = 1..k-1)
   std::vector<S2<T>> rD, vD;
   std::vector<D2<T>> rA, vA;
@@ -38,7 +39,7 @@ struct Impl2 : ImplBase {
   int ad_min = getenv("MG_AD_MINO") && atoi(getenv("MG_AD_MINO")) >= 1 ? atoi(getenv("MG_AD_MINO")) : 1;
   Lev2<T> *d_lev = nullptr;
   std::vector<Lev2<T>> h_lev;   // host copy of the level descriptors (tail kernel parameters)
-  explicit Impl2(const mg_solver *sv) : s(sv), k(sv->k), n(sv->cfg.n), pitch(sv->pitch) {}
+  explicit Impl2(const mg_solver *sv) : s(sv), k(sv->k), n(sv->cfg.n), pitch(sv->wpitch), cpitch(sv->pitch) {}
   bool fast() const override { return use_fast; }
 
   int64_t pitch_for(int64_t cnt) const { return round_up(cnt, 128 / (int64_t)sizeof(T)); }
@@ -286,15 +287,15 @@ struct Impl2 : ImplBase {
     D2<const T> uc{(const T *)u, pitch}, fc{(const T *)f_eff, pitch};
     launch2_desc_fine<T>(uc, fc, rD[0], M[0], s->cfg.order, coef, sink(), st);
   }
-  void enqueue_residual(const void *u, const void *f, void *r, cudaStream_t st) override {
-    launch2_residual<T>(D2<const T>{(const T *)u, pitch}, D2<const T>{(const T *)f, pitch}, D2<T>{(T *)r, pitch},
+  void enqueue_residual(const void *u, const void *f, void *r, cudaStream_t st, int64_t fp) override {
+    launch2_residual<T>(D2<const T>{(const T *)u, cpitch}, D2<const T>{(const T *)f, fp}, D2<T>{(T *)r, cpitch},
                         M[0], s->cfg.order, coef, st);
   }
-  void enqueue_ftilde(const void *f, void *ft, cudaStream_t st) override {
-    launch2_ftilde<T>(D2<const T>{(const T *)f, pitch}, D2<T>{(T *)ft, pitch}, M[0], st);
+  void enqueue_ftilde(const void *f, void *ft, cudaStream_t st, int64_t ftp) override {
+    launch2_ftilde<T>(D2<const T>{(const T *)f, cpitch}, D2<T>{(T *)ft, ftp}, M[0], st);
   }
-  void enqueue_norm(const void *x, unsigned long long *mx, double *ss, cudaStream_t st) override {
-    launch2_norm<T>(D2<const T>{(const T *)x, pitch}, M[0], mx, ss, st);
+  void enqueue_norm(const void *x, unsigned long long *mx, double *ss, cudaStream_t st, int64_t xp) override {
+    launch2_norm<T>(D2<const T>{(const T *)x, xp}, M[0], mx, ss, st);
   }
   int launches_per_cycle() const override {
     if (use_fast) {
@@ -350,7 +351,8 @@ template <class T>
 struct Impl3 : ImplBase {
   const mg_solver *s;
   int k;
-  int64_t n, pitch;
+  int64_t n, pitch;   // the work layout (mg_solver::wpitch)
+  int64_t cpitch;     // the caller's layout (mg_residual / mg_norm operands)
   std::vector<S3<T>> rR, vR, rM, vM;   // octave 0..k-2
   std::vector<D3<T>> rG, vG;           // octave 1..k-1
   std::vector<int> M;
@@ -363,7 +365,7 @@ struct Impl3 : ImplBase {
   bool use_tail = false;
   Lev3<T> *d_lev = nullptr;
   std::vector<Lev3<T>> h_lev;   // host copy of the level descriptors (tail kernel parameters)
-  explicit Impl3(const mg_solver *sv) : s(sv), k(sv->k), n(sv->cfg.n), pitch(sv->pitch) {}
+  explicit Impl3(const mg_solver *sv) : s(sv), k(sv->k), n(sv->cfg.n), pitch(sv->wpitch), cpitch(sv->pitch) {}
   bool fast() const override { return use_fast; }
   int64_t pitch_for(int64_t cnt) const { return round_up(cnt, 128 / (int64_t)sizeof(T)); }
 
@@ -649,14 +651,15 @@ struct Impl3 : ImplBase {
     zp_next_rev() = 0;
   }
   void enqueue_final_norm(void *u, const void *f_eff, cudaStream_t st) override { desc_fine(u, f_eff, st); }
-  void enqueue_residual(const void *u, const void *f, void *r, cudaStream_t st) override {
-    launch3_residual<T>(cfield(u), cfield(f), field(r), M[0], s->cfg.order, coef, st);
+  void enqueue_residual(const void *u, const void *f, void *r, cudaStream_t st, int64_t fp) override {
+    launch3_residual<T>(D3<const T>{(const T *)u, cpitch, cpitch * n}, D3<const T>{(const T *)f, fp, fp * n},
+                        D3<T>{(T *)r, cpitch, cpitch * n}, M[0], s->cfg.order, coef, st);
   }
-  void enqueue_ftilde(const void *f, void *ft, cudaStream_t st) override {
-    launch3_ftilde<T>(cfield(f), field(ft), M[0], st);
+  void enqueue_ftilde(const void *f, void *ft, cudaStream_t st, int64_t ftp) override {
+    launch3_ftilde<T>(D3<const T>{(const T *)f, cpitch, cpitch * n}, D3<T>{(T *)ft, ftp, ftp * n}, M[0], st);
   }
-  void enqueue_norm(const void *x, unsigned long long *mx, double *ss, cudaStream_t st) override {
-    launch3_norm<T>(cfield(x), M[0], mx, ss, st);
+  void enqueue_norm(const void *x, unsigned long long *mx, double *ss, cudaStream_t st, int64_t xp) override {
+    launch3_norm<T>(D3<const T>{(const T *)x, xp, xp * n}, M[0], mx, ss, st);
   }
   int launches_per_cycle() const override {
     int c = 1;
@@ -796,6 +799,15 @@ int mg_create_ex(const mg_config *cfg, mg_solver **out) {
   s->esz = (cfg->dtype == MG_F64) ? 8 : 4;
   s->pitch = cfg->pitch ? cfg->pitch : cfg->n;
   s->cfg.pitch = s->pitch;
+  {
+    // the work layout: the caller's when its rows are 16-byte multiples, else
+    // n rounded up to 128 bytes for the solvers that run the TMA kernels
+    // (single GPU, diagonal scheme, one sweep); the others read any pitch
+    const bool tma = cfg->nranks <= 1 && !(cfg->flags & MG_FLAG_CONVENTIONAL) && cfg->sweeps <= 1 &&
+                     !env_flag("MG_FORCE_REF");
+    const int64_t q = 128 / s->esz;
+    s->wpitch = ((s->pitch * s->esz) % 16 == 0 || !tma) ? s->pitch : round_up(cfg->n, q);
+  }
   if (cfg->nranks == 0) s->cfg.nranks = 1;
   if (cfg->device >= 0) {
     if (cfg->device >= ndev) return MG_EINVAL;
@@ -847,8 +859,8 @@ int mg_create_ex(const mg_config *cfg, mg_solver **out) {
   }
   for (int l = 0; l < s->L; l++) s->impl->Nl.push_back((double)mg_level_points(sp, l));
   if (cfg->order == 4) {
-    CKS(sp, cudaMalloc(&s->d_ft, s->field_elems() * s->esz));
-    CKS(sp, cudaMemset(s->d_ft, 0, s->field_elems() * s->esz));
+    CKS(sp, cudaMalloc(&s->d_ft, s->work_elems() * s->esz));
+    CKS(sp, cudaMemset(s->d_ft, 0, s->work_elems() * s->esz));
   }
   CKS(sp, cudaDeviceSynchronize());
   *out = s.release();
@@ -924,36 +936,57 @@ int64_t mg_level_points(const mg_solver *s, int lev) {
 
 int mg_launches_per_cycle(const mg_solver *s) { return s ? s->impl->launches_per_cycle() : MG_EINVAL; }
 
+// ---------------------------------------------------------- staging
+// The cycle kernels read u and f (or f~) in the work layout: row pitch
+// s->wpitch (16-byte rows), 16-byte aligned base.  A caller whose layout is
+// that already is read in place; otherwise (pitch = n with n = 2^k+1 never
+// gives 16-byte rows; an offset base pointer) each call copies u and f into
+// the library's work arrays (one 2D copy each), runs the cycles there and
+// copies u back -- the TMA kernels run either way.
+static bool work_layout(const mg_solver *s, const void *a) { return s->wpitch == s->pitch && aligned16(a); }
+
+static int ensure_stage(mg_solver *s) {
+  if (s->d_u_stage) return MG_OK;
+  const size_t bytes = s->work_elems() * s->esz;
+  CKS(s, cudaMalloc(&s->d_u_stage, bytes));
+  CKS(s, cudaMalloc(&s->d_f_stage, bytes));
+  CKS(s, cudaMemsetAsync(s->d_u_stage, 0, bytes, s->st));   // padding columns stay zero
+  CKS(s, cudaMemsetAsync(s->d_f_stage, 0, bytes, s->st));
+  return MG_OK;
+}
+
+// rows x n elements between two layouts (pitches in elements)
+static cudaError_t copy_field(mg_solver *s, void *dst, int64_t dp, const void *src, int64_t sp, cudaMemcpyKind kind) {
+  return cudaMemcpy2DAsync(dst, dp * s->esz, src, sp * s->esz, s->cfg.n * s->esz, s->rows(), kind, s->st);
+}
+
 int mg_residual(mg_solver *s, const void *u, const void *f, void *r) {
   if (!s || !u || !f || !r) return fail(s, MG_EINVAL, "mg_residual: NULL argument");
   DeviceGuard g(s->device);
   int rc = begin(s);
   if (rc) return rc;
-  const void *fe = f;
   if (s->cfg.order == 4) {
-    // r uses f~ formed from f (Efos2/Efos4); reuse the f~ buffer
-    s->impl->enqueue_ftilde(f, s->d_ft, s->st);
-    fe = s->d_ft;
+    // r uses f~ formed from f (Efos2/Efos4), in the f~ buffer (work layout)
+    s->impl->enqueue_ftilde(f, s->d_ft, s->st, s->wpitch);
+    s->impl->enqueue_residual(u, s->d_ft, r, s->st, s->wpitch);
+  } else {
+    s->impl->enqueue_residual(u, f, r, s->st, s->pitch);
   }
-  s->impl->enqueue_residual(u, fe, r, s->st);
   return end(s);
 }
 
-static int vcycle_dev(mg_solver *s, void *u, const void *f, int ncycles, double *res_hist) {
-  const void *fe = f;
-  if (s->cfg.order == 4) {
-    s->impl->enqueue_ftilde(f, s->d_ft, s->st);
-    fe = s->d_ft;
-  }
-  int nslots = ncycles + 1 < kHistCap ? ncycles + 1 : kHistCap;
+// ncycles V-cycles on u_w (work layout, aligned) with the right-hand side
+// f_eff (work layout: f, or f~ for order 4).
+static int cycles_work(mg_solver *s, void *u, const void *fe, int ncycles, double *res_hist) {
+  const int nslots = ncycles + 1;   // <= kHistCap (checked by the callers)
   CKS(s, cudaMemsetAsync(s->d_hist, 0, sizeof(unsigned long long) * nslots, s->st));
   CKS(s, cudaMemsetAsync(s->d_counter, 0, sizeof(int), s->st));
-  // TMA path: u alternates between the caller's array and an internal
-  // partner (the ascent reads the old u in a 2-node halo, so it cannot update
-  // in place); an odd cycle count ends with one copy back.
-  bool alt = s->impl->fast() && aligned16(u) && aligned16(fe);
+  // TMA path: u alternates between u and an internal partner (the ascent
+  // reads the old u in a 2-node halo, so it cannot update in place); an odd
+  // cycle count ends with one copy back.
+  const bool alt = s->impl->fast();
   if (alt && !s->d_ualt) {
-    size_t bytes = s->field_elems() * s->esz;
+    size_t bytes = s->work_elems() * s->esz;
     CKS(s, cudaMalloc(&s->d_ualt, bytes));
     CKS(s, cudaMemsetAsync(s->d_ualt, 0, bytes, s->st));
   }
@@ -971,7 +1004,7 @@ static int vcycle_dev(mg_solver *s, void *u, const void *f, int ncycles, double 
     if (rc) return rc;
     cur = dst;
   }
-  if (cur != u) CKS(s, cudaMemcpyAsync(u, cur, s->field_elems() * s->esz, cudaMemcpyDeviceToDevice, s->st));
+  if (cur != u) CKS(s, cudaMemcpyAsync(u, cur, s->work_elems() * s->esz, cudaMemcpyDeviceToDevice, s->st));
   if (res_hist) {
     if (!xf || ncycles == 0) s->impl->enqueue_final_norm(u, fe, s->st);
     CKS(s, s->impl->reduce_hist(s->d_hist, nslots, s->st));
@@ -980,7 +1013,7 @@ static int vcycle_dev(mg_solver *s, void *u, const void *f, int ncycles, double 
     bool finite = true;
     for (int i = 0; i <= ncycles; i++) {
       double v;
-      unsigned long long b = s->h_hist[i < kHistCap ? i : kHistCap - 1];
+      unsigned long long b = s->h_hist[i];
       std::memcpy(&v, &b, sizeof v);
       res_hist[i] = v;
       if (!std::isfinite(v)) finite = false;
@@ -990,10 +1023,43 @@ static int vcycle_dev(mg_solver *s, void *u, const void *f, int ncycles, double 
   return MG_OK;
 }
 
+// f_eff in the work layout from the caller's f (device, caller layout)
+static int rhs_work(mg_solver *s, const void *f, const void **fe) {
+  if (s->cfg.order == 4) {
+    s->impl->enqueue_ftilde(f, s->d_ft, s->st, s->wpitch);   // reads f in the caller's layout
+    *fe = s->d_ft;
+    return MG_OK;
+  }
+  if (work_layout(s, f)) {
+    *fe = f;
+    return MG_OK;
+  }
+  int rc = ensure_stage(s);
+  if (rc) return rc;
+  CKS(s, copy_field(s, s->d_f_stage, s->wpitch, f, s->pitch, cudaMemcpyDeviceToDevice));
+  *fe = s->d_f_stage;
+  return MG_OK;
+}
+
+static int vcycle_dev(mg_solver *s, void *u, const void *f, int ncycles, double *res_hist) {
+  const void *fe = nullptr;
+  int rc = rhs_work(s, f, &fe);
+  if (rc) return rc;
+  if (work_layout(s, u)) return cycles_work(s, u, fe, ncycles, res_hist);
+  rc = ensure_stage(s);
+  if (rc) return rc;
+  CKS(s, copy_field(s, s->d_u_stage, s->wpitch, u, s->pitch, cudaMemcpyDeviceToDevice));
+  rc = cycles_work(s, s->d_u_stage, fe, ncycles, res_hist);
+  if (rc) return rc;
+  CKS(s, copy_field(s, u, s->pitch, s->d_u_stage, s->wpitch, cudaMemcpyDeviceToDevice));
+  return MG_OK;
+}
+
 int mg_vcycle(mg_solver *s, void *u, const void *f, int ncycles, double *res_hist) {
   if (!s) return MG_EINVAL;
   if (!u || !f) return fail(s, MG_EINVAL, "mg_vcycle: NULL u or f");
   if (ncycles < 0) return fail(s, MG_EINVAL, "mg_vcycle: ncycles < 0");
+  if (res_hist && ncycles + 1 > kHistCap) return fail(s, MG_EINVAL, "mg_vcycle: res_hist needs ncycles < 4096");
   if (ncycles == 0 && !res_hist) return MG_OK;
   DeviceGuard g(s->device);
   int rc = begin(s);
@@ -1008,25 +1074,37 @@ int mg_vcycle(mg_solver *s, void *u, const void *f, int ncycles, double *res_his
   return rc ? rc : rc2;
 }
 
+// Host arrays (caller layout) are copied straight into the work layout.
 int mg_vcycle_host(mg_solver *s, void *u_host, const void *f_host, int ncycles, double *res_hist) {
   if (!s) return MG_EINVAL;
   if (!u_host || !f_host) return fail(s, MG_EINVAL, "mg_vcycle_host: NULL u or f");
   if (ncycles < 0) return fail(s, MG_EINVAL, "mg_vcycle_host: ncycles < 0");
+  if (res_hist && ncycles + 1 > kHistCap) return fail(s, MG_EINVAL, "mg_vcycle_host: res_hist needs ncycles < 4096");
   DeviceGuard g(s->device);
-  size_t bytes = s->field_elems() * s->esz;
-  if (!s->d_u_stage) {
-    CKS(s, cudaMalloc(&s->d_u_stage, bytes));
-    CKS(s, cudaMalloc(&s->d_f_stage, bytes));
-  }
   int rc = begin(s);
   if (rc) return rc;
-  CKS(s, cudaMemcpyAsync(s->d_u_stage, u_host, bytes, cudaMemcpyHostToDevice, s->st));
-  CKS(s, cudaMemcpyAsync(s->d_f_stage, f_host, bytes, cudaMemcpyHostToDevice, s->st));
-  rc = vcycle_dev(s, s->d_u_stage, s->d_f_stage, ncycles, res_hist);
-  if (rc) return rc;
-  CKS(s, cudaMemcpyAsync(u_host, s->d_u_stage, bytes, cudaMemcpyDeviceToHost, s->st));
-  CKS(s, cudaStreamSynchronize(s->st));
-  return end(s);
+  rc = ensure_stage(s);
+  if (!rc) rc = [&]() -> int {
+    CKS(s, copy_field(s, s->d_u_stage, s->wpitch, u_host, s->pitch, cudaMemcpyHostToDevice));
+    const void *fe = s->d_f_stage;
+    if (s->cfg.order == 4) {
+      // f~ is formed on the device from f in the caller's layout (d_f_stage is large enough)
+      CKS(s, cudaMemcpyAsync(s->d_f_stage, f_host, s->field_elems() * s->esz, cudaMemcpyHostToDevice, s->st));
+      s->impl->enqueue_ftilde(s->d_f_stage, s->d_ft, s->st, s->wpitch);
+      fe = s->d_ft;
+    } else {
+      CKS(s, copy_field(s, s->d_f_stage, s->wpitch, f_host, s->pitch, cudaMemcpyHostToDevice));
+    }
+    // (loopback slabs take the raw f: one layout there, so d_f_stage holds it as given)
+    int r = s->impl->vcycle_all(s, s->d_u_stage, s->d_f_stage, ncycles, res_hist);
+    if (r == 1) r = cycles_work(s, s->d_u_stage, fe, ncycles, res_hist);
+    if (r) return r;
+    CKS(s, copy_field(s, u_host, s->pitch, s->d_u_stage, s->wpitch, cudaMemcpyDeviceToHost));
+    CKS(s, cudaStreamSynchronize(s->st));
+    return MG_OK;
+  }();
+  int rc2 = end(s);   // joins the caller's stream on every path
+  return rc ? rc : rc2;
 }
 
 // ---------------------------------------------------- convergence factor
@@ -1035,60 +1113,70 @@ int mg_vcycle_host(mg_solver *s, void *u_host, const void *f_host, int ncycles, 
 // fusion: e is rescaled between cycles), ss = sum e'^2 over the interior
 // (the norm kernel), then k_rate_scale: ratio_k = sqrt(ss) / prev, e = e' /
 // sqrt(ss), prev = 1.
-int mg_convergence_factor(mg_solver *s, void *e, int iters, double *rho, double *ratios) {
+int mg_convergence_factor(mg_solver *s, void *e_user, int iters, double *rho, double *ratios) {
   if (!s) return MG_EINVAL;
-  if (!e || iters < 2 || !rho) return fail(s, MG_EINVAL, "mg_convergence_factor: bad argument");
+  if (!e_user || iters < 2 || !rho) return fail(s, MG_EINVAL, "mg_convergence_factor: bad argument");
   if (s->cfg.nranks > 1) return fail(s, MG_EUNSUPPORTED, "mg_convergence_factor: single GPU only");
   DeviceGuard g(s->device);
   int rc = begin(s);
   if (rc) return rc;
-  const size_t ne = s->field_elems(), bytes = ne * s->esz;
-  if (!s->d_zero) {
-    CKS(s, cudaMalloc(&s->d_zero, bytes));
-    CKS(s, cudaMemsetAsync(s->d_zero, 0, bytes, s->st));
-  }
-  const bool alt = s->impl->fast() && aligned16(e);
-  if (alt && !s->d_ualt) {
-    CKS(s, cudaMalloc(&s->d_ualt, bytes));
-    CKS(s, cudaMemsetAsync(s->d_ualt, 0, bytes, s->st));
-  }
   double *d_rate = nullptr;   // [0] prev, [1] 1/norm, [2 ..] ratios
-  CKS(s, cudaMalloc(&d_rate, sizeof(double) * (iters + 3)));
-  const double one = 1.0;
-  // normalise the start vector first (ratio 0 of the history is its norm)
-  CKS(s, cudaMemcpyAsync(d_rate, &one, sizeof one, cudaMemcpyHostToDevice, s->st));
-  CKS(s, cudaMemsetAsync(s->d_mx, 0, sizeof(unsigned long long), s->st));
-  CKS(s, cudaMemsetAsync(s->d_ss, 0, sizeof(double), s->st));
-  s->impl->enqueue_norm(e, s->d_mx, s->d_ss, s->st);
-  k_rate_norm<<<1, 1, 0, s->st>>>(s->d_ss, d_rate + 2, 0, d_rate, d_rate + 1);
-  const int nb = 148 * 8;
-  if (s->esz == 8)
-    k_rate_scale<double><<<nb, 256, 0, s->st>>>((const double *)e, (double *)e, ne, d_rate + 1);
-  else
-    k_rate_scale<float><<<nb, 256, 0, s->st>>>((const float *)e, (float *)e, ne, d_rate + 1);
-  CKS(s, cudaMemsetAsync(s->d_counter, 0, sizeof(int), s->st));
-  for (int it = 1; it <= iters; it++) {
-    void *dst = alt ? s->d_ualt : e;
-    rc = run_cycle(s, e, dst, s->d_zero, 0);
-    if (rc) {
-      cudaFree(d_rate);
-      return rc;
+  std::vector<double> h(iters + 1);
+  rc = [&]() -> int {
+    // the iteration runs on e in the work layout (staged when the caller's is another)
+    void *e = e_user;
+    const bool staged = !work_layout(s, e_user);
+    if (staged) {
+      int r = ensure_stage(s);
+      if (r) return r;
+      e = s->d_u_stage;
+      CKS(s, copy_field(s, e, s->wpitch, e_user, s->pitch, cudaMemcpyDeviceToDevice));
     }
+    const size_t ne = s->work_elems(), bytes = ne * s->esz;
+    if (!s->d_zero) {
+      CKS(s, cudaMalloc(&s->d_zero, bytes));
+      CKS(s, cudaMemsetAsync(s->d_zero, 0, bytes, s->st));
+    }
+    const bool alt = s->impl->fast();
+    if (alt && !s->d_ualt) {
+      CKS(s, cudaMalloc(&s->d_ualt, bytes));
+      CKS(s, cudaMemsetAsync(s->d_ualt, 0, bytes, s->st));
+    }
+    CKS(s, cudaMalloc(&d_rate, sizeof(double) * (iters + 3)));
+    const double one = 1.0;
+    // normalise the start vector first (ratio 0 of the history is its norm)
+    CKS(s, cudaMemcpyAsync(d_rate, &one, sizeof one, cudaMemcpyHostToDevice, s->st));
     CKS(s, cudaMemsetAsync(s->d_mx, 0, sizeof(unsigned long long), s->st));
     CKS(s, cudaMemsetAsync(s->d_ss, 0, sizeof(double), s->st));
-    s->impl->enqueue_norm(dst, s->d_mx, s->d_ss, s->st);
-    k_rate_norm<<<1, 1, 0, s->st>>>(s->d_ss, d_rate + 2, it, d_rate, d_rate + 1);
+    s->impl->enqueue_norm(e, s->d_mx, s->d_ss, s->st, s->wpitch);
+    k_rate_norm<<<1, 1, 0, s->st>>>(s->d_ss, d_rate + 2, 0, d_rate, d_rate + 1);
+    const int nb = 148 * 8;
     if (s->esz == 8)
-      k_rate_scale<double><<<nb, 256, 0, s->st>>>((const double *)dst, (double *)e, ne, d_rate + 1);
+      k_rate_scale<double><<<nb, 256, 0, s->st>>>((const double *)e, (double *)e, ne, d_rate + 1);
     else
-      k_rate_scale<float><<<nb, 256, 0, s->st>>>((const float *)dst, (float *)e, ne, d_rate + 1);
-  }
-  std::vector<double> h(iters + 1);
-  CKS(s, cudaMemcpyAsync(h.data(), d_rate + 2, sizeof(double) * (iters + 1), cudaMemcpyDeviceToHost, s->st));
-  CKS(s, cudaStreamSynchronize(s->st));
-  cudaFree(d_rate);
-  rc = end(s);
-  if (rc) return rc;
+      k_rate_scale<float><<<nb, 256, 0, s->st>>>((const float *)e, (float *)e, ne, d_rate + 1);
+    CKS(s, cudaMemsetAsync(s->d_counter, 0, sizeof(int), s->st));
+    for (int it = 1; it <= iters; it++) {
+      void *dst = alt ? s->d_ualt : e;
+      int r = run_cycle(s, e, dst, s->d_zero, 0);
+      if (r) return r;
+      CKS(s, cudaMemsetAsync(s->d_mx, 0, sizeof(unsigned long long), s->st));
+      CKS(s, cudaMemsetAsync(s->d_ss, 0, sizeof(double), s->st));
+      s->impl->enqueue_norm(dst, s->d_mx, s->d_ss, s->st, s->wpitch);
+      k_rate_norm<<<1, 1, 0, s->st>>>(s->d_ss, d_rate + 2, it, d_rate, d_rate + 1);
+      if (s->esz == 8)
+        k_rate_scale<double><<<nb, 256, 0, s->st>>>((const double *)dst, (double *)e, ne, d_rate + 1);
+      else
+        k_rate_scale<float><<<nb, 256, 0, s->st>>>((const float *)dst, (float *)e, ne, d_rate + 1);
+    }
+    if (staged) CKS(s, copy_field(s, e_user, s->pitch, e, s->wpitch, cudaMemcpyDeviceToDevice));
+    CKS(s, cudaMemcpyAsync(h.data(), d_rate + 2, sizeof(double) * (iters + 1), cudaMemcpyDeviceToHost, s->st));
+    CKS(s, cudaStreamSynchronize(s->st));
+    return MG_OK;
+  }();
+  if (d_rate) cudaFree(d_rate);
+  int rc2 = end(s);
+  if (rc || rc2) return rc ? rc : rc2;
   // geometric mean of the ratios of the second half of the iterations
   double lg = 0.0;
   int m = 0;
@@ -1106,16 +1194,19 @@ int mg_norm(mg_solver *s, const void *x, int kind, double *out) {
   DeviceGuard g(s->device);
   int rc = begin(s);
   if (rc) return rc;
-  CKS(s, cudaMemsetAsync(s->d_mx, 0, sizeof(unsigned long long), s->st));
-  CKS(s, cudaMemsetAsync(s->d_ss, 0, sizeof(double), s->st));
-  s->impl->enqueue_norm(x, s->d_mx, s->d_ss, s->st);
   unsigned long long mx = 0;
   double ss = 0;
-  CKS(s, cudaMemcpyAsync(&mx, s->d_mx, sizeof mx, cudaMemcpyDeviceToHost, s->st));
-  CKS(s, cudaMemcpyAsync(&ss, s->d_ss, sizeof ss, cudaMemcpyDeviceToHost, s->st));
-  CKS(s, cudaStreamSynchronize(s->st));
-  rc = end(s);
-  if (rc) return rc;
+  rc = [&]() -> int {
+    CKS(s, cudaMemsetAsync(s->d_mx, 0, sizeof(unsigned long long), s->st));
+    CKS(s, cudaMemsetAsync(s->d_ss, 0, sizeof(double), s->st));
+    s->impl->enqueue_norm(x, s->d_mx, s->d_ss, s->st, s->pitch);
+    CKS(s, cudaMemcpyAsync(&mx, s->d_mx, sizeof mx, cudaMemcpyDeviceToHost, s->st));
+    CKS(s, cudaMemcpyAsync(&ss, s->d_ss, sizeof ss, cudaMemcpyDeviceToHost, s->st));
+    CKS(s, cudaStreamSynchronize(s->st));
+    return MG_OK;
+  }();
+  int rc2 = end(s);
+  if (rc || rc2) return rc ? rc : rc2;
   if (kind == MG_NORM_INF) {
     std::memcpy(out, &mx, sizeof(double));
   } else {
@@ -1126,50 +1217,64 @@ int mg_norm(mg_solver *s, const void *x, int kind, double *out) {
   return MG_OK;
 }
 
-int mg_profile(mg_solver *s, void *u, const void *f, int ncycles, mg_step_stat *out, int cap) {
+int mg_profile(mg_solver *s, void *u_user, const void *f, int ncycles, mg_step_stat *out, int cap) {
   if (!s) return MG_EINVAL;
-  if (!u || !f || ncycles < 1 || cap < 0 || (cap > 0 && !out)) return fail(s, MG_EINVAL, "mg_profile: bad argument");
+  if (!u_user || !f || ncycles < 1 || cap < 0 || (cap > 0 && !out)) return fail(s, MG_EINVAL, "mg_profile: bad argument");
   DeviceGuard g(s->device);
   int rc = begin(s);
   if (rc) return rc;
-  const void *fe = f;
-  if (s->cfg.order == 4) {
-    s->impl->enqueue_ftilde(f, s->d_ft, s->st);
-    fe = s->d_ft;
-  }
-  CKS(s, cudaMemsetAsync(s->d_counter, 0, sizeof(int), s->st));
   Prof prof;
   prof.st = s->st;
-  bool alt = s->impl->fast() && aligned16(u) && aligned16(fe);
-  if (alt && !s->d_ualt) {
-    size_t bytes = s->field_elems() * s->esz;
-    CKS(s, cudaMalloc(&s->d_ualt, bytes));
-    CKS(s, cudaMemsetAsync(s->d_ualt, 0, bytes, s->st));
-  }
-  // with cross-cycle fusion every profiled cycle is a steady-state one: the
-  // descent of the first runs unprofiled before the loop
-  const bool xf = alt && s->impl->fuses_cycles();
-  const int mode = xf ? ImplBase::kSkipDesc | ImplBase::kFuseNext : 0;
-  if (xf) s->impl->enqueue_final_norm(u, fe, s->st);
-  void *cur = u;
-  for (int c = 0; c < ncycles; c++) {
-    void *dst = alt ? (cur == u ? s->d_ualt : u) : u;
-    s->impl->enqueue_cycle_mode(cur, dst, fe, s->st, &prof, mode);
-    prof.end_cycle();
-    cur = dst;
-  }
-  if (cur != u) CKS(s, cudaMemcpyAsync(u, cur, s->field_elems() * s->esz, cudaMemcpyDeviceToDevice, s->st));
-  CKS(s, cudaGetLastError());
-  CKS(s, take_launch_error());
-  CKS(s, cudaStreamSynchronize(s->st));
-  size_t ns = prof.steps.size();
-  std::vector<double> acc(ns, 0.0);
-  for (int c = 0; c < ncycles; c++)
-    for (size_t i = 0; i < ns; i++) {
-      float ms = 0;
-      CKS(s, cudaEventElapsedTime(&ms, prof.evs[c * (ns + 1) + i], prof.evs[c * (ns + 1) + i + 1]));
-      acc[i] += ms;
+  std::vector<double> acc;
+  rc = [&]() -> int {
+    const void *fe = nullptr;
+    int r = rhs_work(s, f, &fe);
+    if (r) return r;
+    void *u = u_user;
+    const bool staged = !work_layout(s, u_user);
+    if (staged) {
+      r = ensure_stage(s);
+      if (r) return r;
+      u = s->d_u_stage;
+      CKS(s, copy_field(s, u, s->wpitch, u_user, s->pitch, cudaMemcpyDeviceToDevice));
     }
+    CKS(s, cudaMemsetAsync(s->d_counter, 0, sizeof(int), s->st));
+    const bool alt = s->impl->fast();
+    if (alt && !s->d_ualt) {
+      size_t bytes = s->work_elems() * s->esz;
+      CKS(s, cudaMalloc(&s->d_ualt, bytes));
+      CKS(s, cudaMemsetAsync(s->d_ualt, 0, bytes, s->st));
+    }
+    // with cross-cycle fusion every profiled cycle is a steady-state one: the
+    // descent of the first runs unprofiled before the loop
+    const bool xf = alt && s->impl->fuses_cycles();
+    const int mode = xf ? ImplBase::kSkipDesc | ImplBase::kFuseNext : 0;
+    if (xf) s->impl->enqueue_final_norm(u, fe, s->st);
+    void *cur = u;
+    for (int c = 0; c < ncycles; c++) {
+      void *dst = alt ? (cur == u ? s->d_ualt : u) : u;
+      s->impl->enqueue_cycle_mode(cur, dst, fe, s->st, &prof, mode);
+      prof.end_cycle();
+      cur = dst;
+    }
+    if (cur != u) CKS(s, cudaMemcpyAsync(u, cur, s->work_elems() * s->esz, cudaMemcpyDeviceToDevice, s->st));
+    if (staged) CKS(s, copy_field(s, u_user, s->pitch, u, s->wpitch, cudaMemcpyDeviceToDevice));
+    CKS(s, cudaGetLastError());
+    CKS(s, take_launch_error());
+    CKS(s, cudaStreamSynchronize(s->st));
+    size_t ns = prof.steps.size();
+    acc.assign(ns, 0.0);
+    for (int c = 0; c < ncycles; c++)
+      for (size_t i = 0; i < ns; i++) {
+        float ms = 0;
+        CKS(s, cudaEventElapsedTime(&ms, prof.evs[c * (ns + 1) + i], prof.evs[c * (ns + 1) + i + 1]));
+        acc[i] += ms;
+      }
+    return MG_OK;
+  }();
+  int rc2 = end(s);
+  if (rc || rc2) return rc ? rc : rc2;
+  const size_t ns = acc.size();
   for (size_t i = 0; i < ns && (int)i < cap; i++) {
     std::memset(out[i].name, 0, sizeof out[i].name);
     std::strncpy(out[i].name, prof.steps[i].name.c_str(), sizeof out[i].name - 1);
@@ -1178,8 +1283,7 @@ int mg_profile(mg_solver *s, void *u, const void *f, int ncycles, mg_step_stat *
     out[i].ms = acc[i] / ncycles;
     out[i].alg_bytes = prof.steps[i].bytes;
   }
-  rc = end(s);
-  return rc ? rc : (int)ns;
+  return (int)ns;
 }
 
 int mg_slab_plan(int dim, int64_t n, int nranks, int rank, int64_t agglom_points, int64_t *lo, int64_t *hi,

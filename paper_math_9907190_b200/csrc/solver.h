@@ -125,9 +125,13 @@ struct ImplBase {
     enqueue_cycle(u_in, u_out, f_eff, st, prof);
   }
   virtual void enqueue_final_norm(void *u, const void *f_eff, cudaStream_t st) = 0;
-  virtual void enqueue_residual(const void *u, const void *f, void *r, cudaStream_t st) = 0;
-  virtual void enqueue_ftilde(const void *f, void *ft, cudaStream_t st) = 0;
-  virtual void enqueue_norm(const void *x, unsigned long long *mx, double *ss, cudaStream_t st) = 0;
+  // Caller-facing helpers.  u, r (residual) and f (f~) are in the caller's layout
+  // (mg_solver::pitch); the extra pitch is that of the other operand: f of the
+  // residual (the caller's f, or the library's f~ in the work layout), the f~
+  // output, the normed array.  Multi-GPU / conventional solvers have one layout.
+  virtual void enqueue_residual(const void *u, const void *f, void *r, cudaStream_t st, int64_t fpitch) = 0;
+  virtual void enqueue_ftilde(const void *f, void *ft, cudaStream_t st, int64_t ftpitch) = 0;
+  virtual void enqueue_norm(const void *x, unsigned long long *mx, double *ss, cudaStream_t st, int64_t xpitch) = 0;
   virtual int launches_per_cycle() const = 0;
   // ---- multi-GPU hooks (single-GPU defaults)
   // elements of one caller field (u, f, r) as this rank holds it
@@ -159,7 +163,10 @@ struct ImplBase {
 struct mg_solver {
   mg_config cfg{};
   int k = 0, L = 0, esz = 8;
-  int64_t pitch = 0;
+  int64_t pitch = 0;    // row pitch of the caller's arrays (elements)
+  int64_t wpitch = 0;   // row pitch of the work layout the cycle kernels read: = pitch when that is
+                        // 16-byte aligned, else n rounded up to 128 bytes (the caller's arrays are
+                        // then staged through d_u_stage / d_f_stage, one 2D copy per array and call)
   int device = 0;
   cudaStream_t user = nullptr, st = nullptr;
   cudaEvent_t ev_in = nullptr, ev_out = nullptr;
@@ -168,8 +175,8 @@ struct mg_solver {
   int *d_counter = nullptr;
   unsigned long long *d_mx = nullptr;
   double *d_ss = nullptr;
-  void *d_ft = nullptr;                    // order-4 f~ (n^d x pitch)
-  void *d_u_stage = nullptr, *d_f_stage = nullptr;   // mg_vcycle_host staging
+  void *d_ft = nullptr;                    // order-4 f~ (work layout)
+  void *d_u_stage = nullptr, *d_f_stage = nullptr;   // work-layout staging of u, f (host calls, unaligned layouts)
   struct GraphEntry {
     cudaGraphExec_t exec;
     const void *uin, *uout, *f;
@@ -180,10 +187,12 @@ struct mg_solver {
   void *d_zero = nullptr;            // zero right-hand side (mg_convergence_factor)
   unsigned long long *h_hist = nullptr;    // pinned
   std::string err;
-  size_t field_elems() const {
+  size_t field_elems() const {   // one caller field (u, f, r), elements
     size_t le = impl ? impl->local_elems() : 0;
     return le ? le : (size_t)((cfg.dim == 2) ? cfg.n * pitch : cfg.n * cfg.n * pitch);
   }
+  size_t rows() const { return field_elems() / (size_t)pitch; }   // rows of one field (n, n^2, or the slab's)
+  size_t work_elems() const { return rows() * (size_t)wpitch; }
 };
 
 // conv.cu: the paper's "usual" V(0,1) multigrid (MG_FLAG_CONVENTIONAL, NEXT-3)

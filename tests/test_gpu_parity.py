@@ -92,17 +92,24 @@ def test_parity_workloads(name, dtype):
     assert np.array_equal(hg, ho)
 
 
-def test_parity_2d_8193_full_size():
-    """BASELINE configs[2] at full size (fp64 and fp32), 2 cycles compared
-    element by element (the oracle takes seconds per cycle at 67M unknowns)."""
-    f64 = W.workload_rhs("2d_8193")
-    for dtype in (np.float64, np.float32):
-        f = f64.astype(dtype)
-        u0 = np.zeros_like(f)
-        ug, hg = _gpu_run(2, 8193, 2, P2, f, u0, 2, dtype)
-        uo, ho = _oracle_run(2, 8193, 2, P2, f, u0, 2, dtype)
-        assert np.array_equal(ug, uo), _rel(ug, uo)
-        assert np.array_equal(hg, ho)
+@pytest.mark.slow
+@pytest.mark.parametrize("dtype", [np.float64, np.float32], ids=["f64", "f32"])
+def test_parity_2d_8193_full_size(dtype):
+    """BASELINE configs[2] at full size and the north star's 10 V-cycles,
+    compared element by element: once with the residual history (every
+    cycle's last pass is the cross-cycle fused asc_desc) and once without
+    (the bench's exact call: the last cycle ends with the plain asc_fine pass,
+    many tiles per CTA)."""
+    f = W.workload_rhs("2d_8193").astype(dtype)
+    u0 = np.zeros_like(f)
+    uo, ho = _oracle_run(2, 8193, 2, P2, f, u0, 10, dtype)
+    tol = 1e-11 if dtype == np.float64 else 1e-5
+    for hist in (True, False):
+        ug, hg = _gpu_run(2, 8193, 2, P2, f, u0, 10, dtype, hist=hist)
+        assert _rel(ug, uo) <= tol
+        assert np.array_equal(ug, uo), (hist, _rel(ug, uo))
+        if hist:
+            assert np.array_equal(hg, ho)
 
 
 @pytest.mark.parametrize("dtype", [np.float64, np.float32], ids=["f64", "f32"])
@@ -134,13 +141,17 @@ def test_cycle_fusion_call_patterns(order, dtype):
 
 @pytest.mark.slow
 def test_parity_3d_513_full_size():
-    """BASELINE configs[4] at full size, one cycle compared element by element."""
+    """BASELINE configs[4] at full size and the north star's 10 V-cycles,
+    compared element by element, with and without the residual history."""
     f = W.workload_rhs("3d_513")
     u0 = np.zeros_like(f)
-    ug, hg = _gpu_run(3, 513, 2, P3, f, u0, 1, np.float64)
-    uo, ho = _oracle_run(3, 513, 2, P3, f, u0, 1, np.float64)
-    assert np.array_equal(ug, uo), _rel(ug, uo)
-    assert np.array_equal(hg, ho)
+    uo, ho = _oracle_run(3, 513, 2, P3, f, u0, 10, np.float64)
+    for hist in (True, False):
+        ug, hg = _gpu_run(3, 513, 2, P3, f, u0, 10, np.float64, hist=hist)
+        assert _rel(ug, uo) <= 1e-11
+        assert np.array_equal(ug, uo), (hist, _rel(ug, uo))
+        if hist:
+            assert np.array_equal(hg, ho)
 
 
 @pytest.mark.parametrize("dim,n", [(2, 65), (3, 17)])

@@ -622,3 +622,67 @@ def test_order4_residual_is_fourth_order(dim):
     r2 = trunc(ns[0], 2) / trunc(ns[1], 2)
     assert 14 < r4 < 18
     assert 3.5 < r2 < 4.5
+
+
+# ------------------------------------------- order 4: the f~ right-hand side
+
+@pytest.mark.parametrize("dim,n", [(2, 33), (3, 17)])
+def test_ftilde_matches_dst_weight(dim, n):
+    """The order-4 right-hand-side combination f~ = ((8 or 6) f + sum of the
+    axis neighbours of f) / 12 (Efos2 P:311-321, Efos4 P:724-745; reading A11:
+    f's boundary values as stored, here zero): applied spectrally it is the
+    f-weight symbol mu of tests/_exact.py (a library DST-I), not a re-typed
+    stencil."""
+    import scipy.fft as sfft
+    f = W.random_field(dim, n, seed=21)
+    inner = (slice(1, -1),) * dim
+    _, mu = _exact.symbols(dim, n, 4)
+    want = sfft.idstn(sfft.dstn(f[inner], type=1, norm="ortho") * mu, type=1, norm="ortho")
+    got = oracle.ftilde(f)
+    assert np.max(np.abs(got[inner] - want)) < 1e-13 * np.max(np.abs(want))
+
+
+@pytest.mark.parametrize("dim,n,p,cycles", [(2, 33, 1.20, 30), (2, 65, 1.20, 30),
+                                            (3, 17, (0.91, 0.80, 0.70, 1.77), 45)])
+def test_order4_vcycle_fixed_point_is_mehrstellen_solution(dim, n, p, cycles):
+    """The order-4 V-cycle (P:324-334 / P:753-756: the second-order cycle on
+    the compact fourth-order residual r = f~ - L9 u, resp. f~ - L19 u) leaves
+    the exact discrete solution of the Mehrstellen system L u = f~ (DST-I,
+    library routine) fixed, and converges to it from u = 0.  An oracle that
+    fed the raw f (not f~) to its order-4 cycles converges to L u = f instead
+    and fails this by O(h^2) relative."""
+    f = W.random_field(dim, n, seed=22)
+    uex = _exact.exact_solution(f, 4)
+    u = uex.copy()
+    oracle.vcycle(u, f, p, 1, order=4)
+    assert np.max(np.abs(u - uex)) < 1e-13 * np.max(np.abs(uex))
+    u = np.zeros_like(f)
+    hist = oracle.vcycle(u, f, p, cycles, order=4, hist=True)
+    assert np.max(np.abs(u - uex)) < 1e-11 * np.max(np.abs(uex))
+    assert hist[-1] < 1e-9 * hist[0]
+    # the raw-f system's solution (L u = f) is measurably different: the pin has teeth
+    raw = np.zeros_like(f)
+    lam4, _ = _exact.symbols(dim, n, 4)
+    import scipy.fft as sfft
+    inner = (slice(1, -1),) * dim
+    raw[inner] = sfft.idstn(sfft.dstn(f[inner], type=1, norm="ortho") / lam4, type=1, norm="ortho")
+    assert np.max(np.abs(raw - uex)) > 1e-4 * np.max(np.abs(uex))
+
+
+# ------------------------------------------- 3D "mean factor" (P:690)
+
+@pytest.mark.parametrize("p,want,tol", [((1.0, 1.0, 1.0, 1.0), 0.140, 0.012),
+                                        ((1.11, 1.42, 1.08, 0.99), 0.043, 0.004)])
+@pytest.mark.parametrize("seed", [0, 1, 2, 3])
+def test_3d_mean_factor_matches_paper(p, want, tol, seed):
+    """The 3D text quotes a "mean factor of convergence rho-bar ~ 0.140"
+    (Table 2 P:709-712 at p = 1, Table 3 P:786-787 0.043 tuned).
+    Reading A12b: the geometric mean of the per-cycle L-inf
+    residual ratios over cycles 7-12 of the error equation (f = 0) from a
+    random start at 17^3.  This is tighter than the spectral-radius window
+    (+-0.05), which the unstated boundary treatment moves to 0.157."""
+    u = W.random_field(3, 17, seed=seed)
+    hist = oracle.vcycle(u, np.zeros_like(u), p, 12, hist=True)
+    ratios = hist[1:] / hist[:-1]
+    mean = float(np.exp(np.mean(np.log(ratios[6:12]))))
+    assert mean == pytest.approx(want, abs=tol)
