@@ -36,6 +36,8 @@ struct NcclApi {
   ncclResult_t (*AllGather)(const void *, void *, size_t, int, ncclComm_t, cudaStream_t) = nullptr;
   ncclResult_t (*AllReduce)(const void *, void *, size_t, int, int, ncclComm_t, cudaStream_t) = nullptr;
   const char *(*GetErrorString)(ncclResult_t) = nullptr;
+  ncclResult_t (*CommGetAsyncError)(ncclComm_t, ncclResult_t *) = nullptr;   // optional
+  ncclResult_t (*CommAbort)(ncclComm_t) = nullptr;                             // optional
   bool load() {
     if (ok) return true;
     const char *names[] = {getenv("MG_NCCL_LIB"), "libnccl.so.2", "libnccl.so"};
@@ -63,6 +65,8 @@ struct NcclApi {
     SYM(AllReduce, "ncclAllReduce");
     SYM(GetErrorString, "ncclGetErrorString");
 #undef SYM
+    CommGetAsyncError = reinterpret_cast<decltype(CommGetAsyncError)>(dlsym(h, "ncclCommGetAsyncError"));
+    CommAbort = reinterpret_cast<decltype(CommAbort)>(dlsym(h, "ncclCommAbort"));
     ok = true;
     return true;
   }
@@ -134,16 +138,18 @@ struct NcclComm : Comm2 {
     const int esz = dtype == ncclFloat64 ? 8 : 4;
     const size_t cnt = g * pb / esz;
     char *a = p[0];
-    nccl().GroupStart();
+    if (!comm) return check(3 /* ncclInternalError */, "halo exchange on an aborted communicator");
+    ncclResult_t r = nccl().GroupStart();
     if (q > 0) {
-      nccl().Send(a + (int64_t)lo[0] * pb, cnt, dtype, q - 1, comm, st);
-      nccl().Recv(a + (int64_t)(lo[0] - g) * pb, cnt, dtype, q - 1, comm, st);
+      if (!r) r = nccl().Send(a + (int64_t)lo[0] * pb, cnt, dtype, q - 1, comm, st);
+      if (!r) r = nccl().Recv(a + (int64_t)(lo[0] - g) * pb, cnt, dtype, q - 1, comm, st);
     }
     if (q + 1 < P) {
-      nccl().Send(a + (int64_t)(hi[0] - g) * pb, cnt, dtype, q + 1, comm, st);
-      nccl().Recv(a + (int64_t)hi[0] * pb, cnt, dtype, q + 1, comm, st);
+      if (!r) r = nccl().Send(a + (int64_t)(hi[0] - g) * pb, cnt, dtype, q + 1, comm, st);
+      if (!r) r = nccl().Recv(a + (int64_t)hi[0] * pb, cnt, dtype, q + 1, comm, st);
     }
-    return check(nccl().GroupEnd(), "halo exchange");
+    ncclResult_t r2 = nccl().GroupEnd();
+    return check(r ? r : r2, "halo exchange");
   }
   cudaError_t allgather(char *full, size_t pb, int lo, int rows, int esz, cudaStream_t st) override {
     const size_t cnt = rows * pb / esz;
@@ -157,6 +163,17 @@ struct NcclComm : Comm2 {
     return check(nccl().AllReduce(d, d, n, ncclFloat64, ncclSum, comm, st), "norm all-reduce");
   }
   std::string error() const override { return err; }
+  std::string poll() override {
+    if (!comm || !nccl().CommGetAsyncError) return comm ? "" : err;
+    ncclResult_t a = 0;
+    ncclResult_t r = nccl().CommGetAsyncError(comm, &a);
+    if (r == 0 && (a == 0 || a == 7 /* ncclInProgress */)) return "";
+    err = std::string("NCCL asynchronous error: ") + nccl().GetErrorString(r ? r : a);
+    if (nccl().CommAbort) nccl().CommAbort(comm);
+    else nccl().CommDestroy(comm);
+    comm = nullptr;
+    return err;
+  }
 };
 
 

@@ -9,6 +9,8 @@
 
 #include <cuda_runtime.h>
 
+#include "../../include/mg.h"
+
 namespace mg {
 
 struct Comm2 {
@@ -22,6 +24,38 @@ struct Comm2 {
   virtual cudaError_t allreduce_max_u64(unsigned long long *d, int n, cudaStream_t st) = 0;
   virtual cudaError_t allreduce_sum_f64(double *d, int n, cudaStream_t st) = 0;
   virtual std::string error() const { return ""; }
+  // asynchronous transport failure (NCCL: ncclCommGetAsyncError); on error the
+  // communicator is aborted and the message returned ("" = healthy)
+  virtual std::string poll() { return ""; }
+};
+
+// Sticky status of a slab solver's enqueue_* calls: the first failed step
+// (kernel launch, halo exchange, all-gather, all-reduce) is kept until the
+// ABI takes it (ImplBase::take_status), then the graph being captured is
+// dropped and the call fails with MG_ENCCL / MG_ECUDA.
+struct TransportStatus {
+  int code = MG_OK;
+  std::string msg;
+  void note(cudaError_t e, const Comm2 *c, const char *what) {
+    if (e == cudaSuccess || code != MG_OK) return;
+    const std::string ce = c ? c->error() : std::string();
+    code = ce.empty() ? MG_ECUDA : MG_ENCCL;
+    msg = std::string(what) + ": " + (ce.empty() ? cudaGetErrorString(e) : ce);
+  }
+  int take(std::string *m, Comm2 *c) {
+    if (code == MG_OK && c) {
+      const std::string a = c->poll();
+      if (!a.empty()) {
+        code = MG_ENCCL;
+        msg = a;
+      }
+    }
+    const int r = code;
+    if (m) *m = msg;
+    code = MG_OK;
+    msg.clear();
+    return r;
+  }
 };
 
 // P virtual ranks in one process on one GPU: device-to-device copies.

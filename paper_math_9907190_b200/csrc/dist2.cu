@@ -284,15 +284,15 @@ struct Dist2 : ImplBase {
     // NCCL mode: one local rank; the caller's arrays are slabs
     std::vector<const T *> ui{vg((const T *)u_in)}, fe{vg((const T *)f_eff)};
     std::vector<T *> uo{vg((T *)u_out)};
-    cudaError_t e = cycle(ui, uo, fe, st, prof);
-    if (e) cudaGetLastError(), last = e;
+    status.note(cycle(ui, uo, fe, st, prof), comm.get(), "V-cycle");
   }
-  cudaError_t last = cudaSuccess;
+  int take_status(std::string *m) override { return status.take(m, comm.get()); }
+  TransportStatus status;
 
   void enqueue_final_norm(void *u, const void *f_eff, cudaStream_t st) override {
     const T *ui = vg((const T *)u), *fe = vg((const T *)f_eff);
-    xchg(0, false, 2, st, [&](int) { return ui; }, pitch);
-    xchg(0, false, 1, st, [&](int) { return fe; }, pitch);
+    status.note(xchg(0, false, 2, st, [&](int) { return ui; }, pitch), comm.get(), "halo exchange");
+    status.note(xchg(0, false, 1, st, [&](int) { return fe; }, pitch), comm.get(), "halo exchange");
     fast2_desc_fine<T>(ui, fe, pitch, rk[0].rD[0], M[0], s->cfg.order, coef, sink(), st, rows_full(0, rk[0].q));
   }
   cudaError_t reduce_hist(unsigned long long *d, int nslots, cudaStream_t st) override {
@@ -305,7 +305,7 @@ struct Dist2 : ImplBase {
       return;
     }
     const T *fv = vg((const T *)f);
-    xchg(0, false, 1, st, [&](int) { return fv; }, pitch);
+    status.note(xchg(0, false, 1, st, [&](int) { return fv; }, pitch), comm.get(), "halo exchange");
     launch2_ftilde_rows<T>(D2<const T>{fv, pitch}, D2<T>{vg((T *)ft), pitch}, M[0], lo(0, rk[0].q), hi(0, rk[0].q), st);
   }
   void enqueue_residual(const void *u, const void *f, void *r, cudaStream_t st, int64_t) override {
@@ -315,7 +315,7 @@ struct Dist2 : ImplBase {
       return;
     }
     const T *uv = vg((const T *)u), *fv = vg((const T *)f);
-    xchg(0, false, 1, st, [&](int) { return uv; }, pitch);
+    status.note(xchg(0, false, 1, st, [&](int) { return uv; }, pitch), comm.get(), "halo exchange");
     launch2_residual_rows<T>(D2<const T>{uv, pitch}, D2<const T>{fv, pitch}, D2<T>{vg((T *)r), pitch}, M[0],
                              s->cfg.order, coef, lo(0, rk[0].q), hi(0, rk[0].q), st);
   }
@@ -325,8 +325,8 @@ struct Dist2 : ImplBase {
       return;
     }
     launch2_norm_rows<T>(D2<const T>{vg((const T *)x), pitch}, M[0], lo(0, rk[0].q), hi(0, rk[0].q), mx, ss, st);
-    comm->allreduce_max_u64(mx, 1, st);
-    comm->allreduce_sum_f64(ss, 1, st);
+    status.note(comm->allreduce_max_u64(mx, 1, st), comm.get(), "norm all-reduce");
+    status.note(comm->allreduce_sum_f64(ss, 1, st), comm.get(), "norm all-reduce");
   }
   int launches_per_cycle() const override {
     int c = nloc;   // desc

@@ -336,17 +336,17 @@ struct Dist3 : ImplBase {
   D3<const T> cfv(const void *p) const { return D3<const T>{vg((const T *)p), pitch, fplane()}; }
   D3<T> fv(void *p) const { return D3<T>{vg((T *)p), pitch, fplane()}; }
 
-  cudaError_t last = cudaSuccess;
+  TransportStatus status;
   void enqueue_cycle(const void *u_in, void *u_out, const void *f_eff, cudaStream_t st, Prof *prof) override {
     std::vector<const T *> ui{vg((const T *)u_in)}, fe{vg((const T *)f_eff)};
     std::vector<T *> uo{vg((T *)u_out)};
-    cudaError_t e = cycle(ui, uo, fe, st, prof);
-    if (e) cudaGetLastError(), last = e;
+    status.note(cycle(ui, uo, fe, st, prof), comm.get(), "V-cycle");
   }
+  int take_status(std::string *m) override { return status.take(m, comm.get()); }
   void enqueue_final_norm(void *u, const void *f_eff, cudaStream_t st) override {
     const T *ui = vg((const T *)u), *fe = vg((const T *)f_eff);
-    xchg(0, false, 2, st, [&](int) { return ui; }, fplane());
-    xchg(0, false, 1, st, [&](int) { return fe; }, fplane());
+    status.note(xchg(0, false, 2, st, [&](int) { return ui; }, fplane()), comm.get(), "halo exchange");
+    status.note(xchg(0, false, 1, st, [&](int) { return fe; }, fplane()), comm.get(), "halo exchange");
     fast3_desc_fine<T>(ui, fe, pitch, rk[0].rR[0], M[0], s->cfg.order, coef, sink(), st, zr_fine(rk[0].q));
   }
   cudaError_t reduce_hist(unsigned long long *d, int nslots, cudaStream_t st) override {
@@ -358,7 +358,7 @@ struct Dist3 : ImplBase {
       return;
     }
     const T *fvp = vg((const T *)f);
-    xchg(0, false, 1, st, [&](int) { return fvp; }, fplane());
+    status.note(xchg(0, false, 1, st, [&](int) { return fvp; }, fplane()), comm.get(), "halo exchange");
     launch3_ftilde<T>(cfv(f), fv(ft), M[0], st, lo(0, rk[0].q), hi(0, rk[0].q));
   }
   void enqueue_residual(const void *u, const void *f, void *r, cudaStream_t st, int64_t) override {
@@ -368,7 +368,7 @@ struct Dist3 : ImplBase {
       return;
     }
     const T *uvp = vg((const T *)u);
-    xchg(0, false, 1, st, [&](int) { return uvp; }, fplane());
+    status.note(xchg(0, false, 1, st, [&](int) { return uvp; }, fplane()), comm.get(), "halo exchange");
     launch3_residual<T>(cfv(u), cfv(f), fv(r), M[0], s->cfg.order, coef, st, lo(0, rk[0].q), hi(0, rk[0].q));
   }
   void enqueue_norm(const void *x, unsigned long long *mx, double *ss, cudaStream_t st, int64_t) override {
@@ -377,8 +377,8 @@ struct Dist3 : ImplBase {
       return;
     }
     launch3_norm<T>(cfv(x), M[0], mx, ss, st, lo(0, rk[0].q), hi(0, rk[0].q));
-    comm->allreduce_max_u64(mx, 1, st);
-    comm->allreduce_sum_f64(ss, 1, st);
+    status.note(comm->allreduce_max_u64(mx, 1, st), comm.get(), "norm all-reduce");
+    status.note(comm->allreduce_sum_f64(ss, 1, st), comm.get(), "norm all-reduce");
   }
   int launches_per_cycle() const override {
     int c = nloc;   // desc

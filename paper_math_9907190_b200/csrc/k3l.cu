@@ -640,6 +640,9 @@ __global__ void __launch_bounds__(512, 1) k3l_tail(const __grid_constant__ Tail3
     o.plane = a.plane;
     return o;
   };
+  int ngp = 0;
+  const bool gdbg = P.dbg && blockIdx.x == 0 && threadIdx.x == 0;
+  if (gdbg) P.dbg[128] = gtimer();
 #define LOOPG(HH, BODY)                                            \
   {                                                                \
     const int H_ = (HH);                                           \
@@ -649,6 +652,7 @@ __global__ void __launch_bounds__(512, 1) k3l_tail(const __grid_constant__ Tail3
       BODY;                                                        \
     }                                                              \
     grid.sync();                                                   \
+    if (gdbg) P.dbg[129 + (ngp++)] = gtimer();                     \
   }
   for (int o = P.om; o < P.oc; o++) {
     const Lev3<T> &L = P.lv[o], &Lc = P.lv[o + 1];
@@ -659,6 +663,7 @@ __global__ void __launch_bounds__(512, 1) k3l_tail(const __grid_constant__ Tail3
   }
   if (blockIdx.x == 0) coarse3_block(P, (T *)dsm);
   grid.sync();
+  if (gdbg) P.dbg[129 + (ngp++)] = gtimer();
   D3<const T> none{nullptr, 0, 0};
   Coef<T> k0{};
   for (int o = P.oc - 1; o >= P.om; o--) {
@@ -800,6 +805,7 @@ bool lv3_tail(const Lev3<T> *h_lev, int om, int oc, int k, int *counter, cudaStr
   cudaStreamIsCapturing(st, &cap);
   const bool debug = env_flag("MG_TAIL_DEBUG") && cap == cudaStreamCaptureStatusNone;
   if (debug && !dbg) cudaMalloc(&dbg, 256 * sizeof(unsigned long long));
+  if (debug) cudaMemsetAsync(dbg, 0, 256 * sizeof(unsigned long long), st);
   P.dbg = debug ? dbg : nullptr;
   size_t elems = 0;
   for (int o = oc; o + 1 < k; o++) {
@@ -839,6 +845,9 @@ bool lv3_tail(const Lev3<T> *h_lev, int om, int oc, int k, int *counter, cudaStr
     cudaStreamSynchronize(st);
     fprintf(stderr, "[tail] CTA0 coarse phases (us):");
     for (int i = 1; i < 64 && h[i] > h[0] && h[i] - h[0] < 1000000000ull; i++)
+      fprintf(stderr, " %.2f", (h[i] - h[i - 1]) * 1e-3);
+    fprintf(stderr, "\n[tail] CTA0 grid phases (us):");
+    for (int i = 129; i < 256 && h[i] > h[128] && h[i] - h[128] < 1000000000ull; i++)
       fprintf(stderr, " %.2f", (h[i] - h[i - 1]) * 1e-3);
     fprintf(stderr, "\n");
   }

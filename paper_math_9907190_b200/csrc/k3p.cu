@@ -31,9 +31,10 @@ struct Masks {
   bool full;             // every own node of every thread is interior in x and y
   bool c0, c1, rA, rB;   // this thread's columns / rows interior
 };
+template <int NW>
 __device__ __forceinline__ Masks item_masks(const Item &it, int M, int xl, int yA) {
   Masks m;
-  m.full = it.x0 - 2 >= 1 && it.x0 + 61 <= M - 1 && it.y0 - 1 >= 1 && it.y0 + 30 <= M - 1;
+  m.full = it.x0 - 2 >= 1 && it.x0 + 61 <= M - 1 && it.y0 - 1 >= 1 && it.y0 + 2 * NW - 2 <= M - 1;
   m.c0 = xl >= 1 && xl <= M - 1;
   m.c1 = xl + 1 >= 1 && xl + 1 <= M - 1;
   m.rA = yA >= 1 && yA <= M - 1;
@@ -61,10 +62,11 @@ __device__ __forceinline__ void sel0(T &v, bool keep) {
 // i.e. PH at z = j-1 and Q = 1-PH at q = j-2; row B the other way round.
 // FINE = false: the same pass one octave down (G(s) -> R(s), s > 1): r is
 // read from the dense level array (the "f" box) instead of computed, no norm.
-template <class T, bool FINE = true>
+template <class T, bool FINE = true, int NW_ = 16, int NSO = 0>
 struct OpDesc3P {
-  using Gm = Geo<T>;
-  static constexpr int NS = FINE ? (sizeof(T) == 8 ? 5 : 8) : 8, GPL = Gm::GPL, PRO = FINE ? 2 : 0, EPI = 2;
+  using Gm = Geo<T, NW_>;
+  static constexpr int NW = NW_, NTH = Gm::NTH, MINB = NW <= 8 ? 2 : 1;
+  static constexpr int NS = NSO ? NSO : FINE ? (sizeof(T) == 8 ? 5 : 8) : 8, GPL = Gm::GPL, PRO = FINE ? 2 : 0, EPI = 2;
   static constexpr int U_OFF = 0, F_OFF = FINE ? al128(Gm::U_BYTES) : 0, SLOT = al128(F_OFF + Gm::F_BYTES);
   static constexpr int SMEM = NS * SLOT + 3 * Gm::GPL;
   struct Params {
@@ -93,13 +95,13 @@ struct OpDesc3P {
   static __device__ void begin(const Params &P, Ctx &C, const Item &it) {
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const int xl = it.x0 - 2 + 2 * lane, yA = it.y0 - 1 + 2 * w;
-    C.m = item_masks(it, P.M, xl, yA);
+    C.m = item_masks<NW>(it, P.M, xl, yA);
     const bool lk = lane >= 1 && lane <= TX / 2;
     // PH = 0: row A red at col 1, row B at col 0; PH = 1: the other way round
     C.oA[0] = lk && w >= 1 && C.m.rA && C.m.c1;
     C.oA[1] = lk && w >= 1 && C.m.rA && C.m.c0;
-    C.oB[0] = lk && w <= 14 && C.m.rB && C.m.c0;
-    C.oB[1] = lk && w <= 14 && C.m.rB && C.m.c1;
+    C.oB[0] = lk && w <= NW - 2 && C.m.rB && C.m.c0;
+    C.oB[1] = lk && w <= NW - 2 && C.m.rB && C.m.c1;
     C.bA = (int64_t)(yA >> 1) * P.out.pitch + (xl >> 1);
     C.bB = (int64_t)((yA + 1) >> 1) * P.out.pitch + (xl >> 1);
   }
@@ -234,7 +236,7 @@ struct OpDesc3P {
     }
   }
   static __device__ void finish(const Params &P, State &S) {
-    if (FINE) block_norm_push<NT>(P.ns, __longlong_as_double((long long)S.mx));
+    if (FINE) block_norm_push<NTH>(P.ns, __longlong_as_double((long long)S.mx));
   }
 };
 
@@ -247,10 +249,12 @@ struct OpDesc3P {
 // column of row A at plane q = j-2 is Q as well.
 // FINE = false: Egprolg/Egprolr one octave down (G(s) from R(s), s > 1): r is
 // read from the dense level array (the "f" box) and v_G(s) is written.
-template <class T, bool FINE = true>
+template <class T, bool FINE = true, int NW_ = 16, int NSO = 0>
 struct OpAsc3P {
-  using Gm = Geo<T>;
-  static constexpr int NS = FINE ? (sizeof(T) == 8 ? 4 : 7) : (sizeof(T) == 8 ? 7 : 10), GPL = Gm::GPL, PRO = 2, EPI = 2;
+  using Gm = Geo<T, NW_>;
+  static constexpr int NW = NW_, NTH = Gm::NTH, MINB = NW <= 8 ? 2 : 1;
+  static constexpr int NS = NSO ? NSO : FINE ? (sizeof(T) == 8 ? 4 : 7) : (sizeof(T) == 8 ? 7 : 10), GPL = Gm::GPL,
+                       PRO = 2, EPI = 2;
   static constexpr int U_OFF = 0, F_OFF = FINE ? al128(Gm::U_BYTES) : 0, V0_OFF = F_OFF + al128(Gm::F_BYTES),
                        V1_OFF = V0_OFF + al128(Gm::V_BYTES), SLOT = al128(V1_OFF + Gm::V_BYTES);
   static constexpr int SMEM = NS * SLOT + 3 * Gm::GPL;
@@ -282,10 +286,10 @@ struct OpAsc3P {
   static __device__ void begin(const Params &P, Ctx &C, const Item &it) {
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const int xl = it.x0 - 2 + 2 * lane, yA = it.y0 - 1 + 2 * w;
-    C.m = item_masks(it, P.M, xl, yA);
+    C.m = item_masks<NW>(it, P.M, xl, yA);
     const bool lk = lane >= 1 && lane <= TX / 2;
     C.oA = lk && w >= 1 && C.m.rA;
-    C.oB = lk && w <= 14 && C.m.rB;
+    C.oB = lk && w <= NW - 2 && C.m.rB;
     C.hx = (xl >> 1) - vx0(it.x0);
   }
   static __device__ void issue(const Params &P, const Item &it, int j, unsigned char *slot, uint64_t *bar) {
@@ -459,15 +463,24 @@ struct OpAsc3P {
 // ================================================================= launch
 template <class Op>
 static cudaError_t run_zpipe(typename Op::Params &P, int M, int zlo, int zhi, cudaStream_t st) {
-  // tiles start at x0 = 60 t - 2 (outputs x = 1 .. M-1), y0 = 30 t
-  return launch_zpipe<Op>(P, TX, TY, -2, 0, (M + 1) / TX + 1, (M + TY - 1) / TY, zlo, zhi, st);
+  // tiles start at x0 = 60 t - 2 (outputs x = 1 .. M-1), y0 = (2NW-2) t
+  constexpr int ty = Op::Gm::TYW;
+  return launch_zpipe<Op>(P, TX, ty, -2, 0, (M + 1) / TX + 1, (M + ty - 1) / ty, zlo, zhi, st);
 }
 
-template <class T>
-cudaError_t fast3p_desc_fine(const T *u, const T *f, int64_t pitch, const S3<T> &rr, int M, const Coef<T> &k,
-                             const NormSink &ns, cudaStream_t st, const ZRange3 &pz) {
-  using Op = OpDesc3P<T>;
-  using Gm = Geo<T>;
+// warps per CTA of the finest passes (MG_K3_NW: 8 = two 256-thread CTAs per SM,
+// the default: measured on B200 at 513^3 fp64, desc 505 -> 468 us, asc 700 -> 655
+// us, cycle -1.6 %; 16 = one 512-thread CTA per SM)
+static int k3p_nw() {
+  static const int nw = getenv("MG_K3_NW") ? atoi(getenv("MG_K3_NW")) : 8;
+  return nw == 8 ? 8 : 16;
+}
+
+template <class T, int NW, int NSO = 0>
+static cudaError_t desc_fine_nw(const T *u, const T *f, int64_t pitch, const S3<T> &rr, int M, const Coef<T> &k,
+                                const NormSink &ns, cudaStream_t st, const ZRange3 &pz) {
+  using Op = OpDesc3P<T, true, NW, NSO>;
+  using Gm = typename Op::Gm;
   typename Op::Params P{};
   const int64_t n = M + 1, plane = pitch * n, nz = pz.fplanes < 0 ? n : pz.fplanes;
   if (!tmap3<T>(&P.tu, u + (int64_t)pz.fz0 * plane, n, n, nz, pitch, plane, Gm::UW, Gm::UH) ||
@@ -482,10 +495,17 @@ cudaError_t fast3p_desc_fine(const T *u, const T *f, int64_t pitch, const S3<T> 
 }
 
 template <class T>
-cudaError_t fast3p_asc_fine(const S3<T> &vr, const T *u_old, const T *f, int64_t pitch, T *u_new, int M, T c,
-                            const Coef<T> &k, cudaStream_t st, const ZRange3 &pz) {
-  using Op = OpAsc3P<T>;
-  using Gm = Geo<T>;
+cudaError_t fast3p_desc_fine(const T *u, const T *f, int64_t pitch, const S3<T> &rr, int M, const Coef<T> &k,
+                             const NormSink &ns, cudaStream_t st, const ZRange3 &pz) {
+  if (k3p_nw() == 8) return desc_fine_nw<T, 8>(u, f, pitch, rr, M, k, ns, st, pz);
+  return desc_fine_nw<T, 16>(u, f, pitch, rr, M, k, ns, st, pz);
+}
+
+template <class T, int NW, int NSO = 0>
+static cudaError_t asc_fine_nw(const S3<T> &vr, const T *u_old, const T *f, int64_t pitch, T *u_new, int M, T c,
+                               const Coef<T> &k, cudaStream_t st, const ZRange3 &pz) {
+  using Op = OpAsc3P<T, true, NW, NSO>;
+  using Gm = typename Op::Gm;
   typename Op::Params P{};
   const int64_t n = M + 1, plane = pitch * n, nz = pz.fplanes < 0 ? n : pz.fplanes;
   if (!tmap3<T>(&P.tu, u_old + (int64_t)pz.fz0 * plane, n, n, nz, pitch, plane, Gm::UW, Gm::UH) ||
@@ -506,9 +526,22 @@ cudaError_t fast3p_asc_fine(const S3<T> &vr, const T *u_old, const T *f, int64_t
 }
 
 template <class T>
-cudaError_t fast3p_rest_gr(const D3<T> &r, const S3<T> &rr, int M, cudaStream_t st) {
-  using Op = OpDesc3P<T, false>;
-  using Gm = Geo<T>;
+cudaError_t fast3p_asc_fine(const S3<T> &vr, const T *u_old, const T *f, int64_t pitch, T *u_new, int M, T c,
+                            const Coef<T> &k, cudaStream_t st, const ZRange3 &pz) {
+  if (k3p_nw() == 8) return asc_fine_nw<T, 8>(vr, u_old, f, pitch, u_new, M, c, k, st, pz);
+  return asc_fine_nw<T, 16>(vr, u_old, f, pitch, u_new, M, c, k, st, pz);
+}
+
+// the G(s) level passes (s > 1): MG_K3_NWL warps (default 16)
+static int k3p_nwl() {
+  static const int nw = getenv("MG_K3_NWL") ? atoi(getenv("MG_K3_NWL")) : 16;
+  return nw == 8 ? 8 : 16;
+}
+
+template <class T, int NW>
+static cudaError_t rest_gr_nw(const D3<T> &r, const S3<T> &rr, int M, cudaStream_t st) {
+  using Op = OpDesc3P<T, false, NW>;
+  using Gm = typename Op::Gm;
   typename Op::Params P{};
   const int64_t n = M + 1;
   if (!tmap3<T>(&P.tf, r.p, n, n, n, r.pitch, r.plane, Gm::FW, Gm::FH)) return cudaErrorInvalidValue;
@@ -516,11 +549,16 @@ cudaError_t fast3p_rest_gr(const D3<T> &r, const S3<T> &rr, int M, cudaStream_t 
   P.M = M;
   return run_zpipe<Op>(P, M, 0, M, st);
 }
-
 template <class T>
-cudaError_t fast3p_jac_g(const S3<T> &vr, const D3<T> &r, const D3<T> &v, int M, T c, cudaStream_t st) {
-  using Op = OpAsc3P<T, false>;
-  using Gm = Geo<T>;
+cudaError_t fast3p_rest_gr(const D3<T> &r, const S3<T> &rr, int M, cudaStream_t st) {
+  if (k3p_nwl() == 8) return rest_gr_nw<T, 8>(r, rr, M, st);
+  return rest_gr_nw<T, 16>(r, rr, M, st);
+}
+
+template <class T, int NW>
+static cudaError_t jac_g_nw(const S3<T> &vr, const D3<T> &r, const D3<T> &v, int M, T c, cudaStream_t st) {
+  using Op = OpAsc3P<T, false, NW>;
+  using Gm = typename Op::Gm;
   typename Op::Params P{};
   const int64_t n = M + 1, H = M / 2 + 1;
   if (!tmap3<T>(&P.tf, r.p, n, n, n, r.pitch, r.plane, Gm::FW, Gm::FH)) return cudaErrorInvalidValue;
@@ -531,6 +569,11 @@ cudaError_t fast3p_jac_g(const S3<T> &vr, const D3<T> &r, const D3<T> &v, int M,
   P.M = M;
   P.c = c;
   return run_zpipe<Op>(P, M, 0, M, st);
+}
+template <class T>
+cudaError_t fast3p_jac_g(const S3<T> &vr, const D3<T> &r, const D3<T> &v, int M, T c, cudaStream_t st) {
+  if (k3p_nwl() == 8) return jac_g_nw<T, 8>(vr, r, v, M, c, st);
+  return jac_g_nw<T, 16>(vr, r, v, M, c, st);
 }
 
 template cudaError_t fast3p_rest_gr<double>(const D3<double> &, const S3<double> &, int, cudaStream_t);

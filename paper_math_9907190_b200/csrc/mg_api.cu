@@ -708,7 +708,13 @@ static int run_cycle(mg_solver *s, const void *u_in, void *u_out, const void *f_
     s->impl->enqueue_cycle_mode(u_in, u_out, f_eff, s->st, nullptr, mode);
     cudaError_t le = cudaGetLastError();
     if (le == cudaSuccess) le = take_launch_error();
+    std::string tmsg;
+    const int tc = s->impl->take_status(&tmsg);   // a failed transport step (multi-GPU)
     cudaError_t e = cudaStreamEndCapture(s->st, &g);
+    if (tc != MG_OK) {   // never instantiate a half-enqueued cycle
+      if (g) cudaGraphDestroy(g);
+      return fail(s, tc, "V-cycle capture: " + tmsg);
+    }
     if (le != cudaSuccess) {
       if (g) cudaGraphDestroy(g);
       return fail(s, MG_ECUDA, std::string("kernel launch during capture: ") + cudaGetErrorString(le));
@@ -733,6 +739,12 @@ static int begin(mg_solver *s) {
 static int end(mg_solver *s) {
   CKS(s, cudaGetLastError());
   CKS(s, take_launch_error());   // a pass whose launch was rejected (kernels.h)
+  std::string tmsg;
+  const int tc = s->impl ? s->impl->take_status(&tmsg) : MG_OK;   // transport (NCCL) failures
+  if (tc != MG_OK) {
+    drop_graphs(s);
+    return fail(s, tc, tmsg);
+  }
   CKS(s, cudaEventRecord(s->ev_out, s->st));
   CKS(s, cudaStreamWaitEvent(s->user, s->ev_out, 0));
   return MG_OK;

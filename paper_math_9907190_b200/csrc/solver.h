@@ -142,8 +142,13 @@ struct ImplBase {
   virtual int vcycle_all(mg_solver *, void *, const void *, int, double *) { return 1; }
   // combine the per-cycle residual-norm maxima over ranks
   virtual cudaError_t reduce_hist(unsigned long long *, int, cudaStream_t) { return cudaSuccess; }
-  // before the cycles of one call: ghost rows of f (or f~)
-  virtual cudaError_t prepare_rhs(const void *, cudaStream_t) { return cudaSuccess; }
+  // sticky failure of an enqueue_* call whose transport step failed (halo
+  // exchange, all-gather, all-reduce) or an asynchronous transport error:
+  // returns an mg_status (MG_OK when healthy) and clears it; *msg says why
+  virtual int take_status(std::string *msg) {
+    (void)msg;
+    return 0;
+  }
   std::vector<void *> bufs;
   size_t bytes = 0;
   std::vector<double> Nl;   // interior nodes per level

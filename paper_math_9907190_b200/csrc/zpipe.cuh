@@ -19,16 +19,33 @@ constexpr int TX = 60, TY = 30, NT = 512;
 constexpr int GS = 34;                       // green-plane ring: 34 x 34 (rows/lanes -1 .. 32)
 constexpr int al128(int n) { return (n + 127) / 128 * 128; }
 
-template <class T>
+// Tile geometry of the fine-resolution passes (k3p.cu) for NW warps of 32
+// lanes: lane l owns columns x0-2+2l, +1 and warp w rows y0-1+2w, +1, so a
+// CTA owns 64 x 2NW nodes per plane and outputs the inner 60 x (2NW-2).
+template <class T, int NW_ = 16>
 struct Geo {
+  static constexpr int NW = NW_, NTH = 32 * NW;
+  static constexpr int TYW = 2 * NW - 2;                 // output rows per tile
+  static constexpr int GR = 2 * NW + 2;                  // green-ring rows (rows -1 .. 2NW)
   static constexpr int AL = 16 / (int)sizeof(T);       // TMA x alignment (elements)
   static constexpr int UXO = (AL == 2) ? 4 : 6;         // u box starts at x0 - UXO (>= 3, aligned)
-  static constexpr int UW = (UXO + 63 + AL - 1) / AL * AL, UH = TY + 4;
-  static constexpr int FW = 64, FH = TY + 2;            // f box: x0-2 .., y0-1 ..
-  static constexpr int VW = (34 + AL - 1 + AL - 1) / AL * AL, VH = TY / 2 + 2;
+  static constexpr int UW = (UXO + 63 + AL - 1) / AL * AL, UH = TYW + 4;
+  static constexpr int FW = 64, FH = TYW + 2;           // f box: x0-2 .., y0-1 ..
+  static constexpr int VW = (34 + AL - 1 + AL - 1) / AL * AL, VH = TYW / 2 + 2;
   static constexpr int U_BYTES = UW * UH * (int)sizeof(T), F_BYTES = FW * FH * (int)sizeof(T);
   static constexpr int V_BYTES = VW * VH * (int)sizeof(T);
-  static constexpr int GPL = al128(GS * GS * (int)sizeof(T));
+  static constexpr int GPL = al128(GS * GR * (int)sizeof(T));
+};
+
+// Threads per CTA and resident CTAs per SM of a pipeline Op: Op::NTH /
+// Op::MINB when it declares them, else one 512-thread CTA per SM.
+template <class Op, class = void>
+struct OpNT {
+  static constexpr int nt = NT, minb = 1;
+};
+template <class Op>
+struct OpNT<Op, std::void_t<decltype(Op::NTH), decltype(Op::MINB)>> {
+  static constexpr int nt = Op::NTH, minb = Op::MINB;
 };
 
 template <class T>
@@ -120,7 +137,7 @@ using namespace zp;
 // A 3-plane ring after the slots is addressed by gz (plane j-1), gq (plane
 // j-2) and gr (plane j-3).
 template <class Op>
-__global__ void __launch_bounds__(NT, 1) zpipe(const __grid_constant__ typename Op::Params P) {
+__global__ void __launch_bounds__(OpNT<Op>::nt, OpNT<Op>::minb) zpipe(const __grid_constant__ typename Op::Params P) {
   constexpr int NS = Op::NS, D = NS - 2;
   extern __shared__ __align__(128) unsigned char smem[];
   __shared__ __align__(8) uint64_t bar[NS];
@@ -226,14 +243,15 @@ static cudaError_t launch_zpipe(typename Op::Params &P, int tx, int ty, int xoff
   P.sc.zhi = zhi;
   P.sc.rev = zp_next_rev();
   zp_next_rev() = 0;
-  P.sc.S = P.sc.T >= sms ? 1 : (sms + P.sc.T - 1) / P.sc.T;
+  const int slots = sms * OpNT<Op>::minb;   // resident CTAs
+  P.sc.S = P.sc.T >= slots ? 1 : (slots + P.sc.T - 1) / P.sc.T;
   if (P.sc.S > zhi - zlo) P.sc.S = zhi - zlo;
   const long long work = (long long)P.sc.T * (zhi - zlo);
-  const int grid = work < sms ? (int)work : sms;
+  const int grid = work < slots ? (int)work : slots;
   // small levels (at most one work unit per CTA): programmatic launch (MG_PDL_SMALL3=1)
   static const bool pdl_small = env_flag("MG_PDL_SMALL3");
   const bool pdl = pdl_enabled() || (pdl_small && (long long)P.sc.T * P.sc.S <= grid);
-  return note_launch(launch_pdl_if(pdl, zpipe<Op>, dim3(grid), dim3(NT), Op::SMEM, st, P));
+  return note_launch(launch_pdl_if(pdl, zpipe<Op>, dim3(grid), dim3(OpNT<Op>::nt), Op::SMEM, st, P));
 }
 
 // 3D tensor map over nx x ny x nz elements (row pitch, plane stride in

@@ -76,6 +76,9 @@ CASES = [
     ({"MG_DA_NT": "256"}, 2, 513, 4, "float64"),
     ({"MG_DA_MINO": "2", "MG_AD_MINO": "3"}, 2, 1025, 2, "float64"),
     ({"MG_3D_NOSERP": "1"}, 3, 129, 2, "float64"),
+    ({"MG_K3_NW": "8"}, 3, 129, 2, "float64"),
+    ({"MG_K3_NW": "8", "MG_K3_NWL": "8"}, 3, 257, 2, "float64"),
+    ({"MG_K3_NW": "8"}, 3, 65, 2, "float32"),
 ]
 
 
