@@ -200,11 +200,15 @@ constexpr int BOX34x33 = al128(34 * 33 * 8), BOX36x33 = al128(36 * 33 * 8);
 // L_j = {v_G(2s)(j), r_B(j-1), r_C(j-2)}.  Step j: centres of plane j-1
 // (Emprolm), corners of plane j-2 from the new centres
 // (Emprolb).
-struct OpJacM3 {
+template <int NW_ = 16>
+struct OpJacM3T {
+  // NW warps: thread rows b0-1+2w+R cover 2NW rows, 2NW-1 of them output rows
+  static constexpr int NW = NW_, NTH = 32 * NW, MINB = NW <= 8 ? 2 : 1;
+  static constexpr int GROWS = 2 * NW + 1, RB2 = RW * 2 * NW * 8;
   static constexpr int NS = 5, PRO = 1, EPI = 2;
-  static constexpr int OG = 0, OR = BOX34x33;   // v_G box, r boxes (B, C)
-  static constexpr int SLOT = OR + 2 * RBOX2;
-  static constexpr int GPL = RBOX2;             // centre ring plane
+  static constexpr int OG = 0, OR = al128(34 * GROWS * 8);   // v_G box, r boxes (B, C)
+  static constexpr int SLOT = OR + 2 * RB2;
+  static constexpr int GPL = RB2;               // centre ring plane
   static constexpr int SMEM = NS * SLOT + 3 * GPL;
   struct Params {
     CUtensorMap tg, tr[2];   // v_G(2s); r_M B, C
@@ -239,10 +243,10 @@ struct OpJacM3 {
   }
   static __device__ void issue(const Params &P, const Item &it, int j, unsigned char *slot, uint64_t *bar) {
     const bool wf = j >= it.zs, wc = j >= it.zs + 2;
-    mbar_expect_tx(bar, 34 * 33 * 8 + (wf ? RBOX2 : 0) + (wc ? RBOX2 : 0));
+    mbar_expect_tx(bar, 34 * GROWS * 8 + (wf ? RB2 : 0) + (wc ? RB2 : 0));
     tma_load_3d(slot + OG, &P.tg, it.x0 - 2, it.y0 - 1, j, bar);
     if (wf) tma_load_3d(slot + OR, &P.tr[0], it.x0 - 2, it.y0 - 1, j - 1, bar);
-    if (wc) tma_load_3d(slot + OR + RBOX2, &P.tr[1], it.x0 - 2, it.y0 - 1, j - 2, bar);
+    if (wc) tma_load_3d(slot + OR + RB2, &P.tr[1], it.x0 - 2, it.y0 - 1, j - 2, bar);
   }
   template <int PH>
   static __device__ __forceinline__ void step(const Params &P, State &S, const Ctx &Cx, const Item &it, int j,
@@ -277,7 +281,7 @@ struct OpJacM3 {
       if (ok && Cx.core[R] && cout) __stcs(P.v.s[B] + (int64_t)c * P.v.plane + (int64_t)b * P.v.pitch + a, bn[R]);
       if (qok && Cx.core[R] && Cx.b1k[R]) {
         const T *G0 = (const T *)gq + orr, *G1 = (const T *)gr + orr;   // centres of planes q, q-1
-        T u = -(P.cc * Rb[RBOX2 / 8]);
+        T u = -(P.cc * Rb[RB2 / 8]);
         u = u + S.bo[PH][R];     // (a, b, c)
         u = u + S.bo[Q][R];      // (a, b, c-1)
         u = u + G0[-RW];         // (a, b-1, c)
@@ -294,6 +298,7 @@ struct OpJacM3 {
   }
   static __device__ void finish(const Params &, State &) {}
 };
+using OpJacM3 = OpJacM3T<16>;
 
 // ===================================================== R(s) -> M(s): a11
 // Thread columns (a0+l, b0+2w+R), tiles 32 x 32, no ring.
@@ -822,18 +827,30 @@ cudaError_t fast3s_jac_r(const S3<double> &vm, const S3<double> &r, const S3<dou
   return launch_zpipe<Op>(P, 30, 15, 0, 0, cdiv(H - 1, 30), cdiv(H - 1, 15), 0, H - 1, st);
 }
 
-cudaError_t fast3s_jac_m(const D3<double> &vc, const S3<double> &r, const S3<double> &v, int M, double cc,
-                         cudaStream_t st) {
-  using Op = OpJacM3;
-  Op::Params P{};
+template <int NW>
+static cudaError_t jac_m_nw(const D3<double> &vc, const S3<double> &r, const S3<double> &v, int M, double cc,
+                            cudaStream_t st) {
+  using Op = OpJacM3T<NW>;
+  typename Op::Params P{};
   const int H = M / 2 + 1;
-  if (!tmap3<T>(&P.tg, vc.p, H, H, H, vc.pitch, vc.plane, 34, 33) || !tsub(&P.tr[0], r, B, H, RW, RH2) ||
-      !tsub(&P.tr[1], r, C, H, RW, RH2))
+  if (!tmap3<T>(&P.tg, vc.p, H, H, H, vc.pitch, vc.plane, 34, Op::GROWS) || !tsub(&P.tr[0], r, B, H, RW, 2 * NW) ||
+      !tsub(&P.tr[1], r, C, H, RW, 2 * NW))
     return cudaErrorInvalidValue;
   P.v = v;
   P.H = H;
   P.cc = cc;
-  return launch_zpipe<Op>(P, 30, 31, 0, 0, cdiv(H - 1, 30), cdiv(H - 1, 31), 0, H - 1, st);
+  constexpr int tb = 2 * NW - 1;
+  return launch_zpipe<Op>(P, 30, tb, 0, 0, cdiv(H - 1, 30), cdiv(H - 1, tb), 0, H - 1, st);
+}
+
+// warps per CTA of the magenta Jacobi pass (MG_K3S_NW: 8 = two 256-thread CTAs
+// per SM, the default -- measured on B200 at 513^3 fp64: jac_m(1) 142 -> 134 us,
+// cycle -0.7 %; 16 = one 512-thread CTA per SM)
+cudaError_t fast3s_jac_m(const D3<double> &vc, const S3<double> &r, const S3<double> &v, int M, double cc,
+                         cudaStream_t st) {
+  static const int nw = getenv("MG_K3S_NW") ? atoi(getenv("MG_K3S_NW")) : 8;
+  if (nw == 8) return jac_m_nw<8>(vc, r, v, M, cc, st);
+  return jac_m_nw<16>(vc, r, v, M, cc, st);
 }
 
 cudaError_t fast3s_rest_rm(const S3<double> &rr, const S3<double> &rm, int M, cudaStream_t st) {

@@ -79,6 +79,9 @@ CASES = [
     ({"MG_K3_NW": "8"}, 3, 129, 2, "float64"),
     ({"MG_K3_NW": "8", "MG_K3_NWL": "8"}, 3, 257, 2, "float64"),
     ({"MG_K3_NW": "8"}, 3, 65, 2, "float32"),
+    ({"MG_K3_NW": "16"}, 3, 129, 2, "float64"),
+    ({"MG_K3S_NW": "16"}, 3, 129, 2, "float64"),
+    ({"MG_K3S_NW": "8"}, 3, 257, 2, "float64"),
 ]
 
 
