@@ -195,10 +195,59 @@ struct Dist2 : ImplBase {
     return r;
   }
 
+  // Octaves >= oa on the full arrays (every NCCL rank; once in loopback), once
+  // r_A(oa) is complete on every rank: the single-GPU pass sequence, octave
+  // pairs fused (rest_dad, jac_ad) where both levels are full; ends with
+  // v_A(oa) (the distributed ascent starts with jac_d of octave oa - 1).
+  cudaError_t coarse_part(cudaStream_t st, Prof *prof) {
+    const double w = sizeof(T);
+    cudaError_t e;
+    bool a_done = false;
+    for (int o = oa; o < oc; o++) {
+      if (!a_done) {
+        STEP("rest_ad", 2 * o, 1, w * (Nl[2 * o] + Nl[2 * o + 1]));
+        if ((e = fast2_rest_ad<T>(rAf[o], rDf[o], M[o], st))) return e;
+      }
+      a_done = o + 1 < oc;
+      if (a_done) {
+        STEP("rest_dad", 2 * o + 1, 1, w * (Nl[2 * o + 1] + Nl[2 * o + 2] + Nl[2 * o + 3]));
+        if ((e = fast2_rest_dad<T>(rDf[o], rAf[o + 1], rDf[o + 1], M[o + 1], st, false))) return e;
+      } else {
+        STEP("rest_da", 2 * o + 1, 1, w * (Nl[2 * o + 1] + Nl[2 * o + 2]));
+        if ((e = fast2_rest_da<T>(rDf[o], rAf[o + 1], M[o + 1], st))) return e;
+      }
+    }
+    STEP("coarse", 2 * oc, 1, 0);
+    launch2_coarse<T>(d_lev, oc, k, s->d_counter, st);
+    bool d_done = false;
+    for (int o = oc - 1; o >= oa; o--) {
+      if (!d_done) {
+        STEP("jac_d", 2 * o + 1, 1, w * (Nl[2 * o + 2] + 2 * Nl[2 * o + 1]));
+        if ((e = fast2_jac_d<T>(vAf[o + 1], rDf[o], vDf[o], M[o], cD[o], st))) return e;
+      }
+      d_done = o > oa;
+      if (d_done) {
+        STEP("jac_ad", 2 * o, 1, w * (Nl[2 * o + 1] + Nl[2 * o] + 2 * Nl[2 * o - 1]));
+        if ((e = fast2_jac_ad<T>(vDf[o], rAf[o], cA[o], rDf[o - 1], vDf[o - 1], M[o - 1], cD[o - 1], st, false)))
+          return e;
+      } else {
+        STEP("jac_a", 2 * o, 1, w * (Nl[2 * o + 1] + 2 * Nl[2 * o]));
+        if ((e = fast2_jac_a<T>(vDf[o], rAf[o], vAf[o], M[o], cA[o], st))) return e;
+      }
+    }
+    return cudaSuccess;
+  }
+  int coarse_launches() const {
+    int c = 0;
+    for (int o = oa; o < oc; o++) c += (o == oa) + 1;
+    c += 1;
+    for (int o = oc - 1; o >= oa; o--) c += (o == oc - 1) + 1;
+    return c;
+  }
+
   cudaError_t cycle(const std::vector<const T *> &uin, const std::vector<T *> &uout, const std::vector<const T *> &fe,
                     cudaStream_t st, Prof *prof) {
     const double w = sizeof(T);
-    const int L = 2 * k - 1;
     cudaError_t e;
     STEP("halo_u_f", 0, 0, 0);
     if ((e = xchg(0, false, 2, st, [&](int i) { return uin[i]; }, pitch))) return e;
@@ -225,26 +274,7 @@ struct Dist2 : ImplBase {
     STEP("agglomerate", 2 * oa, 0, 0);
     if ((e = comm->allgather((char *)rAf[oa].p, rAf[oa].pitch * sizeof(T), lo(oa, rk[0].q), R(oa), sizeof(T), st)))
       return e;
-    // ---- coarse octaves on full arrays (every NCCL rank; once in loopback)
-    for (int o = oa; o < oc; o++) {
-      if (o > oa) {
-        STEP("rest_ad", 2 * o, 1, w * (Nl[2 * o] + Nl[2 * o + 1]));
-        if ((e = fast2_rest_ad<T>(rAf[o], rDf[o], M[o], st))) return e;
-      } else {
-        STEP("rest_ad", 2 * o, 1, w * (Nl[2 * o] + Nl[2 * o + 1]));
-        if ((e = fast2_rest_ad<T>(rAf[o], rDf[o], M[o], st))) return e;
-      }
-      STEP("rest_da", 2 * o + 1, 1, w * (Nl[2 * o + 1] + Nl[2 * o + 2]));
-      if ((e = fast2_rest_da<T>(rDf[o], rAf[o + 1], M[o + 1], st))) return e;
-    }
-    STEP("coarse", 2 * oc, 1, 0);
-    launch2_coarse<T>(d_lev, oc, k, s->d_counter, st);
-    for (int o = oc - 1; o >= oa; o--) {
-      STEP("jac_d", 2 * o + 1, 1, w * (Nl[2 * o + 2] + 2 * Nl[2 * o + 1]));
-      if ((e = fast2_jac_d<T>(vAf[o + 1], rDf[o], vDf[o], M[o], cD[o], st))) return e;
-      STEP("jac_a", 2 * o, 1, w * (Nl[2 * o + 1] + 2 * Nl[2 * o]));
-      if ((e = fast2_jac_a<T>(vDf[o], rAf[o], vAf[o], M[o], cA[o], st))) return e;
-    }
+    if ((e = coarse_part(st, prof))) return e;
     // ---- distributed ascent
     for (int o = oa - 1; o >= 0; o--) {
       STEP("jac_d", 2 * o + 1, nloc, w * (Nl[2 * o + 2] + 2 * Nl[2 * o + 1]));
@@ -270,7 +300,6 @@ struct Dist2 : ImplBase {
             return e;
       }
     }
-    (void)L;
     return cudaSuccess;
   }
 
@@ -331,9 +360,7 @@ struct Dist2 : ImplBase {
   int launches_per_cycle() const override {
     int c = nloc;   // desc
     for (int o = 0; o < oa; o++) c += ((o >= 1) + 1) * nloc;
-    for (int o = oa; o < oc; o++) c += 2;
-    c += 1;
-    for (int o = oc - 1; o >= oa; o--) c += 2;
+    c += coarse_launches();
     for (int o = oa - 1; o >= 0; o--) c += 2 * nloc;
     return c;
   }
@@ -405,17 +432,309 @@ struct Dist2 : ImplBase {
   }
 };
 
+// ============================================================== Dist2CA
+// Communication-avoiding variant ("one u-exchange per cycle"):
+// every rank keeps full-size level arrays and computes each distributed level
+// on its own rows plus a level-dependent band of ghost rows, redundantly, so
+// that a V-cycle needs ONE halo exchange of u (Gu rows per side) and the
+// all-gather of the agglomeration level r_A(oa), instead of one exchange per
+// level and colour.  The bands follow from the stencils' reach (derived in
+// DESIGN.md 8): the ascent's A(1) output is the own rows; a D(s) level output
+// band w needs v_A(2s) on w + 2s and r_D(s) on w + s; an A(s) band w needs
+// v_D(s) on w + 2s and r_A(s) on w + s; the descent's bands cover both the
+// ascent's r needs and the next restriction's reach (+s per step).  At 8193^2
+// over 8 ranks Gu = 76 fine rows (1024 owned).  The node formulas are those of
+// the single-GPU kernels (the same kernels, on row windows), so the iterate is
+// bit-identical to the single-GPU solver (tests/test_gpu_dist.py).
+// Used when Gu fits in one neighbour's slab (Gu <= rows per rank); otherwise
+// (thin slabs, deep agglomeration) the per-level schedule of Dist2 runs.
+template <class T>
+struct Dist2CA : Dist2<T> {
+  using B = Dist2<T>;
+  using B::comm;
+  using B::k;
+  using B::loop;
+  using B::M;
+  using B::n;
+  using B::nloc;
+  using B::oa;
+  using B::pitch;
+  using B::rk;
+  using B::s;
+  bool ca = false;
+  int Gu = 0;
+  std::vector<int> WD, WA, waD, waA;   // bands (fine rows): descent r_D / r_A, ascent v_D / v_A
+  struct Full {
+    D2<T> u[2], f, ft;
+    std::vector<S2<T>> rD, vD;   // octaves o < oa
+    std::vector<D2<T>> rA, vA;   // 1 <= o < oa
+  };
+  std::vector<Full> fl;   // per local rank
+  cudaGraphExec_t gexec[2] = {nullptr, nullptr};   // NCCL mode: the cycle u[p] -> u[p^1]
+
+  Dist2CA(mg_solver *sv, bool loopback) : B(sv, loopback) {}
+  ~Dist2CA() override {
+    for (auto &g : gexec)
+      if (g) cudaGraphExecDestroy(g);
+  }
+
+  static int up(int v, int m) { return (v + m - 1) / m * m; }
+  void plan() {
+    WD.assign(oa, 0);
+    WA.assign(oa + 1, 0);
+    waD.assign(oa, 0);
+    waA.assign(oa + 1, 0);
+    std::vector<int> rDneed(oa, 0), rAneed(oa + 1, 0);
+    int reqD = 2;   // the finest ascent (A(1), own rows) reads v_D(1) within 2 rows
+    for (int o = 0; o < oa; o++) {
+      const int s_ = 1 << o;
+      waD[o] = up(reqD, 4 * s_);
+      rDneed[o] = waD[o] + s_;
+      const int reqA = waD[o] + 2 * s_;
+      if (o + 1 < oa) {
+        waA[o + 1] = up(reqA, 8 * s_);
+        rAneed[o + 1] = waA[o + 1] + 2 * s_;
+        reqD = waA[o + 1] + 4 * s_;
+      }
+    }
+    WA[oa] = 0;   // the agglomeration level: own rows (all-gathered)
+    for (int o = oa - 1; o >= 0; o--) {
+      const int s_ = 1 << o;
+      WD[o] = up(std::max(rDneed[o], WA[o + 1] + s_), 4 * s_);
+      if (o >= 1) WA[o] = up(std::max(rAneed[o], WD[o] + s_), 4 * s_);
+    }
+    Gu = up(WD[0] + 2, 2);
+  }
+
+  cudaError_t alloc() override {
+    cudaError_t e = B::alloc();
+    if (e) return e;
+    plan();
+    ca = !env_flag("MG_DIST_PERLEVEL") && oa >= 1 && Gu <= B::R(0);
+    if (!ca) return cudaSuccess;
+    fl.resize(nloc);
+    const int64_t nn = n;
+    for (int i = 0; i < nloc; i++) {
+      Full &F = fl[i];
+      void *q;
+      for (D2<T> *d : {&F.u[0], &F.u[1], &F.f}) {
+        if ((e = B::dalloc(&q, sizeof(T) * nn * pitch))) return e;
+        *d = D2<T>{(T *)q, pitch};
+      }
+      if (s->cfg.order == 4) {
+        if ((e = B::dalloc(&q, sizeof(T) * nn * pitch))) return e;
+        F.ft = D2<T>{(T *)q, pitch};
+      }
+      F.rD.resize(oa);
+      F.vD.resize(oa);
+      F.rA.resize(oa);
+      F.vA.resize(oa);
+      for (int o = 0; o < oa; o++) {
+        const int64_t H = M[o] / 2 + 1, ph = B::pitch_for(H);
+        for (S2<T> *d : {&F.rD[o], &F.vD[o]}) {
+          void *ee, *oo;
+          if ((e = B::dalloc(&ee, sizeof(T) * H * ph)) || (e = B::dalloc(&oo, sizeof(T) * H * ph))) return e;
+          *d = S2<T>{(T *)ee, (T *)oo, ph};
+        }
+        if (o >= 1) {
+          const int64_t Wd = M[o] + 1, pa = B::pitch_for(Wd);
+          for (D2<T> *d : {&F.rA[o], &F.vA[o]}) {
+            if ((e = B::dalloc(&q, sizeof(T) * Wd * pa))) return e;
+            *d = D2<T>{(T *)q, pa};
+          }
+        }
+      }
+    }
+    return cudaSuccess;
+  }
+
+  // row window of a level: fine rows [lo - W, hi + W) of rank q in units of u
+  // fine rows, clipped to [0, top)
+  Rows2 win(int q, int W, int unit, int top) const {
+    Rows2 r;
+    r.ylo = std::max(0, (B::lo(0, q) - W) / unit);
+    r.yhi = std::min(top, (B::hi(0, q) + W) / unit);
+    return r;
+  }
+  const T *fe(int i) const { return s->cfg.order == 4 ? fl[i].ft.p : fl[i].f.p; }
+
+  // one V-cycle on the internal arrays, u[cur] -> u[cur ^ 1]
+  cudaError_t cycle_ca(int cur, cudaStream_t st, Prof *prof) {
+    const double w = sizeof(T);
+    auto &Nl = B::Nl;
+    const auto &cD = B::cD;
+    const auto &cA = B::cA;
+    const auto &coef = B::coef;
+    cudaError_t e;
+    STEP("halo_u", 0, 0, 0);
+    if ((e = B::xchg(0, false, Gu, st, [&](int i) { return fl[i].u[cur].p; }, pitch))) return e;
+    STEP("desc_fine", 0, nloc, w * (2 * Nl[0] + Nl[1]));
+    for (int i = 0; i < nloc; i++)
+      if ((e = fast2_desc_fine<T>(fl[i].u[cur].p, fe(i), pitch, fl[i].rD[0], M[0], s->cfg.order, coef, B::sink(), st,
+                                  win(rk[i].q, WD[0], 1, M[0]))))
+        return e;
+    for (int o = 0; o < oa; o++) {
+      const int s_ = 1 << o;
+      if (o >= 1) {
+        STEP("rest_ad", 2 * o, nloc, w * (Nl[2 * o] + Nl[2 * o + 1]));
+        for (int i = 0; i < nloc; i++)
+          if ((e = fast2_rest_ad<T>(fl[i].rA[o], fl[i].rD[o], M[o], st, win(rk[i].q, WD[o], s_, M[o])))) return e;
+      }
+      STEP("rest_da", 2 * o + 1, nloc, w * (Nl[2 * o + 1] + Nl[2 * o + 2]));
+      for (int i = 0; i < nloc; i++) {
+        const D2<T> &out = (o + 1 < oa) ? fl[i].rA[o + 1] : B::rAf[oa];
+        if ((e = fast2_rest_da<T>(fl[i].rD[o], out, M[o + 1], st, win(rk[i].q, WA[o + 1], 2 * s_, M[o + 1]))))
+          return e;
+      }
+    }
+    STEP("agglomerate", 2 * oa, 0, 0);
+    if ((e = comm->allgather((char *)B::rAf[oa].p, B::rAf[oa].pitch * sizeof(T), B::lo(oa, rk[0].q), B::R(oa),
+                             sizeof(T), st)))
+      return e;
+    if ((e = B::coarse_part(st, prof))) return e;
+    for (int o = oa - 1; o >= 0; o--) {
+      const int s_ = 1 << o;
+      STEP("jac_d", 2 * o + 1, nloc, w * (Nl[2 * o + 2] + 2 * Nl[2 * o + 1]));
+      for (int i = 0; i < nloc; i++) {
+        const D2<T> &vc = (o + 1 < oa) ? fl[i].vA[o + 1] : B::vAf[oa];
+        if ((e = fast2_jac_d<T>(vc, fl[i].rD[o], fl[i].vD[o], M[o], cD[o], st, win(rk[i].q, waD[o], 2 * s_, M[o] / 2))))
+          return e;
+      }
+      if (o >= 1) {
+        STEP("jac_a", 2 * o, nloc, w * (Nl[2 * o + 1] + 2 * Nl[2 * o]));
+        for (int i = 0; i < nloc; i++)
+          if ((e = fast2_jac_a<T>(fl[i].vD[o], fl[i].rA[o], fl[i].vA[o], M[o], cA[o], st,
+                                  win(rk[i].q, waA[o], s_, M[o]))))
+            return e;
+      } else {
+        STEP("asc_fine", 0, nloc, w * (Nl[1] + 3 * Nl[0]));
+        for (int i = 0; i < nloc; i++)
+          if ((e = fast2_asc_fine<T>(fl[i].vD[0], fl[i].u[cur].p, fe(i), pitch, fl[i].u[cur ^ 1].p, M[0],
+                                     s->cfg.order, cA[0], coef, st, win(rk[i].q, 0, 1, M[0]))))
+            return e;
+      }
+    }
+    return cudaSuccess;
+  }
+
+  int launches_per_cycle() const override {
+    if (!ca) return B::launches_per_cycle();
+    int c = nloc;   // desc_fine
+    for (int o = 0; o < oa; o++) c += ((o >= 1) + 1) * nloc;
+    c += B::coarse_launches();
+    for (int o = oa - 1; o >= 0; o--) c += 2 * nloc;
+    return c;
+  }
+
+  // the caller's rows [lo, hi) of rank i: full arrays (loopback) or the slab (row 2 = lo)
+  T *caller_row0(void *a, int i) const {
+    return loop ? (T *)a : (T *)a - (int64_t)(B::lo(0, rk[i].q) - 2) * pitch;
+  }
+
+  int run_graph(mg_solver *sv, int cur) {
+    cudaStream_t st = sv->st;
+    if (loop) {   // virtual ranks: direct launches (no NCCL inside)
+      cudaError_t e = cycle_ca(cur, st, nullptr);
+      if (e) return fail(sv, MG_ECUDA, std::string("slab cycle: ") + cudaGetErrorString(e));
+      return MG_OK;
+    }
+    if (!gexec[cur]) {
+      cudaGraph_t g = nullptr;
+      CKS(sv, cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+      cudaError_t e = cycle_ca(cur, st, nullptr);
+      cudaError_t e2 = cudaStreamEndCapture(st, &g);
+      if (e || e2) {
+        if (g) cudaGraphDestroy(g);
+        TransportStatus ts;
+        ts.note(e ? e : e2, comm.get(), "slab cycle capture");
+        std::string m;
+        const int code = ts.take(&m, nullptr);
+        return fail(sv, code, m);
+      }
+      e = cudaGraphInstantiate(&gexec[cur], g, 0);
+      cudaGraphDestroy(g);
+      CKS(sv, e);
+    }
+    CKS(sv, cudaGraphLaunch(gexec[cur], st));
+    return MG_OK;
+  }
+
+  int vcycle_all(mg_solver *sv, void *u, const void *f, int ncycles, double *res_hist) override {
+    if (!ca) return B::vcycle_all(sv, u, f, ncycles, res_hist);
+    cudaStream_t st = sv->st;
+    const size_t pb = pitch * sizeof(T);
+    // caller rows in, then the deep halos of u and f (once per call)
+    for (int i = 0; i < nloc; i++) {
+      const int l = B::lo(0, rk[i].q), h = B::hi(0, rk[i].q);
+      CKS(sv, cudaMemcpyAsync(fl[i].u[0].p + (int64_t)l * pitch, caller_row0(u, i) + (int64_t)l * pitch, (h - l) * pb,
+                              cudaMemcpyDeviceToDevice, st));
+      CKS(sv, cudaMemcpyAsync(fl[i].f.p + (int64_t)l * pitch, caller_row0(const_cast<void *>(f), i) + (int64_t)l * pitch,
+                              (h - l) * pb, cudaMemcpyDeviceToDevice, st));
+    }
+    {
+      TransportStatus ts;
+      ts.note(B::xchg(0, false, Gu, st, [&](int i) { return fl[i].f.p; }, pitch), comm.get(), "halo exchange of f");
+      std::string m;
+      if (int code = ts.take(&m, nullptr)) return fail(sv, code, m);
+    }
+    if (s->cfg.order == 4)
+      for (int i = 0; i < nloc; i++)   // f~ on the band the finest descent reads (f known on Gu rows)
+        launch2_ftilde_rows<T>(D2<const T>{fl[i].f.p, pitch}, fl[i].ft, M[0],
+                               std::max(1, B::lo(0, rk[i].q) - Gu + 1), std::min(M[0], B::hi(0, rk[i].q) + Gu - 1), st);
+    const int nslots = ncycles + 1;
+    CKS(sv, cudaMemsetAsync(sv->d_hist, 0, sizeof(unsigned long long) * nslots, st));
+    CKS(sv, cudaMemsetAsync(sv->d_counter, 0, sizeof(int), st));
+    int cur = 0;
+    for (int c = 0; c < ncycles; c++) {
+      int rc = run_graph(sv, cur);
+      if (rc) return rc;
+      cur ^= 1;
+    }
+    if (res_hist) {   // ||f - L u||_inf after the last cycle: the finest descent on the own rows
+      TransportStatus ts;
+      ts.note(B::xchg(0, false, 2, st, [&](int i) { return fl[i].u[cur].p; }, pitch), comm.get(), "halo exchange");
+      for (int i = 0; i < nloc; i++)
+        ts.note(fast2_desc_fine<T>(fl[i].u[cur].p, fe(i), pitch, fl[i].rD[0], M[0], s->cfg.order, B::coef, B::sink(),
+                                   st, win(rk[i].q, 0, 1, M[0])),
+                nullptr, "final residual");
+      ts.note(B::reduce_hist(sv->d_hist, nslots, st), comm.get(), "norm all-reduce");
+      std::string m;
+      if (int code = ts.take(&m, nullptr)) return fail(sv, code, m);
+    }
+    for (int i = 0; i < nloc; i++) {
+      const int l = B::lo(0, rk[i].q), h = B::hi(0, rk[i].q);
+      CKS(sv, cudaMemcpyAsync(caller_row0(u, i) + (int64_t)l * pitch, fl[i].u[cur].p + (int64_t)l * pitch, (h - l) * pb,
+                              cudaMemcpyDeviceToDevice, st));
+    }
+    CKS(sv, cudaGetLastError());
+    if (res_hist) {
+      CKS(sv, cudaMemcpyAsync(sv->h_hist, sv->d_hist, sizeof(unsigned long long) * nslots, cudaMemcpyDeviceToHost, st));
+      CKS(sv, cudaStreamSynchronize(st));
+      bool finite = true;
+      for (int i = 0; i <= ncycles; i++) {
+        double v;
+        unsigned long long bb = sv->h_hist[i];
+        std::memcpy(&v, &bb, sizeof v);
+        res_hist[i] = v;
+        if (!std::isfinite(v)) finite = false;
+      }
+      if (!finite) return fail(sv, MG_EDIVERGED, "non-finite residual norm");
+    }
+    return MG_OK;
+  }
+};
+
 // factory used by mg_create_ex
 ImplBase *make_dist2(mg_solver *s, bool loopback, std::string *err) {
   Comm2 *c = loopback ? make_loop_comm(s->cfg.nranks)
                       : make_nccl_comm(s->cfg.nranks, s->cfg.rank, s->cfg.nccl_id, s->esz, err);
   if (!c) return nullptr;
   if (s->cfg.dtype == MG_F64) {
-    auto *d = new Dist2<double>(s, loopback);
+    auto *d = new Dist2CA<double>(s, loopback);
     d->comm.reset(c);
     return d;
   }
-  auto *d = new Dist2<float>(s, loopback);
+  auto *d = new Dist2CA<float>(s, loopback);
   d->comm.reset(c);
   return d;
 }

@@ -63,9 +63,9 @@ struct Impl2 : ImplBase {
       int64_t H = M[o] / 2 + 1, ph = pitch_for(H);
       for (auto *lv : {&rD, &vD}) {
         void *e, *oo;
-        cudaError_t st = dalloc(&e, sizeof(T) * H * ph);
+        cudaError_t st = dalloc2d(&e, sizeof(T), H, ph, H);
         if (st) return st;
-        st = dalloc(&oo, sizeof(T) * H * ph);
+        st = dalloc2d(&oo, sizeof(T), H, ph, H);
         if (st) return st;
         (*lv)[o] = S2<T>{(T *)e, (T *)oo, ph};
       }
@@ -74,7 +74,7 @@ struct Impl2 : ImplBase {
       int64_t W = M[o] + 1, pa = pitch_for(W);
       for (auto *lv : {&rA, &vA}) {
         void *q;
-        cudaError_t st = dalloc(&q, sizeof(T) * W * pa);
+        cudaError_t st = dalloc2d(&q, sizeof(T), W, pa, W);
         if (st) return st;
         (*lv)[o] = D2<T>{(T *)q, pa};
       }
@@ -376,7 +376,7 @@ struct Impl3 : ImplBase {
     out.plane = ph * H;
     for (int par : parities) {
       void *q;
-      cudaError_t st = dalloc(&q, sizeof(T) * H * H * ph);
+      cudaError_t st = dalloc2d(&q, sizeof(T), H, ph, H * H);
       if (st) return st;
       out.s[par] = (T *)q;
     }
@@ -418,7 +418,7 @@ struct Impl3 : ImplBase {
       int64_t W = M[o] + 1, pa = pitch_for(W);
       for (auto *lv : {&rG, &vG}) {
         void *q;
-        cudaError_t st = dalloc(&q, sizeof(T) * W * W * pa);
+        cudaError_t st = dalloc2d(&q, sizeof(T), W, pa, W * W);
         if (st) return st;
         (*lv)[o] = D3<T>{(T *)q, pa, pa * W};
       }
@@ -899,6 +899,14 @@ int mg_destroy(mg_solver *s) {
   DeviceGuard g(s->device);
   if (s->st) cudaStreamSynchronize(s->st);
   drop_graphs(s);
+  int rc = MG_OK;
+  if (s->impl && ImplBase::poison()) {
+    const int bad = s->impl->check_guards();
+    if (bad) {
+      fprintf(stderr, "[libmg] MG_POISON: guard bytes of %d level arrays overwritten\n", bad);
+      rc = MG_ECUDA;
+    }
+  }
   cudaFree(s->d_ualt);
   if (s->impl) s->impl->free_all();
   cudaFree(s->d_hist);
@@ -914,7 +922,7 @@ int mg_destroy(mg_solver *s) {
   if (s->ev_out) cudaEventDestroy(s->ev_out);
   if (s->st) cudaStreamDestroy(s->st);
   delete s;
-  return MG_OK;
+  return rc;
 }
 
 int mg_local_extent(const mg_solver *s, int64_t *lo, int64_t *hi, int64_t *ghost) {

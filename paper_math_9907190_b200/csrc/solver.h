@@ -159,6 +159,51 @@ struct ImplBase {
     bytes += n;
     return cudaMemset(*p, 0, n);
   }
+  // A pitched level array of `rows` rows of `width` elements (zeroed).  With
+  // MG_POISON=1 (a bounds check of our own: compute-sanitizer is not available
+  // on the B200 pool) the array gets one guard row above and below and its
+  // pitch padding [width, pitch), all filled with 0xFF bytes (a NaN in fp32 and
+  // fp64): a read outside the level's extent turns the iterate into NaN (the
+  // oracle comparisons fail), a write there is found by check_guards().
+  struct Guard {
+    char *base;
+    size_t rowb, wb;
+    int64_t rows;
+  };
+  std::vector<Guard> guards;
+  static bool poison() {
+    static const bool p = env_flag("MG_POISON");
+    return p;
+  }
+  cudaError_t dalloc2d(void **p, size_t esz, int64_t width, int64_t pitch, int64_t rows) {
+    if (!poison()) return dalloc(p, esz * pitch * rows);
+    void *base;
+    const size_t rowb = esz * pitch, wb = esz * width;
+    cudaError_t e = dalloc(&base, rowb * (rows + 2));
+    if (e) return e;
+    char *b = (char *)base;
+    if ((e = cudaMemset(b, 0xFF, rowb)) || (e = cudaMemset(b + rowb * (rows + 1), 0xFF, rowb))) return e;
+    if (rowb > wb && (e = cudaMemset2D(b + rowb + wb, rowb, 0xFF, rowb - wb, rows))) return e;
+    guards.push_back(Guard{b, rowb, wb, rows});
+    if (guards.size() == 1 && env_flag("MG_POISON_SELFTEST") && (e = cudaMemset(b + rowb + wb, 0, 1)))
+      return e;   // tests/test_gpu_paths.py: a planted stray write must be reported
+    *p = b + rowb;
+    return cudaSuccess;
+  }
+  // number of poisoned arrays whose guard bytes were overwritten (synchronises)
+  int check_guards() {
+    int bad = 0;
+    for (const Guard &g : guards) {
+      std::vector<unsigned char> h(g.rowb * (g.rows + 2));
+      if (cudaMemcpy(h.data(), g.base, h.size(), cudaMemcpyDeviceToHost) != cudaSuccess) return -1;
+      bool ok = true;
+      for (size_t i = 0; i < g.rowb && ok; i++) ok = h[i] == 0xFF && h[g.rowb * (g.rows + 1) + i] == 0xFF;
+      for (int64_t r = 1; r <= g.rows && ok; r++)
+        for (size_t i = g.wb; i < g.rowb && ok; i++) ok = h[g.rowb * r + i] == 0xFF;
+      bad += !ok;
+    }
+    return bad;
+  }
   void free_all() {
     for (void *p : bufs) cudaFree(p);
     bufs.clear();

@@ -130,8 +130,8 @@ def mg_create_ex(cfg: mg_config):
     return h
 
 
-def mg_destroy(h) -> None:
-    load().mg_destroy(h)
+def mg_destroy(h) -> int:
+    return load().mg_destroy(h)
 
 
 def mg_local_extent(h):

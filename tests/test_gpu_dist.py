@@ -94,3 +94,34 @@ def test_residual_and_norm_on_loopback_3d():
     r4 = s4.view(s4.residual(s4.alloc(u), s4.alloc(f))).cpu().numpy()
     assert np.array_equal(r1, r4)
     torch.cuda.synchronize()
+
+
+# ------------------------------------- 2D communication-avoiding schedule
+
+@pytest.mark.parametrize("dtype", [np.float64, np.float32], ids=["f64", "f32"])
+@pytest.mark.parametrize("n,P,agglom", [(1025, 2, 1 << 14), (1025, 4, 1 << 12), (2049, 4, 1 << 14),
+                                        (2049, 8, 1 << 10), (513, 2, 0)])
+def test_loopback_deep_halo_equals_single_gpu(n, P, agglom, dtype):
+    """The one-exchange-per-cycle schedule (Dist2CA: deep ghost bands computed
+    redundantly) and the per-level schedule (MG_DIST_PERLEVEL=1)
+    both equal the single-GPU iterate and residual history bit for bit, with
+    agglomeration thresholds that distribute 1 to 6 octaves."""
+    import os
+    ref, href = _run(n, 2, dtype, 4)
+    for per_level in ("0", "1"):
+        os.environ["MG_DIST_PERLEVEL"] = per_level
+        try:
+            got, h = _run(n, 2, dtype, 4, nranks=P, loopback=True, agglom=agglom)
+        finally:
+            os.environ.pop("MG_DIST_PERLEVEL", None)
+        assert np.array_equal(got, ref), (per_level, float(np.max(np.abs(got - ref))))
+        assert np.array_equal(h, href)
+
+
+@pytest.mark.parametrize("n,P", [(1025, 4), (513, 2)])
+def test_loopback_deep_halo_order4(n, P):
+    for cycles in (1, 3):
+        ref, href = _run(n, 4, np.float64, cycles)
+        got, h = _run(n, 4, np.float64, cycles, nranks=P, loopback=True, agglom=1 << 12)
+        assert np.array_equal(got, ref)
+        assert np.array_equal(h, href)

@@ -38,8 +38,12 @@ h = s.vcycle(u, ft, 3, hist=True)
 ug = s.view(u).cpu().numpy()
 uo = u0.copy()
 ho = oracle.vcycle(uo, f, p, 3, order=order, hist=True)
+from paper_math_9907190_b200 import mg as MG
+rc = MG.load().mg_destroy(s.h)   # MG_POISON: nonzero if a guard band was overwritten
+s.h = None
 print(json.dumps({{"bitwise": bool(np.array_equal(ug, uo)), "hist": bool(np.array_equal(h, ho)),
-                  "rel": float(np.max(np.abs(ug.astype(np.float64) - uo)) / np.max(np.abs(uo)))}}))
+                  "rel": float(np.max(np.abs(ug.astype(np.float64) - uo)) / np.max(np.abs(uo))),
+                  "destroy_rc": int(rc)}}))
 """
 
 CASES = [
@@ -82,6 +86,20 @@ CASES = [
     ({"MG_K3_NW": "16"}, 3, 129, 2, "float64"),
     ({"MG_K3S_NW": "16"}, 3, 129, 2, "float64"),
     ({"MG_K3S_NW": "8"}, 3, 257, 2, "float64"),
+    # bounds checks of our own (compute-sanitizer is closed on the B200 pool): level arrays with
+    # poisoned (NaN) guard rows and pitch padding; a stray read makes the iterate NaN, a stray
+    # write trips the guard check in mg_destroy
+    ({"MG_POISON": "1"}, 2, 257, 2, "float64"),
+    ({"MG_POISON": "1"}, 2, 257, 4, "float64"),
+    ({"MG_POISON": "1"}, 2, 513, 2, "float32"),
+    ({"MG_POISON": "1"}, 2, 129, 4, "float32"),
+    ({"MG_POISON": "1"}, 3, 129, 2, "float64"),
+    ({"MG_POISON": "1"}, 3, 65, 4, "float64"),
+    ({"MG_POISON": "1"}, 3, 65, 2, "float32"),
+    ({"MG_POISON": "1", "MG_FORCE_REF": "1"}, 2, 65, 2, "float64"),
+    ({"MG_POISON": "1", "MG_FORCE_REF": "1"}, 3, 33, 2, "float64"),
+    ({"MG_POISON": "1", "MG_K3_FUSE": "1"}, 3, 129, 2, "float64"),
+    ({"MG_POISON": "1", "MG_2D_NOXFUSE": "1", "MG_2D_NOADFUSE": "1", "MG_2D_NODAFUSE": "1"}, 2, 257, 2, "float64"),
 ]
 
 
@@ -97,3 +115,16 @@ def test_path_is_bit_identical(env, dim, n, order, dtype):
     res = json.loads(out.stdout.strip().splitlines()[-1])
     assert res["bitwise"], res
     assert res["hist"], res
+    assert res["destroy_rc"] == 0, res
+
+
+def test_poison_guard_check_has_teeth():
+    """MG_POISON_SELFTEST plants one stray byte in the pitch padding of the
+    first level array: mg_destroy must report it (the guard check is live)."""
+    code = CHILD.format(root=ROOT, dim=2, n=65, order=2, dtype="float64")
+    env = dict(os.environ, MG_POISON="1", MG_POISON_SELFTEST="1")
+    out = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stderr[-2000:]
+    res = json.loads(out.stdout.strip().splitlines()[-1])
+    assert res["bitwise"] and res["destroy_rc"] != 0, res
+    assert "guard bytes" in out.stderr
