@@ -443,7 +443,7 @@ struct Dist2 : ImplBase {
 // band w needs v_A(2s) on w + 2s and r_D(s) on w + s; an A(s) band w needs
 // v_D(s) on w + 2s and r_A(s) on w + s; the descent's bands cover both the
 // ascent's r needs and the next restriction's reach (+s per step).  At 8193^2
-// over 8 ranks Gu = 76 fine rows (1024 owned).  The node formulas are those of
+// over 8 ranks (agglomeration at A(16)) Gu = 108 fine rows (1024 owned).  The node formulas are those of
 // the single-GPU kernels (the same kernels, on row windows), so the iterate is
 // bit-identical to the single-GPU solver (tests/test_gpu_dist.py).
 // Used when Gu fits in one neighbour's slab (Gu <= rows per rank); otherwise
@@ -485,14 +485,16 @@ struct Dist2CA : Dist2<T> {
     waD.assign(oa, 0);
     waA.assign(oa + 1, 0);
     std::vector<int> rDneed(oa, 0), rAneed(oa + 1, 0);
+    // bands are whole rows of their level: D(s) half rows (2s fine rows), A(s)
+    // rows in pairs (2s; the A-level tiles start on even rows)
     int reqD = 2;   // the finest ascent (A(1), own rows) reads v_D(1) within 2 rows
     for (int o = 0; o < oa; o++) {
       const int s_ = 1 << o;
-      waD[o] = up(reqD, 4 * s_);
+      waD[o] = up(reqD, 2 * s_);
       rDneed[o] = waD[o] + s_;
       const int reqA = waD[o] + 2 * s_;
       if (o + 1 < oa) {
-        waA[o + 1] = up(reqA, 8 * s_);
+        waA[o + 1] = up(reqA, 4 * s_);
         rAneed[o + 1] = waA[o + 1] + 2 * s_;
         reqD = waA[o + 1] + 4 * s_;
       }
@@ -500,8 +502,8 @@ struct Dist2CA : Dist2<T> {
     WA[oa] = 0;   // the agglomeration level: own rows (all-gathered)
     for (int o = oa - 1; o >= 0; o--) {
       const int s_ = 1 << o;
-      WD[o] = up(std::max(rDneed[o], WA[o + 1] + s_), 4 * s_);
-      if (o >= 1) WA[o] = up(std::max(rAneed[o], WD[o] + s_), 4 * s_);
+      WD[o] = up(std::max(rDneed[o], WA[o + 1] + s_), 2 * s_);
+      if (o >= 1) WA[o] = up(std::max(rAneed[o], WD[o] + s_), 2 * s_);
     }
     Gu = up(WD[0] + 2, 2);
   }
@@ -631,13 +633,10 @@ struct Dist2CA : Dist2<T> {
     return loop ? (T *)a : (T *)a - (int64_t)(B::lo(0, rk[i].q) - 2) * pitch;
   }
 
+  // one cycle, captured once per parity into a CUDA graph (NCCL calls and the
+  // loopback copies are capturable) and replayed
   int run_graph(mg_solver *sv, int cur) {
     cudaStream_t st = sv->st;
-    if (loop) {   // virtual ranks: direct launches (no NCCL inside)
-      cudaError_t e = cycle_ca(cur, st, nullptr);
-      if (e) return fail(sv, MG_ECUDA, std::string("slab cycle: ") + cudaGetErrorString(e));
-      return MG_OK;
-    }
     if (!gexec[cur]) {
       cudaGraph_t g = nullptr;
       CKS(sv, cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
