@@ -144,6 +144,16 @@ int mg_residual(mg_solver *s, const void *u, const void *f, void *r);
  * calls) and returns MG_EDIVERGED if any entry is not finite. */
 int mg_vcycle(mg_solver *s, void *u, const void *f, int ncycles, double *res_hist);
 
+/* mg_vcycle with both residual histories of SURVEY 8(a) a16:
+ * res_inf as mg_vcycle's res_hist (required when res_l2 is set), and res_l2
+ * (NULL, or ncycles+1 doubles) = ||f - L u||_{2,h} = (h^d sum r^2)^(1/2) over
+ * the interior nodes before every cycle and after the last.  Both are fused
+ * into the passes that form the finest residual (no extra pass over u, f);
+ * the L2 sums are accumulated in double, in an order that depends on the
+ * launch geometry (equal to a serial sum to rounding).  Synchronises when
+ * res_inf is set; errors as mg_vcycle. */
+int mg_vcycle_norms(mg_solver *s, void *u, const void *f, int ncycles, double *res_inf, double *res_l2);
+
 /* Same as mg_vcycle on HOST arrays (pitch as configured): copies u and f to
  * the device, runs the cycles, copies u back.  Synchronises.  Pinned host
  * memory makes the copies asynchronous DMA. */

@@ -78,10 +78,17 @@ struct Coef {
 
 // Residual-norm sink: max |r| as the bit pattern of a non-negative double
 // (monotone in the value; NaN sorts above +inf so it is never lost).
+// Sum of squares (the L2 norm: ||r||_{2,h} = (h^d sum r^2)^(1/2))
+// into l2[slot] when l2 is set: every node is counted once, by the pass that
+// owns it, and only on rows (3D: planes) [nlo, nhi) of the fine grid (a slab
+// solver's own rows; the ghost bands it also computes are another rank's).
 struct NormSink {
   unsigned long long *slots;   // per-cycle maxima
   int *counter;                // which slot the current cycle writes
   int cap;
+  double *l2 = nullptr;        // per-cycle sums of r^2 (or null)
+  int nlo = 0, nhi = 1 << 30;  // fine rows / planes whose r^2 this launch adds
+  __device__ __forceinline__ bool sums(int y) const { return l2 != nullptr && y >= nlo && y < nhi; }
 };
 
 __device__ __forceinline__ void norm_push(const NormSink &ns, double v) {
@@ -90,6 +97,13 @@ __device__ __forceinline__ void norm_push(const NormSink &ns, double v) {
   if (slot >= ns.cap) slot = ns.cap - 1;
   atomicMax(ns.slots + slot, (unsigned long long)__double_as_longlong(v));
 }
+__device__ __forceinline__ void norm_push_l2(const NormSink &ns, double ss) {
+  if (ns.l2 == nullptr || ns.slots == nullptr) return;
+  int slot = *ns.counter;
+  if (slot >= ns.cap) slot = ns.cap - 1;
+  atomicAdd(ns.l2 + slot, ss);
+}
+__device__ __forceinline__ double sq(double v) { return v * v; }
 
 // max that propagates NaN (a diverged residual must not be hidden).
 __device__ __forceinline__ double nmax(double a, double b) { return (b > a || b != b) ? b : a; }
@@ -99,10 +113,20 @@ __device__ __forceinline__ double absd(T v) {
   return fabs((double)v);
 }
 
-// Block-wide max reduction then one atomic per block.
+// Warp-wide sum of squares, one atomic per warp (lane 0).
+__device__ __forceinline__ void warp_l2_push(const NormSink &ns, double ss) {
+  if (ns.l2 == nullptr) return;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+  if ((threadIdx.x & 31) == 0) norm_push_l2(ns, ss);
+}
+
+// Block-wide max reduction then one atomic per block (and the sum of squares,
+// one atomic per warp, when ns.l2 is set).
 template <int NT>
-__device__ __forceinline__ void block_norm_push(const NormSink &ns, double v) {
+__device__ __forceinline__ void block_norm_push(const NormSink &ns, double v, double ss = 0.0) {
   if (ns.slots == nullptr) return;
+  warp_l2_push(ns, ss);
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
     double w = __shfl_xor_sync(0xffffffffu, v, o);

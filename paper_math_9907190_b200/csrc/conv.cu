@@ -213,13 +213,15 @@ __global__ void k_coarsest(T *v, const T *r, int64_t off, T c, T inv, int *count
 // max |r| over the interior to this cycle's residual-history slot
 template <class T, int DIM>
 __global__ void k_norm_push(const T *r, int64_t pitch, int64_t plane, int M, NormSink ns) {
-  double mx = 0.0;
+  double mx = 0.0, ss = 0.0;
   const int64_t W = M - 1, cnt = DIM == 2 ? W * W : W * W * W;
   for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < cnt; t += (int64_t)gridDim.x * blockDim.x) {
     const int64_t x = t % W + 1, y = (t / W) % W + 1, z = DIM == 2 ? 0 : t / (W * W) + 1;
-    mx = nmax(mx, absd(r[z * plane + y * pitch + x]));
+    const T v = r[z * plane + y * pitch + x];
+    mx = nmax(mx, absd(v));
+    if (ns.sums(DIM == 2 ? (int)y : (int)z)) ss += sq((double)v);
   }
-  block_norm_push<256>(ns, mx);
+  block_norm_push<256>(ns, mx, ss);
 }
 
 template <class T, int DIM>
@@ -263,7 +265,7 @@ struct ImplConv : ImplBase {
     coef.c6 = (T)((double)(n - 1) * (double)(n - 1) / 6.0);
     return cudaSuccess;
   }
-  NormSink sink() const { return NormSink{s->d_hist, s->d_counter, kHistCap}; }
+  NormSink sink() const { return NormSink{s->d_hist, s->d_counter, kHistCap, s->sum_l2 ? s->d_l2 : nullptr}; }
   dim3 grid(int cnt, int nz = 1) const { return dim3((cnt + BX - 1) / BX, (cnt + BY - 1) / BY, nz); }
 
   template <class U>

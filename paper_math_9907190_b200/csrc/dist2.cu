@@ -153,7 +153,7 @@ struct Dist2 : ImplBase {
     return cudaMemcpy(d_lev, lv.data(), sizeof(Lev2<T>) * k, cudaMemcpyHostToDevice);
   }
 
-  NormSink sink() const { return NormSink{s->d_hist, s->d_counter, kHistCap}; }
+  NormSink sink() const { return NormSink{s->d_hist, s->d_counter, kHistCap, s->sum_l2 ? s->d_l2 : nullptr}; }
   size_t local_elems() const override { return loop ? 0 : (size_t)(R(0) + 4) * pitch; }
   bool extent(int64_t *l, int64_t *h, int64_t *g) const override {
     if (loop) return false;
@@ -325,7 +325,8 @@ struct Dist2 : ImplBase {
     fast2_desc_fine<T>(ui, fe, pitch, rk[0].rD[0], M[0], s->cfg.order, coef, sink(), st, rows_full(0, rk[0].q));
   }
   cudaError_t reduce_hist(unsigned long long *d, int nslots, cudaStream_t st) override {
-    return comm->allreduce_max_u64(d, nslots, st);
+    cudaError_t e = comm->allreduce_max_u64(d, nslots, st);
+    return e ? e : comm->allreduce_sum_f64(s->d_l2, nslots, st);
   }
   // f~ (order 4) on the slab: f's ghost row first, then the own rows
   void enqueue_ftilde(const void *f, void *ft, cudaStream_t st, int64_t) override {
@@ -386,7 +387,7 @@ struct Dist2 : ImplBase {
                       st);
     }
     int nslots = ncycles + 1 < kHistCap ? ncycles + 1 : kHistCap;
-    cudaMemsetAsync(sv->d_hist, 0, sizeof(unsigned long long) * nslots, st);
+    clear_hist(sv, nslots, st);
     cudaMemsetAsync(sv->d_counter, 0, sizeof(int), st);
     std::vector<const T *> fe(nloc);
     for (int i = 0; i < nloc; i++) fe[i] = rk[i].f.p;
@@ -415,19 +416,7 @@ struct Dist2 : ImplBase {
       cudaMemcpyAsync((T *)u + (int64_t)lo(0, i) * pitch, rk[i].u[cur].p + (int64_t)lo(0, i) * pitch, R(0) * pb,
                       cudaMemcpyDeviceToDevice, st);
     CKS(sv, cudaGetLastError());
-    if (res_hist) {
-      CKS(sv, cudaMemcpyAsync(sv->h_hist, sv->d_hist, sizeof(unsigned long long) * nslots, cudaMemcpyDeviceToHost, st));
-      CKS(sv, cudaStreamSynchronize(st));
-      bool finite = true;
-      for (int i = 0; i <= ncycles; i++) {
-        double v;
-        unsigned long long bb = sv->h_hist[i < kHistCap ? i : kHistCap - 1];
-        std::memcpy(&v, &bb, sizeof v);
-        res_hist[i] = v;
-        if (!std::isfinite(v)) finite = false;
-      }
-      if (!finite) return fail(sv, MG_EDIVERGED, "non-finite residual norm");
-    }
+    if (res_hist) return read_hist(sv, ncycles, res_hist, st);
     return MG_OK;
   }
 };
@@ -470,12 +459,13 @@ struct Dist2CA : Dist2<T> {
     std::vector<D2<T>> rA, vA;   // 1 <= o < oa
   };
   std::vector<Full> fl;   // per local rank
-  cudaGraphExec_t gexec[2] = {nullptr, nullptr};   // NCCL mode: the cycle u[p] -> u[p^1]
+  cudaGraphExec_t gexec[2][2] = {};   // the cycle u[p] -> u[p^1], [p][L2 sums on]
 
   Dist2CA(mg_solver *sv, bool loopback) : B(sv, loopback) {}
   ~Dist2CA() override {
-    for (auto &g : gexec)
-      if (g) cudaGraphExecDestroy(g);
+    for (auto &gp : gexec)
+      for (auto &g : gp)
+        if (g) cudaGraphExecDestroy(g);
   }
 
   static int up(int v, int m) { return (v + m - 1) / m * m; }
@@ -559,6 +549,14 @@ struct Dist2CA : Dist2<T> {
     return r;
   }
   const T *fe(int i) const { return s->cfg.order == 4 ? fl[i].ft.p : fl[i].f.p; }
+  // the residual-norm sink of rank q: the L2 sum counts its own rows only (the
+  // ghost bands' residuals are the neighbours' own rows)
+  NormSink own_sink(int q) const {
+    NormSink ns = B::sink();
+    ns.nlo = B::lo(0, q);
+    ns.nhi = B::hi(0, q);
+    return ns;
+  }
 
   // one V-cycle on the internal arrays, u[cur] -> u[cur ^ 1]
   cudaError_t cycle_ca(int cur, cudaStream_t st, Prof *prof) {
@@ -572,8 +570,8 @@ struct Dist2CA : Dist2<T> {
     if ((e = B::xchg(0, false, Gu, st, [&](int i) { return fl[i].u[cur].p; }, pitch))) return e;
     STEP("desc_fine", 0, nloc, w * (2 * Nl[0] + Nl[1]));
     for (int i = 0; i < nloc; i++)
-      if ((e = fast2_desc_fine<T>(fl[i].u[cur].p, fe(i), pitch, fl[i].rD[0], M[0], s->cfg.order, coef, B::sink(), st,
-                                  win(rk[i].q, WD[0], 1, M[0]))))
+      if ((e = fast2_desc_fine<T>(fl[i].u[cur].p, fe(i), pitch, fl[i].rD[0], M[0], s->cfg.order, coef,
+                                  own_sink(rk[i].q), st, win(rk[i].q, WD[0], 1, M[0]))))
         return e;
     for (int o = 0; o < oa; o++) {
       const int s_ = 1 << o;
@@ -637,7 +635,8 @@ struct Dist2CA : Dist2<T> {
   // loopback copies are capturable) and replayed
   int run_graph(mg_solver *sv, int cur) {
     cudaStream_t st = sv->st;
-    if (!gexec[cur]) {
+    cudaGraphExec_t &gx = gexec[cur][s->sum_l2 ? 1 : 0];
+    if (!gx) {
       cudaGraph_t g = nullptr;
       CKS(sv, cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
       cudaError_t e = cycle_ca(cur, st, nullptr);
@@ -650,11 +649,11 @@ struct Dist2CA : Dist2<T> {
         const int code = ts.take(&m, nullptr);
         return fail(sv, code, m);
       }
-      e = cudaGraphInstantiate(&gexec[cur], g, 0);
+      e = cudaGraphInstantiate(&gx, g, 0);
       cudaGraphDestroy(g);
       CKS(sv, e);
     }
-    CKS(sv, cudaGraphLaunch(gexec[cur], st));
+    CKS(sv, cudaGraphLaunch(gx, st));
     return MG_OK;
   }
 
@@ -681,7 +680,7 @@ struct Dist2CA : Dist2<T> {
         launch2_ftilde_rows<T>(D2<const T>{fl[i].f.p, pitch}, fl[i].ft, M[0],
                                std::max(1, B::lo(0, rk[i].q) - Gu + 1), std::min(M[0], B::hi(0, rk[i].q) + Gu - 1), st);
     const int nslots = ncycles + 1;
-    CKS(sv, cudaMemsetAsync(sv->d_hist, 0, sizeof(unsigned long long) * nslots, st));
+    CKS(sv, clear_hist(sv, nslots, st));
     CKS(sv, cudaMemsetAsync(sv->d_counter, 0, sizeof(int), st));
     int cur = 0;
     for (int c = 0; c < ncycles; c++) {
@@ -693,8 +692,8 @@ struct Dist2CA : Dist2<T> {
       TransportStatus ts;
       ts.note(B::xchg(0, false, 2, st, [&](int i) { return fl[i].u[cur].p; }, pitch), comm.get(), "halo exchange");
       for (int i = 0; i < nloc; i++)
-        ts.note(fast2_desc_fine<T>(fl[i].u[cur].p, fe(i), pitch, fl[i].rD[0], M[0], s->cfg.order, B::coef, B::sink(),
-                                   st, win(rk[i].q, 0, 1, M[0])),
+        ts.note(fast2_desc_fine<T>(fl[i].u[cur].p, fe(i), pitch, fl[i].rD[0], M[0], s->cfg.order, B::coef,
+                                   own_sink(rk[i].q), st, win(rk[i].q, 0, 1, M[0])),
                 nullptr, "final residual");
       ts.note(B::reduce_hist(sv->d_hist, nslots, st), comm.get(), "norm all-reduce");
       std::string m;
@@ -706,19 +705,7 @@ struct Dist2CA : Dist2<T> {
                               cudaMemcpyDeviceToDevice, st));
     }
     CKS(sv, cudaGetLastError());
-    if (res_hist) {
-      CKS(sv, cudaMemcpyAsync(sv->h_hist, sv->d_hist, sizeof(unsigned long long) * nslots, cudaMemcpyDeviceToHost, st));
-      CKS(sv, cudaStreamSynchronize(st));
-      bool finite = true;
-      for (int i = 0; i <= ncycles; i++) {
-        double v;
-        unsigned long long bb = sv->h_hist[i];
-        std::memcpy(&v, &bb, sizeof v);
-        res_hist[i] = v;
-        if (!std::isfinite(v)) finite = false;
-      }
-      if (!finite) return fail(sv, MG_EDIVERGED, "non-finite residual norm");
-    }
+    if (res_hist) return read_hist(sv, ncycles, res_hist, st);
     return MG_OK;
   }
 };

@@ -176,7 +176,7 @@ struct Dist3 : ImplBase {
     return cudaMemcpy(d_lev, lv.data(), sizeof(Lev3<T>) * k, cudaMemcpyHostToDevice);
   }
 
-  NormSink sink() const { return NormSink{s->d_hist, s->d_counter, kHistCap}; }
+  NormSink sink() const { return NormSink{s->d_hist, s->d_counter, kHistCap, s->sum_l2 ? s->d_l2 : nullptr}; }
   size_t local_elems() const override { return loop ? 0 : (size_t)(R(0) + 4) * fplane(); }
   bool extent(int64_t *l, int64_t *h, int64_t *g) const override {
     if (loop) return false;
@@ -350,7 +350,8 @@ struct Dist3 : ImplBase {
     fast3_desc_fine<T>(ui, fe, pitch, rk[0].rR[0], M[0], s->cfg.order, coef, sink(), st, zr_fine(rk[0].q));
   }
   cudaError_t reduce_hist(unsigned long long *d, int nslots, cudaStream_t st) override {
-    return comm->allreduce_max_u64(d, nslots, st);
+    cudaError_t e = comm->allreduce_max_u64(d, nslots, st);
+    return e ? e : comm->allreduce_sum_f64(s->d_l2, nslots, st);
   }
   void enqueue_ftilde(const void *f, void *ft, cudaStream_t st, int64_t) override {
     if (loop) {
@@ -411,7 +412,7 @@ struct Dist3 : ImplBase {
                       cudaMemcpyDeviceToDevice, st);
     }
     int nslots = ncycles + 1 < kHistCap ? ncycles + 1 : kHistCap;
-    cudaMemsetAsync(sv->d_hist, 0, sizeof(unsigned long long) * nslots, st);
+    clear_hist(sv, nslots, st);
     cudaMemsetAsync(sv->d_counter, 0, sizeof(int), st);
     std::vector<const T *> fe(nloc);
     for (int i = 0; i < nloc; i++) fe[i] = rk[i].f.p;
@@ -440,19 +441,7 @@ struct Dist3 : ImplBase {
       cudaMemcpyAsync((T *)u + (int64_t)lo(0, i) * fplane(), rk[i].u[cur].p + (int64_t)lo(0, i) * fplane(), R(0) * pb,
                       cudaMemcpyDeviceToDevice, st);
     CKS(sv, cudaGetLastError());
-    if (res_hist) {
-      CKS(sv, cudaMemcpyAsync(sv->h_hist, sv->d_hist, sizeof(unsigned long long) * nslots, cudaMemcpyDeviceToHost, st));
-      CKS(sv, cudaStreamSynchronize(st));
-      bool finite = true;
-      for (int i = 0; i <= ncycles; i++) {
-        double v;
-        unsigned long long bb = sv->h_hist[i < kHistCap ? i : kHistCap - 1];
-        std::memcpy(&v, &bb, sizeof v);
-        res_hist[i] = v;
-        if (!std::isfinite(v)) finite = false;
-      }
-      if (!finite) return fail(sv, MG_EDIVERGED, "non-finite residual norm");
-    }
+    if (res_hist) return read_hist(sv, ncycles, res_hist, st);
     return MG_OK;
   }
 };

@@ -30,13 +30,15 @@ __global__ void __launch_bounds__(NT) k2_desc_fine_ref(D2<const T> u, D2<const T
                                                        NormSink ns) {
   int H = M / 2 + 1;
   int64_t t = (int64_t)blockIdx.x * NT + threadIdx.x;
-  double mx = 0.0;
+  double mx = 0.0, ss = 0.0;
   if (t < (int64_t)H * H) {
     int a = (int)(t % H), b = (int)(t / H);
     int x = 2 * a, y = 2 * b;
     T rc = res2z<T, ORDER>(u, f, x, y, M, k);
     T rE = res2z<T, ORDER>(u, f, x + 1, y, M, k);
     T rN = res2z<T, ORDER>(u, f, x, y + 1, M, k);
+    if (ns.sums(y)) ss += sq((double)rc) + sq((double)rE);
+    if (ns.sums(y + 1)) ss += sq((double)rN);
     if (x >= 1 && y >= 1 && x <= M - 1 && y <= M - 1) {
       T rW = res2z<T, ORDER>(u, f, x - 1, y, M, k);
       T rS = res2z<T, ORDER>(u, f, x, y - 1, M, k);
@@ -53,9 +55,10 @@ __global__ void __launch_bounds__(NT) k2_desc_fine_ref(D2<const T> u, D2<const T
       T oN = res2z<T, ORDER>(u, f, x + 1, y + 2, M, k);
       d.o[(int64_t)b * d.pitch + a] = erest2r(ro, oW, oS, oE, oN);
       mx = nmax(mx, absd(ro));
+      if (ns.sums(y + 1)) ss += sq((double)ro);
     }
   }
-  block_norm_push<NT>(ns, mx);
+  block_norm_push<NT>(ns, mx, ss);
 }
 
 // ------------------------------------------------- descent, level kernels

@@ -145,13 +145,16 @@ struct OpDesc2Fine {
     int ylo, yhi, yo, yh;   // output rows [ylo, yhi); TMA y = global y - yo (full rows) / - yh (half rows)
   };
   struct Acc {
-    double mx;
+    double mx, ss;   // max |r|, sum r^2 (a16)
   };
   static __device__ void prefetch(const Params &P) {
     tma_prefetch_desc(&P.tu);
     tma_prefetch_desc(&P.tf);
   }
-  static __device__ void init(Acc &a) { a.mx = 0.0; }
+  static __device__ void init(Acc &a) {
+    a.mx = 0.0;
+    a.ss = 0.0;
+  }
   static __device__ void issue(const Params &P, int t, unsigned char *st, uint64_t *bar) {
     int x0 = (t % P.ntx) * TX, y0 = P.ylo + (t / P.ntx) * TY;
     mbar_expect_tx(bar, U_BYTES + F_BYTES);
@@ -195,7 +198,10 @@ struct OpDesc2Fine {
     for (int y = y0 + w; y < y0 + TY; y += NW) {
       rpair(U, F, xl, y, M, P.k, r0, r1);
       st2(R.at(xl, y), r0, r1);
-      if (y < yhi) acc.mx = nmax(nmax(acc.mx, absd(r0)), absd(r1));
+      if (y < yhi) {
+        acc.mx = nmax(nmax(acc.mx, absd(r0)), absd(r1));
+        if (P.ns.sums(y)) acc.ss += sq((double)r0) + sq((double)r1);
+      }
     }
     if (w < 2) {   // ring rows
       int y = w == 0 ? y0 - 1 : y0 + TY;
@@ -221,7 +227,7 @@ struct OpDesc2Fine {
       if (xl + 1 <= M - 1 && y + 1 <= M - 1) P.out.o[o] = erest2r(ro, rN, rE, R(xl + 2, y + 1), R(xl + 1, y + 2));
     }
   }
-  static __device__ void finish(const Params &P, Acc &acc) { block_norm_push<NT>(P.ns, acc.mx); }
+  static __device__ void finish(const Params &P, Acc &acc) { block_norm_push<NT>(P.ns, acc.mx, acc.ss); }
 };
 
 // ======================================== restriction A(s) -> D(s), s > 1

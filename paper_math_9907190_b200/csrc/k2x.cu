@@ -140,6 +140,8 @@ struct Strip {
   Row<T> N[4];         // u_new
   Pair<T> R[4];        // r(u_new)
   unsigned long long mx;   // max |r| as the bit pattern of a non-negative double (NaN sorts above inf)
+  double ss;               // sum r^2 over the lane's output nodes (a16 L2 norm; single GPU: all rows)
+  bool l2on;
   // interior warps address by increments: next load row offset, next E / O
   // v_D load pointers, u_new store pointer of row j-2, next Erest2r offset
   int64_t lo, rso;
@@ -176,6 +178,8 @@ struct Strip {
       Dv[i] = G[i] = (T)0;
     }
     mx = 0ull;
+    ss = 0.0;
+    l2on = P.ns.l2 != nullptr;
   }
   // incremental addressing from step j0 on (row-interior blocks only)
   __device__ __forceinline__ void start(int j0) {
@@ -332,6 +336,7 @@ struct Strip {
     if (outl && j - 3 >= ys && j - 3 < ye) {
       const unsigned long long a = absbits(R[s3].a), b = absbits(R[s3].b), m = a > b ? a : b;
       mx = m > mx ? m : mx;
+      if (l2on) ss += sq((double)R[s3].a) + sq((double)R[s3].b);
     }
     // Erest2r of the row pair (y, y+1) = (j-5, j-4) when y is even
     if (PAR == 1) {
@@ -363,6 +368,7 @@ __global__ void __launch_bounds__(32, MINB) asc_desc_stream(const __grid_constan
   const int item = blockIdx.x;
   const int nseg = (P.M + P.seg - 1) / P.seg;
   unsigned long long mx = 0ull;
+  double ss = 0.0;
   if (item < P.nstrips * nseg) {   // warp-uniform
     const int strip = item % P.nstrips, sg = item / P.nstrips;
     const int ys = sg * P.seg, ye = min(ys + P.seg, P.M);
@@ -391,6 +397,7 @@ __global__ void __launch_bounds__(32, MINB) asc_desc_stream(const __grid_constan
     }
     for (; j <= jend; j += 4) S.template steps<true, true>(j);
     mx = S.mx;
+    ss = S.ss;
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
@@ -398,6 +405,7 @@ __global__ void __launch_bounds__(32, MINB) asc_desc_stream(const __grid_constan
     mx = w > mx ? w : mx;
   }
   if (lane == 0 && item < P.nstrips * nseg) norm_push(P.ns, __longlong_as_double((long long)mx));
+  if (item < P.nstrips * nseg) warp_l2_push(P.ns, ss);   // warp-uniform
 }
 
 
@@ -448,6 +456,8 @@ struct StripQ {
   float G0[4], G1[4];          // the two greens of the row (x+1, x+3 even rows; x, x+2 odd rows)
   Q4 R[4];
   unsigned long long mx;
+  double ss;   // sum r^2 (a16 L2 norm)
+  bool l2on;
   static constexpr int SLOT = 32 * 40, FO = 32 * 16, DO = 32 * 32;
 
   __device__ __forceinline__ StripQ(const XParamsQ &P, int x_, int ys_, int ye_, unsigned char *ring_) {
@@ -468,6 +478,8 @@ struct StripQ {
       Nw[i] = Ne[i] = D0[i] = D1[i] = G0[i] = G1[i] = 0.f;
     }
     mx = 0ull;
+    ss = 0.0;
+    l2on = P.ns.l2 != nullptr;
   }
   __device__ __forceinline__ bool rin(int y) const { return (unsigned)(y - 1) < (unsigned)(M - 1); }
   __device__ __forceinline__ void issue(int y) const {
@@ -574,6 +586,8 @@ struct StripQ {
         m = max(m, ab(R[s3].c));
         m = max(m, ab(R[s3].d));
         mx = max(mx, m);
+        if (l2on)
+          ss += sq((double)R[s3].a) + sq((double)R[s3].b) + sq((double)R[s3].c) + sq((double)R[s3].d);
       }
     }
     // Erest2r of rows (j-5, j-4) when j-5 is even
@@ -603,6 +617,7 @@ __global__ void __launch_bounds__(32, 16) asc_desc_stream_q(const __grid_constan
   const int item = blockIdx.x;
   const int nseg = (P.M + P.seg - 1) / P.seg;
   unsigned long long mx = 0ull;
+  double ss = 0.0;
   if (item < P.nstrips * nseg) {
     const int strip = item % P.nstrips, sg = item / P.nstrips;
     const int ys = sg * P.seg, ye = min(ys + P.seg, P.M);
@@ -619,6 +634,7 @@ __global__ void __launch_bounds__(32, 16) asc_desc_stream_q(const __grid_constan
       S.template step<3>(j + 3);
     }
     mx = S.mx;
+    ss = S.ss;
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
@@ -626,6 +642,7 @@ __global__ void __launch_bounds__(32, 16) asc_desc_stream_q(const __grid_constan
     mx = w > mx ? w : mx;
   }
   if (lane == 0 && item < P.nstrips * nseg) norm_push(P.ns, __longlong_as_double((long long)mx));
+  if (item < P.nstrips * nseg) warp_l2_push(P.ns, ss);   // warp-uniform
 }
 
 }  // namespace xf

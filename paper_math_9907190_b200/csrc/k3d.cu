@@ -21,13 +21,14 @@ __global__ void __launch_bounds__(NT3) k3_desc_fine_ref(D3<const T> u, D3<const 
                                                         NormSink ns) {
   int H = M / 2 + 1;
   int64_t t = (int64_t)blockIdx.x * NT3 + threadIdx.x;
-  double mx = 0.0;
+  double mx = 0.0, ss = 0.0;
   if (t < (int64_t)H * H * H) {
     int a = (int)(t % H), b = (int)((t / H) % H), c = (int)(t / ((int64_t)H * H));
     for (int par = 0; par < 8; par++) {
       int x = 2 * a + (par & 1), y = 2 * b + ((par >> 1) & 1), z = 2 * c + ((par >> 2) & 1);
       T rc = res3z<T, ORDER>(u, f, x, y, z, M, k);
       mx = nmax(mx, absd(rc));
+      if (ns.sums(z)) ss += sq((double)rc);
       bool red = (((par & 1) + ((par >> 1) & 1) + ((par >> 2) & 1)) & 1) == 0;
       if (!red || !inner3(x, y, z, M)) continue;
       T nb[6];
@@ -36,7 +37,7 @@ __global__ void __launch_bounds__(NT3) k3_desc_fine_ref(D3<const T> u, D3<const 
       rr.ref(x, y, z) = erred(rc, nb);
     }
   }
-  block_norm_push<NT3>(ns, mx);
+  block_norm_push<NT3>(ns, mx, ss);
 }
 
 // ------------------------------------------------- descent, level kernels

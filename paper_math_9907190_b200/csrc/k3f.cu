@@ -190,13 +190,16 @@ struct OpDesc3Fine {
   };
   using Unit = Unit3;
   struct Acc {
-    double mx;
+    double mx, ss;   // max |r|, sum r^2 (a16)
   };
   static __device__ void prefetch(const Params &P) {
     tma_prefetch_desc(&P.tu);
     tma_prefetch_desc(&P.tf);
   }
-  static __device__ void init(Acc &a) { a.mx = 0.0; }
+  static __device__ void init(Acc &a) {
+    a.mx = 0.0;
+    a.ss = 0.0;
+  }
   static __device__ __forceinline__ Unit decode(const Params &P, int u) {
     int tx = u % P.ntx, r = u / P.ntx, ty = r % P.nty, zc = r / P.nty;
     Unit un;
@@ -272,8 +275,10 @@ struct OpDesc3Fine {
       R[0] = r0;
       R[RH2] = r1;
       // norm: every interior node once -- the tile core on the unit's own planes
-      if (p >= un.zs && p < un.ze && w >= 1 && w <= TY3 && lane >= 1 && lane <= TX3 / 2)
+      if (p >= un.zs && p < un.ze && w >= 1 && w <= TY3 && lane >= 1 && lane <= TX3 / 2) {
         acc.mx = nmax(nmax(acc.mx, absd(r0)), absd(r1));
+        if (P.ns.sums(p)) acc.ss += sq((double)r0) + sq((double)r1);
+      }
     }
     const int q = p - 2;   // r(q-1), r(q), r(q+1) were completed in earlier steps
     if (w < TY3 && q >= un.zs && q < un.ze && q >= 1 && q <= M - 1) {
@@ -288,7 +293,7 @@ struct OpDesc3Fine {
       }
     }
   }
-  static __device__ void finish(const Params &P, Acc &acc) { block_norm_push<NT>(P.ns, acc.mx); }
+  static __device__ void finish(const Params &P, Acc &acc) { block_norm_push<NT>(P.ns, acc.mx, acc.ss); }
 };
 
 // ============================================== finest ascent a15 (s = 1)

@@ -81,17 +81,22 @@ struct OpDesc3P {
     T u[2][2][2];   // [z & 1][row A/B][col 0/1]: own u of the two latest planes
     T r[2][2][2];   // own r of the two latest planes
     unsigned long long mx;
+    double ss;      // sum r^2 over the tile's core nodes (a16 L2 norm)
   };
   struct Ctx {
     Masks m;
     bool oA[2], oB[2];   // Erred output at row A / B, by PH
+    bool sA, sB;         // row A / B of this lane lies in the tile's core (counted once in the L2 sum)
     int64_t bA, bB;      // sublattice offsets (y >> 1) * pitch + (xl >> 1) of rows A, B
   };
   static __device__ void prefetch(const Params &P) {
     if (FINE) tma_prefetch_desc(&P.tu);
     tma_prefetch_desc(&P.tf);
   }
-  static __device__ void init(State &S) { S.mx = 0ull; }
+  static __device__ void init(State &S) {
+    S.mx = 0ull;
+    S.ss = 0.0;
+  }
   static __device__ void begin(const Params &P, Ctx &C, const Item &it) {
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const int xl = it.x0 - 2 + 2 * lane, yA = it.y0 - 1 + 2 * w;
@@ -102,6 +107,8 @@ struct OpDesc3P {
     C.oA[1] = lk && w >= 1 && C.m.rA && C.m.c0;
     C.oB[0] = lk && w <= NW - 2 && C.m.rB && C.m.c0;
     C.oB[1] = lk && w <= NW - 2 && C.m.rB && C.m.c1;
+    C.sA = lk && w >= 1;
+    C.sB = lk && w <= NW - 2;
     C.bA = (int64_t)(yA >> 1) * P.out.pitch + (xl >> 1);
     C.bB = (int64_t)((yA + 1) >> 1) * P.out.pitch + (xl >> 1);
   }
@@ -163,6 +170,10 @@ struct OpDesc3P {
       // every computed r is a true residual (or 0): max over all of them
       S.mx = umax64(S.mx, umax64(umax64(absbits(rn[0][0]), absbits(rn[0][1])),
                                  umax64(absbits(rn[1][0]), absbits(rn[1][1]))));
+      if (z >= it.zs && z < it.ze && P.ns.sums(z)) {   // the sum counts the core nodes once
+        if (C.sA) S.ss += sq((double)rn[0][0]) + sq((double)rn[0][1]);
+        if (C.sB) S.ss += sq((double)rn[1][0]) + sq((double)rn[1][1]);
+      }
       }
       // greens of plane z to the ring: red column of row A at z is PH, so its
       // green is column Q; row B (even y) the other way round
@@ -236,7 +247,7 @@ struct OpDesc3P {
     }
   }
   static __device__ void finish(const Params &P, State &S) {
-    if (FINE) block_norm_push<NTH>(P.ns, __longlong_as_double((long long)S.mx));
+    if (FINE) block_norm_push<NTH>(P.ns, __longlong_as_double((long long)S.mx), S.ss);
   }
 };
 

@@ -142,7 +142,7 @@ struct Impl2 : ImplBase {
     return cudaMemcpy(d_lev, lv.data(), sizeof(Lev2<T>) * k, cudaMemcpyHostToDevice);
   }
 
-  NormSink sink() const { return NormSink{s->d_hist, s->d_counter, kHistCap}; }
+  NormSink sink() const { return NormSink{s->d_hist, s->d_counter, kHistCap, s->sum_l2 ? s->d_l2 : nullptr}; }
 
   bool fuses_cycles() const override { return use_fast && xfuse; }
   void enqueue_cycle_mode(const void *u_in, void *u_out, const void *f_eff, cudaStream_t st, Prof *prof,
@@ -477,7 +477,7 @@ struct Impl3 : ImplBase {
     return cudaMemcpy(d_lev, lv.data(), sizeof(Lev3<T>) * k, cudaMemcpyHostToDevice);
   }
 
-  NormSink sink() const { return NormSink{s->d_hist, s->d_counter, kHistCap}; }
+  NormSink sink() const { return NormSink{s->d_hist, s->d_counter, kHistCap, s->sum_l2 ? s->d_l2 : nullptr}; }
   void desc_fine(const void *u, const void *f_eff, cudaStream_t st) {
     if (use_fast && ((uintptr_t)u & 15) == 0 && ((uintptr_t)f_eff & 15) == 0)
       fast3_desc_fine<T>((const T *)u, (const T *)f_eff, pitch, rR[0], M[0], s->cfg.order, coef, sink(), st);
@@ -699,7 +699,7 @@ static void drop_graphs(mg_solver *s) {
 static int run_cycle(mg_solver *s, const void *u_in, void *u_out, const void *f_eff, int mode) {
   cudaGraphExec_t ex = nullptr;
   for (auto &g : s->graphs)
-    if (g.uin == u_in && g.uout == u_out && g.f == f_eff && g.mode == mode) ex = g.exec;
+    if (g.uin == u_in && g.uout == u_out && g.f == f_eff && g.mode == mode && g.l2 == s->sum_l2) ex = g.exec;
   if (!ex) {
     if (s->graphs.size() >= 16) drop_graphs(s);
     cudaGraph_t g = nullptr;
@@ -723,7 +723,7 @@ static int run_cycle(mg_solver *s, const void *u_in, void *u_out, const void *f_
     e = cudaGraphInstantiate(&ex, g, 0);
     cudaGraphDestroy(g);
     CKS(s, e);
-    s->graphs.push_back({ex, u_in, u_out, f_eff, mode});
+    s->graphs.push_back({ex, u_in, u_out, f_eff, mode, s->sum_l2});
   }
   CKS(s, cudaGraphLaunch(ex, s->st));
   return MG_OK;
@@ -840,6 +840,9 @@ int mg_create_ex(const mg_config *cfg, mg_solver **out) {
   CKS(sp, cudaMemset(s->d_hist, 0, sizeof(unsigned long long) * kHistCap));
   CKS(sp, cudaMemset(s->d_counter, 0, sizeof(int)));
   CKS(sp, cudaMallocHost(&s->h_hist, sizeof(unsigned long long) * kHistCap));
+  CKS(sp, cudaMalloc(&s->d_l2, sizeof(double) * kHistCap));
+  CKS(sp, cudaMemset(s->d_l2, 0, sizeof(double) * kHistCap));
+  CKS(sp, cudaMallocHost(&s->h_l2, sizeof(double) * kHistCap));
   if (cfg->flags & MG_FLAG_CONVENTIONAL) {
     if (cfg->nranks > 1) {
       mg_destroy(s.release());
@@ -918,6 +921,8 @@ int mg_destroy(mg_solver *s) {
   cudaFree(s->d_u_stage);
   cudaFree(s->d_f_stage);
   if (s->h_hist) cudaFreeHost(s->h_hist);
+  cudaFree(s->d_l2);
+  if (s->h_l2) cudaFreeHost(s->h_l2);
   if (s->ev_in) cudaEventDestroy(s->ev_in);
   if (s->ev_out) cudaEventDestroy(s->ev_out);
   if (s->st) cudaStreamDestroy(s->st);
@@ -999,7 +1004,7 @@ int mg_residual(mg_solver *s, const void *u, const void *f, void *r) {
 // f_eff (work layout: f, or f~ for order 4).
 static int cycles_work(mg_solver *s, void *u, const void *fe, int ncycles, double *res_hist) {
   const int nslots = ncycles + 1;   // <= kHistCap (checked by the callers)
-  CKS(s, cudaMemsetAsync(s->d_hist, 0, sizeof(unsigned long long) * nslots, s->st));
+  CKS(s, clear_hist(s, nslots, s->st));
   CKS(s, cudaMemsetAsync(s->d_counter, 0, sizeof(int), s->st));
   // TMA path: u alternates between u and an internal partner (the ascent
   // reads the old u in a 2-node halo, so it cannot update in place); an odd
@@ -1028,17 +1033,7 @@ static int cycles_work(mg_solver *s, void *u, const void *fe, int ncycles, doubl
   if (res_hist) {
     if (!xf || ncycles == 0) s->impl->enqueue_final_norm(u, fe, s->st);
     CKS(s, s->impl->reduce_hist(s->d_hist, nslots, s->st));
-    CKS(s, cudaMemcpyAsync(s->h_hist, s->d_hist, sizeof(unsigned long long) * nslots, cudaMemcpyDeviceToHost, s->st));
-    CKS(s, cudaStreamSynchronize(s->st));
-    bool finite = true;
-    for (int i = 0; i <= ncycles; i++) {
-      double v;
-      unsigned long long b = s->h_hist[i];
-      std::memcpy(&v, &b, sizeof v);
-      res_hist[i] = v;
-      if (!std::isfinite(v)) finite = false;
-    }
-    if (!finite) return fail(s, MG_EDIVERGED, "non-finite residual norm");
+    return read_hist(s, ncycles, res_hist, s->st);
   }
   return MG_OK;
 }
@@ -1075,23 +1070,28 @@ static int vcycle_dev(mg_solver *s, void *u, const void *f, int ncycles, double 
   return MG_OK;
 }
 
-int mg_vcycle(mg_solver *s, void *u, const void *f, int ncycles, double *res_hist) {
+int mg_vcycle_norms(mg_solver *s, void *u, const void *f, int ncycles, double *res_inf, double *res_l2) {
   if (!s) return MG_EINVAL;
   if (!u || !f) return fail(s, MG_EINVAL, "mg_vcycle: NULL u or f");
   if (ncycles < 0) return fail(s, MG_EINVAL, "mg_vcycle: ncycles < 0");
-  if (res_hist && ncycles + 1 > kHistCap) return fail(s, MG_EINVAL, "mg_vcycle: res_hist needs ncycles < 4096");
-  if (ncycles == 0 && !res_hist) return MG_OK;
+  if (res_l2 && !res_inf) return fail(s, MG_EINVAL, "mg_vcycle_norms: res_l2 needs res_inf");
+  if (res_inf && ncycles + 1 > kHistCap) return fail(s, MG_EINVAL, "mg_vcycle: res_hist needs ncycles < 4096");
+  if (ncycles == 0 && !res_inf) return MG_OK;
   DeviceGuard g(s->device);
   int rc = begin(s);
   if (rc) return rc;
-  rc = s->impl->vcycle_all(s, u, f, ncycles, res_hist);
-  if (rc != 1) {
-    int rc2 = end(s);
-    return rc ? rc : rc2;
-  }
-  rc = vcycle_dev(s, u, f, ncycles, res_hist);
+  s->l2_out = res_l2;
+  s->sum_l2 = res_l2 != nullptr;
+  rc = s->impl->vcycle_all(s, u, f, ncycles, res_inf);
+  if (rc == 1) rc = vcycle_dev(s, u, f, ncycles, res_inf);
+  s->l2_out = nullptr;
+  s->sum_l2 = false;
   int rc2 = end(s);
   return rc ? rc : rc2;
+}
+
+int mg_vcycle(mg_solver *s, void *u, const void *f, int ncycles, double *res_hist) {
+  return mg_vcycle_norms(s, u, f, ncycles, res_hist, nullptr);
 }
 
 // Host arrays (caller layout) are copied straight into the work layout.

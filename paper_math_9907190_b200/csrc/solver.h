@@ -141,7 +141,7 @@ struct ImplBase {
   // loopback (virtual ranks in one process): the whole mg_vcycle; 1 = not handled
   virtual int vcycle_all(mg_solver *, void *, const void *, int, double *) { return 1; }
   // combine the per-cycle residual-norm maxima over ranks
-  virtual cudaError_t reduce_hist(unsigned long long *, int, cudaStream_t) { return cudaSuccess; }
+  virtual cudaError_t reduce_hist(unsigned long long *, int, cudaStream_t) { return cudaSuccess; }   // + mg_solver::d_l2
   // sticky failure of an enqueue_* call whose transport step failed (halo
   // exchange, all-gather, all-reduce) or an asynchronous transport error:
   // returns an mg_status (MG_OK when healthy) and clears it; *msg says why
@@ -231,11 +231,16 @@ struct mg_solver {
     cudaGraphExec_t exec;
     const void *uin, *uout, *f;
     int mode;
+    bool l2;
   };
   std::vector<GraphEntry> graphs;   // captured cycles keyed by pointers
   void *d_ualt = nullptr;            // out-of-place partner of the caller's u
   void *d_zero = nullptr;            // zero right-hand side (mg_convergence_factor)
   unsigned long long *h_hist = nullptr;    // pinned
+  double *d_l2 = nullptr, *h_l2 = nullptr;  // per-cycle sums of r^2 (kHistCap slots; host copy pinned)
+  double *l2_out = nullptr;                // the current call's L2 history destination (mg_vcycle_norms) or null
+  bool sum_l2 = false;                     // the current call's passes accumulate sum r^2 (only when asked:
+                                           // it costs the issue-bound fp32 fused pass ~7 %)
   std::string err;
   size_t field_elems() const {   // one caller field (u, f, r), elements
     size_t le = impl ? impl->local_elems() : 0;
@@ -262,3 +267,34 @@ static int fail(mg_solver *s, int code, const std::string &msg) {
       return fail((s), e_ == cudaErrorMemoryAllocation ? MG_ENOMEM : MG_ECUDA,                \
                   std::string(#call) + ": " + cudaGetErrorString(e_));                        \
   } while (0)
+
+// The residual histories of a call's ncycles + 1 slots, to the host: res_hist
+// (L-inf, bit patterns of max |r|) and, when the call asked for it, s->l2_out
+// (||r||_{2,h} = (h^d sum r^2)^(1/2)).  Synchronises.
+static int read_hist(mg_solver *s, int ncycles, double *res_hist, cudaStream_t st) {
+  const int nslots = ncycles + 1;
+  CKS(s, cudaMemcpyAsync(s->h_hist, s->d_hist, sizeof(unsigned long long) * nslots, cudaMemcpyDeviceToHost, st));
+  if (s->l2_out) CKS(s, cudaMemcpyAsync(s->h_l2, s->d_l2, sizeof(double) * nslots, cudaMemcpyDeviceToHost, st));
+  CKS(s, cudaStreamSynchronize(st));
+  const double hd = std::pow(1.0 / (double)(s->cfg.n - 1), s->cfg.dim);
+  bool finite = true;
+  for (int i = 0; i <= ncycles; i++) {
+    double v;
+    unsigned long long b = s->h_hist[i];
+    std::memcpy(&v, &b, sizeof v);
+    res_hist[i] = v;
+    if (!std::isfinite(v)) finite = false;
+    if (s->l2_out) {
+      s->l2_out[i] = std::sqrt(hd * s->h_l2[i]);
+      if (!std::isfinite(s->l2_out[i])) finite = false;
+    }
+  }
+  if (!finite) return fail(s, MG_EDIVERGED, "non-finite residual norm");
+  return MG_OK;
+}
+static cudaError_t clear_hist(mg_solver *s, int nslots, cudaStream_t st) {
+  cudaError_t e = cudaMemsetAsync(s->d_hist, 0, sizeof(unsigned long long) * nslots, st);
+  if (e == cudaSuccess) e = cudaMemsetAsync(s->d_l2, 0, sizeof(double) * nslots, st);
+  return e;
+}
+

@@ -6,7 +6,7 @@ and streams.  There is no CPU fallback: if libmg.so cannot be loaded or no
 CUDA device is present the calls raise.
 
 The functions mirror the C ABI one to one (``mg_create``, ``mg_create_ex``,
-``mg_destroy``, ``mg_local_extent``, ``mg_residual``, ``mg_vcycle``,
+``mg_destroy``, ``mg_local_extent``, ``mg_residual``, ``mg_vcycle``, ``mg_vcycle_norms``,
 ``mg_vcycle_host``, ``mg_norm``, ``mg_num_levels``, ``mg_level_points``,
 ``mg_launches_per_cycle``, ``mg_strerror``, ``mg_last_error``);
 :class:`Solver` wraps a handle for torch tensors.
@@ -67,6 +67,8 @@ EXPORTS = {
     "mg_residual": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]),
     "mg_vcycle": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int,
                                  ctypes.POINTER(ctypes.c_double)]),
+    "mg_vcycle_norms": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int,
+                                       ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double)]),
     "mg_vcycle_host": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int,
                                       ctypes.POINTER(ctypes.c_double)]),
     "mg_norm": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, ctypes.POINTER(ctypes.c_double)]),
@@ -148,6 +150,14 @@ def mg_vcycle(h, u_ptr: int, f_ptr: int, ncycles: int, hist: bool = False):
     buf = (ctypes.c_double * (ncycles + 1))() if hist else None
     _check(load().mg_vcycle(h, u_ptr, f_ptr, ncycles, buf), h, "mg_vcycle")
     return np.array(list(buf)) if hist else None
+
+
+def mg_vcycle_norms(h, u_ptr: int, f_ptr: int, ncycles: int):
+    """(L-inf history, L2 history), ncycles + 1 entries each."""
+    inf = (ctypes.c_double * (ncycles + 1))()
+    l2 = (ctypes.c_double * (ncycles + 1))()
+    _check(load().mg_vcycle_norms(h, u_ptr, f_ptr, ncycles, inf, l2), h, "mg_vcycle_norms")
+    return np.array(list(inf)), np.array(list(l2))
 
 
 def mg_vcycle_host(h, u_ptr: int, f_ptr: int, ncycles: int, hist: bool = False):
@@ -331,7 +341,11 @@ class Solver:
         return t.data_ptr()
 
     # -- calls
-    def vcycle(self, u, f, ncycles: int, hist: bool = False):
+    def vcycle(self, u, f, ncycles: int, hist: bool = False, l2: bool = False):
+        """ncycles V-cycles in place on u; hist: the L-inf residual history;
+        l2: (L-inf history, L2 history)."""
+        if l2:
+            return mg_vcycle_norms(self.h, self._chk(u), self._chk(f), ncycles)
         return mg_vcycle(self.h, self._chk(u), self._chk(f), ncycles, hist)
 
     def residual(self, u, f, r=None):

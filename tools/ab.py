@@ -25,7 +25,7 @@ def run(env_kv, workload, steps, dtype):
         k, v = kv.split("=", 1)
         env[k] = v
     out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--workload", workload, "--steps",
-                          str(steps), "--warmup", "5", "--no-cpu", "--no-e2e", "--dtype", dtype], env=env, capture_output=True,
+                          str(steps), "--warmup", "5", "--no-cpu", "--no-e2e", "--no-sub", "--dtype", dtype], env=env, capture_output=True,
                          text=True, timeout=900)
     d = json.loads(out.stdout.strip().splitlines()[-1])
     return d["ms_per_step"], d["clocks"]["sm_mhz"]
