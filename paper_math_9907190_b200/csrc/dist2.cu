@@ -40,6 +40,7 @@ struct Dist2 : ImplBase {
   std::vector<D2<T>> rAf, vAf;
   D2<T> uf_scratch{};            // loopback: full f~ (order 4)
   Lev2<T> *d_lev = nullptr;
+  std::vector<Lev2<T>> h_lev;   // host copy of the descriptors (coarse solver parameters)
 
   Dist2(mg_solver *sv, bool loopback) : s(sv), k(sv->k), P(sv->cfg.nranks), loop(loopback), n(sv->cfg.n),
                                         pitch(sv->pitch) {
@@ -150,6 +151,7 @@ struct Dist2 : ImplBase {
     cudaError_t e = dalloc(&q, sizeof(Lev2<T>) * k);
     if (e) return e;
     d_lev = (Lev2<T> *)q;
+    h_lev = lv;
     return cudaMemcpy(d_lev, lv.data(), sizeof(Lev2<T>) * k, cudaMemcpyHostToDevice);
   }
 
@@ -218,7 +220,7 @@ struct Dist2 : ImplBase {
       }
     }
     STEP("coarse", 2 * oc, 1, 0);
-    launch2_coarse<T>(d_lev, oc, k, s->d_counter, st);
+    launch2_coarse<T>(d_lev, oc, k, s->d_counter, st, h_lev.data());
     bool d_done = false;
     for (int o = oc - 1; o >= oa; o--) {
       if (!d_done) {

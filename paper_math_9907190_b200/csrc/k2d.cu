@@ -213,6 +213,148 @@ __global__ void __launch_bounds__(1024) k2_coarse_smem(const Lev2<T> *lvg, int o
   }
 }
 
+// Compile-time coarse solver (the default): the octaves from M = MC (<= 64,
+// a power of two) down to the single interior node, every level in shared
+// memory at compile-time offsets, every step a loop of compile-time trip
+// count over the nodes it writes (no per-node division by a run-time size,
+// no masked-off iterations: the colour-1 step of an A level walks the green
+// nodes only).  Same node formulas and operand order as node_* (ops2.cuh), so
+// the iterate is unchanged bit for bit.  Measured on B200 at 8193^2 (MC = 64):
+// see DESIGN.md 6.4.
+namespace cc2 {
+__host__ __device__ constexpr int ilog2(int v) { return v <= 1 ? 0 : 1 + ilog2(v / 2); }
+// elements of octave j's arrays (M = MC >> j): rD, vD (E and O, (M/2+1)^2
+// each) and rA, vA of the next octave ((M/2+1)^2 each) -- 6 arrays of side M/2+1
+template <int MC>
+__host__ __device__ constexpr int off(int j) {
+  int e = 0;
+  for (int q = 0; q < j; q++) {
+    const int W = (MC >> q) / 2 + 1;
+    e += 6 * W * W;
+  }
+  return e;
+}
+}  // namespace cc2
+
+template <class T>
+struct CC2P {
+  D2<const T> rA0;   // r_A(oc), global
+  D2<T> vA0;         // v_A(oc), global
+  T cD[6], cA[6];    // Jacobi constants of octaves oc, oc + 1, ..
+  int *counter;
+};
+
+template <class T, int MC, int NTH>
+__global__ void __launch_bounds__(NTH) k2_coarse_ct(const __grid_constant__ CC2P<T> P) {
+  const D2<const T> &rA0 = P.rA0;
+  const D2<T> &vA0 = P.vA0;
+  const T *cDs = P.cD, *cAs = P.cA;
+  int *counter = P.counter;
+  constexpr int K = cc2::ilog2(MC);   // octaves j = 0 .. K-1 (M = MC .. 2); j < K-1 have a D level
+  extern __shared__ __align__(16) unsigned char dsm2[];
+  T *ar = (T *)dsm2;
+  const int tid = threadIdx.x;
+  pdl_trigger();
+  // zero the arena (boundary entries stay zero), then r_A(oc) into a dense
+  // (MC+1)^2 array after the arena
+  constexpr int NA = cc2::off<MC>(K - 1);
+  constexpr int W0 = MC + 1;
+  T *a0r = ar + NA, *a0v = a0r + W0 * W0;
+  for (int t = tid; t < NA + 2 * W0 * W0; t += NTH) ar[t] = (T)0;
+  __syncthreads();
+  pdl_wait();
+  for (int t = tid; t < W0 * W0; t += NTH) {
+    const int x = t % W0, y = t / W0;
+    a0r[t] = rA0.p[(int64_t)y * rA0.pitch + x];
+  }
+  __syncthreads();
+  // A level of octave j: dense, side (M_j + 1); j = 0 is a0, else the "next A"
+  // arrays of octave j - 1
+  auto Ar = [&](int j) -> T * { return j == 0 ? a0r : ar + cc2::off<MC>(j - 1) + 4 * ((MC >> (j - 1)) / 2 + 1) * ((MC >> (j - 1)) / 2 + 1); };
+  auto Av = [&](int j) -> T * { return j == 0 ? a0v : Ar(j) + ((MC >> (j - 1)) / 2 + 1) * ((MC >> (j - 1)) / 2 + 1); };
+#define CC2_DESC(J)                                                                                        \
+  if constexpr ((J) < K - 1) {                                                                             \
+    constexpr int M = MC >> (J), H = M / 2 + 1, WA = M + 1, Mc = M / 2;                                    \
+    const T *A = Ar(J);                                                                                    \
+    T *E = ar + cc2::off<MC>(J), *O = E + H * H;                                                           \
+    for (int t = tid; t < H * H; t += NTH) { /* a2, Erest2r (node_rest_ad) */                             \
+      const int a = t % H, b = t / H, x = 2 * a, y = 2 * b;                                                \
+      if (x >= 2 && y >= 2 && x <= M - 2 && y <= M - 2)                                                    \
+        E[t] = erest2r(A[y * WA + x], A[y * WA + x - 1], A[(y - 1) * WA + x], A[y * WA + x + 1],           \
+                       A[(y + 1) * WA + x]);                                                               \
+      if (x + 1 <= M - 1 && y + 1 <= M - 1) {                                                              \
+        const int c = (y + 1) * WA + x + 1;                                                                \
+        O[t] = erest2r(A[c], A[c - 1], A[c - WA], A[c + 1], A[c + WA]);                                    \
+      }                                                                                                    \
+    }                                                                                                      \
+    __syncthreads();                                                                                       \
+    T *Ac = Ar((J) + 1);                                                                                   \
+    for (int t = tid; t < (Mc - 1) * (Mc - 1); t += NTH) { /* a3, Erest2b (node_rest_da) */               \
+      const int X = t % (Mc - 1) + 1, Y = t / (Mc - 1) + 1;                                                \
+      Ac[Y * (Mc + 1) + X] = erest2b(E[Y * H + X], O[(Y - 1) * H + X - 1], O[(Y - 1) * H + X], O[Y * H + X], \
+                                     O[Y * H + X - 1]);                                                    \
+    }                                                                                                      \
+    __syncthreads();                                                                                       \
+  }
+  CC2_DESC(0) CC2_DESC(1) CC2_DESC(2) CC2_DESC(3) CC2_DESC(4)
+#undef CC2_DESC
+  if (tid == 0) {   // a4: the single interior node of M = 2 (reading A4)
+    const T *A = Ar(K - 1);
+    Av(K - 1)[1 * 3 + 1] = (-(cAs[K - 1] * A[1 * 3 + 1])) * (T)0.25;
+    if (counter) *counter += 1;   // this cycle's norm slot is complete
+  }
+  __syncthreads();
+#define CC2_ASC(J)                                                                                           \
+  if constexpr ((J) < K - 1) {                                                                               \
+    constexpr int M = MC >> (J), H = M / 2 + 1, WA = M + 1, WC = M / 2 + 1, Wd = M / 2;                      \
+    const T *vc = Av((J) + 1), *rE = ar + cc2::off<MC>(J), *rO = rE + H * H;                                 \
+    T *vE = ar + cc2::off<MC>(J) + 2 * H * H, *vO = vE + H * H;                                              \
+    const T cD = cDs[J], cA = cAs[J];                                                                        \
+    for (int t = tid; t < Wd * Wd; t += NTH) { /* a5, Eajacr on O (node_jac_d1) */                          \
+      const int a = t % Wd, b = t / Wd;                                                                      \
+      vO[b * H + a] = jac4(cD, rO[b * H + a], vc[b * WC + a], vc[b * WC + a + 1], vc[(b + 1) * WC + a + 1],  \
+                           vc[(b + 1) * WC + a]);                                                            \
+    }                                                                                                        \
+    __syncthreads();                                                                                         \
+    for (int t = tid; t < (Wd - 1) * (Wd - 1); t += NTH) { /* a6, Eajacb on E (node_jac_d2) */              \
+      const int a = t % (Wd - 1) + 1, b = t / (Wd - 1) + 1;                                                  \
+      vE[b * H + a] = jac4(cD, rE[b * H + a], vO[(b - 1) * H + a - 1], vO[(b - 1) * H + a], vO[b * H + a],   \
+                           vO[b * H + a - 1]);                                                               \
+    }                                                                                                        \
+    __syncthreads();                                                                                         \
+    const T *rA = Ar(J);                                                                                     \
+    T *vA = Av(J);                                                                                           \
+    /* v_D(s) at node (x, y), x + y even: E (both even) or O (both odd) */                                 \
+    auto vd = [&](int x, int y) -> T { return (y & 1) ? vO[(y >> 1) * H + (x >> 1)] : vE[(y >> 1) * H + (x >> 1)]; }; \
+    for (int t = tid; t < (M - 1) * Wd; t += NTH) { /* a7 colour 1: the green node of pair t (node_jac_a1) */ \
+      const int y = t / Wd + 1, x = 2 * (t % Wd) + 1 + (y & 1);                                              \
+      if (x <= M - 1)                                                                                        \
+        vA[y * WA + x] = jac4(cA, rA[y * WA + x], vd(x - 1, y), vd(x, y - 1), vd(x + 1, y), vd(x, y + 1));    \
+    }                                                                                                        \
+    __syncthreads();                                                                                         \
+    for (int t = tid; t < (M - 1) * Wd; t += NTH) { /* a7 colour 2: the D node of pair t (node_jac_a2) */   \
+      const int y = t / Wd + 1, x = 2 * (t % Wd) + 2 - (y & 1);                                              \
+      if (x <= M - 1) {                                                                                      \
+        const int c = y * WA + x;                                                                            \
+        vA[c] = jac4(cA, rA[c], vA[c - 1], vA[c - WA], vA[c + 1], vA[c + WA]);                               \
+      }                                                                                                      \
+    }                                                                                                        \
+    __syncthreads();                                                                                         \
+  }
+  CC2_ASC(4) CC2_ASC(3) CC2_ASC(2) CC2_ASC(1) CC2_ASC(0)
+#undef CC2_ASC
+  for (int t = tid; t < W0 * W0; t += NTH) {
+    const int x = t % W0, y = t / W0;
+    if (x >= 1 && y >= 1 && x <= MC - 1 && y <= MC - 1) vA0.p[(int64_t)y * vA0.pitch + x] = a0v[t];
+  }
+}
+
+template <class T, int MC>
+static size_t cc2_bytes() {
+  constexpr int K = cc2::ilog2(MC);
+  return sizeof(T) * (cc2::off<MC>(K - 1) + 2 * (MC + 1) * (MC + 1));
+}
+
 // Cooperative tail (as k3l_tail): octaves om .. oc-1 grid-wide with a grid
 // barrier between steps, octaves >= oc in CTA 0's shared memory; one launch.
 template <class T>
@@ -598,8 +740,42 @@ void launch2_asc_fine_sweeps(const S2<T> &vd, const D2<T> &u, const D2<const T> 
   k2_update_ref<T><<<blocks_for(W * W), NT, 0, st>>>(cd(u), cd(scratch), un, M);
 }
 
+// The compile-time coarse solver for M(oc) = MC (host descriptors h_lev).
+template <class T, int MC>
+static bool coarse_ct(const Lev2<T> *h_lev, int oc, int *counter, cudaStream_t st) {
+  static_assert(MC >= 2 && MC <= 64, "");
+  constexpr int NTH = MC >= 32 ? 512 : 256;
+  constexpr int K = cc2::ilog2(MC);
+  CC2P<T> P{};
+  P.rA0 = D2<const T>{h_lev[oc].rA.p, h_lev[oc].rA.pitch};
+  P.vA0 = h_lev[oc].vA;
+  for (int j = 0; j < K; j++) {
+    P.cD[j] = h_lev[oc + j].cD;
+    P.cA[j] = h_lev[oc + j].cA;
+  }
+  P.counter = counter;
+  const size_t bytes = cc2_bytes<T, MC>();
+  if (cudaFuncSetAttribute(k2_coarse_ct<T, MC, NTH>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes))
+    return false;
+  note_launch(launch_pdl(k2_coarse_ct<T, MC, NTH>, dim3(1), dim3(NTH), bytes, st, P));
+  return true;
+}
+
 template <class T>
-void launch2_coarse(const Lev2<T> *d_lev, int oc, int k, int *counter, cudaStream_t st) {
+void launch2_coarse(const Lev2<T> *d_lev, int oc, int k, int *counter, cudaStream_t st, const Lev2<T> *h_lev) {
+  static const bool ct = !env_flag("MG_COARSE_NOCT");
+  if (ct && h_lev && oc >= 1 && k - oc <= 6) {
+    bool done = false;
+    switch (k - oc) {   // M(oc) = 2^(k - oc)
+      case 1: done = coarse_ct<T, 2>(h_lev, oc, counter, st); break;
+      case 2: done = coarse_ct<T, 4>(h_lev, oc, counter, st); break;
+      case 3: done = coarse_ct<T, 8>(h_lev, oc, counter, st); break;
+      case 4: done = coarse_ct<T, 16>(h_lev, oc, counter, st); break;
+      case 5: done = coarse_ct<T, 32>(h_lev, oc, counter, st); break;
+      case 6: done = coarse_ct<T, 64>(h_lev, oc, counter, st); break;
+    }
+    if (done) return;
+  }
   static const bool global = env_flag("MG_COARSE_GLOBAL");
   if (!global && oc >= 1 && k <= 32) {
     size_t elems = 0;
@@ -654,7 +830,7 @@ void launch2_norm(const D2<const T> &a, int M, unsigned long long *mx, double *s
   template void launch2_asc_fine<T>(const S2<T> &, const D2<T> &, const D2<const T> &, const D2<T> &, const D2<T> &, \
                                     int, int, T,                                                                   \
                                     const Coef<T> &, cudaStream_t);                                                \
-  template void launch2_coarse<T>(const Lev2<T> *, int, int, int *, cudaStream_t);                                \
+  template void launch2_coarse<T>(const Lev2<T> *, int, int, int *, cudaStream_t, const Lev2<T> *);                                \
   template void launch2_gather_d<T>(const D2<T> &, const S2<T> &, int, cudaStream_t);                              \
   template void launch2_asc_fine_sweeps<T>(const S2<T> &, const D2<T> &, const D2<const T> &, const D2<T> &,        \
                                            const D2<T> &, int, int, T, const Coef<T> &, int, const S2<T> &,        \

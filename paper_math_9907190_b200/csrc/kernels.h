@@ -41,8 +41,11 @@ struct Lev2 {
 };
 // All octaves o >= oc (oc >= 1) in one CTA: restrictions from r_A(oc) down,
 // the coarsest step, the Jacobi steps back up to v_A(oc).
+// h_lev: the host copy of the descriptors (enables the compile-time solver
+// k2_coarse_ct for M(oc) <= 64), or null.
 template <class T>
-void launch2_coarse(const Lev2<T> *d_lev, int oc, int k, int *counter, cudaStream_t st);
+void launch2_coarse(const Lev2<T> *d_lev, int oc, int k, int *counter, cudaStream_t st,
+                    const Lev2<T> *h_lev = nullptr);
 // Octaves om .. oc-1 grid-wide and oc .. k-1 in one CTA's shared memory, one
 // cooperative launch (h_lev: host copy of the descriptors).  false: not launched.
 template <class T>

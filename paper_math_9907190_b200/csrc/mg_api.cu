@@ -274,7 +274,7 @@ struct Impl2 : ImplBase {
       for (int l = 2 * oc; l < L; l++) b += 5 * Nl[l];
       b -= Nl[L - 1] + 2 * Nl[2 * oc];   // coarsest: 4 touches; r_A(oc): read twice, written outside
       STEP("coarse", 2 * oc, 1, w * b);
-      launch2_coarse<T>(d_lev, oc, k, s->d_counter, st);
+      launch2_coarse<T>(d_lev, oc, k, s->d_counter, st, h_lev.data());
       for (int o = oc - 1; o >= od; o--) ascent(o);
     }
     for (int o = od - 1; o >= 0; o--) ascent(o);

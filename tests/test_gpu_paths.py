@@ -58,7 +58,9 @@ CASES = [
     ({"MG_COARSE_GLOBAL": "1", "MG_TAIL_M3": "0"}, 3, 65, 2, "float64"),
     ({"MG_TAIL_M2": "128"}, 2, 513, 2, "float64"),
     ({"MG_STAGES": "3"}, 2, 513, 2, "float64"),
-    ({"MG_COARSE_GLOBAL": "1"}, 2, 257, 2, "float64"),
+    ({"MG_COARSE_GLOBAL": "1", "MG_COARSE_NOCT": "1"}, 2, 257, 2, "float64"),
+    ({"MG_COARSE_NOCT": "1"}, 2, 513, 2, "float64"),
+    ({"MG_COARSE_NOCT": "1"}, 2, 257, 4, "float32"),
     ({"MG_FORCE_REF": "1"}, 2, 129, 4, "float64"),
     ({"MG_PDL": "1"}, 2, 257, 2, "float64"),
     ({"MG_PDL": "1"}, 3, 65, 2, "float64"),
