@@ -29,7 +29,7 @@ COLS = {
 }
 # kernel-name fragment -> step name used by mg_profile / bench.py
 STEPS = {
-    "OpDesc3P<double, 1>": "desc_fine", "OpAsc3P<double, 1>": "asc_fine",
+    "OpDesc3P<double, 1,": "desc_fine", "OpAsc3P<double, 1,": "asc_fine",
     "OpDesc2Fine": "desc_fine", "OpJac2A<double, 2, 1": "asc_fine",
     "asc_desc_stream<double, 2": "asc_desc", "asc_desc_stream<float, 2": "asc_desc",
     "asc_desc_stream_q<": "asc_desc",
