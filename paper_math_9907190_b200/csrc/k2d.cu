@@ -263,9 +263,17 @@ __global__ void __launch_bounds__(NTH) k2_coarse_ct(const __grid_constant__ CC2P
   for (int t = tid; t < NA + 2 * W0 * W0; t += NTH) ar[t] = (T)0;
   __syncthreads();
   pdl_wait();
-  for (int t = tid; t < W0 * W0; t += NTH) {
-    const int x = t % W0, y = t / W0;
-    a0r[t] = rA0.p[(int64_t)y * rA0.pitch + x];
+  {   // all loads of the thread in flight at once (one L2 round trip, not one per element)
+    constexpr int NL = (W0 * W0 + NTH - 1) / NTH;
+    T v[NL];
+#pragma unroll
+    for (int i = 0; i < NL; i++) {
+      const int t = tid + i * NTH;
+      v[i] = t < W0 * W0 ? rA0.p[(int64_t)(t / W0) * rA0.pitch + t % W0] : (T)0;
+    }
+#pragma unroll
+    for (int i = 0; i < NL; i++)
+      if (tid + i * NTH < W0 * W0) a0r[tid + i * NTH] = v[i];
   }
   __syncthreads();
   // A level of octave j: dense, side (M_j + 1); j = 0 is a0, else the "next A"

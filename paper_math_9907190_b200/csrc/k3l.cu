@@ -571,15 +571,35 @@ __device__ __forceinline__ void coarse3_block(const Tail3<T> &P, T *arena) {
     return o;
   };
   auto cd = [](const D3<T> &a) { return D3<const T>{a.p, a.pitch, a.plane}; };
-  // G(s) of octave o: global at o = oc, else the G(2s) arrays of octave o-1
+  // G(oc) (r and v, dense W^3) staged in shared memory after the arena: r_G(oc)
+  // is read from global memory once, with every load of a thread in flight at
+  // once, and v_G(oc) written back at the end (not one L2 round trip per
+  // stencil access)
+  const int W = P.lv[oc].M + 1, W3 = W * W * W;
+  T *g0 = off(k - 1);
+  // G(s) of octave o: the staged copy at o = oc, else the G(2s) arrays of octave o-1
   auto gr = [&](int o, int which) -> D3<T> {
-    if (o == oc) return which ? P.lv[o].vG : P.lv[o].rG;
+    if (o == oc) return D3<T>{g0 + (int64_t)which * W3, W, (int64_t)W * W};
     const int H = P.lv[o - 1].M / 2 + 1;
     return D3<T>{off(o - 1) + (int64_t)(12 + which) * H * H * H, H, (int64_t)H * H};
   };
   D3<const T> none{nullptr, 0, 0};
   Coef<T> k0{};
-  for (size_t t = tid, n = off(k - 1) - arena; t < n; t += bs) arena[t] = (T)0;
+  for (size_t t = tid, n = g0 - arena + 2 * (size_t)W3; t < n; t += bs) arena[t] = (T)0;
+  {
+    const D3<T> &rg = P.lv[oc].rG;
+    for (int b0 = tid; b0 < W3; b0 += 8 * bs) {
+      T v[8];
+#pragma unroll
+      for (int i = 0; i < 8; i++) {
+        const int t = b0 + i * bs;
+        v[i] = t < W3 ? rg.p[(int64_t)(t / (W * W)) * rg.plane + (int64_t)((t / W) % W) * rg.pitch + t % W] : (T)0;
+      }
+#pragma unroll
+      for (int i = 0; i < 8; i++)
+        if (b0 + i * bs < W3) g0[b0 + i * bs] = v[i];
+    }
+  }
   __syncthreads();
 #define LOOPB(HH, BODY)                                            \
   {                                                                \
@@ -624,6 +644,15 @@ __device__ __forceinline__ void coarse3_block(const Tail3<T> &P, T *arena) {
     LOOPB(H, (b3_jac_g2<T, 2, false>(cd(rG), none, none, cd(vG), vG, M, H, L.cG, k0, a, b, c)));
   }
 #undef LOOPB
+  {   // v_G(oc) to global memory (interior nodes; the boundary is never written)
+    const D3<T> &vg = P.lv[oc].vG;
+    const T *src = g0 + W3;
+    for (int t = tid; t < W3; t += bs) {
+      const int x = t % W, y = (t / W) % W, z = t / (W * W);
+      if (x >= 1 && y >= 1 && z >= 1 && x <= W - 2 && y <= W - 2 && z <= W - 2)
+        vg.p[(int64_t)z * vg.plane + (int64_t)y * vg.pitch + x] = src[t];
+    }
+  }
 }
 
 template <class T>
@@ -811,6 +840,10 @@ bool lv3_tail(const Lev3<T> *h_lev, int om, int oc, int k, int *counter, cudaStr
   for (int o = oc; o + 1 < k; o++) {
     const size_t H = h_lev[o].M / 2 + 1;
     elems += 14 * H * H * H;
+  }
+  {
+    const size_t W = h_lev[oc].M + 1;   // the staged r_G(oc), v_G(oc)
+    elems += 2 * W * W * W;
   }
   const size_t bytes = elems * sizeof(T);
   if (bytes > 200 * 1024) return false;
