@@ -453,6 +453,7 @@ struct Dist2CA : Dist2<T> {
   using B::rk;
   using B::s;
   bool ca = false;
+  bool fused = !env_flag("MG_DIST_NOFUSE");   // octave-pair passes on the bands (MG_DIST_NOFUSE=1: level passes)
   int Gu = 0;
   std::vector<int> WD, WA, waD, waA;   // bands (fine rows): descent r_D / r_A, ascent v_D / v_A
   struct Full {
@@ -575,12 +576,30 @@ struct Dist2CA : Dist2<T> {
       if ((e = fast2_desc_fine<T>(fl[i].u[cur].p, fe(i), pitch, fl[i].rD[0], M[0], s->cfg.order, coef,
                                   own_sink(rk[i].q), st, win(rk[i].q, WD[0], 1, M[0]))))
         return e;
+    // the octave-pair passes of the single-GPU cycle on row bands:
+    // rest_dad = rest_da(o) + rest_ad(o+1) on A(o+1)'s band, jac_ad = jac_a(o) +
+    // jac_d(o-1) on D(o-1)'s band (rounded out to an even first row; the extra
+    // rows are never read)
+    bool a_done = false;
     for (int o = 0; o < oa; o++) {
       const int s_ = 1 << o;
-      if (o >= 1) {
+      if (o >= 1 && !a_done) {
         STEP("rest_ad", 2 * o, nloc, w * (Nl[2 * o] + Nl[2 * o + 1]));
         for (int i = 0; i < nloc; i++)
           if ((e = fast2_rest_ad<T>(fl[i].rA[o], fl[i].rD[o], M[o], st, win(rk[i].q, WD[o], s_, M[o])))) return e;
+      }
+      a_done = false;
+      if (o + 1 < oa && fused) {
+        STEP("rest_dad", 2 * o + 1, nloc, w * (Nl[2 * o + 1] + Nl[2 * o + 2] + Nl[2 * o + 3]));
+        const int band = std::max(WA[o + 1], WD[o + 1]);
+        for (int i = 0; i < nloc; i++) {
+          const Rows2 r = win(rk[i].q, band, 2 * s_, M[o + 1] + 1);
+          if ((e = fast2_rest_dad<T>(fl[i].rD[o], fl[i].rA[o + 1], fl[i].rD[o + 1], M[o + 1], st, false, r.ylo,
+                                     r.yhi)))
+            return e;
+        }
+        a_done = true;
+        continue;
       }
       STEP("rest_da", 2 * o + 1, nloc, w * (Nl[2 * o + 1] + Nl[2 * o + 2]));
       for (int i = 0; i < nloc; i++) {
@@ -594,15 +613,29 @@ struct Dist2CA : Dist2<T> {
                              sizeof(T), st)))
       return e;
     if ((e = B::coarse_part(st, prof))) return e;
+    bool d_done = false;
     for (int o = oa - 1; o >= 0; o--) {
       const int s_ = 1 << o;
-      STEP("jac_d", 2 * o + 1, nloc, w * (Nl[2 * o + 2] + 2 * Nl[2 * o + 1]));
-      for (int i = 0; i < nloc; i++) {
-        const D2<T> &vc = (o + 1 < oa) ? fl[i].vA[o + 1] : B::vAf[oa];
-        if ((e = fast2_jac_d<T>(vc, fl[i].rD[o], fl[i].vD[o], M[o], cD[o], st, win(rk[i].q, waD[o], 2 * s_, M[o] / 2))))
-          return e;
+      if (!d_done) {
+        STEP("jac_d", 2 * o + 1, nloc, w * (Nl[2 * o + 2] + 2 * Nl[2 * o + 1]));
+        for (int i = 0; i < nloc; i++) {
+          const D2<T> &vc = (o + 1 < oa) ? fl[i].vA[o + 1] : B::vAf[oa];
+          if ((e = fast2_jac_d<T>(vc, fl[i].rD[o], fl[i].vD[o], M[o], cD[o], st,
+                                  win(rk[i].q, waD[o], 2 * s_, M[o] / 2))))
+            return e;
+        }
       }
-      if (o >= 1) {
+      d_done = false;
+      if (o >= 1 && fused) {
+        STEP("jac_ad", 2 * o, nloc, w * (Nl[2 * o + 1] + Nl[2 * o] + 2 * Nl[2 * o - 1]));
+        for (int i = 0; i < nloc; i++) {
+          const Rows2 r = win(rk[i].q, up(waD[o - 1], 2 * s_), s_, M[o - 1] / 2 + 1);
+          if ((e = fast2_jac_ad<T>(fl[i].vD[o], fl[i].rA[o], cA[o], fl[i].rD[o - 1], fl[i].vD[o - 1], M[o - 1],
+                                   cD[o - 1], st, false, r.ylo, r.yhi)))
+            return e;
+        }
+        d_done = true;
+      } else if (o >= 1) {
         STEP("jac_a", 2 * o, nloc, w * (Nl[2 * o + 1] + 2 * Nl[2 * o]));
         for (int i = 0; i < nloc; i++)
           if ((e = fast2_jac_a<T>(fl[i].vD[o], fl[i].rA[o], fl[i].vA[o], M[o], cA[o], st,
@@ -622,9 +655,10 @@ struct Dist2CA : Dist2<T> {
   int launches_per_cycle() const override {
     if (!ca) return B::launches_per_cycle();
     int c = nloc;   // desc_fine
-    for (int o = 0; o < oa; o++) c += ((o >= 1) + 1) * nloc;
-    c += B::coarse_launches();
-    for (int o = oa - 1; o >= 0; o--) c += 2 * nloc;
+    if (fused)      // rest_dad for o < oa-1, rest_da at oa-1; jac_d at oa-1, jac_ad for o >= 1, asc_fine
+      c += oa * nloc + B::coarse_launches() + (1 + (oa - 1) + 1) * nloc;
+    else
+      c += (2 * oa - 1) * nloc + B::coarse_launches() + 2 * oa * nloc;
     return c;
   }
 

@@ -354,6 +354,7 @@ struct OpRest2DAD {
     S2<T> rd;    // r_D(s+1)
     int Mc, ntx, ntiles;
     int rev;
+    int ylo, yhi;   // output rows [ylo, yhi) of A(s+1) (ylo even); whole level: 0, Mc + 1
   };
   using Acc = NoAcc;
   static __device__ void prefetch(const Params &P) {
@@ -362,13 +363,13 @@ struct OpRest2DAD {
   }
   static __device__ void init(Acc &) {}
   static __device__ void issue(const Params &P, int t, unsigned char *st, uint64_t *bar) {
-    const int X0 = (t % P.ntx) * TX, Y0 = (t / P.ntx) * TY;
+    const int X0 = (t % P.ntx) * TX, Y0 = P.ylo + (t / P.ntx) * TY;
     mbar_expect_tx(bar, E_BYTES + O_BYTES);
     tma_load_2d(st + E_OFF, &P.te, X0 - H1, Y0 - 1, bar);
     tma_load_2d(st + O_OFF, &P.to, X0 - H2, Y0 - 2, bar);
   }
   static __device__ void compute(const Params &P, int t, unsigned char *st, unsigned char *scr, Acc &) {
-    const int X0 = (t % P.ntx) * TX, Y0 = (t / P.ntx) * TY, Mc = P.Mc;
+    const int X0 = (t % P.ntx) * TX, Y0 = P.ylo + (t / P.ntx) * TY, Mc = P.Mc, yhi = P.yhi;
     const T *Eb = (const T *)(st + E_OFF), *Ob = (const T *)(st + O_OFF);
     T *Rb = (T *)scr;
     // r_A(s+1) at (X, Y), X = X0-1 .. X0+TX, Y = Y0-1 .. Y0+TY: pairs (X0-1+2p, X0+2p)
@@ -400,7 +401,7 @@ struct OpRest2DAD {
       T rc, rE, rN, ro;
       ld2(R.at(xl, y), rc, rE);
       ld2(R.at(xl, y + 1), rN, ro);
-      if (y <= Mc - 1) {
+      if (y <= Mc - 1 && y < yhi) {   // (yhi even: the pair's second row is inside too)
         const bool ok0 = xl >= 1 && xl <= Mc - 1, ok1 = xl + 1 <= Mc - 1;
         if (y >= 1) {
           if (ok0 && ok1)
@@ -675,6 +676,7 @@ struct OpJac2AD {
     int M, ntx, ntiles;
     int rev;
     T ca, cd;
+    int ylo, yhi;   // output rows [ylo, yhi) of D(s-1) E/O = A(s) rows (ylo even); whole level: 0, M/2 + 1
   };
   using Acc = NoAcc;
   static __device__ void prefetch(const Params &P) {
@@ -686,7 +688,7 @@ struct OpJac2AD {
   }
   static __device__ void init(Acc &) {}
   static __device__ void issue(const Params &P, int t, unsigned char *st, uint64_t *bar) {
-    const int a0 = (t % P.ntx) * TX, b0 = (t / P.ntx) * TY;
+    const int a0 = (t % P.ntx) * TX, b0 = P.ylo + (t / P.ntx) * TY;
     mbar_expect_tx(bar, RA_BYTES + 2 * VD_BYTES + RO_BYTES + RE_BYTES);
     tma_load_2d(st + RA_OFF, &P.tra, a0 - H2, b0 - 2, bar);
     tma_load_2d(st + VE_OFF, &P.tve, a0 / 2 - H2, b0 / 2 - 2, bar);
@@ -695,7 +697,7 @@ struct OpJac2AD {
     tma_load_2d(st + RE_OFF, &P.tre, a0, b0, bar);
   }
   static __device__ void compute(const Params &P, int t, unsigned char *st, unsigned char *scr, Acc &) {
-    const int a0 = (t % P.ntx) * TX, b0 = (t / P.ntx) * TY, W = P.M / 2;   // A(s) nodes 0 .. W
+    const int a0 = (t % P.ntx) * TX, b0 = P.ylo + (t / P.ntx) * TY, W = P.M / 2, yhi = P.yhi;   // A(s) nodes 0 .. W
     STile<T> RA = stile<T>(st + RA_OFF, RAW, a0 - H2, b0 - 2);
     STile<T> VE = stile<T>(st + VE_OFF, VDW, a0 / 2 - H2, b0 / 2 - 2);
     STile<T> VO = stile<T>(st + VO_OFF, VDW, a0 / 2 - H2, b0 / 2 - 2);
@@ -772,7 +774,7 @@ struct OpJac2AD {
       const T v0 = ok0 ? jac4(cd, ro0, va0, va1, vb1, vb0) : (T)0;
       const T v1 = ok1 ? jac4(cd, ro1, va1, va2, vb2, vb1) : (T)0;
       st2(OS.at(a, b), v0, v1);
-      if (okb && b >= b0 && a >= a0) {
+      if (okb && b >= b0 && b < yhi && a >= a0) {
         if (ok1)
           st2(&P.v.o[(int64_t)b * pitch + a], v0, v1);
         else if (ok0)
@@ -784,7 +786,7 @@ struct OpJac2AD {
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, a = a0 + 2 * lane;
 #pragma unroll
     for (int b = b0 + w; b < b0 + TY; b += NW) {
-      if (b < 1 || b > W - 1) continue;
+      if (b < 1 || b > W - 1 || b >= yhi) continue;
       T re0, re1, s0, s1, n0, n1;
       ld2(RE.at(a, b), re0, re1);
       ld2(OS.at(a, b - 1), s0, s1);
@@ -1045,13 +1047,18 @@ cudaError_t fast2_jac_d(const D2<T> &vc, const S2<T> &r, const S2<T> &v, int M, 
 }
 
 template <class T>
-cudaError_t fast2_rest_dad(const S2<T> &d, const D2<T> &ra, const S2<T> &rd, int Mc, cudaStream_t st, bool rev) {
+cudaError_t fast2_rest_dad(const S2<T> &d, const D2<T> &ra, const S2<T> &rd, int Mc, cudaStream_t st, bool rev,
+                           int ylo, int yhi) {
   using Op = OpRest2DAD<T, 2, 576, 32>;
   typename Op::Params P{};
   const int H = Mc + 1;   // E/O arrays of D(s) have Mc + 1 entries per side
   if (!tm2<T>(&P.te, d.e, H, H, d.pitch, Op::EW, Op::EH) || !tm2<T>(&P.to, d.o, H, H, d.pitch, Op::OW, Op::OH))
     return cudaErrorInvalidValue;
-  const int ntx = (Mc + TX - 1) / TX, nty = (Mc + Op::TY - 1) / Op::TY;
+  if (yhi < 0) yhi = Mc + 1;
+  if (yhi <= ylo) return cudaSuccess;
+  P.ylo = ylo;
+  P.yhi = yhi;
+  const int ntx = (Mc + TX - 1) / TX, nty = (yhi - ylo + Op::TY - 1) / Op::TY;
   P.ra = ra;
   P.rd = rd;
   P.Mc = Mc;
@@ -1067,7 +1074,7 @@ cudaError_t fast2_rest_dad(const S2<T> &d, const D2<T> &ra, const S2<T> &rd, int
 
 template <class T>
 cudaError_t fast2_jac_ad(const S2<T> &vd, const D2<T> &ra, T ca, const S2<T> &rd, const S2<T> &v, int M, T cd,
-                         cudaStream_t st, bool rev) {
+                         cudaStream_t st, bool rev, int ylo, int yhi) {
   using Op = OpJac2AD<T, 2, 512, 32>;   // Params and tile widths do not depend on NT / TY
   typename Op::Params P{};
   const int W = M / 2, H = W + 1, Hs = W / 2 + 1;
@@ -1082,7 +1089,9 @@ cudaError_t fast2_jac_ad(const S2<T> &vd, const D2<T> &ra, T ca, const S2<T> &rd
       !tm2<T>(&P.tro, rd.o, H, H, rd.pitch, Op::ROW, tyv + 1) ||
       !tm2<T>(&P.tre, rd.e, H, H, rd.pitch, Op::REW, tyv))
     return cudaErrorInvalidValue;
-  const int ntx = (W + TX - 1) / TX, nty = (W + tyv - 1) / tyv;
+  if (yhi < 0) yhi = W + 1;
+  if (yhi <= ylo) return cudaSuccess;
+  const int ntx = (W + TX - 1) / TX, nty = (yhi - ylo + tyv - 1) / tyv;
   P.v = v;
   P.M = M;
   P.ntx = ntx;
@@ -1090,6 +1099,8 @@ cudaError_t fast2_jac_ad(const S2<T> &vd, const D2<T> &ra, T ca, const S2<T> &rd
   P.rev = rev;
   P.ca = ca;
   P.cd = cd;
+  P.ylo = ylo;
+  P.yhi = yhi;
 #define AD_RUN(NTV, TYV) \
   return run_op<OpJac2AD<T, 2, NTV, TYV>>(reinterpret_cast<const typename OpJac2AD<T, 2, NTV, TYV>::Params &>(P), st)
   if (tyv == 8) {
@@ -1118,9 +1129,10 @@ cudaError_t fast2_jac_ad(const S2<T> &vd, const D2<T> &ra, T ca, const S2<T> &rd
   template cudaError_t fast2_rest_da<T>(const S2<T> &, const D2<T> &, int, cudaStream_t, const Rows2 &);           \
   template cudaError_t fast2_jac_d<T>(const D2<T> &, const S2<T> &, const S2<T> &, int, T, cudaStream_t,           \
                                       const Rows2 &);                                                              \
-  template cudaError_t fast2_rest_dad<T>(const S2<T> &, const D2<T> &, const S2<T> &, int, cudaStream_t, bool);   \
+  template cudaError_t fast2_rest_dad<T>(const S2<T> &, const D2<T> &, const S2<T> &, int, cudaStream_t, bool, int, \
+                                        int);                                                                      \
   template cudaError_t fast2_jac_ad<T>(const S2<T> &, const D2<T> &, T, const S2<T> &, const S2<T> &, int, T,      \
-                                       cudaStream_t, bool);
+                                       cudaStream_t, bool, int, int);
 
 INSTF(float)
 INSTF(double)

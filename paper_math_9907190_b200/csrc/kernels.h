@@ -111,15 +111,18 @@ template <class T>
 cudaError_t fast2_jac_d(const D2<T> &vc, const S2<T> &r, const S2<T> &v, int M, T c, cudaStream_t st,
                         const Rows2 &rw = Rows2());
 // rest_da of D(s) (r_A(s+1), written) fused with rest_ad of A(s+1) (r_D(s+1));
-// Mc = the size of A(s+1); whole level only (single GPU).
+// Mc = the size of A(s+1).
+// Rows [ylo, yhi) of A(s+1) (ylo even) only -- the slab solvers' bands; yhi < 0: the whole level.
 template <class T>
-cudaError_t fast2_rest_dad(const S2<T> &d, const D2<T> &ra, const S2<T> &rd, int Mc, cudaStream_t st, bool rev);
+cudaError_t fast2_rest_dad(const S2<T> &d, const D2<T> &ra, const S2<T> &rd, int Mc, cudaStream_t st, bool rev,
+                           int ylo = 0, int yhi = -1);
 // jac_a on A(s) (v_A(s) from v_D(s), r_A(s); M = the fine size of D(s-1))
 // fused with jac_d on D(s-1) (v_D(s-1) from v_A(s), r_D(s-1)): v_A(s) stays in
-// shared memory; whole level only (single GPU).
+// shared memory.
+// Rows [ylo, yhi) of D(s-1)'s E/O arrays (= A(s) rows; ylo even) only; yhi < 0: the whole level.
 template <class T>
 cudaError_t fast2_jac_ad(const S2<T> &vd, const D2<T> &ra, T ca, const S2<T> &rd, const S2<T> &v, int M, T cd,
-                         cudaStream_t st, bool rev);
+                         cudaStream_t st, bool rev, int ylo = 0, int yhi = -1);
 template <class T>
 void launch2_gather_d(const D2<T> &v, const S2<T> &d, int M, cudaStream_t st);
 template <class T>

@@ -103,18 +103,20 @@ def test_residual_and_norm_on_loopback_3d():
                                         (2049, 8, 1 << 10), (513, 2, 0)])
 def test_loopback_deep_halo_equals_single_gpu(n, P, agglom, dtype):
     """The one-exchange-per-cycle schedule (Dist2CA: deep ghost bands computed
-    redundantly) and the per-level schedule (MG_DIST_PERLEVEL=1)
-    both equal the single-GPU iterate and residual history bit for bit, with
-    agglomeration thresholds that distribute 1 to 6 octaves."""
+    redundantly) with the octave-pair passes on bands (default)
+    or the level passes (MG_DIST_NOFUSE=1), and the per-level schedule
+    (MG_DIST_PERLEVEL=1) all equal the single-GPU iterate and residual history
+    bit for bit, with agglomeration thresholds that distribute 1 to 6 octaves."""
     import os
     ref, href = _run(n, 2, dtype, 4)
-    for per_level in ("0", "1"):
-        os.environ["MG_DIST_PERLEVEL"] = per_level
+    for env in ({}, {"MG_DIST_NOFUSE": "1"}, {"MG_DIST_PERLEVEL": "1"}):
+        os.environ.update(env)
         try:
             got, h = _run(n, 2, dtype, 4, nranks=P, loopback=True, agglom=agglom)
         finally:
-            os.environ.pop("MG_DIST_PERLEVEL", None)
-        assert np.array_equal(got, ref), (per_level, float(np.max(np.abs(got - ref))))
+            for key in env:
+                os.environ.pop(key, None)
+        assert np.array_equal(got, ref), (env, float(np.max(np.abs(got - ref))))
         assert np.array_equal(h, href)
 
 

@@ -6,7 +6,7 @@ its tuned parameter, at the BASELINE sizes.  time/digit = (ms per V-cycle) /
 (-log10 rho-bar), rho-bar by the GPU power iteration at that size.  One JSON
 document.
 
-    python tools/compare_bench.py > profiles/r1_compare.json
+    python tools/compare_bench.py > profiles/r2_compare.json
 """
 import json
 import math
@@ -42,10 +42,15 @@ def one(dim, n, order, p, conventional, cycles, iters):
     prof = s.profile(s.alloc(), f, 3)
     alg = sum(r["alg_bytes"] for r in prof)
     N = (n - 2) ** dim
+    peak = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"] \
+        if os.path.exists(os.path.join(ROOT, "MEASURED_PEAKS.json")) else 6650.0
     out = dict(scheme="usual" if conventional else "diagonal", dim=dim, n=n, order=order,
                p=list(p) if isinstance(p, tuple) else [p], ms_per_cycle=ms, rho=rho,
                ms_per_digit=ms / -math.log10(rho), alg_bytes_per_cycle=alg,
-               alg_bytes_per_digit_per_dof=alg / N / -math.log10(rho), launches_per_cycle=s.launches_per_cycle)
+               alg_bytes_per_digit_per_dof=alg / N / -math.log10(rho), launches_per_cycle=s.launches_per_cycle,
+               # how close each implementation runs to the copy roofline on its own algorithmic bytes: the
+               # time-per-digit ratio mixes the methods' cost with the two implementations' efficiency
+               roofline_frac=alg / (ms * 1e-3) / 1e9 / peak)
     del s
     torch.cuda.empty_cache()
     return out
@@ -58,7 +63,11 @@ def main():
                                   (3, 257, 4, (0.91, 0.80, 0.70, 1.77), 1.70)]:
         d = one(dim, n, order, pd, False, 50 if dim == 2 else 20, 100)
         u = one(dim, n, order, pu, True, 50 if dim == 2 else 20, 100)
-        runs.append(dict(diagonal=d, usual=u, speedup_time_per_digit=u["ms_per_digit"] / d["ms_per_digit"]))
+        runs.append(dict(diagonal=d, usual=u, speedup_time_per_digit=u["ms_per_digit"] / d["ms_per_digit"],
+                         # the implementation-independent part: bytes per digit (= the time-per-digit ratio if
+                         # both ran at the same fraction of the roofline)
+                         speedup_at_equal_roofline_frac=u["alg_bytes_per_digit_per_dof"] /
+                         d["alg_bytes_per_digit_per_dof"]))
     print(json.dumps({"device": torch.cuda.get_device_name(0), "runs": runs}, indent=1))
 
 
