@@ -53,11 +53,15 @@ using namespace hs;
 // b in [b0, b0+15) (w >= 1); the ring a0-1 / b0-1 is colour 1 only.
 // L_j = {C_M(j), B_M(j), r_Fx/Fy/Fz(j-1), r_C(j-2)}.  Step j: faces of plane
 // j-1 (Erprolr), corners of plane j-2 (Erprolm).
-struct OpJacR3 {
+template <int NW_ = 16>
+struct OpJacR3T {
+  // NW warps: thread rows b0-1+w cover NW rows, NW-1 of them output rows
+  static constexpr int NW = NW_, NTH = 32 * NW, MINB = NW <= 8 ? 2 : 1;
+  static constexpr int RB = RW * NW * 8, BX = al128(34 * (NW + 1) * 8);
   static constexpr int NS = 6, PRO = 2, EPI = 2;
-  static constexpr int OC = 0, OB = BOX34, OR = 2 * BOX34;   // C box, B box, 4 r boxes (Fx, Fy, Fz, C)
-  static constexpr int SLOT = OR + 4 * RBOX;
-  static constexpr int GPL = 3 * RBOX;                       // face ring plane: Fx | Fy | Fz
+  static constexpr int OC = 0, OB = BX, OR = 2 * BX;   // C box, B box, 4 r boxes (Fx, Fy, Fz, C)
+  static constexpr int SLOT = OR + 4 * RB;
+  static constexpr int GPL = 3 * RB;                   // face ring plane: Fx | Fy | Fz
   static constexpr int SMEM = NS * SLOT + 3 * GPL;
   struct Params {
     CUtensorMap tc, tb, tr[4];   // C_M, B_M; r_R Fx, Fy, Fz, C
@@ -91,12 +95,12 @@ struct OpJacR3 {
   }
   static __device__ void issue(const Params &P, const Item &it, int j, unsigned char *slot, uint64_t *bar) {
     const bool wf = j >= it.zs, wc = j >= it.zs + 2;
-    mbar_expect_tx(bar, 2 * 34 * 17 * 8 + (wf ? 3 * RBOX : 0) + (wc ? RBOX : 0));
+    mbar_expect_tx(bar, 2 * 34 * (NW + 1) * 8 + (wf ? 3 * RB : 0) + (wc ? RB : 0));
     tma_load_3d(slot + OC, &P.tc, it.x0 - 2, it.y0 - 1, j, bar);
     tma_load_3d(slot + OB, &P.tb, it.x0 - 4, it.y0 - 2, j, bar);
     if (wf)
-      for (int i = 0; i < 3; i++) tma_load_3d(slot + OR + i * RBOX, &P.tr[i], it.x0 - 2, it.y0 - 1, j - 1, bar);
-    if (wc) tma_load_3d(slot + OR + 3 * RBOX, &P.tr[3], it.x0 - 2, it.y0 - 1, j - 2, bar);
+      for (int i = 0; i < 3; i++) tma_load_3d(slot + OR + i * RB, &P.tr[i], it.x0 - 2, it.y0 - 1, j - 1, bar);
+    if (wc) tma_load_3d(slot + OR + 3 * RB, &P.tr[3], it.x0 - 2, it.y0 - 1, j - 2, bar);
   }
   template <int PH>
   static __device__ __forceinline__ void step(const Params &P, State &S, const Ctx &Cx, const Item &it, int j,
@@ -129,7 +133,7 @@ struct OpJacR3 {
       {   // Fy (2a+1, 2b, 2c+1): normal y; in-plane (+1,0,+1),(-1,0,+1),(-1,0,-1),(+1,0,-1)
         T nrm = bc;
         nrm = nrm + Bc[-34];
-        T t = -(P.c1 * R[RBOX / 8]);
+        T t = -(P.c1 * R[RB / 8]);
         t = t + (T)2 * nrm;
         t = t + Cn[1];
         t = t + Cn[0];
@@ -140,7 +144,7 @@ struct OpJacR3 {
       {   // Fz (2a+1, 2b+1, 2c): normal z; in-plane (+1,+1,0),(+1,-1,0),(-1,-1,0),(-1,+1,0)
         T nrm = bc;
         nrm = nrm + bm;
-        T t = -(P.c1 * R[2 * RBOX / 8]);
+        T t = -(P.c1 * R[2 * RB / 8]);
         t = t + (T)2 * nrm;
         t = t + Cc[35];
         t = t + Cc[1];
@@ -151,8 +155,8 @@ struct OpJacR3 {
       {
         T *g = (T *)gz + orr;
         g[0] = fx;
-        g[RBOX / 8] = fy;
-        g[2 * RBOX / 8] = fz;
+        g[RB / 8] = fy;
+        g[2 * RB / 8] = fz;
       }
       if (Cx.core && c >= it.zs && c < it.ze) {
         const int64_t o = (int64_t)c * P.v.plane + (int64_t)b * P.v.pitch + a;
@@ -163,9 +167,9 @@ struct OpJacR3 {
       // ---- corners of plane q = j-2 from the faces of planes q (own: slot PH, ring gq) and q-1 (slot Q, gr)
       const int q = j - 2;
       if (q >= it.zs && Cx.core && Cx.a1k && Cx.b1k && m.z1(q)) {
-        const T *Gx = (const T *)gq + orr, *Gy = Gx + RBOX / 8, *Gz = Gx + 2 * RBOX / 8;
-        const T *Hx = (const T *)gr + orr, *Hy = Hx + RBOX / 8;
-        T t = -(P.c2 * R[3 * RBOX / 8]);
+        const T *Gx = (const T *)gq + orr, *Gy = Gx + RB / 8, *Gz = Gx + 2 * RB / 8;
+        const T *Hx = (const T *)gr + orr, *Hy = Hx + RB / 8;
+        T t = -(P.c2 * R[3 * RB / 8]);
         t = t + S.fz[PH];      // (+1,+1, 0)
         t = t + Gz[-RW];       // (+1,-1, 0)
         t = t + Gz[-RW - 1];   // (-1,-1, 0)
@@ -188,6 +192,7 @@ struct OpJacR3 {
   }
   static __device__ void finish(const Params &, State &) {}
 };
+using OpJacR3 = OpJacR3T<16>;
 
 // Two half-index rows per thread for the single-colour-ring passes below:
 // warp w owns rows b = b0 + 2w (+ ring offset) and the next one.
@@ -812,19 +817,30 @@ static bool tsub(CUtensorMap *tm, const S3<T> &s, int k, int H, int bx, int by) 
 }
 static inline int cdiv(int a, int b) { return (a + b - 1) / b; }
 
-cudaError_t fast3s_jac_r(const S3<double> &vm, const S3<double> &r, const S3<double> &v, int M, double c1, double c2,
-                         cudaStream_t st) {
-  using Op = OpJacR3;
-  Op::Params P{};
+template <int NW>
+static cudaError_t jac_r_nw(const S3<double> &vm, const S3<double> &r, const S3<double> &v, int M, double c1,
+                            double c2, cudaStream_t st) {
+  using Op = OpJacR3T<NW>;
+  typename Op::Params P{};
   const int H = M / 2 + 1;
-  if (!tsub(&P.tc, vm, C, H, 34, 17) || !tsub(&P.tb, vm, B, H, 34, 17) || !tsub(&P.tr[0], r, FX, H, RW, RH) ||
-      !tsub(&P.tr[1], r, FY, H, RW, RH) || !tsub(&P.tr[2], r, FZ, H, RW, RH) || !tsub(&P.tr[3], r, C, H, RW, RH))
+  if (!tsub(&P.tc, vm, C, H, 34, NW + 1) || !tsub(&P.tb, vm, B, H, 34, NW + 1) ||
+      !tsub(&P.tr[0], r, FX, H, RW, NW) || !tsub(&P.tr[1], r, FY, H, RW, NW) || !tsub(&P.tr[2], r, FZ, H, RW, NW) ||
+      !tsub(&P.tr[3], r, C, H, RW, NW))
     return cudaErrorInvalidValue;
   P.v = v;
   P.H = H;
   P.c1 = c1;
   P.c2 = c2;
-  return launch_zpipe<Op>(P, 30, 15, 0, 0, cdiv(H - 1, 30), cdiv(H - 1, 15), 0, H - 1, st);
+  return launch_zpipe<Op>(P, 30, NW - 1, 0, 0, cdiv(H - 1, 30), cdiv(H - 1, NW - 1), 0, H - 1, st);
+}
+
+// warps per CTA of the red Jacobi pass (MG_K3R_NW: 16 = one 512-thread CTA per
+// SM, 8 = two 256-thread CTAs per SM)
+cudaError_t fast3s_jac_r(const S3<double> &vm, const S3<double> &r, const S3<double> &v, int M, double c1, double c2,
+                         cudaStream_t st) {
+  static const int nw = getenv("MG_K3R_NW") ? atoi(getenv("MG_K3R_NW")) : 16;
+  if (nw == 8) return jac_r_nw<8>(vm, r, v, M, c1, c2, st);
+  return jac_r_nw<16>(vm, r, v, M, c1, c2, st);
 }
 
 template <int NW>

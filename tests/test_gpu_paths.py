@@ -88,6 +88,8 @@ CASES = [
     ({"MG_K3_NW": "16"}, 3, 129, 2, "float64"),
     ({"MG_K3S_NW": "16"}, 3, 129, 2, "float64"),
     ({"MG_K3S_NW": "8"}, 3, 257, 2, "float64"),
+    ({"MG_K3R_NW": "8"}, 3, 129, 2, "float64"),
+    ({"MG_K3R_NW": "8", "MG_K3_NWL": "8"}, 3, 257, 2, "float64"),
     # bounds checks of our own (compute-sanitizer is closed on the B200 pool): level arrays with
     # poisoned (NaN) guard rows and pitch padding; a stray read makes the iterate NaN, a stray
     # write trips the guard check in mg_destroy
