@@ -540,15 +540,22 @@ __device__ __forceinline__ unsigned long long gtimer() {
   return t;
 }
 
-// coarse octaves in shared memory: level arrays at fixed offsets of one arena
-template <class T>
+namespace cc3 {
+__host__ __device__ constexpr int ilog2(int v) { return v <= 1 ? 0 : 1 + ilog2(v / 2); }
+}
+// coarse octaves in shared memory: level arrays at fixed offsets of one arena.
+// MC > 0: M(oc) = MC known at compile time (the octave sizes, strides and
+// offsets become constants; the node bodies fold their bounds); MC = 0: read
+// from the descriptors.  Same steps, same order.
+template <class T, int MC>
 __device__ __forceinline__ void coarse3_block(const Tail3<T> &P, T *arena) {
-  const int tid = threadIdx.x, bs = blockDim.x, oc = P.oc, k = P.k;
+  const int tid = threadIdx.x, bs = blockDim.x, oc = P.oc, k = MC ? P.oc + cc3::ilog2(MC) : P.k;
+  auto Mof = [&](int o) { return MC ? (MC >> (o - oc)) : P.lv[o].M; };
   // octave o's arrays: 14 consecutive H^3 arrays starting at off(o)
   auto off = [&](int o) {
     size_t e = 0;
     for (int q = oc; q < o; q++) {
-      const size_t H = P.lv[q].M / 2 + 1;
+      const size_t H = Mof(q) / 2 + 1;
       e += 14 * H * H * H;
     }
     return arena + e;
@@ -575,12 +582,12 @@ __device__ __forceinline__ void coarse3_block(const Tail3<T> &P, T *arena) {
   // is read from global memory once, with every load of a thread in flight at
   // once, and v_G(oc) written back at the end (not one L2 round trip per
   // stencil access)
-  const int W = P.lv[oc].M + 1, W3 = W * W * W;
+  const int W = Mof(oc) + 1, W3 = W * W * W;
   T *g0 = off(k - 1);
   // G(s) of octave o: the staged copy at o = oc, else the G(2s) arrays of octave o-1
   auto gr = [&](int o, int which) -> D3<T> {
     if (o == oc) return D3<T>{g0 + (int64_t)which * W3, W, (int64_t)W * W};
-    const int H = P.lv[o - 1].M / 2 + 1;
+    const int H = Mof(o - 1) / 2 + 1;
     return D3<T>{off(o - 1) + (int64_t)(12 + which) * H * H * H, H, (int64_t)H * H};
   };
   D3<const T> none{nullptr, 0, 0};
@@ -614,8 +621,9 @@ __device__ __forceinline__ void coarse3_block(const Tail3<T> &P, T *arena) {
   }
   int nph = 0;
   if (P.dbg && tid == 0) P.dbg[0] = gtimer();
+#pragma unroll
   for (int o = oc; o + 1 < k; o++) {
-    const int M = P.lv[o].M, H = M / 2 + 1;
+    const int M = Mof(o), H = M / 2 + 1;
     T *base = off(o);
     const S3<T> rR = sub(base, H, {0, 3, 5, 6}, {0, 1, 2, 3}), rM = sub(base, H, {0, 7}, {8, 9});
     const D3<T> rG = gr(o, 0), rG2 = gr(o + 1, 0);
@@ -629,9 +637,10 @@ __device__ __forceinline__ void coarse3_block(const Tail3<T> &P, T *arena) {
     if (P.counter) *P.counter += 1;
   }
   __syncthreads();
+#pragma unroll
   for (int o = k - 2; o >= oc; o--) {
     const Lev3<T> &L = P.lv[o];
-    const int M = L.M, H = M / 2 + 1;
+    const int M = Mof(o), H = M / 2 + 1;
     T *base = off(o);
     const S3<T> rR = sub(base, H, {0, 3, 5, 6}, {0, 1, 2, 3}), vR = sub(base, H, {0, 3, 5, 6}, {4, 5, 6, 7});
     const S3<T> rM = sub(base, H, {0, 7}, {8, 9}), vM = sub(base, H, {0, 7}, {10, 11});
@@ -655,12 +664,15 @@ __device__ __forceinline__ void coarse3_block(const Tail3<T> &P, T *arena) {
   }
 }
 
-template <class T>
-__global__ void __launch_bounds__(512, 1) k3l_tail(const __grid_constant__ Tail3<T> P) {
+// The tail: the grid-wide octaves om .. oc-1 around CTA 0's coarse octaves
+// (MG = 0: sizes from the descriptors).
+template <class T, int MG>
+__device__ __forceinline__ void tail_run(const Tail3<T> &P, unsigned char *dsm) {
   namespace cg = cooperative_groups;
   cg::grid_group grid = cg::this_grid();
-  extern __shared__ __align__(16) unsigned char dsm[];
   const int gt = blockIdx.x * blockDim.x + threadIdx.x, gs = gridDim.x * blockDim.x;
+  const int om = P.om, oc = MG ? P.om + cc3::ilog2(MG) - cc3::ilog2(16) : P.oc;
+  auto Mof = [&](int o) { return MG ? (MG >> (o - om)) : P.lv[o].M; };
   auto cd = [](const D3<T> &a) { return D3<const T>{a.p, a.pitch, a.plane}; };
   auto cs = [](const S3<T> &a) {
     S3<const T> o;
@@ -683,29 +695,44 @@ __global__ void __launch_bounds__(512, 1) k3l_tail(const __grid_constant__ Tail3
     grid.sync();                                                   \
     if (gdbg) P.dbg[129 + (ngp++)] = gtimer();                     \
   }
-  for (int o = P.om; o < P.oc; o++) {
+#pragma unroll
+  for (int o = om; o < oc; o++) {
     const Lev3<T> &L = P.lv[o], &Lc = P.lv[o + 1];
-    const int H = L.M / 2 + 1;
-    LOOPG(H, b3_rest_gr(cd(L.rG), L.rR, L.M, H, a, b, c));
+    const int M = Mof(o), H = M / 2 + 1, Mc = M / 2;
+    LOOPG(H, b3_rest_gr(cd(L.rG), L.rR, M, H, a, b, c));
     LOOPG(H, b3_rest_rm(cs(L.rR), L.rM, H, a, b, c));
-    LOOPG(Lc.M + 1, b3_rest_mg(cs(L.rM), Lc.rG, Lc.M, a, b, c));
+    LOOPG(Mc + 1, b3_rest_mg(cs(L.rM), Lc.rG, Mc, a, b, c));
   }
-  if (blockIdx.x == 0) coarse3_block(P, (T *)dsm);
+  if (blockIdx.x == 0) {
+    switch (P.lv[P.oc].M) {   // the usual M(oc) <= 16 at compile time (the tail's coarse threshold)
+      case 16: coarse3_block<T, 16>(P, (T *)dsm); break;
+      case 8: coarse3_block<T, 8>(P, (T *)dsm); break;
+      case 4: coarse3_block<T, 4>(P, (T *)dsm); break;
+      default: coarse3_block<T, 0>(P, (T *)dsm); break;
+    }
+  }
   grid.sync();
   if (gdbg) P.dbg[129 + (ngp++)] = gtimer();
   D3<const T> none{nullptr, 0, 0};
   Coef<T> k0{};
-  for (int o = P.oc - 1; o >= P.om; o--) {
+#pragma unroll
+  for (int o = oc - 1; o >= om; o--) {
     const Lev3<T> &L = P.lv[o], &Lc = P.lv[o + 1];
-    const int H = L.M / 2 + 1;
+    const int M = Mof(o), H = M / 2 + 1;
     LOOPG(H, b3_jac_m1(cd(Lc.vG), cs(L.rM), L.vM, H, L.cMg, a, b, c));
     LOOPG(H, b3_jac_m2(cs(L.rM), L.vM, H, L.cMg, a, b, c));
     LOOPG(H, b3_jac_r1(cs(L.vM), cs(L.rR), L.vR, H, L.cR1, a, b, c));
     LOOPG(H, b3_jac_r2(cs(L.rR), L.vR, H, L.cR2, a, b, c));
-    LOOPG(H, (b3_jac_g1<T, 2, false>(cs(L.vR), cd(L.rG), none, none, L.vG, L.M, H, L.cG, k0, a, b, c)));
-    LOOPG(H, (b3_jac_g2<T, 2, false>(cd(L.rG), none, none, cd(L.vG), L.vG, L.M, H, L.cG, k0, a, b, c)));
+    LOOPG(H, (b3_jac_g1<T, 2, false>(cs(L.vR), cd(L.rG), none, none, L.vG, M, H, L.cG, k0, a, b, c)));
+    LOOPG(H, (b3_jac_g2<T, 2, false>(cd(L.rG), none, none, cd(L.vG), L.vG, M, H, L.cG, k0, a, b, c)));
   }
 #undef LOOPG
+}
+
+template <class T>
+__global__ void __launch_bounds__(512, 1) k3l_tail(const __grid_constant__ Tail3<T> P) {
+  extern __shared__ __align__(16) unsigned char dsm[];
+  tail_run<T, 0>(P, dsm);   // (compile-time grid sizes measured no faster: the steps are barrier-bound)
 }
 
 // ================================================================ launchers
