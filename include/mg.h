@@ -210,6 +210,14 @@ int mg_convergence_factor(mg_solver *s, void *e, int iters, double *rho, double 
 int mg_slab_plan(int dim, int64_t n, int nranks, int rank, int64_t agglom_points, int64_t *lo, int64_t *hi,
                  int64_t *ghost, int *agglom_octave);
 
+/* The multi-GPU schedule the slab solver picks (host-only): *schedule = 1 for
+ * the 2D communication-avoiding schedule (one halo exchange of *halo_rows
+ * fine rows of u per V-cycle, deep ghost bands computed redundantly;
+ * DESIGN.md 8), 0 for the per-level schedule (a halo exchange of 1-2 rows
+ * per level; *halo_rows = 2) -- always 0 in 3D and for one rank.
+ * MG_EUNSUPPORTED when the grid cannot be split that way. */
+int mg_slab_schedule(int dim, int64_t n, int nranks, int64_t agglom_points, int *schedule, int64_t *halo_rows);
+
 /* 128-byte NCCL unique id for cfg.nccl_id (call on one rank, broadcast the
  * bytes to all).  Loads the NCCL library at run time; MG_ENCCL if absent. */
 int mg_nccl_unique_id(void *out128);

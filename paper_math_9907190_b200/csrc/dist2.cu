@@ -472,34 +472,7 @@ struct Dist2CA : Dist2<T> {
   }
 
   static int up(int v, int m) { return (v + m - 1) / m * m; }
-  void plan() {
-    WD.assign(oa, 0);
-    WA.assign(oa + 1, 0);
-    waD.assign(oa, 0);
-    waA.assign(oa + 1, 0);
-    std::vector<int> rDneed(oa, 0), rAneed(oa + 1, 0);
-    // bands are whole rows of their level: D(s) half rows (2s fine rows), A(s)
-    // rows in pairs (2s; the A-level tiles start on even rows)
-    int reqD = 2;   // the finest ascent (A(1), own rows) reads v_D(1) within 2 rows
-    for (int o = 0; o < oa; o++) {
-      const int s_ = 1 << o;
-      waD[o] = up(reqD, 2 * s_);
-      rDneed[o] = waD[o] + s_;
-      const int reqA = waD[o] + 2 * s_;
-      if (o + 1 < oa) {
-        waA[o + 1] = up(reqA, 4 * s_);
-        rAneed[o + 1] = waA[o + 1] + 2 * s_;
-        reqD = waA[o + 1] + 4 * s_;
-      }
-    }
-    WA[oa] = 0;   // the agglomeration level: own rows (all-gathered)
-    for (int o = oa - 1; o >= 0; o--) {
-      const int s_ = 1 << o;
-      WD[o] = up(std::max(rDneed[o], WA[o + 1] + s_), 2 * s_);
-      if (o >= 1) WA[o] = up(std::max(rAneed[o], WD[o] + s_), 2 * s_);
-    }
-    Gu = up(WD[0] + 2, 2);
-  }
+  void plan() { Gu = slab_bands_2d(oa, WD, WA, waD, waA); }
 
   cudaError_t alloc() override {
     cudaError_t e = B::alloc();

@@ -1329,6 +1329,29 @@ int mg_slab_plan(int dim, int64_t n, int nranks, int rank, int64_t agglom_points
   return MG_OK;
 }
 
+int mg_slab_schedule(int dim, int64_t n, int nranks, int64_t agglom_points, int *schedule, int64_t *halo_rows) {
+  int k = log2_exact(n - 1);
+  if (k < 2 || nranks < 1 || (dim != 2 && dim != 3)) return MG_EINVAL;
+  if (nranks > 1 && (log2_exact(nranks) < 0 || (n - 1) / nranks < 4)) return MG_EUNSUPPORTED;
+  int sch = 0;
+  int64_t gu = 0;
+  if (nranks > 1) {
+    const int oa = slab_agglom_octave(n, k, nranks, agglom_points > 0 ? agglom_points : (int64_t(1) << 18), dim);
+    gu = 2;
+    if (dim == 2) {
+      std::vector<int> WD, WA, waD, waA;
+      const int g = slab_bands_2d(oa, WD, WA, waD, waA);
+      if (oa >= 1 && g <= (n - 1) / nranks) {   // as Dist2CA::alloc (without the MG_DIST_PERLEVEL override)
+        sch = 1;
+        gu = g;
+      }
+    }
+  }
+  if (schedule) *schedule = sch;
+  if (halo_rows) *halo_rows = gu;
+  return MG_OK;
+}
+
 int mg_nccl_unique_id(void *out) {
   if (!out) return MG_EINVAL;
   std::string err;

@@ -8,6 +8,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <memory>
+#include <algorithm>
 #include <string>
 #include <vector>
 
@@ -54,6 +55,41 @@ static inline int slab_agglom_octave(int64_t n, int k, int P, int64_t ag, int di
     if (pts < ag || M / P < 4) return o;
   }
   return k - 1;
+}
+
+// Ghost bands of the communication-avoiding 2D slab schedule (Dist2CA,
+// DESIGN.md 8), in fine rows, for oa distributed octaves: WD / WA the descent
+// bands of r_D(s) / r_A(s) (octave o), waD / waA the ascent bands of v_D(s) /
+// v_A(s); returns Gu, the rows of u a rank needs from each neighbour per cycle.
+// Bands are whole rows of their level (D(s): 2s fine rows; A(s): pairs of
+// rows, the A-level tiles start on even rows).
+static inline int slab_bands_2d(int oa, std::vector<int> &WD, std::vector<int> &WA, std::vector<int> &waD,
+                                std::vector<int> &waA) {
+  auto up = [](int v, int m) { return (v + m - 1) / m * m; };
+  WD.assign(oa, 0);
+  WA.assign(oa + 1, 0);
+  waD.assign(oa, 0);
+  waA.assign(oa + 1, 0);
+  std::vector<int> rDneed(oa, 0), rAneed(oa + 1, 0);
+  int reqD = 2;   // the finest ascent (A(1), own rows) reads v_D(1) within 2 rows
+  for (int o = 0; o < oa; o++) {
+    const int s_ = 1 << o;
+    waD[o] = up(reqD, 2 * s_);               // D(s) band w: v_A(2s) on w + 2s, r_D(s) on w + s
+    rDneed[o] = waD[o] + s_;
+    const int reqA = waD[o] + 2 * s_;
+    if (o + 1 < oa) {
+      waA[o + 1] = up(reqA, 4 * s_);         // A(2s) band w: v_D(2s) on w + 4s, r_A(2s) on w + 2s
+      rAneed[o + 1] = waA[o + 1] + 2 * s_;
+      reqD = waA[o + 1] + 4 * s_;
+    }
+  }
+  WA[oa] = 0;   // the agglomeration level: own rows (all-gathered)
+  for (int o = oa - 1; o >= 0; o--) {
+    const int s_ = 1 << o;
+    WD[o] = up(std::max(rDneed[o], WA[o + 1] + s_), 2 * s_);     // + the next restriction's reach
+    if (o >= 1) WA[o] = up(std::max(rAneed[o], WD[o] + s_), 2 * s_);
+  }
+  return up(WD[0] + 2, 2);   // the finest descent reads u within 2 rows of its band
 }
 
 // ---------------------------------------------------------------- profiler

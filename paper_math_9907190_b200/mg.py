@@ -82,6 +82,8 @@ EXPORTS = {
     "mg_slab_plan": (ctypes.c_int, [ctypes.c_int, ctypes.c_int64, ctypes.c_int, ctypes.c_int, ctypes.c_int64,
                                     ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_int64),
                                     ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_int)]),
+    "mg_slab_schedule": (ctypes.c_int, [ctypes.c_int, ctypes.c_int64, ctypes.c_int, ctypes.c_int64,
+                                        ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int64)]),
     "mg_nccl_unique_id": (ctypes.c_int, [ctypes.c_void_p]),
     "mg_strerror": (ctypes.c_char_p, [ctypes.c_int]),
     "mg_last_error": (ctypes.c_char_p, [ctypes.c_void_p]),
@@ -209,6 +211,14 @@ def mg_slab_plan(dim: int, n: int, nranks: int, rank: int, agglom_points: int = 
     _check(load().mg_slab_plan(dim, n, nranks, rank, agglom_points, ctypes.byref(lo), ctypes.byref(hi),
                                ctypes.byref(g), ctypes.byref(oa)), None, "mg_slab_plan")
     return lo.value, hi.value, g.value, oa.value
+
+
+def mg_slab_schedule(dim: int, n: int, nranks: int, agglom_points: int = 0):
+    """Host-only: (schedule, halo rows) -- 1 = communication-avoiding 2D slabs, 0 = per-level halos."""
+    sch, gu = ctypes.c_int(), ctypes.c_int64()
+    _check(load().mg_slab_schedule(dim, n, nranks, agglom_points, ctypes.byref(sch), ctypes.byref(gu)), None,
+           "mg_slab_schedule")
+    return sch.value, gu.value
 
 
 def mg_nccl_unique_id() -> bytes:

@@ -95,6 +95,22 @@ def _slab_body(rank, world):
     return bool(np.array_equal(glued, full[:world * (hi - lo)])), bool(ok_below), bool(ok_above)
 
 
+def _schedule_body(rank, world):
+    import torch
+    import torch.distributed as dist
+    from paper_math_9907190_b200 import build, mg
+    build.build()
+    out = []
+    for dim, n, P, ag in ((2, 8193, 8, 0), (2, 8193, 2, 0), (2, 257, 8, 0), (2, 257, 8, 16), (2, 1025, 4, 1 << 12),
+                          (3, 513, 8, 0), (2, 65, 2, 0)):
+        sch, gu = mg.mg_slab_schedule(dim, n, P, ag)
+        t = torch.tensor([sch, gu], dtype=torch.int64)
+        allt = [torch.zeros(2, dtype=torch.int64) for _ in range(world)]
+        dist.all_gather(allt, t)
+        out.append(((dim, n, P, ag), [x.tolist() for x in allt]))
+    return out
+
+
 # ------------------------------------------------------------------ tests
 
 def test_slab_plan_is_consistent_across_ranks():
@@ -124,3 +140,20 @@ def test_slabs_reassemble_the_field():
     out = _spawn("_slab_body")
     for r in (0, 1):
         assert out[r] == (True, True, True), out
+
+
+def test_slab_schedule_is_consistent_and_pinned():
+    """Every rank picks the same multi-GPU schedule: the 2D
+    communication-avoiding one with the band the stencils' reach gives (hand
+    derivation for one distributed octave: the finest ascent reads v_D(1)
+    within 2 rows, D(1) colour 1 r_D(1) within 3, the finest descent's band
+    rounds to 4 half-row-aligned rows, u within 4 + 2 = 6; at 8193^2 / 8 ranks
+    with agglomeration at A(16), 108 rows), the per-level one when the band
+    exceeds a slab and always in 3D."""
+    out = _spawn("_schedule_body")
+    assert not isinstance(out[0], str), out
+    want = {(2, 8193, 8, 0): [1, 108], (2, 8193, 2, 0): [1, 108], (2, 257, 8, 0): [1, 6], (2, 257, 8, 16): [0, 2],
+            (2, 1025, 4, 1 << 12): [1, 108], (3, 513, 8, 0): [0, 2], (2, 65, 2, 0): [1, 6]}
+    for (key, rows), (key1, rows1) in zip(out[0], out[1]):
+        assert key == key1 and rows == rows1
+        assert rows[0] == rows[1] == want[tuple(key)], (key, rows)

@@ -58,29 +58,6 @@ def agglom_octave(dim, n, P, ag=1 << 18):
     return k - 1
 
 
-def band_2d(oa):
-    """Gu of Dist2CA::plan (fine rows)."""
-    up = lambda v, m: (v + m - 1) // m * m
-    WD, WA = [0] * oa, [0] * (oa + 1)
-    waD, waA, rDn, rAn = [0] * oa, [0] * (oa + 1), [0] * oa, [0] * (oa + 1)
-    reqD = 2
-    for o in range(oa):
-        s = 1 << o
-        waD[o] = up(reqD, 2 * s)
-        rDn[o] = waD[o] + s
-        reqA = waD[o] + 2 * s
-        if o + 1 < oa:
-            waA[o + 1] = up(reqA, 4 * s)
-            rAn[o + 1] = waA[o + 1] + 2 * s
-            reqD = waA[o + 1] + 4 * s
-    for o in range(oa - 1, -1, -1):
-        s = 1 << o
-        WD[o] = up(max(rDn[o], WA[o + 1] + s), 2 * s)
-        if o >= 1:
-            WA[o] = up(max(rAn[o], WD[o] + s), 2 * s)
-    return up(WD[0] + 2, 2)
-
-
 def main():
     import torch
     from paper_math_9907190_b200 import workloads as W
@@ -113,7 +90,8 @@ def main():
             row_b = w.n * esz if w.dim == 2 else w.n * w.n * esz
             R = (w.n - 1) // P
             if w.dim == 2:
-                gu = band_2d(oa)
+                from paper_math_9907190_b200.mg import mg_slab_schedule
+                gu = mg_slab_schedule(2, w.n, P)[1]
                 rounds = 1                                   # one u exchange per cycle
                 xbytes = gu * row_b * 2                      # both neighbours (concurrent)
                 ag_bytes = (((w.n - 1) >> oa) + 1) * (((w.n - 1) >> oa) + 1) * esz
