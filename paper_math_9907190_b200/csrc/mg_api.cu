@@ -980,8 +980,11 @@ static int ensure_stage(mg_solver *s) {
   return MG_OK;
 }
 
-// rows x n elements between two layouts (pitches in elements)
+// rows x n elements between two layouts (pitches in elements); one contiguous
+// copy when the layouts agree (a pitched host<->device copy of 64 KB rows is
+// slower than one linear DMA transfer)
 static cudaError_t copy_field(mg_solver *s, void *dst, int64_t dp, const void *src, int64_t sp, cudaMemcpyKind kind) {
+  if (dp == sp) return cudaMemcpyAsync(dst, src, (size_t)s->rows() * sp * s->esz, kind, s->st);
   return cudaMemcpy2DAsync(dst, dp * s->esz, src, sp * s->esz, s->cfg.n * s->esz, s->rows(), kind, s->st);
 }
 
