@@ -95,6 +95,9 @@ enum { MG_FLAG_CONVENTIONAL = 2 };  /* the paper's "usual" multigrid instead of 
                                        reading A18), over-relaxation p = p[0] (2D) / p[3] (3D) on the
                                        residual term.  Single GPU; every call of this header applies
                                        (mg_num_levels / mg_level_points describe the diagonal hierarchy). */
+enum { MG_FLAG_SLABS = 4 };  /* run the multi-GPU slab solver also for nranks = 1 (one rank owns every row:
+                                 the whole transport -- NCCL with cfg.nccl_id, or loopback -- runs with no
+                                 neighbours; used to execute the NCCL path on a one-GPU machine) */
 enum { MG_NORM_INF = 0, MG_NORM_L2 = 1 };
 
 typedef struct {

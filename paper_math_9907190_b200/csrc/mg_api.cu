@@ -766,7 +766,7 @@ static int check_config(const mg_config *c, int *k_out) {
   if (c->sweeps < 0 || c->sweeps > 8) return MG_EINVAL;
   if (c->sweeps > 1 && (c->dim != 2 || c->nranks > 1 || (c->flags & MG_FLAG_CONVENTIONAL))) return MG_EUNSUPPORTED;
   if (c->nranks < 0 || (c->nranks > 1 && (c->rank < 0 || c->rank >= c->nranks))) return MG_EINVAL;
-  if (c->nranks > 1) {
+  if (c->nranks > 1 || (c->flags & MG_FLAG_SLABS)) {
     // y-slabs (2D, dist2.cu) / z-slabs (3D, dist3.cu) of the hierarchy
     if (log2_exact(c->nranks) < 0 || ((c->n - 1) / c->nranks) < 4) return MG_EUNSUPPORTED;
     int64_t pt = c->pitch ? c->pitch : c->n;
@@ -815,7 +815,7 @@ int mg_create_ex(const mg_config *cfg, mg_solver **out) {
     // the work layout: the caller's when its rows are 16-byte multiples, else
     // n rounded up to 128 bytes for the solvers that run the TMA kernels
     // (single GPU, diagonal scheme, one sweep); the others read any pitch
-    const bool tma = cfg->nranks <= 1 && !(cfg->flags & MG_FLAG_CONVENTIONAL) && cfg->sweeps <= 1 &&
+    const bool tma = cfg->nranks <= 1 && !(cfg->flags & (MG_FLAG_CONVENTIONAL | MG_FLAG_SLABS)) && cfg->sweeps <= 1 &&
                      !env_flag("MG_FORCE_REF");
     const int64_t q = 128 / s->esz;
     s->wpitch = ((s->pitch * s->esz) % 16 == 0 || !tma) ? s->pitch : round_up(cfg->n, q);
@@ -844,12 +844,12 @@ int mg_create_ex(const mg_config *cfg, mg_solver **out) {
   CKS(sp, cudaMemset(s->d_l2, 0, sizeof(double) * kHistCap));
   CKS(sp, cudaMallocHost(&s->h_l2, sizeof(double) * kHistCap));
   if (cfg->flags & MG_FLAG_CONVENTIONAL) {
-    if (cfg->nranks > 1) {
+    if (cfg->nranks > 1 || (cfg->flags & MG_FLAG_SLABS)) {
       mg_destroy(s.release());
       return MG_EUNSUPPORTED;
     }
     s->impl.reset(make_conv(sp));
-  } else if (cfg->nranks > 1) {
+  } else if (cfg->nranks > 1 || (cfg->flags & MG_FLAG_SLABS)) {
     std::string why;
     const bool lb = (cfg->flags & MG_FLAG_LOOPBACK) != 0;
     ImplBase *d = cfg->dim == 2 ? make_dist2(sp, lb, &why) : make_dist3(sp, lb, &why);
@@ -1139,7 +1139,8 @@ int mg_vcycle_host(mg_solver *s, void *u_host, const void *f_host, int ncycles, 
 int mg_convergence_factor(mg_solver *s, void *e_user, int iters, double *rho, double *ratios) {
   if (!s) return MG_EINVAL;
   if (!e_user || iters < 2 || !rho) return fail(s, MG_EINVAL, "mg_convergence_factor: bad argument");
-  if (s->cfg.nranks > 1) return fail(s, MG_EUNSUPPORTED, "mg_convergence_factor: single GPU only");
+  if (s->cfg.nranks > 1 || (s->cfg.flags & MG_FLAG_SLABS))
+    return fail(s, MG_EUNSUPPORTED, "mg_convergence_factor: single GPU only");
   DeviceGuard g(s->device);
   int rc = begin(s);
   if (rc) return rc;

@@ -26,6 +26,7 @@ MG_F64, MG_F32 = 0, 1
 MG_NORM_INF, MG_NORM_L2 = 0, 1
 MG_FLAG_LOOPBACK = 1
 MG_FLAG_CONVENTIONAL = 2
+MG_FLAG_SLABS = 4
 
 
 class MGError(RuntimeError):
@@ -277,7 +278,8 @@ class Solver:
 
     def __init__(self, dim: int, n: int, order: int = 2, p=None, dtype=None, device=None,
                  pitch: int | None = None, stream=None, nranks: int = 1, rank: int = 0, group=None,
-                 loopback: bool = False, agglom_points: int = 0, conventional: bool = False, sweeps: int = 1):
+                 loopback: bool = False, agglom_points: int = 0, conventional: bool = False, sweeps: int = 1,
+                 slabs: bool = False):
         import torch
         if not torch.cuda.is_available():
             raise MGError(MG_ENODEV, "no CUDA device (libmg has no CPU path)")
@@ -316,7 +318,13 @@ class Solver:
         elif nranks > 1:
             self._id = ctypes.create_string_buffer(broadcast_nccl_id(group), 128)
             cfg.nccl_id = ctypes.cast(self._id, ctypes.c_void_p)
+        elif slabs:   # the slab solver over a one-rank NCCL communicator (tests the transport on one GPU)
+            self._id = ctypes.create_string_buffer(mg_nccl_unique_id(), 128)
+            cfg.nccl_id = ctypes.cast(self._id, ctypes.c_void_p)
+        if slabs:
+            cfg.flags |= MG_FLAG_SLABS
         self.nranks, self.rank, self.loopback = nranks, rank, loopback
+        self.slabs = (nranks > 1 or slabs) and not loopback
         self.h = mg_create_ex(cfg)
         lo, hi, g = mg_local_extent(self.h)
         self.lo, self.hi, self.ghost = lo, hi, g
@@ -331,7 +339,7 @@ class Solver:
     @property
     def shape(self):
         """Shape of a field as this rank passes it (the slab with ghost rows in multi-GPU mode)."""
-        if self.nranks > 1 and not self.loopback:
+        if self.slabs:
             rows = self.hi - self.lo + 2 * self.ghost
             return (rows, self.pitch) if self.dim == 2 else (rows, self.n, self.pitch)
         return (self.n, self.pitch) if self.dim == 2 else (self.n, self.n, self.pitch)
