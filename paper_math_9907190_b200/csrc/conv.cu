@@ -265,7 +265,9 @@ struct ImplConv : ImplBase {
     coef.c6 = (T)((double)(n - 1) * (double)(n - 1) / 6.0);
     return cudaSuccess;
   }
-  NormSink sink() const { return NormSink{s->d_hist, s->d_counter, kHistCap, s->sum_l2 ? s->d_l2 : nullptr}; }
+  NormSink sink() const {
+    return NormSink{hist_on(s) ? s->d_hist : nullptr, s->d_counter, kHistCap, s->sum_l2 ? s->d_l2 : nullptr};
+  }
   dim3 grid(int cnt, int nz = 1) const { return dim3((cnt + BX - 1) / BX, (cnt + BY - 1) / BY, nz); }
 
   template <class U>

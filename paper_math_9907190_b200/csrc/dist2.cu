@@ -155,7 +155,9 @@ struct Dist2 : ImplBase {
     return cudaMemcpy(d_lev, lv.data(), sizeof(Lev2<T>) * k, cudaMemcpyHostToDevice);
   }
 
-  NormSink sink() const { return NormSink{s->d_hist, s->d_counter, kHistCap, s->sum_l2 ? s->d_l2 : nullptr}; }
+  NormSink sink() const {
+    return NormSink{hist_on(s) ? s->d_hist : nullptr, s->d_counter, kHistCap, s->sum_l2 ? s->d_l2 : nullptr};
+  }
   size_t local_elems() const override { return loop ? 0 : (size_t)(R(0) + 4) * pitch; }
   bool extent(int64_t *l, int64_t *h, int64_t *g) const override {
     if (loop) return false;
@@ -462,7 +464,7 @@ struct Dist2CA : Dist2<T> {
     std::vector<D2<T>> rA, vA;   // 1 <= o < oa
   };
   std::vector<Full> fl;   // per local rank
-  cudaGraphExec_t gexec[2][2] = {};   // the cycle u[p] -> u[p^1], [p][L2 sums on]
+  cudaGraphExec_t gexec[2][4] = {};   // the cycle u[p] -> u[p^1], [p][L2 sums on | history on]
 
   Dist2CA(mg_solver *sv, bool loopback) : B(sv, loopback) {}
   ~Dist2CA() override {
@@ -644,7 +646,7 @@ struct Dist2CA : Dist2<T> {
   // loopback copies are capturable) and replayed
   int run_graph(mg_solver *sv, int cur) {
     cudaStream_t st = sv->st;
-    cudaGraphExec_t &gx = gexec[cur][s->sum_l2 ? 1 : 0];
+    cudaGraphExec_t &gx = gexec[cur][(s->sum_l2 ? 1 : 0) | (s->want_hist ? 2 : 0)];
     if (!gx) {
       cudaGraph_t g = nullptr;
       CKS(sv, cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));

@@ -176,7 +176,9 @@ struct Dist3 : ImplBase {
     return cudaMemcpy(d_lev, lv.data(), sizeof(Lev3<T>) * k, cudaMemcpyHostToDevice);
   }
 
-  NormSink sink() const { return NormSink{s->d_hist, s->d_counter, kHistCap, s->sum_l2 ? s->d_l2 : nullptr}; }
+  NormSink sink() const {
+    return NormSink{hist_on(s) ? s->d_hist : nullptr, s->d_counter, kHistCap, s->sum_l2 ? s->d_l2 : nullptr};
+  }
   size_t local_elems() const override { return loop ? 0 : (size_t)(R(0) + 4) * fplane(); }
   bool extent(int64_t *l, int64_t *h, int64_t *g) const override {
     if (loop) return false;

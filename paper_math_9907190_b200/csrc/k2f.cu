@@ -198,7 +198,7 @@ struct OpDesc2Fine {
     for (int y = y0 + w; y < y0 + TY; y += NW) {
       rpair(U, F, xl, y, M, P.k, r0, r1);
       st2(R.at(xl, y), r0, r1);
-      if (y < yhi) {
+      if (y < yhi && P.ns.slots) {   // the residual norm only when a history is wanted
         acc.mx = nmax(nmax(acc.mx, absd(r0)), absd(r1));
         if (P.ns.sums(y)) acc.ss += sq((double)r0) + sq((double)r1);
       }

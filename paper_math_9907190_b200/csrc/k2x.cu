@@ -141,7 +141,7 @@ struct Strip {
   Pair<T> R[4];        // r(u_new)
   unsigned long long mx;   // max |r| as the bit pattern of a non-negative double (NaN sorts above inf)
   double ss;               // sum r^2 over the lane's output nodes (a16 L2 norm; single GPU: all rows)
-  bool l2on;
+  bool l2on, hist;         // L2 sum / any residual norm wanted
   // interior warps address by increments: next load row offset, next E / O
   // v_D load pointers, u_new store pointer of row j-2, next Erest2r offset
   int64_t lo, rso;
@@ -180,6 +180,7 @@ struct Strip {
     mx = 0ull;
     ss = 0.0;
     l2on = P.ns.l2 != nullptr;
+    hist = P.ns.slots != nullptr;
   }
   // incremental addressing from step j0 on (row-interior blocks only)
   __device__ __forceinline__ void start(int j0) {
@@ -333,7 +334,7 @@ struct Strip {
     }
     // r_new at row j-3 (rows j-4, j-3, j-2 of u_new)
     R[s3] = res(N[s0], N[s3], N[s2], fpair(j - 3), r3, ka, kb);
-    if (outl && j - 3 >= ys && j - 3 < ye) {
+    if (hist && outl && j - 3 >= ys && j - 3 < ye) {
       const unsigned long long a = absbits(R[s3].a), b = absbits(R[s3].b), m = a > b ? a : b;
       mx = m > mx ? m : mx;
       if (l2on) ss += sq((double)R[s3].a) + sq((double)R[s3].b);
@@ -457,7 +458,7 @@ struct StripQ {
   Q4 R[4];
   unsigned long long mx;
   double ss;   // sum r^2 (a16 L2 norm)
-  bool l2on;
+  bool l2on, hist;
   static constexpr int SLOT = 32 * 40, FO = 32 * 16, DO = 32 * 32;
 
   __device__ __forceinline__ StripQ(const XParamsQ &P, int x_, int ys_, int ye_, unsigned char *ring_) {
@@ -480,6 +481,7 @@ struct StripQ {
     mx = 0ull;
     ss = 0.0;
     l2on = P.ns.l2 != nullptr;
+    hist = P.ns.slots != nullptr;
   }
   __device__ __forceinline__ bool rin(int y) const { return (unsigned)(y - 1) < (unsigned)(M - 1); }
   __device__ __forceinline__ void issue(int y) const {
@@ -579,7 +581,7 @@ struct StripQ {
       const Q4 f3 = ld4(ring + ((j - 3) & (DEPTH - 1)) * SLOT + FO);
       const RowQ cr{N4[s3], Nw[s3], Ne[s3]};
       R[s3] = res(N4[s0], cr, N4[s2], f3, r3);
-      if (outl && j - 3 >= ys && j - 3 < ye) {
+      if (hist && outl && j - 3 >= ys && j - 3 < ye) {
         auto ab = [](float v) { return (unsigned long long)__double_as_longlong((double)v) & 0x7fffffffffffffffull; };
         unsigned long long m = ab(R[s3].a);
         m = max(m, ab(R[s3].b));

@@ -275,7 +275,7 @@ struct OpDesc3Fine {
       R[0] = r0;
       R[RH2] = r1;
       // norm: every interior node once -- the tile core on the unit's own planes
-      if (p >= un.zs && p < un.ze && w >= 1 && w <= TY3 && lane >= 1 && lane <= TX3 / 2) {
+      if (P.ns.slots && p >= un.zs && p < un.ze && w >= 1 && w <= TY3 && lane >= 1 && lane <= TX3 / 2) {
         acc.mx = nmax(nmax(acc.mx, absd(r0)), absd(r1));
         if (P.ns.sums(p)) acc.ss += sq((double)r0) + sq((double)r1);
       }

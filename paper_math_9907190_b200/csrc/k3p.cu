@@ -167,9 +167,11 @@ struct OpDesc3P {
         sel0(rn[1][0], zin && C.m.rB && C.m.c0);
         sel0(rn[1][1], zin && C.m.rB && C.m.c1);
       }
-      // every computed r is a true residual (or 0): max over all of them
-      S.mx = umax64(S.mx, umax64(umax64(absbits(rn[0][0]), absbits(rn[0][1])),
-                                 umax64(absbits(rn[1][0]), absbits(rn[1][1]))));
+      // every computed r is a true residual (or 0): max over all of them (only
+      // when a residual history is wanted: the pass is instruction-bound)
+      if (P.ns.slots)
+        S.mx = umax64(S.mx, umax64(umax64(absbits(rn[0][0]), absbits(rn[0][1])),
+                                   umax64(absbits(rn[1][0]), absbits(rn[1][1]))));
       if (z >= it.zs && z < it.ze && P.ns.sums(z)) {   // the sum counts the core nodes once
         if (C.sA) S.ss += sq((double)rn[0][0]) + sq((double)rn[0][1]);
         if (C.sB) S.ss += sq((double)rn[1][0]) + sq((double)rn[1][1]);

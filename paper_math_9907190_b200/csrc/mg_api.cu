@@ -142,7 +142,9 @@ struct Impl2 : ImplBase {
     return cudaMemcpy(d_lev, lv.data(), sizeof(Lev2<T>) * k, cudaMemcpyHostToDevice);
   }
 
-  NormSink sink() const { return NormSink{s->d_hist, s->d_counter, kHistCap, s->sum_l2 ? s->d_l2 : nullptr}; }
+  NormSink sink() const {
+    return NormSink{hist_on(s) ? s->d_hist : nullptr, s->d_counter, kHistCap, s->sum_l2 ? s->d_l2 : nullptr};
+  }
 
   bool fuses_cycles() const override { return use_fast && xfuse; }
   void enqueue_cycle_mode(const void *u_in, void *u_out, const void *f_eff, cudaStream_t st, Prof *prof,
@@ -477,7 +479,9 @@ struct Impl3 : ImplBase {
     return cudaMemcpy(d_lev, lv.data(), sizeof(Lev3<T>) * k, cudaMemcpyHostToDevice);
   }
 
-  NormSink sink() const { return NormSink{s->d_hist, s->d_counter, kHistCap, s->sum_l2 ? s->d_l2 : nullptr}; }
+  NormSink sink() const {
+    return NormSink{hist_on(s) ? s->d_hist : nullptr, s->d_counter, kHistCap, s->sum_l2 ? s->d_l2 : nullptr};
+  }
   void desc_fine(const void *u, const void *f_eff, cudaStream_t st) {
     if (use_fast && ((uintptr_t)u & 15) == 0 && ((uintptr_t)f_eff & 15) == 0)
       fast3_desc_fine<T>((const T *)u, (const T *)f_eff, pitch, rR[0], M[0], s->cfg.order, coef, sink(), st);
@@ -699,7 +703,9 @@ static void drop_graphs(mg_solver *s) {
 static int run_cycle(mg_solver *s, const void *u_in, void *u_out, const void *f_eff, int mode) {
   cudaGraphExec_t ex = nullptr;
   for (auto &g : s->graphs)
-    if (g.uin == u_in && g.uout == u_out && g.f == f_eff && g.mode == mode && g.l2 == s->sum_l2) ex = g.exec;
+    if (g.uin == u_in && g.uout == u_out && g.f == f_eff && g.mode == mode && g.l2 == s->sum_l2 &&
+        g.hist == hist_on(s))
+      ex = g.exec;
   if (!ex) {
     if (s->graphs.size() >= 16) drop_graphs(s);
     cudaGraph_t g = nullptr;
@@ -723,7 +729,7 @@ static int run_cycle(mg_solver *s, const void *u_in, void *u_out, const void *f_
     e = cudaGraphInstantiate(&ex, g, 0);
     cudaGraphDestroy(g);
     CKS(s, e);
-    s->graphs.push_back({ex, u_in, u_out, f_eff, mode, s->sum_l2});
+    s->graphs.push_back({ex, u_in, u_out, f_eff, mode, s->sum_l2, hist_on(s)});
   }
   CKS(s, cudaGraphLaunch(ex, s->st));
   return MG_OK;
@@ -1085,10 +1091,12 @@ int mg_vcycle_norms(mg_solver *s, void *u, const void *f, int ncycles, double *r
   if (rc) return rc;
   s->l2_out = res_l2;
   s->sum_l2 = res_l2 != nullptr;
+  s->want_hist = res_inf != nullptr;
   rc = s->impl->vcycle_all(s, u, f, ncycles, res_inf);
   if (rc == 1) rc = vcycle_dev(s, u, f, ncycles, res_inf);
   s->l2_out = nullptr;
   s->sum_l2 = false;
+  s->want_hist = false;
   int rc2 = end(s);
   return rc ? rc : rc2;
 }
@@ -1119,8 +1127,10 @@ int mg_vcycle_host(mg_solver *s, void *u_host, const void *f_host, int ncycles, 
       CKS(s, copy_field(s, s->d_f_stage, s->wpitch, f_host, s->pitch, cudaMemcpyHostToDevice));
     }
     // (loopback slabs take the raw f: one layout there, so d_f_stage holds it as given)
+    s->want_hist = res_hist != nullptr;
     int r = s->impl->vcycle_all(s, s->d_u_stage, s->d_f_stage, ncycles, res_hist);
     if (r == 1) r = cycles_work(s, s->d_u_stage, fe, ncycles, res_hist);
+    s->want_hist = false;
     if (r) return r;
     CKS(s, copy_field(s, u_host, s->pitch, s->d_u_stage, s->wpitch, cudaMemcpyDeviceToHost));
     CKS(s, cudaStreamSynchronize(s->st));

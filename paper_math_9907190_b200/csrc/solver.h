@@ -140,6 +140,10 @@ struct Prof {
   } while (0)
 
 // ---------------------------------------------------------------- solver
+struct mg_solver;
+// the passes compute the residual norms (MG_NORM_ALWAYS=1: in every call, as round 1 did -- A/B only)
+static bool hist_on(const mg_solver *s);
+
 struct ImplBase {
   virtual ~ImplBase() {}
   virtual cudaError_t alloc() = 0;
@@ -267,7 +271,7 @@ struct mg_solver {
     cudaGraphExec_t exec;
     const void *uin, *uout, *f;
     int mode;
-    bool l2;
+    bool l2, hist;
   };
   std::vector<GraphEntry> graphs;   // captured cycles keyed by pointers
   void *d_ualt = nullptr;            // out-of-place partner of the caller's u
@@ -275,6 +279,8 @@ struct mg_solver {
   unsigned long long *h_hist = nullptr;    // pinned
   double *d_l2 = nullptr, *h_l2 = nullptr;  // per-cycle sums of r^2 (kHistCap slots; host copy pinned)
   double *l2_out = nullptr;                // the current call's L2 history destination (mg_vcycle_norms) or null
+  bool want_hist = false;                  // the current call asked for a residual history: the passes
+                                           // compute the norms only then (the finest passes are instruction-bound)
   bool sum_l2 = false;                     // the current call's passes accumulate sum r^2 (only when asked:
                                            // it costs the issue-bound fp32 fused pass ~7 %)
   std::string err;
@@ -334,3 +340,7 @@ static cudaError_t clear_hist(mg_solver *s, int nslots, cudaStream_t st) {
   return e;
 }
 
+static bool hist_on(const mg_solver *s) {
+  static const bool always = env_flag("MG_NORM_ALWAYS");
+  return s->want_hist || always;
+}
