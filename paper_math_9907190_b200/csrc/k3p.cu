@@ -62,7 +62,7 @@ __device__ __forceinline__ void sel0(T &v, bool keep) {
 // i.e. PH at z = j-1 and Q = 1-PH at q = j-2; row B the other way round.
 // FINE = false: the same pass one octave down (G(s) -> R(s), s > 1): r is
 // read from the dense level array (the "f" box) instead of computed, no norm.
-template <class T, bool FINE = true, int NW_ = 16, int NSO = 0>
+template <class T, bool FINE = true, int NW_ = 16, int NSO = 0, bool UNIF = true>
 struct OpDesc3P {
   using Gm = Geo<T, NW_>;
   static constexpr int NW = NW_, NTH = Gm::NTH, MINB = NW <= 8 ? 2 : 1;
@@ -187,7 +187,9 @@ struct OpDesc3P {
       // ---- Erred at the red nodes of q = j-2: r(q-1) = S.r[Q], r(q) = S.r[PH], r(q+1) = rn.
       // Red column of row A at q is Q, of row B is PH.
       const int q = j - 2;
-      if (q >= it.zs && q >= 1 && q <= M - 1 && (C.oA[PH] || C.oB[PH])) {
+      // warp-uniform condition only: the lanes without an output compute too and
+      // skip the stores (a lane-dependent branch here cost a divergence region per step)
+      if (q >= it.zs && q >= 1 && q <= M - 1 && (UNIF || C.oA[PH] || C.oB[PH])) {
         const T(&R1)[2][2] = S.r[PH];
         const T(&R0)[2][2] = S.r[Q];
         const T *g = (const T *)gq + (2 * w + 1) * GS + (lane + 1);
@@ -262,7 +264,7 @@ struct OpDesc3P {
 // column of row A at plane q = j-2 is Q as well.
 // FINE = false: Egprolg/Egprolr one octave down (G(s) from R(s), s > 1): r is
 // read from the dense level array (the "f" box) and v_G(s) is written.
-template <class T, bool FINE = true, int NW_ = 16, int NSO = 0>
+template <class T, bool FINE = true, int NW_ = 16, int NSO = 0, bool UNIF = true>
 struct OpAsc3P {
   using Gm = Geo<T, NW_>;
   static constexpr int NW = NW_, NTH = Gm::NTH, MINB = NW <= 8 ? 2 : 1;
@@ -415,7 +417,7 @@ struct OpAsc3P {
       }
       // ---- Egprolr at the red nodes of q = j-2 (row A col Q, row B col PH), then u_new
       const int q = j - 2;
-      if (q >= it.zs && q >= 1 && q <= M - 1 && (C.oA || C.oB)) {
+      if (q >= it.zs && q >= 1 && q <= M - 1 && (UNIF || C.oA || C.oB)) {   // warp-uniform (see OpDesc3P)
         const T *g = (const T *)gq + (2 * w + 1) * GS + (lane + 1);
         const T ymA = g[-GS], ypB = g[2 * GS];
         const T(&g1)[2] = S.g[PH];   // greens of plane q
@@ -489,10 +491,10 @@ static int k3p_nw() {
   return nw == 8 ? 8 : 16;
 }
 
-template <class T, int NW, int NSO = 0>
+template <class T, int NW, int NSO = 0, bool UNIF = true>
 static cudaError_t desc_fine_nw(const T *u, const T *f, int64_t pitch, const S3<T> &rr, int M, const Coef<T> &k,
                                 const NormSink &ns, cudaStream_t st, const ZRange3 &pz) {
-  using Op = OpDesc3P<T, true, NW, NSO>;
+  using Op = OpDesc3P<T, true, NW, NSO, UNIF>;
   using Gm = typename Op::Gm;
   typename Op::Params P{};
   const int64_t n = M + 1, plane = pitch * n, nz = pz.fplanes < 0 ? n : pz.fplanes;
@@ -510,14 +512,16 @@ static cudaError_t desc_fine_nw(const T *u, const T *f, int64_t pitch, const S3<
 template <class T>
 cudaError_t fast3p_desc_fine(const T *u, const T *f, int64_t pitch, const S3<T> &rr, int M, const Coef<T> &k,
                              const NormSink &ns, cudaStream_t st, const ZRange3 &pz) {
+  static const bool div = env_flag("MG_K3_DIV");   // A/B: round 1's lane-dependent output branch
+  if (k3p_nw() == 8 && div) return desc_fine_nw<T, 8, 0, false>(u, f, pitch, rr, M, k, ns, st, pz);
   if (k3p_nw() == 8) return desc_fine_nw<T, 8>(u, f, pitch, rr, M, k, ns, st, pz);
   return desc_fine_nw<T, 16>(u, f, pitch, rr, M, k, ns, st, pz);
 }
 
-template <class T, int NW, int NSO = 0>
+template <class T, int NW, int NSO = 0, bool UNIF = true>
 static cudaError_t asc_fine_nw(const S3<T> &vr, const T *u_old, const T *f, int64_t pitch, T *u_new, int M, T c,
                                const Coef<T> &k, cudaStream_t st, const ZRange3 &pz) {
-  using Op = OpAsc3P<T, true, NW, NSO>;
+  using Op = OpAsc3P<T, true, NW, NSO, UNIF>;
   using Gm = typename Op::Gm;
   typename Op::Params P{};
   const int64_t n = M + 1, plane = pitch * n, nz = pz.fplanes < 0 ? n : pz.fplanes;
@@ -541,6 +545,8 @@ static cudaError_t asc_fine_nw(const S3<T> &vr, const T *u_old, const T *f, int6
 template <class T>
 cudaError_t fast3p_asc_fine(const S3<T> &vr, const T *u_old, const T *f, int64_t pitch, T *u_new, int M, T c,
                             const Coef<T> &k, cudaStream_t st, const ZRange3 &pz) {
+  static const bool div = env_flag("MG_K3_DIV");
+  if (k3p_nw() == 8 && div) return asc_fine_nw<T, 8, 0, false>(vr, u_old, f, pitch, u_new, M, c, k, st, pz);
   if (k3p_nw() == 8) return asc_fine_nw<T, 8>(vr, u_old, f, pitch, u_new, M, c, k, st, pz);
   return asc_fine_nw<T, 16>(vr, u_old, f, pitch, u_new, M, c, k, st, pz);
 }
