@@ -76,6 +76,7 @@ struct OpJacR3T {
   };
   struct Ctx {
     bool a0k, a1k, b0k, b1k, core;   // a in [0,H-2] / [1,H-2], b likewise, core column
+    int64_t o0;                      // (a, b) in a plane of the sublattice arrays
   };
   static __device__ void prefetch(const Params &P) {
     tma_prefetch_desc(&P.tc);
@@ -92,6 +93,7 @@ struct OpJacR3T {
     C.b0k = m.z0(b);
     C.b1k = m.z1(b);
     C.core = l >= 2 && w >= 1;
+    C.o0 = (int64_t)b * P.v.pitch + a;
   }
   static __device__ void issue(const Params &P, const Item &it, int j, unsigned char *slot, uint64_t *bar) {
     const bool wf = j >= it.zs, wc = j >= it.zs + 2;
@@ -159,7 +161,7 @@ struct OpJacR3T {
         g[2 * RB / 8] = fz;
       }
       if (Cx.core && c >= it.zs && c < it.ze) {
-        const int64_t o = (int64_t)c * P.v.plane + (int64_t)b * P.v.pitch + a;
+        const int64_t o = (int64_t)c * P.v.plane + Cx.o0;
         if (Cx.a1k && Cx.b0k && cz0) __stcs(P.v.s[FX] + o, fx);
         if (Cx.a0k && Cx.b1k && cz0) __stcs(P.v.s[FY] + o, fy);
         if (Cx.a0k && Cx.b0k && cz1) __stcs(P.v.s[FZ] + o, fz);
@@ -182,7 +184,7 @@ struct OpJacR3T {
         t = t + S.fx[Q];       // ( 0,+1,-1)
         t = t + Hx[-RW];       // ( 0,-1,-1)
         t = t + Gx[-RW];       // ( 0,-1,+1)
-        __stcs(P.v.s[C] + (int64_t)q * P.v.plane + (int64_t)b * P.v.pitch + a, t * (T)(1.0 / 12.0));
+        __stcs(P.v.s[C] + (int64_t)q * P.v.plane + Cx.o0, t * (T)(1.0 / 12.0));
       }
       S.fx[Q] = fx;
       S.fy[Q] = fy;
@@ -227,6 +229,7 @@ struct OpJacM3T {
   };
   struct Ctx {
     bool b0k[2], b1k[2], core[2];   // per row: (a, b) in [0,H-2]^2 / [1,H-2]^2, core node
+    T *pb[2], *pc[2];               // per row: v_M B / C at (a, b) of plane 0 (+ c * plane per step)
   };
   static __device__ void prefetch(const Params &P) {
     tma_prefetch_desc(&P.tg);
@@ -244,6 +247,9 @@ struct OpJacM3T {
       C.b0k[R] = m.z0(a) && m.z0(b);
       C.b1k[R] = m.z1(a) && m.z1(b);
       C.core[R] = l >= 2 && (w >= 1 || R == 1);
+      const int64_t o = (int64_t)b * P.v.pitch + a;
+      C.pb[R] = P.v.s[hs::B] + o;
+      C.pc[R] = P.v.s[hs::C] + o;
     }
   }
   static __device__ void issue(const Params &P, const Item &it, int j, unsigned char *slot, uint64_t *bar) {
@@ -282,8 +288,7 @@ struct OpJacM3T {
       const bool ok = Cx.b0k[R] && czin;
       bn[R] = ok ? t * (T)0.125 : (T)0;
       ((T *)gz)[orr] = bn[R];
-      const int b = it.y0 - 1 + 2 * w + R;
-      if (ok && Cx.core[R] && cout) __stcs(P.v.s[B] + (int64_t)c * P.v.plane + (int64_t)b * P.v.pitch + a, bn[R]);
+      if (ok && Cx.core[R] && cout) __stcs(Cx.pb[R] + (int64_t)c * P.v.plane, bn[R]);
       if (qok && Cx.core[R] && Cx.b1k[R]) {
         const T *G0 = (const T *)gq + orr, *G1 = (const T *)gr + orr;   // centres of planes q, q-1
         T u = -(P.cc * Rb[RB2 / 8]);
@@ -295,7 +300,7 @@ struct OpJacM3T {
         u = u + G1[-1];          // (a-1, b, c-1)
         u = u + G0[-RW - 1];     // (a-1, b-1, c)
         u = u + G1[-RW - 1];     // (a-1, b-1, c-1)
-        __stcs(P.v.s[C] + (int64_t)q * P.v.plane + (int64_t)b * P.v.pitch + a, u * (T)0.125);
+        __stcs(Cx.pc[R] + (int64_t)q * P.v.plane, u * (T)0.125);
       }
     }
     S.bo[Q][0] = bn[0];
