@@ -109,6 +109,11 @@ struct XParams {
   T c;
   Coef<T> k;
   NormSink ns;
+  // octave pair fused in (RD strips): r_A(2) (pitch rap) and
+  // r_D(2) E/O (pitch r2p) of the next cycle's descent; Mc = M / 2
+  T *ra, *r2e, *r2o;
+  int64_t rap, r2p;
+  int Mc;
 };
 
 // prefetched inputs of one row
@@ -122,9 +127,11 @@ struct In {
 // shifted between steps.  Loads are unconditional from clamped addresses:
 // rows outside [0, M] and columns outside [0, M] only feed nodes that are
 // not interior, whose results are all selected away (inside() is false).
-template <class T, int ORDER, int DEPTH>   // DEPTH: ring slots per lane (power of 2)
+template <class T, int ORDER, int DEPTH, bool RD = false>   // DEPTH: ring slots per lane (power of 2)
 struct Strip {
   static constexpr int LA = lookahead<T>();
+  static constexpr int H = RD ? 8 : 4;   // halo columns per side
+  static constexpr int SWK = 64 - 2 * H;  // output columns per strip
   const T *pu, *pf, *pve, *pvo;
   T *pun, *pre, *pro;
   int64_t pitch, vp, rp;
@@ -139,6 +146,7 @@ struct Strip {
   T G[4];              // green value of the row
   Row<T> N[4];         // u_new
   Pair<T> R[4];        // r(u_new)
+  T Os[2], A[2];       // RD: r_D(1) O and r_A(2) of the last two row pairs, by (row pair & 1)
   unsigned long long mx;   // max |r| as the bit pattern of a non-negative double (NaN sorts above inf)
   double ss;               // sum r^2 over the lane's output nodes (a16 L2 norm; single GPU: all rows)
   bool l2on, hist;         // L2 sum / any residual norm wanted
@@ -170,13 +178,14 @@ struct Strip {
     ca = x >= 1 && x <= M - 1;
     cb = x + 1 >= 1 && x + 1 <= M - 1;
     const int lane = threadIdx.x & 31;
-    outl = lane >= 2 && lane < 30;
+    outl = lane >= H / 2 && lane < 32 - H / 2;
 #pragma unroll
     for (int i = 0; i < 4; i++) {
       U[i] = N[i] = Row<T>{0, 0, 0, 0};
       RO[i] = R[i] = Pair<T>{0, 0};
       Dv[i] = G[i] = (T)0;
     }
+    Os[0] = Os[1] = A[0] = A[1] = (T)0;
     mx = 0ull;
     ss = 0.0;
     l2on = P.ns.l2 != nullptr;
@@ -277,7 +286,7 @@ struct Strip {
   // RE: a row of this step (computed, restricted or loaded) may lie outside
   // the interior (masks and clamped loads); CE: the same for the warp's columns
   template <int K, bool RE, bool CE>
-  __device__ __forceinline__ void step(int j) {
+  __device__ __forceinline__ void step(int j, const XParams<T> &P) {
     constexpr int PAR = K & 1;
     constexpr int s0 = K, s1 = (K + 3) & 3, s2 = (K + 2) & 3, s3 = (K + 1) & 3;   // rows j, j-1, j-2, j-3 (j-4: s0)
     // row j: wait for its copies (the LA - 1 younger groups may stay in flight),
@@ -344,59 +353,97 @@ struct Strip {
       const int y = j - 5;
       const Pair<T> R6 = R[s2], R5 = R[s1], R4 = R[s0], R3 = R[s3];
       const T rW = shup(R5.b), rE = shdn(R4.a);
+      // interior D(1) nodes E = (x, y), O = (x+1, y+1) (the lower bounds only matter for halo lanes)
+      const bool inE = (!CE || (x >= 2 && x <= M - 2)) && (!RE || (y >= 2 && y <= M - 2));
+      const bool inO = (!CE || (x + 1 >= 1 && x + 1 <= M - 1)) && (!RE || (y + 1 >= 1 && y + 1 <= M - 1));
+      const T ev = erest2r(R5.a, rW, R6.a, R5.b, R4.a), ov = erest2r(R4.b, R4.a, R5.b, rE, R3.b);
       if (outl && y >= ys && y < ye) {
         const int64_t o = RE ? (int64_t)(y >> 1) * rp + (x >> 1) : rso;
-        if ((!CE || (x >= 2 && x <= M - 2)) && (!RE || (y >= 2 && y <= M - 2)))
-          pre[o] = erest2r(R5.a, rW, R6.a, R5.b, R4.a);
-        if ((!CE || x + 1 <= M - 1) && (!RE || y + 1 <= M - 1)) pro[o] = erest2r(R4.b, R4.a, R5.b, rE, R3.b);
+        if (inE) pre[o] = ev;
+        if (inO) pro[o] = ov;
       }
       if (!RE) rso += rp;
+      if constexpr (RD) restrict_pair<K, RE, CE>(y, inE ? ev : (T)0, inO ? ov : (T)0, P);
     }
     if (!RE) stp += pitch;
   }
+  // RD: the next cycle's octave pair D(1) -> A(2) -> D(2) (OpRest2DAD's node
+  // formulas and operand order) from the row pair (y, y+1) of r_D(1) just
+  // formed: Erest2b at the A(2) node (X, Y) = (x/2, y/2) of the lane,
+  // then Erest2r at the D(2) node of A(2) row Y-1 (E on even rows at
+  // even X, O on odd rows at odd X).  e, o: E(X, Y), O(X, Y) of D(1), zero outside.
+  template <int K, bool RE, bool CE>
+  __device__ __forceinline__ void restrict_pair(int y, T e, T o, const XParams<T> &P) {
+    constexpr int h = K >> 1;   // K = 1: h = 0, K = 3: h = 1 (row pairs alternate)
+    const int X = x >> 1, Y = y >> 1, Mc = P.Mc;
+    const T oW = shup(o), opW = shup(Os[h ^ 1]);   // O(X-1, Y), O(X-1, Y-1)
+    T ra = erest2b(e, opW, Os[h ^ 1], o, oW);
+    const bool inA = (!CE || (X >= 1 && X <= Mc - 1)) && (!RE || (Y >= 1 && Y <= Mc - 1));
+    ra = inA ? ra : (T)0;
+    const bool seg = outl && y >= ys && y < ye;
+    if (seg && inA) P.ra[(int64_t)Y * P.rap + X] = ra;
+    // r_A(2) rows Y-2 (A[h]), Y-1 (A[h^1]), Y (ra) -> D(2) at row Yd = Y - 1
+    const T c = A[h ^ 1], w = shup(c), ea = shdn(c);
+    const T d2 = erest2r(c, w, A[h], ea, ra);
+    const int Yd = Y - 1, yd = 2 * Yd;
+    if (outl && yd >= ys && yd < ye) {
+      const int64_t od = (int64_t)(Yd >> 1) * P.r2p + (X >> 1);
+      if (K == 3) {   // Yd even: E at even X
+        if (!(X & 1) && (!CE || (X >= 2 && X <= Mc - 2)) && (!RE || (Yd >= 2 && Yd <= Mc - 2))) P.r2e[od] = d2;
+      } else {        // Yd odd: O at odd X
+        if ((X & 1) && (!CE || X <= Mc - 1) && (!RE || Yd <= Mc - 1)) P.r2o[od] = d2;
+      }
+    }
+    A[h] = ra;
+    Os[h] = o;
+  }
   template <bool RE, bool CE>
-  __device__ __forceinline__ void steps(int j) {
-    step<0, RE, CE>(j);
-    step<1, RE, CE>(j + 1);
-    step<2, RE, CE>(j + 2);
-    step<3, RE, CE>(j + 3);
+  __device__ __forceinline__ void steps(int j, const XParams<T> &P) {
+    step<0, RE, CE>(j, P);
+    step<1, RE, CE>(j + 1, P);
+    step<2, RE, CE>(j + 2, P);
+    step<3, RE, CE>(j + 3, P);
   }
 };
 
-template <class T, int ORDER, int DEPTH, int MINB>
+template <class T, int ORDER, int DEPTH, int MINB, bool RD = false>
 __global__ void __launch_bounds__(32, MINB) asc_desc_stream(const __grid_constant__ XParams<T> P) {
+  using St = Strip<T, ORDER, DEPTH, RD>;
+  constexpr int H = St::H, SWK = St::SWK;
   const int lane = threadIdx.x & 31;
   const int item = blockIdx.x;
   const int nseg = (P.M + P.seg - 1) / P.seg;
   unsigned long long mx = 0ull;
   double ss = 0.0;
+  (void)SWK;
   if (item < P.nstrips * nseg) {   // warp-uniform
     const int strip = item % P.nstrips, sg = item / P.nstrips;
     const int ys = sg * P.seg, ye = min(ys + P.seg, P.M);
     extern __shared__ __align__(16) unsigned char xsm[];
-    Strip<T, ORDER, DEPTH> S(P, strip * SW - 4 + 2 * lane, ys, ye,
-                      xsm + lane * (2 * sizeof(T)));
-    const int j0 = ys - 4, jend = ye + 3;   // steps j0 .. jend: ye - ys + 8 of them, a multiple of 4
+    St S(P, strip * SWK - H + 2 * lane, ys, ye, xsm + lane * (2 * sizeof(T)));
+    // steps j0 .. jend: ye - ys + 8 (RD: + 16) of them, a multiple of 4; RD
+    // also needs r_D(1) three rows above and below the segment
+    const int j0 = ys - (RD ? 8 : 4), jend = ye + (RD ? 7 : 3);
 #pragma unroll
     constexpr int LA = lookahead<T>();
     for (int i = 0; i < LA; i++) S.issue(j0 + i);
     // A block of 4 steps j..j+3 is row-interior when every row it computes,
-    // restricts or loads lies inside: j >= 8 and j + 3 + LA <= M.
-    // Column-interior warps: lanes' columns x0-4 .. x0+59 inside [1, M-1].
-    const int x0 = strip * SW;
-    const bool ce = x0 - 4 < 1 || x0 + 59 > P.M - 1;
-    auto rowin = [&](int j) { return j >= 8 && j + 3 + LA <= P.M; };
+    // restricts or loads lies inside: j >= 8 (RD: 12) and j + 3 + LA <= M.
+    // Column-interior warps: lanes' columns x0-H .. x0-H+63 inside [1, M-1].
+    const int x0 = strip * SWK;
+    const bool ce = x0 - H < 1 || x0 - H + 63 > P.M - 1;
+    auto rowin = [&](int j) { return j >= (RD ? 12 : 8) && j + 3 + LA <= P.M; };
     int j = j0;
-    for (; j <= jend && !rowin(j); j += 4) S.template steps<true, true>(j);
+    for (; j <= jend && !rowin(j); j += 4) S.template steps<true, true>(j, P);
     if (j <= jend) {
       S.start(j);
       if (ce) {
-        for (; j <= jend && rowin(j); j += 4) S.template steps<false, true>(j);
+        for (; j <= jend && rowin(j); j += 4) S.template steps<false, true>(j, P);
       } else {
-        for (; j <= jend && rowin(j); j += 4) S.template steps<false, false>(j);
+        for (; j <= jend && rowin(j); j += 4) S.template steps<false, false>(j, P);
       }
     }
-    for (; j <= jend; j += 4) S.template steps<true, true>(j);
+    for (; j <= jend; j += 4) S.template steps<true, true>(j, P);
     mx = S.mx;
     ss = S.ss;
   }
@@ -649,7 +696,7 @@ __global__ void __launch_bounds__(32, 16) asc_desc_stream_q(const __grid_constan
 
 }  // namespace xf
 
-template <class T, int ORDER, int DEPTH, int MINB>
+template <class T, int ORDER, int DEPTH, int MINB, bool RD = false>
 static cudaError_t asc_desc_launch_w(const xf::XParams<T> &P0, cudaStream_t st) {
   constexpr int SMEM = DEPTH * 32 * 5 * sizeof(T);
   static int wres = 0, sms = 0;
@@ -657,11 +704,12 @@ static cudaError_t asc_desc_launch_w(const xf::XParams<T> &P0, cudaStream_t st) 
     int dev = 0, nb = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, xf::asc_desc_stream<T, ORDER, DEPTH, MINB>, 32, SMEM);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, xf::asc_desc_stream<T, ORDER, DEPTH, MINB, RD>, 32, SMEM);
     wres = nb > 0 ? nb : 1;
     if (sms <= 0) sms = 148;
   }
   xf::XParams<T> P = P0;
+  P.nstrips = (P.M + xf::Strip<T, ORDER, DEPTH, RD>::SWK - 1) / xf::Strip<T, ORDER, DEPTH, RD>::SWK;
   // exactly one wave: at most sms * wres warps (a second, partial wave would
   // double the tail), a segment of >= 32 rows (multiple of 4) each
   const int S = max(1, (sms * wres) / P.nstrips);
@@ -670,7 +718,7 @@ static cudaError_t asc_desc_launch_w(const xf::XParams<T> &P0, cudaStream_t st) 
   if (seg < 32) seg = 32;
   P.seg = seg;
   const int nitems = P.nstrips * ((P.M + seg - 1) / seg);
-  xf::asc_desc_stream<T, ORDER, DEPTH, MINB><<<nitems, 32, SMEM, st>>>(P);
+  xf::asc_desc_stream<T, ORDER, DEPTH, MINB, RD><<<nitems, 32, SMEM, st>>>(P);
   return cudaGetLastError();
 }
 
@@ -709,6 +757,7 @@ static cudaError_t asc_desc_launch_q(const xf::XParams<float> &P0, cudaStream_t 
 // fp32 +2 %).
 template <class T, int ORDER>
 static cudaError_t asc_desc_launch(const xf::XParams<T> &P, cudaStream_t st) {
+  if (P.ra) return asc_desc_launch_w<T, ORDER, 8, (ORDER == 2 ? 16 : 1), true>(P, st);
   if constexpr (std::is_same<T, float>::value && ORDER == 2) {
     static const bool pairs = env_flag("MG_XF_PAIRS");
     if (!pairs) return asc_desc_launch_q<3>(P, st);   // lookahead 2 / 3 / 4 rows: 0.459 / 0.457 / 0.461 ms
@@ -718,7 +767,8 @@ static cudaError_t asc_desc_launch(const xf::XParams<T> &P, cudaStream_t st) {
 
 template <class T>
 cudaError_t fast2_asc_desc(const S2<T> &vd, const T *u_old, const T *f, int64_t pitch, T *u_new, const S2<T> &d,
-                           int M, int order, T c, const Coef<T> &k, const NormSink &ns, cudaStream_t st, bool rev) {
+                           int M, int order, T c, const Coef<T> &k, const NormSink &ns, cudaStream_t st, bool rev,
+                           const D2<T> *ra, const S2<T> *d2) {
   (void)rev;   // the strips are walked top-down; no serpentine variant
   // vector loads of the pair (x, x+1), x even, may touch column M+1: the row
   // pitch must leave a padding word and rows must be 2-word aligned
@@ -737,6 +787,15 @@ cudaError_t fast2_asc_desc(const S2<T> &vd, const T *u_old, const T *f, int64_t 
   P.rp = d.pitch;
   P.M = M;
   P.nstrips = (M + xf::SW - 1) / xf::SW;
+  if (ra && d2) {   // the next descent's octave pair D(1) -> A(2) -> D(2) as well
+    if (M % 4) return cudaErrorInvalidValue;
+    P.ra = ra->p;
+    P.rap = ra->pitch;
+    P.r2e = d2->e;
+    P.r2o = d2->o;
+    P.r2p = d2->pitch;
+    P.Mc = M / 2;
+  }
   P.c = c;
   P.k = k;
   P.ns = ns;
@@ -745,9 +804,10 @@ cudaError_t fast2_asc_desc(const S2<T> &vd, const T *u_old, const T *f, int64_t 
 
 template cudaError_t fast2_asc_desc<float>(const S2<float> &, const float *, const float *, int64_t, float *,
                                            const S2<float> &, int, int, float, const Coef<float> &, const NormSink &,
-                                           cudaStream_t, bool);
+                                           cudaStream_t, bool, const D2<float> *, const S2<float> *);
 template cudaError_t fast2_asc_desc<double>(const S2<double> &, const double *, const double *, int64_t, double *,
                                             const S2<double> &, int, int, double, const Coef<double> &,
-                                            const NormSink &, cudaStream_t, bool);
+                                            const NormSink &, cudaStream_t, bool, const D2<double> *,
+                                            const S2<double> *);
 
 }  // namespace mg

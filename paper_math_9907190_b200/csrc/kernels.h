@@ -103,10 +103,12 @@ template <class T>
 cudaError_t fast2_rest_da(const S2<T> &d, const D2<T> &r, int Mc, cudaStream_t st, const Rows2 &rw = Rows2());
 // Finest ascent of one cycle fused with the finest descent of the next
 // (u_new = u_old + v_A(1); r = f - L u_new -> Erest2r onto d; max|r| -> ns);
-// whole domain only (single GPU).
+// whole domain only (single GPU).  ra, d2 non-null: the next descent's octave
+// pair as well (r_A(2) -> ra, r_D(2) -> d2, fast2_rest_dad's results).
 template <class T>
 cudaError_t fast2_asc_desc(const S2<T> &vd, const T *u_old, const T *f, int64_t pitch, T *u_new, const S2<T> &d,
-                           int M, int order, T c, const Coef<T> &k, const NormSink &ns, cudaStream_t st, bool rev);
+                           int M, int order, T c, const Coef<T> &k, const NormSink &ns, cudaStream_t st, bool rev,
+                           const D2<T> *ra = nullptr, const S2<T> *d2 = nullptr);
 template <class T>
 cudaError_t fast2_jac_d(const D2<T> &vc, const S2<T> &r, const S2<T> &v, int M, T c, cudaStream_t st,
                         const Rows2 &rw = Rows2());

@@ -30,6 +30,9 @@ struct Impl2 : ImplBase {
   D2<T> tmpA{};            // sweeps > 1: E nodes of v_D(s) as a dense A(2s)-shaped array
   S2<T> tmpD{};            //             D nodes of v_A(s) as split E/O arrays
   bool xfuse = !env_flag("MG_2D_NOXFUSE");   // cross-cycle fusion of the finest ascent and descent
+  // ... which also runs the next descent's octave pair D(1) -> A(2) -> D(2) (r_D(1) not re-read): opt-in
+  // (MG_2D_XRD=1), measured slower on B200 at 8193^2: fp64 0.7575 vs 0.7453 ms, fp32 0.480 vs 0.452
+  bool xrd = env_flag("MG_2D_XRD");
   bool adfuse = !env_flag("MG_2D_NOADFUSE");  // jac_a(s) fused with jac_d(s-1): v_A(s) stays on chip
   // ... for octaves s >= ad_min (MG_AD_MINO, default 1): 16-row tiles, two 90 KB CTAs of 512 threads per SM
   bool dafuse = !env_flag("MG_2D_NODAFUSE");  // rest_da(s) fused with rest_ad(s+1): r_A(s+1) not re-read
@@ -147,6 +150,8 @@ struct Impl2 : ImplBase {
   }
 
   bool fuses_cycles() const override { return use_fast && xfuse; }
+  // the fused pass also ran rest_dad(0) (decided once per solver: producer and consumer cycles agree)
+  bool xrd_on() const { return fuses_cycles() && xrd && dafuse && da_min == 0 && 1 < (use_tail ? om : oc) && M[0] % 4 == 0; }
   void enqueue_cycle_mode(const void *u_in, void *u_out, const void *f_eff, cudaStream_t st, Prof *prof,
                           int mode) override {
     if (use_fast) return enqueue_fast(u_in, u_out, f_eff, st, prof, mode);
@@ -248,15 +253,27 @@ struct Impl2 : ImplBase {
         STEP("jac_a", 2 * o, 1, w * (Nl[2 * o + 1] + 2 * Nl[2 * o]));
         fast2_jac_a<T>(vD[o], rA[o], vA[o], M[o], cA[o], st, bwd);
       } else if (mode & kFuseNext) {
-        STEP("asc_desc", 0, 1, w * (2 * Nl[1] + 3 * Nl[0]));
-        fast2_asc_desc<T>(vD[0], uin, fe, pitch, (T *)u_out, rD[0], M[0], s->cfg.order, cA[0], coef, sink(), st,
-                          serp);
+        if (xrd_on()) {
+          STEP("asc_desc", 0, 1, w * (2 * Nl[1] + 3 * Nl[0] + Nl[2] + Nl[3]));
+          fast2_asc_desc<T>(vD[0], uin, fe, pitch, (T *)u_out, rD[0], M[0], s->cfg.order, cA[0], coef, sink(), st,
+                            serp, &rA[1], &rD[1]);
+        } else {
+          STEP("asc_desc", 0, 1, w * (2 * Nl[1] + 3 * Nl[0]));
+          fast2_asc_desc<T>(vD[0], uin, fe, pitch, (T *)u_out, rD[0], M[0], s->cfg.order, cA[0], coef, sink(), st,
+                            serp);
+        }
       } else {
         STEP("asc_fine", 0, 1, w * (Nl[1] + 3 * Nl[0]));
         fast2_asc_fine<T>(vD[0], uin, fe, pitch, (T *)u_out, M[0], s->cfg.order, cA[0], coef, st, bwd);
       }
     };
-    for (int o = 0; o < od; o++) descent(o);
+    for (int o = 0; o < od; o++) {
+      if (o == 0 && skip && xrd_on()) {   // the previous cycle's fused pass ran rest_dad(0)
+        a_done = true;
+        continue;
+      }
+      descent(o);
+    }
     bool tail_done = false;
     if (use_tail) {
       double b = 0;
@@ -280,6 +297,10 @@ struct Impl2 : ImplBase {
       for (int o = oc - 1; o >= od; o--) ascent(o);
     }
     for (int o = od - 1; o >= 0; o--) ascent(o);
+  }
+  void enqueue_pre_descent(void *u, const void *f_eff, cudaStream_t st) override {
+    enqueue_final_norm(u, f_eff, st);
+    if (xrd_on()) fast2_rest_dad<T>(rD[0], rA[1], rD[1], M[1], st, false);
   }
   void enqueue_final_norm(void *u, const void *f_eff, cudaStream_t st) override {
     if (use_fast) {
@@ -307,7 +328,7 @@ struct Impl2 : ImplBase {
       // jac_a(o) and jac_d(o - 1) share one pass for o >= 1
       return 1 + (od - 1) + od + 1 + 2 * od + (use_tail ? 0 : 3 * (oc - od)) - (fuses_cycles() ? 1 : 0) -
              (adfuse && od > ad_min ? od - ad_min : 0) -
-             (dafuse && od - 1 > da_min ? od - 1 - da_min : 0);
+             (dafuse && od - 1 > da_min ? od - 1 - da_min : 0) - (xrd_on() ? 1 : 0);
     }
     int c = 1;                               // desc fine
     for (int o = 0; o + 1 < k; o++) c += (o >= 1) + 1;
@@ -1283,7 +1304,7 @@ int mg_profile(mg_solver *s, void *u_user, const void *f, int ncycles, mg_step_s
     // descent of the first runs unprofiled before the loop
     const bool xf = alt && s->impl->fuses_cycles();
     const int mode = xf ? ImplBase::kSkipDesc | ImplBase::kFuseNext : 0;
-    if (xf) s->impl->enqueue_final_norm(u, fe, s->st);
+    if (xf) s->impl->enqueue_pre_descent(u, fe, s->st);
     void *cur = u;
     for (int c = 0; c < ncycles; c++) {
       void *dst = alt ? (cur == u ? s->d_ualt : u) : u;

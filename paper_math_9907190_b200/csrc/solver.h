@@ -165,6 +165,8 @@ struct ImplBase {
     enqueue_cycle(u_in, u_out, f_eff, st, prof);
   }
   virtual void enqueue_final_norm(void *u, const void *f_eff, cudaStream_t st) = 0;
+  // what a kSkipDesc cycle expects to have run before it (mg_profile's unprofiled descent)
+  virtual void enqueue_pre_descent(void *u, const void *f_eff, cudaStream_t st) { enqueue_final_norm(u, f_eff, st); }
   // Caller-facing helpers.  u, r (residual) and f (f~) are in the caller's layout
   // (mg_solver::pitch); the extra pitch is that of the other operand: f of the
   // residual (the caller's f, or the library's f~ in the work layout), the f~

@@ -75,6 +75,10 @@ CASES = [
     ({"MG_AD_TY": "32", "MG_AD_NT": "256"}, 2, 1025, 4, "float32"),
     ({"MG_AD_TY": "8"}, 2, 513, 2, "float64"),
     ({"MG_AD_NT": "576"}, 2, 513, 2, "float32"),
+    ({"MG_2D_XRD": "1"}, 2, 513, 2, "float64"),
+    ({"MG_2D_XRD": "1"}, 2, 1025, 2, "float32"),
+    ({"MG_2D_XRD": "1"}, 2, 257, 4, "float32"),
+    ({"MG_2D_XRD": "1", "MG_POISON": "1"}, 2, 257, 2, "float64"),
     ({"MG_2D_NODAFUSE": "1"}, 2, 513, 2, "float64"),
     ({"MG_2D_NODAFUSE": "1"}, 2, 257, 4, "float32"),
     ({"MG_DA_MINO": "1"}, 2, 513, 2, "float32"),
