@@ -515,7 +515,7 @@ template <class T>
 cudaError_t fast3_desc_fine(const T *u, const T *f, int64_t pitch, const S3<T> &rr, int M, int order, const Coef<T> &k,
                             const NormSink &ns, cudaStream_t st, const ZRange3 &pz) {
   static const bool gen1 = env_flag("MG_K3_GEN1");   // A/B switch to the first-generation kernel
-  if (order == 2 && !gen1) return fast3p_desc_fine<T>(u, f, pitch, rr, M, k, ns, st, pz);
+  if (!gen1) return fast3p_desc_fine<T>(u, f, pitch, rr, M, order, k, ns, st, pz);
   return order == 2 ? desc3_impl<T, 2>(u, f, pitch, rr, M, k, ns, st, pz)
                     : desc3_impl<T, 4>(u, f, pitch, rr, M, k, ns, st, pz);
 }
@@ -557,7 +557,7 @@ template <class T>
 cudaError_t fast3_asc_fine(const S3<T> &vr, const T *u_old, const T *f, int64_t pitch, T *u_new, int M, int order, T c,
                            const Coef<T> &k, cudaStream_t st, const ZRange3 &pz) {
   static const bool gen1 = env_flag("MG_K3_GEN1");
-  if (order == 2 && !gen1) return fast3p_asc_fine<T>(vr, u_old, f, pitch, u_new, M, c, k, st, pz);
+  if (!gen1) return fast3p_asc_fine<T>(vr, u_old, f, pitch, u_new, M, order, c, k, st, pz);
   return order == 2 ? asc3_impl<T, 2>(vr, u_old, f, pitch, u_new, M, c, k, st, pz)
                     : asc3_impl<T, 4>(vr, u_old, f, pitch, u_new, M, c, k, st, pz);
 }

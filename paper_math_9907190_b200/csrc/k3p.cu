@@ -55,6 +55,62 @@ __device__ __forceinline__ void sel0(T &v, bool keep) {
   v = keep ? v : (T)0;
 }
 
+// Efos4 at the thread's 4 nodes (rows yA, yA+1 x columns xl,
+// xl+1) of plane z from the u boxes of planes z-1 (Uq), z (Up), z+1 (Uc),
+// each offset to (xl, yA); F: f~ at the 4 nodes.  Operand order of res3v
+// (ops3.cuh), so bit-identical to the oracle's res3d_o4.
+template <class T, int UW>
+__device__ __forceinline__ void res19_block(const T *Uq, const T *Up, const T *Uc, const T (&F)[2][2],
+                                            const Coef<T> &k, T (&rn)[2][2]) {
+  T P[4][4], Zp[4][4], Zm[4][4], t;   // [row yA-1 .. yA+2][col xl-1 .. xl+2]
+#pragma unroll
+  for (int r = 0; r < 4; r++) {
+    const T *q = Up + (r - 1) * UW;
+    ld2(q - 2, t, P[r][0]);
+    ld2(q, P[r][1], P[r][2]);
+    ld2(q + 2, P[r][3], t);
+  }
+#pragma unroll
+  for (int r = 0; r < 4; r++) {
+    const T *c = Uc + (r - 1) * UW, *m = Uq + (r - 1) * UW;
+    ld2(c, Zp[r][1], Zp[r][2]);
+    ld2(m, Zm[r][1], Zm[r][2]);
+    if (r == 1 || r == 2) {
+      ld2(c - 2, t, Zp[r][0]);
+      ld2(c + 2, Zp[r][3], t);
+      ld2(m - 2, t, Zm[r][0]);
+      ld2(m + 2, Zm[r][3], t);
+    }
+  }
+#pragma unroll
+  for (int R = 0; R < 2; R++)
+#pragma unroll
+    for (int C = 0; C < 2; C++) {
+      const int a = R + 1, b = C + 1;
+      Nb19<T> q;
+      q.c = P[a][b];
+      q.xp = P[a][b + 1];
+      q.xm = P[a][b - 1];
+      q.yp = P[a + 1][b];
+      q.ym = P[a - 1][b];
+      q.zp = Zp[a][b];
+      q.zm = Zm[a][b];
+      q.xpyp = P[a + 1][b + 1];
+      q.xmyp = P[a + 1][b - 1];
+      q.xmym = P[a - 1][b - 1];
+      q.xpym = P[a - 1][b + 1];
+      q.ypzp = Zp[a + 1][b];
+      q.ypzm = Zm[a + 1][b];
+      q.ymzm = Zm[a - 1][b];
+      q.ymzp = Zp[a - 1][b];
+      q.xpzp = Zp[a][b + 1];
+      q.xmzp = Zp[a][b - 1];
+      q.xmzm = Zm[a][b - 1];
+      q.xpzm = Zm[a][b + 1];
+      rn[R][C] = res3v<T, 4>(q, F[R][C], k);
+    }
+}
+
 // =================================================== finest descent a9 + a10
 // Step j: r(j-1) at the thread's 4 nodes (registers; the green ones also to
 // the ring); then Erred at the red nodes of plane q = j-2.
@@ -62,10 +118,13 @@ __device__ __forceinline__ void sel0(T &v, bool keep) {
 // i.e. PH at z = j-1 and Q = 1-PH at q = j-2; row B the other way round.
 // FINE = false: the same pass one octave down (G(s) -> R(s), s > 1): r is
 // read from the dense level array (the "f" box) instead of computed, no norm.
-template <class T, bool FINE = true, int NW_ = 16, int NSO = 0, bool UNIF = true>
+// ORDER = 4 (FINE only): Efos4 with f~; the u boxes of three planes are read
+// (KEEP = 3 ring slots), everything else is the order-2 pass.
+template <class T, bool FINE = true, int NW_ = 16, int NSO = 0, bool UNIF = true, int ORDER = 2>
 struct OpDesc3P {
   using Gm = Geo<T, NW_>;
-  static constexpr int NW = NW_, NTH = Gm::NTH, MINB = NW <= 8 ? 2 : 1;
+  static_assert(ORDER == 2 || FINE, "order 4 on the finest level only");
+  static constexpr int NW = NW_, NTH = Gm::NTH, MINB = NW <= 8 ? 2 : 1, KEEP = ORDER == 4 ? 3 : 2;
   static constexpr int NS = NSO ? NSO : FINE ? (sizeof(T) == 8 ? 5 : 8) : 8, GPL = Gm::GPL, PRO = FINE ? 2 : 0, EPI = 2;
   static constexpr int U_OFF = 0, F_OFF = FINE ? al128(Gm::U_BYTES) : 0, SLOT = al128(F_OFF + Gm::F_BYTES);
   static constexpr int SMEM = NS * SLOT + 3 * Gm::GPL;
@@ -76,6 +135,7 @@ struct OpDesc3P {
     int M, fz0;
     T invh2;
     NormSink ns;
+    Coef<T> k;   // order 4: c6
   };
   struct State {
     T u[2][2][2];   // [z & 1][row A/B][col 0/1]: own u of the two latest planes
@@ -121,7 +181,19 @@ struct OpDesc3P {
   template <int PH>
   static __device__ __forceinline__ void step(const Params &P, State &S, const Ctx &C, const Item &it, int j,
                                               unsigned char *Lc, unsigned char *Lp, unsigned char *gz,
-                                              unsigned char *gq, unsigned char *) {
+                                              unsigned char *gq, unsigned char *gr) {
+    step_o<PH>(P, S, C, it, j, Lc, Lp, nullptr, gz, gq, gr);
+  }
+  template <int PH>
+  static __device__ __forceinline__ void step(const Params &P, State &S, const Ctx &C, const Item &it, int j,
+                                              unsigned char *Lc, unsigned char *Lp, unsigned char *Lq,
+                                              unsigned char *gz, unsigned char *gq, unsigned char *gr) {
+    step_o<PH>(P, S, C, it, j, Lc, Lp, Lq, gz, gq, gr);
+  }
+  template <int PH>
+  static __device__ __forceinline__ void step_o(const Params &P, State &S, const Ctx &C, const Item &it, int j,
+                                                unsigned char *Lc, unsigned char *Lp, unsigned char *Lq,
+                                                unsigned char *gz, unsigned char *gq, unsigned char *) {
     constexpr int Q = PH ^ 1;   // slot of planes j-1, j-3
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, M = P.M;
     const int uo = (2 * w + 1) * Gm::UW + 2 * lane - 2 + Gm::UXO;   // u box offset of (xl, yA)
@@ -154,12 +226,17 @@ struct OpDesc3P {
       ld2(U + Gm::UW + 2, rB, t);
       ld2(F, fA0, fA1);
       ld2(F + Gm::FW, fB0, fB1);
+      if constexpr (ORDER == 4) {   // Efos4 from the u boxes of planes z-1, z, z+1
+        const T Fv[2][2] = {{fA0, fA1}, {fB0, fB1}};
+        res19_block<T, Gm::UW>((const T *)(Lq + U_OFF) + uo, U, (const T *)(Lc + U_OFF) + uo, Fv, P.k, rn);
+      } else {
       const T h = P.invh2;
       // i+1, i-1, j+1, j-1, k+1, k-1
       rn[0][0] = res7(uc[0][0], uc[0][1], lA, uc[1][0], ymA0, un[0][0], um[0][0], fA0, h);
       rn[0][1] = res7(uc[0][1], rA, uc[0][0], uc[1][1], ymA1, un[0][1], um[0][1], fA1, h);
       rn[1][0] = res7(uc[1][0], uc[1][1], lB, ypB0, uc[0][0], un[1][0], um[1][0], fB0, h);
       rn[1][1] = res7(uc[1][1], rB, uc[1][0], ypB1, uc[0][1], un[1][1], um[1][1], fB1, h);
+      }
       const bool zin = z >= 1 && z <= M - 1;
       if (!(C.m.full && zin)) {
         sel0(rn[0][0], zin && C.m.rA && C.m.c0);
@@ -264,10 +341,11 @@ struct OpDesc3P {
 // column of row A at plane q = j-2 is Q as well.
 // FINE = false: Egprolg/Egprolr one octave down (G(s) from R(s), s > 1): r is
 // read from the dense level array (the "f" box) and v_G(s) is written.
-template <class T, bool FINE = true, int NW_ = 16, int NSO = 0, bool UNIF = true>
+template <class T, bool FINE = true, int NW_ = 16, int NSO = 0, bool UNIF = true, int ORDER = 2>
 struct OpAsc3P {
   using Gm = Geo<T, NW_>;
-  static constexpr int NW = NW_, NTH = Gm::NTH, MINB = NW <= 8 ? 2 : 1;
+  static_assert(ORDER == 2 || FINE, "order 4 on the finest level only");
+  static constexpr int NW = NW_, NTH = Gm::NTH, MINB = NW <= 8 ? 2 : 1, KEEP = ORDER == 4 ? 3 : 2;
   static constexpr int NS = NSO ? NSO : FINE ? (sizeof(T) == 8 ? 4 : 7) : (sizeof(T) == 8 ? 7 : 10), GPL = Gm::GPL,
                        PRO = 2, EPI = 2;
   static constexpr int U_OFF = 0, F_OFF = FINE ? al128(Gm::U_BYTES) : 0, V0_OFF = F_OFF + al128(Gm::F_BYTES),
@@ -279,6 +357,7 @@ struct OpAsc3P {
     Sched sc;
     int M, fz0, hz0;
     T c, invh2;
+    Coef<T> k;   // order 4: c6
   };
   struct State {
     T u[2][2][2];   // [z & 1][row][col] own u
@@ -332,7 +411,19 @@ struct OpAsc3P {
   template <int PH>
   static __device__ __forceinline__ void step(const Params &P, State &S, const Ctx &C, const Item &it, int j,
                                               unsigned char *Lc, unsigned char *Lp, unsigned char *gz,
-                                              unsigned char *gq, unsigned char *) {
+                                              unsigned char *gq, unsigned char *gr) {
+    step_o<PH>(P, S, C, it, j, Lc, Lp, nullptr, gz, gq, gr);
+  }
+  template <int PH>
+  static __device__ __forceinline__ void step(const Params &P, State &S, const Ctx &C, const Item &it, int j,
+                                              unsigned char *Lc, unsigned char *Lp, unsigned char *Lq,
+                                              unsigned char *gz, unsigned char *gq, unsigned char *gr) {
+    step_o<PH>(P, S, C, it, j, Lc, Lp, Lq, gz, gq, gr);
+  }
+  template <int PH>
+  static __device__ __forceinline__ void step_o(const Params &P, State &S, const Ctx &C, const Item &it, int j,
+                                                unsigned char *Lc, unsigned char *Lp, unsigned char *Lq,
+                                                unsigned char *gz, unsigned char *gq, unsigned char *) {
     constexpr int Q = PH ^ 1;
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, M = P.M;
     const int uo = (2 * w + 1) * Gm::UW + 2 * lane - 2 + Gm::UXO;
@@ -371,11 +462,16 @@ struct OpAsc3P {
       ld2(U + Gm::UW + 2, rB, t);
       ld2(F, fA0, fA1);
       ld2(F + Gm::FW, fB0, fB1);
+      if constexpr (ORDER == 4) {
+        const T Fv[2][2] = {{fA0, fA1}, {fB0, fB1}};
+        res19_block<T, Gm::UW>((const T *)(Lq + U_OFF) + uo, U, (const T *)(Lc + U_OFF) + uo, Fv, P.k, rn);
+      } else {
       const T h = P.invh2;
       rn[0][0] = res7(uc[0][0], uc[0][1], lA, uc[1][0], ymA0, un[0][0], um[0][0], fA0, h);
       rn[0][1] = res7(uc[0][1], rA, uc[0][0], uc[1][1], ymA1, un[0][1], um[0][1], fA1, h);
       rn[1][0] = res7(uc[1][0], uc[1][1], lB, ypB0, uc[0][0], un[1][0], um[1][0], fB0, h);
       rn[1][1] = res7(uc[1][1], rB, uc[1][0], ypB1, uc[0][1], un[1][1], um[1][1], fB1, h);
+      }
       }
       // ---- Egprolg at the green nodes (row A col Q, row B col PH) of plane z = j-1
       const int z = j - 1;
@@ -491,10 +587,10 @@ static int k3p_nw() {
   return nw == 8 ? 8 : 16;
 }
 
-template <class T, int NW, int NSO = 0, bool UNIF = true>
+template <class T, int NW, int NSO = 0, bool UNIF = true, int ORDER = 2>
 static cudaError_t desc_fine_nw(const T *u, const T *f, int64_t pitch, const S3<T> &rr, int M, const Coef<T> &k,
                                 const NormSink &ns, cudaStream_t st, const ZRange3 &pz) {
-  using Op = OpDesc3P<T, true, NW, NSO, UNIF>;
+  using Op = OpDesc3P<T, true, NW, NSO, UNIF, ORDER>;
   using Gm = typename Op::Gm;
   typename Op::Params P{};
   const int64_t n = M + 1, plane = pitch * n, nz = pz.fplanes < 0 ? n : pz.fplanes;
@@ -506,22 +602,24 @@ static cudaError_t desc_fine_nw(const T *u, const T *f, int64_t pitch, const S3<
   P.fz0 = pz.fz0;
   P.invh2 = k.invh2;
   P.ns = ns;
+  P.k = k;
   return run_zpipe<Op>(P, M, pz.zlo, pz.zhi < 0 ? M : pz.zhi, st);
 }
 
 template <class T>
-cudaError_t fast3p_desc_fine(const T *u, const T *f, int64_t pitch, const S3<T> &rr, int M, const Coef<T> &k,
-                             const NormSink &ns, cudaStream_t st, const ZRange3 &pz) {
+cudaError_t fast3p_desc_fine(const T *u, const T *f, int64_t pitch, const S3<T> &rr, int M, int order,
+                             const Coef<T> &k, const NormSink &ns, cudaStream_t st, const ZRange3 &pz) {
+  if (order == 4) return desc_fine_nw<T, 8, 0, true, 4>(u, f, pitch, rr, M, k, ns, st, pz);
   static const bool div = env_flag("MG_K3_DIV");   // A/B: round 1's lane-dependent output branch
   if (k3p_nw() == 8 && div) return desc_fine_nw<T, 8, 0, false>(u, f, pitch, rr, M, k, ns, st, pz);
   if (k3p_nw() == 8) return desc_fine_nw<T, 8>(u, f, pitch, rr, M, k, ns, st, pz);
   return desc_fine_nw<T, 16>(u, f, pitch, rr, M, k, ns, st, pz);
 }
 
-template <class T, int NW, int NSO = 0, bool UNIF = true>
+template <class T, int NW, int NSO = 0, bool UNIF = true, int ORDER = 2>
 static cudaError_t asc_fine_nw(const S3<T> &vr, const T *u_old, const T *f, int64_t pitch, T *u_new, int M, T c,
                                const Coef<T> &k, cudaStream_t st, const ZRange3 &pz) {
-  using Op = OpAsc3P<T, true, NW, NSO, UNIF>;
+  using Op = OpAsc3P<T, true, NW, NSO, UNIF, ORDER>;
   using Gm = typename Op::Gm;
   typename Op::Params P{};
   const int64_t n = M + 1, plane = pitch * n, nz = pz.fplanes < 0 ? n : pz.fplanes;
@@ -539,12 +637,14 @@ static cudaError_t asc_fine_nw(const S3<T> &vr, const T *u_old, const T *f, int6
   P.hz0 = pz.hz0;
   P.c = c;
   P.invh2 = k.invh2;
+  P.k = k;
   return run_zpipe<Op>(P, M, pz.zlo, pz.zhi < 0 ? M : pz.zhi, st);
 }
 
 template <class T>
-cudaError_t fast3p_asc_fine(const S3<T> &vr, const T *u_old, const T *f, int64_t pitch, T *u_new, int M, T c,
-                            const Coef<T> &k, cudaStream_t st, const ZRange3 &pz) {
+cudaError_t fast3p_asc_fine(const S3<T> &vr, const T *u_old, const T *f, int64_t pitch, T *u_new, int M, int order,
+                            T c, const Coef<T> &k, cudaStream_t st, const ZRange3 &pz) {
+  if (order == 4) return asc_fine_nw<T, 8, 0, true, 4>(vr, u_old, f, pitch, u_new, M, c, k, st, pz);
   static const bool div = env_flag("MG_K3_DIV");
   if (k3p_nw() == 8 && div) return asc_fine_nw<T, 8, 0, false>(vr, u_old, f, pitch, u_new, M, c, k, st, pz);
   if (k3p_nw() == 8) return asc_fine_nw<T, 8>(vr, u_old, f, pitch, u_new, M, c, k, st, pz);
@@ -601,13 +701,13 @@ template cudaError_t fast3p_jac_g<double>(const S3<double> &, const D3<double> &
                                           cudaStream_t);
 template cudaError_t fast3p_jac_g<float>(const S3<float> &, const D3<float> &, const D3<float> &, int, float,
                                          cudaStream_t);
-template cudaError_t fast3p_desc_fine<double>(const double *, const double *, int64_t, const S3<double> &, int,
+template cudaError_t fast3p_desc_fine<double>(const double *, const double *, int64_t, const S3<double> &, int, int,
                                               const Coef<double> &, const NormSink &, cudaStream_t, const ZRange3 &);
-template cudaError_t fast3p_desc_fine<float>(const float *, const float *, int64_t, const S3<float> &, int,
+template cudaError_t fast3p_desc_fine<float>(const float *, const float *, int64_t, const S3<float> &, int, int,
                                              const Coef<float> &, const NormSink &, cudaStream_t, const ZRange3 &);
 template cudaError_t fast3p_asc_fine<double>(const S3<double> &, const double *, const double *, int64_t, double *, int,
-                                             double, const Coef<double> &, cudaStream_t, const ZRange3 &);
+                                             int, double, const Coef<double> &, cudaStream_t, const ZRange3 &);
 template cudaError_t fast3p_asc_fine<float>(const S3<float> &, const float *, const float *, int64_t, float *, int,
-                                            float, const Coef<float> &, cudaStream_t, const ZRange3 &);
+                                            int, float, const Coef<float> &, cudaStream_t, const ZRange3 &);
 
 }  // namespace mg

@@ -190,14 +190,15 @@ template <class T>
 cudaError_t fast3_asc_fine(const S3<T> &vr, const T *u_old, const T *f, int64_t pitch, T *u_new, int M, int order, T c,
                            const Coef<T> &k, cudaStream_t st, const ZRange3 &pz = ZRange3());
 
-// Second-generation register-streaming plane pipelines (k3p.cu), order 2 only;
-// fast3_desc_fine / fast3_asc_fine dispatch to them for order 2.
+// Second-generation register-streaming plane pipelines (k3p.cu), orders 2 and
+// 4 (Efos4 reads the u boxes of three planes); fast3_desc_fine /
+// fast3_asc_fine dispatch to them unless MG_K3_GEN1=1.
 template <class T>
-cudaError_t fast3p_desc_fine(const T *u, const T *f, int64_t pitch, const S3<T> &rr, int M, const Coef<T> &k,
-                             const NormSink &ns, cudaStream_t st, const ZRange3 &pz);
+cudaError_t fast3p_desc_fine(const T *u, const T *f, int64_t pitch, const S3<T> &rr, int M, int order,
+                             const Coef<T> &k, const NormSink &ns, cudaStream_t st, const ZRange3 &pz);
 template <class T>
-cudaError_t fast3p_asc_fine(const S3<T> &vr, const T *u_old, const T *f, int64_t pitch, T *u_new, int M, T c,
-                            const Coef<T> &k, cudaStream_t st, const ZRange3 &pz);
+cudaError_t fast3p_asc_fine(const S3<T> &vr, const T *u_old, const T *f, int64_t pitch, T *u_new, int M, int order,
+                            T c, const Coef<T> &k, cudaStream_t st, const ZRange3 &pz);
 
 // The same pipelines one octave down (s > 1, single GPU): G(s) -> R(s)
 // (Erred from the dense r_G(s)) and G(s) from R(s) (Egprolg + Egprolr, both

@@ -48,6 +48,17 @@ struct OpNT<Op, std::void_t<decltype(Op::NTH), decltype(Op::MINB)>> {
   static constexpr int nt = Op::NTH, minb = Op::MINB;
 };
 
+// Ring slots an Op reads at step j: 2 (L_j, L_{j-1}: the default) or 3 (also
+// L_{j-2}, passed as Lq; Op::KEEP = 3) -- the loads in flight are NS - KEEP.
+template <class Op, class = void>
+struct OpKeep {
+  static constexpr int v = 2;
+};
+template <class Op>
+struct OpKeep<Op, std::void_t<decltype(Op::KEEP)>> {
+  static constexpr int v = Op::KEEP;
+};
+
 template <class T>
 struct V2t;
 template <>
@@ -131,14 +142,15 @@ using namespace zp;
 // Op: NS (slots), SLOT (bytes), SMEM, GPL (bytes of one ring plane), PRO /
 // EPI (steps before zs / after ze-1), Params (with .sc), issue(P, it, j,
 // slot, bar), State, Ctx, begin(P, Ctx&, it), step<PH>(P, State&, Ctx&, it,
-// j, Lc, Lp, gz, gq, gr): item steps run j = zs-PRO .. ze-1+EPI.  PH = j & 1: every parity the step needs (tile origins
+// j, Lc, Lp, [Lq,] gz, gq, gr): item steps run j = zs-PRO .. ze-1+EPI.  PH = j & 1: every parity the step needs (tile origins
 // y0 and x0 are even) is a compile-time function of PH, and the register
 // state is double-buffered by PH, so no selects or register moves remain.
 // A 3-plane ring after the slots is addressed by gz (plane j-1), gq (plane
 // j-2) and gr (plane j-3).
 template <class Op>
 __global__ void __launch_bounds__(OpNT<Op>::nt, OpNT<Op>::minb) zpipe(const __grid_constant__ typename Op::Params P) {
-  constexpr int NS = Op::NS, D = NS - 2;
+  constexpr int KEEP = OpKeep<Op>::v, NS = Op::NS, D = NS - KEEP;
+  static_assert(D >= 1, "at least one load in flight");
   extern __shared__ __align__(128) unsigned char smem[];
   __shared__ __align__(8) uint64_t bar[NS];
   const int G = gridDim.x, b = blockIdx.x;
@@ -183,7 +195,7 @@ __global__ void __launch_bounds__(OpNT<Op>::nt, OpNT<Op>::minb) zpipe(const __gr
 
   typename Op::State S;
   Op::init(S);
-  int cs = 0, cprev = NS - 1;
+  int cs = 0, cprev = NS - 1, cpp = NS - 2;
   uint32_t phase = 0;
   for (int k = 0; k < nit; k++) {
     const Item it = P.sc.get(k, b, G);
@@ -199,9 +211,14 @@ __global__ void __launch_bounds__(OpNT<Op>::nt, OpNT<Op>::minb) zpipe(const __gr
       if (threadIdx.x == 0) produce();
       mbar_wait(&bar[cs], phase);
       const int gr = (gz == 2 * Op::GPL) ? 0 : gz + Op::GPL;   // plane j-3
-      Op::template step<PH>(P, S, C, it, j, smem + cs * Op::SLOT, smem + cprev * Op::SLOT, gring + gz, gring + gq,
-                            gring + gr);
+      if constexpr (KEEP >= 3)
+        Op::template step<PH>(P, S, C, it, j, smem + cs * Op::SLOT, smem + cprev * Op::SLOT, smem + cpp * Op::SLOT,
+                              gring + gz, gring + gq, gring + gr);
+      else
+        Op::template step<PH>(P, S, C, it, j, smem + cs * Op::SLOT, smem + cprev * Op::SLOT, gring + gz, gring + gq,
+                              gring + gr);
       __syncthreads();
+      cpp = cprev;
       cprev = cs;
       if (++cs == NS) {
         cs = 0;

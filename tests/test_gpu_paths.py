@@ -54,6 +54,10 @@ CASES = [
     ({"MG_TAIL_M3": "0"}, 3, 129, 2, "float64"),
     ({"MG_TAIL_M3": "128"}, 3, 129, 2, "float64"),
     ({"MG_K3_GEN1": "1"}, 3, 65, 2, "float64"),
+    ({"MG_K3_GEN1": "1"}, 3, 65, 4, "float64"),
+    ({"MG_K3_GEN1": "1"}, 3, 129, 4, "float32"),
+    ({}, 3, 129, 4, "float64"),
+    ({}, 3, 129, 4, "float32"),
     ({"MG_FORCE_REF": "1"}, 3, 33, 2, "float64"),
     ({"MG_COARSE_GLOBAL": "1", "MG_TAIL_M3": "0"}, 3, 65, 2, "float64"),
     ({"MG_TAIL_M2": "128"}, 2, 513, 2, "float64"),
