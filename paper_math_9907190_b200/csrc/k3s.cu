@@ -23,10 +23,23 @@ namespace hs {
 
 // sublattice slots of S3: (x&1) | (y&1)<<1 | (z&1)<<2
 constexpr int C = 0, FX = 6, FY = 5, FZ = 3, B = 7;
-using T = double;
+using T = double;                                      // the fused passes below are fp64 only
 constexpr int RW = 32, RH = 16;                        // one value per thread
 constexpr int RBOX = RW * RH * 8;                      // 4096 B
 constexpr int BOX34 = al128(34 * 17 * 8), BOX36 = al128(36 * 17 * 8);
+
+// TMA x alignment for element type E: box origins must be 16-byte aligned.
+// Every origin these passes use is even, i.e. 0 or 2 mod A; an origin X is
+// loaded from bx(X) and read back at offset X - bx(X) (<= XP), so a box that
+// must hold w columns from X is W(w) wide.  fp64: A = 2, XP = 0 (nothing
+// changes); fp32: A = 4, XP = 2.
+template <class E>
+struct XA {
+  static constexpr int A = 16 / (int)sizeof(E), XP = A - 2;
+  static constexpr int W(int w) { return (w + XP + A - 1) / A * A; }
+  static __device__ __forceinline__ int bx(int x) { return x & ~(A - 1); }
+  static __device__ __forceinline__ int ox(int x) { return XP ? (x & (A - 1)) : 0; }
+};
 
 struct Sub {
   T *p;
@@ -53,15 +66,20 @@ using namespace hs;
 // b in [b0, b0+15) (w >= 1); the ring a0-1 / b0-1 is colour 1 only.
 // L_j = {C_M(j), B_M(j), r_Fx/Fy/Fz(j-1), r_C(j-2)}.  Step j: faces of plane
 // j-1 (Erprolr), corners of plane j-2 (Erprolm).
-template <int NW_ = 16>
+// E = double or float (E = float: boxes from 16-byte aligned origins, XA).
+template <class E, int NW_ = 16>
 struct OpJacR3T {
+  using T = E;
+  using X = XA<E>;
   // NW warps: thread rows b0-1+w cover NW rows, NW-1 of them output rows
   static constexpr int NW = NW_, NTH = 32 * NW, MINB = NW <= 8 ? 2 : 1;
-  static constexpr int RB = RW * NW * 8, BX = al128(34 * (NW + 1) * 8);
+  static constexpr int BW = X::W(34), RWB = X::W(RW);   // C / B box and r box row strides (elements)
+  static constexpr int RBE = RWB * NW, RB = RBE * (int)sizeof(T), BX = al128(BW * (NW + 1) * (int)sizeof(T));
+  static constexpr int RG = RW * NW;                   // one face array of a ring plane (elements)
   static constexpr int NS = 6, PRO = 2, EPI = 2;
   static constexpr int OC = 0, OB = BX, OR = 2 * BX;   // C box, B box, 4 r boxes (Fx, Fy, Fz, C)
   static constexpr int SLOT = OR + 4 * RB;
-  static constexpr int GPL = 3 * RB;                   // face ring plane: Fx | Fy | Fz
+  static constexpr int GPL = 3 * RG * (int)sizeof(T);  // face ring plane: Fx | Fy | Fz
   static constexpr int SMEM = NS * SLOT + 3 * GPL;
   struct Params {
     CUtensorMap tc, tb, tr[4];   // C_M, B_M; r_R Fx, Fy, Fz, C
@@ -76,6 +94,7 @@ struct OpJacR3T {
   };
   struct Ctx {
     bool a0k, a1k, b0k, b1k, core;   // a in [0,H-2] / [1,H-2], b likewise, core column
+    int ox;                          // box column offset of the item (X)
     int64_t o0;                      // (a, b) in a plane of the sublattice arrays
   };
   static __device__ void prefetch(const Params &P) {
@@ -93,16 +112,18 @@ struct OpJacR3T {
     C.b0k = m.z0(b);
     C.b1k = m.z1(b);
     C.core = l >= 2 && w >= 1;
+    C.ox = X::ox(it.x0 - 2);
     C.o0 = (int64_t)b * P.v.pitch + a;
   }
   static __device__ void issue(const Params &P, const Item &it, int j, unsigned char *slot, uint64_t *bar) {
     const bool wf = j >= it.zs, wc = j >= it.zs + 2;
-    mbar_expect_tx(bar, 2 * 34 * (NW + 1) * 8 + (wf ? 3 * RB : 0) + (wc ? RB : 0));
-    tma_load_3d(slot + OC, &P.tc, it.x0 - 2, it.y0 - 1, j, bar);
-    tma_load_3d(slot + OB, &P.tb, it.x0 - 4, it.y0 - 2, j, bar);
+    const int x2 = X::bx(it.x0 - 2);
+    mbar_expect_tx(bar, 2 * BW * (NW + 1) * (int)sizeof(T) + (wf ? 3 * RB : 0) + (wc ? RB : 0));
+    tma_load_3d(slot + OC, &P.tc, x2, it.y0 - 1, j, bar);
+    tma_load_3d(slot + OB, &P.tb, X::bx(it.x0 - 4), it.y0 - 2, j, bar);
     if (wf)
-      for (int i = 0; i < 3; i++) tma_load_3d(slot + OR + i * RB, &P.tr[i], it.x0 - 2, it.y0 - 1, j - 1, bar);
-    if (wc) tma_load_3d(slot + OR + 3 * RB, &P.tr[3], it.x0 - 2, it.y0 - 1, j - 2, bar);
+      for (int i = 0; i < 3; i++) tma_load_3d(slot + OR + i * RB, &P.tr[i], x2, it.y0 - 1, j - 1, bar);
+    if (wc) tma_load_3d(slot + OR + 3 * RB, &P.tr[3], x2, it.y0 - 1, j - 2, bar);
   }
   template <int PH>
   static __device__ __forceinline__ void step(const Params &P, State &S, const Ctx &Cx, const Item &it, int j,
@@ -110,14 +131,15 @@ struct OpJacR3T {
                                               unsigned char *gq, unsigned char *gr) {
     constexpr int Q = PH ^ 1;
     const int l = threadIdx.x & 31, w = threadIdx.x >> 5;
-    const int a = it.x0 - 2 + l, b = it.y0 - 1 + w;
-    const int oc = w * 34 + l, ob = (w + 1) * 34 + l + 2, orr = w * RW + l;
+    // C and r boxes start at bx(x0 - 2) (offset ox), the B box at bx(x0 - 4) (offset XP - ox)
+    const int oc = w * BW + l + Cx.ox, ob = (w + 1) * BW + l + 2 + X::XP - Cx.ox, orb = w * RWB + l + Cx.ox,
+              orr = w * RW + l;
     const HM m{P.H};
     const T bj = ((const T *)(Lc + OB))[ob];   // own B_M(j)
     if (j >= it.zs) {
       const int c = j - 1;
       const T *Cc = (const T *)(Lp + OC) + oc, *Cn = (const T *)(Lc + OC) + oc, *Bc = (const T *)(Lp + OB) + ob;
-      const T *R = (const T *)(Lc + OR) + orr;
+      const T *R = (const T *)(Lc + OR) + orb;
       const T bc = S.bo[Q], bm = S.bo[PH];   // B(a,b,c), B(a,b,c-1)
       const bool cz0 = m.z0(c), cz1 = m.z1(c);
       T fx, fy, fz;
@@ -126,16 +148,16 @@ struct OpJacR3T {
         nrm = nrm + Bc[-1];
         T t = -(P.c1 * R[0]);
         t = t + (T)2 * nrm;
-        t = t + Cn[34];
-        t = t + Cc[34];
+        t = t + Cn[BW];
+        t = t + Cc[BW];
         t = t + Cc[0];
         t = t + Cn[0];
         fx = (Cx.a1k && Cx.b0k && cz0) ? t * (T)0.125 : (T)0;
       }
       {   // Fy (2a+1, 2b, 2c+1): normal y; in-plane (+1,0,+1),(-1,0,+1),(-1,0,-1),(+1,0,-1)
         T nrm = bc;
-        nrm = nrm + Bc[-34];
-        T t = -(P.c1 * R[RB / 8]);
+        nrm = nrm + Bc[-BW];
+        T t = -(P.c1 * R[RBE]);
         t = t + (T)2 * nrm;
         t = t + Cn[1];
         t = t + Cn[0];
@@ -146,19 +168,19 @@ struct OpJacR3T {
       {   // Fz (2a+1, 2b+1, 2c): normal z; in-plane (+1,+1,0),(+1,-1,0),(-1,-1,0),(-1,+1,0)
         T nrm = bc;
         nrm = nrm + bm;
-        T t = -(P.c1 * R[2 * RB / 8]);
+        T t = -(P.c1 * R[2 * RBE]);
         t = t + (T)2 * nrm;
-        t = t + Cc[35];
+        t = t + Cc[BW + 1];
         t = t + Cc[1];
         t = t + Cc[0];
-        t = t + Cc[34];
+        t = t + Cc[BW];
         fz = (Cx.a0k && Cx.b0k && cz1) ? t * (T)0.125 : (T)0;
       }
       {
         T *g = (T *)gz + orr;
         g[0] = fx;
-        g[RB / 8] = fy;
-        g[2 * RB / 8] = fz;
+        g[RG] = fy;
+        g[2 * RG] = fz;
       }
       if (Cx.core && c >= it.zs && c < it.ze) {
         const int64_t o = (int64_t)c * P.v.plane + Cx.o0;
@@ -169,9 +191,9 @@ struct OpJacR3T {
       // ---- corners of plane q = j-2 from the faces of planes q (own: slot PH, ring gq) and q-1 (slot Q, gr)
       const int q = j - 2;
       if (q >= it.zs && Cx.core && Cx.a1k && Cx.b1k && m.z1(q)) {
-        const T *Gx = (const T *)gq + orr, *Gy = Gx + RB / 8, *Gz = Gx + 2 * RB / 8;
-        const T *Hx = (const T *)gr + orr, *Hy = Hx + RB / 8;
-        T t = -(P.c2 * R[3 * RB / 8]);
+        const T *Gx = (const T *)gq + orr, *Gy = Gx + RG, *Gz = Gx + 2 * RG;
+        const T *Hx = (const T *)gr + orr, *Hy = Hx + RG;
+        T t = -(P.c2 * R[3 * RBE]);
         t = t + S.fz[PH];      // (+1,+1, 0)
         t = t + Gz[-RW];       // (+1,-1, 0)
         t = t + Gz[-RW - 1];   // (-1,-1, 0)
@@ -194,7 +216,6 @@ struct OpJacR3T {
   }
   static __device__ void finish(const Params &, State &) {}
 };
-using OpJacR3 = OpJacR3T<16>;
 
 // Two half-index rows per thread for the single-colour-ring passes below:
 // warp w owns rows b = b0 + 2w (+ ring offset) and the next one.
@@ -207,15 +228,18 @@ constexpr int BOX34x33 = al128(34 * 33 * 8), BOX36x33 = al128(36 * 33 * 8);
 // L_j = {v_G(2s)(j), r_B(j-1), r_C(j-2)}.  Step j: centres of plane j-1
 // (Emprolm), corners of plane j-2 from the new centres
 // (Emprolb).
-template <int NW_ = 16>
+template <class E, int NW_ = 16>
 struct OpJacM3T {
+  using T = E;
+  using X = XA<E>;
   // NW warps: thread rows b0-1+2w+R cover 2NW rows, 2NW-1 of them output rows
   static constexpr int NW = NW_, NTH = 32 * NW, MINB = NW <= 8 ? 2 : 1;
-  static constexpr int GROWS = 2 * NW + 1, RB2 = RW * 2 * NW * 8;
+  static constexpr int BW = X::W(34), RWB = X::W(RW);   // v_G box and r box row strides (elements)
+  static constexpr int GROWS = 2 * NW + 1, RBE2 = RWB * 2 * NW, RB2 = RBE2 * (int)sizeof(T);
   static constexpr int NS = 5, PRO = 1, EPI = 2;
-  static constexpr int OG = 0, OR = al128(34 * GROWS * 8);   // v_G box, r boxes (B, C)
+  static constexpr int OG = 0, OR = al128(BW * GROWS * (int)sizeof(T));   // v_G box, r boxes (B, C)
   static constexpr int SLOT = OR + 2 * RB2;
-  static constexpr int GPL = RB2;               // centre ring plane
+  static constexpr int GPL = RW * 2 * NW * (int)sizeof(T);   // centre ring plane
   static constexpr int SMEM = NS * SLOT + 3 * GPL;
   struct Params {
     CUtensorMap tg, tr[2];   // v_G(2s); r_M B, C
@@ -229,6 +253,7 @@ struct OpJacM3T {
   };
   struct Ctx {
     bool b0k[2], b1k[2], core[2];   // per row: (a, b) in [0,H-2]^2 / [1,H-2]^2, core node
+    int ox;                         // box column offset of the item (X)
     T *pb[2], *pc[2];               // per row: v_M B / C at (a, b) of plane 0 (+ c * plane per step)
   };
   static __device__ void prefetch(const Params &P) {
@@ -241,6 +266,7 @@ struct OpJacM3T {
     const int l = threadIdx.x & 31, w = threadIdx.x >> 5;
     const int a = it.x0 - 2 + l;
     const HM m{P.H};
+    C.ox = X::ox(it.x0 - 2);
 #pragma unroll
     for (int R = 0; R < 2; R++) {
       const int b = it.y0 - 1 + 2 * w + R;
@@ -254,10 +280,11 @@ struct OpJacM3T {
   }
   static __device__ void issue(const Params &P, const Item &it, int j, unsigned char *slot, uint64_t *bar) {
     const bool wf = j >= it.zs, wc = j >= it.zs + 2;
-    mbar_expect_tx(bar, 34 * GROWS * 8 + (wf ? RB2 : 0) + (wc ? RB2 : 0));
-    tma_load_3d(slot + OG, &P.tg, it.x0 - 2, it.y0 - 1, j, bar);
-    if (wf) tma_load_3d(slot + OR, &P.tr[0], it.x0 - 2, it.y0 - 1, j - 1, bar);
-    if (wc) tma_load_3d(slot + OR + RB2, &P.tr[1], it.x0 - 2, it.y0 - 1, j - 2, bar);
+    const int x2 = X::bx(it.x0 - 2);
+    mbar_expect_tx(bar, BW * GROWS * (int)sizeof(T) + (wf ? RB2 : 0) + (wc ? RB2 : 0));
+    tma_load_3d(slot + OG, &P.tg, x2, it.y0 - 1, j, bar);
+    if (wf) tma_load_3d(slot + OR, &P.tr[0], x2, it.y0 - 1, j - 1, bar);
+    if (wc) tma_load_3d(slot + OR + RB2, &P.tr[1], x2, it.y0 - 1, j - 2, bar);
   }
   template <int PH>
   static __device__ __forceinline__ void step(const Params &P, State &S, const Ctx &Cx, const Item &it, int j,
@@ -266,32 +293,31 @@ struct OpJacM3T {
     constexpr int Q = PH ^ 1;
     if (j < it.zs) return;
     const int l = threadIdx.x & 31, w = threadIdx.x >> 5;
-    const int a = it.x0 - 2 + l;
     const HM m{P.H};
     const int c = j - 1, q = j - 2;
     const bool czin = m.z0(c), cout = c >= it.zs && c < it.ze, qok = q >= it.zs && m.z1(q);
     T bn[2];
 #pragma unroll
     for (int R = 0; R < 2; R++) {
-      const int og = (2 * w + R) * 34 + l, orr = (2 * w + R) * RW + l;
+      const int og = (2 * w + R) * BW + l + Cx.ox, orb = (2 * w + R) * RWB + l + Cx.ox, orr = (2 * w + R) * RW + l;
       const T *Gc = (const T *)(Lp + OG) + og, *Gn = (const T *)(Lc + OG) + og;   // v_G planes c, c+1
-      const T *Rb = (const T *)(Lc + OR) + orr;
+      const T *Rb = (const T *)(Lc + OR) + orb;
       T t = -(P.cc * Rb[0]);
-      t = t + Gn[35];   // (+,+,+)
-      t = t + Gc[35];   // (+,+,-)
-      t = t + Gn[1];    // (+,-,+)
-      t = t + Gc[1];    // (+,-,-)
-      t = t + Gn[34];   // (-,+,+)
-      t = t + Gc[34];   // (-,+,-)
-      t = t + Gn[0];    // (-,-,+)
-      t = t + Gc[0];    // (-,-,-)
+      t = t + Gn[BW + 1];   // (+,+,+)
+      t = t + Gc[BW + 1];   // (+,+,-)
+      t = t + Gn[1];        // (+,-,+)
+      t = t + Gc[1];        // (+,-,-)
+      t = t + Gn[BW];       // (-,+,+)
+      t = t + Gc[BW];       // (-,+,-)
+      t = t + Gn[0];        // (-,-,+)
+      t = t + Gc[0];        // (-,-,-)
       const bool ok = Cx.b0k[R] && czin;
       bn[R] = ok ? t * (T)0.125 : (T)0;
       ((T *)gz)[orr] = bn[R];
       if (ok && Cx.core[R] && cout) __stcs(Cx.pb[R] + (int64_t)c * P.v.plane, bn[R]);
       if (qok && Cx.core[R] && Cx.b1k[R]) {
         const T *G0 = (const T *)gq + orr, *G1 = (const T *)gr + orr;   // centres of planes q, q-1
-        T u = -(P.cc * Rb[RB2 / 8]);
+        T u = -(P.cc * Rb[RBE2]);
         u = u + S.bo[PH][R];     // (a, b, c)
         u = u + S.bo[Q][R];      // (a, b, c-1)
         u = u + G0[-RW];         // (a, b-1, c)
@@ -308,16 +334,22 @@ struct OpJacM3T {
   }
   static __device__ void finish(const Params &, State &) {}
 };
-using OpJacM3 = OpJacM3T<16>;
 
 // ===================================================== R(s) -> M(s): a11
 // Thread columns (a0+l, b0+2w+R), tiles 32 x 32, no ring.
 // L_j = {Fx(j), Fy(j), Fz(j+1), C_R(j)}; step j: corners (Ermagc)
-// and centres (Ermagm) of plane j.
+// and centres (Ermagm) of plane j.  a0 is a multiple of 32, so
+// the halo boxes (origin a0-2) sit at offset XP after their aligned origin.
+template <class E>
 struct OpRestRM3 {
+  using T = E;
+  using X = XA<E>;
   static constexpr int NS = 4, PRO = 1, EPI = 0;   // 2 planes ahead: measured 0.133 vs 0.143 ms (4 ahead)
-  static constexpr int OX = 0, OY = BOX36x33, OZ = BOX36x33 + BOX34x33, OCR = BOX36x33 + 2 * BOX34x33;
-  static constexpr int SLOT = OCR + RBOX2;
+  static constexpr int WX = X::W(36), WY = X::W(34);   // Fx box, Fy / Fz box row strides (elements)
+  static constexpr int BXB = al128(WX * 33 * (int)sizeof(T)), BYB = al128(WY * 33 * (int)sizeof(T));
+  static constexpr int RBB = RW * RH2 * (int)sizeof(T);
+  static constexpr int OX = 0, OY = BXB, OZ = BXB + BYB, OCR = BXB + 2 * BYB;
+  static constexpr int SLOT = OCR + RBB;
   static constexpr int GPL = 0;
   static constexpr int SMEM = NS * SLOT + 128;
   struct Params {
@@ -348,10 +380,11 @@ struct OpRestRM3 {
   }
   static __device__ void issue(const Params &P, const Item &it, int j, unsigned char *slot, uint64_t *bar) {
     const bool wc = j >= it.zs;
-    mbar_expect_tx(bar, 36 * 33 * 8 + 2 * 34 * 33 * 8 + (wc ? RBOX2 : 0));
-    tma_load_3d(slot + OX, &P.tx, it.x0 - 2, it.y0 - 1, j, bar);
-    tma_load_3d(slot + OY, &P.ty, it.x0 - 2, it.y0, j, bar);
-    tma_load_3d(slot + OZ, &P.tz, it.x0 - 2, it.y0 - 1, j + 1, bar);
+    const int x2 = it.x0 - 2 - X::XP;
+    mbar_expect_tx(bar, (WX + 2 * WY) * 33 * (int)sizeof(T) + (wc ? RBB : 0));
+    tma_load_3d(slot + OX, &P.tx, x2, it.y0 - 1, j, bar);
+    tma_load_3d(slot + OY, &P.ty, x2, it.y0, j, bar);
+    tma_load_3d(slot + OZ, &P.tz, x2, it.y0 - 1, j + 1, bar);
     if (wc) tma_load_3d(slot + OCR, &P.tc, it.x0, it.y0, j, bar);
   }
   template <int PH>
@@ -366,32 +399,32 @@ struct OpRestRM3 {
 #pragma unroll
     for (int R = 0; R < 2; R++) {
       const int b = it.y0 + 2 * w + R, rr = 2 * w + R;
-      const int ox = (rr + 1) * 36 + l + 2, oy = rr * 34 + l + 2, oz = (rr + 1) * 34 + l + 2;
+      const int ox = (rr + 1) * WX + l + 2 + X::XP, oy = rr * WY + l + 2 + X::XP, oz = (rr + 1) * WY + l + 2 + X::XP;
       const T *Xc = (const T *)(Lc + OX) + ox, *Xp = (const T *)(Lp + OX) + ox;   // Fx planes c, c-1
       const T *Yc = (const T *)(Lc + OY) + oy, *Yp = (const T *)(Lp + OY) + oy;   // Fy planes c, c-1
       const T *Zn = (const T *)(Lc + OZ) + oz, *Zc = (const T *)(Lp + OZ) + oz;   // Fz planes c+1, c
       const int64_t o = (int64_t)c * P.out.plane + (int64_t)b * P.out.pitch + a;
       if (Cx.k1[R] && c1) {
         T t = (T)12 * ((const T *)(Lc + OCR))[rr * RW + l];
-        t = t + Zc[0];         // (+1,+1, 0)
-        t = t + Zc[-34];       // (+1,-1, 0)
-        t = t + Zc[-35];       // (-1,-1, 0)
-        t = t + Zc[-1];        // (-1,+1, 0)
-        t = t + Yc[0];         // (+1, 0,+1)
-        t = t + Yp[0];         // (+1, 0,-1)
-        t = t + Yp[-1];        // (-1, 0,-1)
-        t = t + Yc[-1];        // (-1, 0,+1)
-        t = t + Xc[0];         // ( 0,+1,+1)
-        t = t + Xp[0];         // ( 0,+1,-1)
-        t = t + Xp[-36];       // ( 0,-1,-1)
-        t = t + Xc[-36];       // ( 0,-1,+1)
+        t = t + Zc[0];          // (+1,+1, 0)
+        t = t + Zc[-WY];        // (+1,-1, 0)
+        t = t + Zc[-WY - 1];    // (-1,-1, 0)
+        t = t + Zc[-1];         // (-1,+1, 0)
+        t = t + Yc[0];          // (+1, 0,+1)
+        t = t + Yp[0];          // (+1, 0,-1)
+        t = t + Yp[-1];         // (-1, 0,-1)
+        t = t + Yc[-1];         // (-1, 0,+1)
+        t = t + Xc[0];          // ( 0,+1,+1)
+        t = t + Xp[0];          // ( 0,+1,-1)
+        t = t + Xp[-WX];        // ( 0,-1,-1)
+        t = t + Xc[-WX];        // ( 0,-1,+1)
         __stcs(P.out.s[C] + o, t * (T)(1.0 / 24.0));
       }
       if (Cx.k0[R] && c0) {
         // centre (2a+1, 2b+1, 2c+1): i+1, i-1, j+1, j-1, k+1, k-1
         T t = Xc[1];
         t = t + Xc[0];
-        t = t + Yc[34];
+        t = t + Yc[WY];
         t = t + Yc[0];
         t = t + Zn[0];
         t = t + Zc[0];
@@ -405,10 +438,15 @@ struct OpRestRM3 {
 // ===================================================== M(s) -> G(2s): a12
 // Erblu.  Tiles 32 x 32, two rows per thread.
 // L_j = {C_M(j), B_M(j)}; step j: plane j.
+template <class E>
 struct OpRestMG3 {
+  using T = E;
+  using X = XA<E>;
   static constexpr int NS = 6, PRO = 1, EPI = 0;   // 4 planes ahead: measured 0.0737 vs 0.0761 ms (10 ahead)
-  static constexpr int OB = 0, OCM = BOX34x33;
-  static constexpr int SLOT = OCM + RBOX2;
+  static constexpr int WB = X::W(34);              // B box row stride (elements)
+  static constexpr int RBB = RW * RH2 * (int)sizeof(T);
+  static constexpr int OB = 0, OCM = al128(WB * 33 * (int)sizeof(T));
+  static constexpr int SLOT = OCM + RBB;
   static constexpr int GPL = 0;
   static constexpr int SMEM = NS * SLOT + 128;
   struct Params {
@@ -434,8 +472,8 @@ struct OpRestMG3 {
   }
   static __device__ void issue(const Params &P, const Item &it, int j, unsigned char *slot, uint64_t *bar) {
     const bool wc = j >= it.zs;
-    mbar_expect_tx(bar, 34 * 33 * 8 + (wc ? RBOX2 : 0));
-    tma_load_3d(slot + OB, &P.tb, it.x0 - 2, it.y0 - 1, j, bar);
+    mbar_expect_tx(bar, WB * 33 * (int)sizeof(T) + (wc ? RBB : 0));
+    tma_load_3d(slot + OB, &P.tb, it.x0 - 2 - X::XP, it.y0 - 1, j, bar);
     if (wc) tma_load_3d(slot + OCM, &P.tc, it.x0, it.y0, j, bar);
   }
   template <int PH>
@@ -451,17 +489,17 @@ struct OpRestMG3 {
     for (int R = 0; R < 2; R++) {
       if (!Cx.k1[R]) continue;
       const int b = it.y0 + 2 * w + R, rr = 2 * w + R;
-      const int ob = (rr + 1) * 34 + l + 2;
+      const int ob = (rr + 1) * WB + l + 2 + X::XP;
       const T *Bc = (const T *)(Lc + OB) + ob, *Bp = (const T *)(Lp + OB) + ob;   // B planes c, c-1
       T t = (T)8 * ((const T *)(Lc + OCM))[rr * RW + l];
-      t = t + Bc[0];         // (+,+,+)
-      t = t + Bp[0];         // (+,+,-)
-      t = t + Bc[-34];       // (+,-,+)
-      t = t + Bp[-34];       // (+,-,-)
-      t = t + Bc[-1];        // (-,+,+)
-      t = t + Bp[-1];        // (-,+,-)
-      t = t + Bc[-35];       // (-,-,+)
-      t = t + Bp[-35];       // (-,-,-)
+      t = t + Bc[0];          // (+,+,+)
+      t = t + Bp[0];          // (+,+,-)
+      t = t + Bc[-WB];        // (+,-,+)
+      t = t + Bp[-WB];        // (+,-,-)
+      t = t + Bc[-1];         // (-,+,+)
+      t = t + Bp[-1];         // (-,+,-)
+      t = t + Bc[-WB - 1];    // (-,-,+)
+      t = t + Bp[-WB - 1];    // (-,-,-)
       __stcs(&P.out(a, b, c), t * (T)(1.0 / 16.0));
     }
   }
@@ -817,20 +855,20 @@ struct OpRestRMG3 {
 };
 
 // ================================================================= launch
-static bool tsub(CUtensorMap *tm, const S3<T> &s, int k, int H, int bx, int by) {
-  return tmap3<T>(tm, s.s[k], H, H, H, s.pitch, s.plane, bx, by);
+template <class E>
+static bool tsub(CUtensorMap *tm, const S3<E> &s, int k, int H, int bx, int by) {
+  return tmap3<E>(tm, s.s[k], H, H, H, s.pitch, s.plane, bx, by);
 }
 static inline int cdiv(int a, int b) { return (a + b - 1) / b; }
 
-template <int NW>
-static cudaError_t jac_r_nw(const S3<double> &vm, const S3<double> &r, const S3<double> &v, int M, double c1,
-                            double c2, cudaStream_t st) {
-  using Op = OpJacR3T<NW>;
+template <class E, int NW>
+static cudaError_t jac_r_nw(const S3<E> &vm, const S3<E> &r, const S3<E> &v, int M, E c1, E c2, cudaStream_t st) {
+  using Op = OpJacR3T<E, NW>;
   typename Op::Params P{};
   const int H = M / 2 + 1;
-  if (!tsub(&P.tc, vm, C, H, 34, NW + 1) || !tsub(&P.tb, vm, B, H, 34, NW + 1) ||
-      !tsub(&P.tr[0], r, FX, H, RW, NW) || !tsub(&P.tr[1], r, FY, H, RW, NW) || !tsub(&P.tr[2], r, FZ, H, RW, NW) ||
-      !tsub(&P.tr[3], r, C, H, RW, NW))
+  if (!tsub(&P.tc, vm, C, H, Op::BW, NW + 1) || !tsub(&P.tb, vm, B, H, Op::BW, NW + 1) ||
+      !tsub(&P.tr[0], r, FX, H, Op::RWB, NW) || !tsub(&P.tr[1], r, FY, H, Op::RWB, NW) ||
+      !tsub(&P.tr[2], r, FZ, H, Op::RWB, NW) || !tsub(&P.tr[3], r, C, H, Op::RWB, NW))
     return cudaErrorInvalidValue;
   P.v = v;
   P.H = H;
@@ -841,21 +879,20 @@ static cudaError_t jac_r_nw(const S3<double> &vm, const S3<double> &r, const S3<
 
 // warps per CTA of the red Jacobi pass (MG_K3R_NW: 16 = one 512-thread CTA per
 // SM, 8 = two 256-thread CTAs per SM)
-cudaError_t fast3s_jac_r(const S3<double> &vm, const S3<double> &r, const S3<double> &v, int M, double c1, double c2,
-                         cudaStream_t st) {
+template <class E>
+cudaError_t fast3s_jac_r(const S3<E> &vm, const S3<E> &r, const S3<E> &v, int M, E c1, E c2, cudaStream_t st) {
   static const int nw = getenv("MG_K3R_NW") ? atoi(getenv("MG_K3R_NW")) : 16;
-  if (nw == 8) return jac_r_nw<8>(vm, r, v, M, c1, c2, st);
-  return jac_r_nw<16>(vm, r, v, M, c1, c2, st);
+  if (nw == 8) return jac_r_nw<E, 8>(vm, r, v, M, c1, c2, st);
+  return jac_r_nw<E, 16>(vm, r, v, M, c1, c2, st);
 }
 
-template <int NW>
-static cudaError_t jac_m_nw(const D3<double> &vc, const S3<double> &r, const S3<double> &v, int M, double cc,
-                            cudaStream_t st) {
-  using Op = OpJacM3T<NW>;
+template <class E, int NW>
+static cudaError_t jac_m_nw(const D3<E> &vc, const S3<E> &r, const S3<E> &v, int M, E cc, cudaStream_t st) {
+  using Op = OpJacM3T<E, NW>;
   typename Op::Params P{};
   const int H = M / 2 + 1;
-  if (!tmap3<T>(&P.tg, vc.p, H, H, H, vc.pitch, vc.plane, 34, Op::GROWS) || !tsub(&P.tr[0], r, B, H, RW, 2 * NW) ||
-      !tsub(&P.tr[1], r, C, H, RW, 2 * NW))
+  if (!tmap3<E>(&P.tg, vc.p, H, H, H, vc.pitch, vc.plane, Op::BW, Op::GROWS) ||
+      !tsub(&P.tr[0], r, B, H, Op::RWB, 2 * NW) || !tsub(&P.tr[1], r, C, H, Op::RWB, 2 * NW))
     return cudaErrorInvalidValue;
   P.v = v;
   P.H = H;
@@ -867,35 +904,45 @@ static cudaError_t jac_m_nw(const D3<double> &vc, const S3<double> &r, const S3<
 // warps per CTA of the magenta Jacobi pass (MG_K3S_NW: 8 = two 256-thread CTAs
 // per SM, the default -- measured on B200 at 513^3 fp64: jac_m(1) 142 -> 134 us,
 // cycle -0.7 %; 16 = one 512-thread CTA per SM)
-cudaError_t fast3s_jac_m(const D3<double> &vc, const S3<double> &r, const S3<double> &v, int M, double cc,
-                         cudaStream_t st) {
+template <class E>
+cudaError_t fast3s_jac_m(const D3<E> &vc, const S3<E> &r, const S3<E> &v, int M, E cc, cudaStream_t st) {
   static const int nw = getenv("MG_K3S_NW") ? atoi(getenv("MG_K3S_NW")) : 8;
-  if (nw == 8) return jac_m_nw<8>(vc, r, v, M, cc, st);
-  return jac_m_nw<16>(vc, r, v, M, cc, st);
+  if (nw == 8) return jac_m_nw<E, 8>(vc, r, v, M, cc, st);
+  return jac_m_nw<E, 16>(vc, r, v, M, cc, st);
 }
 
-cudaError_t fast3s_rest_rm(const S3<double> &rr, const S3<double> &rm, int M, cudaStream_t st) {
-  using Op = OpRestRM3;
-  Op::Params P{};
+template <class E>
+cudaError_t fast3s_rest_rm(const S3<E> &rr, const S3<E> &rm, int M, cudaStream_t st) {
+  using Op = OpRestRM3<E>;
+  typename Op::Params P{};
   const int H = M / 2 + 1;
-  if (!tsub(&P.tx, rr, FX, H, 36, 33) || !tsub(&P.ty, rr, FY, H, 34, 33) || !tsub(&P.tz, rr, FZ, H, 34, 33) ||
-      !tsub(&P.tc, rr, C, H, RW, RH2))
+  if (!tsub(&P.tx, rr, FX, H, Op::WX, 33) || !tsub(&P.ty, rr, FY, H, Op::WY, 33) ||
+      !tsub(&P.tz, rr, FZ, H, Op::WY, 33) || !tsub(&P.tc, rr, C, H, RW, RH2))
     return cudaErrorInvalidValue;
   P.out = rm;
   P.H = H;
   return launch_zpipe<Op>(P, 32, 32, 0, 0, cdiv(H - 1, 32), cdiv(H - 1, 32), 0, H - 1, st);
 }
 
-cudaError_t fast3s_rest_mg(const S3<double> &rm, const D3<double> &g2, int Mc, cudaStream_t st) {
-  using Op = OpRestMG3;
-  Op::Params P{};
+template <class E>
+cudaError_t fast3s_rest_mg(const S3<E> &rm, const D3<E> &g2, int Mc, cudaStream_t st) {
+  using Op = OpRestMG3<E>;
+  typename Op::Params P{};
   const int H = Mc + 1;
-  if (!tsub(&P.tb, rm, B, H, 34, 33) || !tsub(&P.tc, rm, C, H, RW, RH2)) return cudaErrorInvalidValue;
+  if (!tsub(&P.tb, rm, B, H, Op::WB, 33) || !tsub(&P.tc, rm, C, H, RW, RH2)) return cudaErrorInvalidValue;
   P.out = g2;
   P.H = H;
   return launch_zpipe<Op>(P, 32, 32, 0, 0, cdiv(H - 1, 32), cdiv(H - 1, 32), 1, H - 1, st);
 }
 
+#define INST3S(E)                                                                                               \
+  template cudaError_t fast3s_jac_r<E>(const S3<E> &, const S3<E> &, const S3<E> &, int, E, E, cudaStream_t); \
+  template cudaError_t fast3s_jac_m<E>(const D3<E> &, const S3<E> &, const S3<E> &, int, E, cudaStream_t);    \
+  template cudaError_t fast3s_rest_rm<E>(const S3<E> &, const S3<E> &, int, cudaStream_t);                     \
+  template cudaError_t fast3s_rest_mg<E>(const S3<E> &, const D3<E> &, int, cudaStream_t);
+INST3S(double)
+INST3S(float)
+#undef INST3S
 
 cudaError_t fast3s_jac_mr(const D3<double> &vc, const S3<double> &rm, const S3<double> &rr, const S3<double> &v, int M,
                           double cm, double c1, double c2, cudaStream_t st) {

@@ -208,17 +208,19 @@ cudaError_t fast3p_rest_gr(const D3<T> &r, const S3<T> &rr, int M, cudaStream_t 
 template <class T>
 cudaError_t fast3p_jac_g(const S3<T> &vr, const D3<T> &r, const D3<T> &v, int M, T c, cudaStream_t st);
 
-// Sublattice level passes as plane pipelines (k3s.cu, fp64, single GPU):
-// R(s) -> M(s), M(s) -> G(2s), G(2s) -> M(s) and M(s) -> R(s) (both colours
-// of each Jacobi level in one pass).
-cudaError_t fast3s_rest_rm(const S3<double> &rr, const S3<double> &rm, int M, cudaStream_t st);
-cudaError_t fast3s_rest_mg(const S3<double> &rm, const D3<double> &g2, int Mc, cudaStream_t st);
-// R(s) -> M(s) -> G(2s) in one pass (r_M written, not re-read): rest_rm and rest_mg fused.
+// Sublattice level passes as plane pipelines (k3s.cu, fp64 and fp32, single
+// GPU): R(s) -> M(s), M(s) -> G(2s), G(2s) -> M(s) and M(s) -> R(s) (both
+// colours of each Jacobi level in one pass).
+template <class T>
+cudaError_t fast3s_rest_rm(const S3<T> &rr, const S3<T> &rm, int M, cudaStream_t st);
+template <class T>
+cudaError_t fast3s_rest_mg(const S3<T> &rm, const D3<T> &g2, int Mc, cudaStream_t st);
+template <class T>
+cudaError_t fast3s_jac_m(const D3<T> &vc, const S3<T> &r, const S3<T> &v, int M, T cc, cudaStream_t st);
+template <class T>
+cudaError_t fast3s_jac_r(const S3<T> &vm, const S3<T> &r, const S3<T> &v, int M, T c1, T c2, cudaStream_t st);
+// R(s) -> M(s) -> G(2s) in one pass (r_M written, not re-read): rest_rm and rest_mg fused (fp64).
 cudaError_t fast3s_rest_rmg(const S3<double> &rr, const S3<double> &rm, const D3<double> &g2, int M, cudaStream_t st);
-cudaError_t fast3s_jac_m(const D3<double> &vc, const S3<double> &r, const S3<double> &v, int M, double cc,
-                         cudaStream_t st);
-cudaError_t fast3s_jac_r(const S3<double> &vm, const S3<double> &r, const S3<double> &v, int M, double c1, double c2,
-                         cudaStream_t st);
 // G(2s) -> M(s) -> R(s) in one pass (v_M(s) stays on chip): jac_m and jac_r fused.
 cudaError_t fast3s_jac_mr(const D3<double> &vc, const S3<double> &rm, const S3<double> &rr, const S3<double> &v, int M,
                           double cm, double c1, double c2, cudaStream_t st);

@@ -339,21 +339,23 @@ struct Impl2 : ImplBase {
 };
 
 // ------------------------------------------------------------------ 3D
-// fp64 sublattice pipelines (k3s.cu); the fp32 overloads are never reached
-// (Impl3 keeps the k3l.cu kernels for fp32).
-static void sub3_rest_rm(const S3<double> &rr, const S3<double> &rm, int M, cudaStream_t st) {
-  fast3s_rest_rm(rr, rm, M, st);
+// sublattice pipelines (k3s.cu, fp64 and fp32); the fused octave passes are
+// fp64 only (their fp32 overloads are never reached: fuse_rmg / fuse_mr need fp64).
+template <class T>
+static void sub3_rest_rm(const S3<T> &rr, const S3<T> &rm, int M, cudaStream_t st) {
+  fast3s_rest_rm<T>(rr, rm, M, st);
 }
-static void sub3_rest_mg(const S3<double> &rm, const D3<double> &g2, int Mc, cudaStream_t st) {
-  fast3s_rest_mg(rm, g2, Mc, st);
+template <class T>
+static void sub3_rest_mg(const S3<T> &rm, const D3<T> &g2, int Mc, cudaStream_t st) {
+  fast3s_rest_mg<T>(rm, g2, Mc, st);
 }
-static void sub3_jac_m(const D3<double> &vc, const S3<double> &r, const S3<double> &v, int M, double c,
-                       cudaStream_t st) {
-  fast3s_jac_m(vc, r, v, M, c, st);
+template <class T>
+static void sub3_jac_m(const D3<T> &vc, const S3<T> &r, const S3<T> &v, int M, T c, cudaStream_t st) {
+  fast3s_jac_m<T>(vc, r, v, M, c, st);
 }
-static void sub3_jac_r(const S3<double> &vm, const S3<double> &r, const S3<double> &v, int M, double c1, double c2,
-                       cudaStream_t st) {
-  fast3s_jac_r(vm, r, v, M, c1, c2, st);
+template <class T>
+static void sub3_jac_r(const S3<T> &vm, const S3<T> &r, const S3<T> &v, int M, T c1, T c2, cudaStream_t st) {
+  fast3s_jac_r<T>(vm, r, v, M, c1, c2, st);
 }
 static void sub3_jac_mr(const D3<double> &vc, const S3<double> &rm, const S3<double> &rr, const S3<double> &v, int M,
                         double cm, double c1, double c2, cudaStream_t st) {
@@ -365,10 +367,6 @@ static void sub3_rest_rmg(const S3<double> &rr, const S3<double> &rm, const D3<d
   fast3s_rest_rmg(rr, rm, g2, M, st);
 }
 static void sub3_rest_rmg(const S3<float> &, const S3<float> &, const D3<float> &, int, cudaStream_t) {}
-static void sub3_rest_rm(const S3<float> &, const S3<float> &, int, cudaStream_t) {}
-static void sub3_rest_mg(const S3<float> &, const D3<float> &, int, cudaStream_t) {}
-static void sub3_jac_m(const D3<float> &, const S3<float> &, const S3<float> &, int, float, cudaStream_t) {}
-static void sub3_jac_r(const S3<float> &, const S3<float> &, const S3<float> &, int, float, float, cudaStream_t) {}
 
 template <class T>
 struct Impl3 : ImplBase {
@@ -563,7 +561,8 @@ struct Impl3 : ImplBase {
     const double w = sizeof(T);
     const int L = 3 * k - 2;
     static const bool gen2 = !env_flag("MG_K3_GEN1");   // plane pipelines for the G(s) levels
-    const bool gen2s = gen2 && sizeof(T) == 8;                    // and for the sublattice levels (fp64)
+    static const bool s32 = !env_flag("MG_K3S_NOF32");   // fp32 sublattice pipelines (round 2)
+    const bool gen2s = gen2 && (sizeof(T) == 8 || s32);   // and for the sublattice levels
     void *u = const_cast<void *>(u_in);
     // fused octave passes: bit-identical, but no measurable gain in graph replay on B200 (A/B in
     // DESIGN.md), so opt-in (MG_K3_FUSE=1)
@@ -585,7 +584,7 @@ struct Impl3 : ImplBase {
         if (gen2) fast3p_rest_gr<T>(rG[o], rR[o], M[o], st);
         else lv3_rest_gr<T>(rG[o], rR[o], M[o], st);
       }
-      if (gen2s && fuse_rmg) {   // R(s) -> M(s) -> G(2s) in one pass (r_M written, not re-read)
+      if (gen2s && fuse_rmg && sizeof(T) == 8) {   // R(s) -> M(s) -> G(2s) in one pass (r_M written, not re-read)
         STEP("rest_rmg", g + 1, 1, w * (Nl[g + 1] + Nl[g + 2] + Nl[g + 3]));
         sub3_rest_rmg(rR[o], rM[o], rG[o + 1], M[o], st);
         return;
@@ -605,7 +604,7 @@ struct Impl3 : ImplBase {
     static const bool fuse_mr = env_flag("MG_K3_FUSE");
     auto jac_mr = [&](int o) {
       int g = 3 * o;
-      if (gen2s && fuse_mr && o >= 1) {
+      if (gen2s && fuse_mr && sizeof(T) == 8 && o >= 1) {
         STEP("jac_mr", g + 1, 1, w * (Nl[g + 3] + Nl[g + 2] + 2 * Nl[g + 1]));
         sub3_jac_mr(vG[o + 1], rM[o], rR[o], vR[o], M[o], cMg[o], cR1[o], cR2[o], st);
         return;
@@ -694,11 +693,11 @@ struct Impl3 : ImplBase {
       c = 1;
       for (int o = 0; o < oc; o++) c += (o >= 1) + 2;
       c += 1;
-      const bool gen2 = !env_flag("MG_K3_GEN1"), gen2s = gen2 && sizeof(T) == 8;
-      const bool fz = gen2s && env_flag("MG_K3_FUSE");
+      const bool gen2 = !env_flag("MG_K3_GEN1"), gen2s = gen2 && (sizeof(T) == 8 || !env_flag("MG_K3S_NOF32"));
+      const bool fz = gen2s && sizeof(T) == 8 && env_flag("MG_K3_FUSE");
       auto per_mr_o = [&](int o) { return gen2s ? (fz && o >= 1 ? 1 : 2) : 4; };
       const int od = use_tail ? om : oc;
-      const bool frmg = gen2s && env_flag("MG_K3_FUSE");
+      const bool frmg = gen2s && sizeof(T) == 8 && env_flag("MG_K3_FUSE");
       c = 1;
       for (int o = 0; o < od; o++) c += (o >= 1) + (frmg ? 1 : 2);
       c += 1;   // tail or coarse

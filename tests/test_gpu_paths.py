@@ -58,6 +58,9 @@ CASES = [
     ({"MG_K3_GEN1": "1"}, 3, 129, 4, "float32"),
     ({}, 3, 129, 4, "float64"),
     ({}, 3, 129, 4, "float32"),
+    ({"MG_K3S_NOF32": "1"}, 3, 129, 2, "float32"),   # round 1's fp32 sublattice kernels (k3l.cu)
+    ({"MG_K3R_NW": "8", "MG_K3S_NW": "16"}, 3, 129, 2, "float32"),
+    ({"MG_POISON": "1"}, 3, 129, 2, "float32"),
     ({"MG_FORCE_REF": "1"}, 3, 33, 2, "float64"),
     ({"MG_COARSE_GLOBAL": "1", "MG_TAIL_M3": "0"}, 3, 65, 2, "float64"),
     ({"MG_TAIL_M2": "128"}, 2, 513, 2, "float64"),
