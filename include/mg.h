@@ -162,6 +162,15 @@ int mg_vcycle_norms(mg_solver *s, void *u, const void *f, int ncycles, double *r
  * memory makes the copies asynchronous DMA. */
 int mg_vcycle_host(mg_solver *s, void *u_host, const void *f_host, int ncycles, double *res_hist);
 
+/* A solve from u = 0 (the V-cycle of P:57-92 iterated from a zero initial
+ * approximation, as in every BASELINE config: "V-cycles from u=0") on HOST
+ * arrays: f is copied to the device, u
+ * starts at 0 there (no upload), `ncycles` V-cycles run, u is copied back
+ * into u_host (output only; its previous contents are ignored).  Otherwise as
+ * mg_vcycle_host: res_hist (NULL or ncycles+1 doubles) as in mg_vcycle,
+ * synchronises, MG_EINVAL on NULL arrays or ncycles < 0. */
+int mg_solve_host(mg_solver *s, void *u_host, const void *f_host, int ncycles, double *res_hist);
+
 /* Global norm of x over the interior nodes: MG_NORM_INF = max |x|,
  * MG_NORM_L2 = (h^d sum x^2)^(1/2).  Reduced over ranks.  Synchronises. */
 int mg_norm(mg_solver *s, const void *x, int kind, double *out);

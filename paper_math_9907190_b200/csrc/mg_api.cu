@@ -1126,17 +1126,21 @@ int mg_vcycle(mg_solver *s, void *u, const void *f, int ncycles, double *res_his
 }
 
 // Host arrays (caller layout) are copied straight into the work layout.
-int mg_vcycle_host(mg_solver *s, void *u_host, const void *f_host, int ncycles, double *res_hist) {
+// mg_vcycle_host / mg_solve_host: host arrays in and out, the work layout in
+// between; zero_start: u starts from 0 on the device (a memset, no upload).
+static int host_cycles(mg_solver *s, void *u_host, const void *f_host, int ncycles, double *res_hist, bool zero_start,
+                       const char *who) {
   if (!s) return MG_EINVAL;
-  if (!u_host || !f_host) return fail(s, MG_EINVAL, "mg_vcycle_host: NULL u or f");
-  if (ncycles < 0) return fail(s, MG_EINVAL, "mg_vcycle_host: ncycles < 0");
-  if (res_hist && ncycles + 1 > kHistCap) return fail(s, MG_EINVAL, "mg_vcycle_host: res_hist needs ncycles < 4096");
+  if (!u_host || !f_host) return fail(s, MG_EINVAL, std::string(who) + ": NULL u or f");
+  if (ncycles < 0) return fail(s, MG_EINVAL, std::string(who) + ": ncycles < 0");
+  if (res_hist && ncycles + 1 > kHistCap) return fail(s, MG_EINVAL, std::string(who) + ": res_hist needs ncycles < 4096");
   DeviceGuard g(s->device);
   int rc = begin(s);
   if (rc) return rc;
   rc = ensure_stage(s);
   if (!rc) rc = [&]() -> int {
-    CKS(s, copy_field(s, s->d_u_stage, s->wpitch, u_host, s->pitch, cudaMemcpyHostToDevice));
+    if (zero_start) CKS(s, cudaMemsetAsync(s->d_u_stage, 0, s->work_elems() * s->esz, s->st));
+    else CKS(s, copy_field(s, s->d_u_stage, s->wpitch, u_host, s->pitch, cudaMemcpyHostToDevice));
     const void *fe = s->d_f_stage;
     if (s->cfg.order == 4) {
       // f~ is formed on the device from f in the caller's layout (d_f_stage is large enough)
@@ -1158,6 +1162,14 @@ int mg_vcycle_host(mg_solver *s, void *u_host, const void *f_host, int ncycles, 
   }();
   int rc2 = end(s);   // joins the caller's stream on every path
   return rc ? rc : rc2;
+}
+
+int mg_vcycle_host(mg_solver *s, void *u_host, const void *f_host, int ncycles, double *res_hist) {
+  return host_cycles(s, u_host, f_host, ncycles, res_hist, false, "mg_vcycle_host");
+}
+
+int mg_solve_host(mg_solver *s, void *u_host, const void *f_host, int ncycles, double *res_hist) {
+  return host_cycles(s, u_host, f_host, ncycles, res_hist, true, "mg_solve_host");
 }
 
 // ---------------------------------------------------- convergence factor

@@ -7,7 +7,7 @@ CUDA device is present the calls raise.
 
 The functions mirror the C ABI one to one (``mg_create``, ``mg_create_ex``,
 ``mg_destroy``, ``mg_local_extent``, ``mg_residual``, ``mg_vcycle``, ``mg_vcycle_norms``,
-``mg_vcycle_host``, ``mg_norm``, ``mg_num_levels``, ``mg_level_points``,
+``mg_vcycle_host``, ``mg_solve_host``, ``mg_norm``, ``mg_num_levels``, ``mg_level_points``,
 ``mg_launches_per_cycle``, ``mg_strerror``, ``mg_last_error``);
 :class:`Solver` wraps a handle for torch tensors.
 """
@@ -72,6 +72,8 @@ EXPORTS = {
                                        ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double)]),
     "mg_vcycle_host": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int,
                                       ctypes.POINTER(ctypes.c_double)]),
+    "mg_solve_host": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int,
+                                     ctypes.POINTER(ctypes.c_double)]),
     "mg_norm": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, ctypes.POINTER(ctypes.c_double)]),
     "mg_num_levels": (ctypes.c_int, [ctypes.c_void_p]),
     "mg_level_points": (ctypes.c_int64, [ctypes.c_void_p, ctypes.c_int]),
@@ -166,6 +168,12 @@ def mg_vcycle_norms(h, u_ptr: int, f_ptr: int, ncycles: int):
 def mg_vcycle_host(h, u_ptr: int, f_ptr: int, ncycles: int, hist: bool = False):
     buf = (ctypes.c_double * (ncycles + 1))() if hist else None
     _check(load().mg_vcycle_host(h, u_ptr, f_ptr, ncycles, buf), h, "mg_vcycle_host")
+    return np.array(list(buf)) if hist else None
+
+
+def mg_solve_host(h, u_ptr: int, f_ptr: int, ncycles: int, hist: bool = False):
+    buf = (ctypes.c_double * (ncycles + 1))() if hist else None
+    _check(load().mg_solve_host(h, u_ptr, f_ptr, ncycles, buf), h, "mg_solve_host")
     return np.array(list(buf)) if hist else None
 
 
@@ -378,6 +386,11 @@ class Solver:
         """u_host / f_host: CPU tensors (ideally pinned) of ``self.shape``."""
         assert u_host.shape == self.shape and f_host.shape == self.shape and not u_host.is_cuda
         return mg_vcycle_host(self.h, u_host.data_ptr(), f_host.data_ptr(), ncycles, hist)
+
+    def solve_host(self, u_host, f_host, ncycles: int, hist: bool = False):
+        """ncycles V-cycles from u = 0 on HOST tensors: f_host in, u_host out."""
+        assert u_host.shape == self.shape and f_host.shape == self.shape and not u_host.is_cuda
+        return mg_solve_host(self.h, u_host.data_ptr(), f_host.data_ptr(), ncycles, hist)
 
     def profile(self, u, f, ncycles: int = 5):
         return mg_profile(self.h, self._chk(u), self._chk(f), ncycles)

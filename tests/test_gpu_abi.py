@@ -12,6 +12,7 @@ import torch
 
 import oracle
 from paper_math_9907190_b200 import mg
+from paper_math_9907190_b200.mg import Solver
 from paper_math_9907190_b200 import workloads as W
 
 pytestmark = pytest.mark.gpu
@@ -114,6 +115,25 @@ def test_vcycle_host_pitch_n(order):
         assert np.array_equal(hg, ho)
     finally:
         mg.mg_destroy(h)
+
+
+@pytest.mark.parametrize("dim,n,order,dt", [(2, 513, 2, "f64"), (2, 257, 4, "f64"), (2, 513, 2, "f32"),
+                                            (3, 65, 2, "f64"), (3, 65, 4, "f32")])
+def test_solve_host_from_zero(dim, n, order, dt):
+    """mg_solve_host: f in, u out, u starts at 0 on the device whatever u_host holds."""
+    npdt = np.float64 if dt == "f64" else np.float32
+    p = (P2 if order == 2 else 1.20) if dim == 2 else (1.11, 1.42, 1.08, 0.99)
+    tdt = torch.float64 if dt == "f64" else torch.float32
+    s = Solver(dim, n, order=order, p=p, dtype=tdt)
+    f = W.random_field(dim, n, seed=49).astype(npdt)
+    fh = torch.zeros(s.shape, dtype=tdt).pin_memory()
+    s.view(fh).copy_(torch.from_numpy(f))
+    uh = torch.full(s.shape, 7.0, dtype=tdt).pin_memory()   # garbage: an output-only array
+    hg = s.solve_host(uh, fh, 5, True)
+    uo = np.zeros_like(f)
+    ho = oracle.vcycle(uo, f, p, 5, order=order, hist=True)
+    assert np.array_equal(s.view(uh).numpy(), uo)
+    assert np.array_equal(hg, ho)
 
 
 @pytest.mark.parametrize("dim,n,order", [(2, 129, 2), (2, 129, 4), (3, 33, 2), (3, 33, 4)])
