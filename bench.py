@@ -379,22 +379,32 @@ def main():
     if rank == 0 and ws == 1 and not args.no_cpu:
         cpu = cpu_baseline(w, np.float64 if args.dtype == "f64" else np.float32)
 
-    # BASELINE configs[4] (3D 513^3 fp64) rides along as a sub-record on one GPU, so
-    # the driver's single line carries both north-star workloads
+    # BASELINE configs[4] (3D 513^3 fp64) and configs[2]'s "fp32 variant also timed"
+    # (2D 8193^2 fp32) ride along as sub-records on one GPU, so the driver's single
+    # line carries every north-star workload
     sub = []
-    if not slabs and not args.no_sub and w.name != "3d_513":
-        for key in ("s", "u", "f"):
-            m.pop(key)
-        del s, u, f
-        torch.cuda.empty_cache()
-        w3 = W.WORKLOADS["3d_513"]
-        m3 = measure(args, w3, torch.float64, ws, rank, local, False, dist)
-        sub.append({"workload": w3.name, "dtype": "f64", "value": m3["value"], "unit": UNIT,
-                    "ms_per_step": m3["ms_per_step"], "steps": args.steps, "warmup": args.warmup,
-                    "unknowns": m3["N"], "survey_frac_of_nominal_8tbs": m3["survey_frac_nominal"],
-                    "gpu_launches": m3["s"].launches_per_cycle * args.steps,
-                    "roofline": m3["roofline"], "clocks": m3["clocks"]})
-        del m3
+    if not slabs and not args.no_sub:
+        extra = []
+        if w.name != "3d_513":
+            extra.append(("3d_513", torch.float64))
+        if w.name == "2d_8193" and tdt == torch.float64:
+            extra.append(("2d_8193", torch.float32))
+        if extra:
+            for key in ("s", "u", "f"):
+                m.pop(key)
+            del s, u, f
+            torch.cuda.empty_cache()
+        for wname, sdt in extra:
+            wx = W.WORKLOADS[wname]
+            mx = measure(args, wx, sdt, ws, rank, local, False, dist)
+            sub.append({"workload": wx.name, "dtype": "f64" if sdt == torch.float64 else "f32",
+                        "value": mx["value"], "unit": UNIT,
+                        "ms_per_step": mx["ms_per_step"], "steps": args.steps, "warmup": args.warmup,
+                        "unknowns": mx["N"], "survey_frac_of_nominal_8tbs": mx["survey_frac_nominal"],
+                        "gpu_launches": mx["s"].launches_per_cycle * args.steps,
+                        "roofline": mx["roofline"], "clocks": mx["clocks"]})
+            del mx
+            torch.cuda.empty_cache()
 
     line = {
         "metric": METRIC, "value": m["value"], "unit": UNIT, "n_gpus": ws, "steps": args.steps,
