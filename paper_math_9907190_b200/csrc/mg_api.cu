@@ -368,6 +368,16 @@ static void sub3_rest_rmg(const S3<double> &rr, const S3<double> &rm, const D3<d
 }
 static void sub3_rest_rmg(const S3<float> &, const S3<float> &, const D3<float> &, int, cudaStream_t) {}
 
+// First octave of the fused fp64 octave passes (k3s.cu): G(2s) -> M(s) -> R(s)
+// (jac_mr) and R(s) -> M(s) -> G(2s) (rest_rmg); 1000 = never.  MG_K3_FUSE=1
+// fuses both everywhere they exist (jac_mr from octave 1, rest_rmg from 0);
+// MG_K3_FUSE_MR / MG_K3_FUSE_RMG = o set the first octave of each.
+static int k3_fuse_min(bool mr) {
+  const char *e = getenv(mr ? "MG_K3_FUSE_MR" : "MG_K3_FUSE_RMG");
+  if (e && *e) return atoi(e) < 0 ? 1000 : (mr ? std::max(1, atoi(e)) : atoi(e));
+  return env_flag("MG_K3_FUSE") ? (mr ? 1 : 0) : 1000;
+}
+
 template <class T>
 struct Impl3 : ImplBase {
   const mg_solver *s;
@@ -566,7 +576,7 @@ struct Impl3 : ImplBase {
     void *u = const_cast<void *>(u_in);
     // fused octave passes: bit-identical, but no measurable gain in graph replay on B200 (A/B in
     // DESIGN.md), so opt-in (MG_K3_FUSE=1)
-    static const bool fuse_rmg = env_flag("MG_K3_FUSE");
+    static const int rmg_min = k3_fuse_min(false);
     // Serpentine item order (zpipe Sched::rev): descent pass d (desc_fine = 0,
     // then rest_rm, rest_mg, rest_gr, ...) runs reversed when d is odd; ascent
     // passes alternate backwards from asc_fine (reversed), so the next
@@ -584,7 +594,7 @@ struct Impl3 : ImplBase {
         if (gen2) fast3p_rest_gr<T>(rG[o], rR[o], M[o], st);
         else lv3_rest_gr<T>(rG[o], rR[o], M[o], st);
       }
-      if (gen2s && fuse_rmg && sizeof(T) == 8) {   // R(s) -> M(s) -> G(2s) in one pass (r_M written, not re-read)
+      if (gen2s && sizeof(T) == 8 && o >= rmg_min) {   // R(s) -> M(s) -> G(2s) in one pass (r_M written, not re-read)
         STEP("rest_rmg", g + 1, 1, w * (Nl[g + 1] + Nl[g + 2] + Nl[g + 3]));
         sub3_rest_rmg(rR[o], rM[o], rG[o + 1], M[o], st);
         return;
@@ -601,10 +611,10 @@ struct Impl3 : ImplBase {
     // G(2s) -> M(s) -> R(s): one fused pass (v_M(s) stays on chip) or the two level kernels.
     // Measured on B200: the fused pass wins on the octaves o >= 1 (2 launches -> 1) but loses at
     // o = 0 (0.41 vs 0.39 ms: its 29 x 13 core tile recomputes 26 % ring and is issue-bound there).
-    static const bool fuse_mr = env_flag("MG_K3_FUSE");
+    static const int mr_min = k3_fuse_min(true);
     auto jac_mr = [&](int o) {
       int g = 3 * o;
-      if (gen2s && fuse_mr && sizeof(T) == 8 && o >= 1) {
+      if (gen2s && sizeof(T) == 8 && o >= mr_min) {
         STEP("jac_mr", g + 1, 1, w * (Nl[g + 3] + Nl[g + 2] + 2 * Nl[g + 1]));
         sub3_jac_mr(vG[o + 1], rM[o], rR[o], vR[o], M[o], cMg[o], cR1[o], cR2[o], st);
         return;
@@ -694,12 +704,12 @@ struct Impl3 : ImplBase {
       for (int o = 0; o < oc; o++) c += (o >= 1) + 2;
       c += 1;
       const bool gen2 = !env_flag("MG_K3_GEN1"), gen2s = gen2 && (sizeof(T) == 8 || !env_flag("MG_K3S_NOF32"));
-      const bool fz = gen2s && sizeof(T) == 8 && env_flag("MG_K3_FUSE");
-      auto per_mr_o = [&](int o) { return gen2s ? (fz && o >= 1 ? 1 : 2) : 4; };
+      const bool f64 = gen2s && sizeof(T) == 8;
+      const int mr_min = k3_fuse_min(true), rmg_min = k3_fuse_min(false);
+      auto per_mr_o = [&](int o) { return gen2s ? (f64 && o >= mr_min ? 1 : 2) : 4; };
       const int od = use_tail ? om : oc;
-      const bool frmg = gen2s && sizeof(T) == 8 && env_flag("MG_K3_FUSE");
       c = 1;
-      for (int o = 0; o < od; o++) c += (o >= 1) + (frmg ? 1 : 2);
+      for (int o = 0; o < od; o++) c += (o >= 1) + (f64 && o >= rmg_min ? 1 : 2);
       c += 1;   // tail or coarse
       if (!use_tail)
         for (int o = oc - 1; o >= od; o--) c += per_mr_o(o) + (gen2 ? 1 : 2);
