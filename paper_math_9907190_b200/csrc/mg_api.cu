@@ -575,7 +575,7 @@ struct Impl3 : ImplBase {
     const bool gen2s = gen2 && (sizeof(T) == 8 || s32);   // and for the sublattice levels
     void *u = const_cast<void *>(u_in);
     // fused octave passes: bit-identical, but no measurable gain in graph replay on B200 (A/B in
-    // DESIGN.md), so opt-in (MG_K3_FUSE=1)
+    // DESIGN.md), so opt-in (MG_K3_FUSE=1, or per octave MG_K3_FUSE_RMG / MG_K3_FUSE_MR)
     static const int rmg_min = k3_fuse_min(false);
     // Serpentine item order (zpipe Sched::rev): descent pass d (desc_fine = 0,
     // then rest_rm, rest_mg, rest_gr, ...) runs reversed when d is odd; ascent
