@@ -171,6 +171,18 @@ int mg_vcycle_host(mg_solver *s, void *u_host, const void *f_host, int ncycles, 
  * synchronises, MG_EINVAL on NULL arrays or ncycles < 0. */
 int mg_solve_host(mg_solver *s, void *u_host, const void *f_host, int ncycles, double *res_hist);
 
+/* `count` independent solves from u = 0, as mg_solve_host, of the HOST right-
+ * hand sides f_hosts[i] into u_hosts[i] (caller layout, pitch as configured).
+ * Problem i's upload, its cycles and its download run on three streams over
+ * two device staging slots, so on a full-duplex link the download of problem
+ * i-1 and the upload of problem i+1 overlap the cycles of problem i; the
+ * results equal count calls of mg_solve_host.  Pinned host memory makes the
+ * copies asynchronous DMA; entries may alias (the downloads run in problem
+ * order, the last one wins).  Synchronises.  MG_EINVAL on count < 0,
+ * ncycles < 0 or a NULL array.  Slab (multi-GPU) solvers run the problems one
+ * by one. */
+int mg_solve_host_batch(mg_solver *s, void *const *u_hosts, const void *const *f_hosts, int count, int ncycles);
+
 /* Global norm of x over the interior nodes: MG_NORM_INF = max |x|,
  * MG_NORM_L2 = (h^d sum x^2)^(1/2).  Reduced over ranks.  Synchronises. */
 int mg_norm(mg_solver *s, const void *x, int kind, double *out);

@@ -956,6 +956,15 @@ int mg_destroy(mg_solver *s) {
   cudaFree(s->d_ft);
   cudaFree(s->d_u_stage);
   cudaFree(s->d_f_stage);
+  cudaFree(s->d_u_stage2);
+  cudaFree(s->d_f_stage2);
+  for (int i = 0; i < 2; i++) {
+    if (s->ev_h2d[i]) cudaEventDestroy(s->ev_h2d[i]);
+    if (s->ev_comp[i]) cudaEventDestroy(s->ev_comp[i]);
+    if (s->ev_d2h[i]) cudaEventDestroy(s->ev_d2h[i]);
+  }
+  if (s->st_h2d) cudaStreamDestroy(s->st_h2d);
+  if (s->st_d2h) cudaStreamDestroy(s->st_d2h);
   if (s->h_hist) cudaFreeHost(s->h_hist);
   cudaFree(s->d_l2);
   if (s->h_l2) cudaFreeHost(s->h_l2);
@@ -1019,9 +1028,13 @@ static int ensure_stage(mg_solver *s) {
 // rows x n elements between two layouts (pitches in elements); one contiguous
 // copy when the layouts agree (a pitched host<->device copy of 64 KB rows is
 // slower than one linear DMA transfer)
+static cudaError_t copy_field_st(mg_solver *s, void *dst, int64_t dp, const void *src, int64_t sp,
+                                 cudaMemcpyKind kind, cudaStream_t st) {
+  if (dp == sp) return cudaMemcpyAsync(dst, src, (size_t)s->rows() * sp * s->esz, kind, st);
+  return cudaMemcpy2DAsync(dst, dp * s->esz, src, sp * s->esz, s->cfg.n * s->esz, s->rows(), kind, st);
+}
 static cudaError_t copy_field(mg_solver *s, void *dst, int64_t dp, const void *src, int64_t sp, cudaMemcpyKind kind) {
-  if (dp == sp) return cudaMemcpyAsync(dst, src, (size_t)s->rows() * sp * s->esz, kind, s->st);
-  return cudaMemcpy2DAsync(dst, dp * s->esz, src, sp * s->esz, s->cfg.n * s->esz, s->rows(), kind, s->st);
+  return copy_field_st(s, dst, dp, src, sp, kind, s->st);
 }
 
 int mg_residual(mg_solver *s, const void *u, const void *f, void *r) {
@@ -1180,6 +1193,85 @@ int mg_vcycle_host(mg_solver *s, void *u_host, const void *f_host, int ncycles, 
 
 int mg_solve_host(mg_solver *s, void *u_host, const void *f_host, int ncycles, double *res_hist) {
   return host_cycles(s, u_host, f_host, ncycles, res_hist, true, "mg_solve_host");
+}
+
+// Independent solves from u = 0 of `count` right-hand sides: problem i's f
+// upload (stream st_h2d), cycles (the solver stream) and u download (st_d2h)
+// run on three streams over two device staging slots, so the download of
+// problem i-1 and the upload of problem i+1 overlap the cycles of problem i
+// (PCIe is full duplex).  Slot reuse is ordered by events: the upload into a
+// slot waits for the cycles that last read its f, the cycles wait for the
+// download that last read its u.
+int mg_solve_host_batch(mg_solver *s, void *const *u_hosts, const void *const *f_hosts, int count, int ncycles) {
+  if (!s) return MG_EINVAL;
+  if (count < 0 || ncycles < 0 || (count > 0 && (!u_hosts || !f_hosts)))
+    return fail(s, MG_EINVAL, "mg_solve_host_batch: bad argument");
+  for (int i = 0; i < count; i++)
+    if (!u_hosts[i] || !f_hosts[i]) return fail(s, MG_EINVAL, "mg_solve_host_batch: NULL u or f");
+  if (s->cfg.nranks > 1 || (s->cfg.flags & MG_FLAG_SLABS)) {   // slab solvers: one problem at a time
+    for (int i = 0; i < count; i++) {
+      int rc = host_cycles(s, u_hosts[i], f_hosts[i], ncycles, nullptr, true, "mg_solve_host_batch");
+      if (rc) return rc;
+    }
+    return MG_OK;
+  }
+  DeviceGuard g(s->device);
+  int rc = begin(s);
+  if (rc) return rc;
+  rc = ensure_stage(s);
+  if (!rc) rc = [&]() -> int {
+    const size_t bytes = s->work_elems() * s->esz;
+    if (!s->d_u_stage2) {
+      CKS(s, cudaMalloc(&s->d_u_stage2, bytes));
+      CKS(s, cudaMalloc(&s->d_f_stage2, bytes));
+      CKS(s, cudaMemsetAsync(s->d_u_stage2, 0, bytes, s->st));
+      CKS(s, cudaMemsetAsync(s->d_f_stage2, 0, bytes, s->st));
+    }
+    if (!s->st_h2d) {
+      CKS(s, cudaStreamCreateWithFlags(&s->st_h2d, cudaStreamNonBlocking));
+      CKS(s, cudaStreamCreateWithFlags(&s->st_d2h, cudaStreamNonBlocking));
+      for (int i = 0; i < 2; i++) {
+        CKS(s, cudaEventCreateWithFlags(&s->ev_h2d[i], cudaEventDisableTiming));
+        CKS(s, cudaEventCreateWithFlags(&s->ev_comp[i], cudaEventDisableTiming));
+        CKS(s, cudaEventCreateWithFlags(&s->ev_d2h[i], cudaEventDisableTiming));
+      }
+    }
+    void *us[2] = {s->d_u_stage, s->d_u_stage2}, *fs[2] = {s->d_f_stage, s->d_f_stage2};
+    // the copy streams start after everything queued so far on the solver stream (and so the caller's)
+    CKS(s, cudaEventRecord(s->ev_comp[0], s->st));
+    CKS(s, cudaStreamWaitEvent(s->st_h2d, s->ev_comp[0], 0));
+    CKS(s, cudaStreamWaitEvent(s->st_d2h, s->ev_comp[0], 0));
+    for (int i = 0; i < count; i++) {
+      const int k = i & 1;
+      if (i >= 2) CKS(s, cudaStreamWaitEvent(s->st_h2d, s->ev_comp[k], 0));   // f[k] free
+      if (s->cfg.order == 4)
+        CKS(s, cudaMemcpyAsync(fs[k], f_hosts[i], s->field_elems() * s->esz, cudaMemcpyHostToDevice, s->st_h2d));
+      else
+        CKS(s, copy_field_st(s, fs[k], s->wpitch, f_hosts[i], s->pitch, cudaMemcpyHostToDevice, s->st_h2d));
+      CKS(s, cudaEventRecord(s->ev_h2d[k], s->st_h2d));
+      CKS(s, cudaStreamWaitEvent(s->st, s->ev_h2d[k], 0));
+      if (i >= 2) CKS(s, cudaStreamWaitEvent(s->st, s->ev_d2h[k], 0));          // u[k] downloaded
+      CKS(s, cudaMemsetAsync(us[k], 0, bytes, s->st));
+      const void *fe = fs[k];
+      if (s->cfg.order == 4) {
+        s->impl->enqueue_ftilde(fs[k], s->d_ft, s->st, s->wpitch);
+        fe = s->d_ft;
+      }
+      int r = cycles_work(s, us[k], fe, ncycles, nullptr);
+      if (r) return r;
+      CKS(s, cudaEventRecord(s->ev_comp[k], s->st));
+      CKS(s, cudaStreamWaitEvent(s->st_d2h, s->ev_comp[k], 0));
+      CKS(s, copy_field_st(s, u_hosts[i], s->pitch, us[k], s->wpitch, cudaMemcpyDeviceToHost, s->st_d2h));
+      CKS(s, cudaEventRecord(s->ev_d2h[k], s->st_d2h));
+    }
+    // the solver stream (and through end() the caller's) ends after the last download
+    CKS(s, cudaEventRecord(s->ev_d2h[0], s->st_d2h));
+    CKS(s, cudaStreamWaitEvent(s->st, s->ev_d2h[0], 0));
+    CKS(s, cudaStreamSynchronize(s->st));
+    return MG_OK;
+  }();
+  int rc2 = end(s);
+  return rc ? rc : rc2;
 }
 
 // ---------------------------------------------------- convergence factor

@@ -269,6 +269,11 @@ struct mg_solver {
   double *d_ss = nullptr;
   void *d_ft = nullptr;                    // order-4 f~ (work layout)
   void *d_u_stage = nullptr, *d_f_stage = nullptr;   // work-layout staging of u, f (host calls, unaligned layouts)
+  // mg_solve_host_batch: a second staging pair and the copy streams, so that one problem's
+  // upload and another's download overlap the current problem's cycles
+  void *d_u_stage2 = nullptr, *d_f_stage2 = nullptr;
+  cudaStream_t st_h2d = nullptr, st_d2h = nullptr;
+  cudaEvent_t ev_h2d[2] = {}, ev_comp[2] = {}, ev_d2h[2] = {};
   struct GraphEntry {
     cudaGraphExec_t exec;
     const void *uin, *uout, *f;

@@ -7,7 +7,7 @@ CUDA device is present the calls raise.
 
 The functions mirror the C ABI one to one (``mg_create``, ``mg_create_ex``,
 ``mg_destroy``, ``mg_local_extent``, ``mg_residual``, ``mg_vcycle``, ``mg_vcycle_norms``,
-``mg_vcycle_host``, ``mg_solve_host``, ``mg_norm``, ``mg_num_levels``, ``mg_level_points``,
+``mg_vcycle_host``, ``mg_solve_host``, ``mg_solve_host_batch``, ``mg_norm``, ``mg_num_levels``, ``mg_level_points``,
 ``mg_launches_per_cycle``, ``mg_strerror``, ``mg_last_error``);
 :class:`Solver` wraps a handle for torch tensors.
 """
@@ -74,6 +74,8 @@ EXPORTS = {
                                       ctypes.POINTER(ctypes.c_double)]),
     "mg_solve_host": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int,
                                      ctypes.POINTER(ctypes.c_double)]),
+    "mg_solve_host_batch": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(ctypes.c_void_p),
+                                           ctypes.POINTER(ctypes.c_void_p), ctypes.c_int, ctypes.c_int]),
     "mg_norm": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, ctypes.POINTER(ctypes.c_double)]),
     "mg_num_levels": (ctypes.c_int, [ctypes.c_void_p]),
     "mg_level_points": (ctypes.c_int64, [ctypes.c_void_p, ctypes.c_int]),
@@ -175,6 +177,14 @@ def mg_solve_host(h, u_ptr: int, f_ptr: int, ncycles: int, hist: bool = False):
     buf = (ctypes.c_double * (ncycles + 1))() if hist else None
     _check(load().mg_solve_host(h, u_ptr, f_ptr, ncycles, buf), h, "mg_solve_host")
     return np.array(list(buf)) if hist else None
+
+
+def mg_solve_host_batch(h, u_ptrs, f_ptrs, ncycles: int) -> None:
+    n = len(u_ptrs)
+    assert len(f_ptrs) == n
+    ua = (ctypes.c_void_p * max(n, 1))(*u_ptrs)
+    fa = (ctypes.c_void_p * max(n, 1))(*f_ptrs)
+    _check(load().mg_solve_host_batch(h, ua, fa, n, ncycles), h, "mg_solve_host_batch")
 
 
 def mg_norm(h, x_ptr: int, kind: int = MG_NORM_INF) -> float:
@@ -391,6 +401,13 @@ class Solver:
         """ncycles V-cycles from u = 0 on HOST tensors: f_host in, u_host out."""
         assert u_host.shape == self.shape and f_host.shape == self.shape and not u_host.is_cuda
         return mg_solve_host(self.h, u_host.data_ptr(), f_host.data_ptr(), ncycles, hist)
+
+    def solve_host_batch(self, u_hosts, f_hosts, ncycles: int):
+        """Independent solves from u = 0: f_hosts[i] in, u_hosts[i] out (HOST tensors of
+        ``self.shape``), uploads and downloads overlapping the cycles (include/mg.h)."""
+        for t in list(u_hosts) + list(f_hosts):
+            assert t.shape == self.shape and not t.is_cuda
+        mg_solve_host_batch(self.h, [t.data_ptr() for t in u_hosts], [t.data_ptr() for t in f_hosts], ncycles)
 
     def profile(self, u, f, ncycles: int = 5):
         return mg_profile(self.h, self._chk(u), self._chk(f), ncycles)

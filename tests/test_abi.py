@@ -27,7 +27,8 @@ def lib():
 def test_header_declares_the_boundary():
     names = _declared()
     for want in ("mg_create", "mg_create_ex", "mg_residual", "mg_vcycle", "mg_norm", "mg_destroy",
-                 "mg_local_extent", "mg_strerror", "mg_last_error", "mg_vcycle_host", "mg_solve_host"):
+                 "mg_local_extent", "mg_strerror", "mg_last_error", "mg_vcycle_host", "mg_solve_host",
+                 "mg_solve_host_batch"):
         assert want in names
 
 

@@ -136,6 +136,30 @@ def test_solve_host_from_zero(dim, n, order, dt):
     assert np.array_equal(hg, ho)
 
 
+@pytest.mark.parametrize("dim,n,order,dt,count", [(2, 513, 2, "f64", 5), (2, 257, 4, "f64", 3), (2, 513, 2, "f32", 4),
+                                                  (3, 65, 2, "f64", 3), (3, 65, 4, "f32", 2), (2, 129, 2, "f64", 1),
+                                                  (2, 129, 2, "f64", 0)])
+def test_solve_host_batch(dim, n, order, dt, count):
+    """mg_solve_host_batch: every problem of the overlapped batch equals its own
+    oracle solve from u = 0 (distinct right-hand sides, garbage in the outputs)."""
+    npdt = np.float64 if dt == "f64" else np.float32
+    p = (P2 if order == 2 else 1.20) if dim == 2 else (1.11, 1.42, 1.08, 0.99)
+    tdt = torch.float64 if dt == "f64" else torch.float32
+    s = Solver(dim, n, order=order, p=p, dtype=tdt)
+    fs = [W.random_field(dim, n, seed=60 + i).astype(npdt) for i in range(count)]
+    fh = []
+    for f in fs:
+        t = torch.zeros(s.shape, dtype=tdt).pin_memory()
+        s.view(t).copy_(torch.from_numpy(f))
+        fh.append(t)
+    uh = [torch.full(s.shape, -3.0, dtype=tdt).pin_memory() for _ in range(count)]
+    s.solve_host_batch(uh, fh, 4)
+    for f, u in zip(fs, uh):
+        uo = np.zeros_like(f)
+        oracle.vcycle(uo, f, p, 4, order=order)
+        assert np.array_equal(s.view(u).numpy(), uo)
+
+
 @pytest.mark.parametrize("dim,n,order", [(2, 129, 2), (2, 129, 4), (3, 33, 2), (3, 33, 4)])
 def test_residual_and_norm_pitch_n(dim, n, order):
     h = mg.mg_create(dim, n, order, 1.0)

@@ -140,15 +140,17 @@ def test_cycle_fusion_call_patterns(order, dtype):
 
 
 @pytest.mark.slow
-def test_parity_3d_513_full_size():
+@pytest.mark.parametrize("dtype", [np.float64, np.float32], ids=["f64", "f32"])
+def test_parity_3d_513_full_size(dtype):
     """BASELINE configs[4] at full size and the north star's 10 V-cycles,
-    compared element by element, with and without the residual history."""
-    f = W.workload_rhs("3d_513")
+    compared element by element, with and without the residual history; fp32
+    as well (the fp32 sublattice passes of round 2, k3s.cu)."""
+    f = W.workload_rhs("3d_513").astype(dtype)
     u0 = np.zeros_like(f)
-    uo, ho = _oracle_run(3, 513, 2, P3, f, u0, 10, np.float64)
+    uo, ho = _oracle_run(3, 513, 2, P3, f, u0, 10, dtype)
     for hist in (True, False):
-        ug, hg = _gpu_run(3, 513, 2, P3, f, u0, 10, np.float64, hist=hist)
-        assert _rel(ug, uo) <= 1e-11
+        ug, hg = _gpu_run(3, 513, 2, P3, f, u0, 10, dtype, hist=hist)
+        assert _rel(ug, uo) <= (1e-11 if dtype == np.float64 else 1e-5)
         assert np.array_equal(ug, uo), (hist, _rel(ug, uo))
         if hist:
             assert np.array_equal(hg, ho)
