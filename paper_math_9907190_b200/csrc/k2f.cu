@@ -654,9 +654,16 @@ struct OpJac2A {
 // A(s)'s node space.  v_A(s) is computed (OpJac2A's two colours, same node
 // formulas and operand order) on the ring [a0-1, a0+TX] x [b0-1, b0+TY] that
 // the O update needs, then OpJac2D's two colours run from shared memory.
-template <class T, int STG, int NTH, int TYA>
+// QD (fp32): the two D(s-1) colours take four columns per item (16-byte
+// vectors from a four-aligned origin) instead of two: half the items and
+// shared-memory instructions of the two largest phases; v_A(s) and O sit two
+// columns further left so every vector is aligned.  Same node formulas and
+// operand order.
+template <class T, int STG, int NTH, int TYA, bool QD = false>
 struct OpJac2AD {
+  static_assert(!QD || sizeof(T) == 4, "four-column items are the fp32 form");
   static constexpr int NT = NTH, STAGES = STG, NW = NT / 32, TY = TYA;
+  static constexpr int XO = QD ? 2 : 0;   // extra scratch columns on the left (v_A(s), O)
   static constexpr int H2 = hx<T>(2), H1 = hx<T>(1);
   static constexpr int RAW = w16<T>(TX + 2 + H2), RAH = TY + 4;            // r_A(s): [a0-2, a0+TX+2) x [b0-2, b0+TY+2)
   static constexpr int VDW = w16<T>(TX / 2 + 2 + H2), VDH = TY / 2 + 4;    // v_D(s) E/O: the D(s) ring of those greens
@@ -666,8 +673,8 @@ struct OpJac2AD {
   static constexpr int RA_OFF = 0, VE_OFF = al128(RA_BYTES), VO_OFF = VE_OFF + al128(VD_BYTES),
                        RO_OFF = VO_OFF + al128(VD_BYTES), RE_OFF = RO_OFF + al128(RO_BYTES);
   static constexpr int STAGE = al128(RE_OFF + RE_BYTES);
-  // scratch: v_A(s) on [a0-2, a0+TX+2) x [b0-2, b0+TY+2); O of v_D(s-1) on [a0-2, a0+TX) x [b0-1, b0+TY)
-  static constexpr int VAW = TX + 4, VAH = TY + 4, OSW = TX + 2, OSH = TY + 1;
+  // scratch: v_A(s) on [a0-2-XO, a0+TX+2+XO) x [b0-2, b0+TY+2); O of v_D(s-1) on [a0-2-XO, a0+TX) x [b0-1, b0+TY)
+  static constexpr int VAW = TX + 4 + 2 * XO, VAH = TY + 4, OSW = TX + 2 + XO, OSH = TY + 1;
   static constexpr int VA_BYTES = al128(VAW * VAH * (int)sizeof(T));
   static constexpr int SMEM = STAGES * STAGE + VA_BYTES + al128(OSW * OSH * sizeof(T));
   struct Params {
@@ -703,15 +710,15 @@ struct OpJac2AD {
     STile<T> VO = stile<T>(st + VO_OFF, VDW, a0 / 2 - H2, b0 / 2 - 2);
     STile<T> RO = stile<T>(st + RO_OFF, ROW, a0 - H1, b0 - 1);
     STile<T> RE = stile<T>(st + RE_OFF, REW, a0, b0);
-    STile<T> VA = stile<T>(scr, VAW, a0 - 2, b0 - 2);
-    STile<T> OS = stile<T>(scr + VA_BYTES, OSW, a0 - 2, b0 - 1);
+    STile<T> VA = stile<T>(scr, VAW, a0 - 2 - XO, b0 - 2);
+    STile<T> OS = stile<T>(scr + VA_BYTES, OSW, a0 - 2 - XO, b0 - 1);
     const SplitTile2<T> VD{VE, VO};
     const T ca = P.ca, cd = P.cd;
     auto in = [&](int x, int y) { return x >= 1 && y >= 1 && x <= W - 1 && y <= W - 1; };
     // A(s) colour 1: the green node (x + y odd) of each column pair (a0-2+2p, a0-1+2p), rows
     // b0-2 .. b0+TY+1 taken two at a time (even, odd) so every E/O choice is static
     const T *Eb = (const T *)(st + VE_OFF), *Ob = (const T *)(st + VO_OFF), *Rb = (const T *)(st + RA_OFF);
-    T *Vb = (T *)scr;
+    T *Vb = (T *)scr + XO;   // raw v_A(s) offsets below are relative to column a0-2
     constexpr int GP = TX / 2 + 2, GR = TY / 2 + 2;
 #pragma unroll
     for (int k = 0; k < (GP * GR + NT - 1) / NT; k++) {
@@ -757,50 +764,109 @@ struct OpJac2AD {
       }
     }
     __syncthreads();
-    // D(s-1) colour 1 (Eajacr) on O nodes, pairs (a, a+1) = (a0-2+2p, a0-1+2p), rows b0-1 .. b0+TY-1
-    const int64_t pitch = P.v.pitch;
+    if constexpr (QD) {
+      // D(s-1) colour 1 on O nodes, four columns a = a0-4+4g .. a+3 per item (g = 0 .. TX/4), rows b0-1 .. b0+TY-1
+      constexpr int QG = TX / 4 + 1;
+      const int64_t pitch = P.v.pitch;
 #pragma unroll
-    for (int k = 0; k < (DP * (TY + 1) + NT - 1) / NT; k++) {
-      const int i = threadIdx.x + k * NT;
-      if (DP * (TY + 1) % NT && i >= DP * (TY + 1)) break;
-      const int b = b0 - 1 + i / DP, a = a0 - 2 + 2 * (i % DP);
-      T ro0, ro1, va0, va1, vb0, vb1;
-      ld2(RO.at(a, b), ro0, ro1);
-      ld2(VA.at(a, b), va0, va1);
-      ld2(VA.at(a, b + 1), vb0, vb1);
-      const T va2 = VA(a + 2, b), vb2 = VA(a + 2, b + 1);
-      const bool okb = b >= 0 && b <= W - 1;
-      const bool ok0 = okb && a >= a0 - 1 && a >= 0 && a <= W - 1, ok1 = okb && a + 1 >= 0 && a + 1 <= W - 1;
-      const T v0 = ok0 ? jac4(cd, ro0, va0, va1, vb1, vb0) : (T)0;
-      const T v1 = ok1 ? jac4(cd, ro1, va1, va2, vb2, vb1) : (T)0;
-      st2(OS.at(a, b), v0, v1);
-      if (okb && b >= b0 && b < yhi && a >= a0) {
-        if (ok1)
-          st2(&P.v.o[(int64_t)b * pitch + a], v0, v1);
-        else if (ok0)
-          P.v.o[(int64_t)b * pitch + a] = v0;
+      for (int k = 0; k < (QG * (TY + 1) + NT - 1) / NT; k++) {
+        const int i = threadIdx.x + k * NT;
+        if (QG * (TY + 1) % NT && i >= QG * (TY + 1)) break;
+        const int b = b0 - 1 + i / QG, a = a0 - 4 + 4 * (i % QG);
+        const float4 ro = *reinterpret_cast<const float4 *>(RO.at(a, b));
+        const float4 va = *reinterpret_cast<const float4 *>(VA.at(a, b));
+        const float4 vb = *reinterpret_cast<const float4 *>(VA.at(a, b + 1));
+        const T va4 = VA(a + 4, b), vb4 = VA(a + 4, b + 1);
+        const bool okb = b >= 0 && b <= W - 1;
+        auto ok = [&](int x) { return okb && x >= a0 - 1 && x >= 0 && x <= W - 1; };
+        float4 o;
+        o.x = ok(a) ? jac4(cd, ro.x, va.x, va.y, vb.y, vb.x) : (T)0;
+        o.y = ok(a + 1) ? jac4(cd, ro.y, va.y, va.z, vb.z, vb.y) : (T)0;
+        o.z = ok(a + 2) ? jac4(cd, ro.z, va.z, va.w, vb.w, vb.z) : (T)0;
+        o.w = ok(a + 3) ? jac4(cd, ro.w, va.w, va4, vb4, vb.w) : (T)0;
+        *reinterpret_cast<float4 *>(OS.at(a, b)) = o;
+        if (okb && b >= b0 && b < yhi && a >= a0) {
+          T *dst = &P.v.o[(int64_t)b * pitch + a];
+          if (a + 3 <= W - 1)
+            *reinterpret_cast<float4 *>(dst) = o;
+          else {
+            if (a <= W - 1) dst[0] = o.x;
+            if (a + 1 <= W - 1) dst[1] = o.y;
+            if (a + 2 <= W - 1) dst[2] = o.z;
+          }
+        }
       }
-    }
-    __syncthreads();
-    // D(s-1) colour 2 (Eajacb) on E nodes, from the new O values
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, a = a0 + 2 * lane;
+      __syncthreads();
+      // D(s-1) colour 2 on E nodes from the new O values: half-warps take rows, lanes four columns
+      const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, a = a0 + 4 * (lane & 15);
 #pragma unroll
-    for (int b = b0 + w; b < b0 + TY; b += NW) {
-      if (b < 1 || b > W - 1 || b >= yhi) continue;
-      T re0, re1, s0, s1, n0, n1;
-      ld2(RE.at(a, b), re0, re1);
-      ld2(OS.at(a, b - 1), s0, s1);
-      ld2(OS.at(a, b), n0, n1);
-      const T sm = OS(a - 1, b - 1), nm = OS(a - 1, b);
-      const T e0 = jac4(cd, re0, sm, s0, n0, nm);
-      const T e1 = jac4(cd, re1, s0, s1, n1, n0);
-      const bool ok0 = a >= 1 && a <= W - 1, ok1 = a + 1 <= W - 1;
-      const int64_t o = (int64_t)b * pitch + a;
-      if (ok0 && ok1)
-        st2(&P.v.e[o], e0, e1);
-      else {
-        if (ok0) P.v.e[o] = e0;
-        if (ok1) P.v.e[o + 1] = e1;
+      for (int b = b0 + 2 * w + (lane >> 4); b < b0 + TY; b += 2 * NW) {
+        if (b < 1 || b > W - 1 || b >= yhi) continue;
+        const float4 re = *reinterpret_cast<const float4 *>(RE.at(a, b));
+        const float4 sv = *reinterpret_cast<const float4 *>(OS.at(a, b - 1));
+        const float4 nv = *reinterpret_cast<const float4 *>(OS.at(a, b));
+        const T sm = OS(a - 1, b - 1), nm = OS(a - 1, b);
+        float4 e;
+        e.x = jac4(cd, re.x, sm, sv.x, nv.x, nm);
+        e.y = jac4(cd, re.y, sv.x, sv.y, nv.y, nv.x);
+        e.z = jac4(cd, re.z, sv.y, sv.z, nv.z, nv.y);
+        e.w = jac4(cd, re.w, sv.z, sv.w, nv.w, nv.z);
+        T *dst = &P.v.e[(int64_t)b * pitch + a];
+        if (a >= 1 && a + 3 <= W - 1)
+          *reinterpret_cast<float4 *>(dst) = e;
+        else {
+          if (a >= 1 && a <= W - 1) dst[0] = e.x;
+          if (a + 1 >= 1 && a + 1 <= W - 1) dst[1] = e.y;
+          if (a + 2 >= 1 && a + 2 <= W - 1) dst[2] = e.z;
+          if (a + 3 >= 1 && a + 3 <= W - 1) dst[3] = e.w;
+        }
+      }
+    } else {
+      // D(s-1) colour 1 (Eajacr) on O nodes, pairs (a, a+1) = (a0-2+2p, a0-1+2p), rows b0-1 .. b0+TY-1
+      const int64_t pitch = P.v.pitch;
+#pragma unroll
+      for (int k = 0; k < (DP * (TY + 1) + NT - 1) / NT; k++) {
+        const int i = threadIdx.x + k * NT;
+        if (DP * (TY + 1) % NT && i >= DP * (TY + 1)) break;
+        const int b = b0 - 1 + i / DP, a = a0 - 2 + 2 * (i % DP);
+        T ro0, ro1, va0, va1, vb0, vb1;
+        ld2(RO.at(a, b), ro0, ro1);
+        ld2(VA.at(a, b), va0, va1);
+        ld2(VA.at(a, b + 1), vb0, vb1);
+        const T va2 = VA(a + 2, b), vb2 = VA(a + 2, b + 1);
+        const bool okb = b >= 0 && b <= W - 1;
+        const bool ok0 = okb && a >= a0 - 1 && a >= 0 && a <= W - 1, ok1 = okb && a + 1 >= 0 && a + 1 <= W - 1;
+        const T v0 = ok0 ? jac4(cd, ro0, va0, va1, vb1, vb0) : (T)0;
+        const T v1 = ok1 ? jac4(cd, ro1, va1, va2, vb2, vb1) : (T)0;
+        st2(OS.at(a, b), v0, v1);
+        if (okb && b >= b0 && b < yhi && a >= a0) {
+          if (ok1)
+            st2(&P.v.o[(int64_t)b * pitch + a], v0, v1);
+          else if (ok0)
+            P.v.o[(int64_t)b * pitch + a] = v0;
+        }
+      }
+      __syncthreads();
+      // D(s-1) colour 2 (Eajacb) on E nodes, from the new O values
+      const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, a = a0 + 2 * lane;
+#pragma unroll
+      for (int b = b0 + w; b < b0 + TY; b += NW) {
+        if (b < 1 || b > W - 1 || b >= yhi) continue;
+        T re0, re1, s0, s1, n0, n1;
+        ld2(RE.at(a, b), re0, re1);
+        ld2(OS.at(a, b - 1), s0, s1);
+        ld2(OS.at(a, b), n0, n1);
+        const T sm = OS(a - 1, b - 1), nm = OS(a - 1, b);
+        const T e0 = jac4(cd, re0, sm, s0, n0, nm);
+        const T e1 = jac4(cd, re1, s0, s1, n1, n0);
+        const bool ok0 = a >= 1 && a <= W - 1, ok1 = a + 1 <= W - 1;
+        const int64_t o = (int64_t)b * pitch + a;
+        if (ok0 && ok1)
+          st2(&P.v.e[o], e0, e1);
+        else {
+          if (ok0) P.v.e[o] = e0;
+          if (ok1) P.v.e[o + 1] = e1;
+        }
       }
     }
   }
@@ -1103,6 +1169,11 @@ cudaError_t fast2_jac_ad(const S2<T> &vd, const D2<T> &ra, T ca, const S2<T> &rd
   P.yhi = yhi;
 #define AD_RUN(NTV, TYV) \
   return run_op<OpJac2AD<T, 2, NTV, TYV>>(reinterpret_cast<const typename OpJac2AD<T, 2, NTV, TYV>::Params &>(P), st)
+  if constexpr (sizeof(T) == 4) {   // fp32: four-column D(s-1) phases (MG_AD_NOQUAD=1: two-column)
+    static const bool quad = !env_flag("MG_AD_NOQUAD");
+    using OpQ = OpJac2AD<T, 2, 256, 16, true>;
+    if (quad && nt == 256 && tyv == 16) return run_op<OpQ>(reinterpret_cast<const typename OpQ::Params &>(P), st);
+  }
   if (tyv == 8) {
     if (nt == 512) AD_RUN(512, 8);
     AD_RUN(256, 8);
