@@ -337,16 +337,20 @@ struct OpRest2DA {
 // Tile [X0, X0+TX) x [Y0, Y0+TYA) of A(s+1): r_A(s+1) is formed (OpRest2DA's
 // formula) on the tile and its one-node ring in shared memory, written for the
 // tile, and restricted onto D(s+1) (OpRest2AD's formulas) from shared memory.
-template <class T, int STG, int NTH, int TYA>
+// QD (fp32): Erest2b takes four columns per item (16-byte vectors of E and O
+// from a four-aligned origin, r_A(s+1) scratch two columns further left).
+template <class T, int STG, int NTH, int TYA, bool QD = false>
 struct OpRest2DAD {
+  static_assert(!QD || sizeof(T) == 4, "four-column items are the fp32 form");
   static constexpr int NT = NTH, STAGES = STG, NW = NT / 32, TY = TYA;
+  static constexpr int XO = QD ? 2 : 0;   // extra scratch columns on the left (r_A(s+1))
   static constexpr int H1 = hx<T>(1), H2 = hx<T>(2);
   static constexpr int EW = w16<T>(TX + 1 + H1), EH = TY + 2;   // E of r_D(s): [X0-1, X0+TX] x [Y0-1, Y0+TY]
   static constexpr int OW = w16<T>(TX + 1 + H2), OH = TY + 3;   // O of r_D(s): [X0-2, X0+TX] x [Y0-2, Y0+TY]
   static constexpr int E_BYTES = EW * EH * sizeof(T), O_BYTES = OW * OH * sizeof(T);
   static constexpr int E_OFF = 0, O_OFF = al128(E_BYTES);
   static constexpr int STAGE = al128(O_OFF + O_BYTES);
-  static constexpr int RSW = TX + 4, RSH = TY + 2;              // r_A(s+1) on [X0-2, X0+TX+2) x [Y0-1, Y0+TY]
+  static constexpr int RSW = TX + 4 + 2 * XO, RSH = TY + 2;     // r_A(s+1) on [X0-2-XO, X0+TX+2+XO) x [Y0-1, Y0+TY]
   static constexpr int SMEM = STAGES * STAGE + al128(RSW * RSH * sizeof(T));
   struct Params {
     CUtensorMap te, to;
@@ -372,6 +376,31 @@ struct OpRest2DAD {
     const int X0 = (t % P.ntx) * TX, Y0 = P.ylo + (t / P.ntx) * TY, Mc = P.Mc, yhi = P.yhi;
     const T *Eb = (const T *)(st + E_OFF), *Ob = (const T *)(st + O_OFF);
     T *Rb = (T *)scr;
+    if constexpr (QD) {
+      // r_A(s+1) at X = X0-4 .. X0+TX+3 (four per item, X0-1 .. X0+TX needed), Y = Y0-1 .. Y0+TY
+      static_assert(H1 == 4 && H2 == 4, "E and O boxes start four columns left of the tile");
+      constexpr int RQ = TX / 4 + 2, RR = TY + 2;
+#pragma unroll
+      for (int k = 0; k < (RQ * RR + NT - 1) / NT; k++) {
+        const int i = threadIdx.x + k * NT;
+        if (RQ * RR % NT && i >= RQ * RR) break;
+        const int p = i % RQ, r = i / RQ, Y = Y0 - 1 + r, X = X0 - 4 + 4 * p;
+        // E(X, Y) at Eb[r * EW + X - X0 + H1]; O(X, Y) at Ob[(r + 1) * OW + X - X0 + H2]
+        const T *e = Eb + r * EW + 4 * p, *o = Ob + (r + 1) * OW + 4 * p;
+        const float4 ec = *reinterpret_cast<const float4 *>(e);
+        const float4 on = *reinterpret_cast<const float4 *>(o), os = *reinterpret_cast<const float4 *>(o - OW);
+        const T onm = o[-1], osm = o[-1 - OW];
+        const bool oky = Y >= 1 && Y <= Mc - 1;
+        auto ok = [&](int x) { return oky && x >= 1 && x <= Mc - 1; };
+        // Erest2b: E(X,Y), O(X-1,Y-1), O(X,Y-1), O(X,Y), O(X-1,Y)
+        float4 v;
+        v.x = ok(X) ? erest2b(ec.x, osm, os.x, on.x, onm) : (T)0;
+        v.y = ok(X + 1) ? erest2b(ec.y, os.x, os.y, on.y, on.x) : (T)0;
+        v.z = ok(X + 2) ? erest2b(ec.z, os.y, os.z, on.z, on.y) : (T)0;
+        v.w = ok(X + 3) ? erest2b(ec.w, os.z, os.w, on.w, on.z) : (T)0;
+        *reinterpret_cast<float4 *>(Rb + r * RSW + 4 * p) = v;   // scratch column 0 = X0-4
+      }
+    } else {
     // r_A(s+1) at (X, Y), X = X0-1 .. X0+TX, Y = Y0-1 .. Y0+TY: pairs (X0-1+2p, X0+2p)
     constexpr int RP = TX / 2 + 1, RR = TY + 2;
 #pragma unroll
@@ -390,10 +419,11 @@ struct OpRest2DAD {
         Rb[r * RSW + 2 * p + 1 + q] = v;
       }
     }
+    }
     __syncthreads();
     // the tile's r_A(s+1) (aligned pairs) and Erest2r onto D(s+1): rows (y, y+1), y = Y0 + 2b
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, xl = X0 + 2 * lane;
-    STile<T> R = stile<T>(scr, RSW, X0 - 2, Y0 - 1);
+    STile<T> R = stile<T>(scr, RSW, X0 - 2 - XO, Y0 - 1);
     const int64_t pitch = P.rd.pitch;
 #pragma unroll
     for (int b = w; b < TY / 2; b += NW) {
@@ -1133,6 +1163,11 @@ cudaError_t fast2_rest_dad(const S2<T> &d, const D2<T> &ra, const S2<T> &rd, int
   P.rev = rev;
   // measured: fp64 576 threads (two CTAs per SM), fp32 256 (four; with 576 the fp32 pass is issue-bound)
   static const int nt = getenv("MG_DA_NT") ? atoi(getenv("MG_DA_NT")) : (sizeof(T) == 4 ? 256 : 576);
+  if constexpr (sizeof(T) == 4) {   // fp32: four-column Erest2b items (MG_DA_NOQUAD=1: two-column)
+    static const bool quad = !env_flag("MG_DA_NOQUAD");
+    using OpQ = OpRest2DAD<T, 2, 256, 32, true>;
+    if (quad && nt == 256) return run_op<OpQ>(reinterpret_cast<const typename OpQ::Params &>(P), st);
+  }
   if (nt == 256)
     return run_op<OpRest2DAD<T, 2, 256, 32>>(reinterpret_cast<const typename OpRest2DAD<T, 2, 256, 32>::Params &>(P), st);
   return run_op<Op>(P, st);

@@ -60,6 +60,8 @@ CASES = [
     ({}, 3, 129, 4, "float32"),
     ({"MG_K3S_NOF32": "1"}, 3, 129, 2, "float32"),   # round 1's fp32 sublattice kernels (k3l.cu)
     ({"MG_AD_NOQUAD": "1"}, 2, 513, 2, "float32"),   # two-column fp32 jac_ad
+    ({"MG_DA_NOQUAD": "1"}, 2, 513, 2, "float32"),   # two-column fp32 rest_dad
+    ({"MG_DA_NOQUAD": "1", "MG_AD_NOQUAD": "1"}, 2, 1025, 4, "float32"),
     ({"MG_AD_NOQUAD": "1"}, 2, 257, 4, "float32"),
     ({"MG_K3_FUSE_MR": "1", "MG_K3_FUSE_RMG": "2"}, 3, 129, 2, "float64"),
     ({"MG_K3_FUSE_MR": "2"}, 3, 257, 2, "float64"),
