@@ -120,8 +120,9 @@ class _OneCore:
         os.sched_setaffinity(0, self.prev)
 
 
-def _oracle_rate(w, dtype, budget_s, max_cycles):
-    """Oracle cycles of the full workload within ~budget_s on one pinned core."""
+def _oracle_rate(w, dtype, budget_s, max_cycles, warmup=1, warm_budget_s=30.0):
+    """Oracle cycles of the full workload within ~budget_s on one pinned core, after
+    min(warmup, ~warm_budget_s worth) untimed warm-up cycles (at least one)."""
     import oracle
     oracle.build()
     f = W.workload_rhs(w.name, dtype)
@@ -131,13 +132,16 @@ def _oracle_rate(w, dtype, budget_s, max_cycles):
         t0 = time.perf_counter()
         oracle.vcycle(u, f, w.p, 1, order=w.order)       # one warm-up cycle (allocation, page faults)
         t_one = time.perf_counter() - t0
+        wu = max(1, min(warmup, int(warm_budget_s / max(t_one, 1e-3)) + 1))
+        if wu > 1:
+            oracle.vcycle(u, f, w.p, wu - 1, order=w.order)
         cyc = max(1, min(max_cycles, int(budget_s / max(t_one, 1e-3))))
         t0 = time.perf_counter()
         oracle.vcycle(u, f, w.p, cyc, order=w.order)
         dt = time.perf_counter() - t0
     sample = (f"{cyc} V-cycle(s) of the full {w.name} workload ({N} unknowns), single-threaded C oracle pinned "
               f"to host core {pin.core} ({dt:.1f} s; host: {os.cpu_count()} cores, {_cpu_model()})")
-    return N * cyc / dt / 1e9, cyc, dt, sample
+    return N * cyc / dt / 1e9, cyc, dt, sample, wu
 
 
 def run_reference(args, w, ws, rank):
@@ -145,15 +149,16 @@ def run_reference(args, w, ws, rank):
     if rank != 0:
         return
     dtype = np.float64 if args.dtype == "f64" else np.float32
-    value, steps, dt, sample = _oracle_rate(w, dtype, 150.0, args.steps)
+    value, steps, dt, sample, wu = _oracle_rate(w, dtype, 150.0, args.steps, args.warmup)
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
-        "steps": steps, "warmup": 1, "ms_per_step": dt / steps * 1e3, "higher_is_better": True,
+        "steps": steps, "warmup": wu, "ms_per_step": dt / steps * 1e3, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": args.dtype, "data": "synthetic",
         "config": {"workload": w.name, "dim": w.dim, "n": w.n, "order": w.order, "p": list(w.p),
                    "unknowns": (w.n - 2) ** w.dim},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle",
-                         "sample": sample + f" (requested {args.steps} steps; capped to ~150 s)"},
+                         "sample": sample + f" (requested {args.steps} steps and {args.warmup} warm-up steps; "
+                                             "capped to ~150 s timed and ~30 s of warm-up)"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -161,7 +166,7 @@ def run_reference(args, w, ws, rank):
 
 def cpu_baseline(w, dtype, seconds=20.0):
     """Oracle throughput on a bounded sample of the same workload (1 pinned host core)."""
-    value, _, _, sample = _oracle_rate(w, dtype, seconds, w.cycles)
+    value, _, _, sample, _ = _oracle_rate(w, dtype, seconds, w.cycles)
     return {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample}
 
 
