@@ -728,20 +728,34 @@ static void drop_graphs(mg_solver *s) {
   s->graphs.clear();
 }
 
-// Launch one V-cycle u_in -> u_out: replay the CUDA graph captured for these
-// pointers (captured on first use; a few are cached).
-static int run_cycle(mg_solver *s, const void *u_in, void *u_out, const void *f_eff, int mode) {
+// Launch `count` V-cycles of one mode, the first u_in -> u_out, each further
+// one reading the previous one's output (u alternates between the two arrays
+// when they differ): replay the CUDA graph captured for these pointers
+// (captured on first use; a few are cached).  Several cycles per graph: a
+// graph launch waits for the previous graph to drain completely, ~4-6 us
+// between the last pass of one cycle and the first of the next (CUPTI
+// timeline), which inside one graph the passes do not pay.
+static int run_cycles(mg_solver *s, const void *u_in, void *u_out, const void *f_eff, int mode, int count) {
   cudaGraphExec_t ex = nullptr;
   for (auto &g : s->graphs)
-    if (g.uin == u_in && g.uout == u_out && g.f == f_eff && g.mode == mode && g.l2 == s->sum_l2 &&
-        g.hist == hist_on(s))
+    if (g.uin == u_in && g.uout == u_out && g.f == f_eff && g.mode == mode && g.count == count &&
+        g.l2 == s->sum_l2 && g.hist == hist_on(s))
       ex = g.exec;
   if (!ex) {
-    if (s->graphs.size() >= 16) drop_graphs(s);
+    if (s->graphs.size() >= 48) drop_graphs(s);
     cudaGraph_t g = nullptr;
     CKS(s, cudaStreamBeginCapture(s->st, cudaStreamCaptureModeThreadLocal));
     take_launch_error();
-    s->impl->enqueue_cycle_mode(u_in, u_out, f_eff, s->st, nullptr, mode);
+    const void *a = u_in;
+    void *b = u_out;
+    for (int i = 0; i < count; i++) {
+      s->impl->enqueue_cycle_mode(a, b, f_eff, s->st, nullptr, mode);
+      if (a != b) {
+        void *t = const_cast<void *>(a);
+        a = b;
+        b = t;
+      }
+    }
     cudaError_t le = cudaGetLastError();
     if (le == cudaSuccess) le = take_launch_error();
     std::string tmsg;
@@ -759,10 +773,23 @@ static int run_cycle(mg_solver *s, const void *u_in, void *u_out, const void *f_
     e = cudaGraphInstantiate(&ex, g, 0);
     cudaGraphDestroy(g);
     CKS(s, e);
-    s->graphs.push_back({ex, u_in, u_out, f_eff, mode, s->sum_l2, hist_on(s)});
+    s->graphs.push_back({ex, u_in, u_out, f_eff, mode, count, s->sum_l2, hist_on(s)});
   }
   CKS(s, cudaGraphLaunch(ex, s->st));
   return MG_OK;
+}
+static int run_cycle(mg_solver *s, const void *u_in, void *u_out, const void *f_eff, int mode) {
+  return run_cycles(s, u_in, u_out, f_eff, mode, 1);
+}
+
+// V-cycles per CUDA graph in a run of cycles of one mode (MG_GRAPH_CYCLES, default 8; 1 = one graph per cycle)
+static int graph_cycles() {
+  static const int k = [] {
+    const char *e = getenv("MG_GRAPH_CYCLES");
+    const int v = e ? atoi(e) : 8;
+    return v < 1 ? 1 : (v > 64 ? 64 : v);
+  }();
+  return k;
 }
 
 static bool aligned16(const void *p) { return ((uintptr_t)p & 15) == 0; }
@@ -1072,14 +1099,24 @@ static int cycles_work(mg_solver *s, void *u, const void *fe, int ncycles, doubl
   // norm comes from the last cycle's when it is wanted).
   const bool xf = alt && s->impl->fuses_cycles();
   void *cur = u;
-  for (int c = 0; c < ncycles; c++) {
-    void *dst = alt ? (cur == u ? s->d_ualt : u) : u;
+  auto mode_of = [&](int c) {
     int mode = 0;
     if (xf && c > 0) mode |= ImplBase::kSkipDesc;
     if (xf && (c + 1 < ncycles || res_hist)) mode |= ImplBase::kFuseNext;
-    int rc = run_cycle(s, cur, dst, fe, mode);
+    return mode;
+  };
+  for (int c = 0; c < ncycles;) {
+    void *dst = alt ? (cur == u ? s->d_ualt : u) : u;
+    const int mode = mode_of(c);
+    // graph_cycles() cycles of this mode per graph while the run has that many left, then one per graph:
+    // only two graph sizes per mode, so a call never captures a graph a shorter earlier call did not
+    int run = 1;
+    while (c + run < ncycles && run < graph_cycles() && mode_of(c + run) == mode) run++;
+    const int cnt = run == graph_cycles() ? run : 1;
+    int rc = run_cycles(s, cur, dst, fe, mode, cnt);
     if (rc) return rc;
-    cur = dst;
+    if (cnt & 1) cur = dst;
+    c += cnt;
   }
   if (cur != u) CKS(s, cudaMemcpyAsync(u, cur, s->work_elems() * s->esz, cudaMemcpyDeviceToDevice, s->st));
   if (res_hist) {

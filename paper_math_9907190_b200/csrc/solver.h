@@ -277,7 +277,7 @@ struct mg_solver {
   struct GraphEntry {
     cudaGraphExec_t exec;
     const void *uin, *uout, *f;
-    int mode;
+    int mode, count;   // count cycles per graph, u alternating uin <-> uout when they differ
     bool l2, hist;
   };
   std::vector<GraphEntry> graphs;   // captured cycles keyed by pointers
