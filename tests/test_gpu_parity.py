@@ -245,3 +245,32 @@ def test_fp32_convergence_factor_within_2pct():
         rates[dtype] = (norms[-1] / norms[-4]) ** (1 / 3)
     assert rates[np.float32] == pytest.approx(rates[np.float64], rel=0.02)
     assert 0.05 <= rates[np.float64] <= 0.09
+
+
+@pytest.mark.parametrize("dim,n", [(2, 129), (3, 33)])
+def test_multi_cycle_graphs(dim, n):
+    """Runs of cycles are replayed as CUDA graphs of MG_GRAPH_CYCLES (8) cycles,
+    the remainder one cycle per graph: cycle counts around the graph size, with
+    and without the residual history, and alternating call lengths on one
+    solver (cached graphs of every size reused) equal the oracle bit for bit."""
+    import torch
+    p = P2 if dim == 2 else P3
+    f = W.random_field(dim, n, seed=41)
+    u0 = W.random_field(dim, n, seed=42) * 0.1
+    for cycles in (8, 9, 10, 17, 18):
+        uo, ho = _oracle_run(dim, n, 2, p, f, u0, cycles, np.float64)
+        for hist in (False, True):
+            ug, hg = _gpu_run(dim, n, 2, p, f, u0, cycles, np.float64, hist=hist)
+            assert np.array_equal(ug, uo), (cycles, hist, _rel(ug, uo))
+            if hist:
+                assert np.array_equal(hg, ho), cycles
+    s = _solver(dim, n, 2, p, np.float64)
+    u = s.alloc(u0)
+    ft = s.alloc(f)
+    total = 0
+    for c in (10, 3, 17, 1, 9):
+        s.vcycle(u, ft, c)
+        total += c
+    torch.cuda.synchronize()
+    uo, _ = _oracle_run(dim, n, 2, p, f, u0, total, np.float64)
+    assert np.array_equal(s.view(u).cpu().numpy(), uo)
