@@ -6,6 +6,8 @@
 // shared-memory slots (one mbarrier each); step j of an item consumes load
 // L_j (and the older slots the Op declares), then one __syncthreads.
 #pragma once
+#include <cooperative_groups.h>
+
 #include <type_traits>
 
 #include "kernels.h"
@@ -59,6 +61,20 @@ struct OpKeep<Op, std::void_t<decltype(Op::KEEP)>> {
   static constexpr int v = Op::KEEP;
 };
 
+// Element size of a pipeline Op (Op::T, else its Geo's TMA alignment; the fp64-only fused Ops: 8).
+template <class Op, class = void>
+struct OpEsz {
+  static constexpr int v = 8;
+};
+template <class Op>
+struct OpEsz<Op, std::void_t<typename Op::T>> {
+  static constexpr int v = (int)sizeof(typename Op::T);
+};
+template <class Op>
+struct OpEsz<Op, std::void_t<typename Op::Gm>> {
+  static constexpr int v = 16 / Op::Gm::AL;
+};
+
 template <class T>
 struct V2t;
 template <>
@@ -109,6 +125,7 @@ struct Sched {
   int T, ntx, zlo, zhi, S;
   int tx, ty, xoff, yoff;   // tile extents and origin offsets: x0 = tx * (t % ntx) + xoff
   int rev;                  // 1: every CTA walks its items in reverse order (serpentine across passes)
+  int wsync;                // 1: grid-wide barrier after every whole wave of G units (cooperative launch)
   __device__ __forceinline__ int count(int G) const { return (T * S) / G + ((T * S) % G ? 1 : 0); }
   __device__ __forceinline__ Item get(int k, int b, int G) const {
     const int U = T * S, W = U / G, R = U % G;
@@ -197,7 +214,11 @@ __global__ void __launch_bounds__(OpNT<Op>::nt, OpNT<Op>::minb) zpipe(const __gr
   Op::init(S);
   int cs = 0, cprev = NS - 1, cpp = NS - 2;
   uint32_t phase = 0;
+  const int W = (P.sc.T * P.sc.S) / G;   // whole waves
   for (int k = 0; k < nit; k++) {
+    // neighbouring tiles of one wave stream side by side and re-read each other's halo rows from L2;
+    // without a barrier the CTAs drift apart over several waves and the halos come back from HBM
+    if (P.sc.wsync && k >= 1 && k <= W) cooperative_groups::this_grid().sync();
     const Item it = P.sc.get(k, b, G);
     if (it.ze <= it.zs) continue;
     typename Op::Ctx C;
@@ -262,12 +283,43 @@ static cudaError_t launch_zpipe(typename Op::Params &P, int tx, int ty, int xoff
   zp_next_rev() = 0;
   const int slots = sms * OpNT<Op>::minb;   // resident CTAs
   P.sc.S = P.sc.T >= slots ? 1 : (slots + P.sc.T - 1) / P.sc.T;
+  // at most MG_K3_ZPIECE planes per work unit (default 384 in fp64, whole tiles in fp32, where it measured
+  // 0.5-0.8 % slower at 513^3 and 1025^3; 0: whole tiles).  Shorter units with a
+  // barrier between waves keep neighbouring tiles within a few planes of each other (halo rows hit in L2):
+  // measured on B200: 1025^3 fp64 cycle 18.79 -> 15.94 ms (asc_fine HBM reads 30.8 -> 22.6 GB), 513^3
+  // 2.153 -> 2.142 ms (256: 15.95 / 2.145 ms; 128 and 192 slower)
+  static const int zpiece_env = getenv("MG_K3_ZPIECE") ? atoi(getenv("MG_K3_ZPIECE")) : -1;
+  const int zpiece = zpiece_env >= 0 ? zpiece_env : (OpEsz<Op>::v == 8 ? 384 : 0);
+  if (zpiece > 0 && (zhi - zlo + zpiece - 1) / zpiece > P.sc.S) P.sc.S = (zhi - zlo + zpiece - 1) / zpiece;
   if (P.sc.S > zhi - zlo) P.sc.S = zhi - zlo;
   const long long work = (long long)P.sc.T * (zhi - zlo);
   const int grid = work < slots ? (int)work : slots;
   // small levels (at most one work unit per CTA): programmatic launch (MG_PDL_SMALL3=1)
   static const bool pdl_small = env_flag("MG_PDL_SMALL3");
   const bool pdl = pdl_enabled() || (pdl_small && (long long)P.sc.T * P.sc.S <= grid);
+  // two or more whole waves: barrier between them (MG_K3_WSYNC=0 turns it off), cooperative launch so
+  // that every CTA is resident (checked: a grid the occupancy cannot hold runs without the barriers)
+  static const bool wsync_on = !getenv("MG_K3_WSYNC") || env_flag("MG_K3_WSYNC");
+  P.sc.wsync = 0;
+  if (wsync_on && !pdl && grid == slots && (long long)P.sc.T * P.sc.S / grid >= 2) {
+    int per_sm = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, zpipe<Op>, OpNT<Op>::nt, Op::SMEM) == cudaSuccess &&
+        per_sm >= OpNT<Op>::minb)
+      P.sc.wsync = 1;
+  }
+  if (P.sc.wsync) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(OpNT<Op>::nt);
+    cfg.dynamicSmemBytes = Op::SMEM;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeCooperative;
+    at[0].val.cooperative = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    return note_launch(cudaLaunchKernelEx(&cfg, zpipe<Op>, P));
+  }
   return note_launch(launch_pdl_if(pdl, zpipe<Op>, dim3(grid), dim3(OpNT<Op>::nt), Op::SMEM, st, P));
 }
 

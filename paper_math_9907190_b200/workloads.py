@@ -46,6 +46,10 @@ WORKLOADS = {
     "3d_65": Workload("3d_65", 3, 65, 2, P3, 10, 4, "manufactured",
                       "f = L7 u* + 1e-3 U[-1,1], u* = sin(pi x) sin(pi y) sin(pi z)"),
     "3d_513": Workload("3d_513", 3, 513, 2, P3, 10, 5, "uniform", "f ~ U[-1,1] interior"),
+    # beyond BASELINE.json: the next size up of configs[2] / configs[4] (same recipes), to show how the
+    # cycle's small-level latency share falls with the problem size
+    "2d_16385": Workload("2d_16385", 2, 16385, 2, P2, 10, 6, "bumps", "16 seeded Gaussian bumps"),
+    "3d_1025": Workload("3d_1025", 3, 1025, 2, P3, 10, 7, "uniform", "f ~ U[-1,1] interior"),
 }
 
 
