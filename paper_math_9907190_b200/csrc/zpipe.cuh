@@ -75,6 +75,16 @@ struct OpEsz<Op, std::void_t<typename Op::Gm>> {
   static constexpr int v = 16 / Op::Gm::AL;
 };
 
+// Sublattice (half-index) passes of k3s.cu declare Op::T; the fine-resolution passes of k3p.cu do not.
+template <class Op, class = void>
+struct OpHalf {
+  static constexpr bool v = false;
+};
+template <class Op>
+struct OpHalf<Op, std::void_t<typename Op::T>> {
+  static constexpr bool v = true;
+};
+
 template <class T>
 struct V2t;
 template <>
@@ -289,7 +299,9 @@ static cudaError_t launch_zpipe(typename Op::Params &P, int tx, int ty, int xoff
   // measured on B200: 1025^3 fp64 cycle 18.79 -> 15.94 ms (asc_fine HBM reads 30.8 -> 22.6 GB), 513^3
   // 2.153 -> 2.142 ms (256: 15.95 / 2.145 ms; 128 and 192 slower)
   static const int zpiece_env = getenv("MG_K3_ZPIECE") ? atoi(getenv("MG_K3_ZPIECE")) : -1;
-  const int zpiece = zpiece_env >= 0 ? zpiece_env : (OpEsz<Op>::v == 8 ? 384 : 0);
+  static const int zpiece_h = getenv("MG_K3_ZPIECE_H") ? atoi(getenv("MG_K3_ZPIECE_H")) : -1;
+  int zpiece = zpiece_env >= 0 ? zpiece_env : (OpEsz<Op>::v == 8 ? 384 : 0);
+  if (OpHalf<Op>::v && zpiece_h >= 0) zpiece = zpiece_h;
   if (zpiece > 0 && (zhi - zlo + zpiece - 1) / zpiece > P.sc.S) P.sc.S = (zhi - zlo + zpiece - 1) / zpiece;
   if (P.sc.S > zhi - zlo) P.sc.S = zhi - zlo;
   const long long work = (long long)P.sc.T * (zhi - zlo);
