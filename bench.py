@@ -343,7 +343,7 @@ def main():
         # CUDA-event timed region.  Headline: mg_solve_host_batch over E2E_PROBLEMS
         # steps (each step's upload / download overlapping another step's cycles:
         # three streams, two device slots); single: one mg_solve_host call.
-        E2E_PROBLEMS = 8
+        E2E_PROBLEMS = 32   # the pipeline's fill and drain (one upload, one compute + download) amortised over 32
         uh = torch.zeros(s.shape, dtype=tdt).pin_memory()
         fh = torch.zeros(s.shape, dtype=tdt).pin_memory()
         s.view(fh).copy_(torch.from_numpy(np.ascontiguousarray(f_host)))
@@ -368,6 +368,29 @@ def main():
                        f"{E2E_PROBLEMS} steps per mg_solve_host_batch call, uploads and downloads overlapping "
                        "other steps' cycles",
                "ms_per_step": t_e2e}
+        # the link's bound: the step's upload and download moved at once on two streams, no compute
+        # (pinned, same sizes; best of 3) -- e2e cannot beat max(this, the cycles' device time)
+        d_a, d_b = torch.empty_like(uh, device="cuda"), torch.empty_like(uh, device="cuda")
+        s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+        tl = []
+        for _ in range(3):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            s1.wait_stream(stream)
+            s2.wait_stream(stream)
+            with torch.cuda.stream(s1):
+                d_a.copy_(fh, non_blocking=True)
+            with torch.cuda.stream(s2):
+                uh.copy_(d_b, non_blocking=True)
+            stream.wait_stream(s1)
+            stream.wait_stream(s2)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            tl.append(e0.elapsed_time(e1))
+        del d_a, d_b
+        t_link = max(min(tl), m["ms_per_step"] * w.cycles)
+        e2e["bound"] = {"ms_per_step": t_link, "what": "max(H2D f + D2H u at once on two streams, measured; the "
+                        "step's V-cycles at the device-timed rate)", "frac": t_link / t_e2e}
         s.solve_host(uh, fh, w.cycles)
         t1 = []
         for _ in range(2):
