@@ -689,9 +689,13 @@ struct OpJac2A {
 // shared-memory instructions of the two largest phases; v_A(s) and O sit two
 // columns further left so every vector is aligned.  Same node formulas and
 // operand order.
-template <class T, int STG, int NTH, int TYA, bool QD = false>
+// SPL (two-column form): v_A(s) in shared memory as two column-parity planes (even / odd local columns), so
+// the stride-2 accesses of the A(s) colours and the O colour's scalar reads become stride-1 (no 2-way bank
+// conflicts); same values, same operand order.
+template <class T, int STG, int NTH, int TYA, bool QD = false, bool SPL = false>
 struct OpJac2AD {
   static_assert(!QD || sizeof(T) == 4, "four-column items are the fp32 form");
+  static_assert(!(QD && SPL), "the split v_A(s) layout is the two-column form");
   static constexpr int NT = NTH, STAGES = STG, NW = NT / 32, TY = TYA;
   static constexpr int XO = QD ? 2 : 0;   // extra scratch columns on the left (v_A(s), O)
   static constexpr int H2 = hx<T>(2), H1 = hx<T>(1);
@@ -749,7 +753,55 @@ struct OpJac2AD {
     // b0-2 .. b0+TY+1 taken two at a time (even, odd) so every E/O choice is static
     const T *Eb = (const T *)(st + VE_OFF), *Ob = (const T *)(st + VO_OFF), *Rb = (const T *)(st + RA_OFF);
     T *Vb = (T *)scr + XO;   // raw v_A(s) offsets below are relative to column a0-2
-    constexpr int GP = TX / 2 + 2, GR = TY / 2 + 2;
+    constexpr int GP = TX / 2 + 2, GR = TY / 2 + 2, DP = TX / 2 + 1, DR = TY / 2 + 1;
+    constexpr int VH2 = VAW / 2;              // SPL: columns per parity plane
+    T *VAe = (T *)scr, *VAo = VAe + VH2 * VAH;   // SPL: local columns 2j and 2j+1 (column a0-2 is local 0)
+    if constexpr (SPL) {
+#pragma unroll
+      for (int k = 0; k < (GP * GR + NT - 1) / NT; k++) {
+        const int i = threadIdx.x + k * NT;
+        if (GP * GR % NT && i >= GP * GR) break;
+        const int p = i % GP, m = i / GP;
+        {   // even row, green at the odd local column 2p+1
+          const int y = b0 - 2 + 2 * m, x = a0 - 1 + 2 * p;
+          const T *e = Eb + (m + 1) * VDW + p + H2, *o = Ob + m * VDW + p + H2 - 1;
+          T g = (T)0;
+          if (in(x, y)) g = jac4(ca, Rb[2 * m * RAW + 2 * p + 1 - 2 + H2], e[-1], o[0], e[0], o[VDW]);
+          VAo[2 * m * VH2 + p] = g;
+        }
+        {   // odd row, green at the even local column 2p
+          const int y = b0 - 1 + 2 * m, x = a0 - 2 + 2 * p;
+          const T *e = Eb + (m + 1) * VDW + p - 1 + H2, *o = Ob + (m + 1) * VDW + p - 1 + H2;
+          T g = (T)0;
+          if (in(x, y)) g = jac4(ca, Rb[(2 * m + 1) * RAW + 2 * p - 2 + H2], o[-1], e[0], o[0], e[VDW]);
+          VAe[(2 * m + 1) * VH2 + p] = g;
+        }
+      }
+      __syncthreads();
+#pragma unroll
+      for (int k = 0; k < (DP * DR + NT - 1) / NT; k++) {
+        const int i = threadIdx.x + k * NT;
+        if (DP * DR % NT && i >= DP * DR) break;
+        const int p = i % DP, m = i / DP;
+        {   // odd row R = 2m+1, D node at the odd local column 2p+1: x-1, y-1, x+1, y+1
+          const int y = b0 - 1 + 2 * m, x = a0 - 1 + 2 * p, R = 2 * m + 1;
+          T v = (T)0;
+          if (in(x, y))
+            v = jac4(ca, Rb[(2 * m + 1) * RAW + 2 * p + 1 - 2 + H2], VAe[R * VH2 + p], VAo[(R - 1) * VH2 + p],
+                     VAe[R * VH2 + p + 1], VAo[(R + 1) * VH2 + p]);
+          VAo[R * VH2 + p] = v;
+        }
+        {   // even row R = 2m+2, D node at the even local column 2p+2
+          const int y = b0 + 2 * m, x = a0 + 2 * p, R = 2 * m + 2;
+          T v = (T)0;
+          if (in(x, y))
+            v = jac4(ca, Rb[(2 * m + 2) * RAW + 2 * p - 2 + H2 + 2], VAo[R * VH2 + p], VAe[(R - 1) * VH2 + p + 1],
+                     VAo[R * VH2 + p + 1], VAe[(R + 1) * VH2 + p + 1]);
+          VAe[R * VH2 + p + 1] = v;
+        }
+      }
+      __syncthreads();
+    } else {
 #pragma unroll
     for (int k = 0; k < (GP * GR + NT - 1) / NT; k++) {
       const int i = threadIdx.x + k * NT;
@@ -772,7 +824,6 @@ struct OpJac2AD {
     }
     __syncthreads();
     // A(s) colour 2: the D(s) node (x + y even) of each pair (a0-1+2p, a0+2p), rows b0-1 .. b0+TY
-    constexpr int DP = TX / 2 + 1, DR = TY / 2 + 1;
 #pragma unroll
     for (int k = 0; k < (DP * DR + NT - 1) / NT; k++) {
       const int i = threadIdx.x + k * NT;
@@ -794,6 +845,7 @@ struct OpJac2AD {
       }
     }
     __syncthreads();
+    }
     if constexpr (QD) {
       // D(s-1) colour 1 on O nodes, four columns a = a0-4+4g .. a+3 per item (g = 0 .. TX/4), rows b0-1 .. b0+TY-1
       constexpr int QG = TX / 4 + 1;
@@ -859,11 +911,22 @@ struct OpJac2AD {
         const int i = threadIdx.x + k * NT;
         if (DP * (TY + 1) % NT && i >= DP * (TY + 1)) break;
         const int b = b0 - 1 + i / DP, a = a0 - 2 + 2 * (i % DP);
-        T ro0, ro1, va0, va1, vb0, vb1;
+        T ro0, ro1, va0, va1, vb0, vb1, va2, vb2;
         ld2(RO.at(a, b), ro0, ro1);
-        ld2(VA.at(a, b), va0, va1);
-        ld2(VA.at(a, b + 1), vb0, vb1);
-        const T va2 = VA(a + 2, b), vb2 = VA(a + 2, b + 1);
+        if constexpr (SPL) {   // local row b - (b0 - 2), even local column 2 (i % DP)
+          const int o0 = (b - b0 + 2) * VH2 + i % DP;
+          va0 = VAe[o0];
+          va1 = VAo[o0];
+          vb0 = VAe[o0 + VH2];
+          vb1 = VAo[o0 + VH2];
+          va2 = VAe[o0 + 1];
+          vb2 = VAe[o0 + VH2 + 1];
+        } else {
+          ld2(VA.at(a, b), va0, va1);
+          ld2(VA.at(a, b + 1), vb0, vb1);
+          va2 = VA(a + 2, b);
+          vb2 = VA(a + 2, b + 1);
+        }
         const bool okb = b >= 0 && b <= W - 1;
         const bool ok0 = okb && a >= a0 - 1 && a >= 0 && a <= W - 1, ok1 = okb && a + 1 >= 0 && a + 1 <= W - 1;
         const T v0 = ok0 ? jac4(cd, ro0, va0, va1, vb1, vb0) : (T)0;
@@ -1216,6 +1279,9 @@ cudaError_t fast2_jac_ad(const S2<T> &vd, const D2<T> &ra, T ca, const S2<T> &rd
   if (tyv == 16) {
     if (nt == 256) AD_RUN(256, 16);
     if (nt == 512) AD_RUN(512, 16);
+    if (!env_flag("MG_AD_NOSPLIT"))   // v_A(s) in column-parity planes (MG_AD_NOSPLIT=1: interleaved)
+      return run_op<OpJac2AD<T, 2, 576, 16, false, true>>(
+          reinterpret_cast<const typename OpJac2AD<T, 2, 576, 16, false, true>::Params &>(P), st);
     AD_RUN(576, 16);   // 18 warps: the O colour (33 x 17 pairs) in one round
   }
   if (nt == 256) AD_RUN(256, 32);
