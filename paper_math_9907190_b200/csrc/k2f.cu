@@ -339,9 +339,13 @@ struct OpRest2DA {
 // tile, and restricted onto D(s+1) (OpRest2AD's formulas) from shared memory.
 // QD (fp32): Erest2b takes four columns per item (16-byte vectors of E and O
 // from a four-aligned origin, r_A(s+1) scratch two columns further left).
-template <class T, int STG, int NTH, int TYA, bool QD = false>
+// CF (two-column form): item p of a row forms r_A(s+1) at X0-1+p and X0+32+p (not at the adjacent pair
+// X0-1+2p, X0+2p), so consecutive threads read and write consecutive shared-memory words (no 2-way bank
+// conflicts), and Erest2r takes its x neighbours from the adjacent lanes by shuffle; same formulas and order.
+template <class T, int STG, int NTH, int TYA, bool QD = false, bool CF = false>
 struct OpRest2DAD {
   static_assert(!QD || sizeof(T) == 4, "four-column items are the fp32 form");
+  static_assert(!(QD && CF), "CF is the two-column form");
   static constexpr int NT = NTH, STAGES = STG, NW = NT / 32, TY = TYA;
   static constexpr int XO = QD ? 2 : 0;   // extra scratch columns on the left (r_A(s+1))
   static constexpr int H1 = hx<T>(1), H2 = hx<T>(2);
@@ -400,6 +404,24 @@ struct OpRest2DAD {
         v.w = ok(X + 3) ? erest2b(ec.w, os.z, os.w, on.w, on.z) : (T)0;
         *reinterpret_cast<float4 *>(Rb + r * RSW + 4 * p) = v;   // scratch column 0 = X0-4
       }
+    } else if constexpr (CF) {
+    // r_A(s+1) at (X, Y), X = X0-1 .. X0+TX, Y = Y0-1 .. Y0+TY: item p takes X0-1+p and X0-1+p+RP
+    constexpr int RP = TX / 2 + 1, RR = TY + 2;
+#pragma unroll
+    for (int k = 0; k < (RP * RR + NT - 1) / NT; k++) {
+      const int i = threadIdx.x + k * NT;
+      if (RP * RR % NT && i >= RP * RR) break;
+      const int p = i % RP, r = i / RP, Y = Y0 - 1 + r;
+      const bool oky = Y >= 1 && Y <= Mc - 1;
+#pragma unroll
+      for (int q = 0; q < 2; q++) {
+        const int X = X0 - 1 + p + RP * q;
+        // E(X, Y) at Eb[r * EW + X - X0 + H1]; O(X, Y) at Ob[(r + 1) * OW + X - X0 + H2]
+        const T *e = Eb + r * EW + X - X0 + H1, *o = Ob + (r + 1) * OW + X - X0 + H2;
+        const T v = (oky && X >= 1 && X <= Mc - 1) ? erest2b(e[0], o[-1 - OW], o[-OW], o[0], o[-1]) : (T)0;
+        Rb[r * RSW + X - X0 + 2] = v;
+      }
+    }
     } else {
     // r_A(s+1) at (X, Y), X = X0-1 .. X0+TX, Y = Y0-1 .. Y0+TY: pairs (X0-1+2p, X0+2p)
     constexpr int RP = TX / 2 + 1, RR = TY + 2;
@@ -431,6 +453,13 @@ struct OpRest2DAD {
       T rc, rE, rN, ro;
       ld2(R.at(xl, y), rc, rE);
       ld2(R.at(xl, y + 1), rN, ro);
+      T rW = (T)0, rEn = (T)0;   // CF: R(xl - 1, y) = lane - 1's rE, R(xl + 2, y + 1) = lane + 1's rN
+      if constexpr (CF) {
+        rW = __shfl_up_sync(0xffffffffu, rE, 1);
+        rEn = __shfl_down_sync(0xffffffffu, rN, 1);
+        if (lane == 0) rW = R(xl - 1, y);
+        if (lane == 31) rEn = R(xl + 2, y + 1);
+      }
       if (y <= Mc - 1 && y < yhi) {   // (yhi even: the pair's second row is inside too)
         const bool ok0 = xl >= 1 && xl <= Mc - 1, ok1 = xl + 1 <= Mc - 1;
         if (y >= 1) {
@@ -450,9 +479,14 @@ struct OpRest2DAD {
           }
         }
         const int64_t o = (int64_t)(y / 2) * pitch + xl / 2;
+        if constexpr (CF) {
+          if (xl >= 2 && xl <= Mc - 2 && y >= 2 && y <= Mc - 2) P.rd.e[o] = erest2r(rc, rW, R(xl, y - 1), rE, rN);
+          if (xl + 1 <= Mc - 1 && y + 1 <= Mc - 1) P.rd.o[o] = erest2r(ro, rN, rE, rEn, R(xl + 1, y + 2));
+        } else {
         if (xl >= 2 && xl <= Mc - 2 && y >= 2 && y <= Mc - 2)
           P.rd.e[o] = erest2r(rc, R(xl - 1, y), R(xl, y - 1), rE, rN);
         if (xl + 1 <= Mc - 1 && y + 1 <= Mc - 1) P.rd.o[o] = erest2r(ro, rN, rE, R(xl + 2, y + 1), R(xl + 1, y + 2));
+        }
       }
     }
   }
@@ -949,7 +983,18 @@ struct OpJac2AD {
         ld2(RE.at(a, b), re0, re1);
         ld2(OS.at(a, b - 1), s0, s1);
         ld2(OS.at(a, b), n0, n1);
-        const T sm = OS(a - 1, b - 1), nm = OS(a - 1, b);
+        T sm, nm;
+        if constexpr (SPL) {   // column a-1 is lane - 1's second column (warp-uniform loop: every lane is here)
+          sm = __shfl_up_sync(0xffffffffu, s1, 1);
+          nm = __shfl_up_sync(0xffffffffu, n1, 1);
+          if (lane == 0) {
+            sm = OS(a - 1, b - 1);
+            nm = OS(a - 1, b);
+          }
+        } else {
+          sm = OS(a - 1, b - 1);
+          nm = OS(a - 1, b);
+        }
         const T e0 = jac4(cd, re0, sm, s0, n0, nm);
         const T e1 = jac4(cd, re1, s0, s1, n1, n0);
         const bool ok0 = a >= 1 && a <= W - 1, ok1 = a + 1 <= W - 1;
@@ -1233,6 +1278,10 @@ cudaError_t fast2_rest_dad(const S2<T> &d, const D2<T> &ra, const S2<T> &rd, int
   }
   if (nt == 256)
     return run_op<OpRest2DAD<T, 2, 256, 32>>(reinterpret_cast<const typename OpRest2DAD<T, 2, 256, 32>::Params &>(P), st);
+  if (!env_flag("MG_DA_NOCF")) {   // conflict-free shared-memory columns (MG_DA_NOCF=1: adjacent pairs)
+    using OpC = OpRest2DAD<T, 2, 576, 32, false, true>;
+    return run_op<OpC>(reinterpret_cast<const typename OpC::Params &>(P), st);
+  }
   return run_op<Op>(P, st);
 }
 
