@@ -377,6 +377,24 @@ static int k3_fuse_min(bool mr) {
   if (e && *e) return atoi(e) < 0 ? 1000 : (mr ? std::max(1, atoi(e)) : atoi(e));
   return env_flag("MG_K3_FUSE") ? (mr ? 1 : 0) : 1000;
 }
+// Octaves with M(o) <= this run their level steps on the one-thread-per-node k3l.cu kernels instead of
+// the plane pipelines (MG_K3_GEN1_M; 0 = never): small levels sit in L2, where a pipeline's prologue and
+// epilogue per z-split work item cost more than the massively parallel kernels' extra launches.
+static int k3_gen1_m() {
+  static const int m = [] {
+    const char *e = getenv("MG_K3_GEN1_M");
+    return e && *e ? atoi(e) : 128;
+  }();
+  return m;
+}
+// The same for the descent's restriction steps alone (MG_K3_GEN1_MD; default: MG_K3_GEN1_M).
+static int k3_gen1_md() {
+  static const int m = [] {
+    const char *e = getenv("MG_K3_GEN1_MD");
+    return e && *e ? atoi(e) : k3_gen1_m();
+  }();
+  return m;
+}
 
 template <class T>
 struct Impl3 : ImplBase {
@@ -577,6 +595,11 @@ struct Impl3 : ImplBase {
     // fused octave passes: bit-identical, but no measurable gain in graph replay on B200 (A/B in
     // DESIGN.md), so opt-in (MG_K3_FUSE=1, or per octave MG_K3_FUSE_RMG / MG_K3_FUSE_MR)
     static const int rmg_min = k3_fuse_min(false);
+    const int g1m = k3_gen1_m(), g1md = k3_gen1_md();
+    auto pipe = [&](int o) { return gen2 && M[o] > g1m; };     // G(s) level steps on plane pipelines
+    auto pipes = [&](int o) { return gen2s && M[o] > g1m; };   // sublattice steps on plane pipelines
+    auto piped = [&](int o) { return gen2 && M[o] > g1md; };   // restriction steps (descent)
+    auto pipeds = [&](int o) { return gen2s && M[o] > g1md; };
     // Serpentine item order (zpipe Sched::rev): descent pass d (desc_fine = 0,
     // then rest_rm, rest_mg, rest_gr, ...) runs reversed when d is odd; ascent
     // passes alternate backwards from asc_fine (reversed), so the next
@@ -591,21 +614,21 @@ struct Impl3 : ImplBase {
       if (o >= 1) {
         STEP("rest_gr", g, 1, w * (Nl[g] + Nl[g + 1]));
         dir(3 * o);
-        if (gen2) fast3p_rest_gr<T>(rG[o], rR[o], M[o], st);
+        if (piped(o)) fast3p_rest_gr<T>(rG[o], rR[o], M[o], st);
         else lv3_rest_gr<T>(rG[o], rR[o], M[o], st);
       }
-      if (gen2s && sizeof(T) == 8 && o >= rmg_min) {   // R(s) -> M(s) -> G(2s) in one pass (r_M written, not re-read)
+      if (pipeds(o) && sizeof(T) == 8 && o >= rmg_min) {   // R(s) -> M(s) -> G(2s) in one pass (r_M written, not re-read)
         STEP("rest_rmg", g + 1, 1, w * (Nl[g + 1] + Nl[g + 2] + Nl[g + 3]));
         sub3_rest_rmg(rR[o], rM[o], rG[o + 1], M[o], st);
         return;
       }
       STEP("rest_rm", g + 1, 1, w * (Nl[g + 1] + Nl[g + 2]));
       dir(3 * o + 1);
-      if (gen2s) sub3_rest_rm(rR[o], rM[o], M[o], st);
+      if (pipeds(o)) sub3_rest_rm(rR[o], rM[o], M[o], st);
       else lv3_rest_rm<T>(rR[o], rM[o], M[o], st);
       STEP("rest_mg", g + 2, 1, w * (Nl[g + 2] + Nl[g + 3]));
       dir(3 * o + 2);
-      if (gen2s) sub3_rest_mg(rM[o], rG[o + 1], M[o + 1], st);
+      if (pipeds(o)) sub3_rest_mg(rM[o], rG[o + 1], M[o + 1], st);
       else lv3_rest_mg<T>(rM[o], rG[o + 1], M[o + 1], st);
     };
     // G(2s) -> M(s) -> R(s): one fused pass (v_M(s) stays on chip) or the two level kernels.
@@ -614,24 +637,24 @@ struct Impl3 : ImplBase {
     static const int mr_min = k3_fuse_min(true);
     auto jac_mr = [&](int o) {
       int g = 3 * o;
-      if (gen2s && sizeof(T) == 8 && o >= mr_min) {
+      if (pipes(o) && sizeof(T) == 8 && o >= mr_min) {
         STEP("jac_mr", g + 1, 1, w * (Nl[g + 3] + Nl[g + 2] + 2 * Nl[g + 1]));
         sub3_jac_mr(vG[o + 1], rM[o], rR[o], vR[o], M[o], cMg[o], cR1[o], cR2[o], st);
         return;
       }
-      STEP("jac_m", g + 2, gen2s ? 1 : 2, w * (Nl[g + 3] + 2 * Nl[g + 2]));
+      STEP("jac_m", g + 2, pipes(o) ? 1 : 2, w * (Nl[g + 3] + 2 * Nl[g + 2]));
       dir(3 * o + 3);
-      if (gen2s) sub3_jac_m(vG[o + 1], rM[o], vM[o], M[o], cMg[o], st);
+      if (pipes(o)) sub3_jac_m(vG[o + 1], rM[o], vM[o], M[o], cMg[o], st);
       else lv3_jac_m<T>(vG[o + 1], rM[o], vM[o], M[o], cMg[o], st);
-      STEP("jac_r", g + 1, gen2s ? 1 : 2, w * (Nl[g + 2] + 2 * Nl[g + 1]));
+      STEP("jac_r", g + 1, pipes(o) ? 1 : 2, w * (Nl[g + 2] + 2 * Nl[g + 1]));
       dir(3 * o + 2);
-      if (gen2s) sub3_jac_r(vM[o], rR[o], vR[o], M[o], cR1[o], cR2[o], st);
+      if (pipes(o)) sub3_jac_r(vM[o], rR[o], vR[o], M[o], cR1[o], cR2[o], st);
       else lv3_jac_r<T>(vM[o], rR[o], vR[o], M[o], cR1[o], cR2[o], st);
     };
     auto ascent = [&](int o) {   // o >= 1
       int g = 3 * o;
       jac_mr(o);
-      if (gen2) {
+      if (pipe(o)) {
         STEP("jac_g", g, 1, w * (Nl[g + 1] + 2 * Nl[g]));
         dir(3 * o + 1);
         fast3p_jac_g<T>(vR[o], rG[o], vG[o], M[o], cG[o], st);
@@ -706,14 +729,17 @@ struct Impl3 : ImplBase {
       const bool gen2 = !env_flag("MG_K3_GEN1"), gen2s = gen2 && (sizeof(T) == 8 || !env_flag("MG_K3S_NOF32"));
       const bool f64 = gen2s && sizeof(T) == 8;
       const int mr_min = k3_fuse_min(true), rmg_min = k3_fuse_min(false);
-      auto per_mr_o = [&](int o) { return gen2s ? (f64 && o >= mr_min ? 1 : 2) : 4; };
+      const int g1m = k3_gen1_m(), g1md = k3_gen1_md();
+      auto p1 = [&](int o) { return gen2 && M[o] > g1m; };
+      auto ps = [&](int o) { return gen2s && M[o] > g1m; };
+      auto per_mr_o = [&](int o) { return ps(o) ? (f64 && o >= mr_min ? 1 : 2) : 4; };
       const int od = use_tail ? om : oc;
       c = 1;
-      for (int o = 0; o < od; o++) c += (o >= 1) + (f64 && o >= rmg_min ? 1 : 2);
+      for (int o = 0; o < od; o++) c += (o >= 1) + (gen2s && M[o] > g1md && f64 && o >= rmg_min ? 1 : 2);
       c += 1;   // tail or coarse
       if (!use_tail)
-        for (int o = oc - 1; o >= od; o--) c += per_mr_o(o) + (gen2 ? 1 : 2);
-      for (int o = od - 1; o >= 0; o--) c += per_mr_o(o) + (o >= 1 ? (gen2 ? 1 : 2) : 1);
+        for (int o = oc - 1; o >= od; o--) c += per_mr_o(o) + (p1(o) ? 1 : 2);
+      for (int o = od - 1; o >= 0; o--) c += per_mr_o(o) + (o >= 1 ? (p1(o) ? 1 : 2) : 1);
       return c;
     }
     for (int o = k - 2; o >= 0; o--) c += 2 + 2 + ((o >= 1) ? 2 : 3);

@@ -59,6 +59,13 @@ CASES = [
     ({}, 3, 129, 4, "float64"),
     ({}, 3, 129, 4, "float32"),
     ({"MG_K3S_NOF32": "1"}, 3, 129, 2, "float32"),   # round 1's fp32 sublattice kernels (k3l.cu)
+    # levels with M <= 128 on the k3l.cu kernels is the default; 0 keeps every octave on the plane pipelines
+    ({"MG_K3_GEN1_M": "0"}, 3, 129, 2, "float64"),
+    ({"MG_K3_GEN1_M": "0"}, 3, 129, 4, "float64"),
+    ({"MG_K3_GEN1_M": "0", "MG_POISON": "1"}, 3, 257, 2, "float32"),
+    ({"MG_K3_GEN1_MD": "256"}, 3, 257, 2, "float64"),   # octave 1's restrictions on k3l.cu as well
+    ({"MG_K3_GEN1_MD": "256"}, 3, 257, 2, "float32"),
+    ({"MG_K3_GEN1_M": "256", "MG_TAIL_M3": "0"}, 3, 257, 4, "float64"),
     ({"MG_AD_NOQUAD": "1"}, 2, 513, 2, "float32"),   # two-column fp32 jac_ad
     ({"MG_DA_NOQUAD": "1"}, 2, 513, 2, "float32"),   # two-column fp32 rest_dad
     ({"MG_DA_NOQUAD": "1", "MG_AD_NOQUAD": "1"}, 2, 1025, 4, "float32"),
@@ -122,6 +129,12 @@ CASES = [
     ({"MG_POISON": "1", "MG_K3_FUSE": "1"}, 3, 129, 2, "float64"),
     ({"MG_POISON": "1", "MG_2D_NOXFUSE": "1", "MG_2D_NOADFUSE": "1", "MG_2D_NODAFUSE": "1"}, 2, 257, 2, "float64"),
 ]
+
+
+# switches of the plane-pipeline small-level passes: tested with every octave on the pipelines
+_PIPE_KEYS = ("MG_K3_FUSE", "MG_K3_FUSE_MR", "MG_K3_FUSE_RMG", "MG_K3S_NW", "MG_K3R_NW", "MG_K3_NWL")
+CASES = [({**e, "MG_K3_GEN1_M": "0"} if d == 3 and any(k in e for k in _PIPE_KEYS) else e, d, n, o, t)
+         for e, d, n, o, t in CASES]
 
 
 @pytest.mark.parametrize("env,dim,n,order,dtype", CASES,
