@@ -64,6 +64,7 @@ CASES = [
     ({"MG_K3_GEN1_M": "0"}, 3, 129, 4, "float64"),
     ({"MG_K3_GEN1_M": "0", "MG_POISON": "1"}, 3, 257, 2, "float32"),
     ({"MG_K3_GEN1_MD": "256"}, 3, 257, 2, "float64"),   # octave 1's restrictions on k3l.cu as well
+    ({"MG_K3L_PDL": "1"}, 3, 257, 2, "float64"),   # k3l.cu level kernels launched programmatically
     ({"MG_K3_GEN1_MD": "256"}, 3, 257, 2, "float32"),
     ({"MG_K3_GEN1_M": "256", "MG_TAIL_M3": "0"}, 3, 257, 4, "float64"),
     ({"MG_AD_NOQUAD": "1"}, 2, 513, 2, "float32"),   # two-column fp32 jac_ad
