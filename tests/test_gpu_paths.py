@@ -53,6 +53,7 @@ CASES = [
     ({"MG_K3_FUSE": "1"}, 3, 257, 2, "float64"),
     ({"MG_TAIL_M3": "0"}, 3, 129, 2, "float64"),
     ({"MG_TAIL_M3": "128"}, 3, 129, 2, "float64"),
+    ({"MG_TAIL_M3": "64"}, 3, 257, 2, "float64"),   # round 2 session 3 default
     ({"MG_K3_GEN1": "1"}, 3, 65, 2, "float64"),
     ({"MG_K3_GEN1": "1"}, 3, 65, 4, "float64"),
     ({"MG_K3_GEN1": "1"}, 3, 129, 4, "float32"),
