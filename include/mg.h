@@ -27,8 +27,8 @@
  *    pointers) are read and updated in place.  Otherwise -- e.g. pitch = n,
  *    since n = 2^k + 1 never gives 16-byte rows -- each mg_vcycle /
  *    mg_profile / mg_convergence_factor call copies u and f into library-owned
- *    work arrays (row pitch n rounded up to 128 bytes; one cudaMemcpy2DAsync
- *    per array, 2 x 2 N element moves per call), runs the same kernels there
+ *    work arrays (row pitch n rounded up to 128 bytes; one launch of the
+ *    library's re-pitch copy kernel per array, 2 x 2 N element moves per call), runs the same kernels there
  *    and copies u back (2 N more).  mg_vcycle_host copies the host arrays
  *    straight into the work layout.  mg_residual and mg_norm read any pitch.
  *  - u, f, r, x are DEVICE pointers on the solver's device unless the name

@@ -49,6 +49,7 @@ def test_mg_create_pitch_n_runs_tma_kernels_2d(order):
             names = _kernels(lambda: got.setdefault("h", mg.mg_vcycle(h, ut.data_ptr(), ft.data_ptr(), cycles, hist)))
             assert any("tile_pipeline" in k for k in names), sorted(names)
             assert any("asc_desc_stream" in k for k in names), sorted(names)
+            assert any("k_repitch" in k for k in names), sorted(names)   # staged by the library's own copy kernel
             uo = u0.copy()
             ho = oracle.vcycle(uo, f, p, cycles, order=order, hist=True)
             assert np.array_equal(ut.cpu().numpy(), uo)

@@ -156,14 +156,16 @@ def test_parity_3d_513_full_size(dtype):
             assert np.array_equal(hg, ho)
 
 
-@pytest.mark.parametrize("dim,n", [(2, 65), (3, 17)])
-def test_unaligned_pitch(dim, n):
-    """Caller arrays with pitch = n (rows not 16-byte aligned) and a wide pitch."""
+@pytest.mark.parametrize("dim,n,dtype", [(2, 65, np.float64), (3, 17, np.float64), (2, 257, np.float64),
+                                         (2, 257, np.float32), (3, 33, np.float32)])
+def test_unaligned_pitch(dim, n, dtype):
+    """Caller arrays with pitch = n (rows not 16-byte aligned) and a wide pitch: staged through the work layout
+    by the re-pitch kernel (n = 257: two full 128-element chunks and a one-element tail per row)."""
     p = P2 if dim == 2 else P3
-    f = W.random_field(dim, n, seed=2)
-    uo, _ = _oracle_run(dim, n, 2, p, f, np.zeros_like(f), 3, np.float64)
+    f = W.random_field(dim, n, seed=2).astype(dtype)
+    uo, _ = _oracle_run(dim, n, 2, p, f, np.zeros_like(f), 3, dtype)
     for pitch in (n, n + 7, 2 * n + 3):
-        ug, _ = _gpu_run(dim, n, 2, p, f, np.zeros_like(f), 3, np.float64, pitch=pitch)
+        ug, _ = _gpu_run(dim, n, 2, p, f, np.zeros_like(f), 3, dtype, pitch=pitch)
         assert np.array_equal(ug, uo), pitch
 
 
